@@ -1,0 +1,317 @@
+"""Workload recipes for BASELINE.json configs 1-5.
+
+Every input is seeded and synthetic.  The paper's own images (``house``,
+ASTRA Shepp-Logan phantoms) are not available;
+these generators stand in for them at the shapes BASELINE.json fixes.
+
+Seeds: master seed ``260522281 + config_index`` split by ``SeedSequence`` into the
+named streams (A, xtrue, noise); sketch seed ``0x5F1A5D + config_index``.
+Noise is scaled to its exact norm, ``e = g * delta*||A x_true|| / ||g||``
+(reading R9; PAPER.md L50-54 defines delta = ||e|| / ||A x_true||).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libsflsqr_gen.so")
+_SRC = os.path.join(_HERE, "csrc", "gen.cpp")
+_lib = None
+
+MASTER_SEED = 260522281
+SKETCH_SEED_BASE = 0x5F1A5D
+
+
+def build_lib(force: bool = False) -> str:
+    """Compile gen/csrc/gen.cpp into gen/libsflsqr_gen.so (g++, -O3, no FMA contraction)."""
+    stale = (not os.path.exists(_LIB_PATH)) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC)
+    if force or stale:
+        tmp = _LIB_PATH + f".tmp{os.getpid()}"
+        cmd = ["g++", "-O3", "-std=c++17", "-fPIC", "-shared", "-pthread", "-ffp-contract=off",
+               _SRC, "-o", tmp]
+        subprocess.run(cmd, check=True)
+        os.replace(tmp, _LIB_PATH)
+    return _LIB_PATH
+
+
+def _get_lib():
+    global _lib
+    if _lib is None:
+        build_lib()
+        lib = ctypes.CDLL(_LIB_PATH)
+        i64p = ctypes.POINTER(ctypes.c_int64)
+        i32p = ctypes.POINTER(ctypes.c_int32)
+        f64p = ctypes.POINTER(ctypes.c_double)
+        ci = ctypes.c_int
+        for nm in ("gen_siddon_rownnz", "gen_pixbp_rownnz"):
+            getattr(lib, nm).argtypes = [ci, ci, ci, i64p, ci]
+            getattr(lib, nm).restype = ci
+        for nm in ("gen_siddon_fill", "gen_pixbp_fill"):
+            getattr(lib, nm).argtypes = [ci, ci, ci, i64p, i32p, f64p, ci]
+            getattr(lib, nm).restype = ci
+        lib.gen_csr_matvec.argtypes = [ctypes.c_int64, i64p, i32p, f64p, f64p, f64p, ci]
+        lib.gen_csr_matvec.restype = ci
+        _lib = lib
+    return _lib
+
+
+def _p(a, ct):
+    return a.ctypes.data_as(ctypes.POINTER(ct))
+
+
+@dataclass
+class CSR:
+    """Canonical CSR: int64 rowptr (nrows+1), int32 col, float64 val."""
+    nrows: int
+    ncols: int
+    rowptr: np.ndarray
+    col: np.ndarray
+    val: np.ndarray
+
+    @property
+    def nnz(self) -> int:
+        return int(self.rowptr[-1])
+
+    def matvec(self, x: np.ndarray, nthreads: int = 0) -> np.ndarray:
+        """Generator-side y = M x (used only to form b = A x_true)."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.empty(self.nrows, dtype=np.float64)
+        _get_lib().gen_csr_matvec(self.nrows, _p(self.rowptr, ctypes.c_int64), _p(self.col, ctypes.c_int32),
+                                  _p(self.val, ctypes.c_double), _p(x, ctypes.c_double),
+                                  _p(y, ctypes.c_double), nthreads)
+        return y
+
+    @staticmethod
+    def from_dense(M: np.ndarray) -> "CSR":
+        M = np.asarray(M, dtype=np.float64)
+        r, c = M.shape
+        rowptr = np.arange(0, r * c + 1, c, dtype=np.int64)
+        col = np.tile(np.arange(c, dtype=np.int32), r)
+        return CSR(r, c, rowptr, col, np.ascontiguousarray(M.reshape(-1)))
+
+    def to_dense(self) -> np.ndarray:
+        D = np.zeros((self.nrows, self.ncols))
+        for i in range(self.nrows):
+            s, e = self.rowptr[i], self.rowptr[i + 1]
+            D[i, self.col[s:e]] += self.val[s:e]
+        return D
+
+
+def _rowptr_from_counts(cnt: np.ndarray) -> np.ndarray:
+    rp = np.zeros(cnt.size + 1, dtype=np.int64)
+    np.cumsum(cnt, out=rp[1:])
+    return rp
+
+
+def siddon_csr(N: int, n_angles: int, nb: int, nthreads: int = 0) -> CSR:
+    """Siddon ray-pixel intersection-length matrix, m = n_angles*nb rows, n = N*N columns."""
+    lib = _get_lib()
+    m = n_angles * nb
+    cnt = np.empty(m, dtype=np.int64)
+    if lib.gen_siddon_rownnz(N, n_angles, nb, _p(cnt, ctypes.c_int64), nthreads) != 0:
+        raise RuntimeError("gen_siddon_rownnz failed")
+    rp = _rowptr_from_counts(cnt)
+    nnz = int(rp[-1])
+    col = np.empty(nnz, dtype=np.int32)
+    val = np.empty(nnz, dtype=np.float64)
+    if lib.gen_siddon_fill(N, n_angles, nb, _p(rp, ctypes.c_int64), _p(col, ctypes.c_int32),
+                           _p(val, ctypes.c_double), nthreads) != 0:
+        raise RuntimeError("gen_siddon_fill failed")
+    return CSR(m, N * N, rp, col, val)
+
+
+def pixbp_csr(N: int, n_angles: int, nb: int, nthreads: int = 0) -> CSR:
+    """Pixel-driven linear-interpolation backprojector B (n x m), B ~ A^T but unmatched."""
+    lib = _get_lib()
+    n = N * N
+    cnt = np.empty(n, dtype=np.int64)
+    if lib.gen_pixbp_rownnz(N, n_angles, nb, _p(cnt, ctypes.c_int64), nthreads) != 0:
+        raise RuntimeError("gen_pixbp_rownnz failed")
+    rp = _rowptr_from_counts(cnt)
+    nnz = int(rp[-1])
+    col = np.empty(nnz, dtype=np.int32)
+    val = np.empty(nnz, dtype=np.float64)
+    if lib.gen_pixbp_fill(N, n_angles, nb, _p(rp, ctypes.c_int64), _p(col, ctypes.c_int32),
+                          _p(val, ctypes.c_double), nthreads) != 0:
+        raise RuntimeError("gen_pixbp_fill failed")
+    return CSR(n, n_angles * nb, rp, col, val)
+
+
+def ellipse_phantom(N: int, rng: np.random.Generator, n_ell: int = 10) -> np.ndarray:
+    """Random-ellipse phantom (BASELINE.json configs 3-5; reading R15).
+
+    Centres uniform-by-area in the inscribed disk, semi-axes U[0.02,0.6]*N/2,
+    rotation U[0,pi), additive intensities U[-0.3,1]; sum, then clip >= 0.
+    Returns the row-major vectorised image (n = N*N).
+    """
+    half = 0.5 * N
+    c = np.arange(N, dtype=np.float64) + 0.5 - half
+    X, Y = np.meshgrid(c, c)  # X varies along ix (columns), Y along iy (rows)
+    img = np.zeros((N, N))
+    for _ in range(n_ell):
+        r = half * np.sqrt(rng.uniform())
+        phi = 2.0 * np.pi * rng.uniform()
+        cx, cy = r * np.cos(phi), r * np.sin(phi)
+        a = rng.uniform(0.02, 0.6) * half
+        b = rng.uniform(0.02, 0.6) * half
+        rot = rng.uniform(0.0, np.pi)
+        inten = rng.uniform(-0.3, 1.0)
+        xr = (X - cx) * np.cos(rot) + (Y - cy) * np.sin(rot)
+        yr = -(X - cx) * np.sin(rot) + (Y - cy) * np.cos(rot)
+        img[(xr / a) ** 2 + (yr / b) ** 2 <= 1.0] += inten
+    np.maximum(img, 0.0, out=img)
+    return img.reshape(-1)
+
+
+def rect_image(N: int, rng: np.random.Generator, n_rect: int = 4) -> np.ndarray:
+    """Piecewise-constant N x N image: n_rect axis-aligned rectangles, values U[0,1],
+    overwritten in order on a zero background (config 1; reading R15)."""
+    img = np.zeros((N, N))
+    for _ in range(n_rect):
+        y0, y1 = np.sort(rng.integers(0, N, size=2))
+        x0, x1 = np.sort(rng.integers(0, N, size=2))
+        img[y0:y1 + 1, x0:x1 + 1] = rng.uniform(0.0, 1.0)
+    return img.reshape(-1)
+
+
+def star_field(N: int, rng: np.random.Generator, frac: float = 0.02) -> np.ndarray:
+    """Sparse star field: round(frac*n) distinct pixels with values U[0.5,1] (config 2)."""
+    n = N * N
+    k = int(round(frac * n))
+    x = np.zeros(n)
+    idx = rng.choice(n, size=k, replace=False)
+    x[idx] = rng.uniform(0.5, 1.0, size=k)
+    return x
+
+
+def gen_blur_taps(sigma: float, radius: int) -> np.ndarray:
+    t = np.arange(-radius, radius + 1, dtype=np.float64)
+    g = np.exp(-t * t / (2.0 * sigma * sigma))
+    return g / g.sum()
+
+
+def gen_blur_apply(x: np.ndarray, H: int, W: int, sigma: float, radius: int) -> np.ndarray:
+    """Generator-side separable Gaussian blur, zero boundary (used only to form b)."""
+    from scipy.ndimage import correlate1d
+    g = gen_blur_taps(sigma, radius)
+    X = x.reshape(H, W)
+    Y = correlate1d(X, g, axis=1, mode="constant", cval=0.0)
+    Y = correlate1d(Y, g, axis=0, mode="constant", cval=0.0)
+    return Y.reshape(-1)
+
+
+@dataclass
+class SolverSpec:
+    method: str          # "sflsqr" | "sflsmr"
+    maxit: int
+    window: int          # orthogonalisation window ell
+    d: int               # sketch rows
+    s_nz: int            # nonzeros per sketch column
+    precond: str         # "irn" | "nonneg" | "identity"
+    p: float = 1.0       # IRN exponent (l_p prior)
+    eps_rel: float = 1e-3
+    eta: float = 0.0     # discrepancy safety factor (0 = off)
+    tol: float = 0.0
+    orth_mode: str = "P"
+
+
+@dataclass
+class Problem:
+    name: str
+    config_index: int
+    m: int
+    n: int
+    A: Optional[CSR]                 # None for the matrix-free blur
+    T: Optional[CSR]                 # given transpose-side operator (B) or None
+    t_mode: str                      # "build" (A^T) | "given" (B) | "same" (symmetric blur)
+    blur: Optional[dict]
+    x_true: np.ndarray
+    b: np.ndarray
+    e: np.ndarray
+    delta: float
+    delta_e: float
+    sketch_seed: int
+    solvers: list = field(default_factory=list)
+    geometry: dict = field(default_factory=dict)
+
+
+CONFIGS = {
+    1: dict(name="c1_dense256", kind="dense", N=16, delta=0.01,
+            solvers=[("sflsqr", 40, 2, 80, 4, "irn", 1.01), ("sflsmr", 40, 2, 80, 4, "irn", 1.01)]),
+    2: dict(name="c2_blur256", kind="blur", N=256, sigma=2.5, radius=7, delta=0.01,
+            solvers=[("sflsqr", 100, 3, 200, 8, "irn", 0.0)]),
+    3: dict(name="c3_ct512", kind="ct", N=512, n_angles=360, nb=725, delta=0.02, matched=True,
+            solvers=[("sflsqr", 150, 3, 300, 8, "nonneg", 0.0), ("sflsmr", 150, 3, 300, 8, "nonneg", 0.0)]),
+    4: dict(name="c4_ct1024_unmatched", kind="ct", N=1024, n_angles=720, nb=1449, delta=0.01, matched=False,
+            solvers=[("sflsqr", 200, 4, 400, 8, "identity", 0.0)]),
+    5: dict(name="c5_ct2048", kind="ct", N=2048, n_angles=1440, nb=2897, delta=0.01, matched=True,
+            solvers=[("sflsqr", 300, 5, 600, 8, "irn", 0.0), ("sflsmr", 300, 5, 600, 8, "irn", 0.0)]),
+}
+
+
+def make_problem(config_index: int, N: Optional[int] = None, n_angles: Optional[int] = None,
+                 nb: Optional[int] = None, nthreads: int = 0, seed_offset: int = 0) -> Problem:
+    """Build the seeded problem for a BASELINE.json config (1-based index).
+
+    ``N``/``n_angles``/``nb`` override the geometry to produce reduced-size
+    variants of the same recipe (parity tests); defaults are BASELINE.json's.
+    """
+    cfg = CONFIGS[config_index]
+    ss = np.random.SeedSequence(MASTER_SEED + config_index + seed_offset)
+    s_A, s_x, s_e = ss.spawn(3)
+    rA, rx, re = (np.random.Generator(np.random.PCG64(s)) for s in (s_A, s_x, s_e))
+    kind = cfg["kind"]
+    geometry = {}
+    A = T = None
+    blur = None
+    if kind == "dense":
+        Nimg = N or cfg["N"]
+        n = Nimg * Nimg
+        U = np.linalg.qr(rA.standard_normal((n, n)))[0]
+        V = np.linalg.qr(rA.standard_normal((n, n)))[0]
+        sig = 10.0 ** (-6.0 * np.arange(n) / (n - 1))
+        Ad = (U * sig) @ V.T
+        A = CSR.from_dense(Ad)
+        t_mode = "build"
+        x_true = rect_image(Nimg, rx)
+        m = n
+        geometry = dict(N=Nimg, sigma_min=float(sig[-1]))
+        Ax = A.matvec(x_true)
+    elif kind == "blur":
+        Nimg = N or cfg["N"]
+        n = m = Nimg * Nimg
+        blur = dict(H=Nimg, W=Nimg, sigma=cfg["sigma"], radius=cfg["radius"])
+        t_mode = "same"
+        x_true = star_field(Nimg, rx)
+        geometry = dict(N=Nimg)
+        Ax = gen_blur_apply(x_true, Nimg, Nimg, cfg["sigma"], cfg["radius"])
+    elif kind == "ct":
+        Nimg = N or cfg["N"]
+        na = n_angles or cfg["n_angles"]
+        nbins = nb or cfg["nb"]
+        A = siddon_csr(Nimg, na, nbins, nthreads)
+        if cfg["matched"]:
+            t_mode = "build"
+        else:
+            T = pixbp_csr(Nimg, na, nbins, nthreads)
+            t_mode = "given"
+        m, n = A.nrows, A.ncols
+        x_true = ellipse_phantom(Nimg, rx)
+        geometry = dict(N=Nimg, n_angles=na, nb=nbins)
+        Ax = A.matvec(x_true, nthreads)
+    else:
+        raise ValueError(kind)
+    g = re.standard_normal(m)
+    e = g * (cfg["delta"] * np.linalg.norm(Ax) / np.linalg.norm(g))
+    b = Ax + e
+    solvers = [SolverSpec(method=s[0], maxit=s[1], window=s[2], d=s[3], s_nz=s[4], precond=s[5], eta=s[6])
+               for s in cfg["solvers"]]
+    return Problem(name=cfg["name"], config_index=config_index, m=m, n=n, A=A, T=T, t_mode=t_mode,
+                   blur=blur, x_true=x_true, b=b, e=e, delta=cfg["delta"], delta_e=float(np.linalg.norm(e)),
+                   sketch_seed=SKETCH_SEED_BASE + config_index, solvers=solvers, geometry=geometry)

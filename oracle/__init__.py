@@ -1,0 +1,22 @@
+"""CPU oracle for the sketched flexible Golub-Kahan step (sFLSQR / sFLSMR).
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` leg may import, call,
+link or execute anything under ``oracle/``.  The product path
+(``paper_2605_22281_b200``) never imports it and shares no code with it.
+
+Plain, slow, fp64: NumPy for vector algebra, a plain single-threaded C CSR
+product (``csrc/oracle_csr.c``, -ffp-contract=off), Householder QR written out
+(``lsq.py``), Philox4x32-10 written out from its published definition
+(``philox.py``).  Every function cites the PAPER.md passage it follows; the
+readings of paper-silent points are listed in DESIGN.md.
+
+Parity pins (tests/test_oracle_*.py, ``-m "not gpu"``): Philox known-answer
+vectors; sketch table properties; Householder vs numpy.linalg.lstsq;
+reductions to SciPy LSQR/LSMR (tau = id, S = I, full window); fixed-diagonal
+tau vs LSQR on A D^{1/2}; AB-/BA-GMRES brute force for unmatched B; the
+Remark sFLSMR == sFLSQR with sketch S A^T; rank-k exactness; Theorem 2.1's
+identity; FGK relations.  "Parity unpinned": the IRN and NONNEG weight
+formulas themselves (paper-silent, readings R7/R8) are pinned only through the
+fixed-diagonal reduction and GPU-vs-oracle agreement.
+"""

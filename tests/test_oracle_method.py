@@ -1,0 +1,255 @@
+"""Pins P2, P4a-c, P5, P6, P7 and the GKB reduction for the oracle's sFLSQR/sFLSMR.
+
+Each test fixes the oracle against something other than itself: SciPy's
+textbook LSQR/LSMR, brute-force Krylov least squares (AB-/BA-GMRES), the
+Remark of PAPER.md L810-822, the rank-k exactness remark (L1083-1111),
+the exact identity in the proof of Theorem 2.1 (L1046-1078) and the factorisation
+eq. FGK (L400-404).
+"""
+import numpy as np
+import pytest
+from scipy.sparse.linalg import lsmr, lsqr
+
+from oracle.operators import DenseOperator
+from oracle.sflsqr import BREAKDOWN, DISCREPANCY, MAXIT, solve
+from oracle.sketch import DenseSketch, IdentitySketch, SparseSignSketch
+
+
+def _dense_problem(m, n, cond, seed, noise=0.05):
+    rng = np.random.default_rng(seed)
+    U = np.linalg.qr(rng.standard_normal((m, n)))[0]
+    V = np.linalg.qr(rng.standard_normal((n, n)))[0]
+    A = (U * np.logspace(0, -np.log10(cond), n)) @ V.T
+    x = rng.standard_normal(n)
+    b = A @ x
+    e = rng.standard_normal(m)
+    b = b + e * (noise * np.linalg.norm(b) / np.linalg.norm(e))
+    return A, b, rng
+
+
+def _rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+# ---------------------------------------------------------------- P4a -----
+@pytest.mark.parametrize("K", [12])
+def test_sflsqr_identity_sketch_equals_scipy_lsqr(K):
+    A, b, _ = _dense_problem(60, 40, 1e2, 1)
+    op = DenseOperator(A)
+    r = solve(op, b, "sflsqr", maxit=K, window=K, sketch=IdentitySketch(60), precond="identity")
+    assert r.status == MAXIT
+    for k in range(1, K + 1):
+        xk = lsqr(A, b, atol=0, btol=0, conlim=0, iter_lim=k)[0]
+        assert _rel(r.xs[k - 1], xk) < 1e-8, k
+
+
+@pytest.mark.parametrize("K", [12])
+def test_sflsmr_identity_sketch_equals_scipy_lsmr(K):
+    A, b, _ = _dense_problem(60, 40, 1e2, 2)
+    op = DenseOperator(A)
+    r = solve(op, b, "sflsmr", maxit=K, window=K, sketch=IdentitySketch(40), precond="identity")
+    for k in range(1, K + 1):
+        xk = lsmr(A, b, atol=0, btol=0, conlim=0, maxiter=k)[0]
+        assert _rel(r.xs[k - 1], xk) < 1e-8, k
+
+
+def test_gkb_reduction_bidiagonal_H():
+    # tau = id, matched A, full window: FGK = GKB, H = B_{k+1,k}.
+    A, b, _ = _dense_problem(50, 30, 1e2, 3)
+    K = 10
+    r = solve(DenseOperator(A), b, "sflsqr", maxit=K, window=K, sketch=IdentitySketch(50))
+    # textbook Golub-Kahan recurrence (eq. GKB)
+    beta = np.linalg.norm(b); u = b / beta
+    v = A.T @ u; alpha = np.linalg.norm(v); v /= alpha
+    Bk = np.zeros((K + 1, K))
+    for i in range(K):
+        Bk[i, i] = alpha
+        u = A @ v - alpha * u
+        beta = np.linalg.norm(u); u /= beta
+        Bk[i + 1, i] = beta
+        v = A.T @ u - beta * v
+        alpha = np.linalg.norm(v); v /= alpha
+    np.testing.assert_allclose(r.H, Bk, atol=1e-10 * np.abs(Bk).max())
+
+
+# ---------------------------------------------------------------- P4b -----
+@pytest.mark.parametrize("method,ref", [("sflsqr", "lsqr"), ("sflsmr", "lsmr")])
+def test_fixed_diagonal_tau_equals_lsqr_on_scaled_operator(method, ref):
+    # span(Z_k) = K_k(D A^T A, D A^T b)  =>  x_k = D^{1/2} xtilde_k, xtilde = LSQR/LSMR(A D^{1/2})
+    A, b, rng = _dense_problem(70, 45, 1e2, 4)
+    D = rng.uniform(0.3, 2.0, 45)
+    K = 10
+    sk = IdentitySketch(70 if method == "sflsqr" else 45)
+    r = solve(DenseOperator(A), b, method, maxit=K, window=K, sketch=sk, precond="diag", fixed_diag=D)
+    As = A * np.sqrt(D)
+    for k in range(1, K + 1):
+        if ref == "lsqr":
+            xt = lsqr(As, b, atol=0, btol=0, conlim=0, iter_lim=k)[0]
+        else:
+            # sFLSMR with S = I minimises ||A^T (b - A x)|| over span(Z_k); with Z_k = D^{1/2}Ztilde
+            # that is || D^{-1/2} As^T (b - As xt) || - not LSMR's norm unless D = I, so compare by brute force
+            Kry = [D * (A.T @ b)]
+            for _ in range(k - 1):
+                Kry.append(D * (A.T @ (A @ Kry[-1])))
+            Q = np.linalg.qr(np.column_stack(Kry))[0]
+            c = np.linalg.lstsq(A.T @ A @ Q, A.T @ b, rcond=None)[0]
+            xk = Q @ c
+            assert _rel(r.xs[k - 1], xk) < 1e-8, k
+            continue
+        assert _rel(r.xs[k - 1], np.sqrt(D) * xt) < 1e-8, k
+
+
+# ---------------------------------------------------------------- P4c -----
+def test_unmatched_B_equals_ab_and_ba_gmres():
+    # tau = id, S = I, full window, T = B != A^T: sFLSQR == AB-GMRES, sFLSMR == BA-GMRES (L1646-1647)
+    A, b, rng = _dense_problem(55, 40, 50, 5)
+    B = A.T + 0.05 * rng.standard_normal((40, 55)) / np.sqrt(55)
+    op = DenseOperator(A, B)
+    K = 9
+    rq = solve(op, b, "sflsqr", maxit=K, window=K, sketch=IdentitySketch(55))
+    rm = solve(op, b, "sflsmr", maxit=K, window=K, sketch=IdentitySketch(40))
+    for k in range(1, K + 1):
+        Kry = [B @ b]
+        for _ in range(k - 1):
+            Kry.append(B @ (A @ Kry[-1]))
+        Q = np.linalg.qr(np.column_stack(Kry))[0]
+        x_ab = Q @ np.linalg.lstsq(A @ Q, b, rcond=None)[0]
+        x_ba = Q @ np.linalg.lstsq(B @ A @ Q, B @ b, rcond=None)[0]
+        assert _rel(rq.xs[k - 1], x_ab) < 1e-8, k
+        assert _rel(rm.xs[k - 1], x_ba) < 1e-8, k
+
+
+# ---------------------------------------------------------------- P5 ------
+@pytest.mark.parametrize("precond", ["identity", "irn"])
+def test_remark_sflsmr_is_sflsqr_with_sketch_SAt(precond):
+    # ||S A^T (A Z y - b)|| = ||S (A^T A Z y - A^T b)||
+    A, b, _ = _dense_problem(80, 50, 1e2, 6)
+    sk = SparseSignSketch(17, 30, 4, 50)
+    K = 12
+    rm = solve(DenseOperator(A), b, "sflsmr", maxit=K, window=2, sketch=sk, precond=precond)
+    rq = solve(DenseOperator(A), b, "sflsqr", maxit=K, window=2, sketch=DenseSketch(sk.dense() @ A.T),
+               precond=precond)
+    for k in range(K):
+        assert _rel(rm.ys[k], rq.ys[k]) < 1e-8, k
+        assert _rel(rm.xs[k], rq.xs[k]) < 1e-8, k
+
+
+def test_rank_k_exactness_of_sflsmr():
+    # rank(A) = k  =>  r_k^sFLSMR = r_k^opt (no breakdown)
+    kr = 10
+    for seed in range(5):
+        rng = np.random.default_rng(100 + seed)
+        A = rng.standard_normal((200, kr)) @ rng.standard_normal((kr, 100))
+        b = rng.standard_normal(200)
+        sk = SparseSignSketch(1000 + seed, 25, 4, 100)
+        r = solve(DenseOperator(A), b, "sflsmr", maxit=kr, window=2, sketch=sk, precond="irn")
+        assert r.status == MAXIT and r.k == kr
+        AZ = A @ r.Z
+        r_opt = np.linalg.norm(b - AZ @ np.linalg.lstsq(AZ, b, rcond=None)[0])
+        assert abs(r.true_res[-1] - r_opt) <= 1e-8 * r_opt
+        # sFLSQR with a sketch of the same size is NOT optimal in general
+        skq = SparseSignSketch(2000 + seed, 25, 4, 200)
+        rq = solve(DenseOperator(A), b, "sflsqr", maxit=kr, window=2, sketch=skq, precond="irn")
+        AZq = A @ rq.Z
+        r_optq = np.linalg.norm(b - AZq @ np.linalg.lstsq(AZq, b, rcond=None)[0])
+        assert rq.true_res[-1] >= r_optq * (1 - 1e-12)
+
+
+# ---------------------------------------------------------------- P6 ------
+@pytest.mark.parametrize("method", ["sflsqr", "sflsmr"])
+def test_theorem_2_1_identity_and_bound(method):
+    # Proof of Theorem 2.1 (L1046-1078): r^2 = ||(S'Q)^+ S' Q_perp Q_perp^T b||^2 + ||Q_perp^T b||^2,
+    # S' = S (sFLSQR) or S A^T (sFLSMR); hence bounds (bound1), (bound2).
+    m, n = 90, 60
+    A, b, _ = _dense_problem(m, n, 1e3, 7, noise=0.2)
+    dim = m if method == "sflsqr" else n
+    sk = SparseSignSketch(23, 40, 8, dim)
+    K = 15
+    r = solve(DenseOperator(A), b, method, maxit=K, window=3, sketch=sk, precond="irn")
+    S = sk.dense() if method == "sflsqr" else sk.dense() @ A.T
+    for k in range(1, K + 1):
+        AZ = A @ r.Z[:, :k]
+        Qf = np.linalg.qr(AZ, mode="complete")[0]
+        Q, Qp = Qf[:, :k], Qf[:, k:]
+        r_opt = np.linalg.norm(Qp.T @ b)
+        SQp = np.linalg.pinv(S @ Q)
+        first = np.linalg.norm(SQp @ (S @ Qp) @ (Qp.T @ b))
+        r_k = r.true_res[k - 1]
+        assert abs(r_k ** 2 - (first ** 2 + r_opt ** 2)) <= 1e-9 * r_k ** 2, k
+        bound = r_opt * np.sqrt(1 + np.linalg.norm(SQp @ (S @ Qp), 2) ** 2)
+        assert r_k <= bound * (1 + 1e-9), k
+
+
+# ---------------------------------------------------------------- P2 ------
+@pytest.mark.parametrize("method", ["sflsqr", "sflsmr"])
+@pytest.mark.parametrize("precond,matched", [("irn", True), ("nonneg", True), ("identity", False)])
+def test_fgk_relations(method, precond, matched):
+    A, b, rng = _dense_problem(70, 50, 1e3, 8)
+    B = None if matched else A.T + 0.03 * rng.standard_normal((50, 70)) / np.sqrt(70)
+    op = DenseOperator(A, B)
+    T = op.Td
+    ell, K = 2, 20
+    sk = SparseSignSketch(3, 41, 4, 70 if method == "sflsqr" else 50)
+    r = solve(op, b, method, maxit=K, window=ell, sketch=sk, precond=precond)
+    Z, W, H, P, Tm = r.Z, r.W, r.H, r.P, r.T
+    AZ = A @ Z
+    assert np.linalg.norm(AZ - W @ H) <= 1e-12 * np.linalg.norm(AZ)          # A Z_k = W_{k+1} H_{k+1,k}
+    TW = T @ W[:, :K]
+    assert np.linalg.norm(TW - P @ Tm) <= 1e-12 * np.linalg.norm(TW)         # T W_k = P_k T_k (orth mode P)
+    for k in range(K):                                                        # banded structure
+        assert np.all(H[:max(0, k - ell), k] == 0)
+        assert np.all(Tm[:max(0, k - ell), k] == 0)
+        assert np.all(H[k + 2:, k] == 0)
+    G = W.T @ W                                                              # windowed orthonormality
+    for i in range(K + 1):
+        assert abs(G[i, i] - 1) < 1e-13
+        for j in range(max(0, i - ell - 1), i):
+            assert abs(G[i, j]) < 1e-12
+    GP = P.T @ P
+    for i in range(K):
+        assert abs(GP[i, i] - 1) < 1e-13
+        for j in range(max(0, i - ell), i):
+            assert abs(GP[i, j]) < 1e-12
+
+
+def test_literal_orth_mode_equals_P_mode_for_identity_tau():
+    A, b, _ = _dense_problem(40, 30, 1e2, 9)
+    sk = SparseSignSketch(1, 25, 2, 40)
+    r1 = solve(DenseOperator(A), b, "sflsqr", maxit=10, window=2, sketch=sk, orth_mode="P")
+    r2 = solve(DenseOperator(A), b, "sflsqr", maxit=10, window=2, sketch=sk, orth_mode="Z")
+    np.testing.assert_array_equal(r1.x, r2.x)
+
+
+# ---------------------------------------------------------------- P7 ------
+def test_discrepancy_stop_index():
+    A, b0, rng = _dense_problem(120, 80, 1e4, 10, noise=0.0)
+    e = rng.standard_normal(120)
+    e *= 0.05 * np.linalg.norm(b0) / np.linalg.norm(e)
+    b = b0 + e
+    delta_e = np.linalg.norm(e)
+    sk = SparseSignSketch(5, 61, 4, 120)
+    full = solve(DenseOperator(A), b, "sflsqr", maxit=30, window=2, sketch=sk, precond="irn")
+    eta = max(1.01, full.true_res[14] / delta_e * (1 + 1e-9))   # a level the run reaches mid-way
+    hits = [k + 1 for k, r in enumerate(full.true_res) if r <= eta * delta_e]
+    assert hits, "test problem should reach the discrepancy level"
+    stop = solve(DenseOperator(A), b, "sflsqr", maxit=30, window=2, sketch=sk, precond="irn",
+                 eta=eta, delta_e=delta_e)
+    assert stop.status == DISCREPANCY and stop.k == hits[0]
+    np.testing.assert_array_equal(stop.x, full.xs[hits[0] - 1])
+
+
+def test_sketched_residual_nonincreasing_sflsqr():
+    A, b, _ = _dense_problem(100, 70, 1e3, 11)
+    r = solve(DenseOperator(A), b, "sflsqr", maxit=25, window=2, sketch=SparseSignSketch(2, 51, 4, 100),
+              precond="irn")
+    s = np.array(r.sketch_res)
+    assert np.all(s[1:] <= s[:-1] * (1 + 1e-12))
+
+
+def test_breakdown_returns_previous_iterate():
+    # A = I (n = 3): the Krylov space is exhausted -> breakdown, x_{k-1} returned (reading R11)
+    A = np.diag([1.0, 2.0, 3.0])
+    b = np.array([1.0, 1.0, 0.0])
+    r = solve(DenseOperator(A), b, "sflsqr", maxit=6, window=6, sketch=IdentitySketch(3))
+    assert r.status == BREAKDOWN
+    np.testing.assert_allclose(A @ r.x, b, atol=1e-12)
