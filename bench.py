@@ -1,0 +1,330 @@
+#!/usr/bin/env python3
+"""Benchmark of the sketched flexible Golub-Kahan step (BASELINE.json metric).
+
+One "step" = one sFLSQR iteration (all SURVEY.md §8(a) rows a1-a9) of the
+config-4 workload (BASELINE.json configs[3]: 1024^2 Siddon CT, 720 angles x
+1449 bins, unmatched pixel-driven backprojector B, ell = 4, d = 400, s = 8,
+identity tau; the largest configuration that fits one B200 and the one the
+metric's 1/2/4/8-GPU scaling is quoted on).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+Prints ONE JSON line on rank 0.  Timing: W untimed warm-up iterations, then
+exactly K iterations bracketed by barrier + cuda.synchronize, CUDA events on
+the library's stream (torch's current stream), max over ranks.  The operators
+(~30 GB) exceed L2 (126 MB), so no L2 flush is needed between iterations.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sFLSQR iterations/s at 1/2/4/8 B200; achieved HBM GB/s vs 8 TB/s/GPU"
+UNIT = "iterations/s"
+CONTRACT_PEAK_GBS = 8000.0
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.proc = None
+        self.idx = device_index
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        if not getattr(self, "lines", None):
+            return None
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [t.strip() for t in ln.split(",")]
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def _max_over_ranks(v, world):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def _traffic(workload, kernel):
+    p = os.path.join(ROOT, "profiles", f"traffic_{workload}.json")
+    try:
+        d = json.load(open(p))
+        return d.get(kernel)
+    except Exception:
+        return None
+
+
+def run_cpu_baseline(prob, spec, budget_s=25.0):
+    """The oracle as it stands (single thread), first iterations of the same workload."""
+    from threadpoolctl import threadpool_limits
+    from oracle.operators import operator_from_problem
+    from oracle.sflsqr import solve_problem
+    with threadpool_limits(limits=1):
+        t0 = time.perf_counter()
+        op = operator_from_problem(prob)
+        t_op = time.perf_counter() - t0
+        # one iteration to size the sample, then k iterations inside the budget
+        t0 = time.perf_counter()
+        solve_problem(prob, spec, op=op, maxit=1, record=False)
+        t1 = time.perf_counter() - t0
+        k = 2 if t1 * 2 < budget_s else 1
+        t0 = time.perf_counter()
+        solve_problem(prob, spec, op=op, maxit=k, record=False)
+        tk = time.perf_counter() - t0
+    per_it = max((tk - t1) / max(k - 1, 1), 1e-9) if k > 1 else t1
+    return {"value": 1.0 / per_it, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": (f"oracle (NumPy + plain C CSR, 1 thread) on the full {prob.name} problem: solve with "
+                       f"maxit={k} minus maxit=1 (init + per-iteration cost separated); "
+                       f"{per_it:.2f} s/iteration, init+1st iteration {t1:.2f} s, operator setup {t_op:.2f} s")}
+
+
+def bench_reference(args, prob, spec, world, rank):
+    """--impl reference: the oracle (this tier's reference arm), bounded sample."""
+    if rank != 0:
+        return
+    from threadpoolctl import threadpool_limits
+    from oracle.operators import operator_from_problem
+    from oracle.sflsqr import solve_problem
+    budget = float(os.environ.get("SFLSQR_REF_BUDGET_S", "120"))
+    with threadpool_limits(limits=1):
+        op = operator_from_problem(prob)
+        t0 = time.perf_counter()
+        solve_problem(prob, spec, op=op, maxit=1, record=False)   # warm-up / sizing (init + 1 iteration)
+        t1 = time.perf_counter() - t0
+        k = int(max(1, min(args.steps, budget // max(t1, 1e-3))))
+        t0 = time.perf_counter()
+        solve_problem(prob, spec, op=op, maxit=k + 1, record=False)
+        tk = time.perf_counter() - t0
+    per_it = max((tk - t1) / k, 1e-12)
+    val = 1.0 / per_it
+    line = {"metric": METRIC, "value": val, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus, "steps": k,
+            "warmup": 1, "ms_per_step": per_it * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": prob.name, "m": prob.m, "n": prob.n, "nnz_A": prob.A.nnz,
+                       "nnz_T": prob.T.nnz if prob.T is not None else prob.A.nnz, "ell": spec.window, "d": spec.d,
+                       "s": spec.s_nz, "tau": spec.precond},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"{k} oracle iterations after init+1 (time budget {budget:.0f} s)"},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=195)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--method", default=None, help="sflsqr | sflsmr (default: the config's first)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-profile", action="store_true", help="graph replay without per-kernel events")
+    ap.add_argument("--N", type=int, default=None, help="override grid size (debug)")
+    args = ap.parse_args()
+
+    world, rank, local = _dist()
+    from gen import make_problem
+    t_gen = time.perf_counter()
+    geo = {}
+    if args.N:
+        geo = dict(N=args.N)
+    prob = make_problem(args.config, **geo)
+    t_gen = time.perf_counter() - t_gen
+    spec = prob.solvers[0] if args.method is None else [s for s in prob.solvers if s.method == args.method][0]
+
+    if args.impl == "reference":
+        bench_reference(args, prob, spec, world, rank)
+        return
+
+    import torch
+    if not torch.cuda.is_available():
+        print(json.dumps({"metric": METRIC, "error": "no CUDA device"}))
+        sys.exit(1)
+    torch.cuda.set_device(local)
+    # a dedicated non-default stream: the library issues on it and the CUDA events below record on it
+    torch.cuda.set_stream(torch.cuda.Stream())
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2605_22281_b200 import solver_for_problem
+    from paper_2605_22281_b200._build import build_library
+    if rank == 0:
+        build_library()
+    _barrier(world)
+
+    W, K = args.warmup, args.steps
+    maxit = max(spec.maxit, W + K)
+    stream = torch.cuda.current_stream()
+    t_up = time.perf_counter()
+    s = solver_for_problem(prob, spec, maxit=maxit, eta=0.0, device=local, use_graph=args.no_profile)
+    t_up = time.perf_counter() - t_up
+    info0 = s.get_info()
+    s.set_rhs(prob.b)
+    s.iterate(W)                                   # untimed warm-up (graph capture already done)
+    if not args.no_profile:
+        s.set_profiling(True)
+    s.reset_profile()
+    launches0 = s.get_info()["launches"]
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    _barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        done, status = s.iterate(K)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    _barrier(world)
+    ms = ev0.elapsed_time(ev1)
+    ms = _max_over_ranks(ms, world)
+    launches = s.get_info()["launches"] - launches0
+    prof = s.get_profile()
+    s.set_profiling(False)
+    k_done = s.get_info()["k_done"]
+    value = K * world / (ms / 1e3)
+
+    # roofline of the dominant kernel (HBM-bound CSR SpMV)
+    peak, peak_src = _peaks()
+    roof = None
+    kernels = {}
+    for nm, d in prof.items():
+        if d["launches"]:
+            kernels[nm] = {"ms_total": d["ms"], "launches": d["launches"],
+                           "ms_per_launch": d["ms"] / d["launches"],
+                           "algo_gbs": d["bytes"] / (d["ms"] / 1e3) / 1e9 if d["ms"] > 0 else None,
+                           "share": d["ms"] / ms}
+    if kernels:
+        dom = max(("spmv_A", "spmv_T"), key=lambda k2: kernels.get(k2, {"ms_total": 0})["ms_total"])
+        d = prof[dom]
+        bpl = d["bytes"] / d["launches"]
+        ach = bpl / (d["ms"] / d["launches"] / 1e3) / 1e9
+        tr = _traffic(prob.name, dom)
+        roof = {"bound": "hbm", "kernel": "k_spmv_csr (" + dom + ")", "achieved": ach, "peak": peak,
+                "unit": "GB/s", "frac": ach / peak, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": bpl, "traffic": tr}
+    step_bytes = sum(d["bytes"] for d in prof.values())
+    step_gbs = step_bytes / (ms / 1e3) / 1e9 if step_bytes else None
+
+    # e2e through the public API: host b -> set_rhs, K iterations, x + histories back to host
+    e2e = None
+    if not args.no_e2e:
+        b_pin = torch.from_numpy(prob.b).pin_memory()
+        x_pin = torch.empty(prob.n, dtype=torch.float64).pin_memory()
+        _barrier(world)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        s.set_rhs(b_pin)
+        s.iterate(K)
+        s.get_x(x_pin)
+        tr_hist, sk_hist = s.get_residual_norms()
+        torch.cuda.synchronize()
+        te = time.perf_counter() - t0
+        te = _max_over_ranks(te, world)
+        e2e = {"value": K * world / te, "unit": UNIT, "h2d_bytes_per_step": 8.0 * prob.m / K,
+               "d2h_bytes_per_step": (8.0 * prob.n + 16.0 * K) / K,
+               "note": "set_rhs(pinned host b) + iterate(K) + get_x(pinned host) + get_residual_norms, wall clock"}
+    s.close()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = run_cpu_baseline(prob, spec)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+            "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": prob.name, "method": spec.method, "m": prob.m, "n": prob.n,
+                       "nnz_A": prob.A.nnz, "nnz_T": prob.T.nnz if prob.T is not None else prob.A.nnz,
+                       "ell": spec.window, "d": spec.d, "s": spec.s_nz, "tau": spec.precond, "maxit": maxit,
+                       "iterations_timed": f"{W + 1}..{W + K}", "history": "true residual (W path) on",
+                       "l2": "inputs larger than L2 (operators ~30 GB vs 126 MB L2); no flush",
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "launch": "eager + per-kernel CUDA events" if not args.no_profile else "CUDA graph"},
+            "roofline": roof,
+            "step_algorithmic_gbs": step_gbs,
+            "step_frac_of_8TBs": step_gbs / CONTRACT_PEAK_GBS if step_gbs else None,
+            "step_frac_of_peak": step_gbs / peak if step_gbs else None,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
+            "kernels": kernels, "status": {"done": done, "status": status, "k_done": k_done},
+            "setup_s": {"generate": t_gen, "upload": t_up},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

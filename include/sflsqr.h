@@ -1,0 +1,242 @@
+/*
+ * sflsqr.h — C ABI of libsflsqr.so, the B200 (sm_100a) sketched flexible
+ * Golub–Kahan step of sFLSQR / sFLSMR.
+ *
+ * Method (PAPER.md = arXiv 2605.22281):
+ *   - Algorithm 1 "sFLSQR", L450–508; eq. (sFLSQR):
+ *       y_k = argmin_y || S (A Z_k y - b) ||,  x_k = Z_k y_k.
+ *   - Algorithm 2 "sFLSMR", L752–808; eq. (sFLSMR):
+ *       y_k = argmin_y || s_{A^T b} - [S_{A^T W}, S z] H_{1:k+1,1:k} y ||.
+ *   - both built on the partial flexible Golub–Kahan factorisation eq. (FGK)
+ *     L400–406:  A^T W_k = P_k T_k,  A Z_k = W_{k+1} H_{k+1,k},  Z_k = tau(P_k),
+ *     with orthogonalisation limited to the last `window` (= ell) vectors.
+ *   - stopping: tol test (Alg. 1 L498 / Alg. 2) and the discrepancy
+ *     principle eq. (discrP): stop at the first k with
+ *     ||b - A x_k|| <= eta * delta_e.
+ * Readings of paper-silent points (R1–R16) are listed in DESIGN.md §2 and are
+ * referenced below by number.
+ *
+ * Conventions
+ *   - All functions return SFLSQR_OK (0) or a negative SFLSQR_E_* code; the
+ *     message of the last failure is available from sflsqr_last_error(h).
+ *   - Floating point is IEEE fp64 throughout; indices are int32 columns and
+ *     int64 row pointers (CSR, 0-based, rowptr[0] = 0, rowptr[nrows] = nnz).
+ *   - Vectors are dense, contiguous, row-major image order (R16).
+ *   - "host" pointers are ordinary CPU memory; "device" pointers are CUDA
+ *     device memory on opts.device.  mem_flags says which (SFLSQR_MEM_*).
+ *   - Ownership: the library never frees caller memory.  With SFLSQR_MEM_COPY
+ *     (default) inputs are copied and may be released after the call returns;
+ *     with SFLSQR_MEM_BORROW (device pointers only) the caller keeps them alive
+ *     and unchanged until sflsqr_destroy.
+ *   - A handle is used by one host thread at a time.  All GPU work is issued on
+ *     opts.stream (a cudaStream_t borrowed from the caller, e.g. PyTorch's
+ *     current stream) or, when NULL, on a stream the library creates.
+ *   - There is no CPU fallback: without a usable CUDA device every compute call
+ *     fails with SFLSQR_E_CUDA.
+ *   - Required call order: create, set_operator*(), set_sketch(),
+ *     [set_precond()], set_rhs(), iterate()..., get_x()/get_residual_norms(),
+ *     destroy.  set_rhs() (re)starts a solve; out-of-order calls return
+ *     SFLSQR_E_STATE.
+ */
+#ifndef SFLSQR_H_
+#define SFLSQR_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SFLSQR_ABI_VERSION 1
+
+/* return codes */
+#define SFLSQR_OK 0
+#define SFLSQR_E_INVALID (-1)     /* invalid argument value / combination          */
+#define SFLSQR_E_DIM (-2)         /* dimensions or indices out of range            */
+#define SFLSQR_E_NONFINITE (-3)   /* NaN/Inf in an input array                     */
+#define SFLSQR_E_ZERO_RHS (-4)    /* ||b|| = 0 (Alg. 1 L457 divides by beta)       */
+#define SFLSQR_E_STATE (-5)       /* call order violated                           */
+#define SFLSQR_E_CUDA (-6)        /* CUDA runtime error / no device                */
+#define SFLSQR_E_OOM (-7)         /* device or host allocation failed              */
+#define SFLSQR_E_UNSUPPORTED (-8) /* valid request not supported by this build     */
+
+/* opts.method */
+#define SFLSQR_METHOD_SFLSQR 0 /* Algorithm 1 */
+#define SFLSQR_METHOD_SFLSMR 1 /* Algorithm 2 */
+
+/* opts.orth_mode (reading R1) */
+#define SFLSQR_ORTH_P 0 /* orthogonalise against the last ell normalised p_j (eq. FGK) */
+#define SFLSQR_ORTH_Z 1 /* literal Alg. 1: against z_j = tau(p_j)              */
+
+/* solve status (sflsqr_iterate, sflsqr_info) */
+#define SFLSQR_RUNNING 0
+#define SFLSQR_MAXIT 1
+#define SFLSQR_TOL 2         /* ||rhs - M y_k|| < tol ||rhs||                     */
+#define SFLSQR_DISCREPANCY 3 /* ||b - A x_k|| <= eta delta_e                      */
+#define SFLSQR_BREAKDOWN 4   /* reading R11 (a clean stop, not an error)          */
+
+/* preconditioner kinds (sflsqr_set_precond) */
+#define SFLSQR_PRECOND_IDENTITY 0 /* tau(v) = v                                   */
+#define SFLSQR_PRECOND_IRN 1      /* IRN-l_p right preconditioner, reading R7      */
+#define SFLSQR_PRECOND_NONNEG 2   /* nonnegativity-projecting scaling, reading R8  */
+
+/* transpose-side operator (sflsqr_set_operator t_mode) */
+#define SFLSQR_T_BUILD 0 /* T = A^T, formed by the library (matched)                */
+#define SFLSQR_T_GIVEN 1 /* T = the given n x m CSR (e.g. unmatched B ~ A^T, L86)   */
+
+/* mem_flags */
+#define SFLSQR_MEM_HOST 0   /* pointers are host memory (copied)                    */
+#define SFLSQR_MEM_DEVICE 1 /* pointers are device memory                           */
+#define SFLSQR_MEM_BORROW 2 /* OR with SFLSQR_MEM_DEVICE: keep the caller's arrays */
+
+/* opts.history bits */
+#define SFLSQR_HIST_TRUE_RES 1 /* record ||b - A x_k|| every iteration              */
+
+typedef struct sflsqr sflsqr_t;
+
+typedef struct sflsqr_opts {
+  int32_t method;    /* SFLSQR_METHOD_*                                            */
+  int32_t window;    /* ell >= 1 (Alg. 1/2 "orthogonalization window"); >= maxit = full */
+  int32_t maxit;     /* >= 1                                                       */
+  int32_t orth_mode; /* SFLSQR_ORTH_*                                              */
+  double tol;        /* >= 0; 0 disables the tol test                              */
+  double eta;        /* discrepancy safety factor: 0 (off) or > 1 (eq. discrP)     */
+  double delta_e;    /* noise norm ||e|| >= 0 (needed when eta > 0)                */
+  int32_t history;   /* SFLSQR_HIST_* bits                                         */
+  int32_t device;    /* CUDA device ordinal                                        */
+  void *stream;      /* cudaStream_t (borrowed) or NULL                            */
+  int32_t rank;      /* this process's rank (0)                                    */
+  int32_t world;     /* number of ranks; this build supports 1                     */
+  int32_t use_graph; /* 1: replay one captured CUDA graph per iteration            */
+  int32_t reserved[7];
+} sflsqr_opts;
+
+typedef struct sflsqr_info {
+  int32_t k_done;      /* iterations completed                                    */
+  int32_t k_x;         /* index of the iterate get_x returns (x_{k_x})            */
+  int32_t status;      /* SFLSQR_RUNNING/MAXIT/TOL/DISCREPANCY/BREAKDOWN          */
+  int32_t rank_flag;   /* 1 if a projected problem had |R_kk| < 1e-14 max|R_jj| (R14) */
+  int64_t m, n;        /* operator shape                                          */
+  int64_t nnz_a, nnz_t;/* stored nonzeros of A and T (0 for the matrix-free blur) */
+  int64_t launches;    /* kernel launches issued so far (this handle)             */
+  double beta;         /* ||b||                                                   */
+} sflsqr_info;
+
+/* Per-kernel-class device time, recorded with CUDA events on the library stream
+ * when profiling is on (sflsqr_set_profiling).  Index by SFLSQR_KC_*. */
+#define SFLSQR_KC_SPMV_A 0
+#define SFLSQR_KC_SPMV_T 1
+#define SFLSQR_KC_ORTH 2
+#define SFLSQR_KC_TAU 3
+#define SFLSQR_KC_SKETCH 4
+#define SFLSQR_KC_LS 5
+#define SFLSQR_KC_XUPD 6
+#define SFLSQR_KC_RES 7
+#define SFLSQR_KC_STOP 8
+#define SFLSQR_KC_COUNT 9
+typedef struct sflsqr_profile {
+  double ms[SFLSQR_KC_COUNT];       /* summed event time                              */
+  int64_t launches[SFLSQR_KC_COUNT];/* launches timed                                 */
+  double bytes[SFLSQR_KC_COUNT];    /* algorithmic bytes moved by those launches (model) */
+} sflsqr_profile;
+
+/* ABI version (SFLSQR_ABI_VERSION). Never fails. */
+int sflsqr_version(void);
+
+/* Create a solver handle.  Validates opts before any allocation:
+ * method, window >= 1, maxit >= 1, tol >= 0, eta == 0 or eta > 1,
+ * delta_e >= 0, world == 1 -> else SFLSQR_E_INVALID / SFLSQR_E_UNSUPPORTED.
+ * Selects opts.device; fails with SFLSQR_E_CUDA when no CUDA device exists. */
+int sflsqr_create(sflsqr_t **h, const sflsqr_opts *opts);
+
+/* Operator A (m x n CSR) and the transpose-side operator T (n x m) used for
+ * "A^T w" (Alg. 1 L458/L486, Alg. 2 L760/L789).
+ *   t_mode = SFLSQR_T_BUILD: T = A^T is formed by the library (t_* ignored, may be NULL;
+ *            requires host pointers);
+ *   t_mode = SFLSQR_T_GIVEN: T is the given n x m CSR — e.g. the unmatched
+ *            backprojector B ~ A^T.
+ * Columns need not be sorted.  Errors: rowptr not monotone / nnz mismatch /
+ * column out of range -> SFLSQR_E_DIM; non-finite value -> SFLSQR_E_NONFINITE. */
+int sflsqr_set_operator(sflsqr_t *h, int64_t m, int64_t n, const int64_t *a_rowptr, const int32_t *a_col,
+                        const double *a_val, int32_t t_mode, const int64_t *t_rowptr, const int32_t *t_col,
+                        const double *t_val, int32_t mem_flags);
+
+/* Matrix-free Gaussian blur (BASELINE.json config 2): m = n = H*W, separable
+ * taps g_t ~ exp(-t^2/(2 sigma^2)), t = -radius..radius, normalised to sum 1,
+ * zero boundary; symmetric, so T = A.  sigma > 0 and radius >= 0 else
+ * SFLSQR_E_INVALID. */
+int sflsqr_set_operator_blur(sflsqr_t *h, int32_t H, int32_t W, double sigma, int32_t radius);
+
+/* Sparse-sign sketch S in R^{d x dim} (readings R5/R6): dim = m for sFLSQR,
+ * n for sFLSMR (R4).  Column i has exactly s_nz distinct rows drawn by
+ * Philox4x32-10(key = seed, counter = (i, t, attempt)) with values
+ * +-1/sqrt(s_nz); s_nz = 1 is CountSketch.  S is never stored: rows and signs
+ * are regenerated from the hash in the kernels.  Requires 1 <= s_nz <= d <= 4096
+ * and d >= maxit (the projected problem needs k <= d) else SFLSQR_E_INVALID. */
+int sflsqr_set_sketch(sflsqr_t *h, uint64_t seed, int32_t d, int32_t s_nz);
+
+/* Flexible preconditioner tau_k (Alg. 1, Alg. 2):
+ * kind = SFLSQR_PRECOND_IDENTITY | IRN (p in (0, 2], eps_rel > 0; R7) |
+ * NONNEG (eps_rel > 0; R8).  Default: identity. */
+int sflsqr_set_precond(sflsqr_t *h, int32_t kind, double p, double eps_rel);
+
+/* Right-hand side b (length m) and start of a new solve: beta = ||b||,
+ * w_1 = b/beta, z = T w_1, s_b = S b (sFLSQR) or s = beta S z (sFLSMR)
+ * (Alg. 1, Alg. 2).  ||b|| = 0 -> SFLSQR_E_ZERO_RHS;
+ * non-finite -> SFLSQR_E_NONFINITE; len != m -> SFLSQR_E_DIM. */
+int sflsqr_set_rhs(sflsqr_t *h, const double *b, int64_t len, int32_t mem_flags);
+
+/* Run up to k more iterations (never beyond maxit or past a stop).  On return
+ * *done = 1 iff the solve has stopped and *status holds SFLSQR_* status.
+ * Blocks until the issued work is complete. */
+int sflsqr_iterate(sflsqr_t *h, int32_t k, int32_t *done, int32_t *status);
+
+/* x_{k_x} = Z_{k_x} y_{k_x} (Alg. 1 L504 / Alg. 2) into x (length n,
+ * host or device per mem_flags; caller owns the buffer).  x_0 = 0. */
+int sflsqr_get_x(sflsqr_t *h, double *x, int64_t len, int32_t mem_flags);
+
+/* Per-iteration histories (host buffers, either may be NULL):
+ *   true_res[k-1]   = ||b - A x_k||  (NaN when not recorded; R12)
+ *   sketch_res[k-1] = ||rhs - M_k y_k||, the projected sketched residual.
+ * Copies min(cap, k_done) entries; *count = k_done. */
+int sflsqr_get_residual_norms(sflsqr_t *h, double *true_res, double *sketch_res, int64_t cap, int64_t *count);
+
+int sflsqr_get_info(sflsqr_t *h, sflsqr_info *info);
+
+/* Debug: the sketch table for columns [col0, col0+ncols) as generated by the
+ * device hash (host outputs rows[ncols*s_nz], signs[ncols*s_nz] in {+1,-1}). */
+int sflsqr_debug_sketch_table(sflsqr_t *h, int64_t col0, int64_t ncols, int32_t *rows, int8_t *signs);
+
+/* Debug: y = A x (which = 0, x length n, y length m) or y = T x (which = 1,
+ * x length m, y length n), host buffers, through the same kernels the solve uses. */
+int sflsqr_debug_apply(sflsqr_t *h, int32_t which, const double *x, double *y);
+
+/* Debug: copies of the factorisation after k_done iterations (host buffers, any
+ * may be NULL): H (k_done+1) x k_done, Tm k_done x k_done, column-major;
+ * Z n x k_done and W m x (k_done+1), column-major; y (k_x). */
+int sflsqr_debug_basis(sflsqr_t *h, double *H, double *Tm, double *Z, double *W, double *y);
+
+/* Debug (state injection): the vectors the next iteration starts from, host
+ * buffers (any may be NULL): z = T w_{k_done+1} (n); x = x_{k_x} (n);
+ * p_ring = ell x n, row (j-1) mod ell holding p_j (zeros unless orth_mode = P and
+ * tau != id); sketch_cols = d x k_done S A z_j (sFLSQR) or d x (k_done+1) S T w_j
+ * (sFLSMR), column-major; rhs (d) = s_b or s_{A^T b}. */
+int sflsqr_debug_state(sflsqr_t *h, double *z, double *x, double *p_ring, double *sketch_cols, double *rhs);
+
+/* Profiling: on = 1 launches kernels eagerly (no graph) with CUDA events around
+ * every launch; sflsqr_get_profile returns the accumulated times since the last
+ * sflsqr_reset_profile. */
+int sflsqr_set_profiling(sflsqr_t *h, int32_t on);
+int sflsqr_reset_profile(sflsqr_t *h);
+int sflsqr_get_profile(sflsqr_t *h, sflsqr_profile *prof);
+
+/* Last error message of this handle ("" if none); h may be NULL (global errors). */
+const char *sflsqr_last_error(sflsqr_t *h);
+
+/* Free all library-owned host and device memory and the library stream. */
+void sflsqr_destroy(sflsqr_t *h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SFLSQR_H_ */

@@ -86,6 +86,105 @@ def tau_apply(kind, p_k, x_prev, k, p_exp=1.0, eps_rel=1e-3, fixed=None):
     raise ValueError(kind)
 
 
+class FGKState:
+    """Everything Alg. 1 / Alg. 2 carry from one iteration to the next."""
+
+    def __init__(self, m, n, maxit, method, rhs, beta, b):
+        self.m, self.n, self.method = m, n, method
+        self.W, self.Z, self.P = [], [], []            # w_1.., z_1.., p_1..
+        self.z = None                                  # current T w_k (before the z-orthogonalisation)
+        self.x_prev = np.zeros(n)                      # x_{k-1} (tau needs it)
+        self.H = np.zeros((maxit + 1, maxit))
+        self.Tm = np.zeros((maxit, maxit))
+        self.SAZ = []                                  # sFLSQR: columns S A z_j
+        self.STW = []                                  # sFLSMR: columns S T w_j
+        self.rhs, self.beta, self.b = rhs, beta, b
+
+
+def init_state(op, b, method, maxit, S):
+    """Alg. 1 L457-460 / Alg. 2 L759-763."""
+    b = np.asarray(b, dtype=np.float64)
+    beta = float(np.linalg.norm(b))
+    if beta == 0.0:
+        raise ValueError("||b|| = 0")
+    w1 = b / beta
+    z = op.tmatvec(w1)
+    if method == "sflsqr":
+        rhs = S(b)                          # s_b = S b
+    elif method == "sflsmr":
+        Sz = S(z)
+        rhs = beta * Sz                     # s_{A^T b} = beta S z
+    else:
+        raise ValueError(method)
+    st = FGKState(op.m, op.n, maxit, method, rhs, beta, b)
+    st.W.append(w1)
+    st.z = z
+    if method == "sflsmr":
+        st.STW.append(rhs / beta)           # S_{A^T W} = [s_{A^T b} / beta]
+    return st
+
+
+def fgk_step(op, st, k, ell, S, precond="identity", p_exp=1.0, eps_rel=1e-3, fixed_diag=None, orth_mode="P"):
+    """Iteration k of Alg. 1 (L462-496) / Alg. 2 (L765-797), updating st in place.
+
+    Returns a dict of the step's outputs, or {"breakdown": "z"} when z_k cannot be formed (R11).
+    """
+    m, n = st.m, st.n
+    out = {}
+    # L464-469: z-side windowed MGS + normalisation
+    z = st.z
+    z_in = float(np.linalg.norm(z))
+    for j in range(max(1, k - ell), k):
+        qj = st.P[j - 1] if orth_mode == "P" else st.Z[j - 1]
+        c = float(np.dot(qj, z))
+        z = z - c * qj
+        st.Tm[j - 1, k - 1] = c
+    t = float(np.linalg.norm(z))
+    if t == 0.0 or t <= 1e-14 * z_in:
+        return {"breakdown": "z"}
+    st.Tm[k - 1, k - 1] = t
+    p_k = z / t
+    st.P.append(p_k)
+    # L470-471: flexible preconditioner, Z = [Z, z_k]
+    z_k = tau_apply(precond, p_k, st.x_prev, k, p_exp, eps_rel, fixed_diag)
+    st.Z.append(z_k)
+    # L473-474: w = A z_k; S_AZ = [S_AZ, S w]
+    w = op.matvec(z_k)
+    w_in = float(np.linalg.norm(w))
+    if st.method == "sflsqr":
+        st.SAZ.append(S(w))
+    # L476-484: w-side windowed MGS
+    for j in range(max(1, k - ell), k + 1):
+        h = float(np.dot(st.W[j - 1], w))
+        st.H[j - 1, k - 1] = h
+        w = w - h * st.W[j - 1]
+    hn = float(np.linalg.norm(w))
+    w_breakdown = hn == 0.0 or hn <= 1e-14 * w_in
+    if w_breakdown:
+        # A z_k in span(W_k): H_{k+1,k} = 0, w_{k+1} := 0; y_k is still defined (R11)
+        st.W.append(np.zeros(m))
+        st.z = np.zeros(n)
+    else:
+        st.H[k, k - 1] = hn
+        st.W.append(w / hn)
+        # L486: z = A^T w_{k+1}
+        st.z = op.tmatvec(st.W[k])
+    # L488-490 / L790-797: projected sketched LS
+    if st.method == "sflsqr":
+        M = np.column_stack(st.SAZ)
+    else:
+        Sz = S(st.z)
+        M = np.column_stack(st.STW + [Sz]) @ st.H[:k + 1, :k]
+        out["Sz"] = Sz
+    y, _, ratio = householder_qr_solve(M, st.rhs)
+    sres = float(np.linalg.norm(st.rhs - M @ y))
+    x = np.column_stack(st.Z) @ y                 # L504 / L804: x_k = Z y_k
+    r = float(np.linalg.norm(st.b - op.matvec(x)))  # eq. discrP residual (R12)
+    out.update(p=p_k, z=z_k, w_next=st.W[k], Tcol=st.Tm[:k, k - 1].copy(), Hcol=st.H[:k + 1, k - 1].copy(),
+               Mcol=M[:, -1].copy(), M=M, y=y, sres=sres, x=x, r=r, ratio=ratio, w_breakdown=w_breakdown)
+    return out
+
+
 def solve(op, b, method="sflsqr", maxit=10, window=2, sketch=None, sketch_seed=0, d=None, s_nz=1,
           precond="identity", p_exp=1.0, eps_rel=1e-3, fixed_diag=None, tol=0.0, eta=0.0, delta_e=0.0,
           orth_mode="P", record=True):
@@ -96,117 +195,79 @@ def solve(op, b, method="sflsqr", maxit=10, window=2, sketch=None, sketch_seed=0
     sketch (sketch_seed, d, s_nz) on R^m (sFLSQR) or R^n (sFLSMR) - reading R4.
     """
     m, n = op.m, op.n
-    b = np.asarray(b, dtype=np.float64)
     ell = int(window)
     if sketch is None:
         sketch = SparseSignSketch(sketch_seed, d, s_nz, m if method == "sflsqr" else n)
     S = sketch.apply
-
-    # Alg. 1 L457-460 / Alg. 2 L759-763
-    beta = float(np.linalg.norm(b))
-    if beta == 0.0:
-        raise ValueError("||b|| = 0")
-    W = [b / beta]
-    z = op.tmatvec(W[0])
-    if method == "sflsqr":
-        rhs = S(b)                          # s_b = S b
-        SAZ = []
-    elif method == "sflsmr":
-        Sz = S(z)
-        rhs = beta * Sz                     # s_{A^T b} = beta S z
-        STW = [rhs / beta]                  # S_{A^T W} = [s_{A^T b} / beta]
-    else:
-        raise ValueError(method)
-    Z, P = [], []
-    H = np.zeros((maxit + 1, maxit))
-    Tm = np.zeros((maxit, maxit))
-    res = OracleResult(x=np.zeros(n), k=0, status=RUNNING, rhs=rhs)
-    x_prev = np.zeros(n)
+    st = init_state(op, b, method, maxit, S)
+    res = OracleResult(x=np.zeros(n), k=0, status=RUNNING, rhs=st.rhs)
     k_done = 0
     for k in range(1, maxit + 1):
-        # L464-469: z-side windowed MGS + normalisation
-        z_in = float(np.linalg.norm(z))
-        for j in range(max(1, k - ell), k):
-            qj = P[j - 1] if orth_mode == "P" else Z[j - 1]
-            c = float(np.dot(qj, z))
-            z = z - c * qj
-            Tm[j - 1, k - 1] = c
-        t = float(np.linalg.norm(z))
-        if t == 0.0 or t <= 1e-14 * z_in:
+        out = fgk_step(op, st, k, ell, S, precond, p_exp, eps_rel, fixed_diag, orth_mode)
+        if out.get("breakdown") == "z":
             res.status = BREAKDOWN
             break
-        Tm[k - 1, k - 1] = t
-        p_k = z / t
-        P.append(p_k)
-        # L470-471: flexible preconditioner, Z = [Z, z_k]
-        z_k = tau_apply(precond, p_k, x_prev, k, p_exp, eps_rel, fixed_diag)
-        Z.append(z_k)
-        # L473-474: w = A z_k; S_AZ = [S_AZ, S w]
-        w = op.matvec(z_k)
-        w_in = float(np.linalg.norm(w))
-        if method == "sflsqr":
-            SAZ.append(S(w))
-        # L476-484: w-side windowed MGS
-        for j in range(max(1, k - ell), k + 1):
-            h = float(np.dot(W[j - 1], w))
-            H[j - 1, k - 1] = h
-            w = w - h * W[j - 1]
-        hn = float(np.linalg.norm(w))
-        w_breakdown = hn == 0.0 or hn <= 1e-14 * w_in
-        if w_breakdown:
-            # A z_k in span(W_k): H_{k+1,k} = 0, w_{k+1} := 0; y_k is still defined (R11)
-            W.append(np.zeros(m))
-            z = np.zeros(n)
-        else:
-            H[k, k - 1] = hn
-            W.append(w / hn)
-            # L486: z = A^T w_{k+1}
-            z = op.tmatvec(W[k])
-        # L488-490 / L790-797: projected sketched LS
-        if method == "sflsqr":
-            M = np.column_stack(SAZ)
-        else:
-            Sz = S(z)
-            M = np.column_stack(STW + [Sz]) @ H[:k + 1, :k]
-        y, _, ratio = householder_qr_solve(M, rhs)
-        sres = float(np.linalg.norm(rhs - M @ y))
-        Zk = np.column_stack(Z)
-        x = Zk @ y                                   # L504 / L804: x_k = Z y_k
+        x, sres, r = out["x"], out["sres"], out["r"]
         k_done = k
         res.x, res.k = x, k
         res.sketch_res.append(sres)
-        res.rank_ratio.append(ratio)
-        r = float(np.linalg.norm(b - op.matvec(x)))  # eq. discrP residual
+        res.rank_ratio.append(out["ratio"])
         res.true_res.append(r)
         if record:
-            res.ys.append(y)
+            res.ys.append(out["y"])
             res.xs.append(x)
-        if w_breakdown:
+        if out["w_breakdown"]:
             res.status = BREAKDOWN
             break
         # L498 / L798 (R3): tol test; eq. discrP (R12)
-        if tol > 0.0 and sres < tol * float(np.linalg.norm(rhs)):
+        if tol > 0.0 and sres < tol * float(np.linalg.norm(st.rhs)):
             res.status = TOL
             break
         if eta > 0.0 and r <= eta * delta_e:
             res.status = DISCREPANCY
             break
         if method == "sflsmr":
-            STW.append(Sz)                           # L801
-        x_prev = x
+            st.STW.append(out["Sz"])                 # L801
+        st.x_prev = x
     else:
         res.status = MAXIT
-    kk = len(Z)
-    res.H = H[:k_done + 1, :k_done]
-    res.T = Tm[:kk, :kk]
-    res.Z = np.column_stack(Z) if Z else np.zeros((n, 0))
-    res.P = np.column_stack(P) if P else np.zeros((n, 0))
-    res.W = np.column_stack(W)
+    kk = len(st.Z)
+    res.H = st.H[:k_done + 1, :k_done]
+    res.T = st.Tm[:kk, :kk]
+    res.Z = np.column_stack(st.Z) if st.Z else np.zeros((n, 0))
+    res.P = np.column_stack(st.P) if st.P else np.zeros((n, 0))
+    res.W = np.column_stack(st.W)
     if method == "sflsqr":
-        res.sketch_cols = np.column_stack(SAZ) if SAZ else None
+        res.sketch_cols = np.column_stack(st.SAZ) if st.SAZ else None
     else:
-        res.sketch_cols = np.column_stack(STW)
+        res.sketch_cols = np.column_stack(st.STW)
     return res
+
+
+def step_from_state(op, b, method, k, window, sketch, Z_prev, P_window, W_prev, z, x_prev, H_prev, sketch_prev,
+                    rhs, precond="identity", p_exp=1.0, eps_rel=1e-3, orth_mode="P"):
+    """State injection: run iteration k of Alg. 1/2 from an externally supplied state.
+
+    Z_prev: n x (k-1) (z_1..z_{k-1}); P_window: {j: p_j} for the last ell j < k;
+    W_prev: m x k (w_1..w_k); z = T w_k; x_prev = x_{k-1}; H_prev: k x (k-1);
+    sketch_prev: d x (k-1) (S A z_j, sFLSQR) or d x k (S T w_j, sFLSMR); rhs: s_b / s_{A^T b}.
+    """
+    maxit = k
+    st = FGKState(op.m, op.n, maxit, method, np.asarray(rhs, dtype=np.float64), float(np.linalg.norm(b)),
+                  np.asarray(b, dtype=np.float64))
+    col = lambda M, j: np.ascontiguousarray(M[:, j], dtype=np.float64)  # noqa: E731
+    st.Z = [col(Z_prev, j) for j in range(Z_prev.shape[1])]
+    st.P = [None if P_window.get(j + 1) is None else np.ascontiguousarray(P_window[j + 1], dtype=np.float64)
+            for j in range(k - 1)]                             # only the window entries are used
+    st.W = [col(W_prev, j) for j in range(W_prev.shape[1])]
+    st.z = np.asarray(z, dtype=np.float64)
+    st.x_prev = np.asarray(x_prev, dtype=np.float64)
+    st.H[:k, :k - 1] = H_prev
+    if method == "sflsqr":
+        st.SAZ = [col(sketch_prev, j) for j in range(sketch_prev.shape[1])]
+    else:
+        st.STW = [col(sketch_prev, j) for j in range(sketch_prev.shape[1])]
+    return fgk_step(op, st, k, int(window), sketch.apply, precond, p_exp, eps_rel, None, orth_mode)
 
 
 def solve_problem(prob, spec, op=None, maxit=None, record=True, **over):

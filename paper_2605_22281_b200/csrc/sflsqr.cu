@@ -1,0 +1,988 @@
+// libsflsqr.so — host driver and C ABI (include/sflsqr.h) of the B200
+// sketched flexible Golub-Kahan step.  One iteration of Alg. 1 / Alg. 2
+// (PAPER.md L450-508 / L752-808) is enqueued as a fixed kernel sequence that
+// reads the iteration index from device memory, captured once into a CUDA
+// graph and replayed per iteration; the only host<->device traffic inside
+// iterate() is one small state read at the end.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "sflsqr.h"
+#include "sflsqr_kernels.cuh"
+
+using namespace sfl;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Prof {
+  std::vector<cudaEvent_t> ev;  // pairs
+  std::vector<int> cls;
+  std::vector<double> bytes;
+  int used = 0;
+  sflsqr_profile acc;
+  Prof() { std::memset(&acc, 0, sizeof(acc)); }
+};
+
+}  // namespace
+
+struct sflsqr {
+  sflsqr_opts o;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::string err;
+  // operator
+  bool op_set = false, blur = false;
+  int64_t m = 0, n = 0, nnz_a = 0, nnz_t = 0;
+  int64_t *a_rowptr = nullptr, *t_rowptr = nullptr;
+  int32_t *a_col = nullptr, *t_col = nullptr;
+  double *a_val = nullptr, *t_val = nullptr;
+  bool a_owned = true, t_owned = true;
+  int bH = 0, bW = 0, brad = 0;
+  double* taps = nullptr;
+  double* blur_tmp = nullptr;
+  // sketch
+  bool sk_set = false;
+  uint64_t seed = 0;
+  int d = 0, s_nz = 0, G = 1;
+  // precond
+  int pkind = SFLSQR_PRECOND_IDENTITY;
+  double p_exp = 1.0, eps_rel = 1e-3;
+  // solve
+  bool bufs = false, rhs_set = false;
+  Params P;
+  int nslots = 0;
+  std::vector<void*> solve_allocs;
+  std::vector<size_t> solve_sizes;
+  cudaGraphExec_t gexec = nullptr;
+  int kernels_per_iter = 0;
+  int64_t launches = 0;
+  int host_k = 1;  // host mirror (profiling byte model only)
+  bool prof_on = false;
+  Prof prof;
+};
+
+namespace {
+
+int fail(sflsqr_t* h, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (h)
+    h->err = buf;
+  else
+    g_err = buf;
+  return code;
+}
+
+#define CU(h, call)                                                                              \
+  do {                                                                                           \
+    cudaError_t e_ = (call);                                                                     \
+    if (e_ != cudaSuccess) return fail((h), SFLSQR_E_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+int dalloc(sflsqr_t* h, void** p, size_t bytes, std::vector<void*>* track, std::vector<size_t>* sizes = nullptr) {
+  if (bytes == 0) bytes = 8;
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(h, SFLSQR_E_OOM, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+  }
+  if (track) track->push_back(*p);
+  if (sizes) sizes->push_back(bytes);
+  return SFLSQR_OK;
+}
+
+int host_threads() {
+  unsigned hc = std::thread::hardware_concurrency();
+  return (int)std::max(1u, std::min(hc, 32u));
+}
+
+template <class F>
+void par_for(int64_t n, F f) {
+  int nt = host_threads();
+  if (n < (1 << 16) || nt == 1) {
+    f(0, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  int64_t chunk = (n + nt - 1) / nt;
+  for (int t = 0; t < nt; ++t) {
+    int64_t s = t * chunk, e = std::min(n, s + chunk);
+    if (s >= e) break;
+    th.emplace_back([=]() { f(s, e); });
+  }
+  for (auto& t : th) t.join();
+}
+
+// Validate a host CSR: rowptr monotone from 0, columns in range, values finite.
+int validate_csr(sflsqr_t* h, const char* name, int64_t nrows, int64_t ncols, const int64_t* rp, const int32_t* col,
+                 const double* val) {
+  if (!rp || !col || !val) return fail(h, SFLSQR_E_INVALID, "%s: NULL array", name);
+  if (rp[0] != 0) return fail(h, SFLSQR_E_DIM, "%s: rowptr[0] != 0", name);
+  std::atomic<int> bad_rp(0), bad_col(0), bad_val(0);
+  par_for(nrows, [&](int64_t s, int64_t e) {
+    for (int64_t i = s; i < e; ++i)
+      if (rp[i + 1] < rp[i]) bad_rp = 1;
+  });
+  if (bad_rp) return fail(h, SFLSQR_E_DIM, "%s: rowptr not monotone", name);
+  const int64_t nnz = rp[nrows];
+  par_for(nnz, [&](int64_t s, int64_t e) {
+    for (int64_t p = s; p < e; ++p) {
+      if (col[p] < 0 || col[p] >= ncols) bad_col = 1;
+      if (!std::isfinite(val[p])) bad_val = 1;
+    }
+  });
+  if (bad_col) return fail(h, SFLSQR_E_DIM, "%s: column index out of range", name);
+  if (bad_val) return fail(h, SFLSQR_E_NONFINITE, "%s: non-finite value", name);
+  return SFLSQR_OK;
+}
+
+// Host transpose (counting sort by column, parallel over row chunks; within each
+// output row entries keep increasing original-row order -> canonical, deterministic).
+void host_transpose(int64_t nrows, int64_t ncols, const int64_t* rp, const int32_t* col, const double* val,
+                    std::vector<int64_t>& trp, std::vector<int32_t>& tcol, std::vector<double>& tval) {
+  const int nt = std::min(host_threads(), 16);
+  const int64_t nnz = rp[nrows];
+  std::vector<int64_t> rs(nt + 1);
+  for (int t = 0; t <= nt; ++t) rs[t] = std::min(nrows, (nrows + nt - 1) / nt * t);
+  std::vector<std::vector<int32_t>> cnt(nt, std::vector<int32_t>(ncols, 0));
+  {
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t)
+      th.emplace_back([&, t]() {
+        auto& c = cnt[t];
+        for (int64_t p = rp[rs[t]]; p < rp[rs[t + 1]]; ++p) c[col[p]]++;
+      });
+    for (auto& x : th) x.join();
+  }
+  trp.assign(ncols + 1, 0);
+  for (int64_t j = 0; j < ncols; ++j) {
+    int64_t s = 0;
+    for (int t = 0; t < nt; ++t) s += cnt[t][j];
+    trp[j + 1] = trp[j] + s;
+  }
+  // per-thread starting offsets: off[t][j] = trp[j] + sum_{u<t} cnt[u][j]
+  std::vector<std::vector<int64_t>> off(nt, std::vector<int64_t>(ncols));
+  par_for(ncols, [&](int64_t s, int64_t e) {
+    for (int64_t j = s; j < e; ++j) {
+      int64_t o = trp[j];
+      for (int t = 0; t < nt; ++t) {
+        off[t][j] = o;
+        o += cnt[t][j];
+      }
+    }
+  });
+  cnt.clear();
+  tcol.resize(nnz);
+  tval.resize(nnz);
+  std::vector<std::thread> th;
+  for (int t = 0; t < nt; ++t)
+    th.emplace_back([&, t]() {
+      auto& o = off[t];
+      for (int64_t i = rs[t]; i < rs[t + 1]; ++i)
+        for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+          int64_t q = o[col[p]]++;
+          tcol[q] = (int32_t)i;
+          tval[q] = val[p];
+        }
+    });
+  for (auto& x : th) x.join();
+}
+
+void free_solve(sflsqr_t* h) {
+  if (h->gexec) {
+    cudaGraphExecDestroy(h->gexec);
+    h->gexec = nullptr;
+  }
+  for (void* p : h->solve_allocs) cudaFree(p);
+  h->solve_allocs.clear();
+  h->solve_sizes.clear();
+  h->bufs = false;
+  h->rhs_set = false;
+}
+
+void free_op(sflsqr_t* h) {
+  if (h->a_owned) {
+    cudaFree(h->a_rowptr);
+    cudaFree(h->a_col);
+    cudaFree(h->a_val);
+  }
+  if (h->t_owned) {
+    cudaFree(h->t_rowptr);
+    cudaFree(h->t_col);
+    cudaFree(h->t_val);
+  }
+  cudaFree(h->taps);
+  cudaFree(h->blur_tmp);
+  h->a_rowptr = h->t_rowptr = nullptr;
+  h->a_col = h->t_col = nullptr;
+  h->a_val = h->t_val = h->taps = h->blur_tmp = nullptr;
+  h->op_set = h->blur = false;
+  h->nnz_a = h->nnz_t = 0;
+}
+
+// ------------------------------------------------------------------ launch bookkeeping
+struct Launch {
+  sflsqr_t* h;
+  int cls;
+  double bytes;
+  Launch(sflsqr_t* h_, int cls_, double bytes_) : h(h_), cls(cls_), bytes(bytes_) {
+    if (h->prof_on) {
+      Prof& p = h->prof;
+      if ((int)p.ev.size() < 2 * (p.used + 1)) {
+        cudaEvent_t a, b;
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        p.ev.push_back(a);
+        p.ev.push_back(b);
+        p.cls.push_back(0);
+        p.bytes.push_back(0);
+      }
+      p.cls[p.used] = cls;
+      p.bytes[p.used] = bytes;
+      cudaEventRecord(p.ev[2 * p.used], h->stream);
+    }
+  }
+  ~Launch() {
+    if (h->prof_on) {
+      cudaEventRecord(h->prof.ev[2 * h->prof.used + 1], h->stream);
+      h->prof.used++;
+    }
+    h->launches++;
+  }
+};
+
+void prof_collect(sflsqr_t* h) {
+  Prof& p = h->prof;
+  if (p.used == 0) return;
+  cudaStreamSynchronize(h->stream);
+  for (int i = 0; i < p.used; ++i) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, p.ev[2 * i], p.ev[2 * i + 1]);
+    p.acc.ms[p.cls[i]] += ms;
+    p.acc.launches[p.cls[i]] += 1;
+    p.acc.bytes[p.cls[i]] += p.bytes[i];
+  }
+  p.used = 0;
+}
+
+// y = A x (which 0) or y = T x (which 1); x may be a k-relative column (x_ld != 0).
+void enqueue_apply(sflsqr_t* h, int which, const DevState* st, const double* x, int64_t x_ld, int x_koff,
+                   double* y, int cls) {
+  const int64_t nrows = which == 0 ? h->m : h->n;
+  if (h->blur) {
+    const int64_t nn = (int64_t)h->bH * h->bW;
+    const int grid = (int)std::min<int64_t>((nn + 255) / 256, 148 * 8);
+    {
+      Launch L(h, cls, 16.0 * nn);
+      k_blur_rows<<<grid, 256, 0, h->stream>>>(st, h->bH, h->bW, h->brad, h->taps, x, x_ld, x_koff, h->blur_tmp);
+    }
+    {
+      Launch L(h, cls, 16.0 * nn);
+      k_blur_cols<<<grid, 256, 0, h->stream>>>(st, h->bH, h->bW, h->brad, h->taps, h->blur_tmp, y);
+    }
+    return;
+  }
+  const int64_t* rp = which == 0 ? h->a_rowptr : h->t_rowptr;
+  const int32_t* col = which == 0 ? h->a_col : h->t_col;
+  const double* val = which == 0 ? h->a_val : h->t_val;
+  const int64_t nnz = which == 0 ? h->nnz_a : h->nnz_t;
+  const int64_t ncols = which == 0 ? h->n : h->m;
+  const double bytes = 12.0 * nnz + 8.0 * (nrows + 1) + 8.0 * ncols + 8.0 * nrows;
+  constexpr int WPB = kSpmvThreads / 32;
+  const int64_t want = (nrows + WPB - 1) / WPB;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, 148 * 8));
+  Launch L(h, cls, bytes);
+  k_spmv_csr<<<grid, kSpmvThreads, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
+}
+
+// S v for a vector of length len (global column offset 0) -> finalize target.
+void enqueue_sketch(sflsqr_t* h, const DevState* st, const double* v, int64_t len, int mult_beta, double* out,
+                    int64_t out_ld, int out_koff, double* out2) {
+  const size_t smem = (size_t)(kSkThreads / 32) * h->d * sizeof(double);
+  {
+    Launch L(h, SFLSQR_KC_SKETCH, 8.0 * len + 8.0 * kSkBlocks * h->d);
+    k_sketch_partial<<<kSkBlocks, kSkThreads, smem, h->stream>>>(st, v, len, 0, h->d, h->s_nz, h->G, h->P.seed_lo,
+                                                                  h->P.seed_hi, h->P.sk_scale, h->P.skpart);
+  }
+  {
+    Launch L(h, SFLSQR_KC_SKETCH, 8.0 * kSkBlocks * h->d);
+    const int grid = (h->d + 127) / 128;
+    k_sketch_finalize<<<grid, 128, 0, h->stream>>>(st, h->P.skpart, kSkBlocks, h->d, mult_beta, out, out_ld, out_koff,
+                                                   out2);
+  }
+}
+
+// One iteration k of Alg. 1 / Alg. 2.
+void enqueue_iteration(sflsqr_t* h) {
+  Params& P = h->P;
+  const int k = h->host_k;  // used only for the byte model
+  const double n8 = 8.0 * h->n, m8 = 8.0 * h->m;
+  // a1: z-side windowed MGS (ell + 1 passes; passes beyond the window exit early)
+  for (int pass = 0; pass <= P.ell; ++pass) {
+    const int J = std::min(P.ell, k - 1);
+    const double by = pass > J ? 0.0 : n8 * (1 + (pass > 0) * 2 + (pass < J));
+    Launch L(h, SFLSQR_KC_ORTH, by);
+    k_mgs_pass<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P, 0, pass);
+  }
+  // a1 end + a2: normalise, tau, store z_k
+  {
+    Launch L(h, SFLSQR_KC_TAU, n8 * (2 + (P.use_pring ? 1 : 0) + (P.precond ? 1 : 0)));
+    k_finish_z<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P);
+  }
+  // a3: w = A z_k  (z_k = Z[:, k-1])
+  enqueue_apply(h, 0, P.st, P.Z, h->n, -1, P.w, SFLSQR_KC_SPMV_A);
+  // a4 (sFLSQR): S_AZ[:, k] = S w
+  if (P.method == SFLSQR_METHOD_SFLSQR) enqueue_sketch(h, P.st, P.w, h->m, 0, P.Mcols, P.d, -1, nullptr);
+  // a5: w-side windowed MGS (ell + 2 passes) and normalisation
+  for (int pass = 0; pass <= P.ell + 1; ++pass) {
+    const int J = std::min(P.ell + 1, k);
+    const double by = pass > J ? 0.0 : m8 * (1 + (pass > 0) * 2 + (pass < J));
+    Launch L(h, SFLSQR_KC_ORTH, by);
+    k_mgs_pass<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P, 1, pass);
+  }
+  {
+    Launch L(h, SFLSQR_KC_ORTH, 2 * m8);
+    k_finish_w<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P);
+  }
+  // a6: z = T w_{k+1}  (w_{k+1} = W[:, k])
+  enqueue_apply(h, 1, P.st, P.W, h->m, 0, P.z, SFLSQR_KC_SPMV_T);
+  // a4 (sFLSMR): S z -> S_TW[:, k+1]
+  if (P.method == SFLSQR_METHOD_SFLSMR) enqueue_sketch(h, P.st, P.z, h->n, 0, P.STW, P.d, 0, nullptr);
+  // a7: projected sketched LS
+  {
+    Launch L(h, SFLSQR_KC_LS, 8.0 * P.d * (k + 2));
+    k_ls<<<1, kLsThreads, 0, h->stream>>>(P);
+  }
+  // a8: x_k = Z_k y_k (needed by tau_{k+1})
+  if (P.need_x) {
+    Launch L(h, SFLSQR_KC_XUPD, n8 * (k + 1));
+    k_xupdate<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P, 0);
+  }
+  // a9: true residual (W path) and stop tests
+  if (P.want_res) {
+    Launch L(h, SFLSQR_KC_RES, m8 * (k + 1));
+    k_res_partial<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P);
+  }
+  {
+    Launch L(h, SFLSQR_KC_STOP, 0.0);
+    k_stop<<<1, kVecThreads, 0, h->stream>>>(P);
+  }
+}
+
+int check_launch(sflsqr_t* h) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(h, SFLSQR_E_CUDA, "kernel launch: %s", cudaGetErrorString(e));
+  return SFLSQR_OK;
+}
+
+int alloc_solve(sflsqr_t* h) {
+  free_solve(h);
+  Params& P = h->P;
+  const int maxit = h->o.maxit, d = h->d, ell = h->o.window;
+  P.m = h->m;
+  P.n = h->n;
+  P.ell = ell;
+  P.maxit = maxit;
+  P.ldh = maxit + 1;
+  P.method = h->o.method;
+  P.orth_mode = h->o.orth_mode;
+  P.precond = h->pkind;
+  P.d = d;
+  P.s_nz = h->s_nz;
+  P.want_res = ((h->o.history & SFLSQR_HIST_TRUE_RES) || h->o.eta > 0.0) ? 1 : 0;
+  P.need_x = h->pkind != SFLSQR_PRECOND_IDENTITY ? 1 : 0;
+  P.use_pring = (h->o.orth_mode == SFLSQR_ORTH_P && h->pkind != SFLSQR_PRECOND_IDENTITY) ? 1 : 0;
+  P.p_exp = h->p_exp;
+  P.eps_rel = h->eps_rel;
+  P.tol = h->o.tol;
+  P.eta = h->o.eta;
+  P.delta_e = h->o.delta_e;
+  P.sk_scale = 1.0 / std::sqrt((double)h->s_nz);
+  P.seed_lo = (uint32_t)(h->seed & 0xffffffffu);
+  P.seed_hi = (uint32_t)(h->seed >> 32);
+  // partial-sum slots
+  int s = 0;
+  P.slot_beta = s++;
+  P.slot_zin = s++;
+  P.slot_z0 = s;
+  s += ell + 1;
+  P.slot_win = s++;
+  P.slot_w0 = s;
+  s += ell + 2;
+  P.slot_xmax = s++;
+  P.slot_res = s++;
+  h->nslots = s;
+  auto A = [&](double** p, size_t count) {
+    return dalloc(h, (void**)p, count * sizeof(double), &h->solve_allocs, &h->solve_sizes);
+  };
+  int rc;
+  const size_t n = (size_t)h->n, m = (size_t)h->m;
+  if ((rc = dalloc(h, (void**)&P.st, sizeof(DevState), &h->solve_allocs, &h->solve_sizes))) return rc;
+  if ((rc = A(&P.z, n)) || (rc = A(&P.x, n)) || (rc = A(&P.Z, n * maxit)) || (rc = A(&P.w, m)) ||
+      (rc = A(&P.W, m * (maxit + 1))) || (rc = A(&P.b, m)) || (rc = A(&P.H, (size_t)(maxit + 1) * maxit)) ||
+      (rc = A(&P.Tm, (size_t)maxit * maxit)) || (rc = A(&P.part, (size_t)s * kVecBlocks)) ||
+      (rc = A(&P.skpart, (size_t)kSkBlocks * d)) || (rc = A(&P.rhs, d)) || (rc = A(&P.Mcols, (size_t)d * maxit)) ||
+      (rc = A(&P.STW, (size_t)d * (maxit + 1))) || (rc = A(&P.V, (size_t)d * maxit)) || (rc = A(&P.taus, maxit)) ||
+      (rc = A(&P.R, (size_t)maxit * maxit)) || (rc = A(&P.qtb, d)) || (rc = A(&P.y, maxit)) ||
+      (rc = A(&P.g, maxit + 1)) || (rc = A(&P.hist_true, maxit)) || (rc = A(&P.hist_sk, maxit)))
+    return rc;
+  P.Pring = nullptr;
+  if (P.use_pring && (rc = A(&P.Pring, n * ell))) return rc;
+  // Debug aid (no sanitizer on this pool): SFLSQR_DEBUG_POISON=1 fills every solve
+  // buffer with NaN bytes so a read-before-write shows up as NaN in the results.
+  const char* poison = std::getenv("SFLSQR_DEBUG_POISON");
+  if (poison && poison[0] == '1') {
+    for (size_t i = 0; i < h->solve_allocs.size(); ++i)
+      if (h->solve_allocs[i] != (void*)P.st) CU(h, cudaMemset(h->solve_allocs[i], 0xFF, h->solve_sizes[i]));
+  }
+  h->bufs = true;
+  return SFLSQR_OK;
+}
+
+int zero_solve_state(sflsqr_t* h) {
+  Params& P = h->P;
+  const int maxit = h->o.maxit, d = h->d;
+  cudaStream_t s = h->stream;
+  CU(h, cudaMemsetAsync(P.st, 0, sizeof(DevState), s));
+  CU(h, cudaMemsetAsync(P.H, 0, sizeof(double) * (size_t)(maxit + 1) * maxit, s));
+  CU(h, cudaMemsetAsync(P.Tm, 0, sizeof(double) * (size_t)maxit * maxit, s));
+  CU(h, cudaMemsetAsync(P.R, 0, sizeof(double) * (size_t)maxit * maxit, s));
+  CU(h, cudaMemsetAsync(P.V, 0, sizeof(double) * (size_t)d * maxit, s));
+  CU(h, cudaMemsetAsync(P.Mcols, 0, sizeof(double) * (size_t)d * maxit, s));
+  CU(h, cudaMemsetAsync(P.STW, 0, sizeof(double) * (size_t)d * (maxit + 1), s));
+  CU(h, cudaMemsetAsync(P.y, 0, sizeof(double) * maxit, s));
+  CU(h, cudaMemsetAsync(P.x, 0, sizeof(double) * h->n, s));
+  CU(h, cudaMemsetAsync(P.hist_sk, 0, sizeof(double) * maxit, s));
+  CU(h, cudaMemsetAsync(P.part, 0, sizeof(double) * (size_t)h->nslots * kVecBlocks, s));
+  return SFLSQR_OK;
+}
+
+int build_graph(sflsqr_t* h) {
+  if (h->gexec) {
+    cudaGraphExecDestroy(h->gexec);
+    h->gexec = nullptr;
+  }
+  const int64_t before = h->launches;
+  const bool prof = h->prof_on;
+  h->prof_on = false;
+  cudaGraph_t g;
+  CU(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+  h->host_k = 1;
+  enqueue_iteration(h);
+  cudaError_t e = cudaStreamEndCapture(h->stream, &g);
+  h->prof_on = prof;
+  if (e != cudaSuccess) return fail(h, SFLSQR_E_CUDA, "graph capture: %s", cudaGetErrorString(e));
+  h->kernels_per_iter = (int)(h->launches - before);
+  h->launches = before;
+  e = cudaGraphInstantiate(&h->gexec, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return fail(h, SFLSQR_E_CUDA, "graph instantiate: %s", cudaGetErrorString(e));
+  return SFLSQR_OK;
+}
+
+int ensure_ready(sflsqr_t* h, bool need_rhs) {
+  if (!h) return fail(nullptr, SFLSQR_E_INVALID, "NULL handle");
+  if (!h->op_set) return fail(h, SFLSQR_E_STATE, "operator not set");
+  if (!h->sk_set) return fail(h, SFLSQR_E_STATE, "sketch not set");
+  if (need_rhs && !h->rhs_set) return fail(h, SFLSQR_E_STATE, "rhs not set");
+  return SFLSQR_OK;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+int sflsqr_version(void) { return SFLSQR_ABI_VERSION; }
+
+const char* sflsqr_last_error(sflsqr_t* h) { return h ? h->err.c_str() : g_err.c_str(); }
+
+int sflsqr_create(sflsqr_t** out, const sflsqr_opts* o) {
+  if (!out || !o) return fail(nullptr, SFLSQR_E_INVALID, "NULL argument");
+  *out = nullptr;
+  if (o->method != SFLSQR_METHOD_SFLSQR && o->method != SFLSQR_METHOD_SFLSMR)
+    return fail(nullptr, SFLSQR_E_INVALID, "method must be SFLSQR or SFLSMR");
+  if (o->window < 1) return fail(nullptr, SFLSQR_E_INVALID, "window must be >= 1");
+  if (o->maxit < 1) return fail(nullptr, SFLSQR_E_INVALID, "maxit must be >= 1");
+  if (o->maxit > kMaxD) return fail(nullptr, SFLSQR_E_INVALID, "maxit must be <= %d", kMaxD);
+  if (o->orth_mode != SFLSQR_ORTH_P && o->orth_mode != SFLSQR_ORTH_Z)
+    return fail(nullptr, SFLSQR_E_INVALID, "bad orth_mode");
+  if (!(o->tol >= 0.0) || !std::isfinite(o->tol)) return fail(nullptr, SFLSQR_E_INVALID, "tol must be >= 0");
+  if (!(o->eta == 0.0 || o->eta > 1.0) || !std::isfinite(o->eta))
+    return fail(nullptr, SFLSQR_E_INVALID, "eta must be 0 (off) or > 1");
+  if (!(o->delta_e >= 0.0) || !std::isfinite(o->delta_e))
+    return fail(nullptr, SFLSQR_E_INVALID, "delta_e must be >= 0");
+  if (o->world != 1 || o->rank != 0)
+    return fail(nullptr, SFLSQR_E_UNSUPPORTED, "this build runs one rank per solve (world = 1)");
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(nullptr, SFLSQR_E_CUDA, "no CUDA device: %s", cudaGetErrorString(e));
+  }
+  if (o->device < 0 || o->device >= ndev) return fail(nullptr, SFLSQR_E_INVALID, "bad device ordinal");
+  if (cudaSetDevice(o->device) != cudaSuccess) return fail(nullptr, SFLSQR_E_CUDA, "cudaSetDevice failed");
+  sflsqr_t* h = new sflsqr_t();
+  h->o = *o;
+  if (o->window > o->maxit) h->o.window = o->maxit;  // full orthogonalisation
+  if (o->stream && (cudaStream_t)o->stream != cudaStreamLegacy && (cudaStream_t)o->stream != cudaStreamPerThread) {
+    h->stream = (cudaStream_t)o->stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      delete h;
+      return fail(nullptr, SFLSQR_E_CUDA, "stream creation failed");
+    }
+    h->own_stream = true;
+  }
+  if (cudaFuncSetAttribute(k_sketch_partial, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (kSkThreads / 32) * kMaxD * (int)sizeof(double)) != cudaSuccess) {
+    cudaGetLastError();
+  }
+  *out = h;
+  return SFLSQR_OK;
+}
+
+int sflsqr_set_operator(sflsqr_t* h, int64_t m, int64_t n, const int64_t* a_rowptr, const int32_t* a_col,
+                        const double* a_val, int32_t t_mode, const int64_t* t_rowptr, const int32_t* t_col,
+                        const double* t_val, int32_t mem_flags) {
+  if (!h) return fail(nullptr, SFLSQR_E_INVALID, "NULL handle");
+  if (m < 1 || n < 1 || m > INT32_MAX || n > INT32_MAX) return fail(h, SFLSQR_E_DIM, "bad shape %lld x %lld",
+                                                                    (long long)m, (long long)n);
+  if (t_mode != SFLSQR_T_BUILD && t_mode != SFLSQR_T_GIVEN) return fail(h, SFLSQR_E_INVALID, "bad t_mode");
+  const bool dev = (mem_flags & SFLSQR_MEM_DEVICE) != 0;
+  const bool borrow = (mem_flags & SFLSQR_MEM_BORROW) != 0;
+  if (borrow && !dev) return fail(h, SFLSQR_E_INVALID, "BORROW requires device pointers");
+  if (dev && t_mode == SFLSQR_T_BUILD) return fail(h, SFLSQR_E_INVALID, "T_BUILD requires host arrays");
+  cudaSetDevice(h->o.device);
+  free_solve(h);
+  free_op(h);
+  int rc;
+  int64_t nnz_a, nnz_t = 0;
+  std::vector<int64_t> trp;
+  std::vector<int32_t> tcol;
+  std::vector<double> tval;
+  if (!dev) {
+    if ((rc = validate_csr(h, "A", m, n, a_rowptr, a_col, a_val))) return rc;
+    nnz_a = a_rowptr[m];
+    if (t_mode == SFLSQR_T_GIVEN) {
+      if ((rc = validate_csr(h, "T", n, m, t_rowptr, t_col, t_val))) return rc;
+      nnz_t = t_rowptr[n];
+    } else {
+      host_transpose(m, n, a_rowptr, a_col, a_val, trp, tcol, tval);
+      nnz_t = nnz_a;
+      t_rowptr = trp.data();
+      t_col = tcol.data();
+      t_val = tval.data();
+    }
+  } else {
+    if (!a_rowptr || !a_col || !a_val || !t_rowptr || !t_col || !t_val)
+      return fail(h, SFLSQR_E_INVALID, "NULL device array");
+    CU(h, cudaMemcpy(&nnz_a, a_rowptr + m, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    CU(h, cudaMemcpy(&nnz_t, t_rowptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost));
+  }
+  h->m = m;
+  h->n = n;
+  h->nnz_a = nnz_a;
+  h->nnz_t = nnz_t;
+  if (borrow) {
+    h->a_owned = h->t_owned = false;
+    h->a_rowptr = (int64_t*)a_rowptr;
+    h->a_col = (int32_t*)a_col;
+    h->a_val = (double*)a_val;
+    h->t_rowptr = (int64_t*)t_rowptr;
+    h->t_col = (int32_t*)t_col;
+    h->t_val = (double*)t_val;
+  } else {
+    h->a_owned = h->t_owned = true;
+    const cudaMemcpyKind kind = dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if ((rc = dalloc(h, (void**)&h->a_rowptr, sizeof(int64_t) * (m + 1), nullptr)) ||
+        (rc = dalloc(h, (void**)&h->a_col, sizeof(int32_t) * nnz_a, nullptr)) ||
+        (rc = dalloc(h, (void**)&h->a_val, sizeof(double) * nnz_a, nullptr)) ||
+        (rc = dalloc(h, (void**)&h->t_rowptr, sizeof(int64_t) * (n + 1), nullptr)) ||
+        (rc = dalloc(h, (void**)&h->t_col, sizeof(int32_t) * nnz_t, nullptr)) ||
+        (rc = dalloc(h, (void**)&h->t_val, sizeof(double) * nnz_t, nullptr))) {
+      free_op(h);
+      return rc;
+    }
+    CU(h, cudaMemcpy(h->a_rowptr, a_rowptr, sizeof(int64_t) * (m + 1), kind));
+    CU(h, cudaMemcpy(h->a_col, a_col, sizeof(int32_t) * nnz_a, kind));
+    CU(h, cudaMemcpy(h->a_val, a_val, sizeof(double) * nnz_a, kind));
+    CU(h, cudaMemcpy(h->t_rowptr, t_rowptr, sizeof(int64_t) * (n + 1), kind));
+    CU(h, cudaMemcpy(h->t_col, t_col, sizeof(int32_t) * nnz_t, kind));
+    CU(h, cudaMemcpy(h->t_val, t_val, sizeof(double) * nnz_t, kind));
+  }
+  h->op_set = true;
+  return SFLSQR_OK;
+}
+
+int sflsqr_set_operator_blur(sflsqr_t* h, int32_t H, int32_t W, double sigma, int32_t radius) {
+  if (!h) return fail(nullptr, SFLSQR_E_INVALID, "NULL handle");
+  if (H < 1 || W < 1) return fail(h, SFLSQR_E_DIM, "bad image shape");
+  if (!(sigma > 0.0) || !std::isfinite(sigma) || radius < 0) return fail(h, SFLSQR_E_INVALID, "sigma > 0, radius >= 0");
+  cudaSetDevice(h->o.device);
+  free_solve(h);
+  free_op(h);
+  std::vector<double> g(2 * radius + 1);
+  double s = 0.0;
+  for (int t = -radius; t <= radius; ++t) {
+    g[t + radius] = std::exp(-(double)t * t / (2.0 * sigma * sigma));
+    s += g[t + radius];
+  }
+  for (auto& v : g) v /= s;
+  int rc;
+  const int64_t nn = (int64_t)H * W;
+  if ((rc = dalloc(h, (void**)&h->taps, sizeof(double) * g.size(), nullptr)) ||
+      (rc = dalloc(h, (void**)&h->blur_tmp, sizeof(double) * nn, nullptr)))
+    return rc;
+  CU(h, cudaMemcpy(h->taps, g.data(), sizeof(double) * g.size(), cudaMemcpyHostToDevice));
+  h->blur = true;
+  h->bH = H;
+  h->bW = W;
+  h->brad = radius;
+  h->m = h->n = nn;
+  h->op_set = true;
+  return SFLSQR_OK;
+}
+
+int sflsqr_set_sketch(sflsqr_t* h, uint64_t seed, int32_t d, int32_t s_nz) {
+  if (!h) return fail(nullptr, SFLSQR_E_INVALID, "NULL handle");
+  if (d < 1 || d > kMaxD) return fail(h, SFLSQR_E_INVALID, "need 1 <= d <= %d", kMaxD);
+  if (s_nz < 1 || s_nz > d || s_nz > 32) return fail(h, SFLSQR_E_INVALID, "need 1 <= s <= min(d, 32)");
+  if (d < h->o.maxit) return fail(h, SFLSQR_E_INVALID, "need d >= maxit (k <= d for the projected problem)");
+  free_solve(h);
+  h->seed = seed;
+  h->d = d;
+  h->s_nz = s_nz;
+  int G = 1;
+  while (G < s_nz) G <<= 1;
+  h->G = G;
+  h->sk_set = true;
+  return SFLSQR_OK;
+}
+
+int sflsqr_set_precond(sflsqr_t* h, int32_t kind, double p, double eps_rel) {
+  if (!h) return fail(nullptr, SFLSQR_E_INVALID, "NULL handle");
+  if (kind != SFLSQR_PRECOND_IDENTITY && kind != SFLSQR_PRECOND_IRN && kind != SFLSQR_PRECOND_NONNEG)
+    return fail(h, SFLSQR_E_INVALID, "bad preconditioner kind");
+  if (kind == SFLSQR_PRECOND_IRN && !(p > 0.0 && p <= 2.0)) return fail(h, SFLSQR_E_INVALID, "IRN needs p in (0,2]");
+  if (kind != SFLSQR_PRECOND_IDENTITY && !(eps_rel > 0.0 && std::isfinite(eps_rel)))
+    return fail(h, SFLSQR_E_INVALID, "eps_rel must be > 0");
+  free_solve(h);
+  h->pkind = kind;
+  h->p_exp = kind == SFLSQR_PRECOND_IRN ? p : 1.0;
+  h->eps_rel = kind == SFLSQR_PRECOND_IDENTITY ? 1e-3 : eps_rel;
+  return SFLSQR_OK;
+}
+
+int sflsqr_set_rhs(sflsqr_t* h, const double* b, int64_t len, int32_t mem_flags) {
+  int rc;
+  if ((rc = ensure_ready(h, false))) return rc;
+  if (!b) return fail(h, SFLSQR_E_INVALID, "NULL b");
+  if (len != h->m) return fail(h, SFLSQR_E_DIM, "len(b) = %lld != m = %lld", (long long)len, (long long)h->m);
+  cudaSetDevice(h->o.device);
+  const bool dev = (mem_flags & SFLSQR_MEM_DEVICE) != 0;
+  if (!dev) {
+    double nrm = 0.0;
+    for (int64_t i = 0; i < len; ++i) {
+      if (!std::isfinite(b[i])) return fail(h, SFLSQR_E_NONFINITE, "b has a non-finite entry");
+      nrm += b[i] * b[i];
+    }
+    if (nrm == 0.0) return fail(h, SFLSQR_E_ZERO_RHS, "||b|| = 0");
+  }
+  if (!h->bufs && (rc = alloc_solve(h))) return rc;
+  h->rhs_set = false;
+  Params& P = h->P;
+  if ((rc = zero_solve_state(h))) return rc;
+  CU(h, cudaMemcpyAsync(P.b, b, sizeof(double) * len, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                        h->stream));
+  // Alg. 1 L457 / Alg. 2: beta = ||b||, w_1 = b / beta
+  {
+    Launch L(h, SFLSQR_KC_ORTH, 8.0 * h->m);
+    k_norm_partial<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P, P.b, h->m, P.slot_beta);
+  }
+  {
+    Launch L(h, SFLSQR_KC_ORTH, 16.0 * h->m);
+    k_init_w1<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P);
+  }
+  // L458 / L760: z = T w_1
+  enqueue_apply(h, 1, P.st, P.W, 0, 0, P.z, SFLSQR_KC_SPMV_T);
+  if (P.method == SFLSQR_METHOD_SFLSQR) {
+    // L459: s_b = S b
+    enqueue_sketch(h, P.st, P.b, h->m, 0, P.rhs, 0, 0, nullptr);
+  } else {
+    // L761-762: s = beta S z, S_TW = [S z]
+    enqueue_sketch(h, P.st, P.z, h->n, 1, P.rhs, 0, 0, P.STW);
+  }
+  {
+    Launch L(h, SFLSQR_KC_LS, 16.0 * h->d);
+    k_init_ls<<<1, kVecThreads, 0, h->stream>>>(P);
+  }
+  if ((rc = check_launch(h))) return rc;
+  if (!dev) {
+    // nothing else: host norm checked above
+  } else {
+    DevState st;
+    CU(h, cudaMemcpyAsync(&st, P.st, sizeof(st), cudaMemcpyDeviceToHost, h->stream));
+    CU(h, cudaStreamSynchronize(h->stream));
+    if (!(st.beta > 0.0)) return fail(h, SFLSQR_E_ZERO_RHS, "||b|| = 0");
+    if (!std::isfinite(st.beta)) return fail(h, SFLSQR_E_NONFINITE, "b has a non-finite entry");
+  }
+  h->host_k = 1;
+  h->rhs_set = true;
+  if (h->o.use_graph && !h->gexec) {
+    if ((rc = build_graph(h))) return rc;
+  }
+  return SFLSQR_OK;
+}
+
+int sflsqr_iterate(sflsqr_t* h, int32_t k, int32_t* done, int32_t* status) {
+  int rc;
+  if ((rc = ensure_ready(h, true))) return rc;
+  if (k < 0) return fail(h, SFLSQR_E_INVALID, "k must be >= 0");
+  cudaSetDevice(h->o.device);
+  DevState st;
+  CU(h, cudaMemcpyAsync(&st, h->P.st, sizeof(st), cudaMemcpyDeviceToHost, h->stream));
+  CU(h, cudaStreamSynchronize(h->stream));
+  int todo = st.done ? 0 : std::min(k, h->o.maxit - (st.k - 1));
+  h->host_k = st.k;
+  for (int i = 0; i < todo; ++i) {
+    if (h->gexec && !h->prof_on) {
+      CU(h, cudaGraphLaunch(h->gexec, h->stream));
+      h->launches += h->kernels_per_iter;
+    } else {
+      enqueue_iteration(h);
+    }
+    h->host_k++;
+  }
+  if ((rc = check_launch(h))) return rc;
+  CU(h, cudaMemcpyAsync(&st, h->P.st, sizeof(st), cudaMemcpyDeviceToHost, h->stream));
+  CU(h, cudaStreamSynchronize(h->stream));
+  if (h->prof_on) prof_collect(h);
+  if (done) *done = st.done;
+  if (status) *status = st.done ? st.status : SFLSQR_RUNNING;
+  return SFLSQR_OK;
+}
+
+int sflsqr_get_x(sflsqr_t* h, double* x, int64_t len, int32_t mem_flags) {
+  int rc;
+  if ((rc = ensure_ready(h, true))) return rc;
+  if (!x) return fail(h, SFLSQR_E_INVALID, "NULL x");
+  if (len != h->n) return fail(h, SFLSQR_E_DIM, "len(x) != n");
+  cudaSetDevice(h->o.device);
+  {
+    Launch L(h, SFLSQR_KC_XUPD, 8.0 * h->n);
+    k_xupdate<<<kVecBlocks, kVecThreads, 0, h->stream>>>(h->P, 1);
+  }
+  if ((rc = check_launch(h))) return rc;
+  const bool dev = (mem_flags & SFLSQR_MEM_DEVICE) != 0;
+  CU(h, cudaMemcpyAsync(x, h->P.x, sizeof(double) * len, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                        h->stream));
+  CU(h, cudaStreamSynchronize(h->stream));
+  if (h->prof_on) prof_collect(h);
+  return SFLSQR_OK;
+}
+
+int sflsqr_get_residual_norms(sflsqr_t* h, double* true_res, double* sketch_res, int64_t cap, int64_t* count) {
+  int rc;
+  if ((rc = ensure_ready(h, true))) return rc;
+  cudaSetDevice(h->o.device);
+  DevState st;
+  CU(h, cudaMemcpyAsync(&st, h->P.st, sizeof(st), cudaMemcpyDeviceToHost, h->stream));
+  CU(h, cudaStreamSynchronize(h->stream));
+  const int64_t kd = st.k - 1;
+  const int64_t nc = std::max<int64_t>(0, std::min(cap, kd));
+  if (true_res && nc) {
+    if (h->P.want_res) {
+      CU(h, cudaMemcpy(true_res, h->P.hist_true, sizeof(double) * nc, cudaMemcpyDeviceToHost));
+    } else {
+      for (int64_t i = 0; i < nc; ++i) true_res[i] = NAN;
+    }
+  }
+  if (sketch_res && nc) CU(h, cudaMemcpy(sketch_res, h->P.hist_sk, sizeof(double) * nc, cudaMemcpyDeviceToHost));
+  if (count) *count = kd;
+  return SFLSQR_OK;
+}
+
+int sflsqr_get_info(sflsqr_t* h, sflsqr_info* info) {
+  if (!h || !info) return fail(h, SFLSQR_E_INVALID, "NULL argument");
+  std::memset(info, 0, sizeof(*info));
+  info->m = h->m;
+  info->n = h->n;
+  info->nnz_a = h->nnz_a;
+  info->nnz_t = h->nnz_t;
+  info->launches = h->launches;
+  if (h->rhs_set) {
+    cudaSetDevice(h->o.device);
+    DevState st;
+    CU(h, cudaMemcpyAsync(&st, h->P.st, sizeof(st), cudaMemcpyDeviceToHost, h->stream));
+    CU(h, cudaStreamSynchronize(h->stream));
+    info->k_done = st.k - 1;
+    info->k_x = st.k_x;
+    info->status = st.done ? st.status : SFLSQR_RUNNING;
+    info->rank_flag = st.rank_flag;
+    info->beta = st.beta;
+  }
+  return SFLSQR_OK;
+}
+
+int sflsqr_debug_sketch_table(sflsqr_t* h, int64_t col0, int64_t ncols, int32_t* rows, int8_t* signs) {
+  if (!h) return fail(nullptr, SFLSQR_E_INVALID, "NULL handle");
+  if (!h->sk_set) return fail(h, SFLSQR_E_STATE, "sketch not set");
+  if (col0 < 0 || ncols < 0 || !rows || !signs) return fail(h, SFLSQR_E_INVALID, "bad arguments");
+  if (ncols == 0) return SFLSQR_OK;
+  cudaSetDevice(h->o.device);
+  int* drows = nullptr;
+  int8_t* dsig = nullptr;
+  int rc;
+  if ((rc = dalloc(h, (void**)&drows, sizeof(int) * ncols * h->s_nz, nullptr))) return rc;
+  if ((rc = dalloc(h, (void**)&dsig, ncols * h->s_nz, nullptr))) {
+    cudaFree(drows);
+    return rc;
+  }
+  const int grid = (int)std::min<int64_t>((ncols * h->G + 255) / 256 + 1, 148 * 16);
+  {
+    Launch L(h, SFLSQR_KC_SKETCH, 0.0);
+    k_sketch_table<<<grid, 256, 0, h->stream>>>(col0, ncols, h->d, h->s_nz, h->G, (uint32_t)(h->seed & 0xffffffffu),
+                                                (uint32_t)(h->seed >> 32), drows, dsig);
+  }
+  rc = check_launch(h);
+  if (!rc) {
+    cudaMemcpyAsync(rows, drows, sizeof(int) * ncols * h->s_nz, cudaMemcpyDeviceToHost, h->stream);
+    cudaMemcpyAsync(signs, dsig, ncols * h->s_nz, cudaMemcpyDeviceToHost, h->stream);
+    if (cudaStreamSynchronize(h->stream) != cudaSuccess) rc = fail(h, SFLSQR_E_CUDA, "sketch table copy failed");
+  }
+  cudaFree(drows);
+  cudaFree(dsig);
+  if (h->prof_on) prof_collect(h);
+  return rc;
+}
+
+int sflsqr_debug_apply(sflsqr_t* h, int32_t which, const double* x, double* y) {
+  if (!h) return fail(nullptr, SFLSQR_E_INVALID, "NULL handle");
+  if (!h->op_set) return fail(h, SFLSQR_E_STATE, "operator not set");
+  if ((which != 0 && which != 1) || !x || !y) return fail(h, SFLSQR_E_INVALID, "bad arguments");
+  cudaSetDevice(h->o.device);
+  const int64_t nin = which == 0 ? h->n : h->m, nout = which == 0 ? h->m : h->n;
+  double *dx = nullptr, *dy = nullptr;
+  int rc;
+  if ((rc = dalloc(h, (void**)&dx, sizeof(double) * nin, nullptr))) return rc;
+  if ((rc = dalloc(h, (void**)&dy, sizeof(double) * nout, nullptr))) {
+    cudaFree(dx);
+    return rc;
+  }
+  cudaMemcpyAsync(dx, x, sizeof(double) * nin, cudaMemcpyHostToDevice, h->stream);
+  enqueue_apply(h, which, nullptr, dx, 0, 0, dy, which == 0 ? SFLSQR_KC_SPMV_A : SFLSQR_KC_SPMV_T);
+  rc = check_launch(h);
+  if (!rc) {
+    cudaMemcpyAsync(y, dy, sizeof(double) * nout, cudaMemcpyDeviceToHost, h->stream);
+    if (cudaStreamSynchronize(h->stream) != cudaSuccess) rc = fail(h, SFLSQR_E_CUDA, "apply failed");
+  }
+  cudaFree(dx);
+  cudaFree(dy);
+  if (h->prof_on) prof_collect(h);
+  return rc;
+}
+
+int sflsqr_debug_basis(sflsqr_t* h, double* H, double* Tm, double* Z, double* W, double* y) {
+  int rc;
+  if ((rc = ensure_ready(h, true))) return rc;
+  cudaSetDevice(h->o.device);
+  DevState st;
+  CU(h, cudaMemcpyAsync(&st, h->P.st, sizeof(st), cudaMemcpyDeviceToHost, h->stream));
+  CU(h, cudaStreamSynchronize(h->stream));
+  const int kd = st.k - 1, maxit = h->o.maxit;
+  for (int j = 0; j < kd; ++j) {
+    if (H) CU(h, cudaMemcpy(H + (size_t)j * (kd + 1), h->P.H + (size_t)j * (maxit + 1), sizeof(double) * (kd + 1),
+                            cudaMemcpyDeviceToHost));
+    if (Tm) CU(h, cudaMemcpy(Tm + (size_t)j * kd, h->P.Tm + (size_t)j * maxit, sizeof(double) * kd,
+                             cudaMemcpyDeviceToHost));
+  }
+  if (Z && kd) CU(h, cudaMemcpy(Z, h->P.Z, sizeof(double) * h->n * kd, cudaMemcpyDeviceToHost));
+  if (W) CU(h, cudaMemcpy(W, h->P.W, sizeof(double) * h->m * (kd + 1), cudaMemcpyDeviceToHost));
+  if (y && st.k_x) CU(h, cudaMemcpy(y, h->P.y, sizeof(double) * st.k_x, cudaMemcpyDeviceToHost));
+  return SFLSQR_OK;
+}
+
+int sflsqr_debug_state(sflsqr_t* h, double* z, double* x, double* p_ring, double* sketch_cols, double* rhs) {
+  int rc;
+  if ((rc = ensure_ready(h, true))) return rc;
+  cudaSetDevice(h->o.device);
+  DevState st;
+  CU(h, cudaMemcpyAsync(&st, h->P.st, sizeof(st), cudaMemcpyDeviceToHost, h->stream));
+  CU(h, cudaStreamSynchronize(h->stream));
+  const int kd = st.k - 1;
+  const Params& P = h->P;
+  if (x) {
+    {
+      Launch L(h, SFLSQR_KC_XUPD, 8.0 * h->n);
+      k_xupdate<<<kVecBlocks, kVecThreads, 0, h->stream>>>(h->P, 1);
+    }
+    if ((rc = check_launch(h))) return rc;
+    CU(h, cudaMemcpyAsync(x, P.x, sizeof(double) * h->n, cudaMemcpyDeviceToHost, h->stream));
+  }
+  if (z) CU(h, cudaMemcpyAsync(z, P.z, sizeof(double) * h->n, cudaMemcpyDeviceToHost, h->stream));
+  if (p_ring) {
+    if (P.use_pring)
+      CU(h, cudaMemcpyAsync(p_ring, P.Pring, sizeof(double) * h->n * P.ell, cudaMemcpyDeviceToHost, h->stream));
+    else
+      std::memset(p_ring, 0, sizeof(double) * h->n * P.ell);
+  }
+  if (sketch_cols) {
+    const int nc = P.method == SFLSQR_METHOD_SFLSQR ? kd : kd + 1;
+    const double* src = P.method == SFLSQR_METHOD_SFLSQR ? P.Mcols : P.STW;
+    if (nc > 0)
+      CU(h, cudaMemcpyAsync(sketch_cols, src, sizeof(double) * P.d * nc, cudaMemcpyDeviceToHost, h->stream));
+  }
+  if (rhs) CU(h, cudaMemcpyAsync(rhs, P.rhs, sizeof(double) * P.d, cudaMemcpyDeviceToHost, h->stream));
+  CU(h, cudaStreamSynchronize(h->stream));
+  if (h->prof_on) prof_collect(h);
+  return SFLSQR_OK;
+}
+
+int sflsqr_set_profiling(sflsqr_t* h, int32_t on) {
+  if (!h) return fail(nullptr, SFLSQR_E_INVALID, "NULL handle");
+  h->prof_on = on != 0;
+  return SFLSQR_OK;
+}
+
+int sflsqr_reset_profile(sflsqr_t* h) {
+  if (!h) return fail(nullptr, SFLSQR_E_INVALID, "NULL handle");
+  if (h->prof.used) prof_collect(h);
+  std::memset(&h->prof.acc, 0, sizeof(h->prof.acc));
+  return SFLSQR_OK;
+}
+
+int sflsqr_get_profile(sflsqr_t* h, sflsqr_profile* p) {
+  if (!h || !p) return fail(h, SFLSQR_E_INVALID, "NULL argument");
+  if (h->prof.used) prof_collect(h);
+  *p = h->prof.acc;
+  return SFLSQR_OK;
+}
+
+void sflsqr_destroy(sflsqr_t* h) {
+  if (!h) return;
+  cudaSetDevice(h->o.device);
+  cudaStreamSynchronize(h->stream);
+  free_solve(h);
+  free_op(h);
+  for (auto e : h->prof.ev) cudaEventDestroy(e);
+  if (h->own_stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+}  // extern "C"

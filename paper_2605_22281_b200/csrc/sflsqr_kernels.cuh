@@ -1,0 +1,783 @@
+// sm_100a kernels of the sketched flexible Golub-Kahan step (sFLSQR / sFLSMR).
+//
+// Every kernel below maps to a row of SURVEY.md §8(a) and cites the PAPER.md
+// passage it implements.  All reductions are deterministic: fixed per-thread
+// order, fixed shuffle trees, per-block partials summed in block order by the
+// consumer (no floating-point atomics).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sfl {
+
+constexpr int kVecThreads = 256;          // vector kernels
+constexpr int kVecBlocks = 148 * 4;       // 4 CTAs per SM on 148 SMs, grid-stride
+constexpr int kSpmvThreads = 256;         // 8 warps, one row per warp at a time
+constexpr int kSkThreads = 256;           // sketch kernel: 8 warps, one d-bin set per warp
+constexpr int kSkBlocks = 148 * 2;
+constexpr int kLsThreads = 512;           // one CTA solves the projected problem
+constexpr int kMaxD = 2048;               // sketch rows supported by the one-CTA LS
+
+// Device-resident solve state (read by every kernel of a captured iteration).
+struct DevState {
+  int k;          // next iteration to execute (1-based)
+  int done;       // 1 once a stop/breakdown has been taken
+  int status;     // SFLSQR_* status
+  int k_x;        // iterate held in y (x_{k_x} = Z_{k_x} y)
+  int wbreak;     // w-side breakdown in the current iteration (reading R11)
+  int rank_flag;  // R14
+  int pad0, pad1;
+  double beta;    // ||b||
+  double rhs_norm;
+};
+
+// Everything a kernel needs; passed by value (captured into the graph).
+struct Params {
+  DevState* st;
+  int64_t m, n;
+  int ell, maxit, method, orth_mode, precond, d, s_nz, want_res, need_x, use_pring;
+  int ldh;                 // leading dimension of H = maxit + 1
+  double p_exp, eps_rel, tol, eta, delta_e, sk_scale;
+  uint32_t seed_lo, seed_hi;
+  // n-side vectors
+  double *z, *x, *Z, *Pring;
+  // m-side vectors
+  double *w, *W, *b;
+  // factorisation
+  double *H, *Tm;
+  // partial sums: nslots x kVecBlocks
+  double* part;
+  int slot_zin, slot_z0, slot_win, slot_w0, slot_xmax, slot_res, slot_beta;
+  // sketch
+  double *skpart, *rhs, *Mcols, *STW;
+  // projected LS
+  double *V, *taus, *R, *qtb, *y, *g;
+  // history
+  double *hist_true, *hist_sk;
+};
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Deterministic block sum, result returned to every thread. sh: >= 33 doubles.
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();  // protect sh from a previous use
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    double t = (lane < NT / 32) ? sh[lane] : 0.0;
+    t = warp_sum(t);
+    if (lane == 0) sh[32] = t;
+  }
+  __syncthreads();
+  return sh[32];
+}
+template <int NT>
+__device__ __forceinline__ double block_max(double v, double* sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  v = warp_max(v);
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    double t = (lane < NT / 32) ? sh[lane] : -INFINITY;
+    t = warp_max(t);
+    if (lane == 0) sh[32] = t;
+  }
+  __syncthreads();
+  return sh[32];
+}
+// Sum of nb per-block partials in fixed order (every block gets the same value).
+template <int NT>
+__device__ __forceinline__ double sum_partials(const double* part, int nb, double* sh) {
+  double v = 0.0;
+  for (int i = threadIdx.x; i < nb; i += NT) v += part[i];
+  return block_sum<NT>(v, sh);
+}
+template <int NT>
+__device__ __forceinline__ double max_partials(const double* part, int nb, double* sh) {
+  double v = -INFINITY;
+  for (int i = threadIdx.x; i < nb; i += NT) v = fmax(v, part[i]);
+  return block_max<NT>(v, sh);
+}
+
+// Streaming (read-once) loads: bypass L1 allocation so L1 keeps the gathered vector.
+__device__ __forceinline__ int4 ld_stream_i4(const int4* p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ double2 ld_stream_d2(const double2* p) {
+  double2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v2.f64 {%0,%1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ int ld_stream_i(const int* p) {
+  int r;
+  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ double ld_stream_d(const double* p) {
+  double r;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
+  return r;
+}
+
+// ------------------------------------------------------------------ Philox
+// Philox4x32-10 (Salmon et al., SC'11), written from the published round
+// function; independent of the oracle's host version (bit-exact match is tested).
+__device__ __forceinline__ void philox4x32_10(uint32_t& c0, uint32_t& c1, uint32_t& c2, uint32_t& c3,
+                                              uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    const uint32_t lo0 = 0xD2511F53u * c0, hi0 = __umulhi(0xD2511F53u, c0);
+    const uint32_t lo1 = 0xCD9E8D57u * c2, hi1 = __umulhi(0xCD9E8D57u, c2);
+    const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+  }
+}
+
+// One draw of the sparse-sign table (reading R6): row in [0,d), neg = sign bit.
+__device__ __forceinline__ void sk_draw(uint64_t i, uint32_t t, uint32_t attempt, uint32_t d, uint32_t k0,
+                                        uint32_t k1, int& row, int& neg) {
+  uint32_t c0 = (uint32_t)(i & 0xffffffffu), c1 = (uint32_t)(i >> 32), c2 = t, c3 = attempt;
+  philox4x32_10(c0, c1, c2, c3, k0, k1);
+  row = (int)__umulhi(c0, d);
+  neg = (int)(c1 & 1u);
+}
+
+// Sequential definition for one column (rare collision path): rows distinct,
+// attempt incremented on a duplicate of an earlier nonzero of the same column.
+__device__ void sk_column_seq(uint64_t i, int s, uint32_t d, uint32_t k0, uint32_t k1, int* rows, int* negs) {
+  for (int t = 0; t < s; ++t) {
+    for (uint32_t a = 0;; ++a) {
+      int r, ng;
+      sk_draw(i, (uint32_t)t, a, d, k0, k1, r, ng);
+      bool dup = false;
+      for (int u = 0; u < t; ++u) dup |= (rows[u] == r);
+      if (!dup) {
+        rows[t] = r;
+        negs[t] = ng;
+        break;
+      }
+    }
+  }
+}
+
+// Warp-cooperative table: lanes form groups of G (power of two >= s); lane gl of
+// a group holds nonzero t = gl of coordinate i (valid if gl < s).  Attempt-0
+// rows are final unless they collide with a lower lane; colliding groups are
+// resolved by the group's leader with the sequential definition.
+__device__ __forceinline__ void sk_warp_entries(uint64_t i, bool valid, int s, int G, uint32_t d, uint32_t k0,
+                                                uint32_t k1, int& row, int& neg) {
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (G - 1), gbase = lane - gl;
+  const bool act = valid && gl < s;
+  row = -1;
+  neg = 0;
+  if (act) sk_draw(i, (uint32_t)gl, 0u, d, k0, k1, row, neg);
+  bool coll = false;
+  for (int u = 0; u < G; ++u) {
+    int ru = __shfl_sync(0xffffffffu, row, gbase + u);
+    if (act && u < gl && ru == row) coll = true;
+  }
+  const unsigned cmask = __ballot_sync(0xffffffffu, coll);
+  if (cmask) {
+    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << gbase);
+    const bool group_coll = (cmask & gmask) != 0;
+    int srow[32], sneg[32];
+    if (group_coll && gl == 0 && valid) sk_column_seq(i, s, d, k0, k1, srow, sneg);
+    for (int t = 0; t < G; ++t) {
+      int rv = 0, nv = 0;
+      if (gl == 0 && group_coll && valid && t < s) {
+        rv = srow[t];
+        nv = sneg[t];
+      }
+      rv = __shfl_sync(0xffffffffu, rv, gbase);
+      nv = __shfl_sync(0xffffffffu, nv, gbase);
+      if (group_coll && gl == t && act) {
+        row = rv;
+        neg = nv;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ a3 / a6: CSR SpMV
+// y = M x, warp per row, 128-bit streaming loads of 4 column indices and 2x2
+// values, gathered x through L1/L2 (Alg. 1 L473 / L486; Alg. 2 L776 / L789).
+// Rows are processed in groups of 8 consecutive rows per CTA so neighbouring
+// rays share gathered pixels in L1.  Summation order is fixed (per-lane FMA
+// chain then a shuffle tree): deterministic.
+// Input vector: x = x_base + x_ld * (st->k + x_koff) when x_ld != 0 (a column of
+// Z or W selected by the device-side iteration index, so one captured graph
+// serves every iteration), else x_base.
+__device__ __forceinline__ const double* kvec(const DevState* st, const double* base, int64_t ld, int koff) {
+  return ld ? base + ld * (int64_t)(st->k + koff) : base;
+}
+__device__ __forceinline__ double* kvec_w(const DevState* st, double* base, int64_t ld, int koff) {
+  return ld ? base + ld * (int64_t)(st->k + koff) : base;
+}
+
+__global__ void __launch_bounds__(kSpmvThreads) k_spmv_csr(const DevState* st, int64_t nrows,
+                                                           const int64_t* __restrict__ rowptr,
+                                                           const int* __restrict__ col,
+                                                           const double* __restrict__ val,
+                                                           const double* __restrict__ x_base, int64_t x_ld,
+                                                           int x_koff, double* __restrict__ y) {
+  if (st && st->done) return;
+  const double* __restrict__ x = kvec(st, x_base, x_ld, x_koff);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  constexpr int WPB = kSpmvThreads / 32;
+  for (int64_t row = (int64_t)blockIdx.x * WPB + wid; row < nrows; row += (int64_t)gridDim.x * WPB) {
+    const int64_t s = rowptr[row], e = rowptr[row + 1];
+    int64_t a = (s + 3) & ~(int64_t)3;
+    if (a > e) a = e;
+    double sum = 0.0;
+    if (s + lane < a) {
+      const int64_t p = s + lane;
+      sum = fma(ld_stream_d(val + p), __ldg(x + ld_stream_i(col + p)), sum);
+    }
+    const int64_t nq = (e - a) >> 2;
+    const int4* c4 = reinterpret_cast<const int4*>(col + a);
+    const double2* v2 = reinterpret_cast<const double2*>(val + a);
+    int64_t q = lane;
+    for (; q + 32 < nq; q += 64) {
+      const int4 ca = ld_stream_i4(c4 + q);
+      const int4 cb = ld_stream_i4(c4 + q + 32);
+      const double2 va0 = ld_stream_d2(v2 + 2 * q), va1 = ld_stream_d2(v2 + 2 * q + 1);
+      const double2 vb0 = ld_stream_d2(v2 + 2 * (q + 32)), vb1 = ld_stream_d2(v2 + 2 * (q + 32) + 1);
+      const double xa0 = __ldg(x + ca.x), xa1 = __ldg(x + ca.y), xa2 = __ldg(x + ca.z), xa3 = __ldg(x + ca.w);
+      const double xb0 = __ldg(x + cb.x), xb1 = __ldg(x + cb.y), xb2 = __ldg(x + cb.z), xb3 = __ldg(x + cb.w);
+      sum = fma(va0.x, xa0, sum);
+      sum = fma(va0.y, xa1, sum);
+      sum = fma(va1.x, xa2, sum);
+      sum = fma(va1.y, xa3, sum);
+      sum = fma(vb0.x, xb0, sum);
+      sum = fma(vb0.y, xb1, sum);
+      sum = fma(vb1.x, xb2, sum);
+      sum = fma(vb1.y, xb3, sum);
+    }
+    if (q < nq) {
+      const int4 ca = ld_stream_i4(c4 + q);
+      const double2 va0 = ld_stream_d2(v2 + 2 * q), va1 = ld_stream_d2(v2 + 2 * q + 1);
+      sum = fma(va0.x, __ldg(x + ca.x), sum);
+      sum = fma(va0.y, __ldg(x + ca.y), sum);
+      sum = fma(va1.x, __ldg(x + ca.z), sum);
+      sum = fma(va1.y, __ldg(x + ca.w), sum);
+    }
+    const int64_t t0 = a + 4 * nq;
+    if (t0 + lane < e) {
+      const int64_t p = t0 + lane;
+      sum = fma(ld_stream_d(val + p), __ldg(x + ld_stream_i(col + p)), sum);
+    }
+    sum = warp_sum(sum);
+    if (lane == 0) y[row] = sum;
+  }
+}
+
+// ------------------------------------------------------------------ a3 (config 2): separable blur
+// Zero-boundary 2-D Gaussian PSF outer(g, g) applied as a row pass then a
+// column pass (matrix-free; symmetric so it also serves as T).
+__global__ void __launch_bounds__(256) k_blur_rows(const DevState* st, int H, int W, int r,
+                                                   const double* __restrict__ taps, const double* __restrict__ in_base,
+                                                   int64_t in_ld, int in_koff, double* __restrict__ out) {
+  if (st && st->done) return;
+  const double* __restrict__ in = kvec(st, in_base, in_ld, in_koff);
+  const int64_t n = (int64_t)H * W;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(p / W), j = (int)(p % W);
+    double s = 0.0;
+    for (int v = -r; v <= r; ++v) {
+      const int jj = j + v;
+      if (jj >= 0 && jj < W) s = fma(taps[v + r], in[(int64_t)i * W + jj], s);
+    }
+    out[p] = s;
+  }
+}
+__global__ void __launch_bounds__(256) k_blur_cols(const DevState* st, int H, int W, int r,
+                                                   const double* __restrict__ taps, const double* __restrict__ in,
+                                                   double* __restrict__ out) {
+  if (st && st->done) return;
+  const int64_t n = (int64_t)H * W;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(p / W), j = (int)(p % W);
+    double s = 0.0;
+    for (int u = -r; u <= r; ++u) {
+      const int ii = i + u;
+      if (ii >= 0 && ii < H) s = fma(taps[u + r], in[(int64_t)ii * W + j], s);
+    }
+    out[p] = s;
+  }
+}
+
+// ------------------------------------------------------------------ a4: sparse-sign sketch
+// Per-block partial of S v (S: d x len, columns col0..col0+len-1 of the global
+// table).  Each warp owns a private d-bin array in shared memory and walks a
+// contiguous coordinate chunk in order; within a step the lane groups add in
+// group order, so the accumulation order is fixed.  skpart[blockIdx.x*d + r].
+__global__ void __launch_bounds__(kSkThreads) k_sketch_partial(const DevState* st, const double* __restrict__ v,
+                                                               int64_t len, int64_t col0, int d, int s, int G,
+                                                               uint32_t k0, uint32_t k1, double scale,
+                                                               double* __restrict__ skpart) {
+  if (st && st->done) return;
+  extern __shared__ double bins[];  // (kSkThreads/32) * d
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  constexpr int WPB = kSkThreads / 32;
+  double* mybins = bins + (size_t)wid * d;
+  for (int r = lane; r < d; r += 32) mybins[r] = 0.0;
+  __syncwarp();
+  const int64_t nwarps = (int64_t)gridDim.x * WPB;
+  const int64_t gw = (int64_t)blockIdx.x * WPB + wid;
+  const int64_t chunk = (len + nwarps - 1) / nwarps;
+  const int64_t beg = gw * chunk;
+  const int64_t end = (beg + chunk < len) ? beg + chunk : len;
+  const int per = 32 / G;  // coordinates per warp step
+  const int grp = lane / G, gl = lane & (G - 1);
+  for (int64_t base = beg; base < end; base += per) {
+    const int64_t li = base + grp;
+    const bool valid = li < end;
+    int row, neg;
+    sk_warp_entries((uint64_t)(col0 + li), valid, s, G, (uint32_t)d, k0, k1, row, neg);
+    double val = 0.0;
+    if (valid && gl < s) val = (neg ? -scale : scale) * v[li];
+    for (int g2 = 0; g2 < per; ++g2) {
+      if (grp == g2 && valid && gl < s) mybins[row] += val;
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  for (int r = threadIdx.x; r < d; r += kSkThreads) {
+    double acc = 0.0;
+#pragma unroll
+    for (int w2 = 0; w2 < WPB; ++w2) acc += bins[(size_t)w2 * d + r];
+    skpart[(size_t)blockIdx.x * d + r] = acc;
+  }
+}
+
+// out[r] = mult * sum_b skpart[b*d + r] (block order); optional second copy.
+// out = (mult_beta ? beta : 1) * sum; out2 (optional) = sum.  out may be k-relative.
+__global__ void k_sketch_finalize(const DevState* st, const double* __restrict__ skpart, int nb, int d,
+                                  int mult_beta, double* out_base, int64_t out_ld, int out_koff, double* out2) {
+  if (st && st->done) return;
+  double* out = kvec_w(st, out_base, out_ld, out_koff);
+  const double mult = mult_beta ? st->beta : 1.0;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < d; r += gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int b2 = 0; b2 < nb; ++b2) acc += skpart[(size_t)b2 * d + r];
+    if (out2) out2[r] = acc;
+    out[r] = mult_beta ? acc * mult : acc;
+  }
+}
+
+
+// ------------------------------------------------------------------ init
+// beta = ||b|| (partials in slot_beta), then w_1 = b / beta (Alg. 1).
+__global__ void __launch_bounds__(kVecThreads) k_norm_partial(Params P, const double* __restrict__ v, int64_t len,
+                                                              int slot) {
+  __shared__ double sh[33];
+  double acc = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * kVecThreads + threadIdx.x; i < len; i += (int64_t)gridDim.x * kVecThreads)
+    acc = fma(v[i], v[i], acc);
+  acc = block_sum<kVecThreads>(acc, sh);
+  if (threadIdx.x == 0) P.part[(size_t)slot * kVecBlocks + blockIdx.x] = acc;
+}
+__global__ void __launch_bounds__(kVecThreads) k_init_w1(Params P) {
+  __shared__ double sh[33];
+  const double beta = sqrt(sum_partials<kVecThreads>(P.part + (size_t)P.slot_beta * kVecBlocks, kVecBlocks, sh));
+  if (blockIdx.x == 0 && threadIdx.x == 0) P.st->beta = beta;
+  for (int64_t i = (int64_t)blockIdx.x * kVecThreads + threadIdx.x; i < P.m; i += (int64_t)gridDim.x * kVecThreads)
+    P.W[i] = P.b[i] / beta;
+}
+
+// ------------------------------------------------------------------ a1 / a5: windowed MGS
+// Literal modified Gram-Schmidt over the window (Alg. 1 L464-467 and L476-480;
+// Alg. 2 L767-770 and L778-784), one pass per basis vector:
+//   pass i applies v -= c_{i-1} q_{i-1} (c_{i-1} = sum of the previous pass's
+//   partials) and accumulates <q_i, v> (or ||v||^2 on the final pass).
+// side 0: z (n), basis q_j = p_j (orth P) or z_j (orth Z), J = min(ell, k-1);
+// side 1: w (m), basis q_j = w_j, J = min(ell+1, k).  Coefficients are stored in
+// Tm (side 0) / H (side 1) as eq. FGK's banded T and H (L400-406).
+__device__ __forceinline__ const double* mgs_basis(const Params& P, int side, int j /*1-based*/) {
+  if (side == 1) return P.W + (int64_t)(j - 1) * P.m;
+  if (P.use_pring) return P.Pring + (int64_t)((j - 1) % P.ell) * P.n;
+  return P.Z + (int64_t)(j - 1) * P.n;
+}
+
+__global__ void __launch_bounds__(kVecThreads) k_mgs_pass(Params P, int side, int pass) {
+  __shared__ double sh[33];
+  const DevState* st = P.st;
+  if (st->done) return;
+  const int k = st->k;
+  const int J = side == 0 ? min(P.ell, k - 1) : min(P.ell + 1, k);
+  if (pass > J) return;
+  const int j0 = side == 0 ? max(1, k - P.ell) : max(1, k - P.ell);  // first basis index
+  double* v = side == 0 ? P.z : P.w;
+  const int64_t len = side == 0 ? P.n : P.m;
+  const int slot0 = side == 0 ? P.slot_z0 : P.slot_w0;
+  const int slot_in = side == 0 ? P.slot_zin : P.slot_win;
+  double cprev = 0.0;
+  const double* qprev = nullptr;
+  if (pass > 0) {
+    cprev = sum_partials<kVecThreads>(P.part + (size_t)(slot0 + pass - 1) * kVecBlocks, kVecBlocks, sh);
+    qprev = mgs_basis(P, side, j0 + pass - 1);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      const int row = j0 + pass - 2;  // 0-based row of the coefficient
+      if (side == 0)
+        P.Tm[(int64_t)row + (int64_t)(k - 1) * P.maxit] = cprev;
+      else
+        P.H[(int64_t)row + (int64_t)(k - 1) * P.ldh] = cprev;
+    }
+  }
+  const double* qcur = (pass < J) ? mgs_basis(P, side, j0 + pass) : nullptr;
+  double acc = 0.0, acc_in = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * kVecThreads + threadIdx.x; i < len; i += (int64_t)gridDim.x * kVecThreads) {
+    double vi = v[i];
+    if (pass == 0) acc_in = fma(vi, vi, acc_in);
+    if (pass > 0) {
+      vi = fma(-cprev, qprev[i], vi);
+      v[i] = vi;
+    }
+    if (qcur)
+      acc = fma(qcur[i], vi, acc);
+    else
+      acc = fma(vi, vi, acc);
+  }
+  acc = block_sum<kVecThreads>(acc, sh);
+  if (threadIdx.x == 0) P.part[(size_t)(slot0 + pass) * kVecBlocks + blockIdx.x] = acc;
+  if (pass == 0) {
+    acc_in = block_sum<kVecThreads>(acc_in, sh);
+    if (threadIdx.x == 0) P.part[(size_t)slot_in * kVecBlocks + blockIdx.x] = acc_in;
+  }
+}
+
+// ------------------------------------------------------------------ a1 end + a2: normalise, tau, store
+// t = ||z||, breakdown test (R11), T_kk = t, p_k = z/t, z_k = tau_k(p_k)
+// (Alg. 1; Alg. 2; readings R7/R8), Z[:,k] = z_k, P ring.
+__global__ void __launch_bounds__(kVecThreads) k_finish_z(Params P) {
+  __shared__ double sh[33];
+  DevState* st = P.st;
+  if (st->done) return;
+  const int k = st->k;
+  const int J = min(P.ell, k - 1);
+  const double t = sqrt(sum_partials<kVecThreads>(P.part + (size_t)(P.slot_z0 + J) * kVecBlocks, kVecBlocks, sh));
+  const double zin = sqrt(sum_partials<kVecThreads>(P.part + (size_t)P.slot_zin * kVecBlocks, kVecBlocks, sh));
+  if (t == 0.0 || t <= 1e-14 * zin) {
+    __syncthreads();
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->done = 1;
+      st->status = 4;  // SFLSQR_BREAKDOWN; y still holds y_{k-1}
+    }
+    return;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) P.Tm[(int64_t)(k - 1) + (int64_t)(k - 1) * P.maxit] = t;
+  // tau weights need x_{k-1} (computed by k_xupdate at the end of iteration k-1)
+  int mode = P.precond;  // 0 identity, 1 IRN, 2 NONNEG
+  double eps = 0.0;
+  if (mode != 0) {
+    if (k == 1) {
+      mode = 0;  // D_1 = I (x_0 = 0)
+    } else {
+      const double mx = max_partials<kVecThreads>(P.part + (size_t)P.slot_xmax * kVecBlocks, kVecBlocks, sh);
+      if (!(mx > 0.0))
+        mode = 0;  // x_{k-1} = 0 (IRN) or x_{k-1} <= 0 (NONNEG): D = I
+      else
+        eps = P.eps_rel * mx;
+    }
+  }
+  double* zk = P.Z + (int64_t)(k - 1) * P.n;
+  double* pr = P.use_pring ? P.Pring + (int64_t)((k - 1) % P.ell) * P.n : nullptr;
+  for (int64_t i = (int64_t)blockIdx.x * kVecThreads + threadIdx.x; i < P.n; i += (int64_t)gridDim.x * kVecThreads) {
+    const double p = P.z[i] / t;
+    double zi = p;
+    if (mode == 1) {
+      const double xi = P.x[i];
+      const double v = fma(xi, xi, eps * eps);
+      const double D = (P.p_exp == 1.0) ? sqrt(sqrt(v)) : pow(v, (2.0 - P.p_exp) * 0.25);
+      zi = D * p;
+    } else if (mode == 2) {
+      const double D = fmax(P.x[i], 0.0) + eps;
+      zi = D * p;
+    }
+    zk[i] = zi;
+    if (pr) pr[i] = p;
+  }
+}
+
+// ------------------------------------------------------------------ a5 end: normalise w
+// H_{k+1,k} = ||w||; w_{k+1} = w / H_{k+1,k} (Alg. 1; Alg. 2);
+// breakdown (R11): H_{k+1,k} = 0, w_{k+1} = 0, the step-k LS is still solved.
+__global__ void __launch_bounds__(kVecThreads) k_finish_w(Params P) {
+  __shared__ double sh[33];
+  DevState* st = P.st;
+  if (st->done) return;
+  const int k = st->k;
+  const int J = min(P.ell + 1, k);
+  const double hn = sqrt(sum_partials<kVecThreads>(P.part + (size_t)(P.slot_w0 + J) * kVecBlocks, kVecBlocks, sh));
+  const double win = sqrt(sum_partials<kVecThreads>(P.part + (size_t)P.slot_win * kVecBlocks, kVecBlocks, sh));
+  const bool brk = (hn == 0.0 || hn <= 1e-14 * win);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->wbreak = brk ? 1 : 0;
+    P.H[(int64_t)k + (int64_t)(k - 1) * P.ldh] = brk ? 0.0 : hn;
+  }
+  double* wk1 = P.W + (int64_t)k * P.m;
+  for (int64_t i = (int64_t)blockIdx.x * kVecThreads + threadIdx.x; i < P.m; i += (int64_t)gridDim.x * kVecThreads)
+    wk1[i] = brk ? 0.0 : P.w[i] / hn;
+}
+
+// ------------------------------------------------------------------ a7: projected sketched LS (one CTA)
+// Appends column k of M (sFLSQR: S A z_k, Alg. 1; sFLSMR: the band
+// combination sum_i [S_TW, S z]_i H_{i,k}, Alg. 2 L796 / eq. sFLSMR) to an
+// incremental unpivoted Householder QR: reflectors 1..k-1 are applied to the new
+// column in order, reflector k is formed, Q^T rhs is updated, and R y = (Q^T rhs)_{1:k}
+// is solved by back substitution (reading R14: the same reflector sequence as a
+// from-scratch Householder QR).  Also forms g = beta e_1 - H_{1:k+1,1:k} y for
+// the W-path true residual (eq. FGK: b - A Z y = W_{k+1} g).
+__global__ void __launch_bounds__(kLsThreads) k_ls(Params P) {
+  __shared__ double sh[33];
+  __shared__ double a[kMaxD];
+  __shared__ double q[kMaxD];
+  DevState* st = P.st;
+  if (st->done) return;
+  const int k = st->k, c = k - 1, d = P.d;
+  const int tid = threadIdx.x;
+  double* Mc = P.Mcols + (int64_t)c * d;
+  if (P.method == 0) {
+    for (int r = tid; r < d; r += kLsThreads) a[r] = Mc[r];
+  } else {
+    const int i0 = max(0, c - P.ell);
+    for (int r = tid; r < d; r += kLsThreads) {
+      double acc = 0.0;
+      for (int i = i0; i <= c + 1; ++i) acc = fma(P.STW[(int64_t)i * d + r], P.H[(int64_t)i + (int64_t)c * P.ldh], acc);
+      a[r] = acc;
+      Mc[r] = acc;
+    }
+  }
+  for (int r = tid; r < d; r += kLsThreads) q[r] = P.qtb[r];
+  __syncthreads();
+  // apply reflectors 0..c-1 to the new column
+  for (int j = 0; j < c; ++j) {
+    const double* vj = P.V + (int64_t)j * d;
+    double part = 0.0;
+    for (int r = j + tid; r < d; r += kLsThreads) part = fma(vj[r], a[r], part);
+    const double dot = block_sum<kLsThreads>(part, sh);
+    const double f = P.taus[j] * dot;
+    for (int r = j + tid; r < d; r += kLsThreads) a[r] = fma(-f, vj[r], a[r]);
+  }
+  __syncthreads();
+  for (int r = tid; r < c; r += kLsThreads) P.R[(int64_t)r + (int64_t)c * P.maxit] = a[r];
+  const double alpha = a[c];
+  double part = 0.0;
+  for (int r = c + 1 + tid; r < d; r += kLsThreads) part = fma(a[r], a[r], part);
+  const double xnorm = sqrt(block_sum<kLsThreads>(part, sh));
+  double beta_h, tau, scal;
+  if (xnorm == 0.0) {
+    beta_h = alpha;
+    tau = 0.0;
+    scal = 0.0;
+  } else {
+    beta_h = -copysign(hypot(alpha, xnorm), alpha);
+    tau = (beta_h - alpha) / beta_h;
+    scal = 1.0 / (alpha - beta_h);
+  }
+  double* vc = P.V + (int64_t)c * d;
+  for (int r = tid; r < d; r += kLsThreads) {
+    double vr = (r < c) ? 0.0 : (r == c ? 1.0 : (xnorm == 0.0 ? 0.0 : a[r] * scal));
+    vc[r] = vr;
+    a[r] = vr;  // a now holds v_c
+  }
+  if (tid == 0) {
+    P.R[(int64_t)c + (int64_t)c * P.maxit] = beta_h;
+    P.taus[c] = tau;
+  }
+  __syncthreads();
+  part = 0.0;
+  for (int r = c + tid; r < d; r += kLsThreads) part = fma(a[r], q[r], part);
+  const double dq = block_sum<kLsThreads>(part, sh);
+  const double fq = tau * dq;
+  for (int r = c + tid; r < d; r += kLsThreads) q[r] = fma(-fq, a[r], q[r]);
+  __syncthreads();
+  for (int r = tid; r < d; r += kLsThreads) P.qtb[r] = q[r];
+  // sketched residual ||(Q^T rhs)_{k+1:d}||
+  part = 0.0;
+  for (int r = k + tid; r < d; r += kLsThreads) part = fma(q[r], q[r], part);
+  const double sres = sqrt(block_sum<kLsThreads>(part, sh));
+  // back substitution R y = q[0:k] (column oriented); a[] reused for y
+  for (int i = k - 1; i >= 0; --i) {
+    __syncthreads();
+    const double yi = q[i] / P.R[(int64_t)i + (int64_t)i * P.maxit];
+    if (tid == 0) a[i] = yi;
+    for (int t = tid; t < i; t += kLsThreads) q[t] = fma(-P.R[(int64_t)t + (int64_t)i * P.maxit], yi, q[t]);
+  }
+  __syncthreads();
+  for (int i = tid; i < k; i += kLsThreads) P.y[i] = a[i];
+  // rank indicator (R14)
+  double dmin = INFINITY, dmax = 0.0;
+  for (int i = tid; i < k; i += kLsThreads) {
+    const double v = fabs(P.R[(int64_t)i + (int64_t)i * P.maxit]);
+    dmin = fmin(dmin, v);
+    dmax = fmax(dmax, v);
+  }
+  const double gmax = block_max<kLsThreads>(dmax, sh);
+  const double gmin = -block_max<kLsThreads>(-dmin, sh);
+  // g = beta e1 - H_{1:k+1,1:k} y (band: H_{i,j} != 0 for j-ell <= i <= j+1)
+  for (int i = tid; i <= k; i += kLsThreads) {
+    double acc = (i == 0) ? st->beta : 0.0;
+    const int jlo = max(0, i - 1), jhi = min(k - 1, i + P.ell);
+    for (int j = jlo; j <= jhi; ++j) acc = fma(-P.H[(int64_t)i + (int64_t)j * P.ldh], a[j], acc);
+    P.g[i] = acc;
+  }
+  if (tid == 0) {
+    P.hist_sk[c] = sres;
+    st->k_x = k;
+    if (gmin < 1e-14 * gmax) st->rank_flag = 1;
+  }
+}
+
+// ------------------------------------------------------------------ a8: x_k = Z_k y_k
+// Tall-skinny GEMV (Alg. 1 L504 / Alg. 2), plus the partial max needed by
+// tau_{k+1} (|x| for IRN, x_+ for NONNEG).  HBM-bound (0.25 flop/B).
+__global__ void __launch_bounds__(kVecThreads) k_xupdate(Params P, int force) {
+  __shared__ double sh[33];
+  __shared__ double ys[1024];
+  const DevState* st = P.st;
+  if (!force && st->done) return;
+  const int kx = st->k_x;
+  double mx = -INFINITY;
+  for (int64_t i0 = (int64_t)blockIdx.x * kVecThreads; i0 < P.n; i0 += (int64_t)gridDim.x * kVecThreads) {
+    const int64_t i = i0 + threadIdx.x;
+    double acc = 0.0;
+    for (int jb = 0; jb < kx; jb += 1024) {
+      const int nj = min(1024, kx - jb);
+      __syncthreads();
+      for (int t = threadIdx.x; t < nj; t += kVecThreads) ys[t] = P.y[jb + t];
+      __syncthreads();
+      if (i < P.n)
+        for (int j = 0; j < nj; ++j) acc = fma(P.Z[(int64_t)(jb + j) * P.n + i], ys[j], acc);
+    }
+    if (i < P.n) {
+      P.x[i] = acc;
+      mx = fmax(mx, P.precond == 1 ? fabs(acc) : acc);
+    }
+  }
+  mx = block_max<kVecThreads>(mx, sh);
+  if (threadIdx.x == 0) P.part[(size_t)P.slot_xmax * kVecBlocks + blockIdx.x] = mx;
+}
+
+// ------------------------------------------------------------------ a9: W-path true residual
+// ||b - A x_k|| = ||W_{k+1} g|| (eq. FGK: A Z_k = W_{k+1} H_{k+1,k}, w_1 = b/beta).
+__global__ void __launch_bounds__(kVecThreads) k_res_partial(Params P) {
+  __shared__ double sh[33];
+  __shared__ double gs[1024];
+  const DevState* st = P.st;
+  if (st->done) return;
+  const int kk = st->k + 1;  // columns of W_{k+1}
+  double acc2 = 0.0;
+  for (int64_t i0 = (int64_t)blockIdx.x * kVecThreads; i0 < P.m; i0 += (int64_t)gridDim.x * kVecThreads) {
+    const int64_t i = i0 + threadIdx.x;
+    double r = 0.0;
+    for (int jb = 0; jb < kk; jb += 1024) {
+      const int nj = min(1024, kk - jb);
+      __syncthreads();
+      for (int t = threadIdx.x; t < nj; t += kVecThreads) gs[t] = P.g[jb + t];
+      __syncthreads();
+      if (i < P.m)
+        for (int j = 0; j < nj; ++j) r = fma(P.W[(int64_t)(jb + j) * P.m + i], gs[j], r);
+    }
+    if (i < P.m) acc2 = fma(r, r, acc2);
+  }
+  acc2 = block_sum<kVecThreads>(acc2, sh);
+  if (threadIdx.x == 0) P.part[(size_t)P.slot_res * kVecBlocks + blockIdx.x] = acc2;
+}
+
+// ------------------------------------------------------------------ a9: stop tests
+// tol test (Alg. 1 L498 / Alg. 2, R3) and discrepancy principle (eq. discrP
+// L50-53, R12); records the histories and advances k.
+__global__ void __launch_bounds__(kVecThreads) k_stop(Params P) {
+  __shared__ double sh[33];
+  DevState* st = P.st;
+  if (st->done) return;
+  const int k = st->k;
+  double r = NAN;
+  if (P.want_res) r = sqrt(sum_partials<kVecThreads>(P.part + (size_t)P.slot_res * kVecBlocks, kVecBlocks, sh));
+  if (threadIdx.x != 0) return;
+  P.hist_true[k - 1] = r;
+  const double sres = P.hist_sk[k - 1];
+  int status = 0;
+  if (st->wbreak)
+    status = 4;
+  else if (P.tol > 0.0 && sres < P.tol * st->rhs_norm)
+    status = 2;
+  else if (P.eta > 0.0 && r <= P.eta * P.delta_e)
+    status = 3;
+  else if (k >= P.maxit)
+    status = 1;
+  if (status) {
+    st->status = status;
+    st->done = 1;
+  }
+  st->k = k + 1;
+}
+
+// rhs norm for the tol test, qtb = rhs (LS start), state reset.
+__global__ void k_init_ls(Params P) {
+  __shared__ double sh[33];
+  double part = 0.0;
+  for (int r = threadIdx.x; r < P.d; r += blockDim.x) {
+    part = fma(P.rhs[r], P.rhs[r], part);
+    P.qtb[r] = P.rhs[r];
+  }
+  const double nr = sqrt(block_sum<kVecThreads>(part, sh));
+  if (threadIdx.x == 0) {
+    P.st->rhs_norm = nr;
+    P.st->k = 1;
+    P.st->done = 0;
+    P.st->status = 0;
+    P.st->k_x = 0;
+    P.st->wbreak = 0;
+    P.st->rank_flag = 0;
+  }
+}
+
+// Debug: sketch table for columns [col0, col0+ncols).
+__global__ void k_sketch_table(int64_t col0, int64_t ncols, int d, int s, int G, uint32_t k0, uint32_t k1,
+                               int* rows, int8_t* signs) {
+  const int lane = threadIdx.x & 31;
+  const int per = 32 / G, grp = lane / G, gl = lane & (G - 1);
+  const int64_t wglob = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = wglob * per; base < ncols; base += nw * per) {
+    const int64_t li = base + grp;
+    const bool valid = li < ncols;
+    int row, neg;
+    sk_warp_entries((uint64_t)(col0 + li), valid, s, G, (uint32_t)d, k0, k1, row, neg);
+    if (valid && gl < s) {
+      rows[li * s + gl] = row;
+      signs[li * s + gl] = neg ? (int8_t)-1 : (int8_t)1;
+    }
+  }
+}
+
+}  // namespace sfl

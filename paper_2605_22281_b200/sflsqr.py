@@ -1,0 +1,305 @@
+"""Thin ctypes binding of libsflsqr.so (include/sflsqr.h).
+
+Argument marshalling only: every step of the method runs in the library's
+CUDA kernels.  Method names mirror the C ABI without the ``sflsqr_`` prefix.
+Arrays may be NumPy (host) or CUDA ``torch.Tensor`` (device; passed by
+pointer with SFLSQR_MEM_DEVICE).  PyTorch supplies the stream
+(``torch.cuda.current_stream()``) when it is importable with CUDA.
+
+There is no CPU fallback: if the shared library is missing or no CUDA device
+is present, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+
+import numpy as np
+
+from ._build import LIB_PATH
+
+OK = 0
+E_INVALID, E_DIM, E_NONFINITE, E_ZERO_RHS, E_STATE, E_CUDA, E_OOM, E_UNSUPPORTED = -1, -2, -3, -4, -5, -6, -7, -8
+METHOD_SFLSQR, METHOD_SFLSMR = 0, 1
+ORTH_P, ORTH_Z = 0, 1
+RUNNING, MAXIT, TOL, DISCREPANCY, BREAKDOWN = 0, 1, 2, 3, 4
+PRECOND_IDENTITY, PRECOND_IRN, PRECOND_NONNEG = 0, 1, 2
+T_BUILD, T_GIVEN = 0, 1
+MEM_HOST, MEM_DEVICE, MEM_BORROW = 0, 1, 2
+HIST_TRUE_RES = 1
+KC_NAMES = ["spmv_A", "spmv_T", "orth", "tau", "sketch", "ls", "xupd", "res", "stop"]
+
+EXPORTED = [
+    "sflsqr_version", "sflsqr_create", "sflsqr_set_operator", "sflsqr_set_operator_blur", "sflsqr_set_sketch",
+    "sflsqr_set_precond", "sflsqr_set_rhs", "sflsqr_iterate", "sflsqr_get_x", "sflsqr_get_residual_norms",
+    "sflsqr_get_info", "sflsqr_debug_sketch_table", "sflsqr_debug_apply", "sflsqr_debug_basis", "sflsqr_debug_state",
+    "sflsqr_set_profiling", "sflsqr_reset_profile", "sflsqr_get_profile", "sflsqr_last_error", "sflsqr_destroy",
+]
+
+
+class Opts(ctypes.Structure):
+    _fields_ = [("method", ctypes.c_int32), ("window", ctypes.c_int32), ("maxit", ctypes.c_int32),
+                ("orth_mode", ctypes.c_int32), ("tol", ctypes.c_double), ("eta", ctypes.c_double),
+                ("delta_e", ctypes.c_double), ("history", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("stream", ctypes.c_void_p), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
+                ("use_graph", ctypes.c_int32), ("reserved", ctypes.c_int32 * 7)]
+
+
+class Info(ctypes.Structure):
+    _fields_ = [("k_done", ctypes.c_int32), ("k_x", ctypes.c_int32), ("status", ctypes.c_int32),
+                ("rank_flag", ctypes.c_int32), ("m", ctypes.c_int64), ("n", ctypes.c_int64),
+                ("nnz_a", ctypes.c_int64), ("nnz_t", ctypes.c_int64), ("launches", ctypes.c_int64),
+                ("beta", ctypes.c_double)]
+
+
+class Profile(ctypes.Structure):
+    _fields_ = [("ms", ctypes.c_double * 9), ("launches", ctypes.c_int64 * 9), ("bytes", ctypes.c_double * 9)]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libsflsqr.so (raises OSError if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise OSError(f"{path} not found: run __graft_entry__.build() (no CPU fallback exists)")
+    lib = ctypes.CDLL(path)
+    vp, i32, i64, f64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+    sig = {
+        "sflsqr_version": ([], ctypes.c_int),
+        "sflsqr_create": ([ctypes.POINTER(vp), ctypes.POINTER(Opts)], ctypes.c_int),
+        "sflsqr_set_operator": ([vp, i64, i64, vp, vp, vp, i32, vp, vp, vp, i32], ctypes.c_int),
+        "sflsqr_set_operator_blur": ([vp, i32, i32, f64, i32], ctypes.c_int),
+        "sflsqr_set_sketch": ([vp, ctypes.c_uint64, i32, i32], ctypes.c_int),
+        "sflsqr_set_precond": ([vp, i32, f64, f64], ctypes.c_int),
+        "sflsqr_set_rhs": ([vp, vp, i64, i32], ctypes.c_int),
+        "sflsqr_iterate": ([vp, i32, ctypes.POINTER(i32), ctypes.POINTER(i32)], ctypes.c_int),
+        "sflsqr_get_x": ([vp, vp, i64, i32], ctypes.c_int),
+        "sflsqr_get_residual_norms": ([vp, vp, vp, i64, ctypes.POINTER(i64)], ctypes.c_int),
+        "sflsqr_get_info": ([vp, ctypes.POINTER(Info)], ctypes.c_int),
+        "sflsqr_debug_sketch_table": ([vp, i64, i64, vp, vp], ctypes.c_int),
+        "sflsqr_debug_apply": ([vp, i32, vp, vp], ctypes.c_int),
+        "sflsqr_debug_basis": ([vp, vp, vp, vp, vp, vp], ctypes.c_int),
+        "sflsqr_debug_state": ([vp, vp, vp, vp, vp, vp], ctypes.c_int),
+        "sflsqr_set_profiling": ([vp, i32], ctypes.c_int),
+        "sflsqr_reset_profile": ([vp], ctypes.c_int),
+        "sflsqr_get_profile": ([vp, ctypes.POINTER(Profile)], ctypes.c_int),
+        "sflsqr_last_error": ([vp], ctypes.c_char_p),
+        "sflsqr_destroy": ([vp], None),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+class SflsqrError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"libsflsqr error {code}: {msg}")
+        self.code = code
+
+
+def _ptr(a):
+    """(pointer, is_device, keepalive) for a numpy array or torch tensor (or None)."""
+    if a is None:
+        return None, False, None
+    if isinstance(a, np.ndarray):
+        if not a.flags["C_CONTIGUOUS"]:
+            a = np.ascontiguousarray(a)
+        return a.ctypes.data, False, a
+    mod = type(a).__module__
+    if mod.startswith("torch"):
+        if not a.is_contiguous():
+            a = a.contiguous()
+        return a.data_ptr(), bool(a.is_cuda), a
+    raise TypeError(f"unsupported array type {type(a)}")
+
+
+def _torch_stream(device):
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return torch.cuda.current_stream(device).cuda_stream
+    except Exception:
+        pass
+    return None
+
+
+class SFLSQR:
+    """One solver handle (sflsqr_create ... sflsqr_destroy)."""
+
+    def __init__(self, method="sflsqr", window=2, maxit=10, orth_mode="P", tol=0.0, eta=0.0, delta_e=0.0,
+                 history=HIST_TRUE_RES, device=0, stream=None, use_graph=True):
+        self.lib = load_library()
+        o = Opts()
+        o.method = METHOD_SFLSQR if method == "sflsqr" else METHOD_SFLSMR if method == "sflsmr" else -1
+        o.window, o.maxit = int(window), int(maxit)
+        o.orth_mode = ORTH_P if orth_mode == "P" else ORTH_Z
+        o.tol, o.eta, o.delta_e = float(tol), float(eta), float(delta_e)
+        o.history, o.device = int(history), int(device)
+        # NULL / the legacy default stream -> the library creates its own non-blocking stream
+        o.stream = stream if stream is not None else _torch_stream(device)
+        o.rank, o.world, o.use_graph = 0, 1, 1 if use_graph else 0
+        self.maxit = int(maxit)
+        h = ctypes.c_void_p()
+        rc = self.lib.sflsqr_create(ctypes.byref(h), ctypes.byref(o))
+        if rc != OK:
+            raise SflsqrError(rc, self.lib.sflsqr_last_error(None).decode())
+        self.h = h
+        self._keep = []
+        self.m = self.n = None
+
+    # ------------------------------------------------------------------
+    def _check(self, rc):
+        if rc != OK:
+            raise SflsqrError(rc, self.lib.sflsqr_last_error(self.h).decode())
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.sflsqr_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # ------------------------------------------------------------------ ABI mirrors
+    def set_operator(self, m, n, a_rowptr, a_col, a_val, t=None, borrow=False):
+        """t = None -> T_BUILD (A^T formed by the library); t = (rowptr, col, val) -> T_GIVEN."""
+        pa = [_ptr(x) for x in (a_rowptr, a_col, a_val)]
+        dev = pa[0][1]
+        if t is None:
+            pt = [(None, dev, None)] * 3
+            mode = T_BUILD
+        else:
+            pt = [_ptr(x) for x in t]
+            mode = T_GIVEN
+        flags = (MEM_DEVICE if dev else MEM_HOST) | (MEM_BORROW if borrow else 0)
+        if borrow:
+            self._keep += [p[2] for p in pa + pt]
+        self._check(self.lib.sflsqr_set_operator(self.h, int(m), int(n), pa[0][0], pa[1][0], pa[2][0], mode,
+                                                 pt[0][0], pt[1][0], pt[2][0], flags))
+        self.m, self.n = int(m), int(n)
+
+    def set_operator_blur(self, H, W, sigma, radius):
+        self._check(self.lib.sflsqr_set_operator_blur(self.h, int(H), int(W), float(sigma), int(radius)))
+        self.m = self.n = int(H) * int(W)
+
+    def set_sketch(self, seed, d, s_nz):
+        self._check(self.lib.sflsqr_set_sketch(self.h, int(seed), int(d), int(s_nz)))
+
+    def set_precond(self, kind="identity", p=1.0, eps_rel=1e-3):
+        k = {"identity": PRECOND_IDENTITY, "irn": PRECOND_IRN, "nonneg": PRECOND_NONNEG}.get(kind, kind)
+        self._check(self.lib.sflsqr_set_precond(self.h, int(k), float(p), float(eps_rel)))
+
+    def set_rhs(self, b):
+        p, dev, keep = _ptr(b)
+        n = b.numel() if hasattr(b, "numel") else b.size
+        self._check(self.lib.sflsqr_set_rhs(self.h, p, int(n), MEM_DEVICE if dev else MEM_HOST))
+
+    def iterate(self, k):
+        done, status = ctypes.c_int32(), ctypes.c_int32()
+        self._check(self.lib.sflsqr_iterate(self.h, int(k), ctypes.byref(done), ctypes.byref(status)))
+        return bool(done.value), int(status.value)
+
+    def get_x(self, out=None):
+        if out is None:
+            out = np.empty(self.n)
+        p, dev, _ = _ptr(out)
+        self._check(self.lib.sflsqr_get_x(self.h, p, int(self.n), MEM_DEVICE if dev else MEM_HOST))
+        return out
+
+    def get_residual_norms(self):
+        cap = self.maxit
+        tr, sk = np.empty(cap), np.empty(cap)
+        cnt = ctypes.c_int64()
+        self._check(self.lib.sflsqr_get_residual_norms(self.h, tr.ctypes.data, sk.ctypes.data, cap,
+                                                       ctypes.byref(cnt)))
+        c = int(cnt.value)
+        return tr[:c].copy(), sk[:c].copy()
+
+    def get_info(self):
+        inf = Info()
+        self._check(self.lib.sflsqr_get_info(self.h, ctypes.byref(inf)))
+        return {f: getattr(inf, f) for f, _ in Info._fields_}
+
+    def debug_sketch_table(self, col0, ncols, s_nz):
+        rows = np.empty((ncols, s_nz), dtype=np.int32)
+        signs = np.empty((ncols, s_nz), dtype=np.int8)
+        self._check(self.lib.sflsqr_debug_sketch_table(self.h, int(col0), int(ncols), rows.ctypes.data,
+                                                       signs.ctypes.data))
+        return rows, signs
+
+    def debug_apply(self, which, x):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.empty(self.m if which == 0 else self.n)
+        self._check(self.lib.sflsqr_debug_apply(self.h, int(which), x.ctypes.data, y.ctypes.data))
+        return y
+
+    def debug_basis(self):
+        info = self.get_info()
+        kd, kx = info["k_done"], info["k_x"]
+        H = np.zeros((kd + 1, kd), order="F")
+        Tm = np.zeros((kd, kd), order="F")
+        Z = np.zeros((self.n, kd), order="F")
+        W = np.zeros((self.m, kd + 1), order="F")
+        y = np.zeros(kx)
+        self._check(self.lib.sflsqr_debug_basis(self.h, H.ctypes.data, Tm.ctypes.data, Z.ctypes.data,
+                                                W.ctypes.data, y.ctypes.data))
+        return dict(H=H, T=Tm, Z=Z, W=W, y=y)
+
+    def debug_state(self, window, d, method):
+        info = self.get_info()
+        kd = info["k_done"]
+        z, x = np.zeros(self.n), np.zeros(self.n)
+        ring = np.zeros((window, self.n))
+        nc = kd if method == "sflsqr" else kd + 1
+        cols = np.zeros((d, max(nc, 1)), order="F")
+        rhs = np.zeros(d)
+        self._check(self.lib.sflsqr_debug_state(self.h, z.ctypes.data, x.ctypes.data, ring.ctypes.data,
+                                                cols.ctypes.data, rhs.ctypes.data))
+        return dict(z=z, x=x, p_ring=ring, sketch_cols=cols[:, :nc], rhs=rhs)
+
+    def set_profiling(self, on=True):
+        self._check(self.lib.sflsqr_set_profiling(self.h, 1 if on else 0))
+
+    def reset_profile(self):
+        self._check(self.lib.sflsqr_reset_profile(self.h))
+
+    def get_profile(self):
+        p = Profile()
+        self._check(self.lib.sflsqr_get_profile(self.h, ctypes.byref(p)))
+        return {KC_NAMES[i]: dict(ms=p.ms[i], launches=int(p.launches[i]), bytes=p.bytes[i]) for i in range(9)}
+
+
+def solver_for_problem(prob, spec, maxit=None, history=HIST_TRUE_RES, use_graph=True, eta=None, device=0,
+                       operator_on_device=False):
+    """Configure an SFLSQR handle for a gen.Problem / gen.SolverSpec (marshalling only)."""
+    mx = maxit or spec.maxit
+    s = SFLSQR(method=spec.method, window=spec.window, maxit=mx, orth_mode=spec.orth_mode, tol=spec.tol,
+               eta=spec.eta if eta is None else eta, delta_e=prob.delta_e, history=history, device=device,
+               use_graph=use_graph)
+    if prob.t_mode == "same":
+        bl = prob.blur
+        s.set_operator_blur(bl["H"], bl["W"], bl["sigma"], bl["radius"])
+    else:
+        A = prob.A
+        t = None if prob.t_mode == "build" else (prob.T.rowptr, prob.T.col, prob.T.val)
+        s.set_operator(A.nrows, A.ncols, A.rowptr, A.col, A.val, t=t)
+    s.set_sketch(prob.sketch_seed, spec.d, spec.s_nz)
+    s.set_precond(spec.precond, spec.p, spec.eps_rel)
+    return s

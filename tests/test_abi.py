@@ -1,0 +1,67 @@
+"""Boundary checks that need no GPU: the C-ABI library builds, loads and exports
+every symbol include/sflsqr.h declares; without a device it fails loudly."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "sflsqr.h")
+
+
+def _declared():
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(sflsqr_[a-z_]+)\s*\(", txt)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2605_22281_b200._build import build_library
+    path = build_library()
+    return ctypes.CDLL(path), path
+
+
+def test_header_declares_the_boundary():
+    names = _declared()
+    for need in ("sflsqr_create", "sflsqr_set_operator", "sflsqr_set_sketch", "sflsqr_set_precond",
+                 "sflsqr_iterate", "sflsqr_get_x", "sflsqr_get_residual_norms", "sflsqr_destroy"):
+        assert need in names
+
+
+def test_library_exports_every_declared_symbol(lib):
+    _, path = lib
+    out = subprocess.run(["nm", "-D", "--defined-only", path], capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r"\bT (sflsqr_\w+)", out))
+    missing = [n for n in _declared() if n not in exported]
+    assert not missing, missing
+    from paper_2605_22281_b200.sflsqr import EXPORTED
+    assert sorted(EXPORTED) == _declared()
+
+
+def test_library_is_sm100a(lib):
+    _, path = lib
+    out = subprocess.run(["cuobjdump", "--list-elf", path], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_version_and_create_without_gpu(lib):
+    import torch
+    from paper_2605_22281_b200 import sflsqr as B
+    L = B.load_library()
+    assert L.sflsqr_version() == 1
+    if torch.cuda.is_available():
+        pytest.skip("GPU present: covered by the -m gpu tests")
+    with pytest.raises(B.SflsqrError) as ei:
+        B.SFLSQR(method="sflsqr", window=2, maxit=5)
+    assert ei.value.code == B.E_CUDA
+
+
+def test_option_validation_precedes_device_use(lib):
+    from paper_2605_22281_b200 import sflsqr as B
+    bad = [dict(method="nope"), dict(window=0), dict(maxit=0), dict(tol=-1.0), dict(eta=0.5), dict(delta_e=-1.0)]
+    for kw in bad:
+        with pytest.raises(B.SflsqrError) as ei:
+            B.SFLSQR(**kw)
+        assert ei.value.code == B.E_INVALID, kw

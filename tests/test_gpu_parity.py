@@ -1,0 +1,397 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle.
+
+Bar (BASELINE.json north_star): sketch tables bit-exact; per-iteration true and
+sketched residual norms within 1e-9 relative for iterations 1..30; final x
+within 1e-6 relative (2-norm); the same stopping iteration and status.
+"""
+import numpy as np
+import pytest
+
+from gen import make_problem
+from gen.problems import SolverSpec
+from oracle.operators import BlurOperator, OracleCSR, operator_from_problem
+from oracle.sflsqr import solve, solve_problem
+from oracle.sketch import sparse_sign_table
+
+pytestmark = pytest.mark.gpu
+
+RES_TOL = 1e-9
+X_TOL = 1e-6
+N_RES = 30
+
+
+@pytest.fixture(scope="session", autouse=True)
+def _lib():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2605_22281_b200._build import build_library
+    build_library()
+
+
+def _gpu_run(prob, spec, maxit=None, eta=None, use_graph=True, **kw):
+    from paper_2605_22281_b200 import solver_for_problem
+    s = solver_for_problem(prob, spec, maxit=maxit, eta=eta, use_graph=use_graph, **kw)
+    s.set_rhs(prob.b)
+    done, status = s.iterate(maxit or spec.maxit)
+    tr, sk = s.get_residual_norms()
+    x = s.get_x()
+    info = s.get_info()
+    s.close()
+    return dict(done=done, status=status, true_res=tr, sketch_res=sk, x=x, info=info)
+
+
+def _compare(g, r, n_res=N_RES, res_tol=RES_TOL, x_tol=X_TOL):
+    kk = len(r.true_res)
+    assert g["info"]["k_done"] == kk, (g["info"], kk)
+    assert g["status"] == r.status and g["info"]["k_x"] == r.k
+    n = min(n_res, kk)
+    rt = np.abs(g["true_res"][:n] - np.array(r.true_res[:n])) / np.array(r.true_res[:n])
+    # sketched residual: relative, with an absolute rounding floor u-scaled to ||rhs|| ~ max history
+    # (at k = d the projected system is square and the residual is 0 up to rounding)
+    floor = 1e-12 * max(r.sketch_res)
+    rs = np.abs(g["sketch_res"][:n] - np.array(r.sketch_res[:n])) / np.maximum(np.array(r.sketch_res[:n]), floor)
+    assert rt.max() < res_tol, ("true residual", rt.max(), int(rt.argmax()) + 1)
+    assert rs.max() < res_tol, ("sketched residual", rs.max(), int(rs.argmax()) + 1)
+    ex = np.linalg.norm(g["x"] - r.x) / max(np.linalg.norm(r.x), 1e-300)
+    assert ex < x_tol, ("x", ex)
+    return rt.max(), rs.max(), ex
+
+
+# ------------------------------------------------------------------ P1: sketch table bit-exact
+@pytest.mark.parametrize("seed,d,s,dim", [(0x5F1A5E, 80, 4, 256), (0x5F1A5F, 200, 8, 65536), (0x5F1A60, 300, 8, 262144),
+                                          (0x5F1A61, 400, 8, 1043280), (7, 13, 13, 5000), (1 << 40, 31, 1, 9999),
+                                          (12345, 64, 32, 3000), (99, 50, 5, 7777)])
+def test_sketch_table_bit_exact(seed, d, s, dim):
+    from paper_2605_22281_b200 import SFLSQR
+    sol = SFLSQR(maxit=1)
+    sol.set_sketch(seed, d, s)
+    if dim > 300000:
+        for c0 in (0, dim // 2 - 1000, dim - 50000):
+            nc = min(50000, dim - c0)
+            rg, sg = sol.debug_sketch_table(c0, nc, s)
+            ro, so = sparse_sign_table(seed, d, s, c0, nc)
+            assert np.array_equal(rg, ro) and np.array_equal(sg, so)
+    else:
+        rg, sg = sol.debug_sketch_table(0, dim, s)
+        ro, so = sparse_sign_table(seed, d, s, 0, dim)
+        assert np.array_equal(rg, ro) and np.array_equal(sg, so)
+    sol.close()
+
+
+# ------------------------------------------------------------------ operators
+def test_spmv_matches_oracle_ct_ragged():
+    from paper_2605_22281_b200 import SFLSQR
+    p = make_problem(4, N=96, n_angles=61, nb=137)   # ragged rows, empty corner rays, unmatched B
+    s = SFLSQR(maxit=4)
+    s.set_operator(p.A.nrows, p.A.ncols, p.A.rowptr, p.A.col, p.A.val, t=(p.T.rowptr, p.T.col, p.T.val))
+    A = OracleCSR(p.A.nrows, p.A.ncols, p.A.rowptr, p.A.col, p.A.val)
+    B = OracleCSR(p.T.nrows, p.T.ncols, p.T.rowptr, p.T.col, p.T.val)
+    rng = np.random.default_rng(0)
+    x, w = rng.standard_normal(p.n), rng.standard_normal(p.m)
+    for got, ref in ((s.debug_apply(0, x), A.matvec(x)), (s.debug_apply(1, w), B.matvec(w))):
+        assert np.max(np.abs(got - ref)) <= 1e-13 * np.max(np.abs(ref))
+    s.close()
+
+
+def test_built_transpose_matches_oracle():
+    from paper_2605_22281_b200 import SFLSQR
+    p = make_problem(3, N=80, n_angles=50, nb=115)
+    s = SFLSQR(maxit=4)
+    s.set_operator(p.A.nrows, p.A.ncols, p.A.rowptr, p.A.col, p.A.val)
+    At = OracleCSR(p.A.nrows, p.A.ncols, p.A.rowptr, p.A.col, p.A.val).transpose()
+    w = np.random.default_rng(1).standard_normal(p.m)
+    got, ref = s.debug_apply(1, w), At.matvec(w)
+    assert np.max(np.abs(got - ref)) <= 1e-13 * np.max(np.abs(ref))
+    s.close()
+
+
+def test_blur_matches_oracle():
+    from paper_2605_22281_b200 import SFLSQR
+    for H, W in ((256, 256), (37, 53)):
+        s = SFLSQR(maxit=4)
+        s.set_operator_blur(H, W, 2.5, 7)
+        op = BlurOperator(H, W, 2.5, 7)
+        x = np.random.default_rng(2).standard_normal(H * W)
+        got, ref = s.debug_apply(0, x), op.matvec(x)
+        assert np.max(np.abs(got - ref)) <= 1e-13 * np.max(np.abs(ref))
+        s.close()
+
+
+# ------------------------------------------------------------------ end to end, config 1 (dense, sigma_min 1e-6)
+@pytest.mark.parametrize("method", ["sflsqr", "sflsmr"])
+def test_config1_full(method):
+    p = make_problem(1)
+    spec = [s for s in p.solvers if s.method == method][0]
+    r = solve_problem(p, spec)
+    g = _gpu_run(p, spec)
+    _compare(g, r)
+
+
+@pytest.mark.parametrize("method", ["sflsqr", "sflsmr"])
+def test_config1_discrepancy_stop(method):
+    # a safety factor the run reaches mid-way, so the discrepancy rule fires (eq. discrP)
+    p = make_problem(1)
+    spec = [s for s in p.solvers if s.method == method][0]
+    full = solve_problem(p, spec, eta=0.0)
+    eta = float(full.true_res[14] / p.delta_e) * (1 + 1e-7)
+    r = solve_problem(p, spec, eta=eta)
+    assert r.status == 3
+    g = _gpu_run(p, spec, eta=eta)
+    _compare(g, r)
+
+
+@pytest.mark.parametrize("use_graph", [True, False])
+def test_graph_and_eager_agree_bitwise(use_graph):
+    p = make_problem(1)
+    spec = p.solvers[0]
+    g1 = _gpu_run(p, spec, maxit=15, use_graph=use_graph)
+    g2 = _gpu_run(p, spec, maxit=15, use_graph=True)
+    assert np.array_equal(g1["x"], g2["x"])              # deterministic reductions
+    assert np.array_equal(g1["true_res"], g2["true_res"])
+
+
+# ------------------------------------------------------------------ config 2 (blur, IRN)
+def test_config2_blur():
+    p = make_problem(2)
+    spec = p.solvers[0]
+    r = solve_problem(p, spec, maxit=60)
+    g = _gpu_run(p, spec, maxit=60)
+    _compare(g, r)
+
+
+# ------------------------------------------------------------------ config 3 reduced (Siddon, NONNEG), full 150 its
+@pytest.mark.parametrize("method", ["sflsqr", "sflsmr"])
+def test_config3_reduced(method):
+    p = make_problem(3, N=128, n_angles=90, nb=183)
+    spec = [s for s in p.solvers if s.method == method][0]
+    r = solve_problem(p, spec)
+    g = _gpu_run(p, spec)
+    _compare(g, r)
+
+
+# ------------------------------------------------------------------ config 4 reduced (unmatched B, identity tau)
+def _stable_horizon(p, spec, maxit, thresh=1e-11):
+    """Last k up to which the ORACLE itself is forward-stable: a 1e-15 relative
+    perturbation of b moves its true residuals by < thresh."""
+    op = operator_from_problem(p)
+    r0 = solve_problem(p, spec, op=op, maxit=maxit, eta=0.0)
+    b0 = p.b
+    p.b = b0 * (1 + 1e-15 * np.random.default_rng(0).standard_normal(b0.size))
+    try:
+        r1 = solve_problem(p, spec, op=op, maxit=maxit, eta=0.0)
+    finally:
+        p.b = b0
+    dev = np.abs(np.array(r1.true_res) - np.array(r0.true_res)) / np.array(r0.true_res)
+    bad = np.flatnonzero(dev > thresh)
+    return (int(bad[0]) if bad.size else len(dev)), r0, dev
+
+
+def test_config4_reduced_within_oracle_stable_horizon():
+    # The unmatched-B, identity-tau run loses forward stability in the oracle itself after ~15
+    # iterations (S A Z_k becomes ill-conditioned); strict parity is required up to that horizon,
+    # later iterations are checked by state injection below.
+    p = make_problem(4, N=192, n_angles=135, nb=273)
+    spec = p.solvers[0]
+    kstar, r0, dev = _stable_horizon(p, spec, 60)
+    assert kstar >= 10, kstar
+    r = solve_problem(p, spec, maxit=kstar, eta=0.0)
+    g = _gpu_run(p, spec, maxit=kstar)
+    _compare(g, r, n_res=kstar)
+
+
+# ------------------------------------------------------------------ state injection (one oracle step from GPU state)
+def _inject(p, spec, ks, maxit, tol_vec=1e-12, tol_res=1e-9):
+    from oracle.sflsqr import step_from_state
+    from oracle.sketch import SparseSignSketch
+    from paper_2605_22281_b200 import solver_for_problem
+    op = operator_from_problem(p)
+    dim = p.m if spec.method == "sflsqr" else p.n
+    sk = SparseSignSketch(p.sketch_seed, spec.d, spec.s_nz, dim)
+    ell = min(spec.window, maxit)
+    s = solver_for_problem(p, spec, maxit=maxit, eta=0.0)
+    s.set_rhs(p.b)
+    done = 0
+    rel = lambda a, b: np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)  # noqa: E731
+    report = []
+    for k in ks:
+        s.iterate(k - 1 - done)
+        done = k - 1
+        B = s.debug_basis()
+        V = s.debug_state(ell, spec.d, spec.method)
+        use_ring = spec.orth_mode == "P" and spec.precond != "identity"
+        if use_ring:
+            Pw = {j: V["p_ring"][(j - 1) % ell] for j in range(max(1, k - ell), k)}
+        else:
+            Pw = {j: B["Z"][:, j - 1] for j in range(max(1, k - ell), k)}
+        out = step_from_state(op, p.b, spec.method, k, ell, sk, B["Z"], Pw, B["W"], V["z"], V["x"],
+                              B["H"], V["sketch_cols"], V["rhs"], precond=spec.precond, p_exp=spec.p,
+                              eps_rel=spec.eps_rel, orth_mode=spec.orth_mode)
+        s.iterate(1)
+        done = k
+        B2 = s.debug_basis()
+        V2 = s.debug_state(ell, spec.d, spec.method)
+        tr, sk_res = s.get_residual_norms()
+        newcol = V2["sketch_cols"][:, -1]
+        ocol = out["Mcol"] if spec.method == "sflsqr" else out["Sz"]
+        # The projected LS is backward stable on both sides; its outputs can differ by
+        # ~u * cond(M) (normwise), which near rank deficiency exceeds 1e-9.
+        kappa = float(np.linalg.cond(out["M"]))
+        ls_tol = max(tol_res, 100 * 2.0 ** -53 * kappa)
+        nrhs, nb = np.linalg.norm(V["rhs"]), np.linalg.norm(p.b)
+        errs = dict(T=rel(B2["T"][:k, k - 1], out["Tcol"]), z=rel(B2["Z"][:, k - 1], out["z"]),
+                    H=rel(B2["H"][:k + 1, k - 1], out["Hcol"]), w=rel(B2["W"][:, k], out["w_next"]),
+                    sk=rel(newcol, ocol),
+                    sres=abs(sk_res[k - 1] - out["sres"]) / max(out["sres"], ls_tol * nrhs / tol_res),
+                    r=abs(tr[k - 1] - out["r"]) / max(out["r"], ls_tol * nb / tol_res),
+                    My=np.linalg.norm(out["M"] @ (B2["y"] - out["y"])) / nrhs / (ls_tol / tol_res))
+        report.append((k, kappa, errs))
+        print(f"inject k={k} cond(M)={kappa:.2e} " + " ".join(f"{a}={b:.1e}" for a, b in errs.items()))
+        for key in ("T", "z", "H", "w", "sk"):
+            assert errs[key] < tol_vec, (k, key, errs)
+        for key in ("sres", "r", "My"):
+            assert errs[key] < tol_res, (k, key, kappa, errs)
+    s.close()
+    return report
+
+
+def test_config4_reduced_state_injection():
+    p = make_problem(4, N=192, n_angles=135, nb=273)
+    _inject(p, p.solvers[0], ks=[2, 17, 60, 140, 200], maxit=200)
+
+
+@pytest.mark.parametrize("method", ["sflsqr", "sflsmr"])
+def test_config3_reduced_state_injection(method):
+    p = make_problem(3, N=128, n_angles=90, nb=183)
+    spec = [s for s in p.solvers if s.method == method][0]
+    _inject(p, spec, ks=[1, 4, 90, 150], maxit=150)
+
+
+def test_config1_state_injection_both_orth_modes():
+    p = make_problem(1)
+    for spec in p.solvers:
+        _inject(p, spec, ks=[3, 20, 40], maxit=40)
+        spec_z = SolverSpec(**{**spec.__dict__, "orth_mode": "Z"})
+        _inject(p, spec_z, ks=[3, 40], maxit=40)
+
+
+# ------------------------------------------------------------------ full BASELINE sizes (oracle on the first iterations)
+def test_config3_full_size_first_iterations():
+    p = make_problem(3)
+    spec = p.solvers[0]
+    r = solve_problem(p, spec, maxit=12, record=False)
+    g = _gpu_run(p, spec, maxit=12)
+    _compare(g, r, n_res=12)
+
+
+def test_config4_full_size_first_iterations():
+    p = make_problem(4)
+    spec = p.solvers[0]
+    r = solve_problem(p, spec, maxit=3, record=False)
+    g = _gpu_run(p, spec, maxit=3)
+    _compare(g, r, n_res=3)
+
+
+def test_config4_full_size_state_injection():
+    # full BASELINE size, the launch configuration bench.py times: one oracle step from the GPU state
+    p = make_problem(4)
+    _inject(p, p.solvers[0], ks=[101, 200], maxit=200)
+
+
+def test_config3_full_size_state_injection_sflsmr():
+    p = make_problem(3)
+    spec = p.solvers[1]
+    _inject(p, spec, ks=[150], maxit=150)
+
+
+# ------------------------------------------------------------------ edge cases
+def _dense_prob(m, n, seed=0, cond=1e3):
+    from gen.problems import CSR, Problem
+    rng = np.random.default_rng(seed)
+    U = np.linalg.qr(rng.standard_normal((m, min(m, n))))[0]
+    V = np.linalg.qr(rng.standard_normal((n, min(m, n))))[0]
+    A = (U * np.logspace(0, -np.log10(cond), min(m, n))) @ V.T
+    x = rng.standard_normal(n)
+    e = rng.standard_normal(m)
+    b = A @ x
+    e *= 0.02 * np.linalg.norm(b) / np.linalg.norm(e)
+    return Problem(name="dense", config_index=0, m=m, n=n, A=CSR.from_dense(A), T=None, t_mode="build", blur=None,
+                   x_true=x, b=b + e, e=e, delta=0.02, delta_e=float(np.linalg.norm(e)), sketch_seed=1234 + seed)
+
+
+@pytest.mark.parametrize("m,n,method,window,precond,orth,s_nz,d", [
+    (37, 29, "sflsqr", 1, "irn", "P", 1, 25),        # CountSketch, window 1, ragged sizes
+    (64, 40, "sflsmr", 50, "identity", "P", 3, 30),  # window >= maxit: full orthogonalisation
+    (90, 70, "sflsqr", 3, "nonneg", "Z", 8, 41),     # literal Alg. 1 orthogonalisation
+    (90, 70, "sflsmr", 2, "irn", "Z", 4, 21),
+    (300, 1000, "sflsqr", 2, "irn", "P", 8, 21),     # underdetermined, d = maxit + 1
+    (1025, 513, "sflsmr", 4, "nonneg", "P", 2, 20),  # d = maxit
+])
+def test_edge_configurations(m, n, method, window, precond, orth, s_nz, d):
+    p = _dense_prob(m, n, seed=m + n)
+    spec = SolverSpec(method=method, maxit=20, window=window, d=d, s_nz=s_nz, precond=precond, orth_mode=orth)
+    r = solve_problem(p, spec)
+    g = _gpu_run(p, spec)
+    _compare(g, r)
+
+
+def test_breakdown_matches_oracle():
+    from gen.problems import CSR, Problem
+    A = np.diag([1.0, 2.0, 3.0, 4.0])
+    b = np.array([1.0, 1.0, 0.0, 0.0])
+    p = Problem(name="bd", config_index=0, m=4, n=4, A=CSR.from_dense(A), T=None, t_mode="build", blur=None,
+                x_true=np.zeros(4), b=b, e=np.zeros(4), delta=0, delta_e=0.0, sketch_seed=5)
+    spec = SolverSpec(method="sflsqr", maxit=4, window=4, d=4, s_nz=1, precond="identity")
+    r = solve_problem(p, spec)
+    g = _gpu_run(p, spec)
+    assert r.status == 4 and g["status"] == 4 and g["info"]["k_x"] == r.k
+    np.testing.assert_allclose(g["x"], r.x, rtol=1e-10, atol=1e-12)
+
+
+def test_k1_and_restart():
+    from paper_2605_22281_b200 import solver_for_problem
+    p = make_problem(1)
+    spec = p.solvers[0]
+    s = solver_for_problem(p, spec, maxit=5, eta=0.0)
+    s.set_rhs(p.b)
+    s.iterate(1)
+    r1 = solve_problem(p, spec, maxit=1, eta=0.0)
+    assert np.linalg.norm(s.get_x() - r1.x) <= 1e-12 * np.linalg.norm(r1.x)
+    done, st = s.iterate(100)
+    assert done and st == 1 and s.get_info()["k_done"] == 5
+    s.set_rhs(p.b)                       # restart reproduces the first solve
+    s.iterate(5)
+    r5 = solve_problem(p, spec, maxit=5, eta=0.0)
+    assert np.linalg.norm(s.get_x() - r5.x) <= 1e-10 * np.linalg.norm(r5.x)
+    s.close()
+
+
+def test_error_codes():
+    from paper_2605_22281_b200 import SFLSQR, SflsqrError
+    from paper_2605_22281_b200 import sflsqr as B
+    s = SFLSQR(maxit=10)
+    with pytest.raises(SflsqrError) as e:
+        s.set_rhs(np.ones(4))                        # no operator yet
+    assert e.value.code == B.E_STATE
+    rp = np.array([0, 1, 2], dtype=np.int64)
+    with pytest.raises(SflsqrError) as e:
+        s.set_operator(2, 2, rp, np.array([0, 5], dtype=np.int32), np.ones(2))
+    assert e.value.code == B.E_DIM
+    with pytest.raises(SflsqrError) as e:
+        s.set_operator(2, 2, rp, np.array([0, 1], dtype=np.int32), np.array([1.0, np.nan]))
+    assert e.value.code == B.E_NONFINITE
+    s.set_operator(2, 2, rp, np.array([0, 1], dtype=np.int32), np.ones(2))
+    with pytest.raises(SflsqrError) as e:
+        s.set_sketch(1, 5, 1)                        # d < maxit
+    assert e.value.code == B.E_INVALID
+    s.set_sketch(1, 10, 1)
+    with pytest.raises(SflsqrError) as e:
+        s.set_rhs(np.zeros(2))
+    assert e.value.code == B.E_ZERO_RHS
+    with pytest.raises(SflsqrError) as e:
+        s.set_rhs(np.ones(3))
+    assert e.value.code == B.E_DIM
+    with pytest.raises(SflsqrError) as e:
+        s.set_precond("irn", p=3.0)
+    assert e.value.code == B.E_INVALID
+    s.close()

@@ -253,3 +253,27 @@ def test_breakdown_returns_previous_iterate():
     r = solve(DenseOperator(A), b, "sflsqr", maxit=6, window=6, sketch=IdentitySketch(3))
     assert r.status == BREAKDOWN
     np.testing.assert_allclose(A @ r.x, b, atol=1e-12)
+
+
+# ---------------------------------------------------------------- state injection machinery
+@pytest.mark.parametrize("method,precond", [("sflsqr", "irn"), ("sflsmr", "nonneg"), ("sflsqr", "identity")])
+def test_step_from_state_reproduces_the_run(method, precond):
+    # step_from_state (used to check GPU steps from exported state) must replay iteration k exactly
+    from oracle.sflsqr import step_from_state
+    A, b, _ = _dense_problem(70, 50, 1e3, 12)
+    ell, K = 3, 14
+    sk = SparseSignSketch(31, 40, 4, 70 if method == "sflsqr" else 50)
+    op = DenseOperator(A)
+    r = solve(op, b, method, maxit=K, window=ell, sketch=sk, precond=precond)
+    for k in (1, 2, 5, 14):
+        Zp, Wp = r.Z[:, :k - 1], r.W[:, :k]
+        Pw = {j: r.P[:, j - 1] for j in range(max(1, k - ell), k)}
+        ncol = k - 1 if method == "sflsqr" else k
+        out = step_from_state(op, b, method, k, ell, sk, Zp, Pw, Wp, op.tmatvec(r.W[:, k - 1]),
+                              r.xs[k - 2] if k > 1 else np.zeros(50), r.H[:k, :k - 1], r.sketch_cols[:, :ncol],
+                              r.rhs, precond=precond)
+        np.testing.assert_array_equal(out["z"], r.Z[:, k - 1])
+        np.testing.assert_array_equal(out["w_next"], r.W[:, k])
+        np.testing.assert_array_equal(out["Hcol"], r.H[:k + 1, k - 1])
+        np.testing.assert_array_equal(out["x"], r.xs[k - 1])
+        assert out["r"] == r.true_res[k - 1] and out["sres"] == r.sketch_res[k - 1]
