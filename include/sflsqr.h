@@ -223,6 +223,15 @@ int sflsqr_debug_basis(sflsqr_t *h, double *H, double *Tm, double *Z, double *W,
  * (sFLSMR), column-major; rhs (d) = s_b or s_{A^T b}. */
 int sflsqr_debug_state(sflsqr_t *h, double *z, double *x, double *p_ring, double *sketch_cols, double *rhs);
 
+/* Tuning knob (performance only; every variant is deterministic and
+ * oracle-checked): spmv_mode -1 (default) = per-operator rule on the average
+ * row length; 0 = warp-per-row CSR with 128-bit per-lane loads; 1..10 = row-group
+ * CSR variants (rows per CTA x chunks in flight: 1: 16x4, 2: 8x4, 3: 32x4,
+ * 4: 16x8, 5: 8x8, 6: 16x2, 7/9: 32x4 contiguous ranges, 8: 64 half-warp rows,
+ * 10: 32x2); band_shift is reserved (8..30).  Invalidates a captured graph
+ * (rebuilt at the next set_rhs). */
+int sflsqr_debug_set_tuning(sflsqr_t *h, int32_t spmv_mode, int32_t band_shift);
+
 /* Profiling: on = 1 launches kernels eagerly (no graph) with CUDA events around
  * every launch; sflsqr_get_profile returns the accumulated times since the last
  * sflsqr_reset_profile. */

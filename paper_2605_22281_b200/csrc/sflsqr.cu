@@ -69,6 +69,8 @@ struct sflsqr {
   int kernels_per_iter = 0;
   int64_t launches = 0;
   int host_k = 1;  // host mirror (profiling byte model only)
+  int spmv_mode = -1;    // -1: per-operator rule (select_spmv_mode); 0..10: forced variant (tuning)
+  int band_shift = 16;   // reserved
   bool prof_on = false;
   Prof prof;
 };
@@ -280,6 +282,14 @@ void prof_collect(sflsqr_t* h) {
   p.used = 0;
 }
 
+// Deterministic per-operator SpMV variant (measured on configs 3-4):
+// long rows (>= 1024 nnz average, e.g. the pixel-driven backprojector) -> half-warp
+// rows, 64 adjacent rows per CTA; otherwise one warp per row, 32 rows per CTA.
+int select_spmv_mode(int64_t nnz, int64_t nrows) {
+  const double avg = nrows > 0 ? (double)nnz / (double)nrows : 0.0;
+  return avg >= 1024.0 ? 8 : 3;
+}
+
 // y = A x (which 0) or y = T x (which 1); x may be a k-relative column (x_ld != 0).
 void enqueue_apply(sflsqr_t* h, int which, const DevState* st, const double* x, int64_t x_ld, int x_koff,
                    double* y, int cls) {
@@ -303,11 +313,48 @@ void enqueue_apply(sflsqr_t* h, int which, const DevState* st, const double* x, 
   const int64_t nnz = which == 0 ? h->nnz_a : h->nnz_t;
   const int64_t ncols = which == 0 ? h->n : h->m;
   const double bytes = 12.0 * nnz + 8.0 * (nrows + 1) + 8.0 * ncols + 8.0 * nrows;
-  constexpr int WPB = kSpmvThreads / 32;
-  const int64_t want = (nrows + WPB - 1) / WPB;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, 148 * 8));
   Launch L(h, cls, bytes);
-  k_spmv_csr<<<grid, kSpmvThreads, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
+  auto grid_for = [&](int wpb, int per_sm) {
+    const int64_t want = (nrows + wpb - 1) / wpb;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(want, 148 * per_sm));
+  };
+  const int mode = h->spmv_mode >= 0 ? h->spmv_mode : select_spmv_mode(nnz, nrows);
+  switch (mode) {
+    case 0:
+      k_spmv_csr<<<grid_for(kSpmvThreads / 32, 8), kSpmvThreads, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld,
+                                                                               x_koff, y);
+      break;
+    case 2:
+      k_spmv_csr_rows<8, 4><<<grid_for(8, 8), 256, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
+      break;
+    case 3:
+      k_spmv_csr_rows<32, 4><<<grid_for(32, 2), 1024, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
+      break;
+    case 4:
+      k_spmv_csr_rows<16, 8><<<grid_for(16, 4), 512, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
+      break;
+    case 5:
+      k_spmv_csr_rows<8, 8><<<grid_for(8, 8), 256, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
+      break;
+    case 6:
+      k_spmv_csr_rows<16, 2><<<grid_for(16, 4), 512, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
+      break;
+    case 7:
+      k_spmv_csr_rows_contig<32, 4><<<148 * 2, 1024, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
+      break;
+    case 8:
+      k_spmv_csr_half<32, 4><<<grid_for(64, 2), 1024, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
+      break;
+    case 9:
+      k_spmv_csr_rows_contig<32, 4><<<148 * 4, 1024, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
+      break;
+    case 10:
+      k_spmv_csr_rows<32, 2><<<grid_for(32, 2), 1024, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
+      break;
+    default:
+      k_spmv_csr_rows<16, 4><<<grid_for(16, 4), 512, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
+      break;
+  }
 }
 
 // S v for a vector of length len (global column offset 0) -> finalize target.
@@ -549,6 +596,8 @@ int sflsqr_create(sflsqr_t** out, const sflsqr_opts* o) {
     }
     h->own_stream = true;
   }
+  if (const char* e = std::getenv("SFLSQR_SPMV_MODE")) h->spmv_mode = std::atoi(e);
+  if (const char* e = std::getenv("SFLSQR_BAND_SHIFT")) h->band_shift = std::atoi(e);
   if (cudaFuncSetAttribute(k_sketch_partial, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (kSkThreads / 32) * kMaxD * (int)sizeof(double)) != cudaSuccess) {
     cudaGetLastError();
@@ -951,6 +1000,19 @@ int sflsqr_debug_state(sflsqr_t* h, double* z, double* x, double* p_ring, double
   if (rhs) CU(h, cudaMemcpyAsync(rhs, P.rhs, sizeof(double) * P.d, cudaMemcpyDeviceToHost, h->stream));
   CU(h, cudaStreamSynchronize(h->stream));
   if (h->prof_on) prof_collect(h);
+  return SFLSQR_OK;
+}
+
+int sflsqr_debug_set_tuning(sflsqr_t* h, int32_t spmv_mode, int32_t band_shift) {
+  if (!h) return fail(nullptr, SFLSQR_E_INVALID, "NULL handle");
+  if (spmv_mode < -1 || spmv_mode > 10 || band_shift < 8 || band_shift > 30)
+    return fail(h, SFLSQR_E_INVALID, "bad tuning values");
+  h->spmv_mode = spmv_mode;
+  h->band_shift = band_shift;
+  if (h->gexec) {
+    cudaGraphExecDestroy(h->gexec);
+    h->gexec = nullptr;
+  }
   return SFLSQR_OK;
 }
 

@@ -298,6 +298,124 @@ __global__ void __launch_bounds__(kSpmvThreads) k_spmv_csr(const DevState* st, i
   }
 }
 
+// Row-group CSR SpMV (default).  Each CTA owns WPB consecutive rows at a time
+// (one warp per row; adjacent rays / adjacent pixels, so their gathered x lines
+// overlap and are served from L1), grid-stride over row groups.  Within a row the
+// entries are consumed in order in lane-strided chunks (lane L takes element
+// p + L, so one gather instruction touches consecutive entries of the row and the
+// column / value streams are fully coalesced), UNR chunks in flight per warp.
+// Summation order is fixed (per-lane FMA chain, then a shuffle tree): deterministic.
+template <int WPB, int UNR>
+__global__ void __launch_bounds__(WPB * 32) k_spmv_csr_rows(const DevState* st, int64_t nrows,
+                                                            const int64_t* __restrict__ rowptr,
+                                                            const int* __restrict__ col,
+                                                            const double* __restrict__ val,
+                                                            const double* __restrict__ x_base, int64_t x_ld,
+                                                            int x_koff, double* __restrict__ y) {
+  if (st && st->done) return;
+  const double* __restrict__ x = kvec(st, x_base, x_ld, x_koff);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int64_t row = (int64_t)blockIdx.x * WPB + wid; row < nrows; row += (int64_t)gridDim.x * WPB) {
+    const int64_t s = rowptr[row], e = rowptr[row + 1];
+    double sum = 0.0;
+    int64_t p = s + lane;
+    for (; p + 32 * (UNR - 1) < e; p += 32 * UNR) {
+      int c[UNR];
+      double v[UNR], xv[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) c[u] = ld_stream_i(col + p + 32 * u);
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) v[u] = ld_stream_d(val + p + 32 * u);
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) xv[u] = __ldg(x + c[u]);
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) sum = fma(v[u], xv[u], sum);
+    }
+    for (; p < e; p += 32) sum = fma(ld_stream_d(val + p), __ldg(x + ld_stream_i(col + p)), sum);
+    sum = warp_sum(sum);
+    if (lane == 0) y[row] = sum;
+  }
+}
+
+// Variant: each CTA walks a CONTIGUOUS range of row groups (consecutive groups
+// of adjacent rows re-use the L1 lines of the previous group).
+template <int WPB, int UNR>
+__global__ void __launch_bounds__(WPB * 32) k_spmv_csr_rows_contig(const DevState* st, int64_t nrows,
+                                                                   const int64_t* __restrict__ rowptr,
+                                                                   const int* __restrict__ col,
+                                                                   const double* __restrict__ val,
+                                                                   const double* __restrict__ x_base, int64_t x_ld,
+                                                                   int x_koff, double* __restrict__ y) {
+  if (st && st->done) return;
+  const double* __restrict__ x = kvec(st, x_base, x_ld, x_koff);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t ngroups = (nrows + WPB - 1) / WPB;
+  const int64_t per = (ngroups + gridDim.x - 1) / gridDim.x;
+  const int64_t g0 = (int64_t)blockIdx.x * per, g1 = min(ngroups, g0 + per);
+  for (int64_t g = g0; g < g1; ++g) {
+    const int64_t row = g * WPB + wid;
+    if (row >= nrows) continue;
+    const int64_t s = rowptr[row], e = rowptr[row + 1];
+    double sum = 0.0;
+    int64_t p = s + lane;
+    for (; p + 32 * (UNR - 1) < e; p += 32 * UNR) {
+      int c[UNR];
+      double v[UNR], xv[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) c[u] = ld_stream_i(col + p + 32 * u);
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) v[u] = ld_stream_d(val + p + 32 * u);
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) xv[u] = __ldg(x + c[u]);
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) sum = fma(v[u], xv[u], sum);
+    }
+    for (; p < e; p += 32) sum = fma(ld_stream_d(val + p), __ldg(x + ld_stream_i(col + p)), sum);
+    sum = warp_sum(sum);
+    if (lane == 0) y[row] = sum;
+  }
+}
+
+// Variant: half-warp per row (2 rows per warp, 2*WPB adjacent rows per CTA).
+template <int WPB, int UNR>
+__global__ void __launch_bounds__(WPB * 32) k_spmv_csr_half(const DevState* st, int64_t nrows,
+                                                            const int64_t* __restrict__ rowptr,
+                                                            const int* __restrict__ col,
+                                                            const double* __restrict__ val,
+                                                            const double* __restrict__ x_base, int64_t x_ld,
+                                                            int x_koff, double* __restrict__ y) {
+  if (st && st->done) return;
+  const double* __restrict__ x = kvec(st, x_base, x_ld, x_koff);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int hl = lane & 15, half = lane >> 4;
+  for (int64_t r0 = (int64_t)blockIdx.x * 2 * WPB; r0 < nrows; r0 += (int64_t)gridDim.x * 2 * WPB) {
+    const int64_t row = r0 + 2 * wid + half;
+    int64_t s = 0, e = 0;
+    if (row < nrows) {
+      s = rowptr[row];
+      e = rowptr[row + 1];
+    }
+    double sum = 0.0;
+    int64_t p = s + hl;
+    for (; p + 16 * (UNR - 1) < e; p += 16 * UNR) {
+      int c[UNR];
+      double v[UNR], xv[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) c[u] = ld_stream_i(col + p + 16 * u);
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) v[u] = ld_stream_d(val + p + 16 * u);
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) xv[u] = __ldg(x + c[u]);
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) sum = fma(v[u], xv[u], sum);
+    }
+    for (; p < e; p += 16) sum = fma(ld_stream_d(val + p), __ldg(x + ld_stream_i(col + p)), sum);
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (hl == 0 && row < nrows) y[row] = sum;
+  }
+}
+
 // ------------------------------------------------------------------ a3 (config 2): separable blur
 // Zero-boundary 2-D Gaussian PSF outer(g, g) applied as a row pass then a
 // column pass (matrix-free; symmetric so it also serves as T).

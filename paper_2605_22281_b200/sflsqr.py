@@ -34,6 +34,7 @@ EXPORTED = [
     "sflsqr_version", "sflsqr_create", "sflsqr_set_operator", "sflsqr_set_operator_blur", "sflsqr_set_sketch",
     "sflsqr_set_precond", "sflsqr_set_rhs", "sflsqr_iterate", "sflsqr_get_x", "sflsqr_get_residual_norms",
     "sflsqr_get_info", "sflsqr_debug_sketch_table", "sflsqr_debug_apply", "sflsqr_debug_basis", "sflsqr_debug_state",
+    "sflsqr_debug_set_tuning",
     "sflsqr_set_profiling", "sflsqr_reset_profile", "sflsqr_get_profile", "sflsqr_last_error", "sflsqr_destroy",
 ]
 
@@ -85,6 +86,7 @@ def load_library(path: str = LIB_PATH):
         "sflsqr_debug_apply": ([vp, i32, vp, vp], ctypes.c_int),
         "sflsqr_debug_basis": ([vp, vp, vp, vp, vp, vp], ctypes.c_int),
         "sflsqr_debug_state": ([vp, vp, vp, vp, vp, vp], ctypes.c_int),
+        "sflsqr_debug_set_tuning": ([vp, i32, i32], ctypes.c_int),
         "sflsqr_set_profiling": ([vp, i32], ctypes.c_int),
         "sflsqr_reset_profile": ([vp], ctypes.c_int),
         "sflsqr_get_profile": ([vp, ctypes.POINTER(Profile)], ctypes.c_int),
@@ -273,6 +275,9 @@ class SFLSQR:
         self._check(self.lib.sflsqr_debug_state(self.h, z.ctypes.data, x.ctypes.data, ring.ctypes.data,
                                                 cols.ctypes.data, rhs.ctypes.data))
         return dict(z=z, x=x, p_ring=ring, sketch_cols=cols[:, :nc], rhs=rhs)
+
+    def debug_set_tuning(self, spmv_mode=-1, band_shift=16):
+        self._check(self.lib.sflsqr_debug_set_tuning(self.h, int(spmv_mode), int(band_shift)))
 
     def set_profiling(self, on=True):
         self._check(self.lib.sflsqr_set_profiling(self.h, 1 if on else 0))

@@ -47,9 +47,14 @@ def _compare(g, r, n_res=N_RES, res_tol=RES_TOL, x_tol=X_TOL):
     assert g["status"] == r.status and g["info"]["k_x"] == r.k
     n = min(n_res, kk)
     rt = np.abs(g["true_res"][:n] - np.array(r.true_res[:n])) / np.array(r.true_res[:n])
-    # sketched residual: relative, with an absolute rounding floor u-scaled to ||rhs|| ~ max history
-    # (at k = d the projected system is square and the residual is 0 up to rounding)
-    floor = 1e-12 * max(r.sketch_res)
+    # sketched residual: relative, with an absolute rounding floor 100 u cond(M) ||rhs|| (the LS is
+    # backward stable on both sides; at k = d it is square and the residual is 0 up to rounding)
+    if r.sketch_cols.shape[1] >= kk + 1:        # sFLSMR: M = [S_TW, S z] H
+        M = r.sketch_cols[:, :kk + 1] @ r.H[:kk + 1, :kk]
+    else:                                        # sFLSQR: M = S A Z (or a stopped sFLSMR: approximate)
+        M = r.sketch_cols[:, :kk]
+    kappa = float(np.linalg.cond(M)) if kk else 1.0
+    floor = max(1e-12, 100 * 2.0 ** -53 * kappa) * np.linalg.norm(r.rhs)
     rs = np.abs(g["sketch_res"][:n] - np.array(r.sketch_res[:n])) / np.maximum(np.array(r.sketch_res[:n]), floor)
     assert rt.max() < res_tol, ("true residual", rt.max(), int(rt.argmax()) + 1)
     assert rs.max() < res_tol, ("sketched residual", rs.max(), int(rs.argmax()) + 1)
