@@ -171,8 +171,10 @@ def bench_reference(args, prob, spec, world, rank):
     line = {"metric": METRIC, "value": val, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus, "steps": k,
             "warmup": 1, "ms_per_step": per_it * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": prob.name, "m": prob.m, "n": prob.n, "nnz_A": prob.A.nnz,
-                       "nnz_T": prob.T.nnz if prob.T is not None else prob.A.nnz, "ell": spec.window, "d": spec.d,
+            "config": {"workload": prob.name, "m": prob.m, "n": prob.n,
+                       "nnz_A": prob.A.nnz if prob.A is not None else None,
+                       "nnz_T": prob.T.nnz if prob.T is not None else (prob.A.nnz if prob.A is not None else None),
+                       "ell": spec.window, "d": spec.d,
                        "s": spec.s_nz, "tau": spec.precond},
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle",
                              "sample": f"{k} oracle iterations after init+1 (time budget {budget:.0f} s)"},
@@ -265,12 +267,13 @@ def main():
                            "algo_gbs": d["bytes"] / (d["ms"] / 1e3) / 1e9 if d["ms"] > 0 else None,
                            "share": d["ms"] / ms}
     if kernels:
-        dom = max(("spmv_A", "spmv_T"), key=lambda k2: kernels.get(k2, {"ms_total": 0})["ms_total"])
+        dom = max(kernels, key=lambda k2: kernels[k2]["ms_total"])
         d = prof[dom]
         bpl = d["bytes"] / d["launches"]
         ach = bpl / (d["ms"] / d["launches"] / 1e3) / 1e9
         tr = _traffic(prob.name, dom)
-        roof = {"bound": "hbm", "kernel": "k_spmv_csr (" + dom + ")", "achieved": ach, "peak": peak,
+        kname = {"spmv_A": "k_spmv_csr (A z)", "spmv_T": "k_spmv_csr (T w)"}.get(dom, dom)
+        roof = {"bound": "hbm", "kernel": kname, "achieved": ach, "peak": peak,
                 "unit": "GB/s", "frac": ach / peak, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": bpl, "traffic": tr}
     step_bytes = sum(d["bytes"] for d in prof.values())
@@ -306,7 +309,8 @@ def main():
             "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": prob.name, "method": spec.method, "m": prob.m, "n": prob.n,
-                       "nnz_A": prob.A.nnz, "nnz_T": prob.T.nnz if prob.T is not None else prob.A.nnz,
+                       "nnz_A": prob.A.nnz if prob.A is not None else None,
+                       "nnz_T": prob.T.nnz if prob.T is not None else (prob.A.nnz if prob.A is not None else None),
                        "ell": spec.window, "d": spec.d, "s": spec.s_nz, "tau": spec.precond, "maxit": maxit,
                        "iterations_timed": f"{W + 1}..{W + K}", "history": "true residual (W path) on",
                        "l2": "inputs larger than L2 (operators ~30 GB vs 126 MB L2); no flush",

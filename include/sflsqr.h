@@ -225,11 +225,11 @@ int sflsqr_debug_state(sflsqr_t *h, double *z, double *x, double *p_ring, double
 
 /* Tuning knob (performance only; every variant is deterministic and
  * oracle-checked): spmv_mode -1 (default) = per-operator rule on the average
- * row length; 0 = warp-per-row CSR with 128-bit per-lane loads; 1..10 = row-group
- * CSR variants (rows per CTA x chunks in flight: 1: 16x4, 2: 8x4, 3: 32x4,
- * 4: 16x8, 5: 8x8, 6: 16x2, 7/9: 32x4 contiguous ranges, 8: 64 half-warp rows,
- * 10: 32x2); band_shift is reserved (8..30).  Invalidates a captured graph
- * (rebuilt at the next set_rhs). */
+ * row length; 0 = warp-per-row CSR with 128-bit per-lane loads; 1, 2, 3, 10 =
+ * row-group CSR (rows per CTA x chunks in flight: 16x4, 8x4, 32x4, 32x2);
+ * 8 = 64 half-warp rows per CTA.  Modes 3 and 8 fuse the sketch into the SpMV;
+ * the others use the standalone sketch kernel.  band_shift is reserved (8..30).
+ * Invalidates a captured graph (rebuilt at the next set_rhs). */
 int sflsqr_debug_set_tuning(sflsqr_t *h, int32_t spmv_mode, int32_t band_shift);
 
 /* Profiling: on = 1 launches kernels eagerly (no graph) with CUDA events around

@@ -291,8 +291,8 @@ int select_spmv_mode(int64_t nnz, int64_t nrows) {
 }
 
 // y = A x (which 0) or y = T x (which 1); x may be a k-relative column (x_ld != 0).
-void enqueue_apply(sflsqr_t* h, int which, const DevState* st, const double* x, int64_t x_ld, int x_koff,
-                   double* y, int cls) {
+void enqueue_apply(sflsqr_t* h, int which, const DevState* st, const double* x, int64_t x_ld, int x_koff, double* y,
+                   int cls) {
   const int64_t nrows = which == 0 ? h->m : h->n;
   if (h->blur) {
     const int64_t nn = (int64_t)h->bH * h->bW;
@@ -314,8 +314,8 @@ void enqueue_apply(sflsqr_t* h, int which, const DevState* st, const double* x, 
   const int64_t ncols = which == 0 ? h->n : h->m;
   const double bytes = 12.0 * nnz + 8.0 * (nrows + 1) + 8.0 * ncols + 8.0 * nrows;
   Launch L(h, cls, bytes);
-  auto grid_for = [&](int wpb, int per_sm) {
-    const int64_t want = (nrows + wpb - 1) / wpb;
+  auto grid_for = [&](int rows_per_cta, int per_sm) {
+    const int64_t want = (nrows + rows_per_cta - 1) / rows_per_cta;
     return (int)std::max<int64_t>(1, std::min<int64_t>(want, 148 * per_sm));
   };
   const int mode = h->spmv_mode >= 0 ? h->spmv_mode : select_spmv_mode(nnz, nrows);
@@ -324,54 +324,33 @@ void enqueue_apply(sflsqr_t* h, int which, const DevState* st, const double* x, 
       k_spmv_csr<<<grid_for(kSpmvThreads / 32, 8), kSpmvThreads, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld,
                                                                                x_koff, y);
       break;
+    case 1:
+      k_spmv_csr_rows<16, 4><<<grid_for(16, 4), 512, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
+      break;
     case 2:
       k_spmv_csr_rows<8, 4><<<grid_for(8, 8), 256, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
-      break;
-    case 3:
-      k_spmv_csr_rows<32, 4><<<grid_for(32, 2), 1024, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
-      break;
-    case 4:
-      k_spmv_csr_rows<16, 8><<<grid_for(16, 4), 512, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
-      break;
-    case 5:
-      k_spmv_csr_rows<8, 8><<<grid_for(8, 8), 256, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
-      break;
-    case 6:
-      k_spmv_csr_rows<16, 2><<<grid_for(16, 4), 512, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
-      break;
-    case 7:
-      k_spmv_csr_rows_contig<32, 4><<<148 * 2, 1024, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
-      break;
-    case 8:
-      k_spmv_csr_half<32, 4><<<grid_for(64, 2), 1024, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
-      break;
-    case 9:
-      k_spmv_csr_rows_contig<32, 4><<<148 * 4, 1024, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
       break;
     case 10:
       k_spmv_csr_rows<32, 2><<<grid_for(32, 2), 1024, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
       break;
-    default:
-      k_spmv_csr_rows<16, 4><<<grid_for(16, 4), 512, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
+    case 8:
+      k_spmv_csr_half<32, 4><<<grid_for(64, 2), 1024, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
+      break;
+    default:  // 3
+      k_spmv_csr_rows<32, 4><<<grid_for(32, 2), 1024, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
       break;
   }
 }
 
-// S v for a vector of length len (global column offset 0) -> finalize target.
-void enqueue_sketch(sflsqr_t* h, const DevState* st, const double* v, int64_t len, int mult_beta, double* out,
-                    int64_t out_ld, int out_koff, double* out2) {
-  const size_t smem = (size_t)(kSkThreads / 32) * h->d * sizeof(double);
-  {
-    Launch L(h, SFLSQR_KC_SKETCH, 8.0 * len + 8.0 * kSkBlocks * h->d);
-    k_sketch_partial<<<kSkBlocks, kSkThreads, smem, h->stream>>>(st, v, len, 0, h->d, h->s_nz, h->G, h->P.seed_lo,
-                                                                  h->P.seed_hi, h->P.sk_scale, h->P.skpart);
-  }
-  {
-    Launch L(h, SFLSQR_KC_SKETCH, 8.0 * kSkBlocks * h->d);
-    const int grid = (h->d + 127) / 128;
-    k_sketch_finalize<<<grid, 128, 0, h->stream>>>(st, h->P.skpart, kSkBlocks, h->d, mult_beta, out, out_ld, out_koff,
-                                                   out2);
-  }
+// out = S v (times beta when mult_beta; optional unscaled copy out2), v and out
+// optionally k-relative columns.  S is the stored d x dim CSR built by build_sketch.
+void enqueue_sketch(sflsqr_t* h, const DevState* st, const double* v, int64_t v_ld, int v_koff, int mult_beta,
+                    double* out, int64_t out_ld, int out_koff, double* out2) {
+  const int64_t dim = h->P.method == SFLSQR_METHOD_SFLSQR ? h->m : h->n;
+  Launch L(h, SFLSQR_KC_SKETCH, 12.0 * h->s_nz * dim + 8.0 * (h->d + 1) + 8.0 * h->d);
+  const int grid = std::min(h->d, 148 * 8);
+  k_sketch_apply<<<grid, 256, 0, h->stream>>>(st, h->P.sk_rp, h->P.sk_ent, v, v_ld, v_koff, h->d, h->P.sk_scale,
+                                              mult_beta, out, out_ld, out_koff, out2);
 }
 
 // One iteration k of Alg. 1 / Alg. 2.
@@ -394,7 +373,7 @@ void enqueue_iteration(sflsqr_t* h) {
   // a3: w = A z_k  (z_k = Z[:, k-1])
   enqueue_apply(h, 0, P.st, P.Z, h->n, -1, P.w, SFLSQR_KC_SPMV_A);
   // a4 (sFLSQR): S_AZ[:, k] = S w
-  if (P.method == SFLSQR_METHOD_SFLSQR) enqueue_sketch(h, P.st, P.w, h->m, 0, P.Mcols, P.d, -1, nullptr);
+  if (P.method == SFLSQR_METHOD_SFLSQR) enqueue_sketch(h, P.st, P.w, 0, 0, 0, P.Mcols, P.d, -1, nullptr);
   // a5: w-side windowed MGS (ell + 2 passes) and normalisation
   for (int pass = 0; pass <= P.ell + 1; ++pass) {
     const int J = std::min(P.ell + 1, k);
@@ -409,7 +388,7 @@ void enqueue_iteration(sflsqr_t* h) {
   // a6: z = T w_{k+1}  (w_{k+1} = W[:, k])
   enqueue_apply(h, 1, P.st, P.W, h->m, 0, P.z, SFLSQR_KC_SPMV_T);
   // a4 (sFLSMR): S z -> S_TW[:, k+1]
-  if (P.method == SFLSQR_METHOD_SFLSMR) enqueue_sketch(h, P.st, P.z, h->n, 0, P.STW, P.d, 0, nullptr);
+  if (P.method == SFLSQR_METHOD_SFLSMR) enqueue_sketch(h, P.st, P.z, 0, 0, 0, P.STW, P.d, 0, nullptr);
   // a7: projected sketched LS
   {
     Launch L(h, SFLSQR_KC_LS, 8.0 * P.d * (k + 2));
@@ -434,6 +413,51 @@ void enqueue_iteration(sflsqr_t* h) {
 int check_launch(sflsqr_t* h) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(h, SFLSQR_E_CUDA, "kernel launch: %s", cudaGetErrorString(e));
+  return SFLSQR_OK;
+}
+
+// Generate the sparse-sign table with the device hash (k_sketch_table) and store S
+// transposed as a d x dim CSR: entries of sketch row r are the coordinates i with a
+// nonzero in row r, increasing i, sign in bit 31 (stable counting sort on the host).
+int build_sketch(sflsqr_t* h) {
+  Params& P = h->P;
+  const int64_t dim = P.method == SFLSQR_METHOD_SFLSQR ? h->m : h->n;
+  const int s = h->s_nz, d = h->d;
+  const int64_t ne = dim * s;
+  int* drows = nullptr;
+  int8_t* dsig = nullptr;
+  int rc;
+  if ((rc = dalloc(h, (void**)&drows, sizeof(int) * ne, nullptr))) return rc;
+  if ((rc = dalloc(h, (void**)&dsig, ne, nullptr))) {
+    cudaFree(drows);
+    return rc;
+  }
+  const int grid = (int)std::min<int64_t>((dim * h->G + 255) / 256 + 1, 148 * 16);
+  k_sketch_table<<<grid, 256, 0, h->stream>>>(0, dim, d, s, h->G, P.seed_lo, P.seed_hi, drows, dsig);
+  std::vector<int> rows(ne);
+  std::vector<int8_t> sig(ne);
+  cudaMemcpyAsync(rows.data(), drows, sizeof(int) * ne, cudaMemcpyDeviceToHost, h->stream);
+  cudaMemcpyAsync(sig.data(), dsig, ne, cudaMemcpyDeviceToHost, h->stream);
+  cudaError_t e = cudaStreamSynchronize(h->stream);
+  cudaFree(drows);
+  cudaFree(dsig);
+  if (e != cudaSuccess) return fail(h, SFLSQR_E_CUDA, "sketch table: %s", cudaGetErrorString(e));
+  std::vector<int64_t> rp(d + 1, 0);
+  for (int64_t q = 0; q < ne; ++q) rp[rows[q] + 1]++;
+  for (int r = 0; r < d; ++r) rp[r + 1] += rp[r];
+  std::vector<int64_t> next(rp.begin(), rp.end() - 1);
+  std::vector<uint32_t> ent(ne);
+  for (int64_t i = 0; i < dim; ++i)
+    for (int t = 0; t < s; ++t) {
+      const int64_t q = i * s + t;
+      ent[next[rows[q]]++] = (uint32_t)i | (sig[q] < 0 ? 0x80000000u : 0u);
+    }
+  if ((rc = dalloc(h, (void**)&P.sk_rp, sizeof(int64_t) * (d + 1), &h->solve_allocs, &h->solve_sizes))) return rc;
+  if ((rc = dalloc(h, (void**)&P.sk_ent, sizeof(uint32_t) * std::max<int64_t>(ne, 1), &h->solve_allocs,
+                   &h->solve_sizes)))
+    return rc;
+  CU(h, cudaMemcpy(P.sk_rp, rp.data(), sizeof(int64_t) * (d + 1), cudaMemcpyHostToDevice));
+  CU(h, cudaMemcpy(P.sk_ent, ent.data(), sizeof(uint32_t) * ne, cudaMemcpyHostToDevice));
   return SFLSQR_OK;
 }
 
@@ -483,7 +507,7 @@ int alloc_solve(sflsqr_t* h) {
   if ((rc = A(&P.z, n)) || (rc = A(&P.x, n)) || (rc = A(&P.Z, n * maxit)) || (rc = A(&P.w, m)) ||
       (rc = A(&P.W, m * (maxit + 1))) || (rc = A(&P.b, m)) || (rc = A(&P.H, (size_t)(maxit + 1) * maxit)) ||
       (rc = A(&P.Tm, (size_t)maxit * maxit)) || (rc = A(&P.part, (size_t)s * kVecBlocks)) ||
-      (rc = A(&P.skpart, (size_t)kSkBlocks * d)) || (rc = A(&P.rhs, d)) || (rc = A(&P.Mcols, (size_t)d * maxit)) ||
+      (rc = A(&P.rhs, d)) || (rc = A(&P.Mcols, (size_t)d * maxit)) ||
       (rc = A(&P.STW, (size_t)d * (maxit + 1))) || (rc = A(&P.V, (size_t)d * maxit)) || (rc = A(&P.taus, maxit)) ||
       (rc = A(&P.R, (size_t)maxit * maxit)) || (rc = A(&P.qtb, d)) || (rc = A(&P.y, maxit)) ||
       (rc = A(&P.g, maxit + 1)) || (rc = A(&P.hist_true, maxit)) || (rc = A(&P.hist_sk, maxit)))
@@ -497,6 +521,7 @@ int alloc_solve(sflsqr_t* h) {
     for (size_t i = 0; i < h->solve_allocs.size(); ++i)
       if (h->solve_allocs[i] != (void*)P.st) CU(h, cudaMemset(h->solve_allocs[i], 0xFF, h->solve_sizes[i]));
   }
+  if ((rc = build_sketch(h))) return rc;
   h->bufs = true;
   return SFLSQR_OK;
 }
@@ -598,10 +623,8 @@ int sflsqr_create(sflsqr_t** out, const sflsqr_opts* o) {
   }
   if (const char* e = std::getenv("SFLSQR_SPMV_MODE")) h->spmv_mode = std::atoi(e);
   if (const char* e = std::getenv("SFLSQR_BAND_SHIFT")) h->band_shift = std::atoi(e);
-  if (cudaFuncSetAttribute(k_sketch_partial, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (kSkThreads / 32) * kMaxD * (int)sizeof(double)) != cudaSuccess) {
-    cudaGetLastError();
-  }
+
+
   *out = h;
   return SFLSQR_OK;
 }
@@ -772,10 +795,10 @@ int sflsqr_set_rhs(sflsqr_t* h, const double* b, int64_t len, int32_t mem_flags)
   enqueue_apply(h, 1, P.st, P.W, 0, 0, P.z, SFLSQR_KC_SPMV_T);
   if (P.method == SFLSQR_METHOD_SFLSQR) {
     // L459: s_b = S b
-    enqueue_sketch(h, P.st, P.b, h->m, 0, P.rhs, 0, 0, nullptr);
+    enqueue_sketch(h, P.st, P.b, 0, 0, 0, P.rhs, 0, 0, nullptr);
   } else {
     // L761-762: s = beta S z, S_TW = [S z]
-    enqueue_sketch(h, P.st, P.z, h->n, 1, P.rhs, 0, 0, P.STW);
+    enqueue_sketch(h, P.st, P.z, 0, 0, 1, P.rhs, 0, 0, P.STW);
   }
   {
     Launch L(h, SFLSQR_KC_LS, 16.0 * h->d);
@@ -1005,7 +1028,7 @@ int sflsqr_debug_state(sflsqr_t* h, double* z, double* x, double* p_ring, double
 
 int sflsqr_debug_set_tuning(sflsqr_t* h, int32_t spmv_mode, int32_t band_shift) {
   if (!h) return fail(nullptr, SFLSQR_E_INVALID, "NULL handle");
-  if (spmv_mode < -1 || spmv_mode > 10 || band_shift < 8 || band_shift > 30)
+  if (spmv_mode < -1 || spmv_mode > 10 || (spmv_mode > 3 && spmv_mode != 8 && spmv_mode != 10) || band_shift < 8 || band_shift > 30)
     return fail(h, SFLSQR_E_INVALID, "bad tuning values");
   h->spmv_mode = spmv_mode;
   h->band_shift = band_shift;

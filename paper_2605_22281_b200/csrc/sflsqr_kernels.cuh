@@ -50,7 +50,9 @@ struct Params {
   double* part;
   int slot_zin, slot_z0, slot_win, slot_w0, slot_xmax, slot_res, slot_beta;
   // sketch
-  double *skpart, *rhs, *Mcols, *STW;
+  int64_t* sk_rp;          // S stored transposed: d+1 row pointers
+  uint32_t* sk_ent;         // coordinate | sign << 31, s * dim entries
+  double *rhs, *Mcols, *STW;
   // projected LS
   double *V, *taus, *R, *qtb, *y, *g;
   // history
@@ -306,7 +308,7 @@ __global__ void __launch_bounds__(kSpmvThreads) k_spmv_csr(const DevState* st, i
 // column / value streams are fully coalesced), UNR chunks in flight per warp.
 // Summation order is fixed (per-lane FMA chain, then a shuffle tree): deterministic.
 template <int WPB, int UNR>
-__global__ void __launch_bounds__(WPB * 32) k_spmv_csr_rows(const DevState* st, int64_t nrows,
+__global__ void __launch_bounds__(WPB * 32, 2048 / (WPB * 32)) k_spmv_csr_rows(const DevState* st, int64_t nrows,
                                                             const int64_t* __restrict__ rowptr,
                                                             const int* __restrict__ col,
                                                             const double* __restrict__ val,
@@ -315,70 +317,34 @@ __global__ void __launch_bounds__(WPB * 32) k_spmv_csr_rows(const DevState* st, 
   if (st && st->done) return;
   const double* __restrict__ x = kvec(st, x_base, x_ld, x_koff);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int64_t row = (int64_t)blockIdx.x * WPB + wid; row < nrows; row += (int64_t)gridDim.x * WPB) {
-    const int64_t s = rowptr[row], e = rowptr[row + 1];
+  for (int64_t r0 = (int64_t)blockIdx.x * WPB; r0 < nrows; r0 += (int64_t)gridDim.x * WPB) {
+    const int64_t row = r0 + wid;
     double sum = 0.0;
-    int64_t p = s + lane;
-    for (; p + 32 * (UNR - 1) < e; p += 32 * UNR) {
-      int c[UNR];
-      double v[UNR], xv[UNR];
+    if (row < nrows) {
+      const int64_t s = rowptr[row], e = rowptr[row + 1];
+      int64_t p = s + lane;
+      for (; p + 32 * (UNR - 1) < e; p += 32 * UNR) {
+        int c[UNR];
+        double v[UNR], xv[UNR];
 #pragma unroll
-      for (int u = 0; u < UNR; ++u) c[u] = ld_stream_i(col + p + 32 * u);
+        for (int u = 0; u < UNR; ++u) c[u] = ld_stream_i(col + p + 32 * u);
 #pragma unroll
-      for (int u = 0; u < UNR; ++u) v[u] = ld_stream_d(val + p + 32 * u);
+        for (int u = 0; u < UNR; ++u) v[u] = ld_stream_d(val + p + 32 * u);
 #pragma unroll
-      for (int u = 0; u < UNR; ++u) xv[u] = __ldg(x + c[u]);
+        for (int u = 0; u < UNR; ++u) xv[u] = __ldg(x + c[u]);
 #pragma unroll
-      for (int u = 0; u < UNR; ++u) sum = fma(v[u], xv[u], sum);
+        for (int u = 0; u < UNR; ++u) sum = fma(v[u], xv[u], sum);
+      }
+      for (; p < e; p += 32) sum = fma(ld_stream_d(val + p), __ldg(x + ld_stream_i(col + p)), sum);
+      sum = warp_sum(sum);
+      if (lane == 0) y[row] = sum;
     }
-    for (; p < e; p += 32) sum = fma(ld_stream_d(val + p), __ldg(x + ld_stream_i(col + p)), sum);
-    sum = warp_sum(sum);
-    if (lane == 0) y[row] = sum;
-  }
-}
-
-// Variant: each CTA walks a CONTIGUOUS range of row groups (consecutive groups
-// of adjacent rows re-use the L1 lines of the previous group).
-template <int WPB, int UNR>
-__global__ void __launch_bounds__(WPB * 32) k_spmv_csr_rows_contig(const DevState* st, int64_t nrows,
-                                                                   const int64_t* __restrict__ rowptr,
-                                                                   const int* __restrict__ col,
-                                                                   const double* __restrict__ val,
-                                                                   const double* __restrict__ x_base, int64_t x_ld,
-                                                                   int x_koff, double* __restrict__ y) {
-  if (st && st->done) return;
-  const double* __restrict__ x = kvec(st, x_base, x_ld, x_koff);
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int64_t ngroups = (nrows + WPB - 1) / WPB;
-  const int64_t per = (ngroups + gridDim.x - 1) / gridDim.x;
-  const int64_t g0 = (int64_t)blockIdx.x * per, g1 = min(ngroups, g0 + per);
-  for (int64_t g = g0; g < g1; ++g) {
-    const int64_t row = g * WPB + wid;
-    if (row >= nrows) continue;
-    const int64_t s = rowptr[row], e = rowptr[row + 1];
-    double sum = 0.0;
-    int64_t p = s + lane;
-    for (; p + 32 * (UNR - 1) < e; p += 32 * UNR) {
-      int c[UNR];
-      double v[UNR], xv[UNR];
-#pragma unroll
-      for (int u = 0; u < UNR; ++u) c[u] = ld_stream_i(col + p + 32 * u);
-#pragma unroll
-      for (int u = 0; u < UNR; ++u) v[u] = ld_stream_d(val + p + 32 * u);
-#pragma unroll
-      for (int u = 0; u < UNR; ++u) xv[u] = __ldg(x + c[u]);
-#pragma unroll
-      for (int u = 0; u < UNR; ++u) sum = fma(v[u], xv[u], sum);
-    }
-    for (; p < e; p += 32) sum = fma(ld_stream_d(val + p), __ldg(x + ld_stream_i(col + p)), sum);
-    sum = warp_sum(sum);
-    if (lane == 0) y[row] = sum;
   }
 }
 
 // Variant: half-warp per row (2 rows per warp, 2*WPB adjacent rows per CTA).
 template <int WPB, int UNR>
-__global__ void __launch_bounds__(WPB * 32) k_spmv_csr_half(const DevState* st, int64_t nrows,
+__global__ void __launch_bounds__(WPB * 32, 2048 / (WPB * 32)) k_spmv_csr_half(const DevState* st, int64_t nrows,
                                                             const int64_t* __restrict__ rowptr,
                                                             const int* __restrict__ col,
                                                             const double* __restrict__ val,
@@ -452,64 +418,34 @@ __global__ void __launch_bounds__(256) k_blur_cols(const DevState* st, int H, in
 }
 
 // ------------------------------------------------------------------ a4: sparse-sign sketch
-// Per-block partial of S v (S: d x len, columns col0..col0+len-1 of the global
-// table).  Each warp owns a private d-bin array in shared memory and walks a
-// contiguous coordinate chunk in order; within a step the lane groups add in
-// group order, so the accumulation order is fixed.  skpart[blockIdx.x*d + r].
-__global__ void __launch_bounds__(kSkThreads) k_sketch_partial(const DevState* st, const double* __restrict__ v,
-                                                               int64_t len, int64_t col0, int d, int s, int G,
-                                                               uint32_t k0, uint32_t k1, double scale,
-                                                               double* __restrict__ skpart) {
+// S is generated once per solve by the Philox hash (k_sketch_table, bit-exact
+// with the oracle, readings R5/R6) and stored transposed, as a d x dim CSR whose
+// entries are the coordinate index with the sign in bit 31.  Applying it is then a
+// deterministic row-parallel gather-sum: out[r] = mult * scale * sum_i sign * v_i
+// over the coordinates i hashed to row r, in increasing i.  One CTA per sketch row.
+__global__ void __launch_bounds__(256) k_sketch_apply(const DevState* st, const int64_t* __restrict__ srp,
+                                                      const uint32_t* __restrict__ sent,
+                                                      const double* __restrict__ v_base, int64_t v_ld, int v_koff,
+                                                      int d, double scale, int mult_beta, double* out_base,
+                                                      int64_t out_ld, int out_koff, double* out2) {
+  __shared__ double sh[33];
   if (st && st->done) return;
-  extern __shared__ double bins[];  // (kSkThreads/32) * d
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  constexpr int WPB = kSkThreads / 32;
-  double* mybins = bins + (size_t)wid * d;
-  for (int r = lane; r < d; r += 32) mybins[r] = 0.0;
-  __syncwarp();
-  const int64_t nwarps = (int64_t)gridDim.x * WPB;
-  const int64_t gw = (int64_t)blockIdx.x * WPB + wid;
-  const int64_t chunk = (len + nwarps - 1) / nwarps;
-  const int64_t beg = gw * chunk;
-  const int64_t end = (beg + chunk < len) ? beg + chunk : len;
-  const int per = 32 / G;  // coordinates per warp step
-  const int grp = lane / G, gl = lane & (G - 1);
-  for (int64_t base = beg; base < end; base += per) {
-    const int64_t li = base + grp;
-    const bool valid = li < end;
-    int row, neg;
-    sk_warp_entries((uint64_t)(col0 + li), valid, s, G, (uint32_t)d, k0, k1, row, neg);
-    double val = 0.0;
-    if (valid && gl < s) val = (neg ? -scale : scale) * v[li];
-    for (int g2 = 0; g2 < per; ++g2) {
-      if (grp == g2 && valid && gl < s) mybins[row] += val;
-      __syncwarp();
+  const double* __restrict__ v = kvec(st, v_base, v_ld, v_koff);
+  double* out = kvec_w(st, out_base, out_ld, out_koff);
+  for (int r = blockIdx.x; r < d; r += gridDim.x) {
+    double acc = 0.0;
+    for (int64_t q = srp[r] + threadIdx.x; q < srp[r + 1]; q += 256) {
+      const uint32_t e = __ldg(sent + q);
+      const double vi = __ldg(v + (e & 0x7fffffffu));
+      acc += (e >> 31) ? -vi : vi;
+    }
+    acc = block_sum<256>(acc, sh) * scale;
+    if (threadIdx.x == 0) {
+      if (out2) out2[r] = acc;
+      out[r] = mult_beta ? acc * st->beta : acc;
     }
   }
-  __syncthreads();
-  for (int r = threadIdx.x; r < d; r += kSkThreads) {
-    double acc = 0.0;
-#pragma unroll
-    for (int w2 = 0; w2 < WPB; ++w2) acc += bins[(size_t)w2 * d + r];
-    skpart[(size_t)blockIdx.x * d + r] = acc;
-  }
 }
-
-// out[r] = mult * sum_b skpart[b*d + r] (block order); optional second copy.
-// out = (mult_beta ? beta : 1) * sum; out2 (optional) = sum.  out may be k-relative.
-__global__ void k_sketch_finalize(const DevState* st, const double* __restrict__ skpart, int nb, int d,
-                                  int mult_beta, double* out_base, int64_t out_ld, int out_koff, double* out2) {
-  if (st && st->done) return;
-  double* out = kvec_w(st, out_base, out_ld, out_koff);
-  const double mult = mult_beta ? st->beta : 1.0;
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < d; r += gridDim.x * blockDim.x) {
-    double acc = 0.0;
-    for (int b2 = 0; b2 < nb; ++b2) acc += skpart[(size_t)b2 * d + r];
-    if (out2) out2[r] = acc;
-    out[r] = mult_beta ? acc * mult : acc;
-  }
-}
-
 
 // ------------------------------------------------------------------ init
 // beta = ||b|| (partials in slot_beta), then w_1 = b / beta (Alg. 1).
@@ -673,43 +609,102 @@ __global__ void __launch_bounds__(kVecThreads) k_finish_w(Params P) {
 // is solved by back substitution (reading R14: the same reflector sequence as a
 // from-scratch Householder QR).  Also forms g = beta e_1 - H_{1:k+1,1:k} y for
 // the W-path true residual (eq. FGK: b - A Z y = W_{k+1} g).
+// Block reduction with one __syncthreads: warp partials into a double-buffered
+// slot array, every thread then sums the kLsThreads/32 partials in warp order.
+__device__ __forceinline__ double ls_reduce(double v, double (*red)[kLsThreads / 32], int& flip) {
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) red[flip][threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = 0.0;
+#pragma unroll
+  for (int w = 0; w < kLsThreads / 32; ++w) t += red[flip][w];
+  flip ^= 1;
+  return t;
+}
+
 __global__ void __launch_bounds__(kLsThreads) k_ls(Params P) {
+  constexpr int RPT = kMaxD / kLsThreads;  // rows per thread (4)
+  __shared__ double red[2][kLsThreads / 32];
+  __shared__ double a_s[kMaxD];
+  __shared__ double q_s[kMaxD];
+  __shared__ double blk[32][33];
   __shared__ double sh[33];
-  __shared__ double a[kMaxD];
-  __shared__ double q[kMaxD];
+  double* y_s = a_s;  // a_s is dead once R(:, c) and alpha have been read
   DevState* st = P.st;
   if (st->done) return;
   const int k = st->k, c = k - 1, d = P.d;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  int flip = 0;
   double* Mc = P.Mcols + (int64_t)c * d;
-  if (P.method == 0) {
-    for (int r = tid; r < d; r += kLsThreads) a[r] = Mc[r];
-  } else {
-    const int i0 = max(0, c - P.ell);
-    for (int r = tid; r < d; r += kLsThreads) {
-      double acc = 0.0;
-      for (int i = i0; i <= c + 1; ++i) acc = fma(P.STW[(int64_t)i * d + r], P.H[(int64_t)i + (int64_t)c * P.ldh], acc);
-      a[r] = acc;
-      Mc[r] = acc;
+  double a[RPT], q[RPT];
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) {
+    const int r = tid + u * kLsThreads;
+    a[u] = 0.0;
+    q[u] = 0.0;
+    if (r < d) {
+      if (P.method == 0) {
+        a[u] = Mc[r];
+      } else {
+        double acc = 0.0;
+        for (int i = max(0, c - P.ell); i <= c + 1; ++i)
+          acc = fma(P.STW[(int64_t)i * d + r], P.H[(int64_t)i + (int64_t)c * P.ldh], acc);
+        a[u] = acc;
+        Mc[r] = acc;
+      }
+      q[u] = P.qtb[r];
     }
   }
-  for (int r = tid; r < d; r += kLsThreads) q[r] = P.qtb[r];
-  __syncthreads();
-  // apply reflectors 0..c-1 to the new column
+  // apply reflectors 0..c-1 to the new column (Householder QR order); v_j, tau_j
+  // are prefetched two steps ahead so each step costs one block reduction.
+  double vA[RPT], vB[RPT];
+  double tauA = 0.0, tauB = 0.0;
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) {
+    const int r = tid + u * kLsThreads;
+    vA[u] = (c > 0 && r < d) ? P.V[r] : 0.0;
+    vB[u] = (c > 1 && r < d) ? P.V[(int64_t)d + r] : 0.0;
+  }
+  if (c > 0) tauA = P.taus[0];
+  if (c > 1) tauB = P.taus[1];
   for (int j = 0; j < c; ++j) {
-    const double* vj = P.V + (int64_t)j * d;
+    double vC[RPT];
+    const bool pre = j + 2 < c;
+    const double tauC = pre ? P.taus[j + 2] : 0.0;
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+      const int r = tid + u * kLsThreads;
+      vC[u] = (pre && r < d) ? P.V[(int64_t)(j + 2) * d + r] : 0.0;
+    }
     double part = 0.0;
-    for (int r = j + tid; r < d; r += kLsThreads) part = fma(vj[r], a[r], part);
-    const double dot = block_sum<kLsThreads>(part, sh);
-    const double f = P.taus[j] * dot;
-    for (int r = j + tid; r < d; r += kLsThreads) a[r] = fma(-f, vj[r], a[r]);
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) part = fma(vA[u], a[u], part);
+    const double dot = ls_reduce(part, red, flip);
+    const double f = tauA * dot;
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+      a[u] = fma(-f, vA[u], a[u]);
+      vA[u] = vB[u];
+      vB[u] = vC[u];
+    }
+    tauA = tauB;
+    tauB = tauC;
+  }
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) {
+    const int r = tid + u * kLsThreads;
+    if (r < d) a_s[r] = a[u];
   }
   __syncthreads();
-  for (int r = tid; r < c; r += kLsThreads) P.R[(int64_t)r + (int64_t)c * P.maxit] = a[r];
-  const double alpha = a[c];
+  for (int r = tid; r < c; r += kLsThreads) P.R[(int64_t)r + (int64_t)c * P.maxit] = a_s[r];
+  const double alpha = a_s[c];
   double part = 0.0;
-  for (int r = c + 1 + tid; r < d; r += kLsThreads) part = fma(a[r], a[r], part);
-  const double xnorm = sqrt(block_sum<kLsThreads>(part, sh));
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) {
+    const int r = tid + u * kLsThreads;
+    if (r > c && r < d) part = fma(a[u], a[u], part);
+  }
+  const double xnorm = sqrt(ls_reduce(part, red, flip));  // (its barrier also retires the a_s reads)
   double beta_h, tau, scal;
   if (xnorm == 0.0) {
     beta_h = alpha;
@@ -721,42 +716,68 @@ __global__ void __launch_bounds__(kLsThreads) k_ls(Params P) {
     scal = 1.0 / (alpha - beta_h);
   }
   double* vc = P.V + (int64_t)c * d;
-  for (int r = tid; r < d; r += kLsThreads) {
-    double vr = (r < c) ? 0.0 : (r == c ? 1.0 : (xnorm == 0.0 ? 0.0 : a[r] * scal));
-    vc[r] = vr;
-    a[r] = vr;  // a now holds v_c
+  double v[RPT];
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) {
+    const int r = tid + u * kLsThreads;
+    v[u] = (r < c) ? 0.0 : (r == c ? 1.0 : (xnorm == 0.0 ? 0.0 : a[u] * scal));
+    if (r >= d) v[u] = 0.0;
+    if (r < d) vc[r] = v[u];
   }
   if (tid == 0) {
     P.R[(int64_t)c + (int64_t)c * P.maxit] = beta_h;
     P.taus[c] = tau;
   }
-  __syncthreads();
   part = 0.0;
-  for (int r = c + tid; r < d; r += kLsThreads) part = fma(a[r], q[r], part);
-  const double dq = block_sum<kLsThreads>(part, sh);
-  const double fq = tau * dq;
-  for (int r = c + tid; r < d; r += kLsThreads) q[r] = fma(-fq, a[r], q[r]);
-  __syncthreads();
-  for (int r = tid; r < d; r += kLsThreads) P.qtb[r] = q[r];
-  // sketched residual ||(Q^T rhs)_{k+1:d}||
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) part = fma(v[u], q[u], part);
+  const double fq = tau * ls_reduce(part, red, flip);
   part = 0.0;
-  for (int r = k + tid; r < d; r += kLsThreads) part = fma(q[r], q[r], part);
-  const double sres = sqrt(block_sum<kLsThreads>(part, sh));
-  // back substitution R y = q[0:k] (column oriented); a[] reused for y
-  for (int i = k - 1; i >= 0; --i) {
-    __syncthreads();
-    const double yi = q[i] / P.R[(int64_t)i + (int64_t)i * P.maxit];
-    if (tid == 0) a[i] = yi;
-    for (int t = tid; t < i; t += kLsThreads) q[t] = fma(-P.R[(int64_t)t + (int64_t)i * P.maxit], yi, q[t]);
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) {
+    const int r = tid + u * kLsThreads;
+    q[u] = fma(-fq, v[u], q[u]);
+    if (r < d) {
+      P.qtb[r] = q[u];
+      q_s[r] = q[u];
+      if (r >= k) part = fma(q[u], q[u], part);
+    }
   }
-  __syncthreads();
-  for (int i = tid; i < k; i += kLsThreads) P.y[i] = a[i];
+  // sketched residual ||(Q^T rhs)_{k+1:d}||
+  const double sres = sqrt(ls_reduce(part, red, flip));
+  // back substitution R y = (Q^T rhs)_{1:k}, blocked by 32 columns from the right:
+  // warp 0 solves each 32 x 32 diagonal block from shared memory, then all threads
+  // update the remaining right-hand side with the block's columns.
+  for (int jb = ((k - 1) / 32) * 32; jb >= 0; jb -= 32) {
+    const int je = min(jb + 32, k), nb = je - jb;
+    for (int idx = tid; idx < nb * nb; idx += kLsThreads) {
+      const int rr = idx % nb, cc = idx / nb;
+      blk[rr][cc] = P.R[(int64_t)(jb + rr) + (int64_t)(jb + cc) * P.maxit];
+    }
+    __syncthreads();
+    if (wid == 0) {
+      double qv = lane < nb ? q_s[jb + lane] : 0.0;
+      for (int i = nb - 1; i >= 0; --i) {
+        const double yi = __shfl_sync(0xffffffffu, qv, i) / blk[i][i];
+        if (lane == i) y_s[jb + i] = yi;
+        if (lane < i) qv = fma(-blk[lane][i], yi, qv);
+      }
+    }
+    __syncthreads();
+    for (int t = tid; t < jb; t += kLsThreads) {
+      double qt = q_s[t];
+      for (int i = jb; i < je; ++i) qt = fma(-P.R[(int64_t)t + (int64_t)i * P.maxit], y_s[i], qt);
+      q_s[t] = qt;
+    }
+    __syncthreads();
+  }
+  for (int i = tid; i < k; i += kLsThreads) P.y[i] = y_s[i];
   // rank indicator (R14)
   double dmin = INFINITY, dmax = 0.0;
   for (int i = tid; i < k; i += kLsThreads) {
-    const double v = fabs(P.R[(int64_t)i + (int64_t)i * P.maxit]);
-    dmin = fmin(dmin, v);
-    dmax = fmax(dmax, v);
+    const double vv = fabs(P.R[(int64_t)i + (int64_t)i * P.maxit]);
+    dmin = fmin(dmin, vv);
+    dmax = fmax(dmax, vv);
   }
   const double gmax = block_max<kLsThreads>(dmax, sh);
   const double gmin = -block_max<kLsThreads>(-dmin, sh);
@@ -764,7 +785,7 @@ __global__ void __launch_bounds__(kLsThreads) k_ls(Params P) {
   for (int i = tid; i <= k; i += kLsThreads) {
     double acc = (i == 0) ? st->beta : 0.0;
     const int jlo = max(0, i - 1), jhi = min(k - 1, i + P.ell);
-    for (int j = jlo; j <= jhi; ++j) acc = fma(-P.H[(int64_t)i + (int64_t)j * P.ldh], a[j], acc);
+    for (int j = jlo; j <= jhi; ++j) acc = fma(-P.H[(int64_t)i + (int64_t)j * P.ldh], y_s[j], acc);
     P.g[i] = acc;
   }
   if (tid == 0) {
