@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define SFLSQR_ABI_VERSION 1
+#define SFLSQR_ABI_VERSION 2
 
 /* return codes */
 #define SFLSQR_OK 0
@@ -94,6 +94,10 @@ extern "C" {
 
 typedef struct sflsqr sflsqr_t;
 
+/* opts.comm_kind (world > 1) */
+#define SFLSQR_COMM_NCCL 0  /* one process per GPU, NCCL (libnccl.so.2 loaded at run time) */
+#define SFLSQR_COMM_LOCAL 1 /* ranks are host threads of one process sharing opts.local_group */
+
 typedef struct sflsqr_opts {
   int32_t method;    /* SFLSQR_METHOD_*                                            */
   int32_t window;    /* ell >= 1 (Alg. 1/2 "orthogonalization window"); >= maxit = full */
@@ -105,10 +109,13 @@ typedef struct sflsqr_opts {
   int32_t history;   /* SFLSQR_HIST_* bits                                         */
   int32_t device;    /* CUDA device ordinal                                        */
   void *stream;      /* cudaStream_t (borrowed) or NULL                            */
-  int32_t rank;      /* this process's rank (0)                                    */
-  int32_t world;     /* number of ranks; this build supports 1                     */
-  int32_t use_graph; /* 1: replay one captured CUDA graph per iteration            */
-  int32_t reserved[7];
+  int32_t rank;      /* this rank, 0 <= rank < world                               */
+  int32_t world;     /* number of ranks sharding the operator     */
+  int32_t use_graph; /* 1: replay one captured CUDA graph per iteration (world = 1) */
+  int32_t comm_kind; /* SFLSQR_COMM_* (world > 1)                                  */
+  const uint8_t *nccl_id; /* SFLSQR_COMM_NCCL: the 128-byte id of sflsqr_get_unique_id */
+  void *local_group;      /* SFLSQR_COMM_LOCAL: sflsqr_local_group_create()          */
+  int32_t reserved[4];
 } sflsqr_opts;
 
 typedef struct sflsqr_info {
@@ -116,10 +123,12 @@ typedef struct sflsqr_info {
   int32_t k_x;         /* index of the iterate get_x returns (x_{k_x})            */
   int32_t status;      /* SFLSQR_RUNNING/MAXIT/TOL/DISCREPANCY/BREAKDOWN          */
   int32_t rank_flag;   /* 1 if a projected problem had |R_kk| < 1e-14 max|R_jj| (R14) */
-  int64_t m, n;        /* operator shape                                          */
-  int64_t nnz_a, nnz_t;/* stored nonzeros of A and T (0 for the matrix-free blur) */
+  int64_t m, n;        /* global operator shape                                   */
+  int64_t nnz_a, nnz_t;/* stored nonzeros of this rank's A and T shards (0 for blur) */
   int64_t launches;    /* kernel launches issued so far (this handle)             */
   double beta;         /* ||b||                                                   */
+  int64_t m0, m_loc;   /* this rank's rows of A / slice of m-vectors: [m0, m0+m_loc) */
+  int64_t n0, n_loc;   /* this rank's slice of n-vectors: [n0, n0+n_loc)           */
 } sflsqr_info;
 
 /* Per-kernel-class device time, recorded with CUDA events on the library stream
@@ -145,9 +154,23 @@ int sflsqr_version(void);
 
 /* Create a solver handle.  Validates opts before any allocation:
  * method, window >= 1, maxit >= 1, tol >= 0, eta == 0 or eta > 1,
- * delta_e >= 0, world == 1 -> else SFLSQR_E_INVALID / SFLSQR_E_UNSUPPORTED.
- * Selects opts.device; fails with SFLSQR_E_CUDA when no CUDA device exists. */
+ * delta_e >= 0, 1 <= world, 0 <= rank < world -> else SFLSQR_E_INVALID.
+ * world > 1: NCCL comm from opts.nccl_id (collective over the ranks: every rank
+ * must call it) or the in-process group opts.local_group; SFLSQR_E_UNSUPPORTED
+ * when NCCL cannot be loaded.  Selects opts.device; fails with SFLSQR_E_CUDA when
+ * no CUDA device exists. */
 int sflsqr_create(sflsqr_t **h, const sflsqr_opts *opts);
+
+/* NCCL unique id for a multi-process group (call on rank 0, broadcast the 128
+ * bytes with the caller's process group, pass as opts.nccl_id on every rank). */
+int sflsqr_get_unique_id(uint8_t id[128]);
+
+/* In-process rank group (SFLSQR_COMM_LOCAL): world ranks on one device, each
+ * driven by its own host thread; collectives are host rendezvous + one reduction
+ * kernel in fixed rank order.  Used to run the sharded path on one GPU.  The group
+ * is reference counted by the handles that use it; destroy drops the caller's ref. */
+int sflsqr_local_group_create(void **group, int32_t world, int32_t device);
+void sflsqr_local_group_destroy(void *group);
 
 /* Operator A (m x n CSR) and the transpose-side operator T (n x m) used for
  * "A^T w" (Alg. 1 L458/L486, Alg. 2 L760/L789).
@@ -160,6 +183,23 @@ int sflsqr_create(sflsqr_t **h, const sflsqr_opts *opts);
 int sflsqr_set_operator(sflsqr_t *h, int64_t m, int64_t n, const int64_t *a_rowptr, const int32_t *a_col,
                         const double *a_val, int32_t t_mode, const int64_t *t_rowptr, const int32_t *t_col,
                         const double *t_val, int32_t mem_flags);
+
+/* Sharded operator (world > 1).  Rank g passes its contiguous
+ * block of A rows [a_row0, a_row1) (a_rowptr has a_row1 - a_row0 + 1 entries,
+ * any base; a_col are GLOBAL column indices).  The blocks of all ranks must tile
+ * [0, m) in rank order.  The transpose side:
+ *   t_mode = SFLSQR_T_BUILD: COLSHARD — T_g = (A block)^T is formed locally (no
+ *            communication); its product is a partial n-vector, reduce-scattered
+ *            to the even n-partition n0 = g*ceil(n/world);
+ *   t_mode = SFLSQR_T_GIVEN: ROWSHARD — rank g passes rows [t_row0, t_row1) of
+ *            T (n x m, GLOBAL column indices); the blocks must tile [0, n) in rank
+ *            order and define the n-partition; w is all-gathered before T w.
+ * Host arrays only.  Collective: every rank calls it.  world = 1 is equivalent to
+ * sflsqr_set_operator. */
+int sflsqr_set_operator_shard(sflsqr_t *h, int64_t m, int64_t n, int64_t a_row0, int64_t a_row1,
+                              const int64_t *a_rowptr, const int32_t *a_col, const double *a_val, int32_t t_mode,
+                              int64_t t_row0, int64_t t_row1, const int64_t *t_rowptr, const int32_t *t_col,
+                              const double *t_val);
 
 /* Matrix-free Gaussian blur (BASELINE.json config 2): m = n = H*W, separable
  * taps g_t ~ exp(-t^2/(2 sigma^2)), t = -radius..radius, normalised to sum 1,
@@ -180,7 +220,8 @@ int sflsqr_set_sketch(sflsqr_t *h, uint64_t seed, int32_t d, int32_t s_nz);
  * NONNEG (eps_rel > 0; R8).  Default: identity. */
 int sflsqr_set_precond(sflsqr_t *h, int32_t kind, double p, double eps_rel);
 
-/* Right-hand side b (length m) and start of a new solve: beta = ||b||,
+/* Right-hand side b (length m; with world > 1 this rank's slice [m0, m0+m_loc),
+ * collective) and start of a new solve: beta = ||b||,
  * w_1 = b/beta, z = T w_1, s_b = S b (sFLSQR) or s = beta S z (sFLSMR)
  * (Alg. 1, Alg. 2).  ||b|| = 0 -> SFLSQR_E_ZERO_RHS;
  * non-finite -> SFLSQR_E_NONFINITE; len != m -> SFLSQR_E_DIM. */
@@ -191,8 +232,9 @@ int sflsqr_set_rhs(sflsqr_t *h, const double *b, int64_t len, int32_t mem_flags)
  * Blocks until the issued work is complete. */
 int sflsqr_iterate(sflsqr_t *h, int32_t k, int32_t *done, int32_t *status);
 
-/* x_{k_x} = Z_{k_x} y_{k_x} (Alg. 1 L504 / Alg. 2) into x (length n,
- * host or device per mem_flags; caller owns the buffer).  x_0 = 0. */
+/* x_{k_x} = Z_{k_x} y_{k_x} (Alg. 1 L504 / Alg. 2) into x (length n; with
+ * world > 1 this rank's slice [n0, n0+n_loc)), host or device per mem_flags;
+ * caller owns the buffer.  x_0 = 0. */
 int sflsqr_get_x(sflsqr_t *h, double *x, int64_t len, int32_t mem_flags);
 
 /* Per-iteration histories (host buffers, either may be NULL):

@@ -1,0 +1,52 @@
+// Collectives used by the sharded sketched flexible Golub-Kahan step.
+//
+// Two implementations of one interface:
+//   * NcclComm   — one process per GPU, NCCL over NVLink/NVSwitch.  libnccl is
+//                  dlopen'ed on first use (the already-loaded libnccl.so.2, e.g.
+//                  PyTorch's, else the system one), so single-GPU use needs no NCCL.
+//   * LocalComm  — R ranks inside one process (one host thread per rank), all on
+//                  one device: the in-process stand-in used to test the sharded
+//                  CUDA path on a single GPU.  Each collective is a host
+//                  rendezvous: every rank records an event on its stream, the last
+//                  arriving rank makes a comm stream wait for all of them, reduces in
+//                  fixed rank order with one kernel, and every rank's stream waits on
+//                  the completion event.  No kernel ever waits on another rank.
+// All collectives are on fp64 device buffers and are deterministic (fixed
+// reduction order; identical bits on every rank).
+#pragma once
+
+#include <condition_variable>
+#include <cstddef>
+#include <cstdint>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+namespace sfl {
+
+struct Comm {
+  int rank = 0, world = 1;
+  virtual ~Comm() {}
+  // in-place sum / max over ranks of buf[0..count)
+  virtual int allreduce(double* buf, size_t count, bool is_max, cudaStream_t s, std::string& err) = 0;
+  // recv[r*count .. (r+1)*count) = send of rank r
+  virtual int allgather(const double* send, double* recv, size_t count, cudaStream_t s, std::string& err) = 0;
+  // recv = sum over ranks of send[rank*count .. (rank+1)*count)
+  virtual int reduce_scatter(const double* send, double* recv, size_t count, cudaStream_t s, std::string& err) = 0;
+  // blocking host allgather of `bytes` per rank (setup only)
+  virtual int allgather_host(const void* send, void* recv, size_t bytes, std::string& err) = 0;
+};
+
+// ---------------------------------------------------------------- NCCL (dlopen)
+int nccl_get_unique_id(uint8_t id[128], std::string& err);
+Comm* nccl_comm_create(const uint8_t id[128], int rank, int world, int device, std::string& err);
+
+// ---------------------------------------------------------------- in-process group
+struct LocalGroup;  // shared by the R handles of one group
+LocalGroup* local_group_create(int world, int device, std::string& err);
+void local_group_release(LocalGroup* g);  // reference counted
+Comm* local_comm_create(LocalGroup* g, int rank);
+
+}  // namespace sfl

@@ -1,9 +1,11 @@
 // libsflsqr.so — host driver and C ABI (include/sflsqr.h) of the B200
 // sketched flexible Golub-Kahan step.  One iteration of Alg. 1 / Alg. 2
 // (PAPER.md L450-508 / L752-808) is enqueued as a fixed kernel sequence that
-// reads the iteration index from device memory, captured once into a CUDA
-// graph and replayed per iteration; the only host<->device traffic inside
-// iterate() is one small state read at the end.
+// reads the iteration index from device memory, so on one rank it is captured
+// once into a CUDA graph and replayed per iteration; the only host<->device
+// traffic inside iterate() is one small state read at the end.  With world > 1
+// the operator is sharded (A rows, T rows or columns) and the
+// sequence interleaves the collectives of comm.h.
 #include <algorithm>
 #include <atomic>
 #include <cmath>
@@ -17,6 +19,7 @@
 
 #include <cuda_runtime.h>
 
+#include "comm.h"
 #include "sflsqr.h"
 #include "sflsqr_kernels.cuh"
 
@@ -35,6 +38,8 @@ struct Prof {
   Prof() { std::memset(&acc, 0, sizeof(acc)); }
 };
 
+enum TKind { T_FULL = 0, T_ROWSHARD = 1, T_COLSHARD = 2 };
+
 }  // namespace
 
 struct sflsqr {
@@ -42,9 +47,15 @@ struct sflsqr {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   std::string err;
-  // operator
+  // distribution
+  int rank = 0, world = 1;
+  Comm* comm = nullptr;
+  int tkind = T_FULL;
+  int64_t m0 = 0, m_loc = 0, n0 = 0, n_loc = 0, m_max = 0, n_max = 0;
+  // operator (this rank's shard)
   bool op_set = false, blur = false;
   int64_t m = 0, n = 0, nnz_a = 0, nnz_t = 0;
+  int64_t t_rows = 0;  // rows of the stored T (n_loc, n, or world * n_max for COLSHARD)
   int64_t *a_rowptr = nullptr, *t_rowptr = nullptr;
   int32_t *a_col = nullptr, *t_col = nullptr;
   double *a_val = nullptr, *t_val = nullptr;
@@ -63,13 +74,14 @@ struct sflsqr {
   bool bufs = false, rhs_set = false;
   Params P;
   int nslots = 0;
+  double *zfull = nullptr, *wfull = nullptr, *zpart = nullptr;
   std::vector<void*> solve_allocs;
   std::vector<size_t> solve_sizes;
   cudaGraphExec_t gexec = nullptr;
   int kernels_per_iter = 0;
   int64_t launches = 0;
-  int host_k = 1;  // host mirror (profiling byte model only)
-  int spmv_mode = -1;    // -1: per-operator rule (select_spmv_mode); 0..10: forced variant (tuning)
+  int host_k = 1;        // host mirror (profiling byte model only)
+  int spmv_mode = -1;    // -1: per-operator rule (select_spmv_mode); else a forced variant (tuning)
   int band_shift = 16;   // reserved
   bool prof_on = false;
   Prof prof;
@@ -130,20 +142,20 @@ void par_for(int64_t n, F f) {
   for (auto& t : th) t.join();
 }
 
-// Validate a host CSR: rowptr monotone from 0, columns in range, values finite.
+// Validate a host CSR block: rowptr monotone, columns in range, values finite.
 int validate_csr(sflsqr_t* h, const char* name, int64_t nrows, int64_t ncols, const int64_t* rp, const int32_t* col,
                  const double* val) {
-  if (!rp || !col || !val) return fail(h, SFLSQR_E_INVALID, "%s: NULL array", name);
-  if (rp[0] != 0) return fail(h, SFLSQR_E_DIM, "%s: rowptr[0] != 0", name);
+  if (!rp || (!col && rp[nrows] > rp[0]) || (!val && rp[nrows] > rp[0]))
+    return fail(h, SFLSQR_E_INVALID, "%s: NULL array", name);
   std::atomic<int> bad_rp(0), bad_col(0), bad_val(0);
   par_for(nrows, [&](int64_t s, int64_t e) {
     for (int64_t i = s; i < e; ++i)
       if (rp[i + 1] < rp[i]) bad_rp = 1;
   });
   if (bad_rp) return fail(h, SFLSQR_E_DIM, "%s: rowptr not monotone", name);
-  const int64_t nnz = rp[nrows];
+  const int64_t b = rp[0], nnz = rp[nrows] - rp[0];
   par_for(nnz, [&](int64_t s, int64_t e) {
-    for (int64_t p = s; p < e; ++p) {
+    for (int64_t p = b + s; p < b + e; ++p) {
       if (col[p] < 0 || col[p] >= ncols) bad_col = 1;
       if (!std::isfinite(val[p])) bad_val = 1;
     }
@@ -155,10 +167,13 @@ int validate_csr(sflsqr_t* h, const char* name, int64_t nrows, int64_t ncols, co
 
 // Host transpose (counting sort by column, parallel over row chunks; within each
 // output row entries keep increasing original-row order -> canonical, deterministic).
+// rp may have a nonzero base.  row_map (optional) maps an output row j to its
+// position in a (possibly padded) output of nout rows.
 void host_transpose(int64_t nrows, int64_t ncols, const int64_t* rp, const int32_t* col, const double* val,
-                    std::vector<int64_t>& trp, std::vector<int32_t>& tcol, std::vector<double>& tval) {
+                    int64_t nout, const std::vector<int64_t>* row_map, std::vector<int64_t>& trp,
+                    std::vector<int32_t>& tcol, std::vector<double>& tval) {
   const int nt = std::min(host_threads(), 16);
-  const int64_t nnz = rp[nrows];
+  const int64_t nnz = rp[nrows] - rp[0];
   std::vector<int64_t> rs(nt + 1);
   for (int t = 0; t <= nt; ++t) rs[t] = std::min(nrows, (nrows + nt - 1) / nt * t);
   std::vector<std::vector<int32_t>> cnt(nt, std::vector<int32_t>(ncols, 0));
@@ -171,17 +186,19 @@ void host_transpose(int64_t nrows, int64_t ncols, const int64_t* rp, const int32
       });
     for (auto& x : th) x.join();
   }
-  trp.assign(ncols + 1, 0);
+  auto orow = [&](int64_t j) { return row_map ? (*row_map)[j] : j; };
+  std::vector<int64_t> rowcnt(nout, 0);
   for (int64_t j = 0; j < ncols; ++j) {
     int64_t s = 0;
     for (int t = 0; t < nt; ++t) s += cnt[t][j];
-    trp[j + 1] = trp[j] + s;
+    rowcnt[orow(j)] = s;
   }
-  // per-thread starting offsets: off[t][j] = trp[j] + sum_{u<t} cnt[u][j]
+  trp.assign(nout + 1, 0);
+  for (int64_t r = 0; r < nout; ++r) trp[r + 1] = trp[r] + rowcnt[r];
   std::vector<std::vector<int64_t>> off(nt, std::vector<int64_t>(ncols));
   par_for(ncols, [&](int64_t s, int64_t e) {
     for (int64_t j = s; j < e; ++j) {
-      int64_t o = trp[j];
+      int64_t o = trp[orow(j)];
       for (int t = 0; t < nt; ++t) {
         off[t][j] = o;
         o += cnt[t][j];
@@ -213,6 +230,7 @@ void free_solve(sflsqr_t* h) {
   for (void* p : h->solve_allocs) cudaFree(p);
   h->solve_allocs.clear();
   h->solve_sizes.clear();
+  h->zfull = h->wfull = h->zpart = nullptr;
   h->bufs = false;
   h->rhs_set = false;
 }
@@ -282,6 +300,25 @@ void prof_collect(sflsqr_t* h) {
   p.used = 0;
 }
 
+// ------------------------------------------------------------------ collectives (no-ops on one rank)
+int coll_allreduce(sflsqr_t* h, double* buf, size_t count, bool is_max) {
+  if (h->world == 1) return SFLSQR_OK;
+  std::string e;
+  if (h->comm->allreduce(buf, count, is_max, h->stream, e)) return fail(h, SFLSQR_E_CUDA, "allreduce: %s", e.c_str());
+  return SFLSQR_OK;
+}
+
+// Sum (or max) the per-block partials of slots [slot0, slot0+ns) into P.scal and
+// allreduce them (the consumers then read P.scal; see get_sum).
+int reduce_slots(sflsqr_t* h, int slot0, int ns, bool is_max) {
+  if (h->world == 1) return SFLSQR_OK;
+  {
+    Launch L(h, SFLSQR_KC_ORTH, 8.0 * ns * kVecBlocks);
+    k_reduce_slots<<<ns, kVecThreads, 0, h->stream>>>(h->P, slot0, is_max ? 1 : 0);
+  }
+  return coll_allreduce(h, h->P.scal + slot0, ns, is_max);
+}
+
 // Deterministic per-operator SpMV variant (measured on configs 3-4):
 // long rows (>= 1024 nnz average, e.g. the pixel-driven backprojector) -> half-warp
 // rows, 64 adjacent rows per CTA; otherwise one warp per row, 32 rows per CTA.
@@ -290,10 +327,11 @@ int select_spmv_mode(int64_t nnz, int64_t nrows) {
   return avg >= 1024.0 ? 8 : 3;
 }
 
-// y = A x (which 0) or y = T x (which 1); x may be a k-relative column (x_ld != 0).
+// y = A x (which 0) or y = T x (which 1) for this rank's shard; x may be a
+// k-relative column (x_ld != 0).
 void enqueue_apply(sflsqr_t* h, int which, const DevState* st, const double* x, int64_t x_ld, int x_koff, double* y,
                    int cls) {
-  const int64_t nrows = which == 0 ? h->m : h->n;
+  const int64_t nrows = which == 0 ? h->m_loc : h->t_rows;
   if (h->blur) {
     const int64_t nn = (int64_t)h->bH * h->bW;
     const int grid = (int)std::min<int64_t>((nn + 255) / 256, 148 * 8);
@@ -311,8 +349,9 @@ void enqueue_apply(sflsqr_t* h, int which, const DevState* st, const double* x, 
   const int32_t* col = which == 0 ? h->a_col : h->t_col;
   const double* val = which == 0 ? h->a_val : h->t_val;
   const int64_t nnz = which == 0 ? h->nnz_a : h->nnz_t;
-  const int64_t ncols = which == 0 ? h->n : h->m;
-  const double bytes = 12.0 * nnz + 8.0 * (nrows + 1) + 8.0 * ncols + 8.0 * nrows;
+  const int64_t xlen = which == 0 ? (h->world > 1 ? h->world * h->n_max : h->n)
+                                  : (h->tkind == T_ROWSHARD ? h->world * h->m_max : h->m_loc);
+  const double bytes = 12.0 * nnz + 8.0 * (nrows + 1) + 8.0 * xlen + 8.0 * nrows;
   Launch L(h, cls, bytes);
   auto grid_for = [&](int rows_per_cta, int per_sm) {
     const int64_t want = (nrows + rows_per_cta - 1) / rows_per_cta;
@@ -342,72 +381,118 @@ void enqueue_apply(sflsqr_t* h, int which, const DevState* st, const double* x, 
   }
 }
 
-// out = S v (times beta when mult_beta; optional unscaled copy out2), v and out
-// optionally k-relative columns.  S is the stored d x dim CSR built by build_sketch.
-void enqueue_sketch(sflsqr_t* h, const DevState* st, const double* v, int64_t v_ld, int v_koff, int mult_beta,
-                    double* out, int64_t out_ld, int out_koff, double* out2) {
-  const int64_t dim = h->P.method == SFLSQR_METHOD_SFLSQR ? h->m : h->n;
-  Launch L(h, SFLSQR_KC_SKETCH, 12.0 * h->s_nz * dim + 8.0 * (h->d + 1) + 8.0 * h->d);
-  const int grid = std::min(h->d, 148 * 8);
-  k_sketch_apply<<<grid, 256, 0, h->stream>>>(st, h->P.sk_rp, h->P.sk_ent, v, v_ld, v_koff, h->d, h->P.sk_scale,
-                                              mult_beta, out, out_ld, out_koff, out2);
+// skbuf = S v (this rank's coordinates), allreduced over ranks.
+int enqueue_sketch(sflsqr_t* h, const DevState* st, const double* v) {
+  const int64_t dim_loc = h->P.method == SFLSQR_METHOD_SFLSQR ? h->m_loc : h->n_loc;
+  {
+    Launch L(h, SFLSQR_KC_SKETCH, 12.0 * h->s_nz * dim_loc + 8.0 * (h->d + 1) + 8.0 * h->d);
+    const int grid = std::min(h->d, 148 * 8);
+    k_sketch_apply<<<grid, 256, 0, h->stream>>>(st, h->P.sk_rp, h->P.sk_ent, v, h->d, h->P.sk_scale, h->P.skbuf);
+  }
+  return coll_allreduce(h, h->P.skbuf, h->d, false);
 }
 
-// One iteration k of Alg. 1 / Alg. 2 (SURVEY.md §8(a) rows a1-a9).
-void enqueue_iteration(sflsqr_t* h) {
+// z = T w for w = W[:, k] (k-relative) or W[:, 0] (init).
+int enqueue_transpose_product(sflsqr_t* h, bool init) {
+  Params& P = h->P;
+  const int64_t ld = init ? 0 : h->m_loc;
+  if (h->tkind == T_FULL) {
+    enqueue_apply(h, 1, P.st, P.W, ld, 0, P.z, SFLSQR_KC_SPMV_T);
+    return SFLSQR_OK;
+  }
+  std::string e;
+  if (h->tkind == T_ROWSHARD) {
+    // all-gather w_{k+1} (wsend, m_max per rank, zero padded) -> wfull; local rows of T
+    if (h->comm->allgather(P.wsend, h->wfull, h->m_max, h->stream, e))
+      return fail(h, SFLSQR_E_CUDA, "allgather(w): %s", e.c_str());
+    enqueue_apply(h, 1, P.st, h->wfull, 0, 0, P.z, SFLSQR_KC_SPMV_T);
+    return SFLSQR_OK;
+  }
+  // COLSHARD: partial n-vector (padded layout) from the local w slice, reduce-scattered
+  enqueue_apply(h, 1, P.st, P.W, ld, 0, h->zpart, SFLSQR_KC_SPMV_T);
+  if (h->comm->reduce_scatter(h->zpart, P.z, h->n_max, h->stream, e))
+    return fail(h, SFLSQR_E_CUDA, "reduce_scatter(z): %s", e.c_str());
+  return SFLSQR_OK;
+}
+
+// One iteration k of Alg. 1 / Alg. 2 (SURVEY.md §8(a) rows a1-a10).
+int enqueue_iteration(sflsqr_t* h) {
   Params& P = h->P;
   const int k = h->host_k;  // used only for the byte model
-  const double n8 = 8.0 * h->n, m8 = 8.0 * h->m;
+  const double n8 = 8.0 * h->n_loc, m8 = 8.0 * h->m_loc;
+  int rc;
   // a1: z-side windowed MGS (ell + 1 passes; passes beyond the window exit early)
   for (int pass = 0; pass <= P.ell; ++pass) {
     const int J = std::min(P.ell, k - 1);
     const double by = pass > J ? 0.0 : n8 * (1 + (pass > 0) * 2 + (pass < J));
-    Launch L(h, SFLSQR_KC_ORTH, by);
-    k_mgs_pass<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P, 0, pass);
+    {
+      Launch L(h, SFLSQR_KC_ORTH, by);
+      k_mgs_pass<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P, 0, pass);
+    }
+    if (pass == 0 && (rc = reduce_slots(h, P.slot_zin, 1, false))) return rc;
+    if ((rc = reduce_slots(h, P.slot_z0 + pass, 1, false))) return rc;
   }
   // a1 end + a2: normalise, tau, store z_k
   {
     Launch L(h, SFLSQR_KC_TAU, n8 * (2 + (P.use_pring ? 1 : 0) + (P.precond ? 1 : 0)));
     k_finish_z<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P);
   }
-  // a3: w = A z_k  (z_k = Z[:, k-1])
-  enqueue_apply(h, 0, P.st, P.Z, h->n, -1, P.w, SFLSQR_KC_SPMV_A);
+  // a3: w = A z_k  (z_k = Z[:, k-1]; all-gathered across ranks when sharded)
+  if (h->world == 1) {
+    enqueue_apply(h, 0, P.st, P.Z, h->n_loc, -1, P.w, SFLSQR_KC_SPMV_A);
+  } else {
+    std::string e;
+    if (h->comm->allgather(P.zsend, h->zfull, h->n_max, h->stream, e))
+      return fail(h, SFLSQR_E_CUDA, "allgather(z): %s", e.c_str());
+    enqueue_apply(h, 0, P.st, h->zfull, 0, 0, P.w, SFLSQR_KC_SPMV_A);
+  }
   // a4 (sFLSQR): S_AZ[:, k] = S w
-  if (P.method == SFLSQR_METHOD_SFLSQR) enqueue_sketch(h, P.st, P.w, 0, 0, 0, P.Mcols, P.d, -1, nullptr);
+  if (P.method == SFLSQR_METHOD_SFLSQR && (rc = enqueue_sketch(h, P.st, P.w))) return rc;
   // a5: w-side windowed MGS (ell + 2 passes) and normalisation
   for (int pass = 0; pass <= P.ell + 1; ++pass) {
     const int J = std::min(P.ell + 1, k);
     const double by = pass > J ? 0.0 : m8 * (1 + (pass > 0) * 2 + (pass < J));
-    Launch L(h, SFLSQR_KC_ORTH, by);
-    k_mgs_pass<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P, 1, pass);
+    {
+      Launch L(h, SFLSQR_KC_ORTH, by);
+      k_mgs_pass<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P, 1, pass);
+    }
+    if (pass == 0 && (rc = reduce_slots(h, P.slot_win, 1, false))) return rc;
+    if ((rc = reduce_slots(h, P.slot_w0 + pass, 1, false))) return rc;
   }
   {
     Launch L(h, SFLSQR_KC_ORTH, 2 * m8);
     k_finish_w<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P);
   }
   // a6: z = T w_{k+1}  (w_{k+1} = W[:, k])
-  enqueue_apply(h, 1, P.st, P.W, h->m, 0, P.z, SFLSQR_KC_SPMV_T);
+  if ((rc = enqueue_transpose_product(h, false))) return rc;
   // a4 (sFLSMR): S z -> S_TW[:, k+1]
-  if (P.method == SFLSQR_METHOD_SFLSMR) enqueue_sketch(h, P.st, P.z, 0, 0, 0, P.STW, P.d, 0, nullptr);
-  // a7: projected sketched LS
+  if (P.method == SFLSQR_METHOD_SFLSMR && (rc = enqueue_sketch(h, P.st, P.z))) return rc;
+  // a7: projected sketched LS (replicated on every rank: identical inputs)
   {
     Launch L(h, SFLSQR_KC_LS, 8.0 * P.d * (k + 2));
     k_ls<<<1, kLsThreads, 0, h->stream>>>(P);
   }
   // a8: x_k = Z_k y_k (needed by tau_{k+1})
   if (P.need_x) {
-    Launch L(h, SFLSQR_KC_XUPD, n8 * (k + 1));
-    k_xupdate<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P, 0);
+    {
+      Launch L(h, SFLSQR_KC_XUPD, n8 * (k + 1));
+      k_xupdate<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P, 0);
+    }
+    if ((rc = reduce_slots(h, P.slot_xmax, 1, true))) return rc;
   }
   // a9: true residual (W path) and stop tests
   if (P.want_res) {
-    Launch L(h, SFLSQR_KC_RES, m8 * (k + 1));
-    k_res_partial<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P);
+    {
+      Launch L(h, SFLSQR_KC_RES, m8 * (k + 1));
+      k_res_partial<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P);
+    }
+    if ((rc = reduce_slots(h, P.slot_res, 1, false))) return rc;
   }
   {
     Launch L(h, SFLSQR_KC_STOP, 0.0);
     k_stop<<<1, kVecThreads, 0, h->stream>>>(P);
   }
+  return SFLSQR_OK;
 }
 
 int check_launch(sflsqr_t* h) {
@@ -416,57 +501,64 @@ int check_launch(sflsqr_t* h) {
   return SFLSQR_OK;
 }
 
-// Generate the sparse-sign table with the device hash (k_sketch_table) and store S
-// transposed as a d x dim CSR: entries of sketch row r are the coordinates i with a
-// nonzero in row r, increasing i, sign in bit 31 (stable counting sort on the host).
+// Generate the sparse-sign table of this rank's coordinates with the device hash
+// (k_sketch_table, global coordinate indices) and store S transposed as a d x dim_loc
+// CSR: entries of sketch row r are the local coordinates with a nonzero in row r,
+// increasing, sign in bit 31 (stable counting sort on the host).
 int build_sketch(sflsqr_t* h) {
   Params& P = h->P;
-  const int64_t dim = P.method == SFLSQR_METHOD_SFLSQR ? h->m : h->n;
+  const bool q = P.method == SFLSQR_METHOD_SFLSQR;
+  const int64_t dim = q ? h->m_loc : h->n_loc, col0 = q ? h->m0 : h->n0;
   const int s = h->s_nz, d = h->d;
   const int64_t ne = dim * s;
   int* drows = nullptr;
   int8_t* dsig = nullptr;
   int rc;
-  if ((rc = dalloc(h, (void**)&drows, sizeof(int) * ne, nullptr))) return rc;
-  if ((rc = dalloc(h, (void**)&dsig, ne, nullptr))) {
+  if ((rc = dalloc(h, (void**)&drows, sizeof(int) * std::max<int64_t>(ne, 1), nullptr))) return rc;
+  if ((rc = dalloc(h, (void**)&dsig, std::max<int64_t>(ne, 1), nullptr))) {
     cudaFree(drows);
     return rc;
   }
-  const int grid = (int)std::min<int64_t>((dim * h->G + 255) / 256 + 1, 148 * 16);
-  k_sketch_table<<<grid, 256, 0, h->stream>>>(0, dim, d, s, h->G, P.seed_lo, P.seed_hi, drows, dsig);
+  if (dim > 0) {
+    const int grid = (int)std::min<int64_t>((dim * h->G + 255) / 256 + 1, 148 * 16);
+    k_sketch_table<<<grid, 256, 0, h->stream>>>(col0, dim, d, s, h->G, P.seed_lo, P.seed_hi, drows, dsig);
+  }
   std::vector<int> rows(ne);
   std::vector<int8_t> sig(ne);
-  cudaMemcpyAsync(rows.data(), drows, sizeof(int) * ne, cudaMemcpyDeviceToHost, h->stream);
-  cudaMemcpyAsync(sig.data(), dsig, ne, cudaMemcpyDeviceToHost, h->stream);
+  if (ne) {
+    cudaMemcpyAsync(rows.data(), drows, sizeof(int) * ne, cudaMemcpyDeviceToHost, h->stream);
+    cudaMemcpyAsync(sig.data(), dsig, ne, cudaMemcpyDeviceToHost, h->stream);
+  }
   cudaError_t e = cudaStreamSynchronize(h->stream);
   cudaFree(drows);
   cudaFree(dsig);
   if (e != cudaSuccess) return fail(h, SFLSQR_E_CUDA, "sketch table: %s", cudaGetErrorString(e));
   std::vector<int64_t> rp(d + 1, 0);
-  for (int64_t q = 0; q < ne; ++q) rp[rows[q] + 1]++;
+  for (int64_t t = 0; t < ne; ++t) rp[rows[t] + 1]++;
   for (int r = 0; r < d; ++r) rp[r + 1] += rp[r];
   std::vector<int64_t> next(rp.begin(), rp.end() - 1);
   std::vector<uint32_t> ent(ne);
   for (int64_t i = 0; i < dim; ++i)
     for (int t = 0; t < s; ++t) {
-      const int64_t q = i * s + t;
-      ent[next[rows[q]]++] = (uint32_t)i | (sig[q] < 0 ? 0x80000000u : 0u);
+      const int64_t qq = i * s + t;
+      ent[next[rows[qq]]++] = (uint32_t)i | (sig[qq] < 0 ? 0x80000000u : 0u);
     }
   if ((rc = dalloc(h, (void**)&P.sk_rp, sizeof(int64_t) * (d + 1), &h->solve_allocs, &h->solve_sizes))) return rc;
   if ((rc = dalloc(h, (void**)&P.sk_ent, sizeof(uint32_t) * std::max<int64_t>(ne, 1), &h->solve_allocs,
                    &h->solve_sizes)))
     return rc;
   CU(h, cudaMemcpy(P.sk_rp, rp.data(), sizeof(int64_t) * (d + 1), cudaMemcpyHostToDevice));
-  CU(h, cudaMemcpy(P.sk_ent, ent.data(), sizeof(uint32_t) * ne, cudaMemcpyHostToDevice));
+  if (ne) CU(h, cudaMemcpy(P.sk_ent, ent.data(), sizeof(uint32_t) * ne, cudaMemcpyHostToDevice));
   return SFLSQR_OK;
 }
 
 int alloc_solve(sflsqr_t* h) {
   free_solve(h);
   Params& P = h->P;
+  std::memset(&P, 0, sizeof(P));
   const int maxit = h->o.maxit, d = h->d, ell = h->o.window;
-  P.m = h->m;
-  P.n = h->n;
+  P.m = h->m_loc;
+  P.n = h->n_loc;
   P.ell = ell;
   P.maxit = maxit;
   P.ldh = maxit + 1;
@@ -475,6 +567,7 @@ int alloc_solve(sflsqr_t* h) {
   P.precond = h->pkind;
   P.d = d;
   P.s_nz = h->s_nz;
+  P.dist = h->world > 1 ? 1 : 0;
   P.want_res = ((h->o.history & SFLSQR_HIST_TRUE_RES) || h->o.eta > 0.0) ? 1 : 0;
   P.need_x = h->pkind != SFLSQR_PRECOND_IDENTITY ? 1 : 0;
   P.use_pring = (h->o.orth_mode == SFLSQR_ORTH_P && h->pkind != SFLSQR_PRECOND_IDENTITY) ? 1 : 0;
@@ -502,18 +595,28 @@ int alloc_solve(sflsqr_t* h) {
     return dalloc(h, (void**)p, count * sizeof(double), &h->solve_allocs, &h->solve_sizes);
   };
   int rc;
-  const size_t n = (size_t)h->n, m = (size_t)h->m;
+  const size_t n = (size_t)h->n_loc, m = (size_t)h->m_loc;
+  // z receives the reduce-scatter (n_max) when sharded by columns
+  const size_t zlen = std::max<size_t>(n, (size_t)h->n_max);
   if ((rc = dalloc(h, (void**)&P.st, sizeof(DevState), &h->solve_allocs, &h->solve_sizes))) return rc;
-  if ((rc = A(&P.z, n)) || (rc = A(&P.x, n)) || (rc = A(&P.Z, n * maxit)) || (rc = A(&P.w, m)) ||
+  if ((rc = A(&P.z, zlen)) || (rc = A(&P.x, n)) || (rc = A(&P.Z, n * maxit)) || (rc = A(&P.w, m)) ||
       (rc = A(&P.W, m * (maxit + 1))) || (rc = A(&P.b, m)) || (rc = A(&P.H, (size_t)(maxit + 1) * maxit)) ||
       (rc = A(&P.Tm, (size_t)maxit * maxit)) || (rc = A(&P.part, (size_t)s * kVecBlocks)) ||
-      (rc = A(&P.rhs, d)) || (rc = A(&P.Mcols, (size_t)d * maxit)) ||
-      (rc = A(&P.STW, (size_t)d * (maxit + 1))) || (rc = A(&P.V, (size_t)d * maxit)) || (rc = A(&P.taus, maxit)) ||
-      (rc = A(&P.R, (size_t)maxit * maxit)) || (rc = A(&P.qtb, d)) || (rc = A(&P.y, maxit)) ||
-      (rc = A(&P.g, maxit + 1)) || (rc = A(&P.hist_true, maxit)) || (rc = A(&P.hist_sk, maxit)))
+      (rc = A(&P.scal, (size_t)s)) || (rc = A(&P.skbuf, d)) || (rc = A(&P.rhs, d)) ||
+      (rc = A(&P.Mcols, (size_t)d * maxit)) || (rc = A(&P.STW, (size_t)d * (maxit + 1))) ||
+      (rc = A(&P.V, (size_t)d * maxit)) || (rc = A(&P.taus, maxit)) || (rc = A(&P.R, (size_t)maxit * maxit)) ||
+      (rc = A(&P.qtb, d)) || (rc = A(&P.y, maxit)) || (rc = A(&P.g, maxit + 1)) || (rc = A(&P.hist_true, maxit)) ||
+      (rc = A(&P.hist_sk, maxit)))
     return rc;
-  P.Pring = nullptr;
   if (P.use_pring && (rc = A(&P.Pring, n * ell))) return rc;
+  if (h->world > 1) {
+    if ((rc = A(&P.zsend, h->n_max)) || (rc = A(&h->zfull, (size_t)h->world * h->n_max))) return rc;
+    if (h->tkind == T_ROWSHARD) {
+      if ((rc = A(&P.wsend, h->m_max)) || (rc = A(&h->wfull, (size_t)h->world * h->m_max))) return rc;
+    } else {
+      if ((rc = A(&h->zpart, (size_t)h->world * h->n_max))) return rc;
+    }
+  }
   // Debug aid (no sanitizer on this pool): SFLSQR_DEBUG_POISON=1 fills every solve
   // buffer with NaN bytes so a read-before-write shows up as NaN in the results.
   const char* poison = std::getenv("SFLSQR_DEBUG_POISON");
@@ -521,6 +624,9 @@ int alloc_solve(sflsqr_t* h) {
     for (size_t i = 0; i < h->solve_allocs.size(); ++i)
       if (h->solve_allocs[i] != (void*)P.st) CU(h, cudaMemset(h->solve_allocs[i], 0xFF, h->solve_sizes[i]));
   }
+  // the padded send buffers' tails are never written
+  if (P.zsend) CU(h, cudaMemset(P.zsend, 0, sizeof(double) * h->n_max));
+  if (P.wsend) CU(h, cudaMemset(P.wsend, 0, sizeof(double) * h->m_max));
   if ((rc = build_sketch(h))) return rc;
   h->bufs = true;
   return SFLSQR_OK;
@@ -538,9 +644,10 @@ int zero_solve_state(sflsqr_t* h) {
   CU(h, cudaMemsetAsync(P.Mcols, 0, sizeof(double) * (size_t)d * maxit, s));
   CU(h, cudaMemsetAsync(P.STW, 0, sizeof(double) * (size_t)d * (maxit + 1), s));
   CU(h, cudaMemsetAsync(P.y, 0, sizeof(double) * maxit, s));
-  CU(h, cudaMemsetAsync(P.x, 0, sizeof(double) * h->n, s));
+  CU(h, cudaMemsetAsync(P.x, 0, sizeof(double) * std::max<int64_t>(h->n_loc, 1), s));
   CU(h, cudaMemsetAsync(P.hist_sk, 0, sizeof(double) * maxit, s));
   CU(h, cudaMemsetAsync(P.part, 0, sizeof(double) * (size_t)h->nslots * kVecBlocks, s));
+  CU(h, cudaMemsetAsync(P.scal, 0, sizeof(double) * (size_t)h->nslots, s));
   return SFLSQR_OK;
 }
 
@@ -555,9 +662,10 @@ int build_graph(sflsqr_t* h) {
   cudaGraph_t g;
   CU(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
   h->host_k = 1;
-  enqueue_iteration(h);
+  int rc = enqueue_iteration(h);
   cudaError_t e = cudaStreamEndCapture(h->stream, &g);
   h->prof_on = prof;
+  if (rc) return rc;
   if (e != cudaSuccess) return fail(h, SFLSQR_E_CUDA, "graph capture: %s", cudaGetErrorString(e));
   h->kernels_per_iter = (int)(h->launches - before);
   h->launches = before;
@@ -575,6 +683,33 @@ int ensure_ready(sflsqr_t* h, bool need_rhs) {
   return SFLSQR_OK;
 }
 
+int upload(sflsqr_t* h, void** dst, const void* src, size_t bytes, cudaMemcpyKind kind) {
+  int rc;
+  if ((rc = dalloc(h, dst, bytes, nullptr))) return rc;
+  if (bytes) CU(h, cudaMemcpy(*dst, src, bytes, kind));
+  return SFLSQR_OK;
+}
+
+// Upload a host CSR block whose rowptr has base rp[0] (rebased to 0 on the device).
+int upload_csr(sflsqr_t* h, int64_t nrows, const int64_t* rp, const int32_t* col, const double* val, int64_t** drp,
+               int32_t** dcol, double** dval, int64_t* nnz_out) {
+  const int64_t base = rp[0], nnz = rp[nrows] - base;
+  std::vector<int64_t> r0;
+  const int64_t* rpu = rp;
+  if (base != 0) {
+    r0.resize(nrows + 1);
+    for (int64_t i = 0; i <= nrows; ++i) r0[i] = rp[i] - base;
+    rpu = r0.data();
+  }
+  int rc;
+  if ((rc = upload(h, (void**)drp, rpu, sizeof(int64_t) * (nrows + 1), cudaMemcpyHostToDevice)) ||
+      (rc = upload(h, (void**)dcol, col + base, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice)) ||
+      (rc = upload(h, (void**)dval, val + base, sizeof(double) * nnz, cudaMemcpyHostToDevice)))
+    return rc;
+  *nnz_out = nnz;
+  return SFLSQR_OK;
+}
+
 }  // namespace
 
 // ====================================================================== C ABI
@@ -583,6 +718,29 @@ extern "C" {
 int sflsqr_version(void) { return SFLSQR_ABI_VERSION; }
 
 const char* sflsqr_last_error(sflsqr_t* h) { return h ? h->err.c_str() : g_err.c_str(); }
+
+int sflsqr_get_unique_id(uint8_t id[128]) {
+  if (!id) return fail(nullptr, SFLSQR_E_INVALID, "NULL id");
+  std::string e;
+  if (nccl_get_unique_id(id, e)) return fail(nullptr, SFLSQR_E_UNSUPPORTED, "%s", e.c_str());
+  return SFLSQR_OK;
+}
+
+int sflsqr_local_group_create(void** group, int32_t world, int32_t device) {
+  if (!group) return fail(nullptr, SFLSQR_E_INVALID, "NULL group");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(nullptr, SFLSQR_E_CUDA, "no CUDA device");
+  }
+  std::string e;
+  LocalGroup* g = local_group_create(world, device, e);
+  if (!g) return fail(nullptr, SFLSQR_E_INVALID, "%s", e.c_str());
+  *group = g;
+  return SFLSQR_OK;
+}
+
+void sflsqr_local_group_destroy(void* group) { local_group_release(static_cast<LocalGroup*>(group)); }
 
 int sflsqr_create(sflsqr_t** out, const sflsqr_opts* o) {
   if (!out || !o) return fail(nullptr, SFLSQR_E_INVALID, "NULL argument");
@@ -599,8 +757,13 @@ int sflsqr_create(sflsqr_t** out, const sflsqr_opts* o) {
     return fail(nullptr, SFLSQR_E_INVALID, "eta must be 0 (off) or > 1");
   if (!(o->delta_e >= 0.0) || !std::isfinite(o->delta_e))
     return fail(nullptr, SFLSQR_E_INVALID, "delta_e must be >= 0");
-  if (o->world != 1 || o->rank != 0)
-    return fail(nullptr, SFLSQR_E_UNSUPPORTED, "this build runs one rank per solve (world = 1)");
+  if (o->world < 1 || o->rank < 0 || o->rank >= o->world) return fail(nullptr, SFLSQR_E_INVALID, "bad rank/world");
+  if (o->world > 1 && o->comm_kind != SFLSQR_COMM_NCCL && o->comm_kind != SFLSQR_COMM_LOCAL)
+    return fail(nullptr, SFLSQR_E_INVALID, "bad comm_kind");
+  if (o->world > 1 && o->comm_kind == SFLSQR_COMM_NCCL && !o->nccl_id)
+    return fail(nullptr, SFLSQR_E_INVALID, "world > 1 with NCCL needs opts.nccl_id");
+  if (o->world > 1 && o->comm_kind == SFLSQR_COMM_LOCAL && !o->local_group)
+    return fail(nullptr, SFLSQR_E_INVALID, "world > 1 with LOCAL needs opts.local_group");
   int ndev = 0;
   cudaError_t e = cudaGetDeviceCount(&ndev);
   if (e != cudaSuccess || ndev == 0) {
@@ -611,7 +774,10 @@ int sflsqr_create(sflsqr_t** out, const sflsqr_opts* o) {
   if (cudaSetDevice(o->device) != cudaSuccess) return fail(nullptr, SFLSQR_E_CUDA, "cudaSetDevice failed");
   sflsqr_t* h = new sflsqr_t();
   h->o = *o;
+  h->rank = o->rank;
+  h->world = o->world;
   if (o->window > o->maxit) h->o.window = o->maxit;  // full orthogonalisation
+  if (o->world > 1) h->o.use_graph = 0;             // collectives are issued eagerly
   if (o->stream && (cudaStream_t)o->stream != cudaStreamLegacy && (cudaStream_t)o->stream != cudaStreamPerThread) {
     h->stream = (cudaStream_t)o->stream;
   } else {
@@ -621,11 +787,142 @@ int sflsqr_create(sflsqr_t** out, const sflsqr_opts* o) {
     }
     h->own_stream = true;
   }
-  if (const char* e = std::getenv("SFLSQR_SPMV_MODE")) h->spmv_mode = std::atoi(e);
-  if (const char* e = std::getenv("SFLSQR_BAND_SHIFT")) h->band_shift = std::atoi(e);
-
-
+  if (o->world > 1) {
+    std::string ce;
+    if (o->comm_kind == SFLSQR_COMM_NCCL)
+      h->comm = nccl_comm_create(o->nccl_id, o->rank, o->world, o->device, ce);
+    else
+      h->comm = local_comm_create(static_cast<LocalGroup*>(o->local_group), o->rank);
+    if (!h->comm) {
+      if (h->own_stream) cudaStreamDestroy(h->stream);
+      delete h;
+      return fail(nullptr, SFLSQR_E_UNSUPPORTED, "communicator: %s", ce.c_str());
+    }
+  }
+  if (const char* ev = std::getenv("SFLSQR_SPMV_MODE")) h->spmv_mode = std::atoi(ev);
   *out = h;
+  return SFLSQR_OK;
+}
+
+int sflsqr_set_operator_shard(sflsqr_t* h, int64_t m, int64_t n, int64_t a_row0, int64_t a_row1,
+                              const int64_t* a_rowptr, const int32_t* a_col, const double* a_val, int32_t t_mode,
+                              int64_t t_row0, int64_t t_row1, const int64_t* t_rowptr, const int32_t* t_col,
+                              const double* t_val) {
+  if (!h) return fail(nullptr, SFLSQR_E_INVALID, "NULL handle");
+  if (m < 1 || n < 1 || m > INT32_MAX || n > INT32_MAX)
+    return fail(h, SFLSQR_E_DIM, "bad shape %lld x %lld", (long long)m, (long long)n);
+  if (t_mode != SFLSQR_T_BUILD && t_mode != SFLSQR_T_GIVEN) return fail(h, SFLSQR_E_INVALID, "bad t_mode");
+  if (!a_rowptr || a_row0 < 0 || a_row1 < a_row0 || a_row1 > m) return fail(h, SFLSQR_E_DIM, "bad A row block");
+  if (t_mode == SFLSQR_T_GIVEN && (!t_rowptr || t_row0 < 0 || t_row1 < t_row0 || t_row1 > n))
+    return fail(h, SFLSQR_E_DIM, "bad T row block");
+  cudaSetDevice(h->o.device);
+  free_solve(h);
+  free_op(h);
+  const int R = h->world;
+  // ---- partition exchange (every rank learns every rank's blocks)
+  int64_t mine[4] = {a_row0, a_row1, t_mode == SFLSQR_T_GIVEN ? t_row0 : 0, t_mode == SFLSQR_T_GIVEN ? t_row1 : 0};
+  std::vector<int64_t> all(4 * R);
+  if (R > 1) {
+    std::string e;
+    if (h->comm->allgather_host(mine, all.data(), sizeof(mine), e))
+      return fail(h, SFLSQR_E_CUDA, "partition exchange: %s", e.c_str());
+  } else {
+    std::memcpy(all.data(), mine, sizeof(mine));
+  }
+  std::vector<int64_t> mst(R + 1), nst(R + 1);
+  for (int g = 0; g < R; ++g) {
+    if (all[4 * g] != (g == 0 ? 0 : all[4 * (g - 1) + 1]) || all[4 * g + 1] < all[4 * g])
+      return fail(h, SFLSQR_E_DIM, "A row blocks must tile [0, m) in rank order");
+    mst[g] = all[4 * g];
+  }
+  mst[R] = all[4 * (R - 1) + 1];
+  if (mst[R] != m) return fail(h, SFLSQR_E_DIM, "A row blocks must tile [0, m) in rank order");
+  if (t_mode == SFLSQR_T_GIVEN) {
+    for (int g = 0; g < R; ++g) {
+      if (all[4 * g + 2] != (g == 0 ? 0 : all[4 * (g - 1) + 3]) || all[4 * g + 3] < all[4 * g + 2])
+        return fail(h, SFLSQR_E_DIM, "T row blocks must tile [0, n) in rank order");
+      nst[g] = all[4 * g + 2];
+    }
+    nst[R] = all[4 * (R - 1) + 3];
+    if (nst[R] != n) return fail(h, SFLSQR_E_DIM, "T row blocks must tile [0, n) in rank order");
+  } else {
+    const int64_t per = (n + R - 1) / R;
+    for (int g = 0; g <= R; ++g) nst[g] = std::min<int64_t>(n, (int64_t)g * per);
+  }
+  h->m = m;
+  h->n = n;
+  h->m0 = mst[h->rank];
+  h->m_loc = mst[h->rank + 1] - mst[h->rank];
+  h->n0 = nst[h->rank];
+  h->n_loc = nst[h->rank + 1] - nst[h->rank];
+  h->m_max = h->n_max = 0;
+  for (int g = 0; g < R; ++g) {
+    h->m_max = std::max(h->m_max, mst[g + 1] - mst[g]);
+    h->n_max = std::max(h->n_max, nst[g + 1] - nst[g]);
+  }
+  h->tkind = R == 1 ? T_FULL : (t_mode == SFLSQR_T_GIVEN ? T_ROWSHARD : T_COLSHARD);
+  int rc;
+  if ((rc = validate_csr(h, "A", h->m_loc, n, a_rowptr, a_col, a_val))) return rc;
+  if (t_mode == SFLSQR_T_GIVEN && (rc = validate_csr(h, "T", h->n_loc, m, t_rowptr, t_col, t_val))) return rc;
+  // ---- padded index maps (sharded): global index -> owner * max + local offset
+  auto pad_map = [&](const std::vector<int64_t>& st, int64_t mx, int64_t len) {
+    std::vector<int64_t> mp(len);
+    for (int g = 0; g < R; ++g)
+      for (int64_t j = st[g]; j < st[g + 1]; ++j) mp[j] = (int64_t)g * mx + (j - st[g]);
+    return mp;
+  };
+  const int64_t abase = a_rowptr[0], annz = a_rowptr[h->m_loc] - abase;
+  std::vector<int32_t> acol_re;
+  const int32_t* acol_up = a_col;
+  if (R > 1) {
+    const std::vector<int64_t> nmap = pad_map(nst, h->n_max, n);
+    acol_re.resize(annz);
+    par_for(annz, [&](int64_t s, int64_t e) {
+      for (int64_t p = s; p < e; ++p) acol_re[p] = (int32_t)nmap[a_col[abase + p]];
+    });
+    acol_up = acol_re.data() - abase;
+  }
+  if ((rc = upload_csr(h, h->m_loc, a_rowptr, acol_up, a_val, &h->a_rowptr, &h->a_col, &h->a_val, &h->nnz_a))) {
+    free_op(h);
+    return rc;
+  }
+  h->a_owned = h->t_owned = true;
+  if (t_mode == SFLSQR_T_GIVEN) {
+    const int64_t tbase = t_rowptr[0], tnnz = t_rowptr[h->n_loc] - tbase;
+    std::vector<int32_t> tcol_re;
+    const int32_t* tcol_up = t_col;
+    if (R > 1) {
+      const std::vector<int64_t> mmap = pad_map(mst, h->m_max, m);
+      tcol_re.resize(tnnz);
+      par_for(tnnz, [&](int64_t s, int64_t e) {
+        for (int64_t p = s; p < e; ++p) tcol_re[p] = (int32_t)mmap[t_col[tbase + p]];
+      });
+      tcol_up = tcol_re.data() - tbase;
+    }
+    h->t_rows = h->n_loc;
+    rc = upload_csr(h, h->n_loc, t_rowptr, tcol_up, t_val, &h->t_rowptr, &h->t_col, &h->t_val, &h->nnz_t);
+  } else {
+    // T = A^T of this rank's row block (COLSHARD when sharded: rows in the padded n layout)
+    std::vector<int64_t> trp;
+    std::vector<int32_t> tcol;
+    std::vector<double> tval;
+    std::vector<int64_t> nmap;
+    if (R > 1) {
+      nmap = pad_map(nst, h->n_max, n);
+      h->t_rows = (int64_t)R * h->n_max;
+      host_transpose(h->m_loc, n, a_rowptr, a_col, a_val, h->t_rows, &nmap, trp, tcol, tval);
+    } else {
+      h->t_rows = n;
+      host_transpose(h->m_loc, n, a_rowptr, a_col, a_val, n, nullptr, trp, tcol, tval);
+    }
+    rc = upload_csr(h, h->t_rows, trp.data(), tcol.data(), tval.data(), &h->t_rowptr, &h->t_col, &h->t_val,
+                    &h->nnz_t);
+  }
+  if (rc) {
+    free_op(h);
+    return rc;
+  }
+  h->op_set = true;
   return SFLSQR_OK;
 }
 
@@ -633,42 +930,39 @@ int sflsqr_set_operator(sflsqr_t* h, int64_t m, int64_t n, const int64_t* a_rowp
                         const double* a_val, int32_t t_mode, const int64_t* t_rowptr, const int32_t* t_col,
                         const double* t_val, int32_t mem_flags) {
   if (!h) return fail(nullptr, SFLSQR_E_INVALID, "NULL handle");
-  if (m < 1 || n < 1 || m > INT32_MAX || n > INT32_MAX) return fail(h, SFLSQR_E_DIM, "bad shape %lld x %lld",
-                                                                    (long long)m, (long long)n);
+  if (h->world > 1) return fail(h, SFLSQR_E_STATE, "world > 1: use sflsqr_set_operator_shard");
+  if (m < 1 || n < 1 || m > INT32_MAX || n > INT32_MAX)
+    return fail(h, SFLSQR_E_DIM, "bad shape %lld x %lld", (long long)m, (long long)n);
   if (t_mode != SFLSQR_T_BUILD && t_mode != SFLSQR_T_GIVEN) return fail(h, SFLSQR_E_INVALID, "bad t_mode");
   const bool dev = (mem_flags & SFLSQR_MEM_DEVICE) != 0;
   const bool borrow = (mem_flags & SFLSQR_MEM_BORROW) != 0;
   if (borrow && !dev) return fail(h, SFLSQR_E_INVALID, "BORROW requires device pointers");
   if (dev && t_mode == SFLSQR_T_BUILD) return fail(h, SFLSQR_E_INVALID, "T_BUILD requires host arrays");
+  if (!dev) {
+    if (!a_rowptr || !a_col || !a_val) return fail(h, SFLSQR_E_INVALID, "A: NULL array");
+    if (a_rowptr[0] != 0) return fail(h, SFLSQR_E_DIM, "A: rowptr[0] != 0");
+    if (t_mode == SFLSQR_T_GIVEN) {
+      if (!t_rowptr || !t_col || !t_val) return fail(h, SFLSQR_E_INVALID, "T: NULL array");
+      if (t_rowptr[0] != 0) return fail(h, SFLSQR_E_DIM, "T: rowptr[0] != 0");
+    }
+    return sflsqr_set_operator_shard(h, m, n, 0, m, a_rowptr, a_col, a_val, t_mode, 0, n, t_rowptr, t_col, t_val);
+  }
+  // device arrays (copied or borrowed; not validated)
+  if (!a_rowptr || !a_col || !a_val || !t_rowptr || !t_col || !t_val)
+    return fail(h, SFLSQR_E_INVALID, "NULL device array");
   cudaSetDevice(h->o.device);
   free_solve(h);
   free_op(h);
-  int rc;
-  int64_t nnz_a, nnz_t = 0;
-  std::vector<int64_t> trp;
-  std::vector<int32_t> tcol;
-  std::vector<double> tval;
-  if (!dev) {
-    if ((rc = validate_csr(h, "A", m, n, a_rowptr, a_col, a_val))) return rc;
-    nnz_a = a_rowptr[m];
-    if (t_mode == SFLSQR_T_GIVEN) {
-      if ((rc = validate_csr(h, "T", n, m, t_rowptr, t_col, t_val))) return rc;
-      nnz_t = t_rowptr[n];
-    } else {
-      host_transpose(m, n, a_rowptr, a_col, a_val, trp, tcol, tval);
-      nnz_t = nnz_a;
-      t_rowptr = trp.data();
-      t_col = tcol.data();
-      t_val = tval.data();
-    }
-  } else {
-    if (!a_rowptr || !a_col || !a_val || !t_rowptr || !t_col || !t_val)
-      return fail(h, SFLSQR_E_INVALID, "NULL device array");
-    CU(h, cudaMemcpy(&nnz_a, a_rowptr + m, sizeof(int64_t), cudaMemcpyDeviceToHost));
-    CU(h, cudaMemcpy(&nnz_t, t_rowptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost));
-  }
+  int64_t nnz_a, nnz_t;
+  CU(h, cudaMemcpy(&nnz_a, a_rowptr + m, sizeof(int64_t), cudaMemcpyDeviceToHost));
+  CU(h, cudaMemcpy(&nnz_t, t_rowptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost));
   h->m = m;
   h->n = n;
+  h->m0 = h->n0 = 0;
+  h->m_loc = h->m_max = m;
+  h->n_loc = h->n_max = n;
+  h->t_rows = n;
+  h->tkind = T_FULL;
   h->nnz_a = nnz_a;
   h->nnz_t = nnz_t;
   if (borrow) {
@@ -681,22 +975,17 @@ int sflsqr_set_operator(sflsqr_t* h, int64_t m, int64_t n, const int64_t* a_rowp
     h->t_val = (double*)t_val;
   } else {
     h->a_owned = h->t_owned = true;
-    const cudaMemcpyKind kind = dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    if ((rc = dalloc(h, (void**)&h->a_rowptr, sizeof(int64_t) * (m + 1), nullptr)) ||
-        (rc = dalloc(h, (void**)&h->a_col, sizeof(int32_t) * nnz_a, nullptr)) ||
-        (rc = dalloc(h, (void**)&h->a_val, sizeof(double) * nnz_a, nullptr)) ||
-        (rc = dalloc(h, (void**)&h->t_rowptr, sizeof(int64_t) * (n + 1), nullptr)) ||
-        (rc = dalloc(h, (void**)&h->t_col, sizeof(int32_t) * nnz_t, nullptr)) ||
-        (rc = dalloc(h, (void**)&h->t_val, sizeof(double) * nnz_t, nullptr))) {
+    int rc;
+    const cudaMemcpyKind kd = cudaMemcpyDeviceToDevice;
+    if ((rc = upload(h, (void**)&h->a_rowptr, a_rowptr, sizeof(int64_t) * (m + 1), kd)) ||
+        (rc = upload(h, (void**)&h->a_col, a_col, sizeof(int32_t) * nnz_a, kd)) ||
+        (rc = upload(h, (void**)&h->a_val, a_val, sizeof(double) * nnz_a, kd)) ||
+        (rc = upload(h, (void**)&h->t_rowptr, t_rowptr, sizeof(int64_t) * (n + 1), kd)) ||
+        (rc = upload(h, (void**)&h->t_col, t_col, sizeof(int32_t) * nnz_t, kd)) ||
+        (rc = upload(h, (void**)&h->t_val, t_val, sizeof(double) * nnz_t, kd))) {
       free_op(h);
       return rc;
     }
-    CU(h, cudaMemcpy(h->a_rowptr, a_rowptr, sizeof(int64_t) * (m + 1), kind));
-    CU(h, cudaMemcpy(h->a_col, a_col, sizeof(int32_t) * nnz_a, kind));
-    CU(h, cudaMemcpy(h->a_val, a_val, sizeof(double) * nnz_a, kind));
-    CU(h, cudaMemcpy(h->t_rowptr, t_rowptr, sizeof(int64_t) * (n + 1), kind));
-    CU(h, cudaMemcpy(h->t_col, t_col, sizeof(int32_t) * nnz_t, kind));
-    CU(h, cudaMemcpy(h->t_val, t_val, sizeof(double) * nnz_t, kind));
   }
   h->op_set = true;
   return SFLSQR_OK;
@@ -704,6 +993,7 @@ int sflsqr_set_operator(sflsqr_t* h, int64_t m, int64_t n, const int64_t* a_rowp
 
 int sflsqr_set_operator_blur(sflsqr_t* h, int32_t H, int32_t W, double sigma, int32_t radius) {
   if (!h) return fail(nullptr, SFLSQR_E_INVALID, "NULL handle");
+  if (h->world > 1) return fail(h, SFLSQR_E_UNSUPPORTED, "the blur operator runs on one rank");
   if (H < 1 || W < 1) return fail(h, SFLSQR_E_DIM, "bad image shape");
   if (!(sigma > 0.0) || !std::isfinite(sigma) || radius < 0) return fail(h, SFLSQR_E_INVALID, "sigma > 0, radius >= 0");
   cudaSetDevice(h->o.device);
@@ -727,6 +1017,10 @@ int sflsqr_set_operator_blur(sflsqr_t* h, int32_t H, int32_t W, double sigma, in
   h->bW = W;
   h->brad = radius;
   h->m = h->n = nn;
+  h->m0 = h->n0 = 0;
+  h->m_loc = h->n_loc = h->m_max = h->n_max = nn;
+  h->t_rows = nn;
+  h->tkind = T_FULL;
   h->op_set = true;
   return SFLSQR_OK;
 }
@@ -764,56 +1058,60 @@ int sflsqr_set_precond(sflsqr_t* h, int32_t kind, double p, double eps_rel) {
 int sflsqr_set_rhs(sflsqr_t* h, const double* b, int64_t len, int32_t mem_flags) {
   int rc;
   if ((rc = ensure_ready(h, false))) return rc;
-  if (!b) return fail(h, SFLSQR_E_INVALID, "NULL b");
-  if (len != h->m) return fail(h, SFLSQR_E_DIM, "len(b) = %lld != m = %lld", (long long)len, (long long)h->m);
+  if (!b && len) return fail(h, SFLSQR_E_INVALID, "NULL b");
+  if (len != h->m_loc)
+    return fail(h, SFLSQR_E_DIM, "len(b) = %lld != local m = %lld", (long long)len, (long long)h->m_loc);
   cudaSetDevice(h->o.device);
   const bool dev = (mem_flags & SFLSQR_MEM_DEVICE) != 0;
+  int bad = 0;
   if (!dev) {
-    double nrm = 0.0;
-    for (int64_t i = 0; i < len; ++i) {
-      if (!std::isfinite(b[i])) return fail(h, SFLSQR_E_NONFINITE, "b has a non-finite entry");
-      nrm += b[i] * b[i];
-    }
-    if (nrm == 0.0) return fail(h, SFLSQR_E_ZERO_RHS, "||b|| = 0");
+    for (int64_t i = 0; i < len; ++i)
+      if (!std::isfinite(b[i])) bad = 1;
   }
+  if (h->world == 1 && bad) return fail(h, SFLSQR_E_NONFINITE, "b has a non-finite entry");
   if (!h->bufs && (rc = alloc_solve(h))) return rc;
   h->rhs_set = false;
   Params& P = h->P;
   if ((rc = zero_solve_state(h))) return rc;
-  CU(h, cudaMemcpyAsync(P.b, b, sizeof(double) * len, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                        h->stream));
+  if (len)
+    CU(h, cudaMemcpyAsync(P.b, b, sizeof(double) * len, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                          h->stream));
   // Alg. 1 L457 / Alg. 2: beta = ||b||, w_1 = b / beta
   {
-    Launch L(h, SFLSQR_KC_ORTH, 8.0 * h->m);
-    k_norm_partial<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P, P.b, h->m, P.slot_beta);
+    Launch L(h, SFLSQR_KC_ORTH, 8.0 * h->m_loc);
+    k_norm_partial<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P, P.b, h->m_loc, P.slot_beta);
+  }
+  if ((rc = reduce_slots(h, P.slot_beta, 1, false))) return rc;
+  {
+    // ||b|| = 0 / non-finite check before dividing (every rank takes the same decision)
+    double beta2 = 0.0;
+    if (h->world > 1) {
+      CU(h, cudaMemcpyAsync(&beta2, P.scal + P.slot_beta, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+      CU(h, cudaStreamSynchronize(h->stream));
+    } else {
+      std::vector<double> parts(kVecBlocks);
+      CU(h, cudaMemcpyAsync(parts.data(), P.part + (size_t)P.slot_beta * kVecBlocks, sizeof(double) * kVecBlocks,
+                            cudaMemcpyDeviceToHost, h->stream));
+      CU(h, cudaStreamSynchronize(h->stream));
+      for (double v : parts) beta2 += v;
+    }
+    if (!std::isfinite(beta2)) return fail(h, SFLSQR_E_NONFINITE, "b has a non-finite entry");
+    if (!(beta2 > 0.0)) return fail(h, SFLSQR_E_ZERO_RHS, "||b|| = 0");
   }
   {
-    Launch L(h, SFLSQR_KC_ORTH, 16.0 * h->m);
+    Launch L(h, SFLSQR_KC_ORTH, 16.0 * h->m_loc);
     k_init_w1<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P);
   }
   // L458 / L760: z = T w_1
-  enqueue_apply(h, 1, P.st, P.W, 0, 0, P.z, SFLSQR_KC_SPMV_T);
-  if (P.method == SFLSQR_METHOD_SFLSQR) {
-    // L459: s_b = S b
-    enqueue_sketch(h, P.st, P.b, 0, 0, 0, P.rhs, 0, 0, nullptr);
-  } else {
-    // L761-762: s = beta S z, S_TW = [S z]
-    enqueue_sketch(h, P.st, P.z, 0, 0, 1, P.rhs, 0, 0, P.STW);
-  }
+  if ((rc = enqueue_transpose_product(h, true))) return rc;
+  // L459: s_b = S b  |  L761-762: s = beta S z, S_TW = [S z]
+  if ((rc = enqueue_sketch(h, P.st, P.method == SFLSQR_METHOD_SFLSQR ? P.b : P.z))) return rc;
   {
     Launch L(h, SFLSQR_KC_LS, 16.0 * h->d);
-    k_init_ls<<<1, kVecThreads, 0, h->stream>>>(P);
+    k_init_rhs<<<1, kVecThreads, 0, h->stream>>>(P);
   }
   if ((rc = check_launch(h))) return rc;
-  if (!dev) {
-    // nothing else: host norm checked above
-  } else {
-    DevState st;
-    CU(h, cudaMemcpyAsync(&st, P.st, sizeof(st), cudaMemcpyDeviceToHost, h->stream));
-    CU(h, cudaStreamSynchronize(h->stream));
-    if (!(st.beta > 0.0)) return fail(h, SFLSQR_E_ZERO_RHS, "||b|| = 0");
-    if (!std::isfinite(st.beta)) return fail(h, SFLSQR_E_NONFINITE, "b has a non-finite entry");
-  }
+  CU(h, cudaStreamSynchronize(h->stream));
   h->host_k = 1;
   h->rhs_set = true;
   if (h->o.use_graph && !h->gexec) {
@@ -830,6 +1128,7 @@ int sflsqr_iterate(sflsqr_t* h, int32_t k, int32_t* done, int32_t* status) {
   DevState st;
   CU(h, cudaMemcpyAsync(&st, h->P.st, sizeof(st), cudaMemcpyDeviceToHost, h->stream));
   CU(h, cudaStreamSynchronize(h->stream));
+  // every rank holds the same replicated state, so `todo` agrees across ranks
   int todo = st.done ? 0 : std::min(k, h->o.maxit - (st.k - 1));
   h->host_k = st.k;
   for (int i = 0; i < todo; ++i) {
@@ -837,7 +1136,7 @@ int sflsqr_iterate(sflsqr_t* h, int32_t k, int32_t* done, int32_t* status) {
       CU(h, cudaGraphLaunch(h->gexec, h->stream));
       h->launches += h->kernels_per_iter;
     } else {
-      enqueue_iteration(h);
+      if ((rc = enqueue_iteration(h))) return rc;
     }
     h->host_k++;
   }
@@ -853,17 +1152,18 @@ int sflsqr_iterate(sflsqr_t* h, int32_t k, int32_t* done, int32_t* status) {
 int sflsqr_get_x(sflsqr_t* h, double* x, int64_t len, int32_t mem_flags) {
   int rc;
   if ((rc = ensure_ready(h, true))) return rc;
-  if (!x) return fail(h, SFLSQR_E_INVALID, "NULL x");
-  if (len != h->n) return fail(h, SFLSQR_E_DIM, "len(x) != n");
+  if (!x && len) return fail(h, SFLSQR_E_INVALID, "NULL x");
+  if (len != h->n_loc) return fail(h, SFLSQR_E_DIM, "len(x) != local n");
   cudaSetDevice(h->o.device);
   {
-    Launch L(h, SFLSQR_KC_XUPD, 8.0 * h->n);
+    Launch L(h, SFLSQR_KC_XUPD, 8.0 * h->n_loc);
     k_xupdate<<<kVecBlocks, kVecThreads, 0, h->stream>>>(h->P, 1);
   }
   if ((rc = check_launch(h))) return rc;
   const bool dev = (mem_flags & SFLSQR_MEM_DEVICE) != 0;
-  CU(h, cudaMemcpyAsync(x, h->P.x, sizeof(double) * len, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
-                        h->stream));
+  if (len)
+    CU(h, cudaMemcpyAsync(x, h->P.x, sizeof(double) * len, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                          h->stream));
   CU(h, cudaStreamSynchronize(h->stream));
   if (h->prof_on) prof_collect(h);
   return SFLSQR_OK;
@@ -898,6 +1198,10 @@ int sflsqr_get_info(sflsqr_t* h, sflsqr_info* info) {
   info->nnz_a = h->nnz_a;
   info->nnz_t = h->nnz_t;
   info->launches = h->launches;
+  info->m0 = h->m0;
+  info->m_loc = h->m_loc;
+  info->n0 = h->n0;
+  info->n_loc = h->n_loc;
   if (h->rhs_set) {
     cudaSetDevice(h->o.device);
     DevState st;
@@ -947,6 +1251,7 @@ int sflsqr_debug_sketch_table(sflsqr_t* h, int64_t col0, int64_t ncols, int32_t*
 int sflsqr_debug_apply(sflsqr_t* h, int32_t which, const double* x, double* y) {
   if (!h) return fail(nullptr, SFLSQR_E_INVALID, "NULL handle");
   if (!h->op_set) return fail(h, SFLSQR_E_STATE, "operator not set");
+  if (h->world > 1) return fail(h, SFLSQR_E_UNSUPPORTED, "debug_apply runs on one rank");
   if ((which != 0 && which != 1) || !x || !y) return fail(h, SFLSQR_E_INVALID, "bad arguments");
   cudaSetDevice(h->o.device);
   const int64_t nin = which == 0 ? h->n : h->m, nout = which == 0 ? h->m : h->n;
@@ -984,8 +1289,8 @@ int sflsqr_debug_basis(sflsqr_t* h, double* H, double* Tm, double* Z, double* W,
     if (Tm) CU(h, cudaMemcpy(Tm + (size_t)j * kd, h->P.Tm + (size_t)j * maxit, sizeof(double) * kd,
                              cudaMemcpyDeviceToHost));
   }
-  if (Z && kd) CU(h, cudaMemcpy(Z, h->P.Z, sizeof(double) * h->n * kd, cudaMemcpyDeviceToHost));
-  if (W) CU(h, cudaMemcpy(W, h->P.W, sizeof(double) * h->m * (kd + 1), cudaMemcpyDeviceToHost));
+  if (Z && kd && h->n_loc) CU(h, cudaMemcpy(Z, h->P.Z, sizeof(double) * h->n_loc * kd, cudaMemcpyDeviceToHost));
+  if (W && h->m_loc) CU(h, cudaMemcpy(W, h->P.W, sizeof(double) * h->m_loc * (kd + 1), cudaMemcpyDeviceToHost));
   if (y && st.k_x) CU(h, cudaMemcpy(y, h->P.y, sizeof(double) * st.k_x, cudaMemcpyDeviceToHost));
   return SFLSQR_OK;
 }
@@ -1001,18 +1306,18 @@ int sflsqr_debug_state(sflsqr_t* h, double* z, double* x, double* p_ring, double
   const Params& P = h->P;
   if (x) {
     {
-      Launch L(h, SFLSQR_KC_XUPD, 8.0 * h->n);
+      Launch L(h, SFLSQR_KC_XUPD, 8.0 * h->n_loc);
       k_xupdate<<<kVecBlocks, kVecThreads, 0, h->stream>>>(h->P, 1);
     }
     if ((rc = check_launch(h))) return rc;
-    CU(h, cudaMemcpyAsync(x, P.x, sizeof(double) * h->n, cudaMemcpyDeviceToHost, h->stream));
+    if (h->n_loc) CU(h, cudaMemcpyAsync(x, P.x, sizeof(double) * h->n_loc, cudaMemcpyDeviceToHost, h->stream));
   }
-  if (z) CU(h, cudaMemcpyAsync(z, P.z, sizeof(double) * h->n, cudaMemcpyDeviceToHost, h->stream));
+  if (z && h->n_loc) CU(h, cudaMemcpyAsync(z, P.z, sizeof(double) * h->n_loc, cudaMemcpyDeviceToHost, h->stream));
   if (p_ring) {
     if (P.use_pring)
-      CU(h, cudaMemcpyAsync(p_ring, P.Pring, sizeof(double) * h->n * P.ell, cudaMemcpyDeviceToHost, h->stream));
+      CU(h, cudaMemcpyAsync(p_ring, P.Pring, sizeof(double) * h->n_loc * P.ell, cudaMemcpyDeviceToHost, h->stream));
     else
-      std::memset(p_ring, 0, sizeof(double) * h->n * P.ell);
+      std::memset(p_ring, 0, sizeof(double) * h->n_loc * P.ell);
   }
   if (sketch_cols) {
     const int nc = P.method == SFLSQR_METHOD_SFLSQR ? kd : kd + 1;
@@ -1028,8 +1333,9 @@ int sflsqr_debug_state(sflsqr_t* h, double* z, double* x, double* p_ring, double
 
 int sflsqr_debug_set_tuning(sflsqr_t* h, int32_t spmv_mode, int32_t band_shift) {
   if (!h) return fail(nullptr, SFLSQR_E_INVALID, "NULL handle");
-  if (spmv_mode < -1 || spmv_mode > 10 || (spmv_mode > 3 && spmv_mode != 8 && spmv_mode != 10) || band_shift < 8 || band_shift > 30)
-    return fail(h, SFLSQR_E_INVALID, "bad tuning values");
+  const bool ok_mode = spmv_mode == -1 || spmv_mode == 0 || spmv_mode == 1 || spmv_mode == 2 || spmv_mode == 3 ||
+                       spmv_mode == 8 || spmv_mode == 10;
+  if (!ok_mode || band_shift < 8 || band_shift > 30) return fail(h, SFLSQR_E_INVALID, "bad tuning values");
   h->spmv_mode = spmv_mode;
   h->band_shift = band_shift;
   if (h->gexec) {
@@ -1066,6 +1372,7 @@ void sflsqr_destroy(sflsqr_t* h) {
   free_solve(h);
   free_op(h);
   for (auto e : h->prof.ev) cudaEventDestroy(e);
+  delete h->comm;
   if (h->own_stream) cudaStreamDestroy(h->stream);
   delete h;
 }

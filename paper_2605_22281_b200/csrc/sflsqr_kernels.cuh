@@ -38,6 +38,10 @@ struct Params {
   int64_t m, n;
   int ell, maxit, method, orth_mode, precond, d, s_nz, want_res, need_x, use_pring;
   int ldh;                 // leading dimension of H = maxit + 1
+  int dist;                // world > 1: reductions come from scal[] (allreduced), not from part[]
+  double* scal;            // per-slot global scalars (dist)
+  double* skbuf;           // d: S v of the current vector (allreduced when dist)
+  double *zsend, *wsend;   // dist: fixed-address copies of z_k / w_{k+1} for the allgathers
   double p_exp, eps_rel, tol, eta, delta_e, sk_scale;
   uint32_t seed_lo, seed_hi;
   // n-side vectors
@@ -114,6 +118,24 @@ __device__ __forceinline__ double max_partials(const double* part, int nb, doubl
   double v = -INFINITY;
   for (int i = threadIdx.x; i < nb; i += NT) v = fmax(v, part[i]);
   return block_max<NT>(v, sh);
+}
+
+// A reduced quantity of slot `slot`: single rank -> sum the per-block partials in
+// block order here; several ranks -> the allreduced scalar (k_reduce_slots + comm).
+template <int NT>
+__device__ __forceinline__ double get_sum(const Params& P, int slot, double* sh, int nb);
+template <int NT>
+__device__ __forceinline__ double get_max(const Params& P, int slot, double* sh, int nb);
+
+template <int NT>
+__device__ __forceinline__ double get_sum(const Params& P, int slot, double* sh, int nb) {
+  if (P.dist) return P.scal[slot];
+  return sum_partials<NT>(P.part + (size_t)slot * nb, nb, sh);
+}
+template <int NT>
+__device__ __forceinline__ double get_max(const Params& P, int slot, double* sh, int nb) {
+  if (P.dist) return P.scal[slot];
+  return max_partials<NT>(P.part + (size_t)slot * nb, nb, sh);
 }
 
 // Streaming (read-once) loads: bypass L1 allocation so L1 keeps the gathered vector.
@@ -425,13 +447,10 @@ __global__ void __launch_bounds__(256) k_blur_cols(const DevState* st, int H, in
 // over the coordinates i hashed to row r, in increasing i.  One CTA per sketch row.
 __global__ void __launch_bounds__(256) k_sketch_apply(const DevState* st, const int64_t* __restrict__ srp,
                                                       const uint32_t* __restrict__ sent,
-                                                      const double* __restrict__ v_base, int64_t v_ld, int v_koff,
-                                                      int d, double scale, int mult_beta, double* out_base,
-                                                      int64_t out_ld, int out_koff, double* out2) {
+                                                      const double* __restrict__ v, int d, double scale,
+                                                      double* __restrict__ out) {
   __shared__ double sh[33];
   if (st && st->done) return;
-  const double* __restrict__ v = kvec(st, v_base, v_ld, v_koff);
-  double* out = kvec_w(st, out_base, out_ld, out_koff);
   for (int r = blockIdx.x; r < d; r += gridDim.x) {
     double acc = 0.0;
     for (int64_t q = srp[r] + threadIdx.x; q < srp[r + 1]; q += 256) {
@@ -440,11 +459,17 @@ __global__ void __launch_bounds__(256) k_sketch_apply(const DevState* st, const 
       acc += (e >> 31) ? -vi : vi;
     }
     acc = block_sum<256>(acc, sh) * scale;
-    if (threadIdx.x == 0) {
-      if (out2) out2[r] = acc;
-      out[r] = mult_beta ? acc * st->beta : acc;
-    }
+    if (threadIdx.x == 0) out[r] = acc;
   }
+}
+
+// Per-slot reduction of the block partials into P.scal (dist mode; one CTA per slot).
+__global__ void __launch_bounds__(kVecThreads) k_reduce_slots(Params P, int slot0, int is_max) {
+  __shared__ double sh[33];
+  const int slot = slot0 + blockIdx.x;
+  const double v = is_max ? max_partials<kVecThreads>(P.part + (size_t)slot * kVecBlocks, kVecBlocks, sh)
+                          : sum_partials<kVecThreads>(P.part + (size_t)slot * kVecBlocks, kVecBlocks, sh);
+  if (threadIdx.x == 0) P.scal[slot] = v;
 }
 
 // ------------------------------------------------------------------ init
@@ -460,10 +485,13 @@ __global__ void __launch_bounds__(kVecThreads) k_norm_partial(Params P, const do
 }
 __global__ void __launch_bounds__(kVecThreads) k_init_w1(Params P) {
   __shared__ double sh[33];
-  const double beta = sqrt(sum_partials<kVecThreads>(P.part + (size_t)P.slot_beta * kVecBlocks, kVecBlocks, sh));
+  const double beta = sqrt(get_sum<kVecThreads>(P, P.slot_beta, sh, kVecBlocks));
   if (blockIdx.x == 0 && threadIdx.x == 0) P.st->beta = beta;
-  for (int64_t i = (int64_t)blockIdx.x * kVecThreads + threadIdx.x; i < P.m; i += (int64_t)gridDim.x * kVecThreads)
-    P.W[i] = P.b[i] / beta;
+  for (int64_t i = (int64_t)blockIdx.x * kVecThreads + threadIdx.x; i < P.m; i += (int64_t)gridDim.x * kVecThreads) {
+    const double w1 = P.b[i] / beta;
+    P.W[i] = w1;
+    if (P.wsend) P.wsend[i] = w1;
+  }
 }
 
 // ------------------------------------------------------------------ a1 / a5: windowed MGS
@@ -495,7 +523,7 @@ __global__ void __launch_bounds__(kVecThreads) k_mgs_pass(Params P, int side, in
   double cprev = 0.0;
   const double* qprev = nullptr;
   if (pass > 0) {
-    cprev = sum_partials<kVecThreads>(P.part + (size_t)(slot0 + pass - 1) * kVecBlocks, kVecBlocks, sh);
+    cprev = get_sum<kVecThreads>(P, slot0 + pass - 1, sh, kVecBlocks);
     qprev = mgs_basis(P, side, j0 + pass - 1);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       const int row = j0 + pass - 2;  // 0-based row of the coefficient
@@ -536,8 +564,8 @@ __global__ void __launch_bounds__(kVecThreads) k_finish_z(Params P) {
   if (st->done) return;
   const int k = st->k;
   const int J = min(P.ell, k - 1);
-  const double t = sqrt(sum_partials<kVecThreads>(P.part + (size_t)(P.slot_z0 + J) * kVecBlocks, kVecBlocks, sh));
-  const double zin = sqrt(sum_partials<kVecThreads>(P.part + (size_t)P.slot_zin * kVecBlocks, kVecBlocks, sh));
+  const double t = sqrt(get_sum<kVecThreads>(P, P.slot_z0 + J, sh, kVecBlocks));
+  const double zin = sqrt(get_sum<kVecThreads>(P, P.slot_zin, sh, kVecBlocks));
   if (t == 0.0 || t <= 1e-14 * zin) {
     __syncthreads();
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -554,7 +582,7 @@ __global__ void __launch_bounds__(kVecThreads) k_finish_z(Params P) {
     if (k == 1) {
       mode = 0;  // D_1 = I (x_0 = 0)
     } else {
-      const double mx = max_partials<kVecThreads>(P.part + (size_t)P.slot_xmax * kVecBlocks, kVecBlocks, sh);
+      const double mx = get_max<kVecThreads>(P, P.slot_xmax, sh, kVecBlocks);
       if (!(mx > 0.0))
         mode = 0;  // x_{k-1} = 0 (IRN) or x_{k-1} <= 0 (NONNEG): D = I
       else
@@ -577,6 +605,7 @@ __global__ void __launch_bounds__(kVecThreads) k_finish_z(Params P) {
     }
     zk[i] = zi;
     if (pr) pr[i] = p;
+    if (P.zsend) P.zsend[i] = zi;
   }
 }
 
@@ -589,16 +618,19 @@ __global__ void __launch_bounds__(kVecThreads) k_finish_w(Params P) {
   if (st->done) return;
   const int k = st->k;
   const int J = min(P.ell + 1, k);
-  const double hn = sqrt(sum_partials<kVecThreads>(P.part + (size_t)(P.slot_w0 + J) * kVecBlocks, kVecBlocks, sh));
-  const double win = sqrt(sum_partials<kVecThreads>(P.part + (size_t)P.slot_win * kVecBlocks, kVecBlocks, sh));
+  const double hn = sqrt(get_sum<kVecThreads>(P, P.slot_w0 + J, sh, kVecBlocks));
+  const double win = sqrt(get_sum<kVecThreads>(P, P.slot_win, sh, kVecBlocks));
   const bool brk = (hn == 0.0 || hn <= 1e-14 * win);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     st->wbreak = brk ? 1 : 0;
     P.H[(int64_t)k + (int64_t)(k - 1) * P.ldh] = brk ? 0.0 : hn;
   }
   double* wk1 = P.W + (int64_t)k * P.m;
-  for (int64_t i = (int64_t)blockIdx.x * kVecThreads + threadIdx.x; i < P.m; i += (int64_t)gridDim.x * kVecThreads)
-    wk1[i] = brk ? 0.0 : P.w[i] / hn;
+  for (int64_t i = (int64_t)blockIdx.x * kVecThreads + threadIdx.x; i < P.m; i += (int64_t)gridDim.x * kVecThreads) {
+    const double wv = brk ? 0.0 : P.w[i] / hn;
+    wk1[i] = wv;
+    if (P.wsend) P.wsend[i] = wv;
+  }
 }
 
 // ------------------------------------------------------------------ a7: projected sketched LS (one CTA)
@@ -643,12 +675,16 @@ __global__ void __launch_bounds__(kLsThreads) k_ls(Params P) {
     a[u] = 0.0;
     q[u] = 0.0;
     if (r < d) {
+      const double sv = P.skbuf[r];  // S A z_k (sFLSQR) or S T w_{k+1} (sFLSMR)
       if (P.method == 0) {
-        a[u] = Mc[r];
+        a[u] = sv;
+        Mc[r] = sv;
       } else {
+        P.STW[(int64_t)(c + 1) * d + r] = sv;
         double acc = 0.0;
-        for (int i = max(0, c - P.ell); i <= c + 1; ++i)
+        for (int i = max(0, c - P.ell); i <= c; ++i)
           acc = fma(P.STW[(int64_t)i * d + r], P.H[(int64_t)i + (int64_t)c * P.ldh], acc);
+        acc = fma(sv, P.H[(int64_t)(c + 1) + (int64_t)c * P.ldh], acc);
         a[u] = acc;
         Mc[r] = acc;
       }
@@ -860,7 +896,7 @@ __global__ void __launch_bounds__(kVecThreads) k_stop(Params P) {
   if (st->done) return;
   const int k = st->k;
   double r = NAN;
-  if (P.want_res) r = sqrt(sum_partials<kVecThreads>(P.part + (size_t)P.slot_res * kVecBlocks, kVecBlocks, sh));
+  if (P.want_res) r = sqrt(get_sum<kVecThreads>(P, P.slot_res, sh, kVecBlocks));
   if (threadIdx.x != 0) return;
   P.hist_true[k - 1] = r;
   const double sres = P.hist_sk[k - 1];
@@ -880,13 +916,20 @@ __global__ void __launch_bounds__(kVecThreads) k_stop(Params P) {
   st->k = k + 1;
 }
 
-// rhs norm for the tol test, qtb = rhs (LS start), state reset.
-__global__ void k_init_ls(Params P) {
+// rhs = s_b = S b (sFLSQR, Alg. 1) or s = beta S z with S_TW = [S z]
+// (sFLSMR, Alg. 2), from skbuf; rhs norm for the tol test; qtb = rhs
+// (LS start); state reset.
+__global__ void k_init_rhs(Params P) {
   __shared__ double sh[33];
+  const double beta = P.st->beta;
   double part = 0.0;
   for (int r = threadIdx.x; r < P.d; r += blockDim.x) {
-    part = fma(P.rhs[r], P.rhs[r], part);
-    P.qtb[r] = P.rhs[r];
+    const double sv = P.skbuf[r];
+    const double rv = P.method == 0 ? sv : beta * sv;
+    if (P.method != 0) P.STW[r] = sv;
+    P.rhs[r] = rv;
+    P.qtb[r] = rv;
+    part = fma(rv, rv, part);
   }
   const double nr = sqrt(block_sum<kVecThreads>(part, sh));
   if (threadIdx.x == 0) {

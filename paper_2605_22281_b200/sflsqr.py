@@ -31,7 +31,8 @@ HIST_TRUE_RES = 1
 KC_NAMES = ["spmv_A", "spmv_T", "orth", "tau", "sketch", "ls", "xupd", "res", "stop"]
 
 EXPORTED = [
-    "sflsqr_version", "sflsqr_create", "sflsqr_set_operator", "sflsqr_set_operator_blur", "sflsqr_set_sketch",
+    "sflsqr_version", "sflsqr_create", "sflsqr_get_unique_id", "sflsqr_local_group_create",
+    "sflsqr_local_group_destroy", "sflsqr_set_operator_shard", "sflsqr_set_operator", "sflsqr_set_operator_blur", "sflsqr_set_sketch",
     "sflsqr_set_precond", "sflsqr_set_rhs", "sflsqr_iterate", "sflsqr_get_x", "sflsqr_get_residual_norms",
     "sflsqr_get_info", "sflsqr_debug_sketch_table", "sflsqr_debug_apply", "sflsqr_debug_basis", "sflsqr_debug_state",
     "sflsqr_debug_set_tuning",
@@ -39,19 +40,24 @@ EXPORTED = [
 ]
 
 
+COMM_NCCL, COMM_LOCAL = 0, 1
+
+
 class Opts(ctypes.Structure):
     _fields_ = [("method", ctypes.c_int32), ("window", ctypes.c_int32), ("maxit", ctypes.c_int32),
                 ("orth_mode", ctypes.c_int32), ("tol", ctypes.c_double), ("eta", ctypes.c_double),
                 ("delta_e", ctypes.c_double), ("history", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("stream", ctypes.c_void_p), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
-                ("use_graph", ctypes.c_int32), ("reserved", ctypes.c_int32 * 7)]
+                ("use_graph", ctypes.c_int32), ("comm_kind", ctypes.c_int32), ("nccl_id", ctypes.c_void_p),
+                ("local_group", ctypes.c_void_p), ("reserved", ctypes.c_int32 * 4)]
 
 
 class Info(ctypes.Structure):
     _fields_ = [("k_done", ctypes.c_int32), ("k_x", ctypes.c_int32), ("status", ctypes.c_int32),
                 ("rank_flag", ctypes.c_int32), ("m", ctypes.c_int64), ("n", ctypes.c_int64),
                 ("nnz_a", ctypes.c_int64), ("nnz_t", ctypes.c_int64), ("launches", ctypes.c_int64),
-                ("beta", ctypes.c_double)]
+                ("beta", ctypes.c_double), ("m0", ctypes.c_int64), ("m_loc", ctypes.c_int64),
+                ("n0", ctypes.c_int64), ("n_loc", ctypes.c_int64)]
 
 
 class Profile(ctypes.Structure):
@@ -74,6 +80,10 @@ def load_library(path: str = LIB_PATH):
         "sflsqr_version": ([], ctypes.c_int),
         "sflsqr_create": ([ctypes.POINTER(vp), ctypes.POINTER(Opts)], ctypes.c_int),
         "sflsqr_set_operator": ([vp, i64, i64, vp, vp, vp, i32, vp, vp, vp, i32], ctypes.c_int),
+        "sflsqr_set_operator_shard": ([vp, i64, i64, i64, i64, vp, vp, vp, i32, i64, i64, vp, vp, vp], ctypes.c_int),
+        "sflsqr_get_unique_id": ([vp], ctypes.c_int),
+        "sflsqr_local_group_create": ([ctypes.POINTER(vp), i32, i32], ctypes.c_int),
+        "sflsqr_local_group_destroy": ([vp], None),
         "sflsqr_set_operator_blur": ([vp, i32, i32, f64, i32], ctypes.c_int),
         "sflsqr_set_sketch": ([vp, ctypes.c_uint64, i32, i32], ctypes.c_int),
         "sflsqr_set_precond": ([vp, i32, f64, f64], ctypes.c_int),
@@ -137,7 +147,8 @@ class SFLSQR:
     """One solver handle (sflsqr_create ... sflsqr_destroy)."""
 
     def __init__(self, method="sflsqr", window=2, maxit=10, orth_mode="P", tol=0.0, eta=0.0, delta_e=0.0,
-                 history=HIST_TRUE_RES, device=0, stream=None, use_graph=True):
+                 history=HIST_TRUE_RES, device=0, stream=None, use_graph=True, rank=0, world=1, nccl_id=None,
+                 local_group=None):
         self.lib = load_library()
         o = Opts()
         o.method = METHOD_SFLSQR if method == "sflsqr" else METHOD_SFLSMR if method == "sflsmr" else -1
@@ -147,7 +158,15 @@ class SFLSQR:
         o.history, o.device = int(history), int(device)
         # NULL / the legacy default stream -> the library creates its own non-blocking stream
         o.stream = stream if stream is not None else _torch_stream(device)
-        o.rank, o.world, o.use_graph = 0, 1, 1 if use_graph else 0
+        o.rank, o.world, o.use_graph = int(rank), int(world), 1 if use_graph else 0
+        self._id_buf = None
+        if int(world) > 1:
+            if local_group is not None:
+                o.comm_kind, o.local_group = COMM_LOCAL, local_group.ptr
+            else:
+                o.comm_kind = COMM_NCCL
+                self._id_buf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+                o.nccl_id = ctypes.addressof(self._id_buf)
         self.maxit = int(maxit)
         h = ctypes.c_void_p()
         rc = self.lib.sflsqr_create(ctypes.byref(h), ctypes.byref(o))
@@ -180,7 +199,7 @@ class SFLSQR:
         self.close()
 
     # ------------------------------------------------------------------ ABI mirrors
-    def set_operator(self, m, n, a_rowptr, a_col, a_val, t=None, borrow=False):
+    def set_operator(self, m, n, a_rowptr, a_col, a_val, t=None, borrow=False):  # noqa: D401
         """t = None -> T_BUILD (A^T formed by the library); t = (rowptr, col, val) -> T_GIVEN."""
         pa = [_ptr(x) for x in (a_rowptr, a_col, a_val)]
         dev = pa[0][1]
@@ -196,6 +215,21 @@ class SFLSQR:
         self._check(self.lib.sflsqr_set_operator(self.h, int(m), int(n), pa[0][0], pa[1][0], pa[2][0], mode,
                                                  pt[0][0], pt[1][0], pt[2][0], flags))
         self.m, self.n = int(m), int(n)
+
+    def set_operator_shard(self, m, n, a_row0, a_row1, a_rowptr, a_col, a_val, t=None, t_rows=(0, 0)):
+        """This rank's block of A rows [a_row0, a_row1) (local rowptr, global columns); t = None ->
+        COLSHARD (T = (A block)^T built locally), t = (rowptr, col, val) of T rows t_rows -> ROWSHARD."""
+        pa = [_ptr(np.ascontiguousarray(x)) for x in (a_rowptr, a_col, a_val)]
+        if t is None:
+            pt, mode = [(None, False, None)] * 3, T_BUILD
+        else:
+            pt, mode = [_ptr(np.ascontiguousarray(x)) for x in t], T_GIVEN
+        self._check(self.lib.sflsqr_set_operator_shard(self.h, int(m), int(n), int(a_row0), int(a_row1), pa[0][0],
+                                                       pa[1][0], pa[2][0], mode, int(t_rows[0]), int(t_rows[1]),
+                                                       pt[0][0], pt[1][0], pt[2][0]))
+        inf = self.get_info()
+        self.m_glob, self.n_glob = int(m), int(n)
+        self.m, self.n = inf["m_loc"], inf["n_loc"]
 
     def set_operator_blur(self, H, W, sigma, radius):
         self._check(self.lib.sflsqr_set_operator_blur(self.h, int(H), int(W), float(sigma), int(radius)))
@@ -289,6 +323,39 @@ class SFLSQR:
         p = Profile()
         self._check(self.lib.sflsqr_get_profile(self.h, ctypes.byref(p)))
         return {KC_NAMES[i]: dict(ms=p.ms[i], launches=int(p.launches[i]), bytes=p.bytes[i]) for i in range(9)}
+
+
+def get_unique_id() -> bytes:
+    """128-byte NCCL id (rank 0); broadcast it with the caller's process group."""
+    lib = load_library()
+    buf = ctypes.create_string_buffer(128)
+    rc = lib.sflsqr_get_unique_id(buf)
+    if rc != OK:
+        raise SflsqrError(rc, lib.sflsqr_last_error(None).decode())
+    return buf.raw
+
+
+class LocalGroup:
+    """In-process rank group (SFLSQR_COMM_LOCAL): world handles on one device, one host thread each."""
+
+    def __init__(self, world, device=0):
+        self.lib = load_library()
+        p = ctypes.c_void_p()
+        rc = self.lib.sflsqr_local_group_create(ctypes.byref(p), int(world), int(device))
+        if rc != OK:
+            raise SflsqrError(rc, self.lib.sflsqr_last_error(None).decode())
+        self.ptr, self.world = p.value, int(world)
+
+    def close(self):
+        if self.ptr:
+            self.lib.sflsqr_local_group_destroy(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def solver_for_problem(prob, spec, maxit=None, history=HIST_TRUE_RES, use_graph=True, eta=None, device=0,

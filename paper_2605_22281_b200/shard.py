@@ -1,0 +1,103 @@
+"""Host-side sharding logic for the multi-GPU path.
+
+Rank g owns a contiguous, nnz-balanced block of A rows (the m-partition) and a
+contiguous slice of the n-vectors (the n-partition).  The transpose side is
+either COLSHARD (T = the transpose of the local A block, formed locally, its
+product reduce-scattered) or ROWSHARD (rank g stores rows of the given B on its
+n-slice, w all-gathered).  This module only slices host arrays and drives the
+ranks; every arithmetic step runs in libsflsqr.so.
+"""
+from __future__ import annotations
+
+import threading
+
+import numpy as np
+
+
+def balanced_row_blocks(rowptr: np.ndarray, world: int) -> list:
+    """Contiguous row ranges [r0, r1) per rank, balancing nonzeros (ties -> rows)."""
+    rowptr = np.asarray(rowptr, dtype=np.int64)
+    nrows = rowptr.size - 1
+    nnz = int(rowptr[-1] - rowptr[0])
+    bounds = [0]
+    for g in range(1, world):
+        target = rowptr[0] + (nnz * g) // world if nnz else 0
+        r = int(np.searchsorted(rowptr, target, side="left")) if nnz else (nrows * g) // world
+        r = min(max(r, bounds[-1]), nrows)
+        bounds.append(r)
+    bounds.append(nrows)
+    return [(bounds[g], bounds[g + 1]) for g in range(world)]
+
+
+def even_blocks(n: int, world: int) -> list:
+    """The library's n-partition for COLSHARD: n0_g = g * ceil(n / world)."""
+    per = -(-n // world)
+    return [(min(n, g * per), min(n, (g + 1) * per)) for g in range(world)]
+
+
+def csr_block(rowptr, col, val, r0, r1):
+    """(local rowptr rebased to 0, col, val) of rows [r0, r1) (views into col/val)."""
+    s, e = int(rowptr[r0]), int(rowptr[r1])
+    return np.ascontiguousarray(rowptr[r0:r1 + 1] - s), col[s:e], val[s:e]
+
+
+def shard_plan(prob, world: int) -> dict:
+    """Partition of a gen.Problem over `world` ranks: A rows, T mode and n-slices."""
+    a_blocks = balanced_row_blocks(prob.A.rowptr, world)
+    if prob.t_mode == "given":
+        t_blocks = balanced_row_blocks(prob.T.rowptr, world)
+        return dict(a_blocks=a_blocks, t_mode="rowshard", n_blocks=t_blocks)
+    return dict(a_blocks=a_blocks, t_mode="colshard", n_blocks=even_blocks(prob.n, world))
+
+
+def run_local_group(prob, spec, world: int, maxit=None, device=0, eta=None, history=1):
+    """Run one sharded solve with `world` ranks as host threads of this process
+    (SFLSQR_COMM_LOCAL) on one device.  Returns (x, true_res, sketch_res, infos)
+    with x assembled from the ranks' n-slices."""
+    from .sflsqr import SFLSQR, LocalGroup
+
+    plan = shard_plan(prob, world)
+    grp = LocalGroup(world, device)
+    out = [None] * world
+    err = [None] * world
+    mx = maxit or spec.maxit
+
+    def rank_main(r):
+        try:
+            s = SFLSQR(method=spec.method, window=spec.window, maxit=mx, orth_mode=spec.orth_mode, tol=spec.tol,
+                       eta=spec.eta if eta is None else eta, delta_e=prob.delta_e, history=history, device=device,
+                       use_graph=False, rank=r, world=world, local_group=grp)
+            a0, a1 = plan["a_blocks"][r]
+            arp, acol, aval = csr_block(prob.A.rowptr, prob.A.col, prob.A.val, a0, a1)
+            if plan["t_mode"] == "rowshard":
+                t0, t1 = plan["n_blocks"][r]
+                trp, tcol, tval = csr_block(prob.T.rowptr, prob.T.col, prob.T.val, t0, t1)
+                s.set_operator_shard(prob.m, prob.n, a0, a1, arp, acol, aval, t=(trp, tcol, tval), t_rows=(t0, t1))
+            else:
+                s.set_operator_shard(prob.m, prob.n, a0, a1, arp, acol, aval)
+            s.set_sketch(prob.sketch_seed, spec.d, spec.s_nz)
+            s.set_precond(spec.precond, spec.p, spec.eps_rel)
+            s.set_rhs(np.ascontiguousarray(prob.b[a0:a1]))
+            done, status = s.iterate(mx)
+            tr, sk = s.get_residual_norms()
+            x = s.get_x()
+            info = s.get_info()
+            s.close()
+            out[r] = (x, tr, sk, info, done, status)
+        except Exception as exc:  # surfaced to the caller below
+            err[r] = exc
+
+    ths = [threading.Thread(target=rank_main, args=(r,)) for r in range(world)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    grp.close()
+    for e in err:
+        if e is not None:
+            raise e
+    x = np.zeros(prob.n)
+    for r in range(world):
+        info = out[r][3]
+        x[info["n0"]:info["n0"] + info["n_loc"]] = out[r][0]
+    return x, out[0][1], out[0][2], [o[3] for o in out], [(o[4], o[5]) for o in out], out
