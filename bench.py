@@ -198,15 +198,12 @@ def main():
 
     world, rank, local = _dist()
     from gen import make_problem
-    t_gen = time.perf_counter()
-    geo = {}
-    if args.N:
-        geo = dict(N=args.N)
-    prob = make_problem(args.config, **geo)
-    t_gen = time.perf_counter() - t_gen
-    spec = prob.solvers[0] if args.method is None else [s for s in prob.solvers if s.method == args.method][0]
-
+    from gen.problems import CONFIGS
     if args.impl == "reference":
+        if rank != 0:
+            return            # the reference arm runs on rank 0 only
+        prob = make_problem(args.config, **(dict(N=args.N) if args.N else {}))
+        spec = prob.solvers[0] if args.method is None else [x for x in prob.solvers if x.method == args.method][0]
         bench_reference(args, prob, spec, world, rank)
         return
 
@@ -227,13 +224,60 @@ def main():
     _barrier(world)
 
     W, K = args.warmup, args.steps
-    maxit = max(spec.maxit, W + K)
+    sharded = world > 1 and CONFIGS[args.config]["kind"] == "ct" and not args.N
+    t_gen = time.perf_counter()
+    if sharded:
+        # every rank generates and holds only its A (and B) row block
+        from gen.problems import ct_row_nnz, make_ct_shard
+        from paper_2605_22281_b200.shard import balanced_row_blocks
+        from paper_2605_22281_b200.sflsqr import SFLSQR, get_unique_id
+        import torch.distributed as dist
+
+        def allreduce_sum(v):
+            t = torch.tensor([v], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t)
+            return float(t.item())
+
+        a_cnt, t_cnt = ct_row_nnz(args.config)
+        ab = balanced_row_blocks(np.concatenate([[0], np.cumsum(a_cnt)]), world)
+        tb = None if t_cnt is None else balanced_row_blocks(np.concatenate([[0], np.cumsum(t_cnt)]), world)
+        prob = make_ct_shard(args.config, ab[rank], None if tb is None else tb[rank], allreduce_sum)
+        spec = prob.solvers[0] if args.method is None else [x for x in prob.solvers if x.method == args.method][0]
+        t_gen = time.perf_counter() - t_gen
+        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(get_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        maxit = max(spec.maxit, W + K)
+        t_up = time.perf_counter()
+        s = SFLSQR(method=spec.method, window=spec.window, maxit=maxit, orth_mode=spec.orth_mode, tol=spec.tol,
+                   eta=0.0, delta_e=prob.delta_e, device=local, use_graph=False, rank=rank, world=world,
+                   nccl_id=bytes(uid.cpu().numpy()))
+        A = prob.A_loc
+        t = None if prob.T_loc is None else (prob.T_loc.rowptr, prob.T_loc.col, prob.T_loc.val)
+        s.set_operator_shard(prob.m, prob.n, prob.a_rows[0], prob.a_rows[1], A.rowptr, A.col, A.val, t=t,
+                             t_rows=prob.t_rows or (0, 0))
+        s.set_sketch(prob.sketch_seed, spec.d, spec.s_nz)
+        s.set_precond(spec.precond, spec.p, spec.eps_rel)
+        t_up = time.perf_counter() - t_up
+        b_host = prob.b_loc
+        nnz_A = int(allreduce_sum(float(A.nnz)))
+        nnz_T = int(allreduce_sum(float(prob.T_loc.nnz if prob.T_loc is not None else A.nnz)))
+        parallelism = f"shard{world} ({'ROWSHARD' if prob.T_loc is not None else 'COLSHARD'}, NCCL)"
+    else:
+        prob = make_problem(args.config, **(dict(N=args.N) if args.N else {}))
+        spec = prob.solvers[0] if args.method is None else [x for x in prob.solvers if x.method == args.method][0]
+        t_gen = time.perf_counter() - t_gen
+        maxit = max(spec.maxit, W + K)
+        t_up = time.perf_counter()
+        s = solver_for_problem(prob, spec, maxit=maxit, eta=0.0, device=local, use_graph=args.no_profile)
+        t_up = time.perf_counter() - t_up
+        b_host = prob.b
+        nnz_A = prob.A.nnz if prob.A is not None else None
+        nnz_T = prob.T.nnz if prob.T is not None else nnz_A
+        parallelism = "replicas" if world > 1 else "single"
     stream = torch.cuda.current_stream()
-    t_up = time.perf_counter()
-    s = solver_for_problem(prob, spec, maxit=maxit, eta=0.0, device=local, use_graph=args.no_profile)
-    t_up = time.perf_counter() - t_up
-    info0 = s.get_info()
-    s.set_rhs(prob.b)
+    s.set_rhs(b_host)
     s.iterate(W)                                   # untimed warm-up (graph capture already done)
     if not args.no_profile:
         s.set_profiling(True)
@@ -254,7 +298,8 @@ def main():
     prof = s.get_profile()
     s.set_profiling(False)
     k_done = s.get_info()["k_done"]
-    value = K * world / (ms / 1e3)
+    # sharded: the ranks cooperate on one solve (iterations/s of the job); replicas: independent solves
+    value = (K if sharded else K * world) / (ms / 1e3)
 
     # roofline of the dominant kernel (HBM-bound CSR SpMV)
     peak, peak_src = _peaks()
@@ -282,8 +327,8 @@ def main():
     # e2e through the public API: host b -> set_rhs, K iterations, x + histories back to host
     e2e = None
     if not args.no_e2e:
-        b_pin = torch.from_numpy(prob.b).pin_memory()
-        x_pin = torch.empty(prob.n, dtype=torch.float64).pin_memory()
+        b_pin = torch.from_numpy(np.ascontiguousarray(b_host)).pin_memory()
+        x_pin = torch.empty(s.n, dtype=torch.float64).pin_memory()
         _barrier(world)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -294,8 +339,8 @@ def main():
         torch.cuda.synchronize()
         te = time.perf_counter() - t0
         te = _max_over_ranks(te, world)
-        e2e = {"value": K * world / te, "unit": UNIT, "h2d_bytes_per_step": 8.0 * prob.m / K,
-               "d2h_bytes_per_step": (8.0 * prob.n + 16.0 * K) / K,
+        e2e = {"value": (K if sharded else K * world) / te, "unit": UNIT,
+               "h2d_bytes_per_step": 8.0 * len(b_host) / K, "d2h_bytes_per_step": (8.0 * s.n + 16.0 * K) / K,
                "note": "set_rhs(pinned host b) + iterate(K) + get_x(pinned host) + get_residual_norms, wall clock"}
     s.close()
 
@@ -306,15 +351,14 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
-            "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong" if sharded else "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": prob.name, "method": spec.method, "m": prob.m, "n": prob.n,
-                       "nnz_A": prob.A.nnz if prob.A is not None else None,
-                       "nnz_T": prob.T.nnz if prob.T is not None else (prob.A.nnz if prob.A is not None else None),
+                       "nnz_A": nnz_A, "nnz_T": nnz_T,
                        "ell": spec.window, "d": spec.d, "s": spec.s_nz, "tau": spec.precond, "maxit": maxit,
                        "iterations_timed": f"{W + 1}..{W + K}", "history": "true residual (W path) on",
                        "l2": "inputs larger than L2 (operators ~30 GB vs 126 MB L2); no flush",
-                       "parallelism": "replicas" if world > 1 else "single",
+                       "parallelism": parallelism,
                        "launch": "eager + per-kernel CUDA events" if not args.no_profile else "CUDA graph"},
             "roofline": roof,
             "step_algorithmic_gbs": step_gbs,

@@ -153,80 +153,89 @@ void canonicalise(std::vector<Seg>& v) {
 
 extern "C" {
 
-// Number of nonzeros per Siddon row (row = a*nb + j).  Returns 0 on success.
-int gen_siddon_rownnz(int N, int n_angles, int nb, int64_t* row_nnz, int nthreads) {
-  if (N <= 0 || n_angles <= 0 || nb <= 0) return -1;
-  const int64_t m = (int64_t)n_angles * nb;
-  parallel_for(m, nthreads, [&](int64_t r) {
+// Number of nonzeros per Siddon row r in [r0, r1) (row = a*nb + j) into row_nnz[r - r0].
+int gen_siddon_rownnz_range(int N, int n_angles, int nb, int64_t r0, int64_t r1, int64_t* row_nnz, int nthreads) {
+  if (N <= 0 || n_angles <= 0 || nb <= 0 || r0 < 0 || r1 < r0 || r1 > (int64_t)n_angles * nb) return -1;
+  parallel_for(r1 - r0, nthreads, [&](int64_t q) {
     thread_local std::vector<Seg> buf;
+    const int64_t r = r0 + q;
     int a = (int)(r / nb), j = (int)(r % nb);
     double theta = M_PI * (double)a / (double)n_angles;
     double t = (double)j - 0.5 * (double)(nb - 1);
     siddon_ray(N, theta, t, buf);
     canonicalise(buf);
-    row_nnz[r] = (int64_t)buf.size();
+    row_nnz[q] = (int64_t)buf.size();
   });
   return 0;
 }
 
-// Fill col/val given rowptr (exclusive prefix sum of gen_siddon_rownnz).
-int gen_siddon_fill(int N, int n_angles, int nb, const int64_t* rowptr, int32_t* col, double* val,
-                    int nthreads) {
-  if (N <= 0 || n_angles <= 0 || nb <= 0) return -1;
-  const int64_t m = (int64_t)n_angles * nb;
+// Fill col/val of rows [r0, r1) given rowptr (r1 - r0 + 1 entries, base rowptr[0]).
+int gen_siddon_fill_range(int N, int n_angles, int nb, int64_t r0, int64_t r1, const int64_t* rowptr, int32_t* col,
+                          double* val, int nthreads) {
+  if (N <= 0 || n_angles <= 0 || nb <= 0 || r0 < 0 || r1 < r0 || r1 > (int64_t)n_angles * nb) return -1;
   std::atomic<int> bad(0);
-  parallel_for(m, nthreads, [&](int64_t r) {
+  const int64_t base = rowptr[0];
+  parallel_for(r1 - r0, nthreads, [&](int64_t q) {
     thread_local std::vector<Seg> buf;
+    const int64_t r = r0 + q;
     int a = (int)(r / nb), j = (int)(r % nb);
     double theta = M_PI * (double)a / (double)n_angles;
     double t = (double)j - 0.5 * (double)(nb - 1);
     siddon_ray(N, theta, t, buf);
     canonicalise(buf);
-    int64_t s = rowptr[r];
-    if ((int64_t)buf.size() != rowptr[r + 1] - s) {
+    int64_t s = rowptr[q] - base;
+    if ((int64_t)buf.size() != rowptr[q + 1] - rowptr[q]) {
       bad.store(1);
       return;
     }
-    for (size_t q = 0; q < buf.size(); ++q) {
-      col[s + q] = buf[q].col;
-      val[s + q] = buf[q].len;
+    for (size_t k = 0; k < buf.size(); ++k) {
+      col[s + k] = buf[k].col;
+      val[s + k] = buf[k].len;
     }
   });
   return bad.load() ? -2 : 0;
 }
 
-// Pixel-driven linear-interpolation backprojector B (n x m).
-int gen_pixbp_rownnz(int N, int n_angles, int nb, int64_t* row_nnz, int nthreads) {
-  if (N <= 0 || n_angles <= 0 || nb <= 0) return -1;
-  const int64_t n = (int64_t)N * N;
+int gen_siddon_rownnz(int N, int n_angles, int nb, int64_t* row_nnz, int nthreads) {
+  return gen_siddon_rownnz_range(N, n_angles, nb, 0, (int64_t)n_angles * nb, row_nnz, nthreads);
+}
+
+int gen_siddon_fill(int N, int n_angles, int nb, const int64_t* rowptr, int32_t* col, double* val, int nthreads) {
+  return gen_siddon_fill_range(N, n_angles, nb, 0, (int64_t)n_angles * nb, rowptr, col, val, nthreads);
+}
+
+// Pixel-driven linear-interpolation backprojector B (n x m), rows (pixels) [p0, p1).
+int gen_pixbp_rownnz_range(int N, int n_angles, int nb, int64_t p0, int64_t p1, int64_t* row_nnz, int nthreads) {
+  if (N <= 0 || n_angles <= 0 || nb <= 0 || p0 < 0 || p1 < p0 || p1 > (int64_t)N * N) return -1;
   const double half = 0.5 * N, off = 0.5 * (nb - 1);
-  parallel_for(n, nthreads, [&](int64_t p) {
+  parallel_for(p1 - p0, nthreads, [&](int64_t q) {
+    const int64_t p = p0 + q;
     int iy = (int)(p / N), ix = (int)(p % N);
     double x = ix + 0.5 - half, y = iy + 0.5 - half;
     int64_t cnt = 0;
     for (int a = 0; a < n_angles; ++a) {
       double th = M_PI * (double)a / (double)n_angles;
       double u = x * std::cos(th) + y * std::sin(th) + off;
-      double j0 = std::floor(u);
-      long jj = (long)j0;
+      long jj = (long)std::floor(u);
       if (jj >= 0 && jj < nb) ++cnt;
       if (jj + 1 >= 0 && jj + 1 < nb) ++cnt;
     }
-    row_nnz[p] = cnt;
+    row_nnz[q] = cnt;
   });
   return 0;
 }
 
-int gen_pixbp_fill(int N, int n_angles, int nb, const int64_t* rowptr, int32_t* col, double* val,
-                   int nthreads) {
-  if (N <= 0 || n_angles <= 0 || nb <= 0) return -1;
-  const int64_t n = (int64_t)N * N;
+int gen_pixbp_fill_range(int N, int n_angles, int nb, int64_t p0, int64_t p1, const int64_t* rowptr, int32_t* col,
+                         double* val, int nthreads) {
+  if (N <= 0 || n_angles <= 0 || nb <= 0 || p0 < 0 || p1 < p0 || p1 > (int64_t)N * N) return -1;
   const double half = 0.5 * N, off = 0.5 * (nb - 1);
+  const int64_t base = rowptr[0];
   std::atomic<int> bad(0);
-  parallel_for(n, nthreads, [&](int64_t p) {
+  parallel_for(p1 - p0, nthreads, [&](int64_t q) {
+    const int64_t p = p0 + q;
     int iy = (int)(p / N), ix = (int)(p % N);
     double x = ix + 0.5 - half, y = iy + 0.5 - half;
-    int64_t q = rowptr[p];
+    int64_t k = rowptr[q] - base;
     for (int a = 0; a < n_angles; ++a) {
       double th = M_PI * (double)a / (double)n_angles;
       double u = x * std::cos(th) + y * std::sin(th) + off;
@@ -234,19 +243,27 @@ int gen_pixbp_fill(int N, int n_angles, int nb, const int64_t* rowptr, int32_t* 
       double f = u - j0;
       long jj = (long)j0;
       if (jj >= 0 && jj < nb) {
-        col[q] = (int32_t)((int64_t)a * nb + jj);
-        val[q] = 1.0 - f;
-        ++q;
+        col[k] = (int32_t)((int64_t)a * nb + jj);
+        val[k] = 1.0 - f;
+        ++k;
       }
       if (jj + 1 >= 0 && jj + 1 < nb) {
-        col[q] = (int32_t)((int64_t)a * nb + jj + 1);
-        val[q] = f;
-        ++q;
+        col[k] = (int32_t)((int64_t)a * nb + jj + 1);
+        val[k] = f;
+        ++k;
       }
     }
-    if (q != rowptr[p + 1]) bad.store(1);
+    if (k != rowptr[q + 1] - base) bad.store(1);
   });
   return bad.load() ? -2 : 0;
+}
+
+int gen_pixbp_rownnz(int N, int n_angles, int nb, int64_t* row_nnz, int nthreads) {
+  return gen_pixbp_rownnz_range(N, n_angles, nb, 0, (int64_t)N * N, row_nnz, nthreads);
+}
+
+int gen_pixbp_fill(int N, int n_angles, int nb, const int64_t* rowptr, int32_t* col, double* val, int nthreads) {
+  return gen_pixbp_fill_range(N, n_angles, nb, 0, (int64_t)N * N, rowptr, col, val, nthreads);
 }
 
 // y = M x for a CSR matrix (used only to form b = A x_true).

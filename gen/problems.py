@@ -55,6 +55,13 @@ def _get_lib():
         for nm in ("gen_siddon_fill", "gen_pixbp_fill"):
             getattr(lib, nm).argtypes = [ci, ci, ci, i64p, i32p, f64p, ci]
             getattr(lib, nm).restype = ci
+        i64 = ctypes.c_int64
+        for nm in ("gen_siddon_rownnz_range", "gen_pixbp_rownnz_range"):
+            getattr(lib, nm).argtypes = [ci, ci, ci, i64, i64, i64p, ci]
+            getattr(lib, nm).restype = ci
+        for nm in ("gen_siddon_fill_range", "gen_pixbp_fill_range"):
+            getattr(lib, nm).argtypes = [ci, ci, ci, i64, i64, i64p, i32p, f64p, ci]
+            getattr(lib, nm).restype = ci
         lib.gen_csr_matvec.argtypes = [ctypes.c_int64, i64p, i32p, f64p, f64p, f64p, ci]
         lib.gen_csr_matvec.restype = ci
         _lib = lib
@@ -141,6 +148,36 @@ def pixbp_csr(N: int, n_angles: int, nb: int, nthreads: int = 0) -> CSR:
                           _p(val, ctypes.c_double), nthreads) != 0:
         raise RuntimeError("gen_pixbp_fill failed")
     return CSR(n, n_angles * nb, rp, col, val)
+
+
+def _rows_block(kind, N, n_angles, nb, r0, r1, nthreads=0):
+    """Rows [r0, r1) of the Siddon A (kind 'siddon') or the pixel-driven B ('pixbp') as a
+    CSR block (local rowptr from 0, global columns) - the same rows make_problem builds."""
+    lib = _get_lib()
+    cnt = np.empty(r1 - r0, dtype=np.int64)
+    f_cnt = lib.gen_siddon_rownnz_range if kind == "siddon" else lib.gen_pixbp_rownnz_range
+    f_fill = lib.gen_siddon_fill_range if kind == "siddon" else lib.gen_pixbp_fill_range
+    if f_cnt(N, n_angles, nb, r0, r1, _p(cnt, ctypes.c_int64), nthreads) != 0:
+        raise RuntimeError("row count failed")
+    rp = _rowptr_from_counts(cnt)
+    col = np.empty(int(rp[-1]), dtype=np.int32)
+    val = np.empty(int(rp[-1]), dtype=np.float64)
+    if f_fill(N, n_angles, nb, r0, r1, _p(rp, ctypes.c_int64), _p(col, ctypes.c_int32), _p(val, ctypes.c_double),
+              nthreads) != 0:
+        raise RuntimeError("row fill failed")
+    ncols = N * N if kind == "siddon" else n_angles * nb
+    return CSR(r1 - r0, ncols, rp, col, val)
+
+
+def row_nnz(kind, N, n_angles, nb, nthreads=0):
+    """Nonzeros of every row (for the nnz-balanced partition) without storing the matrix."""
+    lib = _get_lib()
+    nrows = n_angles * nb if kind == "siddon" else N * N
+    cnt = np.empty(nrows, dtype=np.int64)
+    f = lib.gen_siddon_rownnz_range if kind == "siddon" else lib.gen_pixbp_rownnz_range
+    if f(N, n_angles, nb, 0, nrows, _p(cnt, ctypes.c_int64), nthreads) != 0:
+        raise RuntimeError("row count failed")
+    return cnt
 
 
 def ellipse_phantom(N: int, rng: np.random.Generator, n_ell: int = 10) -> np.ndarray:
@@ -315,3 +352,63 @@ def make_problem(config_index: int, N: Optional[int] = None, n_angles: Optional[
     return Problem(name=cfg["name"], config_index=config_index, m=m, n=n, A=A, T=T, t_mode=t_mode,
                    blur=blur, x_true=x_true, b=b, e=e, delta=cfg["delta"], delta_e=float(np.linalg.norm(e)),
                    sketch_seed=SKETCH_SEED_BASE + config_index, solvers=solvers, geometry=geometry)
+
+
+@dataclass
+class ShardProblem:
+    """One rank's share of a CT config: its A row block (and B row block), its slice
+    of b, and the global metadata (the multi-GPU bench)."""
+    name: str
+    config_index: int
+    m: int
+    n: int
+    a_rows: tuple
+    t_rows: Optional[tuple]
+    A_loc: CSR
+    T_loc: Optional[CSR]
+    t_mode: str
+    b_loc: np.ndarray
+    delta_e: float
+    sketch_seed: int
+    solvers: list
+
+
+def ct_row_nnz(config_index: int, nthreads: int = 0):
+    """Row lengths of A (and B when unmatched) for the nnz-balanced partition."""
+    cfg = CONFIGS[config_index]
+    a = row_nnz("siddon", cfg["N"], cfg["n_angles"], cfg["nb"], nthreads)
+    t = None if cfg["matched"] else row_nnz("pixbp", cfg["N"], cfg["n_angles"], cfg["nb"], nthreads)
+    return a, t
+
+
+def make_ct_shard(config_index: int, a_rows: tuple, t_rows: Optional[tuple], allreduce_sum,
+                  nthreads: int = 0) -> ShardProblem:
+    """The rows [a_rows) of A (and [t_rows) of B) of make_problem(config_index), and the
+    matching slice of b = A x_true + e.  The same seeded streams as make_problem;
+    ||A x_true|| is the allreduce of the ranks' partial squares (allreduce_sum(float))."""
+    cfg = CONFIGS[config_index]
+    if cfg["kind"] != "ct":
+        raise ValueError("sharded generation is for the CT configs")
+    N, na, nb = cfg["N"], cfg["n_angles"], cfg["nb"]
+    ss = np.random.SeedSequence(MASTER_SEED + config_index)
+    s_A, s_x, s_e = ss.spawn(3)
+    rx, re = (np.random.Generator(np.random.PCG64(s)) for s in (s_x, s_e))
+    m, n = na * nb, N * N
+    A_loc = _rows_block("siddon", N, na, nb, a_rows[0], a_rows[1], nthreads)
+    T_loc = None
+    t_mode = "build"
+    if not cfg["matched"]:
+        T_loc = _rows_block("pixbp", N, na, nb, t_rows[0], t_rows[1], nthreads)
+        t_mode = "given"
+    x_true = ellipse_phantom(N, rx)
+    Ax_loc = A_loc.matvec(x_true, nthreads)
+    norm_ax = float(np.sqrt(allreduce_sum(float(Ax_loc @ Ax_loc))))
+    g = re.standard_normal(m)
+    scale = cfg["delta"] * norm_ax / np.linalg.norm(g)
+    b_loc = Ax_loc + g[a_rows[0]:a_rows[1]] * scale
+    solvers = [SolverSpec(method=s[0], maxit=s[1], window=s[2], d=s[3], s_nz=s[4], precond=s[5], eta=s[6])
+               for s in cfg["solvers"]]
+    return ShardProblem(name=cfg["name"], config_index=config_index, m=m, n=n, a_rows=tuple(a_rows),
+                        t_rows=None if t_rows is None else tuple(t_rows), A_loc=A_loc, T_loc=T_loc, t_mode=t_mode,
+                        b_loc=b_loc, delta_e=cfg["delta"] * norm_ax, sketch_seed=SKETCH_SEED_BASE + config_index,
+                        solvers=solvers)
