@@ -61,13 +61,32 @@ void parallel_for(int64_t n, int nthreads, F f) {
   for (auto& t : th) t.join();
 }
 
+// Pixel vectorisation: tile == 0 -> row-major p = iy*N + ix; tile = T > 0 -> T x T tiles in
+// row-major tile order, row-major inside a tile (N % T == 0).  DESIGN.md reading R16.
+inline int pix_index(int N, int tile, int iy, int ix) {
+  if (tile <= 0) return iy * N + ix;
+  const int ty = iy / tile, tx = ix / tile, ntx = N / tile;
+  return ((ty * ntx + tx) * tile + (iy % tile)) * tile + (ix % tile);
+}
+inline void pix_coords(int N, int tile, int64_t p, int& iy, int& ix) {
+  if (tile <= 0) {
+    iy = (int)(p / N);
+    ix = (int)(p % N);
+    return;
+  }
+  const int64_t tt = (int64_t)tile * tile, ntx = N / tile;
+  const int64_t t = p / tt, r = p % tt;
+  iy = (int)((t / ntx) * tile + r / tile);
+  ix = (int)((t % ntx) * tile + r % tile);
+}
+
 struct Seg {
   int32_t col;
   double len;
 };
 
 // Siddon traversal of one ray; appends (pixel, length) in traversal order.
-void siddon_ray(int N, double theta, double t, std::vector<Seg>& out) {
+void siddon_ray(int N, int tile, double theta, double t, std::vector<Seg>& out) {
   out.clear();
   const double half = 0.5 * N;
   const double c = std::cos(theta), s = std::sin(theta);
@@ -124,7 +143,7 @@ void siddon_ray(int N, double theta, double t, std::vector<Seg>& out) {
       double mid = 0.5 * (aprev + acur);
       double xm = px + mid * dx, ym = py + mid * dy;
       int ix = (int)std::floor(xm + half), iy = (int)std::floor(ym + half);
-      if (ix >= 0 && ix < N && iy >= 0 && iy < N) out.push_back({iy * N + ix, len});
+      if (ix >= 0 && ix < N && iy >= 0 && iy < N) out.push_back({pix_index(N, tile, iy, ix), len});
     }
     if (acur >= amax) break;
     aprev = acur;
@@ -154,15 +173,15 @@ void canonicalise(std::vector<Seg>& v) {
 extern "C" {
 
 // Number of nonzeros per Siddon row r in [r0, r1) (row = a*nb + j) into row_nnz[r - r0].
-int gen_siddon_rownnz_range(int N, int n_angles, int nb, int64_t r0, int64_t r1, int64_t* row_nnz, int nthreads) {
-  if (N <= 0 || n_angles <= 0 || nb <= 0 || r0 < 0 || r1 < r0 || r1 > (int64_t)n_angles * nb) return -1;
+int gen_siddon_rownnz_range(int N, int tile, int n_angles, int nb, int64_t r0, int64_t r1, int64_t* row_nnz, int nthreads) {
+  if (N <= 0 || (tile > 0 && N % tile) || n_angles <= 0 || nb <= 0 || r0 < 0 || r1 < r0 || r1 > (int64_t)n_angles * nb) return -1;
   parallel_for(r1 - r0, nthreads, [&](int64_t q) {
     thread_local std::vector<Seg> buf;
     const int64_t r = r0 + q;
     int a = (int)(r / nb), j = (int)(r % nb);
     double theta = M_PI * (double)a / (double)n_angles;
     double t = (double)j - 0.5 * (double)(nb - 1);
-    siddon_ray(N, theta, t, buf);
+    siddon_ray(N, tile, theta, t, buf);
     canonicalise(buf);
     row_nnz[q] = (int64_t)buf.size();
   });
@@ -170,9 +189,9 @@ int gen_siddon_rownnz_range(int N, int n_angles, int nb, int64_t r0, int64_t r1,
 }
 
 // Fill col/val of rows [r0, r1) given rowptr (r1 - r0 + 1 entries, base rowptr[0]).
-int gen_siddon_fill_range(int N, int n_angles, int nb, int64_t r0, int64_t r1, const int64_t* rowptr, int32_t* col,
+int gen_siddon_fill_range(int N, int tile, int n_angles, int nb, int64_t r0, int64_t r1, const int64_t* rowptr, int32_t* col,
                           double* val, int nthreads) {
-  if (N <= 0 || n_angles <= 0 || nb <= 0 || r0 < 0 || r1 < r0 || r1 > (int64_t)n_angles * nb) return -1;
+  if (N <= 0 || (tile > 0 && N % tile) || n_angles <= 0 || nb <= 0 || r0 < 0 || r1 < r0 || r1 > (int64_t)n_angles * nb) return -1;
   std::atomic<int> bad(0);
   const int64_t base = rowptr[0];
   parallel_for(r1 - r0, nthreads, [&](int64_t q) {
@@ -181,7 +200,7 @@ int gen_siddon_fill_range(int N, int n_angles, int nb, int64_t r0, int64_t r1, c
     int a = (int)(r / nb), j = (int)(r % nb);
     double theta = M_PI * (double)a / (double)n_angles;
     double t = (double)j - 0.5 * (double)(nb - 1);
-    siddon_ray(N, theta, t, buf);
+    siddon_ray(N, tile, theta, t, buf);
     canonicalise(buf);
     int64_t s = rowptr[q] - base;
     if ((int64_t)buf.size() != rowptr[q + 1] - rowptr[q]) {
@@ -197,20 +216,21 @@ int gen_siddon_fill_range(int N, int n_angles, int nb, int64_t r0, int64_t r1, c
 }
 
 int gen_siddon_rownnz(int N, int n_angles, int nb, int64_t* row_nnz, int nthreads) {
-  return gen_siddon_rownnz_range(N, n_angles, nb, 0, (int64_t)n_angles * nb, row_nnz, nthreads);
+  return gen_siddon_rownnz_range(N, 0, n_angles, nb, 0, (int64_t)n_angles * nb, row_nnz, nthreads);
 }
 
 int gen_siddon_fill(int N, int n_angles, int nb, const int64_t* rowptr, int32_t* col, double* val, int nthreads) {
-  return gen_siddon_fill_range(N, n_angles, nb, 0, (int64_t)n_angles * nb, rowptr, col, val, nthreads);
+  return gen_siddon_fill_range(N, 0, n_angles, nb, 0, (int64_t)n_angles * nb, rowptr, col, val, nthreads);
 }
 
 // Pixel-driven linear-interpolation backprojector B (n x m), rows (pixels) [p0, p1).
-int gen_pixbp_rownnz_range(int N, int n_angles, int nb, int64_t p0, int64_t p1, int64_t* row_nnz, int nthreads) {
-  if (N <= 0 || n_angles <= 0 || nb <= 0 || p0 < 0 || p1 < p0 || p1 > (int64_t)N * N) return -1;
+int gen_pixbp_rownnz_range(int N, int tile, int n_angles, int nb, int64_t p0, int64_t p1, int64_t* row_nnz, int nthreads) {
+  if (N <= 0 || (tile > 0 && N % tile) || n_angles <= 0 || nb <= 0 || p0 < 0 || p1 < p0 || p1 > (int64_t)N * N) return -1;
   const double half = 0.5 * N, off = 0.5 * (nb - 1);
   parallel_for(p1 - p0, nthreads, [&](int64_t q) {
     const int64_t p = p0 + q;
-    int iy = (int)(p / N), ix = (int)(p % N);
+    int iy, ix;
+    pix_coords(N, tile, p, iy, ix);
     double x = ix + 0.5 - half, y = iy + 0.5 - half;
     int64_t cnt = 0;
     for (int a = 0; a < n_angles; ++a) {
@@ -225,15 +245,16 @@ int gen_pixbp_rownnz_range(int N, int n_angles, int nb, int64_t p0, int64_t p1, 
   return 0;
 }
 
-int gen_pixbp_fill_range(int N, int n_angles, int nb, int64_t p0, int64_t p1, const int64_t* rowptr, int32_t* col,
+int gen_pixbp_fill_range(int N, int tile, int n_angles, int nb, int64_t p0, int64_t p1, const int64_t* rowptr, int32_t* col,
                          double* val, int nthreads) {
-  if (N <= 0 || n_angles <= 0 || nb <= 0 || p0 < 0 || p1 < p0 || p1 > (int64_t)N * N) return -1;
+  if (N <= 0 || (tile > 0 && N % tile) || n_angles <= 0 || nb <= 0 || p0 < 0 || p1 < p0 || p1 > (int64_t)N * N) return -1;
   const double half = 0.5 * N, off = 0.5 * (nb - 1);
   const int64_t base = rowptr[0];
   std::atomic<int> bad(0);
   parallel_for(p1 - p0, nthreads, [&](int64_t q) {
     const int64_t p = p0 + q;
-    int iy = (int)(p / N), ix = (int)(p % N);
+    int iy, ix;
+    pix_coords(N, tile, p, iy, ix);
     double x = ix + 0.5 - half, y = iy + 0.5 - half;
     int64_t k = rowptr[q] - base;
     for (int a = 0; a < n_angles; ++a) {
@@ -259,11 +280,11 @@ int gen_pixbp_fill_range(int N, int n_angles, int nb, int64_t p0, int64_t p1, co
 }
 
 int gen_pixbp_rownnz(int N, int n_angles, int nb, int64_t* row_nnz, int nthreads) {
-  return gen_pixbp_rownnz_range(N, n_angles, nb, 0, (int64_t)N * N, row_nnz, nthreads);
+  return gen_pixbp_rownnz_range(N, 0, n_angles, nb, 0, (int64_t)N * N, row_nnz, nthreads);
 }
 
 int gen_pixbp_fill(int N, int n_angles, int nb, const int64_t* rowptr, int32_t* col, double* val, int nthreads) {
-  return gen_pixbp_fill_range(N, n_angles, nb, 0, (int64_t)N * N, rowptr, col, val, nthreads);
+  return gen_pixbp_fill_range(N, 0, n_angles, nb, 0, (int64_t)N * N, rowptr, col, val, nthreads);
 }
 
 // y = M x for a CSR matrix (used only to form b = A x_true).

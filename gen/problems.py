@@ -57,10 +57,10 @@ def _get_lib():
             getattr(lib, nm).restype = ci
         i64 = ctypes.c_int64
         for nm in ("gen_siddon_rownnz_range", "gen_pixbp_rownnz_range"):
-            getattr(lib, nm).argtypes = [ci, ci, ci, i64, i64, i64p, ci]
+            getattr(lib, nm).argtypes = [ci, ci, ci, ci, i64, i64, i64p, ci]
             getattr(lib, nm).restype = ci
         for nm in ("gen_siddon_fill_range", "gen_pixbp_fill_range"):
-            getattr(lib, nm).argtypes = [ci, ci, ci, i64, i64, i64p, i32p, f64p, ci]
+            getattr(lib, nm).argtypes = [ci, ci, ci, ci, i64, i64, i64p, i32p, f64p, ci]
             getattr(lib, nm).restype = ci
         lib.gen_csr_matvec.argtypes = [ctypes.c_int64, i64p, i32p, f64p, f64p, f64p, ci]
         lib.gen_csr_matvec.restype = ci
@@ -116,68 +116,57 @@ def _rowptr_from_counts(cnt: np.ndarray) -> np.ndarray:
     return rp
 
 
-def siddon_csr(N: int, n_angles: int, nb: int, nthreads: int = 0) -> CSR:
-    """Siddon ray-pixel intersection-length matrix, m = n_angles*nb rows, n = N*N columns."""
-    lib = _get_lib()
-    m = n_angles * nb
-    cnt = np.empty(m, dtype=np.int64)
-    if lib.gen_siddon_rownnz(N, n_angles, nb, _p(cnt, ctypes.c_int64), nthreads) != 0:
-        raise RuntimeError("gen_siddon_rownnz failed")
-    rp = _rowptr_from_counts(cnt)
-    nnz = int(rp[-1])
-    col = np.empty(nnz, dtype=np.int32)
-    val = np.empty(nnz, dtype=np.float64)
-    if lib.gen_siddon_fill(N, n_angles, nb, _p(rp, ctypes.c_int64), _p(col, ctypes.c_int32),
-                           _p(val, ctypes.c_double), nthreads) != 0:
-        raise RuntimeError("gen_siddon_fill failed")
-    return CSR(m, N * N, rp, col, val)
+def siddon_csr(N: int, n_angles: int, nb: int, nthreads: int = 0, tile: int = 0) -> CSR:
+    """Siddon ray-pixel intersection-length matrix, m = n_angles*nb rows, n = N*N columns
+    (pixel order: row-major, or tile x tile tiles when tile > 0; reading R16)."""
+    return _rows_block("siddon", N, n_angles, nb, 0, n_angles * nb, nthreads, tile)
 
 
-def pixbp_csr(N: int, n_angles: int, nb: int, nthreads: int = 0) -> CSR:
+def pixbp_csr(N: int, n_angles: int, nb: int, nthreads: int = 0, tile: int = 0) -> CSR:
     """Pixel-driven linear-interpolation backprojector B (n x m), B ~ A^T but unmatched."""
-    lib = _get_lib()
-    n = N * N
-    cnt = np.empty(n, dtype=np.int64)
-    if lib.gen_pixbp_rownnz(N, n_angles, nb, _p(cnt, ctypes.c_int64), nthreads) != 0:
-        raise RuntimeError("gen_pixbp_rownnz failed")
-    rp = _rowptr_from_counts(cnt)
-    nnz = int(rp[-1])
-    col = np.empty(nnz, dtype=np.int32)
-    val = np.empty(nnz, dtype=np.float64)
-    if lib.gen_pixbp_fill(N, n_angles, nb, _p(rp, ctypes.c_int64), _p(col, ctypes.c_int32),
-                          _p(val, ctypes.c_double), nthreads) != 0:
-        raise RuntimeError("gen_pixbp_fill failed")
-    return CSR(n, n_angles * nb, rp, col, val)
+    return _rows_block("pixbp", N, n_angles, nb, 0, N * N, nthreads, tile)
 
 
-def _rows_block(kind, N, n_angles, nb, r0, r1, nthreads=0):
+def _rows_block(kind, N, n_angles, nb, r0, r1, nthreads=0, tile=0):
     """Rows [r0, r1) of the Siddon A (kind 'siddon') or the pixel-driven B ('pixbp') as a
     CSR block (local rowptr from 0, global columns) - the same rows make_problem builds."""
     lib = _get_lib()
     cnt = np.empty(r1 - r0, dtype=np.int64)
     f_cnt = lib.gen_siddon_rownnz_range if kind == "siddon" else lib.gen_pixbp_rownnz_range
     f_fill = lib.gen_siddon_fill_range if kind == "siddon" else lib.gen_pixbp_fill_range
-    if f_cnt(N, n_angles, nb, r0, r1, _p(cnt, ctypes.c_int64), nthreads) != 0:
+    if f_cnt(N, tile, n_angles, nb, r0, r1, _p(cnt, ctypes.c_int64), nthreads) != 0:
         raise RuntimeError("row count failed")
     rp = _rowptr_from_counts(cnt)
     col = np.empty(int(rp[-1]), dtype=np.int32)
     val = np.empty(int(rp[-1]), dtype=np.float64)
-    if f_fill(N, n_angles, nb, r0, r1, _p(rp, ctypes.c_int64), _p(col, ctypes.c_int32), _p(val, ctypes.c_double),
-              nthreads) != 0:
+    if f_fill(N, tile, n_angles, nb, r0, r1, _p(rp, ctypes.c_int64), _p(col, ctypes.c_int32),
+              _p(val, ctypes.c_double), nthreads) != 0:
         raise RuntimeError("row fill failed")
     ncols = N * N if kind == "siddon" else n_angles * nb
     return CSR(r1 - r0, ncols, rp, col, val)
 
 
-def row_nnz(kind, N, n_angles, nb, nthreads=0):
+def row_nnz(kind, N, n_angles, nb, nthreads=0, tile=0):
     """Nonzeros of every row (for the nnz-balanced partition) without storing the matrix."""
     lib = _get_lib()
     nrows = n_angles * nb if kind == "siddon" else N * N
     cnt = np.empty(nrows, dtype=np.int64)
     f = lib.gen_siddon_rownnz_range if kind == "siddon" else lib.gen_pixbp_rownnz_range
-    if f(N, n_angles, nb, 0, nrows, _p(cnt, ctypes.c_int64), nthreads) != 0:
+    if f(N, tile, n_angles, nb, 0, nrows, _p(cnt, ctypes.c_int64), nthreads) != 0:
         raise RuntimeError("row count failed")
     return cnt
+
+
+def tiled_order(N: int, tile: int) -> np.ndarray:
+    """perm with x_tiled = x_rowmajor[perm] (tile x tile tiles, row-major tiles and interior)."""
+    if tile <= 0:
+        return np.arange(N * N)
+    p = np.arange(N * N)
+    tt, ntx = tile * tile, N // tile
+    t, r = np.divmod(p, tt)
+    iy = (t // ntx) * tile + r // tile
+    ix = (t % ntx) * tile + r % tile
+    return iy * N + ix
 
 
 def ellipse_phantom(N: int, rng: np.random.Generator, n_ell: int = 10) -> np.ndarray:
@@ -283,11 +272,11 @@ CONFIGS = {
             solvers=[("sflsqr", 40, 2, 80, 4, "irn", 1.01), ("sflsmr", 40, 2, 80, 4, "irn", 1.01)]),
     2: dict(name="c2_blur256", kind="blur", N=256, sigma=2.5, radius=7, delta=0.01,
             solvers=[("sflsqr", 100, 3, 200, 8, "irn", 0.0)]),
-    3: dict(name="c3_ct512", kind="ct", N=512, n_angles=360, nb=725, delta=0.02, matched=True,
+    3: dict(name="c3_ct512", kind="ct", N=512, n_angles=360, nb=725, delta=0.02, matched=True, tile=4,
             solvers=[("sflsqr", 150, 3, 300, 8, "nonneg", 0.0), ("sflsmr", 150, 3, 300, 8, "nonneg", 0.0)]),
-    4: dict(name="c4_ct1024_unmatched", kind="ct", N=1024, n_angles=720, nb=1449, delta=0.01, matched=False,
+    4: dict(name="c4_ct1024_unmatched", kind="ct", N=1024, n_angles=720, nb=1449, delta=0.01, matched=False, tile=4,
             solvers=[("sflsqr", 200, 4, 400, 8, "identity", 0.0)]),
-    5: dict(name="c5_ct2048", kind="ct", N=2048, n_angles=1440, nb=2897, delta=0.01, matched=True,
+    5: dict(name="c5_ct2048", kind="ct", N=2048, n_angles=1440, nb=2897, delta=0.01, matched=True, tile=4,
             solvers=[("sflsqr", 300, 5, 600, 8, "irn", 0.0), ("sflsmr", 300, 5, 600, 8, "irn", 0.0)]),
 }
 
@@ -332,15 +321,16 @@ def make_problem(config_index: int, N: Optional[int] = None, n_angles: Optional[
         Nimg = N or cfg["N"]
         na = n_angles or cfg["n_angles"]
         nbins = nb or cfg["nb"]
-        A = siddon_csr(Nimg, na, nbins, nthreads)
+        tile = cfg.get("tile", 0) if Nimg % max(cfg.get("tile", 1), 1) == 0 else 0
+        A = siddon_csr(Nimg, na, nbins, nthreads, tile)
         if cfg["matched"]:
             t_mode = "build"
         else:
-            T = pixbp_csr(Nimg, na, nbins, nthreads)
+            T = pixbp_csr(Nimg, na, nbins, nthreads, tile)
             t_mode = "given"
         m, n = A.nrows, A.ncols
-        x_true = ellipse_phantom(Nimg, rx)
-        geometry = dict(N=Nimg, n_angles=na, nb=nbins)
+        x_true = ellipse_phantom(Nimg, rx)[tiled_order(Nimg, tile)]
+        geometry = dict(N=Nimg, n_angles=na, nb=nbins, tile=tile)
         Ax = A.matvec(x_true, nthreads)
     else:
         raise ValueError(kind)
@@ -376,8 +366,9 @@ class ShardProblem:
 def ct_row_nnz(config_index: int, nthreads: int = 0):
     """Row lengths of A (and B when unmatched) for the nnz-balanced partition."""
     cfg = CONFIGS[config_index]
-    a = row_nnz("siddon", cfg["N"], cfg["n_angles"], cfg["nb"], nthreads)
-    t = None if cfg["matched"] else row_nnz("pixbp", cfg["N"], cfg["n_angles"], cfg["nb"], nthreads)
+    tile = cfg.get("tile", 0)
+    a = row_nnz("siddon", cfg["N"], cfg["n_angles"], cfg["nb"], nthreads, tile)
+    t = None if cfg["matched"] else row_nnz("pixbp", cfg["N"], cfg["n_angles"], cfg["nb"], nthreads, tile)
     return a, t
 
 
@@ -394,13 +385,14 @@ def make_ct_shard(config_index: int, a_rows: tuple, t_rows: Optional[tuple], all
     s_A, s_x, s_e = ss.spawn(3)
     rx, re = (np.random.Generator(np.random.PCG64(s)) for s in (s_x, s_e))
     m, n = na * nb, N * N
-    A_loc = _rows_block("siddon", N, na, nb, a_rows[0], a_rows[1], nthreads)
+    tile = cfg.get("tile", 0)
+    A_loc = _rows_block("siddon", N, na, nb, a_rows[0], a_rows[1], nthreads, tile)
     T_loc = None
     t_mode = "build"
     if not cfg["matched"]:
-        T_loc = _rows_block("pixbp", N, na, nb, t_rows[0], t_rows[1], nthreads)
+        T_loc = _rows_block("pixbp", N, na, nb, t_rows[0], t_rows[1], nthreads, tile)
         t_mode = "given"
-    x_true = ellipse_phantom(N, rx)
+    x_true = ellipse_phantom(N, rx)[tiled_order(N, tile)]
     Ax_loc = A_loc.matvec(x_true, nthreads)
     norm_ax = float(np.sqrt(allreduce_sum(float(Ax_loc @ Ax_loc))))
     g = re.standard_normal(m)

@@ -421,16 +421,30 @@ int enqueue_iteration(sflsqr_t* h) {
   const int k = h->host_k;  // used only for the byte model
   const double n8 = 8.0 * h->n_loc, m8 = 8.0 * h->m_loc;
   int rc;
-  // a1: z-side windowed MGS (ell + 1 passes; passes beyond the window exit early)
-  for (int pass = 0; pass <= P.ell; ++pass) {
-    const int J = std::min(P.ell, k - 1);
-    const double by = pass > J ? 0.0 : n8 * (1 + (pass > 0) * 2 + (pass < J));
+  // a1: z-side windowed orthogonalisation
+  if (P.fused) {
     {
-      Launch L(h, SFLSQR_KC_ORTH, by);
-      k_mgs_pass<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P, 0, pass);
+      Launch L(h, SFLSQR_KC_ORTH, n8 * (1 + std::min(P.ell, k - 1)));
+      k_orth_dots<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P, 0);
     }
-    if (pass == 0 && (rc = reduce_slots(h, P.slot_zin, 1, false))) return rc;
-    if ((rc = reduce_slots(h, P.slot_z0 + pass, 1, false))) return rc;
+    if ((rc = coll_allreduce(h, P.scal + P.slot_zf, kFuseAcc, false))) return rc;
+    {
+      Launch L(h, SFLSQR_KC_ORTH, n8 * (2 + std::min(P.ell, k - 1)));
+      k_orth_axpy<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P, 0);
+    }
+    if ((rc = coll_allreduce(h, P.scal + P.slot_zout, 1, false))) return rc;
+  } else {
+    // literal MGS, one pass per window vector (ell + 1 passes; passes beyond the window exit early)
+    for (int pass = 0; pass <= P.ell; ++pass) {
+      const int J = std::min(P.ell, k - 1);
+      const double by = pass > J ? 0.0 : n8 * (1 + (pass > 0) * 2 + (pass < J));
+      {
+        Launch L(h, SFLSQR_KC_ORTH, by);
+        k_mgs_pass<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P, 0, pass);
+      }
+      if (pass == 0 && (rc = reduce_slots(h, P.slot_zin, 1, false))) return rc;
+      if ((rc = reduce_slots(h, P.slot_z0 + pass, 1, false))) return rc;
+    }
   }
   // a1 end + a2: normalise, tau, store z_k
   {
@@ -448,16 +462,29 @@ int enqueue_iteration(sflsqr_t* h) {
   }
   // a4 (sFLSQR): S_AZ[:, k] = S w
   if (P.method == SFLSQR_METHOD_SFLSQR && (rc = enqueue_sketch(h, P.st, P.w))) return rc;
-  // a5: w-side windowed MGS (ell + 2 passes) and normalisation
-  for (int pass = 0; pass <= P.ell + 1; ++pass) {
-    const int J = std::min(P.ell + 1, k);
-    const double by = pass > J ? 0.0 : m8 * (1 + (pass > 0) * 2 + (pass < J));
+  // a5: w-side windowed orthogonalisation and normalisation
+  if (P.fused) {
     {
-      Launch L(h, SFLSQR_KC_ORTH, by);
-      k_mgs_pass<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P, 1, pass);
+      Launch L(h, SFLSQR_KC_ORTH, m8 * (1 + std::min(P.ell + 1, k)));
+      k_orth_dots<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P, 1);
     }
-    if (pass == 0 && (rc = reduce_slots(h, P.slot_win, 1, false))) return rc;
-    if ((rc = reduce_slots(h, P.slot_w0 + pass, 1, false))) return rc;
+    if ((rc = coll_allreduce(h, P.scal + P.slot_wf, kFuseAcc, false))) return rc;
+    {
+      Launch L(h, SFLSQR_KC_ORTH, m8 * (2 + std::min(P.ell + 1, k)));
+      k_orth_axpy<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P, 1);
+    }
+    if ((rc = coll_allreduce(h, P.scal + P.slot_wout, 1, false))) return rc;
+  } else {
+    for (int pass = 0; pass <= P.ell + 1; ++pass) {
+      const int J = std::min(P.ell + 1, k);
+      const double by = pass > J ? 0.0 : m8 * (1 + (pass > 0) * 2 + (pass < J));
+      {
+        Launch L(h, SFLSQR_KC_ORTH, by);
+        k_mgs_pass<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P, 1, pass);
+      }
+      if (pass == 0 && (rc = reduce_slots(h, P.slot_win, 1, false))) return rc;
+      if ((rc = reduce_slots(h, P.slot_w0 + pass, 1, false))) return rc;
+    }
   }
   {
     Launch L(h, SFLSQR_KC_ORTH, 2 * m8);
@@ -470,7 +497,12 @@ int enqueue_iteration(sflsqr_t* h) {
   // a7: projected sketched LS (replicated on every rank: identical inputs)
   {
     Launch L(h, SFLSQR_KC_LS, 8.0 * P.d * (k + 2));
-    k_ls<<<1, kLsThreads, 0, h->stream>>>(P);
+    if (P.d <= kLsThreads)
+      k_ls<1><<<1, kLsThreads, 3 * 1 * kLsThreads * sizeof(double), h->stream>>>(P);
+    else if (P.d <= 2 * kLsThreads)
+      k_ls<2><<<1, kLsThreads, 3 * 2 * kLsThreads * sizeof(double), h->stream>>>(P);
+    else
+      k_ls<4><<<1, kLsThreads, 3 * 4 * kLsThreads * sizeof(double), h->stream>>>(P);
   }
   // a8: x_k = Z_k y_k (needed by tau_{k+1})
   if (P.need_x) {
@@ -478,7 +510,7 @@ int enqueue_iteration(sflsqr_t* h) {
       Launch L(h, SFLSQR_KC_XUPD, n8 * (k + 1));
       k_xupdate<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P, 0);
     }
-    if ((rc = reduce_slots(h, P.slot_xmax, 1, true))) return rc;
+    if ((rc = coll_allreduce(h, P.scal + P.slot_xmax, 1, true))) return rc;
   }
   // a9: true residual (W path) and stop tests
   if (P.want_res) {
@@ -486,7 +518,7 @@ int enqueue_iteration(sflsqr_t* h) {
       Launch L(h, SFLSQR_KC_RES, m8 * (k + 1));
       k_res_partial<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P);
     }
-    if ((rc = reduce_slots(h, P.slot_res, 1, false))) return rc;
+    if ((rc = coll_allreduce(h, P.scal + P.slot_res, 1, false))) return rc;
   }
   {
     Launch L(h, SFLSQR_KC_STOP, 0.0);
@@ -590,6 +622,13 @@ int alloc_solve(sflsqr_t* h) {
   s += ell + 2;
   P.slot_xmax = s++;
   P.slot_res = s++;
+  P.fused = (ell + 1 <= kFuseJ) ? 1 : 0;
+  P.slot_zf = s;
+  s += kFuseAcc;
+  P.slot_zout = s++;
+  P.slot_wf = s;
+  s += kFuseAcc;
+  P.slot_wout = s++;
   h->nslots = s;
   auto A = [&](double** p, size_t count) {
     return dalloc(h, (void**)p, count * sizeof(double), &h->solve_allocs, &h->solve_sizes);
@@ -599,12 +638,14 @@ int alloc_solve(sflsqr_t* h) {
   // z receives the reduce-scatter (n_max) when sharded by columns
   const size_t zlen = std::max<size_t>(n, (size_t)h->n_max);
   if ((rc = dalloc(h, (void**)&P.st, sizeof(DevState), &h->solve_allocs, &h->solve_sizes))) return rc;
+  if ((rc = dalloc(h, (void**)&P.ctr, sizeof(int) * CTR_COUNT, &h->solve_allocs, &h->solve_sizes))) return rc;
   if ((rc = A(&P.z, zlen)) || (rc = A(&P.x, n)) || (rc = A(&P.Z, n * maxit)) || (rc = A(&P.w, m)) ||
       (rc = A(&P.W, m * (maxit + 1))) || (rc = A(&P.b, m)) || (rc = A(&P.H, (size_t)(maxit + 1) * maxit)) ||
       (rc = A(&P.Tm, (size_t)maxit * maxit)) || (rc = A(&P.part, (size_t)s * kVecBlocks)) ||
       (rc = A(&P.scal, (size_t)s)) || (rc = A(&P.skbuf, d)) || (rc = A(&P.rhs, d)) ||
       (rc = A(&P.Mcols, (size_t)d * maxit)) || (rc = A(&P.STW, (size_t)d * (maxit + 1))) ||
       (rc = A(&P.V, (size_t)d * maxit)) || (rc = A(&P.taus, maxit)) || (rc = A(&P.R, (size_t)maxit * maxit)) ||
+      (rc = A(&P.Tw, (size_t)maxit * maxit)) ||
       (rc = A(&P.qtb, d)) || (rc = A(&P.y, maxit)) || (rc = A(&P.g, maxit + 1)) || (rc = A(&P.hist_true, maxit)) ||
       (rc = A(&P.hist_sk, maxit)))
     return rc;
@@ -622,8 +663,10 @@ int alloc_solve(sflsqr_t* h) {
   const char* poison = std::getenv("SFLSQR_DEBUG_POISON");
   if (poison && poison[0] == '1') {
     for (size_t i = 0; i < h->solve_allocs.size(); ++i)
-      if (h->solve_allocs[i] != (void*)P.st) CU(h, cudaMemset(h->solve_allocs[i], 0xFF, h->solve_sizes[i]));
+      if (h->solve_allocs[i] != (void*)P.st && h->solve_allocs[i] != (void*)P.ctr)
+        CU(h, cudaMemset(h->solve_allocs[i], 0xFF, h->solve_sizes[i]));
   }
+  CU(h, cudaMemset(P.ctr, 0, sizeof(int) * CTR_COUNT));
   // the padded send buffers' tails are never written
   if (P.zsend) CU(h, cudaMemset(P.zsend, 0, sizeof(double) * h->n_max));
   if (P.wsend) CU(h, cudaMemset(P.wsend, 0, sizeof(double) * h->m_max));
@@ -640,6 +683,7 @@ int zero_solve_state(sflsqr_t* h) {
   CU(h, cudaMemsetAsync(P.H, 0, sizeof(double) * (size_t)(maxit + 1) * maxit, s));
   CU(h, cudaMemsetAsync(P.Tm, 0, sizeof(double) * (size_t)maxit * maxit, s));
   CU(h, cudaMemsetAsync(P.R, 0, sizeof(double) * (size_t)maxit * maxit, s));
+  CU(h, cudaMemsetAsync(P.Tw, 0, sizeof(double) * (size_t)maxit * maxit, s));
   CU(h, cudaMemsetAsync(P.V, 0, sizeof(double) * (size_t)d * maxit, s));
   CU(h, cudaMemsetAsync(P.Mcols, 0, sizeof(double) * (size_t)d * maxit, s));
   CU(h, cudaMemsetAsync(P.STW, 0, sizeof(double) * (size_t)d * (maxit + 1), s));
@@ -800,6 +844,8 @@ int sflsqr_create(sflsqr_t** out, const sflsqr_opts* o) {
     }
   }
   if (const char* ev = std::getenv("SFLSQR_SPMV_MODE")) h->spmv_mode = std::atoi(ev);
+  cudaFuncSetAttribute(k_ls<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 4 * kLsThreads * (int)sizeof(double));
+  cudaGetLastError();
   *out = h;
   return SFLSQR_OK;
 }
@@ -1081,20 +1127,12 @@ int sflsqr_set_rhs(sflsqr_t* h, const double* b, int64_t len, int32_t mem_flags)
     Launch L(h, SFLSQR_KC_ORTH, 8.0 * h->m_loc);
     k_norm_partial<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P, P.b, h->m_loc, P.slot_beta);
   }
-  if ((rc = reduce_slots(h, P.slot_beta, 1, false))) return rc;
+  if ((rc = coll_allreduce(h, P.scal + P.slot_beta, 1, false))) return rc;
   {
     // ||b|| = 0 / non-finite check before dividing (every rank takes the same decision)
     double beta2 = 0.0;
-    if (h->world > 1) {
-      CU(h, cudaMemcpyAsync(&beta2, P.scal + P.slot_beta, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-      CU(h, cudaStreamSynchronize(h->stream));
-    } else {
-      std::vector<double> parts(kVecBlocks);
-      CU(h, cudaMemcpyAsync(parts.data(), P.part + (size_t)P.slot_beta * kVecBlocks, sizeof(double) * kVecBlocks,
-                            cudaMemcpyDeviceToHost, h->stream));
-      CU(h, cudaStreamSynchronize(h->stream));
-      for (double v : parts) beta2 += v;
-    }
+    CU(h, cudaMemcpyAsync(&beta2, P.scal + P.slot_beta, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CU(h, cudaStreamSynchronize(h->stream));
     if (!std::isfinite(beta2)) return fail(h, SFLSQR_E_NONFINITE, "b has a non-finite entry");
     if (!(beta2 > 0.0)) return fail(h, SFLSQR_E_ZERO_RHS, "||b|| = 0");
   }

@@ -18,6 +18,9 @@ constexpr int kSkThreads = 256;           // sketch kernel: 8 warps, one d-bin s
 constexpr int kSkBlocks = 148 * 2;
 constexpr int kLsThreads = 512;           // one CTA solves the projected problem
 constexpr int kMaxD = 2048;               // sketch rows supported by the one-CTA LS
+constexpr int kFuseJ = 6;                 // fused orthogonalisation for windows of up to 6 vectors
+constexpr int kFuseAcc = 1 + kFuseJ + kFuseJ * (kFuseJ - 1) / 2;  // ||v||^2, dots, Gram pairs
+enum CounterIdx { CTR_BETA = 0, CTR_ZDOTS, CTR_ZAXPY, CTR_WDOTS, CTR_WAXPY, CTR_XMAX, CTR_RES, CTR_COUNT };
 
 // Device-resident solve state (read by every kernel of a captured iteration).
 struct DevState {
@@ -53,12 +56,15 @@ struct Params {
   // partial sums: nslots x kVecBlocks
   double* part;
   int slot_zin, slot_z0, slot_win, slot_w0, slot_xmax, slot_res, slot_beta;
+  int fused;               // window of <= kFuseJ vectors: one-pass dots + Gram, then one axpy pass
+  int slot_zf, slot_zout, slot_wf, slot_wout;  // fused orthogonalisation slots (kFuseAcc + 1 per side)
+  int* ctr;                // last-block arrival counters (one per reduction site)
   // sketch
   int64_t* sk_rp;          // S stored transposed: d+1 row pointers
   uint32_t* sk_ent;         // coordinate | sign << 31, s * dim entries
   double *rhs, *Mcols, *STW;
   // projected LS
-  double *V, *taus, *R, *qtb, *y, *g;
+  double *V, *taus, *R, *Tw, *qtb, *y, *g;   // Tw: compact-WY factor (maxit x maxit)
   // history
   double *hist_true, *hist_sk;
 };
@@ -120,6 +126,11 @@ __device__ __forceinline__ double max_partials(const double* part, int nb, doubl
   return block_max<NT>(v, sh);
 }
 
+// Last-block reduction: every block has written part[(s0+t)*kVecBlocks + blockIdx.x]
+// for t < ns; the last block to arrive (threadfence + arrival counter, no waiting)
+// sums them in block order into scal[s0+t] (deterministic) and resets the counter.
+__device__ __forceinline__ void last_block_reduce(const Params& P, int s0, int ns, int ctr_idx, bool is_max);
+
 // A reduced quantity of slot `slot`: single rank -> sum the per-block partials in
 // block order here; several ranks -> the allreduced scalar (k_reduce_slots + comm).
 template <int NT>
@@ -136,6 +147,29 @@ template <int NT>
 __device__ __forceinline__ double get_max(const Params& P, int slot, double* sh, int nb) {
   if (P.dist) return P.scal[slot];
   return max_partials<NT>(P.part + (size_t)slot * nb, nb, sh);
+}
+
+__device__ __forceinline__ void last_block_reduce(const Params& P, int s0, int ns, int ctr_idx, bool is_max) {
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(P.ctr + ctr_idx, 1) == (int)gridDim.x - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int nb = gridDim.x;
+  for (int t = wid; t < ns; t += nw) {
+    const double* pp = P.part + (size_t)(s0 + t) * kVecBlocks;
+    double acc = is_max ? -INFINITY : 0.0;
+    for (int b = lane; b < nb; b += 32) {
+      const double v = __ldcg(pp + b);
+      acc = is_max ? fmax(acc, v) : acc + v;
+    }
+    acc = is_max ? warp_max(acc) : warp_sum(acc);
+    if (lane == 0) P.scal[s0 + t] = acc;
+  }
+  if (threadIdx.x == 0) P.ctr[ctr_idx] = 0;
 }
 
 // Streaming (read-once) loads: bypass L1 allocation so L1 keeps the gathered vector.
@@ -482,10 +516,10 @@ __global__ void __launch_bounds__(kVecThreads) k_norm_partial(Params P, const do
     acc = fma(v[i], v[i], acc);
   acc = block_sum<kVecThreads>(acc, sh);
   if (threadIdx.x == 0) P.part[(size_t)slot * kVecBlocks + blockIdx.x] = acc;
+  last_block_reduce(P, slot, 1, CTR_BETA, false);
 }
 __global__ void __launch_bounds__(kVecThreads) k_init_w1(Params P) {
-  __shared__ double sh[33];
-  const double beta = sqrt(get_sum<kVecThreads>(P, P.slot_beta, sh, kVecBlocks));
+  const double beta = sqrt(P.scal[P.slot_beta]);
   if (blockIdx.x == 0 && threadIdx.x == 0) P.st->beta = beta;
   for (int64_t i = (int64_t)blockIdx.x * kVecThreads + threadIdx.x; i < P.m; i += (int64_t)gridDim.x * kVecThreads) {
     const double w1 = P.b[i] / beta;
@@ -555,6 +589,108 @@ __global__ void __launch_bounds__(kVecThreads) k_mgs_pass(Params P, int side, in
   }
 }
 
+// Fused windowed orthogonalisation (windows of <= kFuseJ vectors).  One pass
+// reads v and the J window vectors once and accumulates ||v||^2, the dots
+// d_j = <q_j, v> and the window Gram matrix G_ij = <q_i, q_j> (i < j); the second
+// pass applies v -= sum_j c_j q_j (in window order) with the MGS coefficients
+// c_j = d_j - sum_{i<j} c_i G_ij — exactly the coefficients of the literal MGS
+// loop (Alg. 1 L464-467 / L476-480) in exact arithmetic — and accumulates ||v||^2.
+template <int JM>
+__device__ __forceinline__ int gram_idx(int i, int j) { return 1 + JM + j * (j - 1) / 2 + i; }
+
+__global__ void __launch_bounds__(kVecThreads) k_orth_dots(Params P, int side) {
+  __shared__ double red[kVecThreads / 32][kFuseAcc + 1];
+  const DevState* st = P.st;
+  if (st->done) return;
+  const int k = st->k;
+  const int J = side == 0 ? min(P.ell, k - 1) : min(P.ell + 1, k);
+  const int j0 = max(1, k - P.ell);
+  const double* __restrict__ v = side == 0 ? P.z : P.w;
+  const int64_t len = side == 0 ? P.n : P.m;
+  const int base = side == 0 ? P.slot_zf : P.slot_wf;
+  const double* q[kFuseJ];
+#pragma unroll
+  for (int j = 0; j < kFuseJ; ++j) q[j] = j < J ? mgs_basis(P, side, j0 + j) : nullptr;
+  double acc[kFuseAcc];
+#pragma unroll
+  for (int a = 0; a < kFuseAcc; ++a) acc[a] = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * kVecThreads + threadIdx.x; i < len; i += (int64_t)gridDim.x * kVecThreads) {
+    const double vi = v[i];
+    acc[0] = fma(vi, vi, acc[0]);
+    double qv[kFuseJ];
+#pragma unroll
+    for (int j = 0; j < kFuseJ; ++j) {
+      qv[j] = j < J ? q[j][i] : 0.0;
+      acc[1 + j] = fma(qv[j], vi, acc[1 + j]);
+    }
+#pragma unroll
+    for (int j = 1; j < kFuseJ; ++j)
+#pragma unroll
+      for (int i2 = 0; i2 < j; ++i2) acc[gram_idx<kFuseJ>(i2, j)] = fma(qv[i2], qv[j], acc[gram_idx<kFuseJ>(i2, j)]);
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int a = 0; a < kFuseAcc; ++a) {
+    const double t = warp_sum(acc[a]);
+    if (lane == 0) red[wid][a] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x < kFuseAcc) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < kVecThreads / 32; ++w) t += red[w][threadIdx.x];
+    P.part[(size_t)(base + threadIdx.x) * kVecBlocks + blockIdx.x] = t;
+  }
+  last_block_reduce(P, base, kFuseAcc, side == 0 ? CTR_ZDOTS : CTR_WDOTS, false);
+}
+
+__global__ void __launch_bounds__(kVecThreads) k_orth_axpy(Params P, int side) {
+  __shared__ double sh[33];
+  const DevState* st = P.st;
+  if (st->done) return;
+  const int k = st->k;
+  const int J = side == 0 ? min(P.ell, k - 1) : min(P.ell + 1, k);
+  const int j0 = max(1, k - P.ell);
+  double* __restrict__ v = side == 0 ? P.z : P.w;
+  const int64_t len = side == 0 ? P.n : P.m;
+  const int base = side == 0 ? P.slot_zf : P.slot_wf;
+  const double* q[kFuseJ];
+  double c[kFuseJ];
+#pragma unroll
+  for (int j = 0; j < kFuseJ; ++j) {
+    q[j] = j < J ? mgs_basis(P, side, j0 + j) : nullptr;
+    double cj = 0.0;
+    if (j < J) {
+      cj = P.scal[base + 1 + j];
+#pragma unroll
+      for (int i2 = 0; i2 < j; ++i2) cj = fma(-c[i2], P.scal[base + gram_idx<kFuseJ>(i2, j)], cj);
+    }
+    c[j] = cj;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    for (int j = 0; j < J; ++j) {
+      const int row = j0 - 1 + j;
+      if (side == 0)
+        P.Tm[(int64_t)row + (int64_t)(k - 1) * P.maxit] = c[j];
+      else
+        P.H[(int64_t)row + (int64_t)(k - 1) * P.ldh] = c[j];
+    }
+  }
+  double acc = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * kVecThreads + threadIdx.x; i < len; i += (int64_t)gridDim.x * kVecThreads) {
+    double vi = v[i];
+#pragma unroll
+    for (int j = 0; j < kFuseJ; ++j)
+      if (j < J) vi = fma(-c[j], q[j][i], vi);
+    v[i] = vi;
+    acc = fma(vi, vi, acc);
+  }
+  acc = block_sum<kVecThreads>(acc, sh);
+  const int so = side == 0 ? P.slot_zout : P.slot_wout;
+  if (threadIdx.x == 0) P.part[(size_t)so * kVecBlocks + blockIdx.x] = acc;
+  last_block_reduce(P, so, 1, side == 0 ? CTR_ZAXPY : CTR_WAXPY, false);
+}
+
 // ------------------------------------------------------------------ a1 end + a2: normalise, tau, store
 // t = ||z||, breakdown test (R11), T_kk = t, p_k = z/t, z_k = tau_k(p_k)
 // (Alg. 1; Alg. 2; readings R7/R8), Z[:,k] = z_k, P ring.
@@ -564,8 +700,8 @@ __global__ void __launch_bounds__(kVecThreads) k_finish_z(Params P) {
   if (st->done) return;
   const int k = st->k;
   const int J = min(P.ell, k - 1);
-  const double t = sqrt(get_sum<kVecThreads>(P, P.slot_z0 + J, sh, kVecBlocks));
-  const double zin = sqrt(get_sum<kVecThreads>(P, P.slot_zin, sh, kVecBlocks));
+  const double t = sqrt(P.fused ? P.scal[P.slot_zout] : get_sum<kVecThreads>(P, P.slot_z0 + J, sh, kVecBlocks));
+  const double zin = sqrt(P.fused ? P.scal[P.slot_zf] : get_sum<kVecThreads>(P, P.slot_zin, sh, kVecBlocks));
   if (t == 0.0 || t <= 1e-14 * zin) {
     __syncthreads();
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -582,7 +718,7 @@ __global__ void __launch_bounds__(kVecThreads) k_finish_z(Params P) {
     if (k == 1) {
       mode = 0;  // D_1 = I (x_0 = 0)
     } else {
-      const double mx = get_max<kVecThreads>(P, P.slot_xmax, sh, kVecBlocks);
+      const double mx = P.scal[P.slot_xmax];
       if (!(mx > 0.0))
         mode = 0;  // x_{k-1} = 0 (IRN) or x_{k-1} <= 0 (NONNEG): D = I
       else
@@ -618,8 +754,8 @@ __global__ void __launch_bounds__(kVecThreads) k_finish_w(Params P) {
   if (st->done) return;
   const int k = st->k;
   const int J = min(P.ell + 1, k);
-  const double hn = sqrt(get_sum<kVecThreads>(P, P.slot_w0 + J, sh, kVecBlocks));
-  const double win = sqrt(get_sum<kVecThreads>(P, P.slot_win, sh, kVecBlocks));
+  const double hn = sqrt(P.fused ? P.scal[P.slot_wout] : get_sum<kVecThreads>(P, P.slot_w0 + J, sh, kVecBlocks));
+  const double win = sqrt(P.fused ? P.scal[P.slot_wf] : get_sum<kVecThreads>(P, P.slot_win, sh, kVecBlocks));
   const bool brk = (hn == 0.0 || hn <= 1e-14 * win);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     st->wbreak = brk ? 1 : 0;
@@ -636,11 +772,15 @@ __global__ void __launch_bounds__(kVecThreads) k_finish_w(Params P) {
 // ------------------------------------------------------------------ a7: projected sketched LS (one CTA)
 // Appends column k of M (sFLSQR: S A z_k, Alg. 1; sFLSMR: the band
 // combination sum_i [S_TW, S z]_i H_{i,k}, Alg. 2 L796 / eq. sFLSMR) to an
-// incremental unpivoted Householder QR: reflectors 1..k-1 are applied to the new
-// column in order, reflector k is formed, Q^T rhs is updated, and R y = (Q^T rhs)_{1:k}
-// is solved by back substitution (reading R14: the same reflector sequence as a
-// from-scratch Householder QR).  Also forms g = beta e_1 - H_{1:k+1,1:k} y for
-// the W-path true residual (eq. FGK: b - A Z y = W_{k+1} g).
+// incremental unpivoted Householder QR (reading R14).  The earlier reflectors are
+// applied in compact-WY form, Q_{k-1}^T a = a - V T^T (V^T a) (T upper triangular,
+// LAPACK dlarft forward/columnwise, maintained one column per step), so the
+// sequential depth per step is a handful of block reductions instead of k of
+// them; mathematically identical to applying H_1..H_{k-1} in order.  Then the new
+// reflector, Q^T rhs, the sketched residual ||(Q^T rhs)_{k+1:d}||, and R y =
+// (Q^T rhs)_{1:k} by blocked back substitution.  Also forms g = beta e_1 -
+// H_{1:k+1,1:k} y for the W-path true residual (eq. FGK: b - A Z y = W_{k+1} g).
+
 // Block reduction with one __syncthreads: warp partials into a double-buffered
 // slot array, every thread then sums the kLsThreads/32 partials in warp order.
 __device__ __forceinline__ double ls_reduce(double v, double (*red)[kLsThreads / 32], int& flip) {
@@ -654,18 +794,34 @@ __device__ __forceinline__ double ls_reduce(double v, double (*red)[kLsThreads /
   return t;
 }
 
+// out[j] = sum_{r >= j} V[r, j] * vec[r] for j < c (warp per column, lanes over rows).
+__device__ __forceinline__ void ls_vt_times(const Params& P, int c, const double* vec, double* out) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, d = P.d;
+  for (int j = wid; j < c; j += kLsThreads / 32) {
+    const double* vj = P.V + (int64_t)j * d;
+    double acc = 0.0;
+    for (int r = j + lane; r < d; r += 32) acc = fma(vj[r], vec[r], acc);
+    acc = warp_sum(acc);
+    if (lane == 0) out[j] = acc;
+  }
+}
+
+template <int RPT>  // rows per thread: d <= RPT * kLsThreads
 __global__ void __launch_bounds__(kLsThreads) k_ls(Params P) {
-  constexpr int RPT = kMaxD / kLsThreads;  // rows per thread (4)
   __shared__ double red[2][kLsThreads / 32];
-  __shared__ double a_s[kMaxD];
-  __shared__ double q_s[kMaxD];
   __shared__ double blk[32][33];
+  extern __shared__ double ls_dyn[];  // 3 * RPT * kLsThreads doubles
+  double* a_s = ls_dyn;
+  double* q_s = ls_dyn + RPT * kLsThreads;
+  double* u_s = ls_dyn + 2 * RPT * kLsThreads;  // c <= maxit - 1 <= d - 1 entries
   __shared__ double sh[33];
-  double* y_s = a_s;  // a_s is dead once R(:, c) and alpha have been read
+  double* y_s = a_s;   // a_s is dead once R(:, c) and alpha have been read
+  double* u2_s = q_s;  // q_s is filled only after the reflector application
   DevState* st = P.st;
   if (st->done) return;
   const int k = st->k, c = k - 1, d = P.d;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t ldt = P.maxit;
   int flip = 0;
   double* Mc = P.Mcols + (int64_t)c * d;
   double a[RPT], q[RPT];
@@ -689,49 +845,37 @@ __global__ void __launch_bounds__(kLsThreads) k_ls(Params P) {
         Mc[r] = acc;
       }
       q[u] = P.qtb[r];
+      a_s[r] = a[u];
     }
   }
-  // apply reflectors 0..c-1 to the new column (Householder QR order); v_j, tau_j
-  // are prefetched two steps ahead so each step costs one block reduction.
-  double vA[RPT], vB[RPT];
-  double tauA = 0.0, tauB = 0.0;
-#pragma unroll
-  for (int u = 0; u < RPT; ++u) {
-    const int r = tid + u * kLsThreads;
-    vA[u] = (c > 0 && r < d) ? P.V[r] : 0.0;
-    vB[u] = (c > 1 && r < d) ? P.V[(int64_t)d + r] : 0.0;
-  }
-  if (c > 0) tauA = P.taus[0];
-  if (c > 1) tauB = P.taus[1];
-  for (int j = 0; j < c; ++j) {
-    double vC[RPT];
-    const bool pre = j + 2 < c;
-    const double tauC = pre ? P.taus[j + 2] : 0.0;
+  __syncthreads();
+  if (c > 0) {
+    // u = V^T a
+    ls_vt_times(P, c, a_s, u_s);
+    __syncthreads();
+    // u2 = T^T u  (u2_i = sum_{j <= i} T[j, i] u_j; warp per output, lanes over j)
+    for (int i = wid; i < c; i += kLsThreads / 32) {
+      const double* ti = P.Tw + (int64_t)i * ldt;
+      double acc = 0.0;
+      for (int j = lane; j <= i; j += 32) acc = fma(ti[j], u_s[j], acc);
+      acc = warp_sum(acc);
+      if (lane == 0) u2_s[i] = acc;
+    }
+    __syncthreads();
+    // a -= V u2
 #pragma unroll
     for (int u = 0; u < RPT; ++u) {
       const int r = tid + u * kLsThreads;
-      vC[u] = (pre && r < d) ? P.V[(int64_t)(j + 2) * d + r] : 0.0;
+      if (r < d) {
+        double acc = 0.0;
+        const int jmax = min(c, r + 1);  // V[r, j] = 0 for j > r
+        for (int j = 0; j < jmax; ++j) acc = fma(P.V[(int64_t)j * d + r], u2_s[j], acc);
+        a[u] -= acc;
+        a_s[r] = a[u];
+      }
     }
-    double part = 0.0;
-#pragma unroll
-    for (int u = 0; u < RPT; ++u) part = fma(vA[u], a[u], part);
-    const double dot = ls_reduce(part, red, flip);
-    const double f = tauA * dot;
-#pragma unroll
-    for (int u = 0; u < RPT; ++u) {
-      a[u] = fma(-f, vA[u], a[u]);
-      vA[u] = vB[u];
-      vB[u] = vC[u];
-    }
-    tauA = tauB;
-    tauB = tauC;
+    __syncthreads();
   }
-#pragma unroll
-  for (int u = 0; u < RPT; ++u) {
-    const int r = tid + u * kLsThreads;
-    if (r < d) a_s[r] = a[u];
-  }
-  __syncthreads();
   for (int r = tid; r < c; r += kLsThreads) P.R[(int64_t)r + (int64_t)c * P.maxit] = a_s[r];
   const double alpha = a_s[c];
   double part = 0.0;
@@ -758,12 +902,28 @@ __global__ void __launch_bounds__(kLsThreads) k_ls(Params P) {
     const int r = tid + u * kLsThreads;
     v[u] = (r < c) ? 0.0 : (r == c ? 1.0 : (xnorm == 0.0 ? 0.0 : a[u] * scal));
     if (r >= d) v[u] = 0.0;
-    if (r < d) vc[r] = v[u];
+    if (r < d) {
+      vc[r] = v[u];
+      a_s[r] = v[u];  // a_s now holds v_c
+    }
   }
   if (tid == 0) {
     P.R[(int64_t)c + (int64_t)c * P.maxit] = beta_h;
     P.taus[c] = tau;
   }
+  __syncthreads();
+  // T update: T[0:c, c] = -tau T[0:c, 0:c] (V^T v_c), T[c, c] = tau
+  if (c > 0) {
+    ls_vt_times(P, c, a_s, u_s);  // u_s = V^T v_c (reads only columns < c)
+    __syncthreads();
+    for (int i = wid; i < c; i += kLsThreads / 32) {
+      double acc = 0.0;
+      for (int j = i + lane; j < c; j += 32) acc = fma(P.Tw[(int64_t)i + (int64_t)j * ldt], u_s[j], acc);
+      acc = warp_sum(acc);
+      if (lane == 0) P.Tw[(int64_t)i + (int64_t)c * ldt] = -tau * acc;
+    }
+  }
+  if (tid == 0) P.Tw[(int64_t)c + (int64_t)c * ldt] = tau;
   part = 0.0;
 #pragma unroll
   for (int u = 0; u < RPT; ++u) part = fma(v[u], q[u], part);
@@ -793,8 +953,9 @@ __global__ void __launch_bounds__(kLsThreads) k_ls(Params P) {
     __syncthreads();
     if (wid == 0) {
       double qv = lane < nb ? q_s[jb + lane] : 0.0;
+      const double rinv = lane < nb ? 1.0 / blk[lane][lane] : 0.0;
       for (int i = nb - 1; i >= 0; --i) {
-        const double yi = __shfl_sync(0xffffffffu, qv, i) / blk[i][i];
+        const double yi = __shfl_sync(0xffffffffu, qv * rinv, i);
         if (lane == i) y_s[jb + i] = yi;
         if (lane < i) qv = fma(-blk[lane][i], yi, qv);
       }
@@ -859,6 +1020,7 @@ __global__ void __launch_bounds__(kVecThreads) k_xupdate(Params P, int force) {
   }
   mx = block_max<kVecThreads>(mx, sh);
   if (threadIdx.x == 0) P.part[(size_t)P.slot_xmax * kVecBlocks + blockIdx.x] = mx;
+  last_block_reduce(P, P.slot_xmax, 1, CTR_XMAX, true);
 }
 
 // ------------------------------------------------------------------ a9: W-path true residual
@@ -885,6 +1047,7 @@ __global__ void __launch_bounds__(kVecThreads) k_res_partial(Params P) {
   }
   acc2 = block_sum<kVecThreads>(acc2, sh);
   if (threadIdx.x == 0) P.part[(size_t)P.slot_res * kVecBlocks + blockIdx.x] = acc2;
+  last_block_reduce(P, P.slot_res, 1, CTR_RES, false);
 }
 
 // ------------------------------------------------------------------ a9: stop tests
@@ -896,7 +1059,7 @@ __global__ void __launch_bounds__(kVecThreads) k_stop(Params P) {
   if (st->done) return;
   const int k = st->k;
   double r = NAN;
-  if (P.want_res) r = sqrt(get_sum<kVecThreads>(P, P.slot_res, sh, kVecBlocks));
+  if (P.want_res) r = sqrt(P.scal[P.slot_res]);
   if (threadIdx.x != 0) return;
   P.hist_true[k - 1] = r;
   const double sres = P.hist_sk[k - 1];
