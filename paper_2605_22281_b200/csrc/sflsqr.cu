@@ -319,12 +319,14 @@ int reduce_slots(sflsqr_t* h, int slot0, int ns, bool is_max) {
   return coll_allreduce(h, h->P.scal + slot0, ns, is_max);
 }
 
-// Deterministic per-operator SpMV variant (measured on configs 3-4):
-// long rows (>= 1024 nnz average, e.g. the pixel-driven backprojector) -> half-warp
-// rows, 64 adjacent rows per CTA; otherwise one warp per row, 32 rows per CTA.
+// Default SpMV variant (measured on configs 3-4, tools/spmv_tune.py):
+// half-warp rows, 32 adjacent rows per 512-thread CTA, 4 CTAs per SM, the next
+// 4 chunks' indices/values loaded before the current gathers (mode 14).  Fixed,
+// so results are reproducible run to run.
 int select_spmv_mode(int64_t nnz, int64_t nrows) {
-  const double avg = nrows > 0 ? (double)nnz / (double)nrows : 0.0;
-  return avg >= 1024.0 ? 8 : 3;
+  (void)nnz;
+  (void)nrows;
+  return 14;
 }
 
 // y = A x (which 0) or y = T x (which 1) for this rank's shard; x may be a
@@ -374,6 +376,18 @@ void enqueue_apply(sflsqr_t* h, int which, const DevState* st, const double* x, 
       break;
     case 8:
       k_spmv_csr_half<32, 4><<<grid_for(64, 2), 1024, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
+      break;
+    case 11:
+      k_spmv_csr_pf<32, 2, 32><<<grid_for(32, 2), 1024, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
+      break;
+    case 12:
+      k_spmv_csr_pf<32, 2, 16><<<grid_for(64, 2), 1024, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
+      break;
+    case 13:
+      k_spmv_csr_pf<16, 4, 32><<<grid_for(16, 4), 512, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
+      break;
+    case 14:
+      k_spmv_csr_pf<16, 4, 16><<<grid_for(32, 4), 512, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
       break;
     default:  // 3
       k_spmv_csr_rows<32, 4><<<grid_for(32, 2), 1024, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
@@ -1372,7 +1386,7 @@ int sflsqr_debug_state(sflsqr_t* h, double* z, double* x, double* p_ring, double
 int sflsqr_debug_set_tuning(sflsqr_t* h, int32_t spmv_mode, int32_t band_shift) {
   if (!h) return fail(nullptr, SFLSQR_E_INVALID, "NULL handle");
   const bool ok_mode = spmv_mode == -1 || spmv_mode == 0 || spmv_mode == 1 || spmv_mode == 2 || spmv_mode == 3 ||
-                       spmv_mode == 8 || spmv_mode == 10;
+                       spmv_mode == 8 || (spmv_mode >= 10 && spmv_mode <= 14);
   if (!ok_mode || band_shift < 8 || band_shift > 30) return fail(h, SFLSQR_E_INVALID, "bad tuning values");
   h->spmv_mode = spmv_mode;
   h->band_shift = band_shift;

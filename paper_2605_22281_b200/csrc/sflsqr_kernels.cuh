@@ -398,6 +398,67 @@ __global__ void __launch_bounds__(WPB * 32, 2048 / (WPB * 32)) k_spmv_csr_rows(c
   }
 }
 
+// Variant: software-pipelined row-group SpMV — the column indices and values of
+// the next UNR chunks are loaded before the gathers of the current ones, so the
+// col -> x dependent latency of one chunk group overlaps the streams of the next.
+template <int WPB, int UNR, int LANES>
+__global__ void __launch_bounds__(WPB * 32, 2048 / (WPB * 32)) k_spmv_csr_pf(const DevState* st, int64_t nrows,
+                                                            const int64_t* __restrict__ rowptr,
+                                                            const int* __restrict__ col,
+                                                            const double* __restrict__ val,
+                                                            const double* __restrict__ x_base, int64_t x_ld,
+                                                            int x_koff, double* __restrict__ y) {
+  if (st && st->done) return;
+  const double* __restrict__ x = kvec(st, x_base, x_ld, x_koff);
+  constexpr int RPW = 32 / LANES;  // rows per warp
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int sl = lane % LANES, sub = lane / LANES;
+  for (int64_t r0 = (int64_t)blockIdx.x * WPB * RPW; r0 < nrows; r0 += (int64_t)gridDim.x * WPB * RPW) {
+    const int64_t row = r0 + (int64_t)wid * RPW + sub;
+    int64_t s = 0, e = 0;
+    if (row < nrows) {
+      s = rowptr[row];
+      e = rowptr[row + 1];
+    }
+    double sum = 0.0;
+    int64_t p = s + sl;
+    int cn[UNR];
+    double vn[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int64_t q = p + (int64_t)LANES * u;
+      cn[u] = q < e ? ld_stream_i(col + q) : 0;
+      vn[u] = q < e ? ld_stream_d(val + q) : 0.0;
+    }
+    while (__any_sync(0xffffffffu, p < e)) {
+      int c[UNR];
+      double v[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        c[u] = cn[u];
+        v[u] = vn[u];
+      }
+      const int64_t pn = p + (int64_t)LANES * UNR;
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int64_t q = pn + (int64_t)LANES * u;
+        cn[u] = q < e ? ld_stream_i(col + q) : 0;
+        vn[u] = q < e ? ld_stream_d(val + q) : 0.0;
+      }
+      double xv[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) xv[u] = (p + (int64_t)LANES * u < e) ? __ldg(x + c[u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < UNR; ++u)
+        if (p + (int64_t)LANES * u < e) sum = fma(v[u], xv[u], sum);
+      p = pn;
+    }
+#pragma unroll
+    for (int o = LANES / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (sl == 0 && row < nrows) y[row] = sum;
+  }
+}
+
 // Variant: half-warp per row (2 rows per warp, 2*WPB adjacent rows per CTA).
 template <int WPB, int UNR>
 __global__ void __launch_bounds__(WPB * 32, 2048 / (WPB * 32)) k_spmv_csr_half(const DevState* st, int64_t nrows,
