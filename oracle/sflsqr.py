@@ -1,4 +1,6 @@
-"""sFLSQR (Algorithm 1) and sFLSMR (Algorithm 2), plain fp64, followed line by line.
+"""sFLSQR (Algorithm 1) and sFLSMR (Algorithm 2), plain fp64, followed line by line;
+and their unsketched full-orthogonalisation parents FLSQR / FLSMR (SURVEY.md §8(f)
+NEXT-1), which share the same flexible Golub-Kahan step.
 
 TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
 
@@ -7,6 +9,14 @@ Sources (PAPER.md):
     Golub-Kahan with window ell) L400-406; cost L444-448.
   * Alg. 2 sFLSMR, L752-808; eq. sFLSMR L730-749 ("compute the columns of
     S A^T W ... then right-multiply by H ... implemented in our code").
+  * FLSQR eq. (FLSQR): x_k = Z_k y_k, y_k = argmin || ||b|| e_1 - H_{k+1,k} y ||,
+    on the FGK factorisation eq. (flsqr-relations) L335-345 with FULL
+    orthogonalisation (P_k, W_{k+1} orthonormal; T_k, H_{k+1,k} fill up, L344-345).
+  * FLSMR L359-368: y_k = argmin || T_{k+1} ( ||b|| e_1 - H_{k+1,k} y ) ||, where
+    T_{k+1} is the (k+1) x (k+1) upper-triangular factor of A^T W_{k+1} = P_{k+1} T_{k+1}:
+    its last column is the orthogonalisation of z = A^T w_{k+1} against p_1..p_k,
+    i.e. the first half of FGK step k+1 (Alg. 1 L464-469 with k -> k+1), computed here
+    at the end of step k by the same code that step k+1 then repeats.
   * Discrepancy principle eq. discrP, L50-53.
   * Flexible preconditioning as tau, L59-64, L322-345.
 Readings of paper-silent / ambiguous points (R1-R14):
@@ -114,6 +124,11 @@ def init_state(op, b, method, maxit, S):
     elif method == "sflsmr":
         Sz = S(z)
         rhs = beta * Sz                     # s_{A^T b} = beta S z
+    elif method == "flsqr":
+        rhs = np.zeros(maxit + 1)           # ||b|| e_1 (eq. FLSQR)
+        rhs[0] = beta
+    elif method == "flsmr":
+        rhs = None                          # ||b|| T_{k+1} e_1 = ||b|| T_11 e_1, T_11 known after step 1's L469
     else:
         raise ValueError(method)
     st = FGKState(op.m, op.n, maxit, method, rhs, beta, b)
@@ -124,6 +139,18 @@ def init_state(op, b, method, maxit, S):
     return st
 
 
+def z_orthogonalise(st, k, ell, orth_mode, z):
+    """Alg. 1 L464-469 / Alg. 2 L767-772 for step k: windowed MGS of z = T w_k against
+    q_j (j = max(1, k-ell) .. k-1) and its norm.  Returns (coefficients {j: c}, t, z_perp)."""
+    coeffs = {}
+    for j in range(max(1, k - ell), k):
+        qj = st.P[j - 1] if orth_mode == "P" else st.Z[j - 1]
+        c = float(np.dot(qj, z))
+        z = z - c * qj
+        coeffs[j] = c
+    return coeffs, float(np.linalg.norm(z)), z
+
+
 def fgk_step(op, st, k, ell, S, precond="identity", p_exp=1.0, eps_rel=1e-3, fixed_diag=None, orth_mode="P"):
     """Iteration k of Alg. 1 (L462-496) / Alg. 2 (L765-797), updating st in place.
 
@@ -132,14 +159,10 @@ def fgk_step(op, st, k, ell, S, precond="identity", p_exp=1.0, eps_rel=1e-3, fix
     m, n = st.m, st.n
     out = {}
     # L464-469: z-side windowed MGS + normalisation
-    z = st.z
-    z_in = float(np.linalg.norm(z))
-    for j in range(max(1, k - ell), k):
-        qj = st.P[j - 1] if orth_mode == "P" else st.Z[j - 1]
-        c = float(np.dot(qj, z))
-        z = z - c * qj
+    z_in = float(np.linalg.norm(st.z))
+    coeffs, t, z = z_orthogonalise(st, k, ell, orth_mode, st.z)
+    for j, c in coeffs.items():
         st.Tm[j - 1, k - 1] = c
-    t = float(np.linalg.norm(z))
     if t == 0.0 or t <= 1e-14 * z_in:
         return {"breakdown": "z"}
     st.Tm[k - 1, k - 1] = t
@@ -172,12 +195,28 @@ def fgk_step(op, st, k, ell, S, precond="identity", p_exp=1.0, eps_rel=1e-3, fix
     # L488-490 / L790-797: projected sketched LS
     if st.method == "sflsqr":
         M = np.column_stack(st.SAZ)
-    else:
+    elif st.method == "sflsmr":
         Sz = S(st.z)
         M = np.column_stack(st.STW + [Sz]) @ st.H[:k + 1, :k]
         out["Sz"] = Sz
-    y, _, ratio = householder_qr_solve(M, st.rhs)
-    sres = float(np.linalg.norm(st.rhs - M @ y))
+    elif st.method == "flsqr":
+        M = st.H[:k + 1, :k]                                  # eq. FLSQR
+        st.rhs_k = st.rhs[:k + 1]
+    else:                                                     # FLSMR L361-367
+        if k == 1:
+            st.rhs = np.zeros(st.H.shape[0])
+            st.rhs[0] = st.beta * st.Tm[0, 0]                 # ||b|| T_{k+1} e_1 (T upper triangular)
+        Tk1 = np.zeros((k + 1, k + 1))
+        Tk1[:k, :k] = st.Tm[:k, :k]
+        coeffs, t1, _ = z_orthogonalise(st, k + 1, ell, orth_mode, st.z)  # column k+1 of T (step k+1's L464-469)
+        for j, c in coeffs.items():
+            Tk1[j - 1, k] = c
+        Tk1[k, k] = t1
+        M = Tk1 @ st.H[:k + 1, :k]
+        st.rhs_k = st.rhs[:k + 1]
+    rhs_k = st.rhs_k if st.method in ("flsqr", "flsmr") else st.rhs
+    y, _, ratio = householder_qr_solve(M, rhs_k)
+    sres = float(np.linalg.norm(rhs_k - M @ y))
     x = np.column_stack(st.Z) @ y                 # L504 / L804: x_k = Z y_k
     r = float(np.linalg.norm(st.b - op.matvec(x)))  # eq. discrP residual (R12)
     out.update(p=p_k, z=z_k, w_next=st.W[k], Tcol=st.Tm[:k, k - 1].copy(), Hcol=st.H[:k + 1, k - 1].copy(),
@@ -188,7 +227,8 @@ def fgk_step(op, st, k, ell, S, precond="identity", p_exp=1.0, eps_rel=1e-3, fix
 def solve(op, b, method="sflsqr", maxit=10, window=2, sketch=None, sketch_seed=0, d=None, s_nz=1,
           precond="identity", p_exp=1.0, eps_rel=1e-3, fixed_diag=None, tol=0.0, eta=0.0, delta_e=0.0,
           orth_mode="P", record=True):
-    """Run sFLSQR / sFLSMR for at most maxit iterations.
+    """Run sFLSQR / sFLSMR (sketched, window ell) or FLSQR / FLSMR (full orthogonalisation,
+    no sketch; `window`, `sketch*` ignored) for at most maxit iterations.
 
     op: object with m, n, matvec(z) = A z, tmatvec(w) = T w.
     sketch: an object with .apply(v) (oracle.sketch.*); default: the sparse-sign
@@ -196,9 +236,13 @@ def solve(op, b, method="sflsqr", maxit=10, window=2, sketch=None, sketch_seed=0
     """
     m, n = op.m, op.n
     ell = int(window)
-    if sketch is None:
-        sketch = SparseSignSketch(sketch_seed, d, s_nz, m if method == "sflsqr" else n)
-    S = sketch.apply
+    if method in ("flsqr", "flsmr"):
+        ell = max(ell, maxit + 1)             # full orthogonalisation (L344-345); no sketch
+        S = None
+    else:
+        if sketch is None:
+            sketch = SparseSignSketch(sketch_seed, d, s_nz, m if method == "sflsqr" else n)
+        S = sketch.apply
     st = init_state(op, b, method, maxit, S)
     res = OracleResult(x=np.zeros(n), k=0, status=RUNNING, rhs=st.rhs)
     k_done = 0
@@ -239,8 +283,9 @@ def solve(op, b, method="sflsqr", maxit=10, window=2, sketch=None, sketch_seed=0
     res.W = np.column_stack(st.W)
     if method == "sflsqr":
         res.sketch_cols = np.column_stack(st.SAZ) if st.SAZ else None
-    else:
+    elif method == "sflsmr":
         res.sketch_cols = np.column_stack(st.STW)
+    res.rhs = st.rhs
     return res
 
 
