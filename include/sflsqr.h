@@ -63,10 +63,25 @@ extern "C" {
 /* opts.method */
 #define SFLSQR_METHOD_SFLSQR 0 /* Algorithm 1 */
 #define SFLSQR_METHOD_SFLSMR 1 /* Algorithm 2 */
+/* The unsketched parents (PAPER.md §"Flexible Golub-Kahan factorization, FLSQR and
+ * FLSMR", L321-373): the same FGK step with FULL orthogonalisation (opts.window is
+ * raised to maxit) and no sketch (sflsqr_set_sketch is not needed and is ignored).
+ *   FLSQR: y_k = argmin || ||b|| e_1 - H_{k+1,k} y ||                 (eq. FLSQR)
+ *   FLSMR: y_k = argmin || T_{k+1} (||b|| e_1 - H_{k+1,k} y) ||       (L359-367)
+ * get_residual_norms' second history then holds that projected residual
+ * (= ||b - A x_k|| for FLSQR, ||T(b - A x_k)|| for FLSMR, in exact arithmetic). */
+#define SFLSQR_METHOD_FLSQR 2
+#define SFLSQR_METHOD_FLSMR 3
 
 /* opts.orth_mode (reading R1) */
 #define SFLSQR_ORTH_P 0 /* orthogonalise against the last ell normalised p_j (eq. FGK) */
 #define SFLSQR_ORTH_Z 1 /* literal Alg. 1: against z_j = tau(p_j)              */
+
+/* opts.orth_kernel: how a window of J vectors is orthogonalised against (performance
+ * choice; every variant computes the MGS coefficients of Alg. 1 L464-467 / L476-480 in
+ * exact arithmetic, reading R10/R18) */
+#define SFLSQR_ORTHK_AUTO 0 /* J <= 6: one-pass dots + Gram (R10); J > 6: CGS2 (R18)      */
+#define SFLSQR_ORTHK_MGS 1  /* literal MGS, one kernel pass per window vector              */
 
 /* solve status (sflsqr_iterate, sflsqr_info) */
 #define SFLSQR_RUNNING 0
@@ -115,7 +130,8 @@ typedef struct sflsqr_opts {
   int32_t comm_kind; /* SFLSQR_COMM_* (world > 1)                                  */
   const uint8_t *nccl_id; /* SFLSQR_COMM_NCCL: the 128-byte id of sflsqr_get_unique_id */
   void *local_group;      /* SFLSQR_COMM_LOCAL: sflsqr_local_group_create()          */
-  int32_t reserved[4];
+  int32_t orth_kernel;    /* SFLSQR_ORTHK_* (0 = auto)                               */
+  int32_t reserved[3];
 } sflsqr_opts;
 
 typedef struct sflsqr_info {
@@ -210,9 +226,12 @@ int sflsqr_set_operator_blur(sflsqr_t *h, int32_t H, int32_t W, double sigma, in
 /* Sparse-sign sketch S in R^{d x dim} (readings R5/R6): dim = m for sFLSQR,
  * n for sFLSMR (R4).  Column i has exactly s_nz distinct rows drawn by
  * Philox4x32-10(key = seed, counter = (i, t, attempt)) with values
- * +-1/sqrt(s_nz); s_nz = 1 is CountSketch.  S is never stored: rows and signs
- * are regenerated from the hash in the kernels.  Requires 1 <= s_nz <= d <= 4096
- * and d >= maxit (the projected problem needs k <= d) else SFLSQR_E_INVALID. */
+ * +-1/sqrt(s_nz); s_nz = 1 is CountSketch.  The table is generated once per
+ * solve by the device hash (bit-exact with the oracle) and kept on the device
+ * transposed, as a d x dim CSR of (coordinate | sign << 31) entries (4 s dim
+ * bytes), so each per-iteration S v is a deterministic gather-sum.
+ * Requires 1 <= s_nz <= min(d, 32), d <= 2048 and d >= maxit (the projected
+ * problem needs k <= d) else SFLSQR_E_INVALID.  FLSQR / FLSMR: not needed, ignored. */
 int sflsqr_set_sketch(sflsqr_t *h, uint64_t seed, int32_t d, int32_t s_nz);
 
 /* Flexible preconditioner tau_k (Alg. 1, Alg. 2):
@@ -269,8 +288,9 @@ int sflsqr_debug_state(sflsqr_t *h, double *z, double *x, double *p_ring, double
  * oracle-checked): spmv_mode -1 (default) = per-operator rule on the average
  * row length; 0 = warp-per-row CSR with 128-bit per-lane loads; 1, 2, 3, 10 =
  * row-group CSR (rows per CTA x chunks in flight: 16x4, 8x4, 32x4, 32x2);
- * 8 = 64 half-warp rows per CTA.  Modes 3 and 8 fuse the sketch into the SpMV;
- * the others use the standalone sketch kernel.  band_shift is reserved (8..30).
+ * 8 = 64 half-warp rows per CTA; 11, 12, 13, 14 = software-pipelined row-group
+ * CSR (next chunks' indices/values loaded ahead of the gathers; 14 = half-warp
+ * rows, 32 rows per 512-thread CTA = the default).  band_shift is reserved (8..30).
  * Invalidates a captured graph (rebuilt at the next set_rhs). */
 int sflsqr_debug_set_tuning(sflsqr_t *h, int32_t spmv_mode, int32_t band_shift);
 

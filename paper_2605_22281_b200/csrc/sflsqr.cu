@@ -429,37 +429,71 @@ int enqueue_transpose_product(sflsqr_t* h, bool init) {
   return SFLSQR_OK;
 }
 
-// One iteration k of Alg. 1 / Alg. 2.
+// Windowed orthogonalisation of z (side 0, Alg. 1 L464-467 / Alg. 2) or w
+// (side 1, Alg. 1 L476-480 / Alg. 2) for iteration st->k + koff, by the
+// handle's algorithm (fused dots+Gram / literal MGS passes / CGS2), leaving ||v||^2
+// where k_finish_z / k_finish_w (and FLSMR's k_ls) read it.
+int enqueue_orth(sflsqr_t* h, int side, int koff) {
+  Params& P = h->P;
+  const int k = h->host_k + koff;  // used only for the byte model
+  const double v8 = 8.0 * (side == 0 ? h->n_loc : h->m_loc);
+  const int Jmax = side == 0 ? P.ell : P.ell + 1;
+  const int J = side == 0 ? std::min(P.ell, k - 1) : std::min(P.ell + 1, k);
+  const int slot_f = side == 0 ? P.slot_zf : P.slot_wf, slot_out = side == 0 ? P.slot_zout : P.slot_wout;
+  int rc;
+  if (P.orth_alg == ORTH_FUSED) {
+    {
+      Launch L(h, SFLSQR_KC_ORTH, v8 * (1 + J));
+      k_orth_dots<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P, side, koff);
+    }
+    if ((rc = coll_allreduce(h, P.scal + slot_f, kFuseAcc, false))) return rc;
+    {
+      Launch L(h, SFLSQR_KC_ORTH, v8 * (2 + J));
+      k_orth_axpy<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P, side, koff);
+    }
+    return coll_allreduce(h, P.scal + slot_out, 1, false);
+  }
+  if (P.orth_alg == ORTH_CGS2) {
+    const size_t sm_dots = sizeof(double) * (kCgsChunk + P.ldc), sm_upd = sizeof(double) * 2 * P.ldc;
+    for (int stage = 0; stage < 2; ++stage) {
+      {
+        Launch L(h, SFLSQR_KC_ORTH, v8 * (1 + J));
+        k_cgs_dots<<<kVecBlocks, kVecThreads, sm_dots, h->stream>>>(P, side, stage, koff);
+      }
+      if ((rc = coll_allreduce(h, P.cscal + (size_t)stage * P.ldc, P.ldc, false))) return rc;
+      if (stage == 0 && (rc = coll_allreduce(h, P.scal + slot_f, 1, false))) return rc;
+      {
+        Launch L(h, SFLSQR_KC_ORTH, v8 * (2 + J));
+        k_cgs_update<<<kVecBlocks, kVecThreads, sm_upd, h->stream>>>(P, side, stage, koff);
+      }
+    }
+    return coll_allreduce(h, P.scal + slot_out, 1, false);
+  }
+  // literal MGS, one pass per window vector (Jmax + 1 passes; passes beyond the window exit early)
+  const int slot0 = side == 0 ? P.slot_z0 : P.slot_w0, slot_in = side == 0 ? P.slot_zin : P.slot_win;
+  for (int pass = 0; pass <= Jmax; ++pass) {
+    const double by = pass > J ? 0.0 : v8 * (1 + (pass > 0) * 2 + (pass < J));
+    {
+      Launch L(h, SFLSQR_KC_ORTH, by);
+      k_mgs_pass<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P, side, pass, koff);
+    }
+    if (pass == 0 && (rc = reduce_slots(h, slot_in, 1, false))) return rc;
+    if ((rc = reduce_slots(h, slot0 + pass, 1, false))) return rc;
+  }
+  return SFLSQR_OK;
+}
+
+// One iteration k of Alg. 1 / Alg. 2, or of FLSQR /
+// FLSMR (full window, no sketch; FLSMR runs the z side of step k+1 before its
+// projected problem, which needs column k+1 of T).
 int enqueue_iteration(sflsqr_t* h) {
   Params& P = h->P;
   const int k = h->host_k;  // used only for the byte model
   const double n8 = 8.0 * h->n_loc, m8 = 8.0 * h->m_loc;
+  const bool sketched = P.method == SFLSQR_METHOD_SFLSQR || P.method == SFLSQR_METHOD_SFLSMR;
   int rc;
-  // a1: z-side windowed orthogonalisation
-  if (P.fused) {
-    {
-      Launch L(h, SFLSQR_KC_ORTH, n8 * (1 + std::min(P.ell, k - 1)));
-      k_orth_dots<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P, 0);
-    }
-    if ((rc = coll_allreduce(h, P.scal + P.slot_zf, kFuseAcc, false))) return rc;
-    {
-      Launch L(h, SFLSQR_KC_ORTH, n8 * (2 + std::min(P.ell, k - 1)));
-      k_orth_axpy<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P, 0);
-    }
-    if ((rc = coll_allreduce(h, P.scal + P.slot_zout, 1, false))) return rc;
-  } else {
-    // literal MGS, one pass per window vector (ell + 1 passes; passes beyond the window exit early)
-    for (int pass = 0; pass <= P.ell; ++pass) {
-      const int J = std::min(P.ell, k - 1);
-      const double by = pass > J ? 0.0 : n8 * (1 + (pass > 0) * 2 + (pass < J));
-      {
-        Launch L(h, SFLSQR_KC_ORTH, by);
-        k_mgs_pass<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P, 0, pass);
-      }
-      if (pass == 0 && (rc = reduce_slots(h, P.slot_zin, 1, false))) return rc;
-      if ((rc = reduce_slots(h, P.slot_z0 + pass, 1, false))) return rc;
-    }
-  }
+  // a1: z-side windowed orthogonalisation (FLSMR: done at the end of the previous step / in set_rhs)
+  if (P.method != SFLSQR_METHOD_FLSMR && (rc = enqueue_orth(h, 0, 0))) return rc;
   // a1 end + a2: normalise, tau, store z_k
   {
     Launch L(h, SFLSQR_KC_TAU, n8 * (2 + (P.use_pring ? 1 : 0) + (P.precond ? 1 : 0)));
@@ -477,29 +511,7 @@ int enqueue_iteration(sflsqr_t* h) {
   // a4 (sFLSQR): S_AZ[:, k] = S w
   if (P.method == SFLSQR_METHOD_SFLSQR && (rc = enqueue_sketch(h, P.st, P.w))) return rc;
   // a5: w-side windowed orthogonalisation and normalisation
-  if (P.fused) {
-    {
-      Launch L(h, SFLSQR_KC_ORTH, m8 * (1 + std::min(P.ell + 1, k)));
-      k_orth_dots<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P, 1);
-    }
-    if ((rc = coll_allreduce(h, P.scal + P.slot_wf, kFuseAcc, false))) return rc;
-    {
-      Launch L(h, SFLSQR_KC_ORTH, m8 * (2 + std::min(P.ell + 1, k)));
-      k_orth_axpy<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P, 1);
-    }
-    if ((rc = coll_allreduce(h, P.scal + P.slot_wout, 1, false))) return rc;
-  } else {
-    for (int pass = 0; pass <= P.ell + 1; ++pass) {
-      const int J = std::min(P.ell + 1, k);
-      const double by = pass > J ? 0.0 : m8 * (1 + (pass > 0) * 2 + (pass < J));
-      {
-        Launch L(h, SFLSQR_KC_ORTH, by);
-        k_mgs_pass<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P, 1, pass);
-      }
-      if (pass == 0 && (rc = reduce_slots(h, P.slot_win, 1, false))) return rc;
-      if ((rc = reduce_slots(h, P.slot_w0 + pass, 1, false))) return rc;
-    }
-  }
+  if ((rc = enqueue_orth(h, 1, 0))) return rc;
   {
     Launch L(h, SFLSQR_KC_ORTH, 2 * m8);
     k_finish_w<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P);
@@ -508,7 +520,10 @@ int enqueue_iteration(sflsqr_t* h) {
   if ((rc = enqueue_transpose_product(h, false))) return rc;
   // a4 (sFLSMR): S z -> S_TW[:, k+1]
   if (P.method == SFLSQR_METHOD_SFLSMR && (rc = enqueue_sketch(h, P.st, P.z))) return rc;
-  // a7: projected sketched LS (replicated on every rank: identical inputs)
+  // FLSMR: z side of step k+1 now (column k+1 of T for T_{k+1} H_{k+1,k}, L361-367)
+  if (P.method == SFLSQR_METHOD_FLSMR && (rc = enqueue_orth(h, 0, 1))) return rc;
+  // a7: projected (sketched) LS (replicated on every rank: identical inputs)
+  (void)sketched;
   {
     Launch L(h, SFLSQR_KC_LS, 8.0 * P.d * (k + 2));
     if (P.d <= kLsThreads)
@@ -602,12 +617,17 @@ int alloc_solve(sflsqr_t* h) {
   free_solve(h);
   Params& P = h->P;
   std::memset(&P, 0, sizeof(P));
-  const int maxit = h->o.maxit, d = h->d, ell = h->o.window;
+  const int maxit = h->o.maxit, ell = h->o.window;
+  const bool sketched = h->o.method <= SFLSQR_METHOD_SFLSMR;
+  // FLSQR / FLSMR: the projected problem has k+1 <= maxit+1 rows and no sketch
+  const int d = sketched ? h->d : maxit + 1;
   P.m = h->m_loc;
   P.n = h->n_loc;
   P.ell = ell;
   P.maxit = maxit;
   P.ldh = maxit + 1;
+  P.ldtm = maxit + 1;
+  P.ldc = ell + 2;
   P.method = h->o.method;
   P.orth_mode = h->o.orth_mode;
   P.precond = h->pkind;
@@ -622,7 +642,7 @@ int alloc_solve(sflsqr_t* h) {
   P.tol = h->o.tol;
   P.eta = h->o.eta;
   P.delta_e = h->o.delta_e;
-  P.sk_scale = 1.0 / std::sqrt((double)h->s_nz);
+  P.sk_scale = h->s_nz > 0 ? 1.0 / std::sqrt((double)h->s_nz) : 0.0;
   P.seed_lo = (uint32_t)(h->seed & 0xffffffffu);
   P.seed_hi = (uint32_t)(h->seed >> 32);
   // partial-sum slots
@@ -636,7 +656,7 @@ int alloc_solve(sflsqr_t* h) {
   s += ell + 2;
   P.slot_xmax = s++;
   P.slot_res = s++;
-  P.fused = (ell + 1 <= kFuseJ) ? 1 : 0;
+  P.orth_alg = h->o.orth_kernel == SFLSQR_ORTHK_MGS ? ORTH_MGS : (ell + 1 <= kFuseJ ? ORTH_FUSED : ORTH_CGS2);
   P.slot_zf = s;
   s += kFuseAcc;
   P.slot_zout = s++;
@@ -655,7 +675,7 @@ int alloc_solve(sflsqr_t* h) {
   if ((rc = dalloc(h, (void**)&P.ctr, sizeof(int) * CTR_COUNT, &h->solve_allocs, &h->solve_sizes))) return rc;
   if ((rc = A(&P.z, zlen)) || (rc = A(&P.x, n)) || (rc = A(&P.Z, n * maxit)) || (rc = A(&P.w, m)) ||
       (rc = A(&P.W, m * (maxit + 1))) || (rc = A(&P.b, m)) || (rc = A(&P.H, (size_t)(maxit + 1) * maxit)) ||
-      (rc = A(&P.Tm, (size_t)maxit * maxit)) || (rc = A(&P.part, (size_t)s * kVecBlocks)) ||
+      (rc = A(&P.Tm, (size_t)(maxit + 1) * (maxit + 1))) || (rc = A(&P.part, (size_t)s * kVecBlocks)) ||
       (rc = A(&P.scal, (size_t)s)) || (rc = A(&P.skbuf, d)) || (rc = A(&P.rhs, d)) ||
       (rc = A(&P.Mcols, (size_t)d * maxit)) || (rc = A(&P.STW, (size_t)d * (maxit + 1))) ||
       (rc = A(&P.V, (size_t)d * maxit)) || (rc = A(&P.taus, maxit)) || (rc = A(&P.R, (size_t)maxit * maxit)) ||
@@ -664,6 +684,9 @@ int alloc_solve(sflsqr_t* h) {
       (rc = A(&P.hist_sk, maxit)))
     return rc;
   if (P.use_pring && (rc = A(&P.Pring, n * ell))) return rc;
+  if (P.orth_alg == ORTH_CGS2 &&
+      ((rc = A(&P.cpart, (size_t)P.ldc * kVecBlocks)) || (rc = A(&P.cscal, (size_t)2 * P.ldc))))
+    return rc;
   if (h->world > 1) {
     if ((rc = A(&P.zsend, h->n_max)) || (rc = A(&h->zfull, (size_t)h->world * h->n_max))) return rc;
     if (h->tkind == T_ROWSHARD) {
@@ -684,18 +707,18 @@ int alloc_solve(sflsqr_t* h) {
   // the padded send buffers' tails are never written
   if (P.zsend) CU(h, cudaMemset(P.zsend, 0, sizeof(double) * h->n_max));
   if (P.wsend) CU(h, cudaMemset(P.wsend, 0, sizeof(double) * h->m_max));
-  if ((rc = build_sketch(h))) return rc;
+  if (sketched && (rc = build_sketch(h))) return rc;
   h->bufs = true;
   return SFLSQR_OK;
 }
 
 int zero_solve_state(sflsqr_t* h) {
   Params& P = h->P;
-  const int maxit = h->o.maxit, d = h->d;
+  const int maxit = h->o.maxit, d = P.d;
   cudaStream_t s = h->stream;
   CU(h, cudaMemsetAsync(P.st, 0, sizeof(DevState), s));
   CU(h, cudaMemsetAsync(P.H, 0, sizeof(double) * (size_t)(maxit + 1) * maxit, s));
-  CU(h, cudaMemsetAsync(P.Tm, 0, sizeof(double) * (size_t)maxit * maxit, s));
+  CU(h, cudaMemsetAsync(P.Tm, 0, sizeof(double) * (size_t)(maxit + 1) * (maxit + 1), s));
   CU(h, cudaMemsetAsync(P.R, 0, sizeof(double) * (size_t)maxit * maxit, s));
   CU(h, cudaMemsetAsync(P.Tw, 0, sizeof(double) * (size_t)maxit * maxit, s));
   CU(h, cudaMemsetAsync(P.V, 0, sizeof(double) * (size_t)d * maxit, s));
@@ -736,7 +759,7 @@ int build_graph(sflsqr_t* h) {
 int ensure_ready(sflsqr_t* h, bool need_rhs) {
   if (!h) return fail(nullptr, SFLSQR_E_INVALID, "NULL handle");
   if (!h->op_set) return fail(h, SFLSQR_E_STATE, "operator not set");
-  if (!h->sk_set) return fail(h, SFLSQR_E_STATE, "sketch not set");
+  if (!h->sk_set && h->o.method <= SFLSQR_METHOD_SFLSMR) return fail(h, SFLSQR_E_STATE, "sketch not set");
   if (need_rhs && !h->rhs_set) return fail(h, SFLSQR_E_STATE, "rhs not set");
   return SFLSQR_OK;
 }
@@ -803,11 +826,13 @@ void sflsqr_local_group_destroy(void* group) { local_group_release(static_cast<L
 int sflsqr_create(sflsqr_t** out, const sflsqr_opts* o) {
   if (!out || !o) return fail(nullptr, SFLSQR_E_INVALID, "NULL argument");
   *out = nullptr;
-  if (o->method != SFLSQR_METHOD_SFLSQR && o->method != SFLSQR_METHOD_SFLSMR)
-    return fail(nullptr, SFLSQR_E_INVALID, "method must be SFLSQR or SFLSMR");
+  if (o->method < SFLSQR_METHOD_SFLSQR || o->method > SFLSQR_METHOD_FLSMR)
+    return fail(nullptr, SFLSQR_E_INVALID, "method must be SFLSQR, SFLSMR, FLSQR or FLSMR");
+  if (o->orth_kernel != SFLSQR_ORTHK_AUTO && o->orth_kernel != SFLSQR_ORTHK_MGS)
+    return fail(nullptr, SFLSQR_E_INVALID, "bad orth_kernel");
   if (o->window < 1) return fail(nullptr, SFLSQR_E_INVALID, "window must be >= 1");
   if (o->maxit < 1) return fail(nullptr, SFLSQR_E_INVALID, "maxit must be >= 1");
-  if (o->maxit > kMaxD) return fail(nullptr, SFLSQR_E_INVALID, "maxit must be <= %d", kMaxD);
+  if (o->maxit > kMaxD - 1) return fail(nullptr, SFLSQR_E_INVALID, "maxit must be <= %d", kMaxD - 1);
   if (o->orth_mode != SFLSQR_ORTH_P && o->orth_mode != SFLSQR_ORTH_Z)
     return fail(nullptr, SFLSQR_E_INVALID, "bad orth_mode");
   if (!(o->tol >= 0.0) || !std::isfinite(o->tol)) return fail(nullptr, SFLSQR_E_INVALID, "tol must be >= 0");
@@ -835,6 +860,7 @@ int sflsqr_create(sflsqr_t** out, const sflsqr_opts* o) {
   h->rank = o->rank;
   h->world = o->world;
   if (o->window > o->maxit) h->o.window = o->maxit;  // full orthogonalisation
+  if (o->method >= SFLSQR_METHOD_FLSQR) h->o.window = o->maxit;  // FLSQR / FLSMR: full (L344-345)
   if (o->world > 1) h->o.use_graph = 0;             // collectives are issued eagerly
   if (o->stream && (cudaStream_t)o->stream != cudaStreamLegacy && (cudaStream_t)o->stream != cudaStreamPerThread) {
     h->stream = (cudaStream_t)o->stream;
@@ -1087,6 +1113,7 @@ int sflsqr_set_operator_blur(sflsqr_t* h, int32_t H, int32_t W, double sigma, in
 
 int sflsqr_set_sketch(sflsqr_t* h, uint64_t seed, int32_t d, int32_t s_nz) {
   if (!h) return fail(nullptr, SFLSQR_E_INVALID, "NULL handle");
+  if (h->o.method >= SFLSQR_METHOD_FLSQR) return SFLSQR_OK;  // unsketched methods: ignored
   if (d < 1 || d > kMaxD) return fail(h, SFLSQR_E_INVALID, "need 1 <= d <= %d", kMaxD);
   if (s_nz < 1 || s_nz > d || s_nz > 32) return fail(h, SFLSQR_E_INVALID, "need 1 <= s <= min(d, 32)");
   if (d < h->o.maxit) return fail(h, SFLSQR_E_INVALID, "need d >= maxit (k <= d for the projected problem)");
@@ -1157,11 +1184,16 @@ int sflsqr_set_rhs(sflsqr_t* h, const double* b, int64_t len, int32_t mem_flags)
   // L458 / L760: z = T w_1
   if ((rc = enqueue_transpose_product(h, true))) return rc;
   // L459: s_b = S b  |  L761-762: s = beta S z, S_TW = [S z]
-  if ((rc = enqueue_sketch(h, P.st, P.method == SFLSQR_METHOD_SFLSQR ? P.b : P.z))) return rc;
+  if (P.method <= SFLSQR_METHOD_SFLSMR &&
+      (rc = enqueue_sketch(h, P.st, P.method == SFLSQR_METHOD_SFLSQR ? P.b : P.z)))
+    return rc;
   {
-    Launch L(h, SFLSQR_KC_LS, 16.0 * h->d);
+    Launch L(h, SFLSQR_KC_LS, 16.0 * P.d);
     k_init_rhs<<<1, kVecThreads, 0, h->stream>>>(P);
   }
+  // FLSMR: the z side of step 1 (its norm is T_11) now; later steps run it one step early
+  h->host_k = 1;
+  if (P.method == SFLSQR_METHOD_FLSMR && (rc = enqueue_orth(h, 0, 0))) return rc;
   if ((rc = check_launch(h))) return rc;
   CU(h, cudaStreamSynchronize(h->stream));
   h->host_k = 1;
@@ -1338,7 +1370,7 @@ int sflsqr_debug_basis(sflsqr_t* h, double* H, double* Tm, double* Z, double* W,
   for (int j = 0; j < kd; ++j) {
     if (H) CU(h, cudaMemcpy(H + (size_t)j * (kd + 1), h->P.H + (size_t)j * (maxit + 1), sizeof(double) * (kd + 1),
                             cudaMemcpyDeviceToHost));
-    if (Tm) CU(h, cudaMemcpy(Tm + (size_t)j * kd, h->P.Tm + (size_t)j * maxit, sizeof(double) * kd,
+    if (Tm) CU(h, cudaMemcpy(Tm + (size_t)j * kd, h->P.Tm + (size_t)j * (maxit + 1), sizeof(double) * kd,
                              cudaMemcpyDeviceToHost));
   }
   if (Z && kd && h->n_loc) CU(h, cudaMemcpy(Z, h->P.Z, sizeof(double) * h->n_loc * kd, cudaMemcpyDeviceToHost));
@@ -1371,7 +1403,7 @@ int sflsqr_debug_state(sflsqr_t* h, double* z, double* x, double* p_ring, double
     else
       std::memset(p_ring, 0, sizeof(double) * h->n_loc * P.ell);
   }
-  if (sketch_cols) {
+  if (sketch_cols && P.method <= SFLSQR_METHOD_SFLSMR) {
     const int nc = P.method == SFLSQR_METHOD_SFLSQR ? kd : kd + 1;
     const double* src = P.method == SFLSQR_METHOD_SFLSQR ? P.Mcols : P.STW;
     if (nc > 0)

@@ -20,7 +20,9 @@ constexpr int kLsThreads = 512;           // one CTA solves the projected proble
 constexpr int kMaxD = 2048;               // sketch rows supported by the one-CTA LS
 constexpr int kFuseJ = 6;                 // fused orthogonalisation for windows of up to 6 vectors
 constexpr int kFuseAcc = 1 + kFuseJ + kFuseJ * (kFuseJ - 1) / 2;  // ||v||^2, dots, Gram pairs
-enum CounterIdx { CTR_BETA = 0, CTR_ZDOTS, CTR_ZAXPY, CTR_WDOTS, CTR_WAXPY, CTR_XMAX, CTR_RES, CTR_COUNT };
+constexpr int kCgsChunk = 2048;           // CGS2 dot kernel: rows of v staged in shared memory per step
+enum CounterIdx { CTR_BETA = 0, CTR_ZDOTS, CTR_ZAXPY, CTR_WDOTS, CTR_WAXPY, CTR_XMAX, CTR_RES, CTR_CGS, CTR_COUNT };
+enum OrthAlg { ORTH_FUSED = 0, ORTH_MGS = 1, ORTH_CGS2 = 2 };
 
 // Device-resident solve state (read by every kernel of a captured iteration).
 struct DevState {
@@ -41,6 +43,7 @@ struct Params {
   int64_t m, n;
   int ell, maxit, method, orth_mode, precond, d, s_nz, want_res, need_x, use_pring;
   int ldh;                 // leading dimension of H = maxit + 1
+  int ldtm;                // leading dimension of Tm = maxit + 1 (FLSMR forms column maxit+1)
   int dist;                // world > 1: reductions come from scal[] (allreduced), not from part[]
   double* scal;            // per-slot global scalars (dist)
   double* skbuf;           // d: S v of the current vector (allreduced when dist)
@@ -56,9 +59,11 @@ struct Params {
   // partial sums: nslots x kVecBlocks
   double* part;
   int slot_zin, slot_z0, slot_win, slot_w0, slot_xmax, slot_res, slot_beta;
-  int fused;               // window of <= kFuseJ vectors: one-pass dots + Gram, then one axpy pass
+  int orth_alg;            // OrthAlg: fused (window <= kFuseJ vectors), literal MGS passes, or CGS2
   int slot_zf, slot_zout, slot_wf, slot_wout;  // fused orthogonalisation slots (kFuseAcc + 1 per side)
   int* ctr;                // last-block arrival counters (one per reduction site)
+  double *cpart, *cscal;   // CGS2: (ell + 2) x kVecBlocks dot partials; 2 stages x ldc reduced dots
+  int ldc;                 // ell + 2
   // sketch
   int64_t* sk_rp;          // S stored transposed: d+1 row pointers
   uint32_t* sk_ent;         // coordinate | sign << 31, s * dim entries
@@ -603,11 +608,13 @@ __device__ __forceinline__ const double* mgs_basis(const Params& P, int side, in
   return P.Z + (int64_t)(j - 1) * P.n;
 }
 
-__global__ void __launch_bounds__(kVecThreads) k_mgs_pass(Params P, int side, int pass) {
+// koff: 0 = the current iteration; 1 = the z side of iteration k+1, run at the end of
+// iteration k by FLSMR (its projected problem needs column k+1 of T, L359-367).
+__global__ void __launch_bounds__(kVecThreads) k_mgs_pass(Params P, int side, int pass, int koff) {
   __shared__ double sh[33];
   const DevState* st = P.st;
   if (st->done) return;
-  const int k = st->k;
+  const int k = st->k + koff;
   const int J = side == 0 ? min(P.ell, k - 1) : min(P.ell + 1, k);
   if (pass > J) return;
   const int j0 = side == 0 ? max(1, k - P.ell) : max(1, k - P.ell);  // first basis index
@@ -623,7 +630,7 @@ __global__ void __launch_bounds__(kVecThreads) k_mgs_pass(Params P, int side, in
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       const int row = j0 + pass - 2;  // 0-based row of the coefficient
       if (side == 0)
-        P.Tm[(int64_t)row + (int64_t)(k - 1) * P.maxit] = cprev;
+        P.Tm[(int64_t)row + (int64_t)(k - 1) * P.ldtm] = cprev;
       else
         P.H[(int64_t)row + (int64_t)(k - 1) * P.ldh] = cprev;
     }
@@ -659,11 +666,11 @@ __global__ void __launch_bounds__(kVecThreads) k_mgs_pass(Params P, int side, in
 template <int JM>
 __device__ __forceinline__ int gram_idx(int i, int j) { return 1 + JM + j * (j - 1) / 2 + i; }
 
-__global__ void __launch_bounds__(kVecThreads) k_orth_dots(Params P, int side) {
+__global__ void __launch_bounds__(kVecThreads) k_orth_dots(Params P, int side, int koff) {
   __shared__ double red[kVecThreads / 32][kFuseAcc + 1];
   const DevState* st = P.st;
   if (st->done) return;
-  const int k = st->k;
+  const int k = st->k + koff;
   const int J = side == 0 ? min(P.ell, k - 1) : min(P.ell + 1, k);
   const int j0 = max(1, k - P.ell);
   const double* __restrict__ v = side == 0 ? P.z : P.w;
@@ -705,11 +712,11 @@ __global__ void __launch_bounds__(kVecThreads) k_orth_dots(Params P, int side) {
   last_block_reduce(P, base, kFuseAcc, side == 0 ? CTR_ZDOTS : CTR_WDOTS, false);
 }
 
-__global__ void __launch_bounds__(kVecThreads) k_orth_axpy(Params P, int side) {
+__global__ void __launch_bounds__(kVecThreads) k_orth_axpy(Params P, int side, int koff) {
   __shared__ double sh[33];
   const DevState* st = P.st;
   if (st->done) return;
-  const int k = st->k;
+  const int k = st->k + koff;
   const int J = side == 0 ? min(P.ell, k - 1) : min(P.ell + 1, k);
   const int j0 = max(1, k - P.ell);
   double* __restrict__ v = side == 0 ? P.z : P.w;
@@ -732,7 +739,7 @@ __global__ void __launch_bounds__(kVecThreads) k_orth_axpy(Params P, int side) {
     for (int j = 0; j < J; ++j) {
       const int row = j0 - 1 + j;
       if (side == 0)
-        P.Tm[(int64_t)row + (int64_t)(k - 1) * P.maxit] = c[j];
+        P.Tm[(int64_t)row + (int64_t)(k - 1) * P.ldtm] = c[j];
       else
         P.H[(int64_t)row + (int64_t)(k - 1) * P.ldh] = c[j];
     }
@@ -752,6 +759,154 @@ __global__ void __launch_bounds__(kVecThreads) k_orth_axpy(Params P, int side) {
   last_block_reduce(P, so, 1, side == 0 ? CTR_ZAXPY : CTR_WAXPY, false);
 }
 
+// ------------------------------------------------------------------ a1 / a5 for long windows: CGS2
+// Windows of more than kFuseJ vectors (full orthogonalisation: FLSQR / FLSMR, L321-373,
+// or a long sFLSQR window) are orthogonalised by classical Gram-Schmidt applied twice
+// (reading R18): c1 = Q^T v, v -= Q c1, c2 = Q^T v, v -= Q c2, coefficient = c1 + c2 —
+// the MGS coefficients of Alg. 1 L464-467 / L476-480 in exact arithmetic, with
+// orthogonality to working precision (CGS2, "twice is enough").  Each kernel streams
+// the J window vectors once (coalesced, column-major Q), so the cost is 4 reads of Q
+// instead of J launches.
+//   k_cgs_dots:   partial dots of every window vector with v; stage 0 also ||v||^2.
+//                 Block b owns a contiguous row range; v is staged through shared
+//                 memory in kCgsChunk rows, warps take window vectors round-robin.
+//   k_cgs_update: v -= sum_j c_j q_j (thread per row); stage 1 also ||v||^2 and writes
+//                 the coefficient column c1 + c2 into Tm (side 0) / H (side 1).
+__device__ __forceinline__ void cgs_window(const Params& P, int side, int kk, int& J, int& j0) {
+  J = side == 0 ? min(P.ell, kk - 1) : min(P.ell + 1, kk);
+  j0 = max(1, kk - P.ell);
+}
+
+__global__ void __launch_bounds__(kVecThreads) k_cgs_dots(Params P, int side, int stage, int koff) {
+  extern __shared__ double cg_sm[];
+  double* vs = cg_sm;                 // kCgsChunk
+  double* acc = cg_sm + kCgsChunk;    // J + 1 (ldc)
+  const DevState* st = P.st;
+  if (st->done) return;
+  int J, j0;
+  cgs_window(P, side, st->k + koff, J, j0);
+  const double* __restrict__ v = side == 0 ? P.z : P.w;
+  const int64_t len = side == 0 ? P.n : P.m;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nb = gridDim.x;
+  const int64_t per = (len + nb - 1) / nb;
+  const int64_t r0 = min(len, (int64_t)blockIdx.x * per), r1 = min(len, r0 + per);
+  for (int j = tid; j <= J; j += kVecThreads) acc[j] = 0.0;
+  double nrm = 0.0;
+  for (int64_t c0 = r0; c0 < r1; c0 += kCgsChunk) {
+    const int cl = (int)min((int64_t)kCgsChunk, r1 - c0);
+    __syncthreads();
+    for (int t = tid; t < cl; t += kVecThreads) {
+      const double vi = v[c0 + t];
+      vs[t] = vi;
+      nrm = fma(vi, vi, nrm);
+    }
+    __syncthreads();
+    for (int j = wid; j < J; j += kVecThreads / 32) {
+      const double* __restrict__ q = mgs_basis(P, side, j0 + j) + c0;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      int t = lane;
+      for (; t + 96 < cl; t += 128) {
+        a0 = fma(__ldg(q + t), vs[t], a0);
+        a1 = fma(__ldg(q + t + 32), vs[t + 32], a1);
+        a2 = fma(__ldg(q + t + 64), vs[t + 64], a2);
+        a3 = fma(__ldg(q + t + 96), vs[t + 96], a3);
+      }
+      for (; t < cl; t += 32) a0 = fma(__ldg(q + t), vs[t], a0);
+      const double a = warp_sum((a0 + a1) + (a2 + a3));
+      if (lane == 0) acc[j] += a;
+    }
+  }
+  __syncthreads();
+  if (stage == 0) {
+    // ||v||^2 (breakdown reference, reading R11) in slot J
+    __shared__ double sh[33];
+    const double t = block_sum<kVecThreads>(nrm, sh);
+    if (tid == 0) acc[J] = t;
+    __syncthreads();
+  }
+  const int ns = J + (stage == 0 ? 1 : 0);
+  for (int j = tid; j < ns; j += kVecThreads) P.cpart[(size_t)j * kVecBlocks + blockIdx.x] = acc[j];
+  // last block: fixed-order sums of the per-block partials -> cscal[stage]
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = (atomicAdd(P.ctr + CTR_CGS, 1) == nb - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  double* out = P.cscal + (size_t)stage * P.ldc;
+  for (int j = wid; j < ns; j += kVecThreads / 32) {
+    const double* pp = P.cpart + (size_t)j * kVecBlocks;
+    double a = 0.0;
+    for (int b = lane; b < nb; b += 32) a += __ldcg(pp + b);
+    a = warp_sum(a);
+    if (lane == 0) out[j] = a;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if (stage == 0) P.scal[side == 0 ? P.slot_zf : P.slot_wf] = out[J];  // ||v_in||^2 where finish_z/w look
+    P.ctr[CTR_CGS] = 0;
+  }
+}
+
+__global__ void __launch_bounds__(kVecThreads) k_cgs_update(Params P, int side, int stage, int koff) {
+  extern __shared__ double cg_sm[];
+  double* cs = cg_sm;                                                // J coefficients of this stage
+  const double** qp = reinterpret_cast<const double**>(cg_sm + P.ldc);  // J window-vector pointers
+  __shared__ double sh[33];
+  const DevState* st = P.st;
+  if (st->done) return;
+  const int kk = st->k + koff;
+  int J, j0;
+  cgs_window(P, side, kk, J, j0);
+  double* __restrict__ v = side == 0 ? P.z : P.w;
+  const int64_t len = side == 0 ? P.n : P.m;
+  const double* c = P.cscal + (size_t)stage * P.ldc;
+  for (int j = threadIdx.x; j < J; j += kVecThreads) {
+    cs[j] = c[j];
+    qp[j] = mgs_basis(P, side, j0 + j);
+  }
+  __syncthreads();
+  if (stage == 1 && blockIdx.x == 0) {
+    const double* c1 = P.cscal;
+    for (int j = threadIdx.x; j < J; j += kVecThreads) {
+      const int row = j0 - 1 + j;
+      const double cf = c1[j] + cs[j];
+      if (side == 0)
+        P.Tm[(int64_t)row + (int64_t)(kk - 1) * P.ldtm] = cf;
+      else
+        P.H[(int64_t)row + (int64_t)(kk - 1) * P.ldh] = cf;
+    }
+  }
+  double acc = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * kVecThreads + threadIdx.x; i < len; i += (int64_t)gridDim.x * kVecThreads) {
+    double vi = v[i];
+    int j = 0;
+    for (; j + 4 <= J; j += 4) {
+      const double q0 = __ldg(qp[j] + i), q1 = __ldg(qp[j + 1] + i);
+      const double q2 = __ldg(qp[j + 2] + i), q3 = __ldg(qp[j + 3] + i);
+      vi = fma(-cs[j], q0, vi);
+      vi = fma(-cs[j + 1], q1, vi);
+      vi = fma(-cs[j + 2], q2, vi);
+      vi = fma(-cs[j + 3], q3, vi);
+    }
+    for (; j < J; ++j) vi = fma(-cs[j], __ldg(qp[j] + i), vi);
+    v[i] = vi;
+    acc = fma(vi, vi, acc);
+  }
+  if (stage == 0) return;
+  acc = block_sum<kVecThreads>(acc, sh);
+  const int so = side == 0 ? P.slot_zout : P.slot_wout;
+  if (threadIdx.x == 0) P.part[(size_t)so * kVecBlocks + blockIdx.x] = acc;
+  last_block_reduce(P, so, 1, CTR_CGS, false);
+}
+
+// ||z_perp||^2 after the z-side orthogonalisation of a window of J vectors.
+template <int NT>
+__device__ __forceinline__ double z_norm2(const Params& P, int J, double* sh) {
+  return P.orth_alg != ORTH_MGS ? P.scal[P.slot_zout] : get_sum<NT>(P, P.slot_z0 + J, sh, kVecBlocks);
+}
+
 // ------------------------------------------------------------------ a1 end + a2: normalise, tau, store
 // t = ||z||, breakdown test (R11), T_kk = t, p_k = z/t, z_k = tau_k(p_k)
 // (Alg. 1; Alg. 2; readings R7/R8), Z[:,k] = z_k, P ring.
@@ -761,8 +916,8 @@ __global__ void __launch_bounds__(kVecThreads) k_finish_z(Params P) {
   if (st->done) return;
   const int k = st->k;
   const int J = min(P.ell, k - 1);
-  const double t = sqrt(P.fused ? P.scal[P.slot_zout] : get_sum<kVecThreads>(P, P.slot_z0 + J, sh, kVecBlocks));
-  const double zin = sqrt(P.fused ? P.scal[P.slot_zf] : get_sum<kVecThreads>(P, P.slot_zin, sh, kVecBlocks));
+  const double t = sqrt(z_norm2<kVecThreads>(P, J, sh));
+  const double zin = sqrt(P.orth_alg != ORTH_MGS ? P.scal[P.slot_zf] : get_sum<kVecThreads>(P, P.slot_zin, sh, kVecBlocks));
   if (t == 0.0 || t <= 1e-14 * zin) {
     __syncthreads();
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -771,7 +926,7 @@ __global__ void __launch_bounds__(kVecThreads) k_finish_z(Params P) {
     }
     return;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) P.Tm[(int64_t)(k - 1) + (int64_t)(k - 1) * P.maxit] = t;
+  if (blockIdx.x == 0 && threadIdx.x == 0) P.Tm[(int64_t)(k - 1) + (int64_t)(k - 1) * P.ldtm] = t;
   // tau weights need x_{k-1} (computed by k_xupdate at the end of iteration k-1)
   int mode = P.precond;  // 0 identity, 1 IRN, 2 NONNEG
   double eps = 0.0;
@@ -815,8 +970,9 @@ __global__ void __launch_bounds__(kVecThreads) k_finish_w(Params P) {
   if (st->done) return;
   const int k = st->k;
   const int J = min(P.ell + 1, k);
-  const double hn = sqrt(P.fused ? P.scal[P.slot_wout] : get_sum<kVecThreads>(P, P.slot_w0 + J, sh, kVecBlocks));
-  const double win = sqrt(P.fused ? P.scal[P.slot_wf] : get_sum<kVecThreads>(P, P.slot_win, sh, kVecBlocks));
+  const double hn =
+      sqrt(P.orth_alg != ORTH_MGS ? P.scal[P.slot_wout] : get_sum<kVecThreads>(P, P.slot_w0 + J, sh, kVecBlocks));
+  const double win = sqrt(P.orth_alg != ORTH_MGS ? P.scal[P.slot_wf] : get_sum<kVecThreads>(P, P.slot_win, sh, kVecBlocks));
   const bool brk = (hn == 0.0 || hn <= 1e-14 * win);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     st->wbreak = brk ? 1 : 0;
@@ -885,6 +1041,8 @@ __global__ void __launch_bounds__(kLsThreads) k_ls(Params P) {
   const int64_t ldt = P.maxit;
   int flip = 0;
   double* Mc = P.Mcols + (int64_t)c * d;
+  // FLSMR: T_{k+1,k+1} = ||z_perp|| of step k+1's z-side orthogonalisation (run just before)
+  const double tdiag = P.method == 3 ? sqrt(z_norm2<kLsThreads>(P, min(P.ell, k), sh)) : 0.0;
   double a[RPT], q[RPT];
 #pragma unroll
   for (int u = 0; u < RPT; ++u) {
@@ -892,23 +1050,39 @@ __global__ void __launch_bounds__(kLsThreads) k_ls(Params P) {
     a[u] = 0.0;
     q[u] = 0.0;
     if (r < d) {
-      const double sv = P.skbuf[r];  // S A z_k (sFLSQR) or S T w_{k+1} (sFLSMR)
       if (P.method == 0) {
+        const double sv = P.skbuf[r];  // S A z_k (sFLSQR)
         a[u] = sv;
-        Mc[r] = sv;
-      } else {
+      } else if (P.method == 1) {
+        const double sv = P.skbuf[r];  // S T w_{k+1} (sFLSMR)
         P.STW[(int64_t)(c + 1) * d + r] = sv;
         double acc = 0.0;
         for (int i = max(0, c - P.ell); i <= c; ++i)
           acc = fma(P.STW[(int64_t)i * d + r], P.H[(int64_t)i + (int64_t)c * P.ldh], acc);
         acc = fma(sv, P.H[(int64_t)(c + 1) + (int64_t)c * P.ldh], acc);
         a[u] = acc;
-        Mc[r] = acc;
+      } else if (P.method == 2) {
+        // FLSQR: column k of H_{k+1,k} (eq. FLSQR)
+        a[u] = r <= c + 1 ? P.H[(int64_t)r + (int64_t)c * P.ldh] : 0.0;
+      } else if (r <= c + 1) {
+        // FLSMR: column k of T_{k+1} H_{k+1,k} (L361-367), T upper triangular
+        double acc = 0.0;
+        for (int i = r; i <= c + 1; ++i) {
+          const double t = (i == c + 1 && r == c + 1) ? tdiag : P.Tm[(int64_t)r + (int64_t)i * P.ldtm];
+          acc = fma(t, P.H[(int64_t)i + (int64_t)c * P.ldh], acc);
+        }
+        a[u] = acc;
       }
+      Mc[r] = a[u];
       q[u] = P.qtb[r];
+      if (P.method == 3 && c == 0) {
+        q[u] = r == 0 ? st->beta * P.Tm[0] : 0.0;  // ||b|| T_{k+1} e_1 = ||b|| T_11 e_1
+        P.rhs[r] = q[u];
+      }
       a_s[r] = a[u];
     }
   }
+  if (P.method == 3 && c == 0 && tid == 0) st->rhs_norm = fabs(st->beta * P.Tm[0]);
   __syncthreads();
   if (c > 0) {
     // u = V^T a
@@ -1148,9 +1322,10 @@ __global__ void k_init_rhs(Params P) {
   const double beta = P.st->beta;
   double part = 0.0;
   for (int r = threadIdx.x; r < P.d; r += blockDim.x) {
-    const double sv = P.skbuf[r];
-    const double rv = P.method == 0 ? sv : beta * sv;
-    if (P.method != 0) P.STW[r] = sv;
+    // FLSQR: ||b|| e_1 (eq. FLSQR); FLSMR: set by k_ls at k = 1 (needs T_11)
+    const double sv = P.method <= 1 ? P.skbuf[r] : (P.method == 2 && r == 0 ? beta : 0.0);
+    const double rv = P.method == 1 ? beta * sv : sv;
+    if (P.method == 1) P.STW[r] = sv;
     P.rhs[r] = rv;
     P.qtb[r] = rv;
     part = fma(rv, rv, part);

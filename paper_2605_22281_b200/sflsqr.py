@@ -21,8 +21,10 @@ from ._build import LIB_PATH
 
 OK = 0
 E_INVALID, E_DIM, E_NONFINITE, E_ZERO_RHS, E_STATE, E_CUDA, E_OOM, E_UNSUPPORTED = -1, -2, -3, -4, -5, -6, -7, -8
-METHOD_SFLSQR, METHOD_SFLSMR = 0, 1
+METHOD_SFLSQR, METHOD_SFLSMR, METHOD_FLSQR, METHOD_FLSMR = 0, 1, 2, 3
+METHODS = {"sflsqr": METHOD_SFLSQR, "sflsmr": METHOD_SFLSMR, "flsqr": METHOD_FLSQR, "flsmr": METHOD_FLSMR}
 ORTH_P, ORTH_Z = 0, 1
+ORTHK_AUTO, ORTHK_MGS = 0, 1
 RUNNING, MAXIT, TOL, DISCREPANCY, BREAKDOWN = 0, 1, 2, 3, 4
 PRECOND_IDENTITY, PRECOND_IRN, PRECOND_NONNEG = 0, 1, 2
 T_BUILD, T_GIVEN = 0, 1
@@ -49,7 +51,8 @@ class Opts(ctypes.Structure):
                 ("delta_e", ctypes.c_double), ("history", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("stream", ctypes.c_void_p), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
                 ("use_graph", ctypes.c_int32), ("comm_kind", ctypes.c_int32), ("nccl_id", ctypes.c_void_p),
-                ("local_group", ctypes.c_void_p), ("reserved", ctypes.c_int32 * 4)]
+                ("local_group", ctypes.c_void_p), ("orth_kernel", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 3)]
 
 
 class Info(ctypes.Structure):
@@ -148,10 +151,11 @@ class SFLSQR:
 
     def __init__(self, method="sflsqr", window=2, maxit=10, orth_mode="P", tol=0.0, eta=0.0, delta_e=0.0,
                  history=HIST_TRUE_RES, device=0, stream=None, use_graph=True, rank=0, world=1, nccl_id=None,
-                 local_group=None):
+                 local_group=None, orth_kernel="auto"):
         self.lib = load_library()
         o = Opts()
-        o.method = METHOD_SFLSQR if method == "sflsqr" else METHOD_SFLSMR if method == "sflsmr" else -1
+        o.method = METHODS.get(method, -1)
+        o.orth_kernel = ORTHK_MGS if orth_kernel == "mgs" else ORTHK_AUTO
         o.window, o.maxit = int(window), int(maxit)
         o.orth_mode = ORTH_P if orth_mode == "P" else ORTH_Z
         o.tol, o.eta, o.delta_e = float(tol), float(eta), float(delta_e)
@@ -303,7 +307,7 @@ class SFLSQR:
         kd = info["k_done"]
         z, x = np.zeros(self.n), np.zeros(self.n)
         ring = np.zeros((window, self.n))
-        nc = kd if method == "sflsqr" else kd + 1
+        nc = kd if method == "sflsqr" else kd + 1 if method == "sflsmr" else 0
         cols = np.zeros((d, max(nc, 1)), order="F")
         rhs = np.zeros(d)
         self._check(self.lib.sflsqr_debug_state(self.h, z.ctypes.data, x.ctypes.data, ring.ctypes.data,
@@ -359,12 +363,13 @@ class LocalGroup:
 
 
 def solver_for_problem(prob, spec, maxit=None, history=HIST_TRUE_RES, use_graph=True, eta=None, device=0,
-                       operator_on_device=False):
-    """Configure an SFLSQR handle for a gen.Problem / gen.SolverSpec (marshalling only)."""
+                       operator_on_device=False, method=None, orth_kernel="auto"):
+    """Configure an SFLSQR handle for a gen.Problem / gen.SolverSpec (marshalling only).
+    method overrides spec.method (e.g. "flsqr" / "flsmr" on a config's operator)."""
     mx = maxit or spec.maxit
-    s = SFLSQR(method=spec.method, window=spec.window, maxit=mx, orth_mode=spec.orth_mode, tol=spec.tol,
+    s = SFLSQR(method=method or spec.method, window=spec.window, maxit=mx, orth_mode=spec.orth_mode, tol=spec.tol,
                eta=spec.eta if eta is None else eta, delta_e=prob.delta_e, history=history, device=device,
-               use_graph=use_graph)
+               use_graph=use_graph, orth_kernel=orth_kernel)
     if prob.t_mode == "same":
         bl = prob.blur
         s.set_operator_blur(bl["H"], bl["W"], bl["sigma"], bl["radius"])

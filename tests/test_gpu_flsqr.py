@@ -1,0 +1,156 @@
+"""GPU parity of the unsketched full-orthogonalisation methods FLSQR / FLSMR
+ and of the CGS2 orthogonalisation kernel
+used for long windows (reading R18), through the C ABI, against the fp64
+oracle (oracle/sflsqr.py, pinned in tests/test_oracle_flsqr.py).
+
+Same bar as tests/test_gpu_parity.py: per-iteration true and projected residuals within
+1e-9 relative over the iterations where the oracle itself is forward-stable, final x
+within 1e-6, identical status and stop index.
+"""
+import numpy as np
+import pytest
+
+from gen import make_problem
+from gen.problems import SolverSpec
+from oracle.operators import operator_from_problem
+from oracle.sflsqr import solve_problem
+
+pytestmark = pytest.mark.gpu
+
+RES_TOL = 1e-9
+X_TOL = 1e-6
+
+
+@pytest.fixture(scope="session", autouse=True)
+def _lib():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2605_22281_b200._build import build_library
+    build_library()
+
+
+def _gpu_run(prob, spec, maxit, method, eta=0.0, orth_kernel="auto", use_graph=True):
+    from paper_2605_22281_b200 import solver_for_problem
+    s = solver_for_problem(prob, spec, maxit=maxit, eta=eta, method=method, orth_kernel=orth_kernel,
+                           use_graph=use_graph)
+    s.set_rhs(prob.b)
+    done, status = s.iterate(maxit)
+    tr, pr = s.get_residual_norms()
+    x = s.get_x()
+    info = s.get_info()
+    basis = s.debug_basis()
+    s.close()
+    return dict(done=done, status=status, true_res=tr, proj_res=pr, x=x, info=info, basis=basis)
+
+
+def _stable_horizon(p, spec, maxit, method, thresh=1e-11):
+    """Last k up to which the oracle itself is forward-stable (reading R17)."""
+    op = operator_from_problem(p)
+    r0 = solve_problem(p, spec, op=op, maxit=maxit, eta=0.0, method=method)
+    b0 = p.b
+    p.b = b0 * (1 + 1e-15 * np.random.default_rng(0).standard_normal(b0.size))
+    try:
+        r1 = solve_problem(p, spec, op=op, maxit=maxit, eta=0.0, method=method)
+    finally:
+        p.b = b0
+    dev = np.abs(np.array(r1.true_res) - np.array(r0.true_res)) / np.array(r0.true_res)
+    bad = np.flatnonzero(dev > thresh)
+    return (int(bad[0]) if bad.size else len(dev)), r0
+
+
+def _compare(g, r, n_res):
+    kk = len(r.true_res)
+    assert g["info"]["k_done"] == kk and g["status"] == r.status and g["info"]["k_x"] == r.k
+    n = min(n_res, kk)
+    rt = np.abs(g["true_res"][:n] - np.array(r.true_res[:n])) / np.array(r.true_res[:n])
+    rp = np.abs(g["proj_res"][:n] - np.array(r.sketch_res[:n])) / np.array(r.sketch_res[:n])
+    ex = np.linalg.norm(g["x"] - r.x) / max(np.linalg.norm(r.x), 1e-300)
+    assert rt.max() < RES_TOL, ("true residual", rt.max(), int(rt.argmax()) + 1)
+    assert rp.max() < RES_TOL, ("projected residual", rp.max(), int(rp.argmax()) + 1)
+    assert ex < X_TOL, ("x", ex)
+    return rt.max(), rp.max(), ex
+
+
+@pytest.mark.parametrize("method", ["flsqr", "flsmr"])
+def test_config1_flsqr_flsmr(method):
+    p = make_problem(1)
+    spec = p.solvers[0]                               # IRN-l1, 40 iterations
+    kstar, r = _stable_horizon(p, spec, 40, method)
+    assert kstar >= 20, kstar
+    g = _gpu_run(p, spec, 40, method)
+    r40 = r
+    # strict bar up to the oracle's stable horizon; identical status and stop index at 40
+    assert g["status"] == r40.status and g["info"]["k_done"] == len(r40.true_res)
+    rk = solve_problem(p, spec, maxit=kstar, eta=0.0, method=method)
+    gk = _gpu_run(p, spec, kstar, method)
+    _compare(gk, rk, kstar)
+
+
+@pytest.mark.parametrize("method", ["flsqr", "flsmr"])
+def test_config3_reduced_flsqr_flsmr(method):
+    p = make_problem(3, N=128, n_angles=90, nb=183)   # Siddon, NONNEG tau
+    spec = p.solvers[0]
+    kstar, _ = _stable_horizon(p, spec, 60, method)
+    assert kstar >= 15, kstar
+    r = solve_problem(p, spec, maxit=kstar, eta=0.0, method=method)
+    g = _gpu_run(p, spec, kstar, method)
+    _compare(g, r, kstar)
+    # full orthogonality of the GPU basis (eq. flsqr-relations)
+    W = g["basis"]["W"]
+    assert np.abs(W.T @ W - np.eye(W.shape[1])).max() < 1e-12
+
+
+@pytest.mark.parametrize("method", ["flsqr", "flsmr"])
+def test_config4_reduced_unmatched(method):
+    p = make_problem(4, N=160, n_angles=113, nb=227)  # unmatched B, identity tau
+    spec = p.solvers[0]
+    kstar, _ = _stable_horizon(p, spec, 50, method)
+    assert kstar >= 10, kstar
+    r = solve_problem(p, spec, maxit=kstar, eta=0.0, method=method)
+    g = _gpu_run(p, spec, kstar, method)
+    _compare(g, r, kstar)
+
+
+@pytest.mark.parametrize("method", ["flsqr", "flsmr"])
+def test_config2_blur(method):
+    p = make_problem(2)
+    spec = p.solvers[0]
+    kstar, _ = _stable_horizon(p, spec, 40, method)
+    assert kstar >= 15, kstar
+    r = solve_problem(p, spec, maxit=kstar, eta=0.0, method=method)
+    g = _gpu_run(p, spec, kstar, method)
+    _compare(g, r, kstar)
+
+
+@pytest.mark.parametrize("method", ["flsqr", "flsmr"])
+def test_discrepancy_stop_and_literal_mgs_kernel(method):
+    p = make_problem(1)
+    spec = p.solvers[0]
+    full = solve_problem(p, spec, maxit=20, eta=0.0, method=method)
+    eta = float(full.true_res[9] / p.delta_e) * (1 + 1e-7)
+    r = solve_problem(p, spec, maxit=20, eta=eta, method=method)
+    assert r.status == 3
+    for ok in ("auto", "mgs"):
+        g = _gpu_run(p, spec, 20, method, eta=eta, orth_kernel=ok)
+        _compare(g, r, 20)
+
+
+def test_cgs2_and_mgs_kernels_agree_on_long_sketched_window():
+    # sFLSQR with window 12 (> 6: CGS2 in auto mode) vs the literal MGS pass kernels
+    p = make_problem(3, N=96, n_angles=70, nb=137)
+    spec = SolverSpec(method="sflsqr", maxit=30, window=12, d=60, s_nz=8, precond="nonneg")
+    ga = _gpu_run(p, spec, 30, "sflsqr", orth_kernel="auto")
+    gm = _gpu_run(p, spec, 30, "sflsqr", orth_kernel="mgs")
+    r = solve_problem(p, spec, maxit=30, eta=0.0)
+    for g in (ga, gm):
+        rt = np.abs(g["true_res"][:20] - np.array(r.true_res[:20])) / np.array(r.true_res[:20])
+        assert rt.max() < RES_TOL, rt.max()
+
+
+def test_graph_and_eager_agree_bitwise_flsmr():
+    p = make_problem(1)
+    spec = p.solvers[0]
+    g1 = _gpu_run(p, spec, 25, "flsmr", use_graph=False)
+    g2 = _gpu_run(p, spec, 25, "flsmr", use_graph=True)
+    assert np.array_equal(g1["x"], g2["x"]) and np.array_equal(g1["proj_res"], g2["proj_res"])
