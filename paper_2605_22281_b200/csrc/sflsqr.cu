@@ -17,6 +17,7 @@
 #include <thread>
 #include <vector>
 
+#include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 
 #include "comm.h"
@@ -40,12 +41,24 @@ struct Prof {
 
 enum TKind { T_FULL = 0, T_ROWSHARD = 1, T_COLSHARD = 2 };
 
+// CSR-16 copy of an operator's column indices (k_spmv_c16): per-chunk int32 base,
+// 16-bit offsets, chunk pointer per row.  ok = false: the operator stays int32 CSR.
+struct C16 {
+  bool ok = false;
+  int64_t nchunks = 0;
+  int64_t* cptr = nullptr;
+  int* base = nullptr;
+  uint16_t* off = nullptr;
+};
+
 }  // namespace
 
 struct sflsqr {
   sflsqr_opts o;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  cudaStream_t side = nullptr;  // second stream: the projected LS overlaps the T product (fork/join)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::string err;
   // distribution
   int rank = 0, world = 1;
@@ -63,6 +76,7 @@ struct sflsqr {
   int bH = 0, bW = 0, brad = 0;
   double* taps = nullptr;
   double* blur_tmp = nullptr;
+  C16 ca, ct;           // CSR-16 index copies of A and T (default SpMV format when ok)
   // sketch
   bool sk_set = false;
   uint64_t seed = 0;
@@ -248,6 +262,12 @@ void free_op(sflsqr_t* h) {
   }
   cudaFree(h->taps);
   cudaFree(h->blur_tmp);
+  for (C16* c : {&h->ca, &h->ct}) {
+    cudaFree(c->cptr);
+    cudaFree(c->base);
+    cudaFree(c->off);
+    *c = C16();
+  }
   h->a_rowptr = h->t_rowptr = nullptr;
   h->a_col = h->t_col = nullptr;
   h->a_val = h->t_val = h->taps = h->blur_tmp = nullptr;
@@ -276,6 +296,10 @@ struct Launch {
       p.bytes[p.used] = bytes;
       cudaEventRecord(p.ev[2 * p.used], h->stream);
     }
+  }
+  void bytes_override(double b) {
+    bytes = b;
+    if (h->prof_on) h->prof.bytes[h->prof.used] = b;
   }
   ~Launch() {
     if (h->prof_on) {
@@ -359,7 +383,16 @@ void enqueue_apply(sflsqr_t* h, int which, const DevState* st, const double* x, 
     const int64_t want = (nrows + rows_per_cta - 1) / rows_per_cta;
     return (int)std::max<int64_t>(1, std::min<int64_t>(want, 148 * per_sm));
   };
-  const int mode = h->spmv_mode >= 0 ? h->spmv_mode : select_spmv_mode(nnz, nrows);
+  const C16& cc = which == 0 ? h->ca : h->ct;
+  int mode = h->spmv_mode >= 0 ? h->spmv_mode : select_spmv_mode(nnz, nrows);
+  if (mode == 15 && !cc.ok) mode = 14;
+  if (mode == 15) {
+    // CSR-16: 8 (value) + 2 (offset) bytes per nonzero + 4 per 16-entry chunk + chunk pointers
+    L.bytes_override(10.0 * nnz + 4.0 * cc.nchunks + 16.0 * (nrows + 1) + 8.0 * xlen + 8.0 * nrows);
+    k_spmv_c16<16, 4><<<grid_for(32, 4), 512, 0, h->stream>>>(st, nrows, rp, cc.cptr, cc.base, cc.off, val, x, x_ld,
+                                                                x_koff, y);
+    return;
+  }
   switch (mode) {
     case 0:
       k_spmv_csr<<<grid_for(kSpmvThreads / 32, 8), kSpmvThreads, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld,
@@ -483,6 +516,29 @@ int enqueue_orth(sflsqr_t* h, int side, int koff) {
   return SFLSQR_OK;
 }
 
+// a7: the one-CTA projected LS, on the main stream or forked onto the side stream
+// (event fork on the main stream, join event recorded on the side stream).
+int enqueue_ls(sflsqr_t* h, bool forked) {
+  Params& P = h->P;
+  cudaStream_t st = h->stream;
+  if (forked) {
+    CU(h, cudaEventRecord(h->ev_fork, h->stream));
+    CU(h, cudaStreamWaitEvent(h->side, h->ev_fork, 0));
+    st = h->side;
+  }
+  {
+    Launch L(h, SFLSQR_KC_LS, 8.0 * P.d * (h->host_k + 2));
+    if (P.d <= kLsThreads)
+      k_ls<1><<<1, kLsThreads, 3 * 1 * kLsThreads * sizeof(double), st>>>(P);
+    else if (P.d <= 2 * kLsThreads)
+      k_ls<2><<<1, kLsThreads, 3 * 2 * kLsThreads * sizeof(double), st>>>(P);
+    else
+      k_ls<4><<<1, kLsThreads, 3 * 4 * kLsThreads * sizeof(double), st>>>(P);
+  }
+  if (forked) CU(h, cudaEventRecord(h->ev_join, h->side));
+  return SFLSQR_OK;
+}
+
 // One iteration k of Alg. 1 / Alg. 2, or of FLSQR /
 // FLSMR (full window, no sketch; FLSMR runs the z side of step k+1 before its
 // projected problem, which needs column k+1 of T).
@@ -510,12 +566,19 @@ int enqueue_iteration(sflsqr_t* h) {
   }
   // a4 (sFLSQR): S_AZ[:, k] = S w
   if (P.method == SFLSQR_METHOD_SFLSQR && (rc = enqueue_sketch(h, P.st, P.w))) return rc;
+  // a7 can start now for sFLSQR (it needs only S A Z_k) / after a5 for FLSQR (it needs
+  // H_{:,k}): it runs on the side stream, overlapped with the T product (a6), and is
+  // joined before a8.  Sequential when profiling (clean per-kernel events).
+  const bool fork_ls = !h->prof_on && h->side &&
+                       (P.method == SFLSQR_METHOD_SFLSQR || P.method == SFLSQR_METHOD_FLSQR);
+  if (fork_ls && P.method == SFLSQR_METHOD_SFLSQR && (rc = enqueue_ls(h, true))) return rc;
   // a5: w-side windowed orthogonalisation and normalisation
   if ((rc = enqueue_orth(h, 1, 0))) return rc;
   {
     Launch L(h, SFLSQR_KC_ORTH, 2 * m8);
     k_finish_w<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P);
   }
+  if (fork_ls && P.method == SFLSQR_METHOD_FLSQR && (rc = enqueue_ls(h, true))) return rc;
   // a6: z = T w_{k+1}  (w_{k+1} = W[:, k])
   if ((rc = enqueue_transpose_product(h, false))) return rc;
   // a4 (sFLSMR): S z -> S_TW[:, k+1]
@@ -524,14 +587,10 @@ int enqueue_iteration(sflsqr_t* h) {
   if (P.method == SFLSQR_METHOD_FLSMR && (rc = enqueue_orth(h, 0, 1))) return rc;
   // a7: projected (sketched) LS (replicated on every rank: identical inputs)
   (void)sketched;
-  {
-    Launch L(h, SFLSQR_KC_LS, 8.0 * P.d * (k + 2));
-    if (P.d <= kLsThreads)
-      k_ls<1><<<1, kLsThreads, 3 * 1 * kLsThreads * sizeof(double), h->stream>>>(P);
-    else if (P.d <= 2 * kLsThreads)
-      k_ls<2><<<1, kLsThreads, 3 * 2 * kLsThreads * sizeof(double), h->stream>>>(P);
-    else
-      k_ls<4><<<1, kLsThreads, 3 * 4 * kLsThreads * sizeof(double), h->stream>>>(P);
+  if (fork_ls) {
+    CU(h, cudaStreamWaitEvent(h->stream, h->ev_join, 0));
+  } else if ((rc = enqueue_ls(h, false))) {
+    return rc;
   }
   // a8: x_k = Z_k y_k (needed by tau_{k+1})
   if (P.need_x) {
@@ -541,19 +600,89 @@ int enqueue_iteration(sflsqr_t* h) {
     }
     if ((rc = coll_allreduce(h, P.scal + P.slot_xmax, 1, true))) return rc;
   }
-  // a9: true residual (W path) and stop tests
+  // a9: true residual (W path) and stop tests (fused into the residual kernel on one rank)
+  const bool fuse_stop = P.want_res && h->world == 1 && !h->prof_on;
   if (P.want_res) {
     {
       Launch L(h, SFLSQR_KC_RES, m8 * (k + 1));
-      k_res_partial<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P);
+      k_res_partial<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P, fuse_stop ? 1 : 0);
     }
     if ((rc = coll_allreduce(h, P.scal + P.slot_res, 1, false))) return rc;
   }
-  {
+  if (!fuse_stop) {
     Launch L(h, SFLSQR_KC_STOP, 0.0);
-    k_stop<<<1, kVecThreads, 0, h->stream>>>(P);
+    k_stop<<<1, 32, 0, h->stream>>>(P);
   }
   return SFLSQR_OK;
+}
+
+// Build the CSR-16 copy of a device CSR (nrows x *, nnz entries); leaves c.ok = false
+// when a 16-entry chunk spans more than 65536 columns.
+int build_c16(sflsqr_t* h, int64_t nrows, const int64_t* rp, const int32_t* col, int64_t nnz, C16& c) {
+  c = C16();
+  if (nrows < 1 || nnz < 1) return SFLSQR_OK;
+  int64_t* cnt = nullptr;
+  void* tmp = nullptr;
+  int* flag = nullptr;
+  size_t tmp_bytes = 0;
+  int rc;
+  auto cleanup = [&]() {
+    cudaFree(cnt);
+    cudaFree(tmp);
+    cudaFree(flag);
+  };
+  if ((rc = dalloc(h, (void**)&cnt, sizeof(int64_t) * (nrows + 1), nullptr)) ||
+      (rc = dalloc(h, (void**)&c.cptr, sizeof(int64_t) * (nrows + 1), nullptr)) ||
+      (rc = dalloc(h, (void**)&flag, sizeof(int), nullptr))) {
+    cleanup();
+    return rc;
+  }
+  const int g = (int)std::min<int64_t>((nrows + 256) / 256 + 1, 148 * 16);
+  k_c16_count<<<g, 256, 0, h->stream>>>(nrows, rp, cnt);
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, c.cptr, nrows + 1, h->stream);
+  if ((rc = dalloc(h, &tmp, tmp_bytes, nullptr))) {
+    cleanup();
+    return rc;
+  }
+  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, c.cptr, nrows + 1, h->stream);
+  CU(h, cudaMemcpyAsync(&c.nchunks, c.cptr + nrows, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+  CU(h, cudaMemsetAsync(flag, 0, sizeof(int), h->stream));
+  CU(h, cudaStreamSynchronize(h->stream));
+  if ((rc = dalloc(h, (void**)&c.base, sizeof(int) * std::max<int64_t>(c.nchunks, 1), nullptr)) ||
+      (rc = dalloc(h, (void**)&c.off, sizeof(uint16_t) * nnz, nullptr))) {
+    cleanup();
+    return rc;
+  }
+  const int gf = (int)std::min<int64_t>((nrows + 15) / 16 + 1, 148 * 32);
+  k_c16_fill<<<gf, 256, 0, h->stream>>>(nrows, rp, col, c.cptr, c.base, c.off, flag);
+  int ovf = 0;
+  CU(h, cudaMemcpyAsync(&ovf, flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CU(h, cudaStreamSynchronize(h->stream));
+  cleanup();
+  if (ovf) {
+    cudaFree(c.cptr);
+    cudaFree(c.base);
+    cudaFree(c.off);
+    c = C16();
+    return SFLSQR_OK;
+  }
+  c.ok = true;
+  return SFLSQR_OK;
+}
+
+// Built only on request (sflsqr_debug_set_tuning(h, 15, ...)): measured slower than the
+// int32 CSR kernel on the CT operators, so it costs no memory by default.
+int build_c16_all(sflsqr_t* h) {
+  int rc;
+  if (h->blur || (h->ca.ok && h->ct.ok)) return SFLSQR_OK;
+  for (C16* c : {&h->ca, &h->ct}) {
+    cudaFree(c->cptr);
+    cudaFree(c->base);
+    cudaFree(c->off);
+    *c = C16();
+  }
+  if ((rc = build_c16(h, h->m_loc, h->a_rowptr, h->a_col, h->nnz_a, h->ca))) return rc;
+  return build_c16(h, h->t_rows, h->t_rowptr, h->t_col, h->nnz_t, h->ct);
 }
 
 int check_launch(sflsqr_t* h) {
@@ -680,7 +809,7 @@ int alloc_solve(sflsqr_t* h) {
       (rc = A(&P.Mcols, (size_t)d * maxit)) || (rc = A(&P.STW, (size_t)d * (maxit + 1))) ||
       (rc = A(&P.V, (size_t)d * maxit)) || (rc = A(&P.taus, maxit)) || (rc = A(&P.R, (size_t)maxit * maxit)) ||
       (rc = A(&P.Tw, (size_t)maxit * maxit)) ||
-      (rc = A(&P.qtb, d)) || (rc = A(&P.y, maxit)) || (rc = A(&P.g, maxit + 1)) || (rc = A(&P.hist_true, maxit)) ||
+      (rc = A(&P.qtb, d)) || (rc = A(&P.y, maxit)) || (rc = A(&P.hist_true, maxit)) ||
       (rc = A(&P.hist_sk, maxit)))
     return rc;
   if (P.use_pring && (rc = A(&P.Pring, n * ell))) return rc;
@@ -884,6 +1013,12 @@ int sflsqr_create(sflsqr_t** out, const sflsqr_opts* o) {
     }
   }
   if (const char* ev = std::getenv("SFLSQR_SPMV_MODE")) h->spmv_mode = std::atoi(ev);
+  if (cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();
+    h->side = nullptr;  // no overlap; the LS runs on the main stream
+  }
   cudaFuncSetAttribute(k_ls<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 4 * kLsThreads * (int)sizeof(double));
   cudaGetLastError();
   *out = h;
@@ -1004,7 +1139,7 @@ int sflsqr_set_operator_shard(sflsqr_t* h, int64_t m, int64_t n, int64_t a_row0,
     rc = upload_csr(h, h->t_rows, trp.data(), tcol.data(), tval.data(), &h->t_rowptr, &h->t_col, &h->t_val,
                     &h->nnz_t);
   }
-  if (rc) {
+  if (rc || (h->spmv_mode == 15 && (rc = build_c16_all(h)))) {
     free_op(h);
     return rc;
   }
@@ -1051,6 +1186,7 @@ int sflsqr_set_operator(sflsqr_t* h, int64_t m, int64_t n, const int64_t* a_rowp
   h->tkind = T_FULL;
   h->nnz_a = nnz_a;
   h->nnz_t = nnz_t;
+  int rc0;
   if (borrow) {
     h->a_owned = h->t_owned = false;
     h->a_rowptr = (int64_t*)a_rowptr;
@@ -1072,6 +1208,10 @@ int sflsqr_set_operator(sflsqr_t* h, int64_t m, int64_t n, const int64_t* a_rowp
       free_op(h);
       return rc;
     }
+  }
+  if (h->spmv_mode == 15 && (rc0 = build_c16_all(h))) {
+    free_op(h);
+    return rc0;
   }
   h->op_set = true;
   return SFLSQR_OK;
@@ -1418,10 +1558,14 @@ int sflsqr_debug_state(sflsqr_t* h, double* z, double* x, double* p_ring, double
 int sflsqr_debug_set_tuning(sflsqr_t* h, int32_t spmv_mode, int32_t band_shift) {
   if (!h) return fail(nullptr, SFLSQR_E_INVALID, "NULL handle");
   const bool ok_mode = spmv_mode == -1 || spmv_mode == 0 || spmv_mode == 1 || spmv_mode == 2 || spmv_mode == 3 ||
-                       spmv_mode == 8 || (spmv_mode >= 10 && spmv_mode <= 14);
+                       spmv_mode == 8 || (spmv_mode >= 10 && spmv_mode <= 15);
   if (!ok_mode || band_shift < 8 || band_shift > 30) return fail(h, SFLSQR_E_INVALID, "bad tuning values");
   h->spmv_mode = spmv_mode;
   h->band_shift = band_shift;
+  if (spmv_mode == 15 && h->op_set) {
+    int rc = build_c16_all(h);
+    if (rc) return rc;
+  }
   if (h->gexec) {
     cudaGraphExecDestroy(h->gexec);
     h->gexec = nullptr;
@@ -1457,6 +1601,9 @@ void sflsqr_destroy(sflsqr_t* h) {
   free_op(h);
   for (auto e : h->prof.ev) cudaEventDestroy(e);
   delete h->comm;
+  if (h->side) cudaStreamDestroy(h->side);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
   if (h->own_stream) cudaStreamDestroy(h->stream);
   delete h;
 }

@@ -6,6 +6,7 @@
 // consumer (no floating-point atomics).
 #pragma once
 
+#include <climits>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -69,7 +70,7 @@ struct Params {
   uint32_t* sk_ent;         // coordinate | sign << 31, s * dim entries
   double *rhs, *Mcols, *STW;
   // projected LS
-  double *V, *taus, *R, *Tw, *qtb, *y, *g;   // Tw: compact-WY factor (maxit x maxit)
+  double *V, *taus, *R, *Tw, *qtb, *y;   // Tw: compact-WY factor (maxit x maxit)
   // history
   double *hist_true, *hist_sk;
 };
@@ -134,7 +135,7 @@ __device__ __forceinline__ double max_partials(const double* part, int nb, doubl
 // Last-block reduction: every block has written part[(s0+t)*kVecBlocks + blockIdx.x]
 // for t < ns; the last block to arrive (threadfence + arrival counter, no waiting)
 // sums them in block order into scal[s0+t] (deterministic) and resets the counter.
-__device__ __forceinline__ void last_block_reduce(const Params& P, int s0, int ns, int ctr_idx, bool is_max);
+__device__ __forceinline__ bool last_block_reduce(const Params& P, int s0, int ns, int ctr_idx, bool is_max);
 
 // A reduced quantity of slot `slot`: single rank -> sum the per-block partials in
 // block order here; several ranks -> the allreduced scalar (k_reduce_slots + comm).
@@ -154,13 +155,13 @@ __device__ __forceinline__ double get_max(const Params& P, int slot, double* sh,
   return max_partials<NT>(P.part + (size_t)slot * nb, nb, sh);
 }
 
-__device__ __forceinline__ void last_block_reduce(const Params& P, int s0, int ns, int ctr_idx, bool is_max) {
+__device__ __forceinline__ bool last_block_reduce(const Params& P, int s0, int ns, int ctr_idx, bool is_max) {
   __shared__ int s_last;
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) s_last = (atomicAdd(P.ctr + ctr_idx, 1) == (int)gridDim.x - 1);
   __syncthreads();
-  if (!s_last) return;
+  if (!s_last) return false;
   __threadfence();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int nb = gridDim.x;
@@ -175,6 +176,8 @@ __device__ __forceinline__ void last_block_reduce(const Params& P, int s0, int n
     if (lane == 0) P.scal[s0 + t] = acc;
   }
   if (threadIdx.x == 0) P.ctr[ctr_idx] = 0;
+  __syncthreads();
+  return true;
 }
 
 // Streaming (read-once) loads: bypass L1 allocation so L1 keeps the gathered vector.
@@ -461,6 +464,130 @@ __global__ void __launch_bounds__(WPB * 32, 2048 / (WPB * 32)) k_spmv_csr_pf(con
 #pragma unroll
     for (int o = LANES / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
     if (sl == 0 && row < nrows) y[row] = sum;
+  }
+}
+
+// ------------------------------------------------------------------ a3 / a6: CSR-16 (compressed column indices)
+// Same traversal as k_spmv_csr_pf<WPB, UNR, 16> (half-warp rows, 16-entry lane-strided
+// chunks, next UNR chunks prefetched), but the int32 column index of entry q of row i
+// is stored as a 16-bit offset from a per-chunk base:
+//     col[q] = cbase[cptr[i] + (q - rowptr[i]) / 16] + off[q]
+// (chunks of 16 consecutive entries of a row, aligned to the row start; cptr[i] = number
+// of chunks of rows < i).  10.25 instead of 12 bytes per nonzero are streamed; the
+// gathered x, the summation order and therefore the result are bit-identical to the
+// int32 CSR kernels.  Built on the device from the CSR (k_c16_count / k_c16_fill) when
+// every chunk's column range fits 16 bits (always for the CT operators).
+__device__ __forceinline__ int ld_stream_u16(const uint16_t* p) {
+  unsigned short r;
+  asm volatile("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=h"(r) : "l"(p));
+  return (int)r;
+}
+
+template <int WPB, int UNR>
+__global__ void __launch_bounds__(WPB * 32, 2048 / (WPB * 32)) k_spmv_c16(const DevState* st, int64_t nrows,
+                                                            const int64_t* __restrict__ rowptr,
+                                                            const int64_t* __restrict__ cptr,
+                                                            const int* __restrict__ cbase,
+                                                            const uint16_t* __restrict__ off,
+                                                            const double* __restrict__ val,
+                                                            const double* __restrict__ x_base, int64_t x_ld,
+                                                            int x_koff, double* __restrict__ y) {
+  if (st && st->done) return;
+  const double* __restrict__ x = kvec(st, x_base, x_ld, x_koff);
+  constexpr int LANES = 16, RPW = 2;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int sl = lane % LANES, sub = lane / LANES;
+  for (int64_t r0 = (int64_t)blockIdx.x * WPB * RPW; r0 < nrows; r0 += (int64_t)gridDim.x * WPB * RPW) {
+    const int64_t row = r0 + (int64_t)wid * RPW + sub;
+    int64_t s = 0, e = 0;
+    const int* cb = cbase;
+    if (row < nrows) {
+      s = rowptr[row];
+      e = rowptr[row + 1];
+      cb = cbase + cptr[row];
+    }
+    double sum = 0.0;
+    int64_t p = s + sl;
+    int ch = 0;  // chunk of p within the row
+    int cn[UNR];
+    double vn[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int64_t q = p + (int64_t)LANES * u;
+      cn[u] = q < e ? __ldg(cb + ch + u) + ld_stream_u16(off + q) : 0;
+      vn[u] = q < e ? ld_stream_d(val + q) : 0.0;
+    }
+    while (__any_sync(0xffffffffu, p < e)) {
+      int c[UNR];
+      double v[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        c[u] = cn[u];
+        v[u] = vn[u];
+      }
+      const int64_t pn = p + (int64_t)LANES * UNR;
+      const int chn = ch + UNR;
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int64_t q = pn + (int64_t)LANES * u;
+        cn[u] = q < e ? __ldg(cb + chn + u) + ld_stream_u16(off + q) : 0;
+        vn[u] = q < e ? ld_stream_d(val + q) : 0.0;
+      }
+      double xv[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) xv[u] = (p + (int64_t)LANES * u < e) ? __ldg(x + c[u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < UNR; ++u)
+        if (p + (int64_t)LANES * u < e) sum = fma(v[u], xv[u], sum);
+      p = pn;
+      ch = chn;
+    }
+#pragma unroll
+    for (int o = LANES / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (sl == 0 && row < nrows) y[row] = sum;
+  }
+}
+
+// CSR-16 construction: chunks per row, then (after an exclusive scan into cptr) the
+// per-chunk minimum column as base and the 16-bit offsets; *overflow = 1 if a chunk's
+// column range exceeds 65535 (the operator then stays in int32 CSR).
+__global__ void k_c16_count(int64_t nrows, const int64_t* __restrict__ rowptr, int64_t* __restrict__ cnt) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= nrows; i += (int64_t)gridDim.x * blockDim.x)
+    cnt[i] = i < nrows ? (rowptr[i + 1] - rowptr[i] + 15) / 16 : 0;
+}
+__global__ void k_c16_fill(int64_t nrows, const int64_t* __restrict__ rowptr, const int* __restrict__ col,
+                           const int64_t* __restrict__ cptr, int* __restrict__ cbase, uint16_t* __restrict__ off,
+                           int* overflow) {
+  const int lane = threadIdx.x & 31, sl = lane & 15;
+  const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;   // warp: rows 2wg, 2wg+1
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r0 = 2 * wg; r0 < nrows; r0 += 2 * nw) {
+    const int64_t row = r0 + (lane >> 4);
+    const bool valid = row < nrows;
+    const int64_t s = valid ? rowptr[row] : 0, e = valid ? rowptr[row + 1] : 0;
+    const int64_t nch = (e - s + 15) / 16;
+    const int64_t c0 = valid ? cptr[row] : 0;
+    // both half-warps loop to the larger chunk count (shuffles need the full warp)
+    const int64_t other = __shfl_xor_sync(0xffffffffu, nch, 16);
+    const int64_t nmax = nch > other ? nch : other;
+    for (int64_t ch = 0; ch < nmax; ++ch) {
+      const int64_t q = s + ch * 16 + sl;
+      const bool in = ch < nch && q < e;
+      const int c = in ? col[q] : 0;
+      int mn = in ? c : INT_MAX, mx = in ? c : INT_MIN;
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) {
+        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      }
+      if (ch < nch) {
+        if (sl == 0) {
+          cbase[c0 + ch] = mn;
+          if ((int64_t)mx - (int64_t)mn > 65535) *overflow = 1;
+        }
+        if (in) off[q] = (uint16_t)(c - mn);
+      }
+    }
   }
 }
 
@@ -1213,13 +1340,6 @@ __global__ void __launch_bounds__(kLsThreads) k_ls(Params P) {
   }
   const double gmax = block_max<kLsThreads>(dmax, sh);
   const double gmin = -block_max<kLsThreads>(-dmin, sh);
-  // g = beta e1 - H_{1:k+1,1:k} y (band: H_{i,j} != 0 for j-ell <= i <= j+1)
-  for (int i = tid; i <= k; i += kLsThreads) {
-    double acc = (i == 0) ? st->beta : 0.0;
-    const int jlo = max(0, i - 1), jhi = min(k - 1, i + P.ell);
-    for (int j = jlo; j <= jhi; ++j) acc = fma(-P.H[(int64_t)i + (int64_t)j * P.ldh], y_s[j], acc);
-    P.g[i] = acc;
-  }
   if (tid == 0) {
     P.hist_sk[c] = sres;
     st->k_x = k;
@@ -1227,30 +1347,65 @@ __global__ void __launch_bounds__(kLsThreads) k_ls(Params P) {
   }
 }
 
-// ------------------------------------------------------------------ a8: x_k = Z_k y_k
-// Tall-skinny GEMV (Alg. 1 L504 / Alg. 2), plus the partial max needed by
+// ------------------------------------------------------------------ a8 / a9: tall-skinny GEMVs
+// (a0, a1) = sum_{j < kc} M[j*ld + i2 + {0, 1}] * c[j]: rows i2, i2+1 of a column-major
+// tall-skinny matrix times a short vector in shared memory.  16-byte loads of row
+// pairs, four columns in flight per step; summation in increasing j (deterministic).
+__device__ __forceinline__ void tsgemv_pair(const double* __restrict__ M, int64_t ld, int64_t len, int64_t i2,
+                                            const double* c, int kc, double& a0, double& a1) {
+  a0 = 0.0;
+  a1 = 0.0;
+  if (i2 + 1 < len && (ld & 1) == 0) {
+    const double* p = M + i2;
+    int j = 0;
+    for (; j + 4 <= kc; j += 4) {
+      const double2 v0 = __ldg(reinterpret_cast<const double2*>(p + (int64_t)j * ld));
+      const double2 v1 = __ldg(reinterpret_cast<const double2*>(p + (int64_t)(j + 1) * ld));
+      const double2 v2 = __ldg(reinterpret_cast<const double2*>(p + (int64_t)(j + 2) * ld));
+      const double2 v3 = __ldg(reinterpret_cast<const double2*>(p + (int64_t)(j + 3) * ld));
+      a0 = fma(v0.x, c[j], a0);
+      a1 = fma(v0.y, c[j], a1);
+      a0 = fma(v1.x, c[j + 1], a0);
+      a1 = fma(v1.y, c[j + 1], a1);
+      a0 = fma(v2.x, c[j + 2], a0);
+      a1 = fma(v2.y, c[j + 2], a1);
+      a0 = fma(v3.x, c[j + 3], a0);
+      a1 = fma(v3.y, c[j + 3], a1);
+    }
+    for (; j < kc; ++j) {
+      const double2 v = __ldg(reinterpret_cast<const double2*>(p + (int64_t)j * ld));
+      a0 = fma(v.x, c[j], a0);
+      a1 = fma(v.y, c[j], a1);
+    }
+  } else {
+    for (int j = 0; j < kc; ++j) {
+      a0 = fma(__ldg(M + (int64_t)j * ld + i2), c[j], a0);
+      if (i2 + 1 < len) a1 = fma(__ldg(M + (int64_t)j * ld + i2 + 1), c[j], a1);
+    }
+  }
+}
+
+// a8: x_k = Z_k y_k (Alg. 1 L504 / Alg. 2), plus the partial max needed by
 // tau_{k+1} (|x| for IRN, x_+ for NONNEG).  HBM-bound (0.25 flop/B).
 __global__ void __launch_bounds__(kVecThreads) k_xupdate(Params P, int force) {
   __shared__ double sh[33];
-  __shared__ double ys[1024];
+  __shared__ double ys[kMaxD];
   const DevState* st = P.st;
   if (!force && st->done) return;
   const int kx = st->k_x;
+  for (int t = threadIdx.x; t < kx; t += kVecThreads) ys[t] = P.y[t];
+  __syncthreads();
   double mx = -INFINITY;
-  for (int64_t i0 = (int64_t)blockIdx.x * kVecThreads; i0 < P.n; i0 += (int64_t)gridDim.x * kVecThreads) {
-    const int64_t i = i0 + threadIdx.x;
-    double acc = 0.0;
-    for (int jb = 0; jb < kx; jb += 1024) {
-      const int nj = min(1024, kx - jb);
-      __syncthreads();
-      for (int t = threadIdx.x; t < nj; t += kVecThreads) ys[t] = P.y[jb + t];
-      __syncthreads();
-      if (i < P.n)
-        for (int j = 0; j < nj; ++j) acc = fma(P.Z[(int64_t)(jb + j) * P.n + i], ys[j], acc);
-    }
-    if (i < P.n) {
-      P.x[i] = acc;
-      mx = fmax(mx, P.precond == 1 ? fabs(acc) : acc);
+  const bool absmax = P.precond == 1;
+  for (int64_t i2 = 2 * ((int64_t)blockIdx.x * kVecThreads + threadIdx.x); i2 < P.n;
+       i2 += 2 * (int64_t)gridDim.x * kVecThreads) {
+    double a0, a1;
+    tsgemv_pair(P.Z, P.n, P.n, i2, ys, kx, a0, a1);
+    P.x[i2] = a0;
+    mx = fmax(mx, absmax ? fabs(a0) : a0);
+    if (i2 + 1 < P.n) {
+      P.x[i2 + 1] = a1;
+      mx = fmax(mx, absmax ? fabs(a1) : a1);
     }
   }
   mx = block_max<kVecThreads>(mx, sh);
@@ -1258,44 +1413,10 @@ __global__ void __launch_bounds__(kVecThreads) k_xupdate(Params P, int force) {
   last_block_reduce(P, P.slot_xmax, 1, CTR_XMAX, true);
 }
 
-// ------------------------------------------------------------------ a9: W-path true residual
-// ||b - A x_k|| = ||W_{k+1} g|| (eq. FGK: A Z_k = W_{k+1} H_{k+1,k}, w_1 = b/beta).
-__global__ void __launch_bounds__(kVecThreads) k_res_partial(Params P) {
-  __shared__ double sh[33];
-  __shared__ double gs[1024];
-  const DevState* st = P.st;
-  if (st->done) return;
-  const int kk = st->k + 1;  // columns of W_{k+1}
-  double acc2 = 0.0;
-  for (int64_t i0 = (int64_t)blockIdx.x * kVecThreads; i0 < P.m; i0 += (int64_t)gridDim.x * kVecThreads) {
-    const int64_t i = i0 + threadIdx.x;
-    double r = 0.0;
-    for (int jb = 0; jb < kk; jb += 1024) {
-      const int nj = min(1024, kk - jb);
-      __syncthreads();
-      for (int t = threadIdx.x; t < nj; t += kVecThreads) gs[t] = P.g[jb + t];
-      __syncthreads();
-      if (i < P.m)
-        for (int j = 0; j < nj; ++j) r = fma(P.W[(int64_t)(jb + j) * P.m + i], gs[j], r);
-    }
-    if (i < P.m) acc2 = fma(r, r, acc2);
-  }
-  acc2 = block_sum<kVecThreads>(acc2, sh);
-  if (threadIdx.x == 0) P.part[(size_t)P.slot_res * kVecBlocks + blockIdx.x] = acc2;
-  last_block_reduce(P, P.slot_res, 1, CTR_RES, false);
-}
-
-// ------------------------------------------------------------------ a9: stop tests
-// tol test (Alg. 1 L498 / Alg. 2, R3) and discrepancy principle (eq. discrP
-// L50-53, R12); records the histories and advances k.
-__global__ void __launch_bounds__(kVecThreads) k_stop(Params P) {
-  __shared__ double sh[33];
-  DevState* st = P.st;
-  if (st->done) return;
+// a9: tol test (Alg. 1 L498 / Alg. 2, R3) and discrepancy principle (eq. discrP
+// L50-53, R12); records the histories and advances k.  One thread.
+__device__ __forceinline__ void stop_body(const Params& P, DevState* st, double r) {
   const int k = st->k;
-  double r = NAN;
-  if (P.want_res) r = sqrt(P.scal[P.slot_res]);
-  if (threadIdx.x != 0) return;
   P.hist_true[k - 1] = r;
   const double sres = P.hist_sk[k - 1];
   int status = 0;
@@ -1312,6 +1433,44 @@ __global__ void __launch_bounds__(kVecThreads) k_stop(Params P) {
     st->done = 1;
   }
   st->k = k + 1;
+}
+
+// a9: W-path true residual ||b - A x_k|| = ||W_{k+1} g||, g = beta e_1 - H_{k+1,k} y_k
+// (eq. FGK: A Z_k = W_{k+1} H_{k+1,k}, w_1 = b/beta).  Every block forms g in
+// shared memory from the band of H; fuse_stop (one rank): the last block also runs
+// the stop tests.
+__global__ void __launch_bounds__(kVecThreads) k_res_partial(Params P, int fuse_stop) {
+  __shared__ double sh[33];
+  __shared__ double gs[kMaxD];
+  DevState* st = P.st;
+  if (st->done) return;
+  const int k = st->k, kk = k + 1;  // columns of W_{k+1}
+  for (int i = threadIdx.x; i <= k; i += kVecThreads) {
+    double acc = (i == 0) ? st->beta : 0.0;
+    const int jlo = max(0, i - 1), jhi = min(k - 1, i + P.ell);  // band: H_ij != 0 for j - ell <= i <= j + 1
+    for (int j = jlo; j <= jhi; ++j) acc = fma(-P.H[(int64_t)i + (int64_t)j * P.ldh], P.y[j], acc);
+    gs[i] = acc;
+  }
+  __syncthreads();
+  double acc2 = 0.0;
+  for (int64_t i2 = 2 * ((int64_t)blockIdx.x * kVecThreads + threadIdx.x); i2 < P.m;
+       i2 += 2 * (int64_t)gridDim.x * kVecThreads) {
+    double r0, r1;
+    tsgemv_pair(P.W, P.m, P.m, i2, gs, kk, r0, r1);
+    acc2 = fma(r0, r0, acc2);
+    acc2 = fma(r1, r1, acc2);  // r1 = 0 past the end
+  }
+  acc2 = block_sum<kVecThreads>(acc2, sh);
+  if (threadIdx.x == 0) P.part[(size_t)P.slot_res * kVecBlocks + blockIdx.x] = acc2;
+  const bool last = last_block_reduce(P, P.slot_res, 1, CTR_RES, false);
+  if (fuse_stop && last && threadIdx.x == 0) stop_body(P, st, sqrt(P.scal[P.slot_res]));
+}
+
+// a9 without the fused residual (no history, or several ranks: after the allreduce).
+__global__ void __launch_bounds__(32) k_stop(Params P) {
+  DevState* st = P.st;
+  if (st->done || threadIdx.x != 0) return;
+  stop_body(P, st, P.want_res ? sqrt(P.scal[P.slot_res]) : NAN);
 }
 
 // rhs = s_b = S b (sFLSQR, Alg. 1) or s = beta S z with S_TW = [S z]

@@ -404,3 +404,47 @@ def test_error_codes():
         s.set_precond("irn", p=3.0)
     assert e.value.code == B.E_INVALID
     s.close()
+
+
+# ------------------------------------------------------------------ CSR-16 index compression
+def test_csr16_bitwise_equal_to_int32_csr_and_oracle():
+    from paper_2605_22281_b200 import SFLSQR
+    p = make_problem(4, N=96, n_angles=61, nb=137)   # ragged rows, empty rays, unmatched B
+    s = SFLSQR(maxit=4)
+    s.set_operator(p.A.nrows, p.A.ncols, p.A.rowptr, p.A.col, p.A.val, t=(p.T.rowptr, p.T.col, p.T.val))
+    rng = np.random.default_rng(3)
+    x, w = rng.standard_normal(p.n), rng.standard_normal(p.m)
+    outs = {}
+    for mode in (15, 14):
+        s.debug_set_tuning(mode)
+        outs[mode] = (s.debug_apply(0, x), s.debug_apply(1, w))
+    assert np.array_equal(outs[15][0], outs[14][0]) and np.array_equal(outs[15][1], outs[14][1])
+    A = OracleCSR(p.A.nrows, p.A.ncols, p.A.rowptr, p.A.col, p.A.val)
+    assert np.max(np.abs(outs[15][0] - A.matvec(x))) <= 1e-13 * np.max(np.abs(A.matvec(x)))
+    s.close()
+
+
+def test_csr16_overflow_falls_back_to_int32():
+    # a 16-entry chunk spanning > 65536 columns cannot be offset-encoded: the operator stays int32 CSR
+    from gen.problems import CSR
+    from paper_2605_22281_b200 import SFLSQR
+    rng = np.random.default_rng(4)
+    m, n = 300, 200000
+    rows = []
+    for i in range(m):
+        k = 1 + (i * 7) % 40
+        rows.append(np.sort(rng.choice(n, size=k, replace=False)))
+    rowptr = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.int64)
+    col = np.concatenate(rows).astype(np.int32)
+    val = rng.standard_normal(col.size)
+    s = SFLSQR(maxit=4)
+    s.set_operator(m, n, rowptr, col, val)
+    A = OracleCSR(m, n, rowptr, col, val)
+    x = rng.standard_normal(n)
+    got = s.debug_apply(0, x)
+    assert np.max(np.abs(got - A.matvec(x))) <= 1e-13 * np.max(np.abs(A.matvec(x)))
+    w = rng.standard_normal(m)
+    got_t = s.debug_apply(1, w)
+    ref_t = A.transpose().matvec(w)
+    assert np.max(np.abs(got_t - ref_t)) <= 1e-13 * np.max(np.abs(ref_t))
+    s.close()
