@@ -72,6 +72,18 @@ extern "C" {
  * (= ||b - A x_k|| for FLSQR, ||T(b - A x_k)|| for FLSMR, in exact arithmetic). */
 #define SFLSQR_METHOD_FLSQR 2
 #define SFLSQR_METHOD_FLSMR 3
+/* Textbook LSQR / LSMR (PAPER.md §"Golub-Kahan bidiagonalization, LSQR and LSMR",
+ * L277-319): Golub-Kahan bidiagonalization with the short recurrences of Paige &
+ * Saunders (LSQR) and Fong & Saunders (LSMR, undamped); x is updated in place, no basis is
+ * stored, no sketch and no flexible preconditioner (set_precond must stay IDENTITY:
+ * SFLSQR_E_INVALID at set_rhs otherwise); T = B != A^T runs "LSQR ignoring A# != A^T"
+ * (L1791-1792).  One rank only (SFLSQR_E_UNSUPPORTED for world > 1).
+ * get_residual_norms: true_res = the recurrence's ||b - A x_k|| (LSQR |phibar_{k+1}|,
+ * LSMR Fong-Saunders estimate) -- also what the discrepancy test uses (reading R19) --;
+ * sketch_res = LSQR the same, LSMR ||T (b - A x_k)|| = |zetabar_{k+1}|.
+ * sflsqr_debug_basis / sflsqr_debug_state: SFLSQR_E_UNSUPPORTED. */
+#define SFLSQR_METHOD_LSQR 4
+#define SFLSQR_METHOD_LSMR 5
 
 /* opts.orth_mode (reading R1) */
 #define SFLSQR_ORTH_P 0 /* orthogonalise against the last ell normalised p_j (eq. FGK) */

@@ -98,8 +98,9 @@ def lsqr(op, b, maxit=10, eta=0.0, delta_e=0.0, record=True):
         rhobar = -c * alpha
         phi = c * phibar
         phibar = s * phibar
-        x = x + (phi / rho) * w
-        w = v - (theta / rho) * w
+        if rho > 0.0:                                       # rho = 0 only at an exact breakdown
+            x = x + (phi / rho) * w
+            w = v - (theta / rho) * w
         res.x, res.k = x, k
         res.est_res.append(abs(phibar))
         res.true_res.append(float(np.linalg.norm(b - op.matvec(x))))

@@ -320,6 +320,14 @@ def solve_problem(prob, spec, op=None, maxit=None, record=True, **over):
     from .operators import operator_from_problem
     if op is None:
         op = operator_from_problem(prob)
+    method = over.pop("method", spec.method)
+    if method in ("lsqr", "lsmr"):                      # textbook GKB baselines (oracle/gkb.py)
+        from . import gkb
+        eta = over.pop("eta", spec.eta)
+        fn = gkb.lsqr if method == "lsqr" else gkb.lsmr
+        return fn(op, prob.b, maxit=maxit or spec.maxit, eta=eta, delta_e=prob.delta_e,
+                  record=over.pop("record", record))
+    over["method"] = method
     kw = dict(method=spec.method, maxit=maxit or spec.maxit, window=spec.window, sketch_seed=prob.sketch_seed,
               d=spec.d, s_nz=spec.s_nz, precond=spec.precond, p_exp=spec.p, eps_rel=spec.eps_rel,
               tol=spec.tol, eta=spec.eta, delta_e=prob.delta_e, orth_mode=spec.orth_mode, record=record)

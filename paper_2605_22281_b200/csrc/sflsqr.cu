@@ -89,6 +89,7 @@ struct sflsqr {
   Params P;
   int nslots = 0;
   double *zfull = nullptr, *wfull = nullptr, *zpart = nullptr;
+  double* gtmp = nullptr;  // GKB: product before the separate epilogue pass (blur / non-default SpMV)
   std::vector<void*> solve_allocs;
   std::vector<size_t> solve_sizes;
   cudaGraphExec_t gexec = nullptr;
@@ -245,6 +246,7 @@ void free_solve(sflsqr_t* h) {
   h->solve_allocs.clear();
   h->solve_sizes.clear();
   h->zfull = h->wfull = h->zpart = nullptr;
+  h->gtmp = nullptr;
   h->bufs = false;
   h->rhs_set = false;
 }
@@ -516,6 +518,52 @@ int enqueue_orth(sflsqr_t* h, int side, int koff) {
   return SFLSQR_OK;
 }
 
+// GKB product with its epilogue (methods 4 / 5): fused into the default CSR kernel, or a
+// plain product followed by k_epi_vec (blur operator / a forced SpMV variant).
+void enqueue_apply_gkb(sflsqr_t* h, int which, const double* x, double* y, int kind, int slot_in, int slot_out,
+                       int ctr_idx) {
+  Params& P = h->P;
+  SpmvEpi E;
+  E.kind = kind;
+  E.aux = y;
+  E.gk = P.gk;
+  E.scal = P.scal;
+  E.part = P.part;
+  E.ctr = P.ctr;
+  E.slot_in = slot_in;
+  E.slot_out = slot_out;
+  E.ctr_idx = ctr_idx;
+  const int64_t nrows = which == 0 ? h->m_loc : h->t_rows;
+  const int mode = h->spmv_mode >= 0 ? h->spmv_mode : 14;
+  const int cls = which == 0 ? SFLSQR_KC_SPMV_A : SFLSQR_KC_SPMV_T;
+  if (!h->blur && mode == 14) {
+    const int64_t nnz = which == 0 ? h->nnz_a : h->nnz_t;
+    const int64_t xlen = which == 0 ? h->n : h->m;
+    Launch L(h, cls, 12.0 * nnz + 8.0 * (nrows + 1) + 8.0 * xlen + 8.0 * nrows + (kind == 3 ? 0.0 : 8.0 * nrows));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nrows + 31) / 32, 148 * 4));
+    k_spmv_csr_pf<16, 4, 16, true><<<grid, 512, 0, h->stream>>>(
+        P.st, nrows, which == 0 ? h->a_rowptr : h->t_rowptr, which == 0 ? h->a_col : h->t_col,
+        which == 0 ? h->a_val : h->t_val, x, 0, 0, y, E);
+    return;
+  }
+  enqueue_apply(h, which, P.st, x, 0, 0, h->gtmp, cls);
+  Launch L(h, SFLSQR_KC_ORTH, 8.0 * nrows * (kind == 3 ? 2 : 3));
+  k_epi_vec<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P.st, E, h->gtmp, y, nrows);
+}
+
+// One step of textbook LSQR / LSMR: u' = A v - (alpha/beta) u'_old and
+// beta'^2; v' = T u'/beta' - beta' v and alpha'^2; then the short-recurrence update.
+int enqueue_gkb_iteration(sflsqr_t* h) {
+  Params& P = h->P;
+  enqueue_apply_gkb(h, 0, P.z, P.w, 1, 0, P.slot_gkb, CTR_GKB_A);
+  enqueue_apply_gkb(h, 1, P.w, P.z, 2, P.slot_gkb, P.slot_gka, CTR_GKB_T);
+  {
+    Launch L(h, SFLSQR_KC_XUPD, 8.0 * h->n_loc * (P.method == SFLSQR_METHOD_LSMR ? 8 : 6));
+    k_gkb_update<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P);
+  }
+  return SFLSQR_OK;
+}
+
 // a7: the one-CTA projected LS, on the main stream or forked onto the side stream
 // (event fork on the main stream, join event recorded on the side stream).
 int enqueue_ls(sflsqr_t* h, bool forked) {
@@ -544,6 +592,7 @@ int enqueue_ls(sflsqr_t* h, bool forked) {
 // projected problem, which needs column k+1 of T).
 int enqueue_iteration(sflsqr_t* h) {
   Params& P = h->P;
+  if (P.method >= SFLSQR_METHOD_LSQR) return enqueue_gkb_iteration(h);
   const int k = h->host_k;  // used only for the byte model
   const double n8 = 8.0 * h->n_loc, m8 = 8.0 * h->m_loc;
   const bool sketched = P.method == SFLSQR_METHOD_SFLSQR || P.method == SFLSQR_METHOD_SFLSMR;
@@ -748,8 +797,12 @@ int alloc_solve(sflsqr_t* h) {
   std::memset(&P, 0, sizeof(P));
   const int maxit = h->o.maxit, ell = h->o.window;
   const bool sketched = h->o.method <= SFLSQR_METHOD_SFLSMR;
-  // FLSQR / FLSMR: the projected problem has k+1 <= maxit+1 rows and no sketch
-  const int d = sketched ? h->d : maxit + 1;
+  const bool gkb = h->o.method >= SFLSQR_METHOD_LSQR;
+  if (gkb && h->pkind != SFLSQR_PRECOND_IDENTITY)
+    return fail(h, SFLSQR_E_INVALID, "LSQR / LSMR take no flexible preconditioner");
+  // FLSQR / FLSMR: the projected problem has k+1 <= maxit+1 rows and no sketch; GKB: none
+  const int d = sketched ? h->d : (gkb ? 1 : maxit + 1);
+  const int ncol = gkb ? 1 : maxit;  // stored basis columns (GKB keeps none)
   P.m = h->m_loc;
   P.n = h->n_loc;
   P.ell = ell;
@@ -792,6 +845,8 @@ int alloc_solve(sflsqr_t* h) {
   P.slot_wf = s;
   s += kFuseAcc;
   P.slot_wout = s++;
+  P.slot_gka = s++;
+  P.slot_gkb = s++;
   h->nslots = s;
   auto A = [&](double** p, size_t count) {
     return dalloc(h, (void**)p, count * sizeof(double), &h->solve_allocs, &h->solve_sizes);
@@ -802,8 +857,8 @@ int alloc_solve(sflsqr_t* h) {
   const size_t zlen = std::max<size_t>(n, (size_t)h->n_max);
   if ((rc = dalloc(h, (void**)&P.st, sizeof(DevState), &h->solve_allocs, &h->solve_sizes))) return rc;
   if ((rc = dalloc(h, (void**)&P.ctr, sizeof(int) * CTR_COUNT, &h->solve_allocs, &h->solve_sizes))) return rc;
-  if ((rc = A(&P.z, zlen)) || (rc = A(&P.x, n)) || (rc = A(&P.Z, n * maxit)) || (rc = A(&P.w, m)) ||
-      (rc = A(&P.W, m * (maxit + 1))) || (rc = A(&P.b, m)) || (rc = A(&P.H, (size_t)(maxit + 1) * maxit)) ||
+  if ((rc = A(&P.z, zlen)) || (rc = A(&P.x, n)) || (rc = A(&P.Z, n * ncol)) || (rc = A(&P.w, m)) ||
+      (rc = A(&P.W, m * (ncol + 1))) || (rc = A(&P.b, m)) || (rc = A(&P.H, (size_t)(maxit + 1) * maxit)) ||
       (rc = A(&P.Tm, (size_t)(maxit + 1) * (maxit + 1))) || (rc = A(&P.part, (size_t)s * kVecBlocks)) ||
       (rc = A(&P.scal, (size_t)s)) || (rc = A(&P.skbuf, d)) || (rc = A(&P.rhs, d)) ||
       (rc = A(&P.Mcols, (size_t)d * maxit)) || (rc = A(&P.STW, (size_t)d * (maxit + 1))) ||
@@ -813,6 +868,9 @@ int alloc_solve(sflsqr_t* h) {
       (rc = A(&P.hist_sk, maxit)))
     return rc;
   if (P.use_pring && (rc = A(&P.Pring, n * ell))) return rc;
+  if (gkb && ((rc = A(&P.gv1, n)) || (rc = A(&P.gv2, n)) || (rc = A(&P.gk, 2 * kGkbState)) ||
+              (rc = A(&h->gtmp, std::max(n, m)))))
+    return rc;
   if (P.orth_alg == ORTH_CGS2 &&
       ((rc = A(&P.cpart, (size_t)P.ldc * kVecBlocks)) || (rc = A(&P.cscal, (size_t)2 * P.ldc))))
     return rc;
@@ -955,8 +1013,10 @@ void sflsqr_local_group_destroy(void* group) { local_group_release(static_cast<L
 int sflsqr_create(sflsqr_t** out, const sflsqr_opts* o) {
   if (!out || !o) return fail(nullptr, SFLSQR_E_INVALID, "NULL argument");
   *out = nullptr;
-  if (o->method < SFLSQR_METHOD_SFLSQR || o->method > SFLSQR_METHOD_FLSMR)
-    return fail(nullptr, SFLSQR_E_INVALID, "method must be SFLSQR, SFLSMR, FLSQR or FLSMR");
+  if (o->method < SFLSQR_METHOD_SFLSQR || o->method > SFLSQR_METHOD_LSMR)
+    return fail(nullptr, SFLSQR_E_INVALID, "method must be SFLSQR, SFLSMR, FLSQR, FLSMR, LSQR or LSMR");
+  if (o->method >= SFLSQR_METHOD_LSQR && o->world > 1)
+    return fail(nullptr, SFLSQR_E_UNSUPPORTED, "LSQR / LSMR run on one rank");
   if (o->orth_kernel != SFLSQR_ORTHK_AUTO && o->orth_kernel != SFLSQR_ORTHK_MGS)
     return fail(nullptr, SFLSQR_E_INVALID, "bad orth_kernel");
   if (o->window < 1) return fail(nullptr, SFLSQR_E_INVALID, "window must be >= 1");
@@ -989,7 +1049,9 @@ int sflsqr_create(sflsqr_t** out, const sflsqr_opts* o) {
   h->rank = o->rank;
   h->world = o->world;
   if (o->window > o->maxit) h->o.window = o->maxit;  // full orthogonalisation
-  if (o->method >= SFLSQR_METHOD_FLSQR) h->o.window = o->maxit;  // FLSQR / FLSMR: full (L344-345)
+  if (o->method == SFLSQR_METHOD_FLSQR || o->method == SFLSQR_METHOD_FLSMR)
+    h->o.window = o->maxit;  // FLSQR / FLSMR: full (L344-345)
+  if (o->method >= SFLSQR_METHOD_LSQR) h->o.window = 1;  // GKB short recurrences: no stored window
   if (o->world > 1) h->o.use_graph = 0;             // collectives are issued eagerly
   if (o->stream && (cudaStream_t)o->stream != cudaStreamLegacy && (cudaStream_t)o->stream != cudaStreamPerThread) {
     h->stream = (cudaStream_t)o->stream;
@@ -1317,6 +1379,25 @@ int sflsqr_set_rhs(sflsqr_t* h, const double* b, int64_t len, int32_t mem_flags)
     if (!std::isfinite(beta2)) return fail(h, SFLSQR_E_NONFINITE, "b has a non-finite entry");
     if (!(beta2 > 0.0)) return fail(h, SFLSQR_E_ZERO_RHS, "||b|| = 0");
   }
+  if (P.method >= SFLSQR_METHOD_LSQR) {
+    // GKB start: u' = b (beta_1 = ||b||), v' = T b / beta_1 (alpha_1^2), v_1, x_0, carried scalars
+    CU(h, cudaMemcpyAsync(P.w, P.b, sizeof(double) * h->m_loc, cudaMemcpyDeviceToDevice, h->stream));
+    {
+      Launch L(h, SFLSQR_KC_LS, 16.0);
+      k_init_rhs<<<1, kVecThreads, 0, h->stream>>>(P);
+    }
+    enqueue_apply_gkb(h, 1, P.w, P.z, 3, P.slot_beta, P.slot_gka, CTR_GKB_T);
+    {
+      Launch L(h, SFLSQR_KC_XUPD, 8.0 * h->n_loc * 4);
+      k_gkb_init<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P);
+    }
+    if ((rc = check_launch(h))) return rc;
+    CU(h, cudaStreamSynchronize(h->stream));
+    h->host_k = 1;
+    h->rhs_set = true;
+    if (h->o.use_graph && !h->gexec && (rc = build_graph(h))) return rc;
+    return SFLSQR_OK;
+  }
   {
     Launch L(h, SFLSQR_KC_ORTH, 16.0 * h->m_loc);
     k_init_w1<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P);
@@ -1379,7 +1460,7 @@ int sflsqr_get_x(sflsqr_t* h, double* x, int64_t len, int32_t mem_flags) {
   if (!x && len) return fail(h, SFLSQR_E_INVALID, "NULL x");
   if (len != h->n_loc) return fail(h, SFLSQR_E_DIM, "len(x) != local n");
   cudaSetDevice(h->o.device);
-  {
+  if (h->P.method < SFLSQR_METHOD_LSQR) {  // x_k = Z_k y_k; GKB methods update x in place
     Launch L(h, SFLSQR_KC_XUPD, 8.0 * h->n_loc);
     k_xupdate<<<kVecBlocks, kVecThreads, 0, h->stream>>>(h->P, 1);
   }
@@ -1502,6 +1583,7 @@ int sflsqr_debug_apply(sflsqr_t* h, int32_t which, const double* x, double* y) {
 int sflsqr_debug_basis(sflsqr_t* h, double* H, double* Tm, double* Z, double* W, double* y) {
   int rc;
   if ((rc = ensure_ready(h, true))) return rc;
+  if (h->o.method >= SFLSQR_METHOD_LSQR) return fail(h, SFLSQR_E_UNSUPPORTED, "LSQR / LSMR keep no basis");
   cudaSetDevice(h->o.device);
   DevState st;
   CU(h, cudaMemcpyAsync(&st, h->P.st, sizeof(st), cudaMemcpyDeviceToHost, h->stream));
@@ -1522,6 +1604,7 @@ int sflsqr_debug_basis(sflsqr_t* h, double* H, double* Tm, double* Z, double* W,
 int sflsqr_debug_state(sflsqr_t* h, double* z, double* x, double* p_ring, double* sketch_cols, double* rhs) {
   int rc;
   if ((rc = ensure_ready(h, true))) return rc;
+  if (h->o.method >= SFLSQR_METHOD_LSQR) return fail(h, SFLSQR_E_UNSUPPORTED, "LSQR / LSMR keep no FGK state");
   cudaSetDevice(h->o.device);
   DevState st;
   CU(h, cudaMemcpyAsync(&st, h->P.st, sizeof(st), cudaMemcpyDeviceToHost, h->stream));

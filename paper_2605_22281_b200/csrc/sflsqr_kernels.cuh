@@ -22,7 +22,11 @@ constexpr int kMaxD = 2048;               // sketch rows supported by the one-CT
 constexpr int kFuseJ = 6;                 // fused orthogonalisation for windows of up to 6 vectors
 constexpr int kFuseAcc = 1 + kFuseJ + kFuseJ * (kFuseJ - 1) / 2;  // ||v||^2, dots, Gram pairs
 constexpr int kCgsChunk = 2048;           // CGS2 dot kernel: rows of v staged in shared memory per step
-enum CounterIdx { CTR_BETA = 0, CTR_ZDOTS, CTR_ZAXPY, CTR_WDOTS, CTR_WAXPY, CTR_XMAX, CTR_RES, CTR_CGS, CTR_COUNT };
+enum CounterIdx {
+  CTR_BETA = 0, CTR_ZDOTS, CTR_ZAXPY, CTR_WDOTS, CTR_WAXPY, CTR_XMAX, CTR_RES, CTR_CGS,
+  CTR_GKB_A, CTR_GKB_T, CTR_GKB_UPD, CTR_COUNT
+};
+constexpr int kGkbState = 24;             // carried LSQR / LSMR scalars, double-buffered by k parity
 enum OrthAlg { ORTH_FUSED = 0, ORTH_MGS = 1, ORTH_CGS2 = 2 };
 
 // Device-resident solve state (read by every kernel of a captured iteration).
@@ -65,6 +69,10 @@ struct Params {
   int* ctr;                // last-block arrival counters (one per reduction site)
   double *cpart, *cscal;   // CGS2: (ell + 2) x kVecBlocks dot partials; 2 stages x ldc reduced dots
   int ldc;                 // ell + 2
+  // textbook LSQR / LSMR (methods 4 / 5): u' = P.w (m, unnormalised), v = P.z (n), x = P.x,
+  // gv1 = LSQR w / LSMR h, gv2 = LSMR hbar (n); gk = 2 x kGkbState carried scalars
+  double *gv1, *gv2, *gk;
+  int slot_gka, slot_gkb;  // ||v'||^2 (alpha^2) and ||u'||^2 (beta^2) partials
   // sketch
   int64_t* sk_rp;          // S stored transposed: d+1 row pointers
   uint32_t* sk_ent;         // coordinate | sign << 31, s * dim entries
@@ -409,14 +417,44 @@ __global__ void __launch_bounds__(WPB * 32, 2048 / (WPB * 32)) k_spmv_csr_rows(c
 // Variant: software-pipelined row-group SpMV — the column indices and values of
 // the next UNR chunks are loaded before the gathers of the current ones, so the
 // col -> x dependent latency of one chunk group overlaps the streams of the next.
-template <int WPB, int UNR, int LANES>
+// GKB epilogue of the product (methods 4 / 5, Golub-Kahan steps of PAPER.md eq. GKB):
+// y_i = a (M x)_i - c aux_i, with ||y||^2 reduced into scal[slot_out] (last block), where
+//   kind 1 (A side):  a = 1,        c = alpha_k / beta_k   (u' = A v_k - alpha_k u_k, u_k = u'_old / beta_k)
+//   kind 2 (T side):  a = 1/beta',  c = beta'              (v' = T u_{k+1} - beta_{k+1} v_k, beta'^2 = scal[slot_in])
+//   kind 3 (T, init): a = 1/beta_1, c = 0                  (v' = T b / ||b||)
+struct SpmvEpi {
+  int kind;               // 0: plain y = M x
+  double* aux;            // may alias y (each row reads and writes only its own entry)
+  const double* gk;       // carried scalars (2 x kGkbState)
+  double* scal;           // reduced slots
+  double* part;           // per-block partials
+  int* ctr;
+  int slot_in, slot_out, ctr_idx;
+};
+
+__device__ __forceinline__ void epi_coefs(const SpmvEpi& E, const DevState* st, double& a, double& c) {
+  a = 1.0;
+  c = 0.0;
+  if (E.kind == 1) {
+    const double* g = E.gk + kGkbState * (st->k & 1);
+    c = g[1] > 0.0 ? g[0] / g[1] : 0.0;
+  } else if (E.kind >= 2) {
+    const double bn = sqrt(E.scal[E.slot_in]);
+    a = bn > 0.0 ? 1.0 / bn : 0.0;
+    c = E.kind == 2 ? bn : 0.0;
+  }
+}
+
+template <int WPB, int UNR, int LANES, bool EPI = false>
 __global__ void __launch_bounds__(WPB * 32, 2048 / (WPB * 32)) k_spmv_csr_pf(const DevState* st, int64_t nrows,
                                                             const int64_t* __restrict__ rowptr,
                                                             const int* __restrict__ col,
                                                             const double* __restrict__ val,
                                                             const double* __restrict__ x_base, int64_t x_ld,
-                                                            int x_koff, double* __restrict__ y) {
+                                                            int x_koff, double* y, SpmvEpi E = SpmvEpi()) {
   if (st && st->done) return;
+  double ea = 1.0, ec = 0.0, nrm = 0.0;
+  if (EPI) epi_coefs(E, st, ea, ec);
   const double* __restrict__ x = kvec(st, x_base, x_ld, x_koff);
   constexpr int RPW = 32 / LANES;  // rows per warp
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -463,7 +501,33 @@ __global__ void __launch_bounds__(WPB * 32, 2048 / (WPB * 32)) k_spmv_csr_pf(con
     }
 #pragma unroll
     for (int o = LANES / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    if (sl == 0 && row < nrows) y[row] = sum;
+    if (sl == 0 && row < nrows) {
+      if (EPI) {
+        sum = E.kind == 3 ? sum * ea : fma(sum, ea, -ec * E.aux[row]);
+        nrm = fma(sum, sum, nrm);
+      }
+      y[row] = sum;
+    }
+  }
+  if (EPI) {
+    __shared__ double sh[33];
+    __shared__ int s_last;
+    nrm = block_sum<WPB * 32>(nrm, sh);
+    if (threadIdx.x == 0) E.part[(size_t)E.slot_out * kVecBlocks + blockIdx.x] = nrm;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(E.ctr + E.ctr_idx, 1) == (int)gridDim.x - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const double* pp = E.part + (size_t)E.slot_out * kVecBlocks;
+    double v = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += WPB * 32) v += __ldcg(pp + b);
+    v = block_sum<WPB * 32>(v, sh);
+    if (threadIdx.x == 0) {
+      E.scal[E.slot_out] = v;
+      E.ctr[E.ctr_idx] = 0;
+    }
   }
 }
 
@@ -1473,6 +1537,213 @@ __global__ void __launch_bounds__(32) k_stop(Params P) {
   stop_body(P, st, P.want_res ? sqrt(P.scal[P.slot_res]) : NAN);
 }
 
+// ------------------------------------------------------------------ textbook LSQR / LSMR (methods 4 / 5)
+// the Golub-Kahan bidiagonalization with the short recurrences of
+// Paige & Saunders (LSQR) and Fong & Saunders (LSMR, undamped), restated from the
+// published algorithms (the oracle's oracle/gkb.py follows the same order).  One GKB step is
+// two products with fused epilogues (k_spmv_csr_pf<.., true>) and one vector update here;
+// the carried scalars live in P.gk, double-buffered by the parity of k so that every block
+// reads the old values while the last block writes the new ones.
+// gk slots: 0 alpha, 1 beta, 2 rhobar, 3 phibar (LSQR) | 4 alphabar, 5 zetabar, 6 rho, 7 rhobarL,
+//           8 cbar, 9 sbar, 10 betadd, 11 betad, 12 rhodold, 13 tautildeold, 14 thetatilde, 15 zeta (LSMR)
+__device__ __forceinline__ void gkb_rot(double a, double b, double& c, double& s, double& r) {
+  r = hypot(a, b);
+  if (r == 0.0) {
+    c = 1.0;
+    s = 0.0;
+  } else {
+    c = a / r;
+    s = b / r;
+  }
+}
+
+struct GkbStep {          // scalars of one step, computed identically by every thread
+  double alpha, beta;     // alpha_{k+1}, beta_{k+1}
+  double cx, cw;          // LSQR: x += cx w, w = v - cw w        | LSMR: x += cx hbar, h = v - cw h
+  double chb;             // LSMR: hbar = h - chb hbar
+  double res, nres;       // ||r_k|| (recurrence), LSMR ||T r_k||
+  double nxt[kGkbState];  // carried scalars for step k+1
+};
+
+__device__ __forceinline__ void gkb_scalars(const Params& P, const double* g, bool lsmr, GkbStep& o) {
+  const double alpha = sqrt(P.scal[P.slot_gka]), beta = sqrt(P.scal[P.slot_gkb]);
+#pragma unroll
+  for (int i = 0; i < kGkbState; ++i) o.nxt[i] = g[i];
+  o.alpha = alpha;
+  o.beta = beta;
+  o.nxt[0] = alpha;
+  o.nxt[1] = beta;
+  o.chb = 0.0;
+  o.nres = 0.0;
+  if (!lsmr) {
+    double c, s, rho;
+    gkb_rot(g[2], beta, c, s, rho);
+    const double theta = s * alpha, phi = c * g[3];
+    o.nxt[2] = -c * alpha;
+    o.nxt[3] = s * g[3];
+    o.cx = rho > 0.0 ? phi / rho : 0.0;
+    o.cw = rho > 0.0 ? theta / rho : 0.0;
+    o.res = fabs(o.nxt[3]);
+    o.nres = o.res;
+    return;
+  }
+  const double rhoold = g[6], rhobarold = g[7], zetaold = g[15];
+  double c, s, rho;
+  gkb_rot(g[4], beta, c, s, rho);                 // Q_k (undamped: alphahat = alphabar)
+  const double thetanew = s * alpha;
+  o.nxt[4] = c * alpha;
+  const double thetabar = g[9] * rho;
+  double cbar, sbar, rhobar;
+  gkb_rot(g[8] * rho, thetanew, cbar, sbar, rhobar);   // Qbar_k
+  const double zeta = cbar * g[5];
+  o.nxt[5] = -sbar * g[5];
+  o.nxt[6] = rho;
+  o.nxt[7] = rhobar;
+  o.nxt[8] = cbar;
+  o.nxt[9] = sbar;
+  o.nxt[15] = zeta;
+  o.chb = (rhoold * rhobarold) != 0.0 ? thetabar * rho / (rhoold * rhobarold) : 0.0;
+  o.cx = (rho * rhobar) != 0.0 ? zeta / (rho * rhobar) : 0.0;
+  o.cw = rho != 0.0 ? thetanew / rho : 0.0;
+  // ||r_k|| estimate: Qhat = I, Q_k, Qtilde_{k-1}
+  const double betaacute = g[10];
+  const double betahat = c * betaacute;
+  o.nxt[10] = -s * betaacute;
+  const double thetatildeold = g[14];
+  double ctildeold, stildeold, rhotildeold;
+  gkb_rot(g[12], thetabar, ctildeold, stildeold, rhotildeold);
+  o.nxt[14] = stildeold * rhobar;
+  o.nxt[12] = ctildeold * rhobar;
+  o.nxt[11] = -stildeold * g[11] + ctildeold * betahat;
+  o.nxt[13] = (zetaold - thetatildeold * g[13]) / rhotildeold;
+  const double taud = (zeta - o.nxt[14] * o.nxt[13]) / o.nxt[12];
+  const double bd = o.nxt[11] - taud;
+  o.res = sqrt(bd * bd + o.nxt[10] * o.nxt[10]);
+  o.nres = fabs(o.nxt[5]);
+}
+
+// GKB vector update of step k: v = v'/alpha_{k+1}; LSQR x += cx w, w = v - cw w; LSMR
+// hbar = h - chb hbar, x += cx hbar, h = v - cw h.  The last block commits the carried
+// scalars, the histories and the stop tests (maxit, discrepancy on the recurrence
+// residual -- reading R19 --, breakdown when alpha or beta vanishes) and advances k.
+__global__ void __launch_bounds__(kVecThreads) k_gkb_update(Params P) {
+  DevState* st = P.st;
+  if (st->done) return;
+  const int k = st->k;
+  const bool lsmr = P.method == 5;
+  const double* g = P.gk + kGkbState * (k & 1);
+  GkbStep o;
+  gkb_scalars(P, g, lsmr, o);
+  const double ia = o.alpha > 0.0 ? 1.0 / o.alpha : 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * kVecThreads + threadIdx.x; i < P.n; i += (int64_t)gridDim.x * kVecThreads) {
+    const double vn = P.z[i] * ia;
+    P.z[i] = vn;
+    if (!lsmr) {
+      const double w = P.gv1[i];
+      P.x[i] = fma(o.cx, w, P.x[i]);
+      P.gv1[i] = fma(-o.cw, w, vn);
+    } else {
+      const double h = P.gv1[i];
+      const double hb = fma(-o.chb, P.gv2[i], h);
+      P.gv2[i] = hb;
+      P.x[i] = fma(o.cx, hb, P.x[i]);
+      P.gv1[i] = fma(-o.cw, h, vn);
+    }
+  }
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(P.ctr + CTR_GKB_UPD, 1) == (int)gridDim.x - 1);
+  __syncthreads();
+  if (!s_last || threadIdx.x != 0) return;
+  P.ctr[CTR_GKB_UPD] = 0;
+  double* gn = P.gk + kGkbState * ((k + 1) & 1);
+  for (int i = 0; i < kGkbState; ++i) gn[i] = o.nxt[i];
+  P.hist_true[k - 1] = o.res;
+  P.hist_sk[k - 1] = o.nres;
+  st->k_x = k;
+  int status = 0;
+  if (o.alpha == 0.0 || o.beta == 0.0)
+    status = 4;
+  else if (P.eta > 0.0 && o.res <= P.eta * P.delta_e)
+    status = 3;
+  else if (k >= P.maxit)
+    status = 1;
+  if (status) {
+    st->status = status;
+    st->done = 1;
+  }
+  st->k = k + 1;
+}
+
+// The same epilogue as a separate pass (matrix-free blur operator or a non-default SpMV
+// variant): y_i = a t_i - c aux_i over t = M x, ||y||^2 into scal[slot_out].
+__global__ void __launch_bounds__(kVecThreads) k_epi_vec(const DevState* st, SpmvEpi E, const double* t, double* y,
+                                                         int64_t len) {
+  __shared__ double sh[33];
+  __shared__ int s_last;
+  if (st->done) return;
+  double a, c;
+  epi_coefs(E, st, a, c);
+  double nrm = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * kVecThreads + threadIdx.x; i < len; i += (int64_t)gridDim.x * kVecThreads) {
+    const double v = E.kind == 3 ? t[i] * a : fma(t[i], a, -c * E.aux[i]);
+    y[i] = v;
+    nrm = fma(v, v, nrm);
+  }
+  nrm = block_sum<kVecThreads>(nrm, sh);
+  if (threadIdx.x == 0) E.part[(size_t)E.slot_out * kVecBlocks + blockIdx.x] = nrm;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(E.ctr + E.ctr_idx, 1) == (int)gridDim.x - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  double v = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += kVecThreads) v += __ldcg(E.part + (size_t)E.slot_out * kVecBlocks + b);
+  v = block_sum<kVecThreads>(v, sh);
+  if (threadIdx.x == 0) {
+    E.scal[E.slot_out] = v;
+    E.ctr[E.ctr_idx] = 0;
+  }
+}
+
+// GKB start (Paige-Saunders / Fong-Saunders initialisation): v_1 = v'/alpha_1, x_0 = 0,
+// LSQR w_1 = v_1 | LSMR h_1 = v_1, hbar_0 = 0; carried scalars of step 1.
+__global__ void __launch_bounds__(kVecThreads) k_gkb_init(Params P) {
+  const bool lsmr = P.method == 5;
+  const double alpha = sqrt(P.scal[P.slot_gka]), beta = sqrt(P.scal[P.slot_beta]);
+  const double ia = alpha > 0.0 ? 1.0 / alpha : 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * kVecThreads + threadIdx.x; i < P.n; i += (int64_t)gridDim.x * kVecThreads) {
+    const double vn = P.z[i] * ia;
+    P.z[i] = vn;
+    P.x[i] = 0.0;
+    P.gv1[i] = vn;
+    if (lsmr) P.gv2[i] = 0.0;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    double* g = P.gk + kGkbState * 1;  // buffer of k = 1
+    for (int i = 0; i < kGkbState; ++i) g[i] = 0.0;
+    g[0] = alpha;
+    g[1] = beta;
+    g[2] = alpha;         // rhobar_1
+    g[3] = beta;          // phibar_1
+    g[4] = alpha;         // alphabar_1
+    g[5] = alpha * beta;  // zetabar_1
+    g[6] = 1.0;           // rho_0
+    g[7] = 1.0;           // rhobar_0
+    g[8] = 1.0;           // cbar_0
+    g[9] = 0.0;           // sbar_0
+    g[10] = beta;         // betadd_1
+    g[11] = 0.0;          // betad
+    g[12] = 1.0;          // rhodold
+    g[13] = 0.0;          // tautildeold
+    g[14] = 0.0;          // thetatilde
+    g[15] = 0.0;          // zeta_0
+    P.st->beta = beta;
+  }
+}
+
 // rhs = s_b = S b (sFLSQR, Alg. 1) or s = beta S z with S_TW = [S z]
 // (sFLSMR, Alg. 2), from skbuf; rhs norm for the tol test; qtb = rhs
 // (LS start); state reset.
@@ -1481,7 +1752,7 @@ __global__ void k_init_rhs(Params P) {
   const double beta = P.st->beta;
   double part = 0.0;
   for (int r = threadIdx.x; r < P.d; r += blockDim.x) {
-    // FLSQR: ||b|| e_1 (eq. FLSQR); FLSMR: set by k_ls at k = 1 (needs T_11)
+    // FLSQR: ||b|| e_1 (eq. FLSQR); FLSMR: set by k_ls at k = 1 (needs T_11); GKB: unused
     const double sv = P.method <= 1 ? P.skbuf[r] : (P.method == 2 && r == 0 ? beta : 0.0);
     const double rv = P.method == 1 ? beta * sv : sv;
     if (P.method == 1) P.STW[r] = sv;

@@ -21,8 +21,9 @@ from ._build import LIB_PATH
 
 OK = 0
 E_INVALID, E_DIM, E_NONFINITE, E_ZERO_RHS, E_STATE, E_CUDA, E_OOM, E_UNSUPPORTED = -1, -2, -3, -4, -5, -6, -7, -8
-METHOD_SFLSQR, METHOD_SFLSMR, METHOD_FLSQR, METHOD_FLSMR = 0, 1, 2, 3
-METHODS = {"sflsqr": METHOD_SFLSQR, "sflsmr": METHOD_SFLSMR, "flsqr": METHOD_FLSQR, "flsmr": METHOD_FLSMR}
+METHOD_SFLSQR, METHOD_SFLSMR, METHOD_FLSQR, METHOD_FLSMR, METHOD_LSQR, METHOD_LSMR = 0, 1, 2, 3, 4, 5
+METHODS = {"sflsqr": METHOD_SFLSQR, "sflsmr": METHOD_SFLSMR, "flsqr": METHOD_FLSQR, "flsmr": METHOD_FLSMR,
+           "lsqr": METHOD_LSQR, "lsmr": METHOD_LSMR}
 ORTH_P, ORTH_Z = 0, 1
 ORTHK_AUTO, ORTHK_MGS = 0, 1
 RUNNING, MAXIT, TOL, DISCREPANCY, BREAKDOWN = 0, 1, 2, 3, 4
@@ -378,5 +379,8 @@ def solver_for_problem(prob, spec, maxit=None, history=HIST_TRUE_RES, use_graph=
         t = None if prob.t_mode == "build" else (prob.T.rowptr, prob.T.col, prob.T.val)
         s.set_operator(A.nrows, A.ncols, A.rowptr, A.col, A.val, t=t)
     s.set_sketch(prob.sketch_seed, spec.d, spec.s_nz)
-    s.set_precond(spec.precond, spec.p, spec.eps_rel)
+    if (method or spec.method) in ("lsqr", "lsmr"):
+        s.set_precond("identity")          # GKB methods take no flexible preconditioner
+    else:
+        s.set_precond(spec.precond, spec.p, spec.eps_rel)
     return s
