@@ -125,6 +125,20 @@ def _traffic(workload, kernel):
         return None
 
 
+def _spec_for(prob, method):
+    """The config's solver spec; method "flsqr" / "flsmr" runs the unsketched full-orthogonalisation
+    parent with the config's operator, tau and maxit."""
+    import dataclasses
+    if method is None:
+        return prob.solvers[0]
+    for x in prob.solvers:
+        if x.method == method:
+            return x
+    if method in ("sflsqr", "sflsmr", "flsqr", "flsmr", "lsqr", "lsmr"):
+        return dataclasses.replace(prob.solvers[0], method=method)
+    raise SystemExit(f"unknown method {method}")
+
+
 def run_cpu_baseline(prob, spec, budget_s=25.0):
     """The oracle as it stands (single thread), first iterations of the same workload."""
     from threadpoolctl import threadpool_limits
@@ -189,7 +203,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--method", default=None, help="sflsqr | sflsmr (default: the config's first)")
+    ap.add_argument("--method", default=None,
+                    help="sflsqr | sflsmr | flsqr | flsmr | lsqr | lsmr (default: the config's first; flsqr/flsmr = unsketched, "
+                         "full orthogonalisation)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-profile", action="store_true", help="graph replay without per-kernel events")
@@ -203,7 +219,7 @@ def main():
         if rank != 0:
             return            # the reference arm runs on rank 0 only
         prob = make_problem(args.config, **(dict(N=args.N) if args.N else {}))
-        spec = prob.solvers[0] if args.method is None else [x for x in prob.solvers if x.method == args.method][0]
+        spec = _spec_for(prob, args.method)
         bench_reference(args, prob, spec, world, rank)
         return
 
@@ -242,7 +258,7 @@ def main():
         ab = balanced_row_blocks(np.concatenate([[0], np.cumsum(a_cnt)]), world)
         tb = None if t_cnt is None else balanced_row_blocks(np.concatenate([[0], np.cumsum(t_cnt)]), world)
         prob = make_ct_shard(args.config, ab[rank], None if tb is None else tb[rank], allreduce_sum)
-        spec = prob.solvers[0] if args.method is None else [x for x in prob.solvers if x.method == args.method][0]
+        spec = _spec_for(prob, args.method)
         t_gen = time.perf_counter() - t_gen
         uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
         if rank == 0:
@@ -266,7 +282,7 @@ def main():
         parallelism = f"shard{world} ({'ROWSHARD' if prob.T_loc is not None else 'COLSHARD'}, NCCL)"
     else:
         prob = make_problem(args.config, **(dict(N=args.N) if args.N else {}))
-        spec = prob.solvers[0] if args.method is None else [x for x in prob.solvers if x.method == args.method][0]
+        spec = _spec_for(prob, args.method)
         t_gen = time.perf_counter() - t_gen
         maxit = max(spec.maxit, W + K)
         t_up = time.perf_counter()

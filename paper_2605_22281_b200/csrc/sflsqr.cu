@@ -100,6 +100,8 @@ struct sflsqr {
   int band_shift = 16;   // reserved
   bool prof_on = false;
   Prof prof;
+  int coop_grid = 0;     // blocks of the cooperative phase kernels (0: not available)
+  bool coop_attr = true; // launch with cudaLaunchAttributeCooperative (cleared if unsupported)
 };
 
 namespace {
@@ -587,6 +589,34 @@ int enqueue_ls(sflsqr_t* h, bool forked) {
   return SFLSQR_OK;
 }
 
+// The cooperative phase kernels replace the standalone a1/a2 and a4/a5 kernels on one rank
+// with the fused window orthogonalisation of a sketched method (opt-in: SFLSQR_COOP=1).
+bool use_coop(sflsqr_t* h) {
+  return h->coop_grid > 0 && h->world == 1 && h->P.orth_alg == ORTH_FUSED && h->P.method <= SFLSQR_METHOD_SFLSMR;
+}
+
+int launch_coop(sflsqr_t* h, void (*kern)(Params), double bytes) {
+  Launch L(h, SFLSQR_KC_ORTH, bytes);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(h->coop_grid);
+  cfg.blockDim = dim3(kCoopThreads);
+  cfg.stream = h->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = h->coop_attr ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, h->P);
+  if (e != cudaSuccess && h->coop_attr) {  // e.g. not capturable: all blocks are co-resident anyway
+    cudaGetLastError();
+    h->coop_attr = false;
+    cfg.numAttrs = 0;
+    e = cudaLaunchKernelEx(&cfg, kern, h->P);
+  }
+  if (e != cudaSuccess) return fail(h, SFLSQR_E_CUDA, "cooperative launch: %s", cudaGetErrorString(e));
+  return SFLSQR_OK;
+}
+
 // One iteration k of Alg. 1 / Alg. 2, or of FLSQR /
 // FLSMR (full window, no sketch; FLSMR runs the z side of step k+1 before its
 // projected problem, which needs column k+1 of T).
@@ -597,10 +627,15 @@ int enqueue_iteration(sflsqr_t* h) {
   const double n8 = 8.0 * h->n_loc, m8 = 8.0 * h->m_loc;
   const bool sketched = P.method == SFLSQR_METHOD_SFLSQR || P.method == SFLSQR_METHOD_SFLSMR;
   int rc;
+  const bool coop = use_coop(h);
+  const int Jz = std::min(P.ell, k - 1), Jw = std::min(P.ell + 1, k);
+  // a1 + a2 in one cooperative kernel
+  if (coop && (rc = launch_coop(h, k_zphase, n8 * (3 + 2 * Jz + (P.use_pring ? 1 : 0) + (P.precond ? 1 : 0)))))
+    return rc;
   // a1: z-side windowed orthogonalisation (FLSMR: done at the end of the previous step / in set_rhs)
-  if (P.method != SFLSQR_METHOD_FLSMR && (rc = enqueue_orth(h, 0, 0))) return rc;
+  if (!coop && P.method != SFLSQR_METHOD_FLSMR && (rc = enqueue_orth(h, 0, 0))) return rc;
   // a1 end + a2: normalise, tau, store z_k
-  {
+  if (!coop) {
     Launch L(h, SFLSQR_KC_TAU, n8 * (2 + (P.use_pring ? 1 : 0) + (P.precond ? 1 : 0)));
     k_finish_z<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P);
   }
@@ -613,8 +648,12 @@ int enqueue_iteration(sflsqr_t* h) {
       return fail(h, SFLSQR_E_CUDA, "allgather(z): %s", e.c_str());
     enqueue_apply(h, 0, P.st, h->zfull, 0, 0, P.w, SFLSQR_KC_SPMV_A);
   }
+  // a4 + a5 in one cooperative kernel (sketch of w, then the w side)
+  if (coop && (rc = launch_coop(h, k_wphase,
+                                m8 * (4 + 2 * Jw) + (P.method == SFLSQR_METHOD_SFLSQR ? 12.0 * h->s_nz * h->m_loc : 0.0))))
+    return rc;
   // a4 (sFLSQR): S_AZ[:, k] = S w
-  if (P.method == SFLSQR_METHOD_SFLSQR && (rc = enqueue_sketch(h, P.st, P.w))) return rc;
+  if (!coop && P.method == SFLSQR_METHOD_SFLSQR && (rc = enqueue_sketch(h, P.st, P.w))) return rc;
   // a7 can start now for sFLSQR (it needs only S A Z_k) / after a5 for FLSQR (it needs
   // H_{:,k}): it runs on the side stream, overlapped with the T product (a6), and is
   // joined before a8.  Sequential when profiling (clean per-kernel events).
@@ -622,8 +661,8 @@ int enqueue_iteration(sflsqr_t* h) {
                        (P.method == SFLSQR_METHOD_SFLSQR || P.method == SFLSQR_METHOD_FLSQR);
   if (fork_ls && P.method == SFLSQR_METHOD_SFLSQR && (rc = enqueue_ls(h, true))) return rc;
   // a5: w-side windowed orthogonalisation and normalisation
-  if ((rc = enqueue_orth(h, 1, 0))) return rc;
-  {
+  if (!coop) {
+    if ((rc = enqueue_orth(h, 1, 0))) return rc;
     Launch L(h, SFLSQR_KC_ORTH, 2 * m8);
     k_finish_w<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P);
   }
@@ -857,6 +896,8 @@ int alloc_solve(sflsqr_t* h) {
   const size_t zlen = std::max<size_t>(n, (size_t)h->n_max);
   if ((rc = dalloc(h, (void**)&P.st, sizeof(DevState), &h->solve_allocs, &h->solve_sizes))) return rc;
   if ((rc = dalloc(h, (void**)&P.ctr, sizeof(int) * CTR_COUNT, &h->solve_allocs, &h->solve_sizes))) return rc;
+  if ((rc = dalloc(h, (void**)&P.bar, sizeof(unsigned int) * 2, &h->solve_allocs, &h->solve_sizes))) return rc;
+  CU(h, cudaMemset(P.bar, 0, sizeof(unsigned int) * 2));
   if ((rc = A(&P.z, zlen)) || (rc = A(&P.x, n)) || (rc = A(&P.Z, n * ncol)) || (rc = A(&P.w, m)) ||
       (rc = A(&P.W, m * (ncol + 1))) || (rc = A(&P.b, m)) || (rc = A(&P.H, (size_t)(maxit + 1) * maxit)) ||
       (rc = A(&P.Tm, (size_t)(maxit + 1) * (maxit + 1))) || (rc = A(&P.part, (size_t)s * kVecBlocks)) ||
@@ -1075,6 +1116,19 @@ int sflsqr_create(sflsqr_t** out, const sflsqr_opts* o) {
     }
   }
   if (const char* ev = std::getenv("SFLSQR_SPMV_MODE")) h->spmv_mode = std::atoi(ev);
+  {
+    // co-resident blocks of the cooperative phase kernels (both kernels, 512 threads)
+    int nsm = 0, oz = 0, ow = 0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, o->device);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oz, k_zphase, kCoopThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ow, k_wphase, kCoopThreads, 0);
+    const int per = std::min(std::min(oz, ow), 2);
+    h->coop_grid = std::min(nsm * per, kVecBlocks);
+    // opt-in (SFLSQR_COOP=1): measured no faster than the standalone kernels
+    const char* nc = std::getenv("SFLSQR_COOP");
+    if (per < 1 || !(nc && nc[0] == '1')) h->coop_grid = 0;
+    cudaGetLastError();
+  }
   if (cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess) {

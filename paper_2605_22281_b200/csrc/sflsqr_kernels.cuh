@@ -67,6 +67,7 @@ struct Params {
   int orth_alg;            // OrthAlg: fused (window <= kFuseJ vectors), literal MGS passes, or CGS2
   int slot_zf, slot_zout, slot_wf, slot_wout;  // fused orthogonalisation slots (kFuseAcc + 1 per side)
   int* ctr;                // last-block arrival counters (one per reduction site)
+  unsigned int* bar;       // grid barrier of the cooperative phase kernels (count, generation)
   double *cpart, *cscal;   // CGS2: (ell + 2) x kVecBlocks dot partials; 2 stages x ldc reduced dots
   int ldc;                 // ell + 2
   // textbook LSQR / LSMR (methods 4 / 5): u' = P.w (m, unnormalised), v = P.z (n), x = P.x,
@@ -446,7 +447,7 @@ __device__ __forceinline__ void epi_coefs(const SpmvEpi& E, const DevState* st, 
 }
 
 template <int WPB, int UNR, int LANES, bool EPI = false>
-__global__ void __launch_bounds__(WPB * 32, 2048 / (WPB * 32)) k_spmv_csr_pf(const DevState* st, int64_t nrows,
+__global__ void __launch_bounds__(WPB * 32, EPI ? 2 : 2048 / (WPB * 32)) k_spmv_csr_pf(const DevState* st, int64_t nrows,
                                                             const int64_t* __restrict__ rowptr,
                                                             const int* __restrict__ col,
                                                             const double* __restrict__ val,
@@ -857,23 +858,21 @@ __global__ void __launch_bounds__(kVecThreads) k_mgs_pass(Params P, int side, in
 template <int JM>
 __device__ __forceinline__ int gram_idx(int i, int j) { return 1 + JM + j * (j - 1) / 2 + i; }
 
-__global__ void __launch_bounds__(kVecThreads) k_orth_dots(Params P, int side, int koff) {
-  __shared__ double red[kVecThreads / 32][kFuseAcc + 1];
-  const DevState* st = P.st;
-  if (st->done) return;
-  const int k = st->k + koff;
-  const int J = side == 0 ? min(P.ell, k - 1) : min(P.ell + 1, k);
-  const int j0 = max(1, k - P.ell);
+// Block-level bodies (NT threads), shared by the standalone kernels below and the
+// cooperative phase kernels (k_zphase / k_wphase).
+// Dots + Gram: block partials of ||v||^2, <q_j, v>, <q_i, q_j> into part[base + a][blockIdx].
+template <int NT>
+__device__ __forceinline__ void orth_dots_block(const Params& P, int side, int J, int j0, int base) {
+  __shared__ double red[NT / 32][kFuseAcc + 1];
   const double* __restrict__ v = side == 0 ? P.z : P.w;
   const int64_t len = side == 0 ? P.n : P.m;
-  const int base = side == 0 ? P.slot_zf : P.slot_wf;
   const double* q[kFuseJ];
 #pragma unroll
   for (int j = 0; j < kFuseJ; ++j) q[j] = j < J ? mgs_basis(P, side, j0 + j) : nullptr;
   double acc[kFuseAcc];
 #pragma unroll
   for (int a = 0; a < kFuseAcc; ++a) acc[a] = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * kVecThreads + threadIdx.x; i < len; i += (int64_t)gridDim.x * kVecThreads) {
+  for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < len; i += (int64_t)gridDim.x * NT) {
     const double vi = v[i];
     acc[0] = fma(vi, vi, acc[0]);
     double qv[kFuseJ];
@@ -897,27 +896,16 @@ __global__ void __launch_bounds__(kVecThreads) k_orth_dots(Params P, int side, i
   if (threadIdx.x < kFuseAcc) {
     double t = 0.0;
 #pragma unroll
-    for (int w = 0; w < kVecThreads / 32; ++w) t += red[w][threadIdx.x];
+    for (int w = 0; w < NT / 32; ++w) t += red[w][threadIdx.x];
     P.part[(size_t)(base + threadIdx.x) * kVecBlocks + blockIdx.x] = t;
   }
-  last_block_reduce(P, base, kFuseAcc, side == 0 ? CTR_ZDOTS : CTR_WDOTS, false);
 }
 
-__global__ void __launch_bounds__(kVecThreads) k_orth_axpy(Params P, int side, int koff) {
-  __shared__ double sh[33];
-  const DevState* st = P.st;
-  if (st->done) return;
-  const int k = st->k + koff;
-  const int J = side == 0 ? min(P.ell, k - 1) : min(P.ell + 1, k);
-  const int j0 = max(1, k - P.ell);
-  double* __restrict__ v = side == 0 ? P.z : P.w;
-  const int64_t len = side == 0 ? P.n : P.m;
-  const int base = side == 0 ? P.slot_zf : P.slot_wf;
-  const double* q[kFuseJ];
-  double c[kFuseJ];
+// MGS coefficients from the reduced dots / Gram (scal[base ..]): c_j = d_j - sum_{i<j} c_i G_ij;
+// block 0 stores them as column k of Tm (side 0) / H (side 1).
+__device__ __forceinline__ void orth_coefs(const Params& P, int side, int k, int J, int j0, int base, double* c) {
 #pragma unroll
   for (int j = 0; j < kFuseJ; ++j) {
-    q[j] = j < J ? mgs_basis(P, side, j0 + j) : nullptr;
     double cj = 0.0;
     if (j < J) {
       cj = P.scal[base + 1 + j];
@@ -935,8 +923,19 @@ __global__ void __launch_bounds__(kVecThreads) k_orth_axpy(Params P, int side, i
         P.H[(int64_t)row + (int64_t)(k - 1) * P.ldh] = c[j];
     }
   }
+}
+
+// v -= sum_j c_j q_j (window order); block partial of ||v||^2 into part[so][blockIdx].
+template <int NT>
+__device__ __forceinline__ void orth_axpy_block(const Params& P, int side, int J, int j0, const double* c, int so) {
+  __shared__ double sh[33];
+  double* __restrict__ v = side == 0 ? P.z : P.w;
+  const int64_t len = side == 0 ? P.n : P.m;
+  const double* q[kFuseJ];
+#pragma unroll
+  for (int j = 0; j < kFuseJ; ++j) q[j] = j < J ? mgs_basis(P, side, j0 + j) : nullptr;
   double acc = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * kVecThreads + threadIdx.x; i < len; i += (int64_t)gridDim.x * kVecThreads) {
+  for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < len; i += (int64_t)gridDim.x * NT) {
     double vi = v[i];
 #pragma unroll
     for (int j = 0; j < kFuseJ; ++j)
@@ -944,9 +943,32 @@ __global__ void __launch_bounds__(kVecThreads) k_orth_axpy(Params P, int side, i
     v[i] = vi;
     acc = fma(vi, vi, acc);
   }
-  acc = block_sum<kVecThreads>(acc, sh);
-  const int so = side == 0 ? P.slot_zout : P.slot_wout;
+  acc = block_sum<NT>(acc, sh);
   if (threadIdx.x == 0) P.part[(size_t)so * kVecBlocks + blockIdx.x] = acc;
+}
+
+__global__ void __launch_bounds__(kVecThreads) k_orth_dots(Params P, int side, int koff) {
+  const DevState* st = P.st;
+  if (st->done) return;
+  const int k = st->k + koff;
+  const int J = side == 0 ? min(P.ell, k - 1) : min(P.ell + 1, k);
+  const int j0 = max(1, k - P.ell);
+  const int base = side == 0 ? P.slot_zf : P.slot_wf;
+  orth_dots_block<kVecThreads>(P, side, J, j0, base);
+  last_block_reduce(P, base, kFuseAcc, side == 0 ? CTR_ZDOTS : CTR_WDOTS, false);
+}
+
+__global__ void __launch_bounds__(kVecThreads) k_orth_axpy(Params P, int side, int koff) {
+  const DevState* st = P.st;
+  if (st->done) return;
+  const int k = st->k + koff;
+  const int J = side == 0 ? min(P.ell, k - 1) : min(P.ell + 1, k);
+  const int j0 = max(1, k - P.ell);
+  const int base = side == 0 ? P.slot_zf : P.slot_wf;
+  double c[kFuseJ];
+  orth_coefs(P, side, k, J, j0, base, c);
+  const int so = side == 0 ? P.slot_zout : P.slot_wout;
+  orth_axpy_block<kVecThreads>(P, side, J, j0, c, so);
   last_block_reduce(P, so, 1, side == 0 ? CTR_ZAXPY : CTR_WAXPY, false);
 }
 
@@ -1101,21 +1123,16 @@ __device__ __forceinline__ double z_norm2(const Params& P, int J, double* sh) {
 // ------------------------------------------------------------------ a1 end + a2: normalise, tau, store
 // t = ||z||, breakdown test (R11), T_kk = t, p_k = z/t, z_k = tau_k(p_k)
 // (Alg. 1; Alg. 2; readings R7/R8), Z[:,k] = z_k, P ring.
-__global__ void __launch_bounds__(kVecThreads) k_finish_z(Params P) {
-  __shared__ double sh[33];
-  DevState* st = P.st;
-  if (st->done) return;
-  const int k = st->k;
-  const int J = min(P.ell, k - 1);
-  const double t = sqrt(z_norm2<kVecThreads>(P, J, sh));
-  const double zin = sqrt(P.orth_alg != ORTH_MGS ? P.scal[P.slot_zf] : get_sum<kVecThreads>(P, P.slot_zin, sh, kVecBlocks));
+// Body (NT threads per block): t = ||z_perp||, zin = ||T w_k||.  Returns false on breakdown.
+template <int NT>
+__device__ __forceinline__ bool finish_z_body(const Params& P, DevState* st, int k, double t, double zin) {
   if (t == 0.0 || t <= 1e-14 * zin) {
     __syncthreads();
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       st->done = 1;
       st->status = 4;  // SFLSQR_BREAKDOWN; y still holds y_{k-1}
     }
-    return;
+    return false;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) P.Tm[(int64_t)(k - 1) + (int64_t)(k - 1) * P.ldtm] = t;
   // tau weights need x_{k-1} (computed by k_xupdate at the end of iteration k-1)
@@ -1134,7 +1151,7 @@ __global__ void __launch_bounds__(kVecThreads) k_finish_z(Params P) {
   }
   double* zk = P.Z + (int64_t)(k - 1) * P.n;
   double* pr = P.use_pring ? P.Pring + (int64_t)((k - 1) % P.ell) * P.n : nullptr;
-  for (int64_t i = (int64_t)blockIdx.x * kVecThreads + threadIdx.x; i < P.n; i += (int64_t)gridDim.x * kVecThreads) {
+  for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < P.n; i += (int64_t)gridDim.x * NT) {
     const double p = P.z[i] / t;
     double zi = p;
     if (mode == 1) {
@@ -1150,11 +1167,38 @@ __global__ void __launch_bounds__(kVecThreads) k_finish_z(Params P) {
     if (pr) pr[i] = p;
     if (P.zsend) P.zsend[i] = zi;
   }
+  return true;
+}
+
+__global__ void __launch_bounds__(kVecThreads) k_finish_z(Params P) {
+  __shared__ double sh[33];
+  DevState* st = P.st;
+  if (st->done) return;
+  const int k = st->k;
+  const int J = min(P.ell, k - 1);
+  const double t = sqrt(z_norm2<kVecThreads>(P, J, sh));
+  const double zin = sqrt(P.orth_alg != ORTH_MGS ? P.scal[P.slot_zf] : get_sum<kVecThreads>(P, P.slot_zin, sh, kVecBlocks));
+  finish_z_body<kVecThreads>(P, st, k, t, zin);
 }
 
 // ------------------------------------------------------------------ a5 end: normalise w
 // H_{k+1,k} = ||w||; w_{k+1} = w / H_{k+1,k} (Alg. 1; Alg. 2);
 // breakdown (R11): H_{k+1,k} = 0, w_{k+1} = 0, the step-k LS is still solved.
+template <int NT>
+__device__ __forceinline__ void finish_w_body(const Params& P, DevState* st, int k, double hn, double win) {
+  const bool brk = (hn == 0.0 || hn <= 1e-14 * win);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->wbreak = brk ? 1 : 0;
+    P.H[(int64_t)k + (int64_t)(k - 1) * P.ldh] = brk ? 0.0 : hn;
+  }
+  double* wk1 = P.W + (int64_t)k * P.m;
+  for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < P.m; i += (int64_t)gridDim.x * NT) {
+    const double wv = brk ? 0.0 : P.w[i] / hn;
+    wk1[i] = wv;
+    if (P.wsend) P.wsend[i] = wv;
+  }
+}
+
 __global__ void __launch_bounds__(kVecThreads) k_finish_w(Params P) {
   __shared__ double sh[33];
   DevState* st = P.st;
@@ -1164,17 +1208,88 @@ __global__ void __launch_bounds__(kVecThreads) k_finish_w(Params P) {
   const double hn =
       sqrt(P.orth_alg != ORTH_MGS ? P.scal[P.slot_wout] : get_sum<kVecThreads>(P, P.slot_w0 + J, sh, kVecBlocks));
   const double win = sqrt(P.orth_alg != ORTH_MGS ? P.scal[P.slot_wf] : get_sum<kVecThreads>(P, P.slot_win, sh, kVecBlocks));
-  const bool brk = (hn == 0.0 || hn <= 1e-14 * win);
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    st->wbreak = brk ? 1 : 0;
-    P.H[(int64_t)k + (int64_t)(k - 1) * P.ldh] = brk ? 0.0 : hn;
+  finish_w_body<kVecThreads>(P, st, k, hn, win);
+}
+
+// ------------------------------------------------------------------ cooperative phase kernels
+// One launch per vector phase instead of three or four (one rank, fused window orth):
+// all blocks are co-resident (cooperative launch), phases are separated by a grid barrier,
+// and each reduction is summed in fixed block order by one designated block per slot.
+//   k_zphase: a1 + a2 (z-side dots/Gram -> axpy + norm -> normalise, tau, store z_k)
+//   k_wphase: a4 (sFLSQR sketch of w) + a5 (w-side dots/Gram -> axpy + norm -> w_{k+1})
+constexpr int kCoopThreads = 512;
+
+__device__ __forceinline__ void grid_sync(unsigned int* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned int* gen = bar + 1;
+    const unsigned int g = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*gen == g) __nanosleep(32);
+    }
+    __threadfence();
   }
-  double* wk1 = P.W + (int64_t)k * P.m;
-  for (int64_t i = (int64_t)blockIdx.x * kVecThreads + threadIdx.x; i < P.m; i += (int64_t)gridDim.x * kVecThreads) {
-    const double wv = brk ? 0.0 : P.w[i] / hn;
-    wk1[i] = wv;
-    if (P.wsend) P.wsend[i] = wv;
+  __syncthreads();
+}
+
+// scal[s0 + t] = sum over blocks of part[s0 + t][b] (block t mod gridDim reduces slot t), then a barrier.
+__device__ __forceinline__ void coop_reduce(const Params& P, int s0, int ns) {
+  __shared__ double sh[33];
+  grid_sync(P.bar);
+  for (int t = blockIdx.x; t < ns; t += gridDim.x) {
+    const double* pp = P.part + (size_t)(s0 + t) * kVecBlocks;
+    double v = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += kCoopThreads) v += __ldcg(pp + b);
+    v = block_sum<kCoopThreads>(v, sh);
+    if (threadIdx.x == 0) P.scal[s0 + t] = v;
   }
+  grid_sync(P.bar);
+}
+
+__global__ void __launch_bounds__(kCoopThreads) k_zphase(Params P) {
+  DevState* st = P.st;
+  if (st->done) return;
+  const int k = st->k;
+  const int J = min(P.ell, k - 1), j0 = max(1, k - P.ell);
+  orth_dots_block<kCoopThreads>(P, 0, J, j0, P.slot_zf);
+  coop_reduce(P, P.slot_zf, kFuseAcc);
+  double c[kFuseJ];
+  orth_coefs(P, 0, k, J, j0, P.slot_zf, c);
+  orth_axpy_block<kCoopThreads>(P, 0, J, j0, c, P.slot_zout);
+  coop_reduce(P, P.slot_zout, 1);
+  finish_z_body<kCoopThreads>(P, st, k, sqrt(P.scal[P.slot_zout]), sqrt(P.scal[P.slot_zf]));
+}
+
+__global__ void __launch_bounds__(kCoopThreads) k_wphase(Params P) {
+  __shared__ double sh[33];
+  DevState* st = P.st;
+  if (st->done) return;
+  const int k = st->k;
+  if (P.method == 0) {  // a4: S_AZ[:, k] = S w (rows of the stored transposed S, fixed order)
+    for (int r = blockIdx.x; r < P.d; r += gridDim.x) {
+      double acc = 0.0;
+      for (int64_t q = P.sk_rp[r] + threadIdx.x; q < P.sk_rp[r + 1]; q += kCoopThreads) {
+        const uint32_t e = __ldg(P.sk_ent + q);
+        const double vi = P.w[e & 0x7fffffffu];
+        acc += (e >> 31) ? -vi : vi;
+      }
+      acc = block_sum<kCoopThreads>(acc, sh) * P.sk_scale;
+      if (threadIdx.x == 0) P.skbuf[r] = acc;
+    }
+  }
+  const int J = min(P.ell + 1, k), j0 = max(1, k - P.ell);
+  orth_dots_block<kCoopThreads>(P, 1, J, j0, P.slot_wf);
+  coop_reduce(P, P.slot_wf, kFuseAcc);
+  double c[kFuseJ];
+  orth_coefs(P, 1, k, J, j0, P.slot_wf, c);
+  orth_axpy_block<kCoopThreads>(P, 1, J, j0, c, P.slot_wout);
+  coop_reduce(P, P.slot_wout, 1);
+  finish_w_body<kCoopThreads>(P, st, k, sqrt(P.scal[P.slot_wout]), sqrt(P.scal[P.slot_wf]));
 }
 
 // ------------------------------------------------------------------ a7: projected sketched LS (one CTA)

@@ -1,0 +1,6 @@
+# GPU tests + short benches of configs 4 and 3 (no CPU baseline / e2e)
+timeout 1500 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+for c in "--config 4" "--config 3" "--config 3 --method sflsmr" ${EXTRA_BENCH:-}; do
+  tag=$(echo $c | tr -d ' -')
+  timeout 900 python bench.py --no-cpu-baseline --no-e2e $c > gpurun_out/bench_$tag.log 2>&1
+done

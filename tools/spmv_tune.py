@@ -21,7 +21,7 @@ nnzA, nnzT = info["nnz_a"], info["nnz_t"]
 rng = np.random.default_rng(0)
 x, w = rng.standard_normal(p.n), rng.standard_normal(p.m)
 ref = None
-variants = [(m, 16) for m in (3, 8, 11, 12, 13, 14)]
+variants = [(m, 16) for m in (14, 3, 8, 10, 11, 12, 13, 15)]
 for mode, sh in variants:
     s.debug_set_tuning(mode, sh)
     s.set_profiling(True)
