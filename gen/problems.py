@@ -245,6 +245,7 @@ class SolverSpec:
     eta: float = 0.0     # discrepancy safety factor (0 = off)
     tol: float = 0.0
     orth_mode: str = "P"
+    sketch: str = "sparse"   # "sparse" (sparse-sign, R5/R6) | "gaussian" (dense N(0, 1/d), R21)
 
 
 @dataclass
@@ -278,6 +279,15 @@ CONFIGS = {
             solvers=[("sflsqr", 200, 4, 400, 8, "identity", 0.0)]),
     5: dict(name="c5_ct2048", kind="ct", N=2048, n_angles=1440, nb=2897, delta=0.01, matched=True, tile=4,
             solvers=[("sflsqr", 300, 5, 600, 8, "irn", 0.0), ("sflsmr", 300, 5, 600, 8, "irn", 0.0)]),
+    # the paper's synthetic family:
+    # A 1024 x 512 with singular values rho^(1-i), rho = 1.01, x_true = ones, ||b_true|| = 1,
+    # white noise ||e|| = delta in {1%, 10%}; Gaussian sketch with s = 2k + 1 rows (k = maxit
+    # = 50, not stated in the paper); sLSQR / sLSMR = sFLSQR / sFLSMR with tau = id and no
+    # truncation (full window, L1150-1152).
+    6: dict(name="c6_decay_rho1.01_noise1", kind="decay", m=1024, n=512, rho=1.01, delta=0.01, sketch="gaussian",
+            solvers=[("sflsqr", 50, 50, 101, 1, "identity", 0.0), ("sflsmr", 50, 50, 101, 1, "identity", 0.0)]),
+    7: dict(name="c7_decay_rho1.01_noise10", kind="decay", m=1024, n=512, rho=1.01, delta=0.10, sketch="gaussian",
+            solvers=[("sflsqr", 50, 50, 101, 1, "identity", 0.0), ("sflsmr", 50, 50, 101, 1, "identity", 0.0)]),
 }
 
 
@@ -332,12 +342,25 @@ def make_problem(config_index: int, N: Optional[int] = None, n_angles: Optional[
         x_true = ellipse_phantom(Nimg, rx)[tiled_order(Nimg, tile)]
         geometry = dict(N=Nimg, n_angles=na, nb=nbins, tile=tile)
         Ax = A.matvec(x_true, nthreads)
+    elif kind == "decay":
+        m, n = cfg["m"], cfg["n"]
+        U = np.linalg.qr(rA.standard_normal((m, n)))[0]
+        V = np.linalg.qr(rA.standard_normal((n, n)))[0]
+        sig = cfg["rho"] ** (-np.arange(n, dtype=np.float64))          # rho^(1-i), i = 1..n
+        Ad = (U * sig) @ V.T
+        x_true = np.ones(n)
+        Ad = Ad / np.linalg.norm(Ad @ x_true)                           # ||b_true|| = 1 (L546)
+        A = CSR.from_dense(Ad)
+        t_mode = "build"
+        geometry = dict(rho=cfg["rho"], sigma_min=float(sig[-1]))
+        Ax = A.matvec(x_true)
     else:
         raise ValueError(kind)
     g = re.standard_normal(m)
     e = g * (cfg["delta"] * np.linalg.norm(Ax) / np.linalg.norm(g))
     b = Ax + e
-    solvers = [SolverSpec(method=s[0], maxit=s[1], window=s[2], d=s[3], s_nz=s[4], precond=s[5], eta=s[6])
+    solvers = [SolverSpec(method=s[0], maxit=s[1], window=s[2], d=s[3], s_nz=s[4], precond=s[5], eta=s[6],
+                          sketch=cfg.get("sketch", "sparse"))
                for s in cfg["solvers"]]
     return Problem(name=cfg["name"], config_index=config_index, m=m, n=n, A=A, T=T, t_mode=t_mode,
                    blur=blur, x_true=x_true, b=b, e=e, delta=cfg["delta"], delta_e=float(np.linalg.norm(e)),

@@ -246,6 +246,20 @@ int sflsqr_set_operator_blur(sflsqr_t *h, int32_t H, int32_t W, double sigma, in
  * problem needs k <= d) else SFLSQR_E_INVALID.  FLSQR / FLSMR: not needed, ignored. */
 int sflsqr_set_sketch(sflsqr_t *h, uint64_t seed, int32_t d, int32_t s_nz);
 
+/* Dense Gaussian sketch S in R^{d x dim} (the paper's Gaussian sketch, PAPER.md L550-552,
+ * Theorem 2.1 / Corollary L1011-1121; reading R21): S[r, i] = g / sqrt(d), g standard
+ * normal from Box-Muller on Philox4x32-10(key = seed, counter = (i_lo, i_hi, r / 2,
+ * 0x47415553)) (cos for even r, sin for odd r), i the global coordinate.  Generated
+ * once per solve on the device and stored row-major (8 d dim bytes); each S v is a
+ * deterministic GEMV.  Replaces a sparse-sign sketch set earlier (and vice versa).
+ * Requires 1 <= d <= 2048 and d >= maxit else SFLSQR_E_INVALID.  FLSQR / FLSMR /
+ * LSQR / LSMR: ignored. */
+int sflsqr_set_sketch_gaussian(sflsqr_t *h, uint64_t seed, int32_t d);
+
+/* Debug: the Gaussian sketch entries of columns [col0, col0+ncols) as generated by the
+ * device (host output, d x ncols row-major); SFLSQR_E_STATE unless a Gaussian sketch is set. */
+int sflsqr_debug_sketch_dense(sflsqr_t *h, int64_t col0, int64_t ncols, double *out);
+
 /* Flexible preconditioner tau_k (Alg. 1, Alg. 2):
  * kind = SFLSQR_PRECOND_IDENTITY | IRN (p in (0, 2], eps_rel > 0; R7) |
  * NONNEG (eps_rel > 0; R8).  Default: identity. */

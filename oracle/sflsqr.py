@@ -328,6 +328,9 @@ def solve_problem(prob, spec, op=None, maxit=None, record=True, **over):
         return fn(op, prob.b, maxit=maxit or spec.maxit, eta=eta, delta_e=prob.delta_e,
                   record=over.pop("record", record))
     over["method"] = method
+    if getattr(spec, "sketch", "sparse") == "gaussian" and method in ("sflsqr", "sflsmr") and "sketch" not in over:
+        from .sketch import GaussianSketch                 # reading R21
+        over["sketch"] = GaussianSketch(prob.sketch_seed, spec.d, prob.m if method == "sflsqr" else prob.n)
     kw = dict(method=spec.method, maxit=maxit or spec.maxit, window=spec.window, sketch_seed=prob.sketch_seed,
               d=spec.d, s_nz=spec.s_nz, precond=spec.precond, p_exp=spec.p, eps_rel=spec.eps_rel,
               tol=spec.tol, eta=spec.eta, delta_e=prob.delta_e, orth_mode=spec.orth_mode, record=record)

@@ -91,3 +91,51 @@ class DenseSketch:
 
     def apply(self, v):
         return self.S @ v
+
+
+GAUSS_DOMAIN = 0x47415553   # 'GAUS': counter word 3 of the Gaussian draws (reading R21)
+
+
+def gaussian_table(seed: int, d: int, col0: int, ncols: int) -> np.ndarray:
+    """Gaussian sketch entries S[r, i] for columns i in [col0, col0+ncols), shape (d, ncols).
+
+    Reading R21: the paper's Gaussian sketch (Theorem 2.1 /
+    Corollary L1011-1121) with i.i.d. N(0, 1/d) entries, drawn by a counter-based
+    generator so that any rank can produce any column: for the pair t of rows (2t, 2t+1)
+    of column i, (w0, w1, w2, w3) = Philox4x32-10(key = (seed_lo, seed_hi),
+    counter = (i_lo, i_hi, t, 'GAUS')); u1 = (((w1 << 32) | w0) >> 11 + 1/2) 2^-53,
+    u2 likewise from (w3, w2); Box-Muller: g_2t = sqrt(-2 ln u1) cos(2 pi u2),
+    g_2t+1 = sqrt(-2 ln u1) sin(2 pi u2); S[r, i] = g_r / sqrt(d).
+    """
+    npair = (d + 1) // 2
+    i = np.arange(col0, col0 + ncols, dtype=np.uint64)
+    key = np.array([seed & 0xFFFFFFFF, (seed >> 32) & 0xFFFFFFFF], dtype=np.uint64)
+    S = np.empty((d, ncols))
+    for t in range(npair):
+        ctr = np.stack([i & np.uint64(0xFFFFFFFF), i >> np.uint64(32), np.full(ncols, t, dtype=np.uint64),
+                        np.full(ncols, GAUSS_DOMAIN, dtype=np.uint64)], axis=-1)
+        w = philox4x32_10(ctr, key).astype(np.uint64)
+        a = ((w[:, 1] << np.uint64(32)) | w[:, 0]) >> np.uint64(11)
+        b = ((w[:, 3] << np.uint64(32)) | w[:, 2]) >> np.uint64(11)
+        u1 = (a.astype(np.float64) + 0.5) * 2.0 ** -53
+        u2 = (b.astype(np.float64) + 0.5) * 2.0 ** -53
+        r = np.sqrt(-2.0 * np.log(u1))
+        th = (2.0 * np.pi) * u2
+        S[2 * t] = r * np.cos(th)
+        if 2 * t + 1 < d:
+            S[2 * t + 1] = r * np.sin(th)
+    return S / np.sqrt(d)
+
+
+class GaussianSketch:
+    """Dense Gaussian S in R^{d x dim} (reading R21); apply(v) = S v (row-wise dot products)."""
+
+    def __init__(self, seed: int, d: int, dim: int):
+        self.seed, self.d, self.dim = seed, d, dim
+        self.S = gaussian_table(seed, d, 0, dim)
+
+    def apply(self, v: np.ndarray) -> np.ndarray:
+        return self.S @ np.asarray(v, dtype=np.float64)
+
+    def dense(self) -> np.ndarray:
+        return self.S

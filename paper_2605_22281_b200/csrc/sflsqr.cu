@@ -79,6 +79,7 @@ struct sflsqr {
   C16 ca, ct;           // CSR-16 index copies of A and T (default SpMV format when ok)
   // sketch
   bool sk_set = false;
+  int sk_kind = 0;  // 0 sparse-sign (R5/R6), 1 dense Gaussian (R21)
   uint64_t seed = 0;
   int d = 0, s_nz = 0, G = 1;
   // precond
@@ -435,7 +436,10 @@ void enqueue_apply(sflsqr_t* h, int which, const DevState* st, const double* x, 
 // skbuf = S v (this rank's coordinates), allreduced over ranks.
 int enqueue_sketch(sflsqr_t* h, const DevState* st, const double* v) {
   const int64_t dim_loc = h->P.method == SFLSQR_METHOD_SFLSQR ? h->m_loc : h->n_loc;
-  {
+  if (h->sk_kind == 1) {
+    Launch L(h, SFLSQR_KC_SKETCH, 8.0 * h->d * dim_loc + 8.0 * dim_loc + 8.0 * h->d);
+    k_sketch_dense<<<std::min(h->d, 148 * 8), 256, 0, h->stream>>>(st, h->P.sk_dense, dim_loc, v, h->d, h->P.skbuf);
+  } else {
     Launch L(h, SFLSQR_KC_SKETCH, 12.0 * h->s_nz * dim_loc + 8.0 * (h->d + 1) + 8.0 * h->d);
     const int grid = std::min(h->d, 148 * 8);
     k_sketch_apply<<<grid, 256, 0, h->stream>>>(st, h->P.sk_rp, h->P.sk_ent, v, h->d, h->P.sk_scale, h->P.skbuf);
@@ -592,7 +596,8 @@ int enqueue_ls(sflsqr_t* h, bool forked) {
 // The cooperative phase kernels replace the standalone a1/a2 and a4/a5 kernels on one rank
 // with the fused window orthogonalisation of a sketched method (opt-in: SFLSQR_COOP=1).
 bool use_coop(sflsqr_t* h) {
-  return h->coop_grid > 0 && h->world == 1 && h->P.orth_alg == ORTH_FUSED && h->P.method <= SFLSQR_METHOD_SFLSMR;
+  return h->coop_grid > 0 && h->world == 1 && h->P.orth_alg == ORTH_FUSED && h->P.method <= SFLSQR_METHOD_SFLSMR &&
+         h->sk_kind == 0;
 }
 
 int launch_coop(sflsqr_t* h, void (*kern)(Params), double bytes) {
@@ -788,6 +793,17 @@ int build_sketch(sflsqr_t* h) {
   const bool q = P.method == SFLSQR_METHOD_SFLSQR;
   const int64_t dim = q ? h->m_loc : h->n_loc, col0 = q ? h->m0 : h->n0;
   const int s = h->s_nz, d = h->d;
+  if (h->sk_kind == 1) {  // dense Gaussian, generated on the device (reading R21)
+    int rc;
+    if ((rc = dalloc(h, (void**)&P.sk_dense, sizeof(double) * (size_t)d * std::max<int64_t>(dim, 1), &h->solve_allocs,
+                     &h->solve_sizes)))
+      return rc;
+    const int grid = (int)std::min<int64_t>(((d + 1) / 2 * dim + 255) / 256 + 1, 148 * 16);
+    k_sketch_gauss_gen<<<grid, 256, 0, h->stream>>>(col0, dim, d, P.seed_lo, P.seed_hi, std::sqrt((double)d),
+                                                    P.sk_dense, dim);
+    CU(h, cudaStreamSynchronize(h->stream));
+    return check_launch(h);
+  }
   const int64_t ne = dim * s;
   int* drows = nullptr;
   int8_t* dsig = nullptr;
@@ -1374,6 +1390,7 @@ int sflsqr_set_sketch(sflsqr_t* h, uint64_t seed, int32_t d, int32_t s_nz) {
   if (s_nz < 1 || s_nz > d || s_nz > 32) return fail(h, SFLSQR_E_INVALID, "need 1 <= s <= min(d, 32)");
   if (d < h->o.maxit) return fail(h, SFLSQR_E_INVALID, "need d >= maxit (k <= d for the projected problem)");
   free_solve(h);
+  h->sk_kind = 0;
   h->seed = seed;
   h->d = d;
   h->s_nz = s_nz;
@@ -1382,6 +1399,42 @@ int sflsqr_set_sketch(sflsqr_t* h, uint64_t seed, int32_t d, int32_t s_nz) {
   h->G = G;
   h->sk_set = true;
   return SFLSQR_OK;
+}
+
+int sflsqr_set_sketch_gaussian(sflsqr_t* h, uint64_t seed, int32_t d) {
+  if (!h) return fail(nullptr, SFLSQR_E_INVALID, "NULL handle");
+  if (h->o.method >= SFLSQR_METHOD_FLSQR) return SFLSQR_OK;  // unsketched methods: ignored
+  if (d < 1 || d > kMaxD) return fail(h, SFLSQR_E_INVALID, "need 1 <= d <= %d", kMaxD);
+  if (d < h->o.maxit) return fail(h, SFLSQR_E_INVALID, "need d >= maxit (k <= d for the projected problem)");
+  free_solve(h);
+  h->seed = seed;
+  h->d = d;
+  h->s_nz = 1;
+  h->G = 1;
+  h->sk_kind = 1;
+  h->sk_set = true;
+  return SFLSQR_OK;
+}
+
+int sflsqr_debug_sketch_dense(sflsqr_t* h, int64_t col0, int64_t ncols, double* out) {
+  if (!h) return fail(nullptr, SFLSQR_E_INVALID, "NULL handle");
+  if (!h->sk_set || h->sk_kind != 1) return fail(h, SFLSQR_E_STATE, "Gaussian sketch not set");
+  if (col0 < 0 || ncols < 0 || !out) return fail(h, SFLSQR_E_INVALID, "bad arguments");
+  if (ncols == 0) return SFLSQR_OK;
+  cudaSetDevice(h->o.device);
+  double* dS = nullptr;
+  int rc;
+  if ((rc = dalloc(h, (void**)&dS, sizeof(double) * (size_t)h->d * ncols, nullptr))) return rc;
+  const int grid = (int)std::min<int64_t>(((h->d + 1) / 2 * ncols + 255) / 256 + 1, 148 * 16);
+  k_sketch_gauss_gen<<<grid, 256, 0, h->stream>>>(col0, ncols, h->d, (uint32_t)(h->seed & 0xffffffffu),
+                                                  (uint32_t)(h->seed >> 32), std::sqrt((double)h->d), dS, ncols);
+  rc = check_launch(h);
+  if (!rc) {
+    cudaMemcpyAsync(out, dS, sizeof(double) * (size_t)h->d * ncols, cudaMemcpyDeviceToHost, h->stream);
+    if (cudaStreamSynchronize(h->stream) != cudaSuccess) rc = fail(h, SFLSQR_E_CUDA, "sketch copy failed");
+  }
+  cudaFree(dS);
+  return rc;
 }
 
 int sflsqr_set_precond(sflsqr_t* h, int32_t kind, double p, double eps_rel) {

@@ -75,6 +75,7 @@ struct Params {
   double *gv1, *gv2, *gk;
   int slot_gka, slot_gkb;  // ||v'||^2 (alpha^2) and ||u'||^2 (beta^2) partials
   // sketch
+  double* sk_dense;        // Gaussian sketch (reading R21): d x dim_loc, row-major (else NULL)
   int64_t* sk_rp;          // S stored transposed: d+1 row pointers
   uint32_t* sk_ent;         // coordinate | sign << 31, s * dim entries
   double *rhs, *Mcols, *STW;
@@ -751,6 +752,55 @@ __global__ void __launch_bounds__(256) k_sketch_apply(const DevState* st, const 
       acc += (e >> 31) ? -vi : vi;
     }
     acc = block_sum<256>(acc, sh) * scale;
+    if (threadIdx.x == 0) out[r] = acc;
+  }
+}
+
+// ------------------------------------------------------------------ a4 (Gaussian sketch, reading R21)
+// S[r, i] = g_r(i) / sqrt(d), g from Box-Muller on Philox4x32-10(key = seed, counter =
+// (i_lo, i_hi, t, 'GAUS')) for the row pair (2t, 2t+1) of global column i -- the paper's
+// Gaussian sketch (Theorem 2.1 / Corollary L1011-1121), stored dense
+// (d x dim, row-major) and applied as a GEMV.  The oracle (oracle/sketch.py) implements
+// the same definition independently; entries agree to the last bits of log / sin / cos.
+constexpr uint32_t kGaussDomain = 0x47415553u;
+
+__device__ __forceinline__ void gauss_pair(uint64_t i, uint32_t t, uint32_t k0, uint32_t k1, double& g0,
+                                           double& g1) {
+  uint32_t c0 = (uint32_t)(i & 0xffffffffu), c1 = (uint32_t)(i >> 32), c2 = t, c3 = kGaussDomain;
+  philox4x32_10(c0, c1, c2, c3, k0, k1);
+  const uint64_t a = (((uint64_t)c1 << 32) | c0) >> 11, b = (((uint64_t)c3 << 32) | c2) >> 11;
+  const double u1 = ((double)a + 0.5) * 0x1p-53, u2 = ((double)b + 0.5) * 0x1p-53;
+  const double r = sqrt(-2.0 * log(u1)), th = (2.0 * 3.141592653589793) * u2;
+  g0 = r * cos(th);
+  g1 = r * sin(th);
+}
+
+__global__ void __launch_bounds__(256) k_sketch_gauss_gen(int64_t col0, int64_t ncols, int d, uint32_t k0,
+                                                          uint32_t k1, double sqrt_d, double* __restrict__ S,
+                                                          int64_t ld) {
+  const int npair = (d + 1) / 2;
+  const int64_t total = (int64_t)npair * ncols;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int t = (int)(idx / ncols);
+    const int64_t j = idx - (int64_t)t * ncols;
+    double g0, g1;
+    gauss_pair((uint64_t)(col0 + j), (uint32_t)t, k0, k1, g0, g1);
+    S[(int64_t)(2 * t) * ld + j] = g0 / sqrt_d;
+    if (2 * t + 1 < d) S[(int64_t)(2 * t + 1) * ld + j] = g1 / sqrt_d;
+  }
+}
+
+// out[r] = sum_i S[r, i] v_i (one CTA per sketch row, fixed order: deterministic).
+__global__ void __launch_bounds__(256) k_sketch_dense(const DevState* st, const double* __restrict__ S, int64_t dim,
+                                                      const double* __restrict__ v, int d, double* __restrict__ out) {
+  __shared__ double sh[33];
+  if (st && st->done) return;
+  for (int r = blockIdx.x; r < d; r += gridDim.x) {
+    const double* row = S + (int64_t)r * dim;
+    double acc = 0.0;
+    for (int64_t i = threadIdx.x; i < dim; i += 256) acc = fma(__ldg(row + i), __ldg(v + i), acc);
+    acc = block_sum<256>(acc, sh);
     if (threadIdx.x == 0) out[r] = acc;
   }
 }

@@ -38,7 +38,7 @@ EXPORTED = [
     "sflsqr_local_group_destroy", "sflsqr_set_operator_shard", "sflsqr_set_operator", "sflsqr_set_operator_blur", "sflsqr_set_sketch",
     "sflsqr_set_precond", "sflsqr_set_rhs", "sflsqr_iterate", "sflsqr_get_x", "sflsqr_get_residual_norms",
     "sflsqr_get_info", "sflsqr_debug_sketch_table", "sflsqr_debug_apply", "sflsqr_debug_basis", "sflsqr_debug_state",
-    "sflsqr_debug_set_tuning",
+    "sflsqr_debug_set_tuning", "sflsqr_set_sketch_gaussian", "sflsqr_debug_sketch_dense",
     "sflsqr_set_profiling", "sflsqr_reset_profile", "sflsqr_get_profile", "sflsqr_last_error", "sflsqr_destroy",
 ]
 
@@ -90,6 +90,8 @@ def load_library(path: str = LIB_PATH):
         "sflsqr_local_group_destroy": ([vp], None),
         "sflsqr_set_operator_blur": ([vp, i32, i32, f64, i32], ctypes.c_int),
         "sflsqr_set_sketch": ([vp, ctypes.c_uint64, i32, i32], ctypes.c_int),
+        "sflsqr_set_sketch_gaussian": ([vp, ctypes.c_uint64, i32], ctypes.c_int),
+        "sflsqr_debug_sketch_dense": ([vp, i64, i64, vp], ctypes.c_int),
         "sflsqr_set_precond": ([vp, i32, f64, f64], ctypes.c_int),
         "sflsqr_set_rhs": ([vp, vp, i64, i32], ctypes.c_int),
         "sflsqr_iterate": ([vp, i32, ctypes.POINTER(i32), ctypes.POINTER(i32)], ctypes.c_int),
@@ -243,6 +245,15 @@ class SFLSQR:
     def set_sketch(self, seed, d, s_nz):
         self._check(self.lib.sflsqr_set_sketch(self.h, int(seed), int(d), int(s_nz)))
 
+    def set_sketch_gaussian(self, seed, d):
+        self._check(self.lib.sflsqr_set_sketch_gaussian(self.h, int(seed), int(d)))
+        self._gauss_d = int(d)
+
+    def debug_sketch_dense(self, col0, ncols):
+        out = np.empty((self._gauss_d, int(ncols)))
+        self._check(self.lib.sflsqr_debug_sketch_dense(self.h, int(col0), int(ncols), out.ctypes.data))
+        return out
+
     def set_precond(self, kind="identity", p=1.0, eps_rel=1e-3):
         k = {"identity": PRECOND_IDENTITY, "irn": PRECOND_IRN, "nonneg": PRECOND_NONNEG}.get(kind, kind)
         self._check(self.lib.sflsqr_set_precond(self.h, int(k), float(p), float(eps_rel)))
@@ -378,7 +389,10 @@ def solver_for_problem(prob, spec, maxit=None, history=HIST_TRUE_RES, use_graph=
         A = prob.A
         t = None if prob.t_mode == "build" else (prob.T.rowptr, prob.T.col, prob.T.val)
         s.set_operator(A.nrows, A.ncols, A.rowptr, A.col, A.val, t=t)
-    s.set_sketch(prob.sketch_seed, spec.d, spec.s_nz)
+    if getattr(spec, "sketch", "sparse") == "gaussian":
+        s.set_sketch_gaussian(prob.sketch_seed, spec.d)
+    else:
+        s.set_sketch(prob.sketch_seed, spec.d, spec.s_nz)
     if (method or spec.method) in ("lsqr", "lsmr"):
         s.set_precond("identity")          # GKB methods take no flexible preconditioner
     else:

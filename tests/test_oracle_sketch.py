@@ -109,3 +109,32 @@ def test_table_seed_sensitivity():
     assert (r1 != r2).mean() > 0.9
     r3, _ = sparse_sign_table(1 + (1 << 32), 400, 8, 0, 1000)   # high seed word is used
     assert (r1 != r3).mean() > 0.9
+
+
+# ---------------------------------------------------------------- Gaussian sketch (reading R21)
+def test_gaussian_sketch_is_standard_normal_iid():
+    from scipy import stats
+    from oracle.sketch import gaussian_table
+    d, n = 64, 4000
+    S = gaussian_table(0xC0FFEE, d, 0, n) * np.sqrt(d)            # N(0, 1) entries
+    g = S.reshape(-1)
+    assert stats.kstest(g, "norm").pvalue > 1e-3                   # marginal: standard normal
+    assert abs(g.mean()) < 4 / np.sqrt(g.size) and abs(g.var() - 1) < 5 * np.sqrt(2 / g.size)
+    C = np.corrcoef(S)                                              # rows uncorrelated
+    off = C[~np.eye(d, dtype=bool)]
+    assert np.abs(off).max() < 6 / np.sqrt(n)
+    # cos/sin pair of one Box-Muller draw: independent, jointly rotation invariant
+    assert abs(np.corrcoef(S[0], S[1])[0, 1]) < 6 / np.sqrt(n)
+    assert stats.kstest(np.arctan2(S[1], S[0]) / (2 * np.pi) + 0.5, "uniform").pvalue > 1e-3
+
+
+def test_gaussian_sketch_norm_preservation_and_columns():
+    from oracle.sketch import GaussianSketch, gaussian_table
+    rng = np.random.default_rng(0)
+    v = rng.standard_normal(300)
+    r = [np.linalg.norm(GaussianSketch(seed, 50, 300).apply(v)) ** 2 for seed in range(200)]
+    assert abs(np.mean(r) / (v @ v) - 1) < 0.05                   # E||S v||^2 = ||v||^2
+    S = gaussian_table(7, 9, 0, 40)                                 # column windows = the full table
+    np.testing.assert_array_equal(gaussian_table(7, 9, 13, 20), S[:, 13:33])
+    # row r of the draw does not depend on d (pairs (2t, 2t+1) share one counter)
+    np.testing.assert_allclose(gaussian_table(7, 10, 0, 40)[:9] * np.sqrt(10), S * np.sqrt(9), rtol=1e-15)
