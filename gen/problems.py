@@ -26,6 +26,7 @@ _lib = None
 
 MASTER_SEED = 260522281
 SKETCH_SEED_BASE = 0x5F1A5D
+LOWRANK_SEED_BASE = 0x10C0A5
 
 
 def build_lib(force: bool = False) -> str:
@@ -232,6 +233,39 @@ def gen_blur_apply(x: np.ndarray, H: int, W: int, sigma: float, radius: int) -> 
     return Y.reshape(-1)
 
 
+def lowrank_image(N: int, rng: np.random.Generator, n_rect: int = 12) -> np.ndarray:
+    """Synthetic stand-in for the `house` image (config 8): a smooth separable background plus
+    n_rect additive axis-aligned rectangles (rank <= n_rect + 1), row-major."""
+    t = np.linspace(0.0, 1.0, N)
+    img = 0.2 * np.outer(0.5 + 0.5 * np.sin(np.pi * t), 0.5 + 0.5 * np.cos(0.5 * np.pi * t))
+    for _ in range(n_rect):
+        y0, y1 = np.sort(rng.integers(0, N, size=2))
+        x0, x1 = np.sort(rng.integers(0, N, size=2))
+        img[y0:y1 + 1, x0:x1 + 1] += rng.uniform(0.1, 0.5)
+    return img.reshape(-1)
+
+
+def blur_mask_csr(N: int, sigma: float, radius: int, keep: np.ndarray) -> CSR:
+    """Rows `keep` of the zero-boundary separable Gaussian blur of an N x N image (row-major):
+    blurring composed with subsampling."""
+    g = gen_blur_taps(sigma, radius)
+    iy, ix = keep // N, keep % N
+    cols, vals, cnt = [], [], np.zeros(keep.size, dtype=np.int64)
+    offs = [(dy, dx) for dy in range(-radius, radius + 1) for dx in range(-radius, radius + 1)]
+    for dy, dx in offs:
+        yy, xx = iy + dy, ix + dx
+        ok = (yy >= 0) & (yy < N) & (xx >= 0) & (xx < N)
+        cols.append(np.where(ok, yy * N + xx, -1))
+        vals.append(np.full(keep.size, g[dy + radius] * g[dx + radius]))
+    C = np.stack(cols, axis=1)
+    V = np.stack(vals, axis=1)
+    ok = C >= 0
+    cnt = ok.sum(axis=1)
+    rowptr = np.zeros(keep.size + 1, dtype=np.int64)
+    np.cumsum(cnt, out=rowptr[1:])
+    return CSR(keep.size, N * N, rowptr, C[ok].astype(np.int32), np.ascontiguousarray(V[ok]))
+
+
 @dataclass
 class SolverSpec:
     method: str          # "sflsqr" | "sflsmr"
@@ -246,6 +280,7 @@ class SolverSpec:
     tol: float = 0.0
     orth_mode: str = "P"
     sketch: str = "sparse"   # "sparse" (sparse-sign, R5/R6) | "gaussian" (dense N(0, 1/d), R21)
+    lowrank: Optional[dict] = None  # tau_r setup for precond "lowrank" / "lowrank_rnd": N, r, oversample, seed
 
 
 @dataclass
@@ -286,6 +321,14 @@ CONFIGS = {
     # truncation (full window, L1150-1152).
     6: dict(name="c6_decay_rho1.01_noise1", kind="decay", m=1024, n=512, rho=1.01, delta=0.01, sketch="gaussian",
             solvers=[("sflsqr", 50, 50, 101, 1, "identity", 0.0), ("sflsmr", 50, 50, 101, 1, "identity", 0.0)]),
+    # deblurring + inpainting with low-rank truncation (PAPER.md L98-109,
+    # L1601-1636): 512 x 512 image, Gaussian PSF of variance 0.25 (sigma 0.5 px, 5 x 5, zero
+    # boundary), half of the pixels dropped (rows removed), 5 % noise; 50 iterations, rank r = 30,
+    # CountSketch with d = 101.  The `house` image is missing: a synthetic low-rank image (sum of
+    # rectangles on a smooth separable background) stands in (reading R22).
+    8: dict(name="c8_deblur_inpaint512", kind="inpaint", N=512, sigma=0.5, radius=2, keep=0.5, delta=0.05,
+            lowrank=dict(r=30, oversample=10),
+            solvers=[("sflsqr", 50, 3, 101, 1, "lowrank_rnd", 0.0), ("sflsmr", 50, 3, 101, 1, "lowrank_rnd", 0.0)]),
     7: dict(name="c7_decay_rho1.01_noise10", kind="decay", m=1024, n=512, rho=1.01, delta=0.10, sketch="gaussian",
             solvers=[("sflsqr", 50, 50, 101, 1, "identity", 0.0), ("sflsmr", 50, 50, 101, 1, "identity", 0.0)]),
 }
@@ -342,6 +385,16 @@ def make_problem(config_index: int, N: Optional[int] = None, n_angles: Optional[
         x_true = ellipse_phantom(Nimg, rx)[tiled_order(Nimg, tile)]
         geometry = dict(N=Nimg, n_angles=na, nb=nbins, tile=tile)
         Ax = A.matvec(x_true, nthreads)
+    elif kind == "inpaint":
+        Nimg = N or cfg["N"]
+        n = Nimg * Nimg
+        keep = np.sort(rA.choice(n, size=int(round(cfg["keep"] * n)), replace=False))
+        A = blur_mask_csr(Nimg, cfg["sigma"], cfg["radius"], keep)
+        t_mode = "build"
+        m = A.nrows
+        x_true = lowrank_image(Nimg, rx)
+        geometry = dict(N=Nimg, keep=cfg["keep"], sigma=cfg["sigma"])
+        Ax = A.matvec(x_true)
     elif kind == "decay":
         m, n = cfg["m"], cfg["n"]
         U = np.linalg.qr(rA.standard_normal((m, n)))[0]
@@ -359,8 +412,11 @@ def make_problem(config_index: int, N: Optional[int] = None, n_angles: Optional[
     g = re.standard_normal(m)
     e = g * (cfg["delta"] * np.linalg.norm(Ax) / np.linalg.norm(g))
     b = Ax + e
+    lowrank = None
+    if "lowrank" in cfg:
+        lowrank = dict(cfg["lowrank"], N=geometry["N"], seed=LOWRANK_SEED_BASE + config_index)
     solvers = [SolverSpec(method=s[0], maxit=s[1], window=s[2], d=s[3], s_nz=s[4], precond=s[5], eta=s[6],
-                          sketch=cfg.get("sketch", "sparse"))
+                          sketch=cfg.get("sketch", "sparse"), lowrank=lowrank)
                for s in cfg["solvers"]]
     return Problem(name=cfg["name"], config_index=config_index, m=m, n=n, A=A, T=T, t_mode=t_mode,
                    blur=blur, x_true=x_true, b=b, e=e, delta=cfg["delta"], delta_e=float(np.linalg.norm(e)),

@@ -106,6 +106,7 @@ extern "C" {
 #define SFLSQR_PRECOND_IDENTITY 0 /* tau(v) = v                                   */
 #define SFLSQR_PRECOND_IRN 1      /* IRN-l_p right preconditioner, reading R7      */
 #define SFLSQR_PRECOND_NONNEG 2   /* nonnegativity-projecting scaling, reading R8  */
+#define SFLSQR_PRECOND_LOWRANK_RND 3 /* low-rank truncation by randomized SVD, R22 (sflsqr_set_precond_lowrank) */
 
 /* transpose-side operator (sflsqr_set_operator t_mode) */
 #define SFLSQR_T_BUILD 0 /* T = A^T, formed by the library (matched)                */
@@ -259,6 +260,15 @@ int sflsqr_set_sketch_gaussian(sflsqr_t *h, uint64_t seed, int32_t d);
 /* Debug: the Gaussian sketch entries of columns [col0, col0+ncols) as generated by the
  * device (host output, d x ncols row-major); SFLSQR_E_STATE unless a Gaussian sketch is set. */
 int sflsqr_debug_sketch_dense(sflsqr_t *h, int64_t col0, int64_t ncols, double *out);
+
+/* Low-rank truncation tau_r (PAPER.md eq. def:lowr-trc L77-81) computed by the randomized SVD
+ * of the "-RND" solvers (L1619-1623; reading R22): the basis vector p is the H x W image
+ * C = vec^{-1}(p) (row-major), Y = C Omega with Omega (W x l, l = min(r + oversample, H, W, 64))
+ * Gaussian from the generator of reading R21 (key = seed), Q = orth(Y), B = Q^T C,
+ * z = vec(Q U_r U_r^T B) with U_r the top-r eigenvectors of B B^T.  Applied at every k
+ * (no x dependence).  One rank; H * W must equal n (checked at set_rhs: SFLSQR_E_DIM).
+ * Errors: H, W, r out of range -> SFLSQR_E_INVALID. */
+int sflsqr_set_precond_lowrank(sflsqr_t *h, int32_t H, int32_t W, int32_t r, int32_t oversample, uint64_t seed);
 
 /* Flexible preconditioner tau_k (Alg. 1, Alg. 2):
  * kind = SFLSQR_PRECOND_IDENTITY | IRN (p in (0, 2], eps_rel > 0; R7) |

@@ -69,11 +69,18 @@ class OracleResult:
 
 
 def tau_apply(kind, p_k, x_prev, k, p_exp=1.0, eps_rel=1e-3, fixed=None):
-    """z_k = tau_k(p_k) (Alg. 1 L470 / Alg. 2; readings R7, R8)."""
+    """z_k = tau_k(p_k) (Alg. 1 L470 / Alg. 2; readings R7, R8, R22).
+    fixed: the diagonal of kind "diag", or the dict (N, r, omega) of the low-rank kinds."""
     if kind == "identity":
         return p_k.copy()
     if kind == "diag":                     # fixed SPD diagonal (pin P4b)
         return fixed * p_k
+    if kind == "lowrank":                  # eq. def:lowr-trc L77-81, truncated SVD
+        from .lowrank import tau_lowrank_exact
+        return tau_lowrank_exact(p_k, fixed["N"], fixed["r"])
+    if kind == "lowrank_rnd":              # randomized SVD (L1619-1623, reading R22)
+        from .lowrank import tau_lowrank_rnd
+        return tau_lowrank_rnd(p_k, fixed["N"], fixed["r"], fixed["omega"])
     if k == 1:
         return p_k.copy()                  # D_1 = I (x_0 = 0)
     if kind == "irn":
@@ -331,6 +338,10 @@ def solve_problem(prob, spec, op=None, maxit=None, record=True, **over):
     if getattr(spec, "sketch", "sparse") == "gaussian" and method in ("sflsqr", "sflsmr") and "sketch" not in over:
         from .sketch import GaussianSketch                 # reading R21
         over["sketch"] = GaussianSketch(prob.sketch_seed, spec.d, prob.m if method == "sflsqr" else prob.n)
+    if spec.precond in ("lowrank", "lowrank_rnd") and "fixed_diag" not in over:
+        from .lowrank import rnd_omega                     # reading R22
+        lr = spec.lowrank
+        over["fixed_diag"] = dict(N=lr["N"], r=lr["r"], omega=rnd_omega(lr["seed"], lr["N"], lr["r"], lr["oversample"]))
     kw = dict(method=spec.method, maxit=maxit or spec.maxit, window=spec.window, sketch_seed=prob.sketch_seed,
               d=spec.d, s_nz=spec.s_nz, precond=spec.precond, p_exp=spec.p, eps_rel=spec.eps_rel,
               tol=spec.tol, eta=spec.eta, delta_e=prob.delta_e, orth_mode=spec.orth_mode, record=record)

@@ -85,6 +85,8 @@ struct sflsqr {
   // precond
   int pkind = SFLSQR_PRECOND_IDENTITY;
   double p_exp = 1.0, eps_rel = 1e-3;
+  int lr_H = 0, lr_W = 0, lr_r = 0, lr_o = 0;  // SFLSQR_PRECOND_LOWRANK_RND
+  uint64_t lr_seed = 0;
   // solve
   bool bufs = false, rhs_set = false;
   Params P;
@@ -622,6 +624,44 @@ int launch_coop(sflsqr_t* h, void (*kern)(Params), double bytes) {
   return SFLSQR_OK;
 }
 
+// a2 for the low-rank truncation: z_k = tau_r(p_k) by the randomized SVD (reading R22).
+void enqueue_lowrank(sflsqr_t* h) {
+  Params& P = h->P;
+  const double hw8 = 8.0 * P.lr_H * P.lr_W, l = P.lr_l;
+  {
+    Launch L(h, SFLSQR_KC_TAU, hw8 + 8.0 * l * (P.lr_W + P.lr_H));
+    k_lr_range<<<std::min(P.lr_H, 148 * 4), 256, sizeof(double) * P.lr_W, h->stream>>>(P);
+  }
+  {
+    Launch L(h, SFLSQR_KC_TAU, 8.0 * l * P.lr_H * 2);
+    k_lr_qr<<<1, 1024, kLrQrSmem, h->stream>>>(P);
+  }
+  {
+    Launch L(h, SFLSQR_KC_TAU, hw8 + 8.0 * l * (P.lr_W + P.lr_H));
+    const int64_t warps = (int64_t)P.lr_l * ((P.lr_W + 31) / 32) * kLrSplit;
+    k_lr_proj<<<(int)std::max<int64_t>(1, std::min<int64_t>((warps + 7) / 8, 148 * 8)), 256, 0, h->stream>>>(P);
+    k_lr_proj_sum<<<(int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)P.lr_l * P.lr_W + 255) / 256, 148 * 4)),
+                    256, 0, h->stream>>>(P);
+  }
+  {
+    Launch L(h, SFLSQR_KC_TAU, 8.0 * l * P.lr_W);
+    k_lr_gram<<<(int)std::max<int64_t>(1, ((int64_t)P.lr_l * P.lr_l + 7) / 8), 256, 0, h->stream>>>(P);
+  }
+  {
+    Launch L(h, SFLSQR_KC_TAU, 16.0 * l * l);
+    k_lr_eig<<<1, 1024, kLrEigSmem, h->stream>>>(P);
+  }
+  {
+    Launch L(h, SFLSQR_KC_TAU, 16.0 * l * P.lr_H);
+    k_lr_qp<<<(int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)P.lr_H * P.lr_l + 255) / 256, 148 * 8)), 256, 0,
+              h->stream>>>(P);
+  }
+  {
+    Launch L(h, SFLSQR_KC_TAU, hw8 + 8.0 * l * (P.lr_W + P.lr_H));
+    k_lr_recon<<<std::min(P.lr_H, 148 * 4), 256, 0, h->stream>>>(P);
+  }
+}
+
 // One iteration k of Alg. 1 / Alg. 2, or of FLSQR /
 // FLSMR (full window, no sketch; FLSMR runs the z side of step k+1 before its
 // projected problem, which needs column k+1 of T).
@@ -644,6 +684,7 @@ int enqueue_iteration(sflsqr_t* h) {
     Launch L(h, SFLSQR_KC_TAU, n8 * (2 + (P.use_pring ? 1 : 0) + (P.precond ? 1 : 0)));
     k_finish_z<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P);
   }
+  if (P.precond == SFLSQR_PRECOND_LOWRANK_RND) enqueue_lowrank(h);
   // a3: w = A z_k  (z_k = Z[:, k-1]; all-gathered across ranks when sharded)
   if (h->world == 1) {
     enqueue_apply(h, 0, P.st, P.Z, h->n_loc, -1, P.w, SFLSQR_KC_SPMV_A);
@@ -872,7 +913,7 @@ int alloc_solve(sflsqr_t* h) {
   P.s_nz = h->s_nz;
   P.dist = h->world > 1 ? 1 : 0;
   P.want_res = ((h->o.history & SFLSQR_HIST_TRUE_RES) || h->o.eta > 0.0) ? 1 : 0;
-  P.need_x = h->pkind != SFLSQR_PRECOND_IDENTITY ? 1 : 0;
+  P.need_x = (h->pkind == SFLSQR_PRECOND_IRN || h->pkind == SFLSQR_PRECOND_NONNEG) ? 1 : 0;
   P.use_pring = (h->o.orth_mode == SFLSQR_ORTH_P && h->pkind != SFLSQR_PRECOND_IDENTITY) ? 1 : 0;
   P.p_exp = h->p_exp;
   P.eps_rel = h->eps_rel;
@@ -925,6 +966,25 @@ int alloc_solve(sflsqr_t* h) {
       (rc = A(&P.hist_sk, maxit)))
     return rc;
   if (P.use_pring && (rc = A(&P.Pring, n * ell))) return rc;
+  if (h->pkind == SFLSQR_PRECOND_LOWRANK_RND) {
+    if ((int64_t)h->lr_H * h->lr_W != h->n_loc || h->world > 1)
+      return fail(h, SFLSQR_E_DIM, "low-rank tau: H*W = %lld != n (one rank)", (long long)h->lr_H * h->lr_W);
+    P.lr_H = h->lr_H;
+    P.lr_W = h->lr_W;
+    P.lr_r = h->lr_r;
+    P.lr_l = std::min(std::min(h->lr_r + h->lr_o, std::min(h->lr_H, h->lr_W)), kLrMaxL);
+    P.lr_sqrt_l = std::sqrt((double)P.lr_l);
+    const size_t l = P.lr_l;
+    if ((rc = A(&P.lr_G, l * h->lr_W)) || (rc = A(&P.lr_Y, l * h->lr_H)) || (rc = A(&P.lr_Q, l * h->lr_H)) ||
+        (rc = A(&P.lr_B, l * h->lr_W)) || (rc = A(&P.lr_PB, 2 * l * l)) ||
+        (rc = A(&P.lr_part, (size_t)kLrSplit * l * h->lr_W)))
+      return rc;
+    // Omega^T / sqrt(l) by the Gaussian generator of reading R21 (oracle: rnd_omega)
+    const int grid = (int)std::min<int64_t>(((int64_t)(l + 1) / 2 * h->lr_W + 255) / 256 + 1, 148 * 16);
+    k_sketch_gauss_gen<<<grid, 256, 0, h->stream>>>(0, h->lr_W, (int)l, (uint32_t)(h->lr_seed & 0xffffffffu),
+                                                    (uint32_t)(h->lr_seed >> 32), P.lr_sqrt_l, P.lr_G, h->lr_W);
+    CU(h, cudaGetLastError());
+  }
   if (gkb && ((rc = A(&P.gv1, n)) || (rc = A(&P.gv2, n)) || (rc = A(&P.gk, 2 * kGkbState)) ||
               (rc = A(&h->gtmp, std::max(n, m)))))
     return rc;
@@ -1152,6 +1212,9 @@ int sflsqr_create(sflsqr_t** out, const sflsqr_opts* o) {
     h->side = nullptr;  // no overlap; the LS runs on the main stream
   }
   cudaFuncSetAttribute(k_ls<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 4 * kLsThreads * (int)sizeof(double));
+  cudaFuncSetAttribute(k_lr_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLrEigSmem);
+  cudaFuncSetAttribute(k_lr_qr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLrQrSmem);
+  cudaFuncSetAttribute(k_lr_range, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * (int)sizeof(double));
   cudaGetLastError();
   *out = h;
   return SFLSQR_OK;
@@ -1435,6 +1498,23 @@ int sflsqr_debug_sketch_dense(sflsqr_t* h, int64_t col0, int64_t ncols, double* 
   }
   cudaFree(dS);
   return rc;
+}
+
+int sflsqr_set_precond_lowrank(sflsqr_t* h, int32_t H, int32_t W, int32_t r, int32_t oversample, uint64_t seed) {
+  if (!h) return fail(nullptr, SFLSQR_E_INVALID, "NULL handle");
+  if (H < 1 || W < 1 || H > 65536 || W > 8192) return fail(h, SFLSQR_E_INVALID, "need 1 <= H <= 65536, 1 <= W <= 8192");
+  if (r < 1 || r > std::min(H, W) || r > kLrMaxL || oversample < 0)
+    return fail(h, SFLSQR_E_INVALID, "need 1 <= r <= min(H, W, %d), oversample >= 0", kLrMaxL);
+  free_solve(h);
+  h->pkind = SFLSQR_PRECOND_LOWRANK_RND;
+  h->lr_H = H;
+  h->lr_W = W;
+  h->lr_r = r;
+  h->lr_o = oversample;
+  h->lr_seed = seed;
+  h->p_exp = 1.0;
+  h->eps_rel = 1e-3;
+  return SFLSQR_OK;
 }
 
 int sflsqr_set_precond(sflsqr_t* h, int32_t kind, double p, double eps_rel) {

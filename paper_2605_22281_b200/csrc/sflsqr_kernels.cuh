@@ -76,6 +76,12 @@ struct Params {
   int slot_gka, slot_gkb;  // ||v'||^2 (alpha^2) and ||u'||^2 (beta^2) partials
   // sketch
   double* sk_dense;        // Gaussian sketch (reading R21): d x dim_loc, row-major (else NULL)
+  // low-rank truncation tau_r by randomized SVD (precond 3, reading R22): the basis vector is an
+  // lr_H x lr_W image; l = lr_l range-finder columns; G = Omega^T / sqrt(l) (l x W, row-major)
+  int lr_H, lr_W, lr_r, lr_l;
+  double lr_sqrt_l;
+  double *lr_G, *lr_Y, *lr_Q, *lr_B, *lr_PB;  // Y, Q: H x l column-major; B: l x W row-major; PB: 2 l x l
+  double* lr_part;                           // kLrSplit x l x W partials of B
   int64_t* sk_rp;          // S stored transposed: d+1 row pointers
   uint32_t* sk_ent;         // coordinate | sign << 31, s * dim entries
   double *rhs, *Mcols, *STW;
@@ -1186,8 +1192,18 @@ __device__ __forceinline__ bool finish_z_body(const Params& P, DevState* st, int
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) P.Tm[(int64_t)(k - 1) + (int64_t)(k - 1) * P.ldtm] = t;
   // tau weights need x_{k-1} (computed by k_xupdate at the end of iteration k-1)
-  int mode = P.precond;  // 0 identity, 1 IRN, 2 NONNEG
+  int mode = P.precond;  // 0 identity, 1 IRN, 2 NONNEG, 3 low-rank (tau applied by the k_lr_* kernels)
   double eps = 0.0;
+  if (mode == 3) {
+    // p_k stays in P.z (and the P ring); k_lr_range .. k_lr_recon form z_k = tau_r(p_k) into Z[:, k-1]
+    double* pr = P.use_pring ? P.Pring + (int64_t)((k - 1) % P.ell) * P.n : nullptr;
+    for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < P.n; i += (int64_t)gridDim.x * NT) {
+      const double p = P.z[i] / t;
+      P.z[i] = p;
+      if (pr) pr[i] = p;
+    }
+    return true;
+  }
   if (mode != 0) {
     if (k == 1) {
       mode = 0;  // D_1 = I (x_0 = 0)
@@ -1229,6 +1245,293 @@ __global__ void __launch_bounds__(kVecThreads) k_finish_z(Params P) {
   const double t = sqrt(z_norm2<kVecThreads>(P, J, sh));
   const double zin = sqrt(P.orth_alg != ORTH_MGS ? P.scal[P.slot_zf] : get_sum<kVecThreads>(P, P.slot_zin, sh, kVecBlocks));
   finish_z_body<kVecThreads>(P, st, k, t, zin);
+}
+
+// ------------------------------------------------------------------ a2 for tau_r: randomized SVD
+// z_k = tau_r(p_k) = vec(Q U_r U_r^T B), C = vec^{-1}(p_k) (H x W, row-major), Y = C Omega,
+// Q = orth(Y) (CGS2), B = Q^T C, U_r = top-r eigenvectors of B B^T (parallel cyclic Jacobi)
+// -- PAPER.md eq. def:lowr-trc L77-81 with the randomized SVD of L1619-1623 (reading R22).
+// Five small kernels: the work is ~4 H W l flops, latency bound at these sizes.
+constexpr int kLrMaxL = 64;
+
+// Y[:, c] = C Omega[:, c]: one CTA per image row, warps over c, lanes over j.
+__global__ void __launch_bounds__(256) k_lr_range(Params P) {
+  extern __shared__ double crow[];
+  if (P.st->done) return;
+  const int H = P.lr_H, W = P.lr_W, l = P.lr_l;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int i = blockIdx.x; i < H; i += gridDim.x) {
+    __syncthreads();
+    for (int j = threadIdx.x; j < W; j += 256) crow[j] = P.z[(int64_t)i * W + j];
+    __syncthreads();
+    for (int c = wid; c < l; c += 8) {
+      const double* g = P.lr_G + (int64_t)c * W;
+      double acc = 0.0;
+      for (int j = lane; j < W; j += 32) acc = fma(crow[j], g[j] * P.lr_sqrt_l, acc);
+      acc = warp_sum(acc);
+      if (lane == 0) P.lr_Y[(int64_t)c * H + i] = acc;
+    }
+  }
+}
+
+// Q = orth(Y) by classical Gram-Schmidt applied twice, one column at a time (one CTA; the
+// H x l panel is staged in shared memory when it fits, kLrQrSmem bytes).
+constexpr int kLrQrSmemDoubles = 26 * 1024;
+constexpr size_t kLrQrSmem = sizeof(double) * kLrQrSmemDoubles;
+__global__ void __launch_bounds__(1024) k_lr_qr(Params P) {
+  extern __shared__ double qs[];
+  __shared__ double d[kLrMaxL];
+  __shared__ double sh[33];
+  if (P.st->done) return;
+  const int H = P.lr_H, l = P.lr_l;
+  const bool staged = (int64_t)H * l <= kLrQrSmemDoubles;
+  double* Qb = staged ? qs : P.lr_Q;  // column-major H x l
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int c = 0; c < l; ++c) {
+    double* q = Qb + (int64_t)c * H;
+    for (int i = threadIdx.x; i < H; i += 1024) q[i] = P.lr_Y[(int64_t)c * H + i];
+    __syncthreads();
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int j = wid; j < c; j += 32) {
+        const double* qj = Qb + (int64_t)j * H;
+        double acc = 0.0;
+        for (int i = lane; i < H; i += 32) acc = fma(qj[i], q[i], acc);
+        acc = warp_sum(acc);
+        if (lane == 0) d[j] = acc;
+      }
+      __syncthreads();
+      for (int i = threadIdx.x; i < H; i += 1024) {
+        double v0 = q[i], v1 = 0.0, v2 = 0.0, v3 = 0.0;  // four chains for latency hiding
+        int j = 0;
+        for (; j + 4 <= c; j += 4) {
+          v0 = fma(-d[j], Qb[(int64_t)j * H + i], v0);
+          v1 = fma(-d[j + 1], Qb[(int64_t)(j + 1) * H + i], v1);
+          v2 = fma(-d[j + 2], Qb[(int64_t)(j + 2) * H + i], v2);
+          v3 = fma(-d[j + 3], Qb[(int64_t)(j + 3) * H + i], v3);
+        }
+        for (; j < c; ++j) v0 = fma(-d[j], Qb[(int64_t)j * H + i], v0);
+        q[i] = (v0 + v1) + (v2 + v3);
+      }
+      __syncthreads();
+    }
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < H; i += 1024) acc = fma(q[i], q[i], acc);
+    const double nrm = sqrt(block_sum<1024>(acc, sh));
+    const double inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
+    for (int i = threadIdx.x; i < H; i += 1024) q[i] *= inv;
+    __syncthreads();
+  }
+  if (staged)
+    for (int64_t e = threadIdx.x; e < (int64_t)H * l; e += 1024) P.lr_Q[e] = qs[e];
+}
+
+// B = Q^T C (l x W), split over kLrSplit chunks of image rows for parallelism: one warp per
+// (row c of B, 32 image columns, row chunk) writes a partial into lr_part; k_lr_proj_sum adds
+// the kLrSplit partials in chunk order (deterministic).
+constexpr int kLrSplit = 16;
+__global__ void __launch_bounds__(256) k_lr_proj(Params P) {
+  if (P.st->done) return;
+  const int H = P.lr_H, W = P.lr_W, l = P.lr_l;
+  const int lane = threadIdx.x & 31;
+  const int ntile = (W + 31) / 32;
+  const int chunk = (H + kLrSplit - 1) / kLrSplit;
+  const int64_t nwarp = (int64_t)l * ntile * kLrSplit;
+  for (int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wg < nwarp;
+       wg += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int part = (int)(wg % kLrSplit);
+    const int64_t rest = wg / kLrSplit;
+    const int c = (int)(rest / ntile), j = (int)(rest % ntile) * 32 + lane;
+    const int i0 = part * chunk, i1 = min(H, i0 + chunk);
+    const double* q = P.lr_Q + (int64_t)c * H;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    if (j < W) {
+      int i = i0;
+      for (; i + 4 <= i1; i += 4) {
+        a0 = fma(__ldg(q + i), __ldg(P.z + (int64_t)i * W + j), a0);
+        a1 = fma(__ldg(q + i + 1), __ldg(P.z + (int64_t)(i + 1) * W + j), a1);
+        a2 = fma(__ldg(q + i + 2), __ldg(P.z + (int64_t)(i + 2) * W + j), a2);
+        a3 = fma(__ldg(q + i + 3), __ldg(P.z + (int64_t)(i + 3) * W + j), a3);
+      }
+      for (; i < i1; ++i) a0 = fma(__ldg(q + i), __ldg(P.z + (int64_t)i * W + j), a0);
+      P.lr_part[((int64_t)part * l + c) * W + j] = (a0 + a1) + (a2 + a3);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_lr_proj_sum(Params P) {
+  if (P.st->done) return;
+  const int64_t lw = (int64_t)P.lr_l * P.lr_W;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < lw; e += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int part = 0; part < kLrSplit; ++part) acc += P.lr_part[part * lw + e];
+    P.lr_B[e] = acc;
+  }
+}
+
+// Mg = B B^T (l x l, into lr_Y's tail-free scratch lr_PB[0 .. l*l)): one warp per entry a <= b.
+__global__ void __launch_bounds__(256) k_lr_gram(Params P) {
+  if (P.st->done) return;
+  const int W = P.lr_W, l = P.lr_l;
+  const int lane = threadIdx.x & 31;
+  for (int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wg < (int64_t)l * l;
+       wg += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int a = (int)(wg / l), b = (int)(wg % l);
+    if (b < a) continue;
+    const double* ba = P.lr_B + (int64_t)a * W;
+    const double* bb = P.lr_B + (int64_t)b * W;
+    double acc0 = 0.0, acc1 = 0.0;
+    int j = lane;
+    for (; j + 32 < W; j += 64) {
+      acc0 = fma(ba[j], bb[j], acc0);
+      acc1 = fma(ba[j + 32], bb[j + 32], acc1);
+    }
+    if (j < W) acc0 = fma(ba[j], bb[j], acc0);
+    const double v = warp_sum(acc0 + acc1);
+    if (lane == 0) {
+      P.lr_PB[(int64_t)a * l + b] = v;
+      P.lr_PB[(int64_t)b * l + a] = v;
+    }
+  }
+}
+
+// Parallel cyclic Jacobi on Mg (round-robin pairs, one warp per pair), then the top-r
+// projector Pr = U_r U_r^T (l x l) into lr_PB[l*l .. 2*l*l).  One CTA of 1024 threads.
+constexpr size_t kLrEigSmem = 2 * sizeof(double) * kLrMaxL * (kLrMaxL + 1);
+__global__ void __launch_bounds__(1024) k_lr_eig(Params P) {
+  extern __shared__ double lr_sm[];  // kLrEigSmem bytes: M then V, each kLrMaxL x (kLrMaxL + 1)
+  double(*M)[kLrMaxL + 1] = reinterpret_cast<double(*)[kLrMaxL + 1]>(lr_sm);
+  double(*V)[kLrMaxL + 1] = reinterpret_cast<double(*)[kLrMaxL + 1]>(lr_sm + kLrMaxL * (kLrMaxL + 1));
+  __shared__ double cs[kLrMaxL / 2][2];
+  __shared__ int pq[kLrMaxL / 2][2];
+  __shared__ double sh[33];
+  __shared__ int top[kLrMaxL];
+  if (P.st->done) return;
+  const int l = P.lr_l, r = P.lr_r;
+  const int L = (l + 1) & ~1;  // even number of slots for the tournament (slot l is a dummy when l is odd)
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int e = tid; e < l * l; e += 1024) M[e / l][e % l] = P.lr_PB[e];
+  for (int e = tid; e < kLrMaxL * kLrMaxL; e += 1024) V[e / kLrMaxL][e % kLrMaxL] = (e / kLrMaxL == e % kLrMaxL) ? 1.0 : 0.0;
+  __syncthreads();
+  double fro = 0.0;
+  for (int e = tid; e < l * l; e += 1024) fro = fma(M[e / l][e % l], M[e / l][e % l], fro);
+  fro = block_sum<1024>(fro, sh);
+  // sweeps until the off-diagonal mass is below (1e-15)^2 ||M||_F^2 or stops shrinking
+  // (Jacobi converges quadratically; once at the rounding floor further sweeps only
+  // shuffle rounding), at most 20
+  double prev = INFINITY;
+  for (int sweep = 0; sweep < 20; ++sweep) {
+    double off = 0.0;
+    for (int e = tid; e < l * l; e += 1024)
+      if (e / l != e % l) off = fma(M[e / l][e % l], M[e / l][e % l], off);
+    off = block_sum<1024>(off, sh);
+    // converged, or at the rounding floor (off-diagonal mass tiny and no longer shrinking)
+    if (!(off > 1e-30 * fro) || (off <= 1e-24 * fro && off > 0.25 * prev)) break;
+    prev = off;
+    for (int step = 0; step < L - 1; ++step) {
+      // round-robin tournament: slot 0 fixed, slots 1..L-1 rotate; warp w owns pair w and
+      // computes its rotation (lane-redundantly) right before applying it to the columns
+      // columns: M <- M J, V <- V J
+      for (int w = wid; w < L / 2; w += 32) {
+        auto slot = [&](int s2) { return s2 == 0 ? 0 : 1 + (s2 - 1 + step) % (L - 1); };
+        int p = slot(w), q = slot(L - 1 - w);
+        if (p > q) {
+          const int t = p;
+          p = q;
+          q = t;
+        }
+        double c = 1.0, s = 0.0;
+        if (q < l && M[p][q] != 0.0) {
+          // t = sgn(theta) / (|theta| + sqrt(theta^2 + 1)), theta = (M_qq - M_pp) / (2 M_pq), written as
+          // t = 2 M_pq sgn(dd) / (|dd| + sqrt(dd^2 + 4 M_pq^2)), dd = M_qq - M_pp (one div, one sqrt)
+          const double apq = M[p][q], dd = M[q][q] - M[p][p];
+          const double sg = ((dd >= 0.0) == (apq >= 0.0)) ? 1.0 : -1.0;
+          const double t = sg * 2.0 * fabs(apq) / (fabs(dd) + sqrt(fma(dd, dd, 4.0 * apq * apq)));
+          c = rsqrt(fma(t, t, 1.0));
+          s = t * c;
+        }
+        __syncwarp();
+        if (lane == 0) {
+          pq[w][0] = p;
+          pq[w][1] = q;
+          cs[w][0] = c;
+          cs[w][1] = s;
+        }
+        if (q >= l) continue;
+        for (int a = lane; a < l; a += 32) {
+          const double mp = M[a][p], mq = M[a][q], vp = V[a][p], vq = V[a][q];
+          M[a][p] = c * mp - s * mq;
+          M[a][q] = s * mp + c * mq;
+          V[a][p] = c * vp - s * vq;
+          V[a][q] = s * vp + c * vq;
+        }
+      }
+      __syncthreads();
+      // rows: M <- J^T M
+      for (int w = wid; w < L / 2; w += 32) {
+        const int p = pq[w][0], q = pq[w][1];
+        if (q >= l) continue;
+        const double c = cs[w][0], s = cs[w][1];
+        for (int b = lane; b < l; b += 32) {
+          const double mp = M[p][b], mq = M[q][b];
+          M[p][b] = c * mp - s * mq;
+          M[q][b] = s * mp + c * mq;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // the r largest eigenvalues (ties by index)
+  if (tid < l) {
+    const double lam = M[tid][tid];
+    int rank = 0;
+    for (int b = 0; b < l; ++b) {
+      const double lb = M[b][b];
+      rank += (lb > lam || (lb == lam && b < tid)) ? 1 : 0;
+    }
+    top[tid] = rank < r ? 1 : 0;
+  }
+  __syncthreads();
+  for (int e = tid; e < l * l; e += 1024) {
+    const int x = e / l, y = e % l;
+    double acc = 0.0;
+    for (int a = 0; a < l; ++a)
+      if (top[a]) acc = fma(V[x][a], V[y][a], acc);
+    P.lr_PB[(int64_t)l * l + e] = acc;
+  }
+}
+
+// QP = Q Pr (H x l, column-major, into lr_Y): thread per entry.
+__global__ void __launch_bounds__(256) k_lr_qp(Params P) {
+  if (P.st->done) return;
+  const int H = P.lr_H, l = P.lr_l;
+  const double* Pr = P.lr_PB + (int64_t)l * l;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)H * l; e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e / H);
+    const int64_t i = e - (int64_t)c * H;
+    double acc = 0.0;
+    for (int y = 0; y < l; ++y) acc = fma(P.lr_Q[(int64_t)y * H + i], Pr[(int64_t)y * l + c], acc);
+    P.lr_Y[e] = acc;
+  }
+}
+
+// z_k = vec(QP B) into Z[:, k-1] (and the all-gather send buffer): one CTA per image row.
+__global__ void __launch_bounds__(256) k_lr_recon(Params P) {
+  __shared__ double qi[kLrMaxL];
+  DevState* st = P.st;
+  if (st->done) return;
+  const int H = P.lr_H, W = P.lr_W, l = P.lr_l;
+  double* zk = P.Z + (int64_t)(st->k - 1) * P.n;
+  for (int i = blockIdx.x; i < H; i += gridDim.x) {
+    __syncthreads();
+    if (threadIdx.x < l) qi[threadIdx.x] = P.lr_Y[(int64_t)threadIdx.x * H + i];
+    __syncthreads();
+    for (int j = threadIdx.x; j < W; j += 256) {
+      double acc = 0.0;
+      for (int c = 0; c < l; ++c) acc = fma(qi[c], P.lr_B[(int64_t)c * W + j], acc);
+      zk[(int64_t)i * W + j] = acc;
+      if (P.zsend) P.zsend[(int64_t)i * W + j] = acc;
+    }
+  }
 }
 
 // ------------------------------------------------------------------ a5 end: normalise w

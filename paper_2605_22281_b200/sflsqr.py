@@ -27,7 +27,7 @@ METHODS = {"sflsqr": METHOD_SFLSQR, "sflsmr": METHOD_SFLSMR, "flsqr": METHOD_FLS
 ORTH_P, ORTH_Z = 0, 1
 ORTHK_AUTO, ORTHK_MGS = 0, 1
 RUNNING, MAXIT, TOL, DISCREPANCY, BREAKDOWN = 0, 1, 2, 3, 4
-PRECOND_IDENTITY, PRECOND_IRN, PRECOND_NONNEG = 0, 1, 2
+PRECOND_IDENTITY, PRECOND_IRN, PRECOND_NONNEG, PRECOND_LOWRANK_RND = 0, 1, 2, 3
 T_BUILD, T_GIVEN = 0, 1
 MEM_HOST, MEM_DEVICE, MEM_BORROW = 0, 1, 2
 HIST_TRUE_RES = 1
@@ -39,6 +39,7 @@ EXPORTED = [
     "sflsqr_set_precond", "sflsqr_set_rhs", "sflsqr_iterate", "sflsqr_get_x", "sflsqr_get_residual_norms",
     "sflsqr_get_info", "sflsqr_debug_sketch_table", "sflsqr_debug_apply", "sflsqr_debug_basis", "sflsqr_debug_state",
     "sflsqr_debug_set_tuning", "sflsqr_set_sketch_gaussian", "sflsqr_debug_sketch_dense",
+    "sflsqr_set_precond_lowrank",
     "sflsqr_set_profiling", "sflsqr_reset_profile", "sflsqr_get_profile", "sflsqr_last_error", "sflsqr_destroy",
 ]
 
@@ -91,6 +92,7 @@ def load_library(path: str = LIB_PATH):
         "sflsqr_set_operator_blur": ([vp, i32, i32, f64, i32], ctypes.c_int),
         "sflsqr_set_sketch": ([vp, ctypes.c_uint64, i32, i32], ctypes.c_int),
         "sflsqr_set_sketch_gaussian": ([vp, ctypes.c_uint64, i32], ctypes.c_int),
+        "sflsqr_set_precond_lowrank": ([vp, i32, i32, i32, i32, ctypes.c_uint64], ctypes.c_int),
         "sflsqr_debug_sketch_dense": ([vp, i64, i64, vp], ctypes.c_int),
         "sflsqr_set_precond": ([vp, i32, f64, f64], ctypes.c_int),
         "sflsqr_set_rhs": ([vp, vp, i64, i32], ctypes.c_int),
@@ -254,6 +256,9 @@ class SFLSQR:
         self._check(self.lib.sflsqr_debug_sketch_dense(self.h, int(col0), int(ncols), out.ctypes.data))
         return out
 
+    def set_precond_lowrank(self, H, W, r, oversample=10, seed=0):
+        self._check(self.lib.sflsqr_set_precond_lowrank(self.h, int(H), int(W), int(r), int(oversample), int(seed)))
+
     def set_precond(self, kind="identity", p=1.0, eps_rel=1e-3):
         k = {"identity": PRECOND_IDENTITY, "irn": PRECOND_IRN, "nonneg": PRECOND_NONNEG}.get(kind, kind)
         self._check(self.lib.sflsqr_set_precond(self.h, int(k), float(p), float(eps_rel)))
@@ -395,6 +400,9 @@ def solver_for_problem(prob, spec, maxit=None, history=HIST_TRUE_RES, use_graph=
         s.set_sketch(prob.sketch_seed, spec.d, spec.s_nz)
     if (method or spec.method) in ("lsqr", "lsmr"):
         s.set_precond("identity")          # GKB methods take no flexible preconditioner
+    elif spec.precond == "lowrank_rnd":
+        lr = spec.lowrank
+        s.set_precond_lowrank(lr["N"], lr["N"], lr["r"], lr["oversample"], lr["seed"])
     else:
         s.set_precond(spec.precond, spec.p, spec.eps_rel)
     return s
