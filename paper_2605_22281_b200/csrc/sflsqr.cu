@@ -444,7 +444,8 @@ int enqueue_sketch(sflsqr_t* h, const DevState* st, const double* v) {
   } else {
     Launch L(h, SFLSQR_KC_SKETCH, 12.0 * h->s_nz * dim_loc + 8.0 * (h->d + 1) + 8.0 * h->d);
     const int grid = std::min(h->d, 148 * 8);
-    k_sketch_apply<<<grid, 256, 0, h->stream>>>(st, h->P.sk_rp, h->P.sk_ent, v, h->d, h->P.sk_scale, h->P.skbuf);
+    k_sketch_apply<<<grid, kSkApplyThreads, 0, h->stream>>>(st, h->P.sk_rp, h->P.sk_ent, v, h->d, h->P.sk_scale,
+                                                            h->P.skbuf);
   }
   return coll_allreduce(h, h->P.skbuf, h->d, false);
 }

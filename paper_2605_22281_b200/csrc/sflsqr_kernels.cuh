@@ -744,20 +744,29 @@ __global__ void __launch_bounds__(256) k_blur_cols(const DevState* st, int H, in
 // entries are the coordinate index with the sign in bit 31.  Applying it is then a
 // deterministic row-parallel gather-sum: out[r] = mult * scale * sum_i sign * v_i
 // over the coordinates i hashed to row r, in increasing i.  One CTA per sketch row.
-__global__ void __launch_bounds__(256) k_sketch_apply(const DevState* st, const int64_t* __restrict__ srp,
+constexpr int kSkApplyThreads = 512;
+__global__ void __launch_bounds__(kSkApplyThreads) k_sketch_apply(const DevState* st, const int64_t* __restrict__ srp,
                                                       const uint32_t* __restrict__ sent,
                                                       const double* __restrict__ v, int d, double scale,
                                                       double* __restrict__ out) {
   __shared__ double sh[33];
   if (st && st->done) return;
   for (int r = blockIdx.x; r < d; r += gridDim.x) {
-    double acc = 0.0;
-    for (int64_t q = srp[r] + threadIdx.x; q < srp[r + 1]; q += 256) {
-      const uint32_t e = __ldg(sent + q);
-      const double vi = __ldg(v + (e & 0x7fffffffu));
-      acc += (e >> 31) ? -vi : vi;
+    double acc0 = 0.0, acc1 = 0.0;  // two chains: twice the gathers in flight
+    int64_t q = srp[r] + threadIdx.x;
+    const int64_t qe = srp[r + 1];
+    for (; q + kSkApplyThreads < qe; q += 2 * kSkApplyThreads) {
+      const uint32_t e0 = __ldg(sent + q), e1 = __ldg(sent + q + kSkApplyThreads);
+      const double v0 = __ldg(v + (e0 & 0x7fffffffu)), v1 = __ldg(v + (e1 & 0x7fffffffu));
+      acc0 += (e0 >> 31) ? -v0 : v0;
+      acc1 += (e1 >> 31) ? -v1 : v1;
     }
-    acc = block_sum<256>(acc, sh) * scale;
+    if (q < qe) {
+      const uint32_t e0 = __ldg(sent + q);
+      const double v0 = __ldg(v + (e0 & 0x7fffffffu));
+      acc0 += (e0 >> 31) ? -v0 : v0;
+    }
+    const double acc = block_sum<kSkApplyThreads>(acc0 + acc1, sh) * scale;
     if (threadIdx.x == 0) out[r] = acc;
   }
 }
@@ -1003,7 +1012,7 @@ __device__ __forceinline__ void orth_axpy_block(const Params& P, int side, int J
   if (threadIdx.x == 0) P.part[(size_t)so * kVecBlocks + blockIdx.x] = acc;
 }
 
-__global__ void __launch_bounds__(kVecThreads) k_orth_dots(Params P, int side, int koff) {
+__global__ void __launch_bounds__(kVecThreads, 4) k_orth_dots(Params P, int side, int koff) {
   const DevState* st = P.st;
   if (st->done) return;
   const int k = st->k + koff;
