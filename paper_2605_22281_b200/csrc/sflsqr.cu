@@ -58,7 +58,7 @@ struct sflsqr {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   cudaStream_t side = nullptr;  // second stream: the projected LS overlaps the T product (fork/join)
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_w = nullptr;
   std::string err;
   // distribution
   int rank = 0, world = 1;
@@ -103,6 +103,8 @@ struct sflsqr {
   int band_shift = 16;   // reserved
   bool prof_on = false;
   Prof prof;
+  bool res_overlap = true;  // W-path residual on the side stream (SFLSQR_RES_OVERLAP=0/1 forces; A/B timing)
+  bool res_overlap_forced = false;
   int coop_grid = 0;     // blocks of the cooperative phase kernels (0: not available)
   bool coop_attr = true; // launch with cudaLaunchAttributeCooperative (cleared if unsupported)
 };
@@ -714,6 +716,22 @@ int enqueue_iteration(sflsqr_t* h) {
     k_finish_w<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P);
   }
   if (fork_ls && P.method == SFLSQR_METHOD_FLSQR && (rc = enqueue_ls(h, true))) return rc;
+  // a9 (W-path residual) on the side stream too, after the LS and a5, overlapped with a6: it
+  // streams W while the T product leaves HBM bandwidth unused.  The stop test then runs on the
+  // main stream after the join (the T product reads st->k, which the stop test advances).
+  // Measured: +3 % on config 3; on config 4 (2.5e9 nnz) the board is power capped
+  // and the concurrent stream lowers the SM clock (-0.5 %), so large operators keep it serial.
+  const bool res_side = fork_ls && P.want_res && h->world == 1 && h->res_overlap &&
+                        (h->res_overlap_forced || h->nnz_a + h->nnz_t < (int64_t)1000000000);
+  if (res_side) {
+    CU(h, cudaEventRecord(h->ev_w, h->stream));
+    CU(h, cudaStreamWaitEvent(h->side, h->ev_w, 0));
+    {
+      Launch L(h, SFLSQR_KC_RES, m8 * (k + 1));
+      k_res_partial<<<kVecBlocks, kVecThreads, 0, h->side>>>(P, 0);
+    }
+    CU(h, cudaEventRecord(h->ev_join, h->side));
+  }
   // a6: z = T w_{k+1}  (w_{k+1} = W[:, k])
   if ((rc = enqueue_transpose_product(h, false))) return rc;
   // a4 (sFLSMR): S z -> S_TW[:, k+1]
@@ -736,8 +754,8 @@ int enqueue_iteration(sflsqr_t* h) {
     if ((rc = coll_allreduce(h, P.scal + P.slot_xmax, 1, true))) return rc;
   }
   // a9: true residual (W path) and stop tests (fused into the residual kernel on one rank)
-  const bool fuse_stop = P.want_res && h->world == 1 && !h->prof_on;
-  if (P.want_res) {
+  const bool fuse_stop = P.want_res && h->world == 1 && !h->prof_on && !res_side;
+  if (P.want_res && !res_side) {
     {
       Launch L(h, SFLSQR_KC_RES, m8 * (k + 1));
       k_res_partial<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P, fuse_stop ? 1 : 0);
@@ -1193,6 +1211,10 @@ int sflsqr_create(sflsqr_t** out, const sflsqr_opts* o) {
     }
   }
   if (const char* ev = std::getenv("SFLSQR_SPMV_MODE")) h->spmv_mode = std::atoi(ev);
+  if (const char* ev = std::getenv("SFLSQR_RES_OVERLAP")) {
+    h->res_overlap = ev[0] != '0';
+    h->res_overlap_forced = h->res_overlap;
+  }
   {
     // co-resident blocks of the cooperative phase kernels (both kernels, 512 threads)
     int nsm = 0, oz = 0, ow = 0;
@@ -1208,7 +1230,8 @@ int sflsqr_create(sflsqr_t** out, const sflsqr_opts* o) {
   }
   if (cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_w, cudaEventDisableTiming) != cudaSuccess) {
     cudaGetLastError();
     h->side = nullptr;  // no overlap; the LS runs on the main stream
   }
@@ -1875,6 +1898,7 @@ void sflsqr_destroy(sflsqr_t* h) {
   if (h->side) cudaStreamDestroy(h->side);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
+  if (h->ev_w) cudaEventDestroy(h->ev_w);
   if (h->own_stream) cudaStreamDestroy(h->stream);
   delete h;
 }
