@@ -152,15 +152,15 @@ def run_cpu_baseline(prob, spec, budget_s=25.0):
         t0 = time.perf_counter()
         solve_problem(prob, spec, op=op, maxit=1, record=False)
         t1 = time.perf_counter() - t0
-        k = 2 if t1 * 2 < budget_s else 1
+        k = int(max(2, min(spec.maxit, budget_s // max(t1, 1e-6)))) if t1 * 2 < budget_s else 1
         t0 = time.perf_counter()
         solve_problem(prob, spec, op=op, maxit=k, record=False)
         tk = time.perf_counter() - t0
     per_it = max((tk - t1) / max(k - 1, 1), 1e-9) if k > 1 else t1
     return {"value": 1.0 / per_it, "unit": UNIT, "cores": 1, "kind": "oracle",
             "sample": (f"oracle (NumPy + plain C CSR, 1 thread) on the full {prob.name} problem: solve with "
-                       f"maxit={k} minus maxit=1 (init + per-iteration cost separated); "
-                       f"{per_it:.2f} s/iteration, init+1st iteration {t1:.2f} s, operator setup {t_op:.2f} s")}
+                       f"maxit={k} minus maxit=1, per iteration (init + per-iteration cost separated); "
+                       f"{per_it:.3g} s/iteration, init+1st iteration {t1:.3g} s, operator setup {t_op:.3g} s")}
 
 
 def bench_reference(args, prob, spec, world, rank):
