@@ -1,0 +1,38 @@
+"""bench.py contract checks that need no GPU: the reference arm (the oracle, this tier's
+reference) prints one JSON line with the contract keys; the method switch maps every method
+name to a solver spec on the config's operator."""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_reference_arm_json_line():
+    env = dict(os.environ, SFLSQR_REF_BUDGET_S="5")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "1",
+                          "--steps", "3", "--warmup", "3"], capture_output=True, text=True, env=env, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for key in ("metric", "value", "unit", "impl", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
+        assert key in d, key
+    assert d["impl"] == "reference" and d["value"] > 0 and d["cpu_baseline"]["kind"] == "oracle"
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+
+
+def test_method_switch():
+    sys.path.insert(0, ROOT)
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(b)
+    from gen import make_problem
+    p = make_problem(1)
+    for m in ("sflsqr", "sflsmr", "flsqr", "flsmr", "lsqr", "lsmr"):
+        s = b._spec_for(p, m)
+        assert s.method == m and s.maxit == p.solvers[0].maxit
+    assert b._spec_for(p, None) is p.solvers[0]
