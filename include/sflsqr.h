@@ -1,6 +1,6 @@
 /*
  * sflsqr.h — C ABI of libsflsqr.so, the B200 (sm_100a) sketched flexible
- * Golub–Kahan step of sFLSQR / sFLSMR.
+ * Golub–Kahan step of sFLSQR / sFLSMR (and of its relatives, below).
  *
  * Method (PAPER.md = arXiv 2605.22281):
  *   - Algorithm 1 "sFLSQR", L450–508; eq. (sFLSQR):
@@ -13,7 +13,11 @@
  *   - stopping: tol test (Alg. 1 L498 / Alg. 2) and the discrepancy
  *     principle eq. (discrP): stop at the first k with
  *     ||b - A x_k|| <= eta * delta_e.
- * Readings of paper-silent points (R1–R16) are listed in DESIGN.md §2 and are
+ *   - also on the same step and kernels: the unsketched parents
+ *     FLSQR / FLSMR (L321–373, full orthogonalisation), textbook LSQR / LSMR on the
+ *     Golub–Kahan bidiagonalisation (L277–319), the dense Gaussian sketch (L550–552)
+ *     and the low-rank truncation tau_r by randomized SVD (L77–81, L1619–1623).
+ * Readings of paper-silent points (R1–R23) are listed in DESIGN.md §2 and are
  * referenced below by number.
  *
  * Conventions
@@ -33,10 +37,11 @@
  *     current stream) or, when NULL, on a stream the library creates.
  *   - There is no CPU fallback: without a usable CUDA device every compute call
  *     fails with SFLSQR_E_CUDA.
- *   - Required call order: create, set_operator*(), set_sketch(),
- *     [set_precond()], set_rhs(), iterate()..., get_x()/get_residual_norms(),
- *     destroy.  set_rhs() (re)starts a solve; out-of-order calls return
- *     SFLSQR_E_STATE.
+ *   - Required call order: create, set_operator*(), set_sketch() or
+ *     set_sketch_gaussian() (sketched methods only), [set_precond() /
+ *     set_precond_lowrank()], set_rhs(), iterate()..., get_x() /
+ *     get_residual_norms(), destroy.  set_rhs() (re)starts a solve; out-of-order
+ *     calls return SFLSQR_E_STATE.
  */
 #ifndef SFLSQR_H_
 #define SFLSQR_H_
