@@ -25,7 +25,8 @@
  *     message of the last failure is available from sflsqr_last_error(h).
  *   - Floating point is IEEE fp64 throughout; indices are int32 columns and
  *     int64 row pointers (CSR, 0-based, rowptr[0] = 0, rowptr[nrows] = nnz).
- *   - Vectors are dense, contiguous, row-major image order (R16).
+ *   - Vectors are dense and contiguous, in the operator's column / row order (the CT
+ *     generators use a 4x4-tiled image order, R16; the low-rank tau_r expects row-major images).
  *   - "host" pointers are ordinary CPU memory; "device" pointers are CUDA
  *     device memory on opts.device.  mem_flags says which (SFLSQR_MEM_*).
  *   - Ownership: the library never frees caller memory.  With SFLSQR_MEM_COPY
