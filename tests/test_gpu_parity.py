@@ -448,3 +448,37 @@ def test_csr16_overflow_falls_back_to_int32():
     ref_t = A.transpose().matvec(w)
     assert np.max(np.abs(got_t - ref_t)) <= 1e-13 * np.max(np.abs(ref_t))
     s.close()
+
+
+# ------------------------------------------------------------------ maximum sizes and tiny problems
+@pytest.mark.parametrize("method,d,maxit,window", [
+    ("sflsqr", 1500, 30, 3),     # d > 1024: the RPT = 4 projected-LS kernel
+    ("sflsmr", 2048, 24, 2),     # the largest sketch the one-CTA LS supports
+    ("sflsqr", 700, 600, 5),     # many columns: blocked back substitution over 19 blocks, long W-path residual
+])
+def test_maximum_sketch_and_iteration_counts(method, d, maxit, window):
+    p = _dense_prob(1600, 900, seed=d + maxit, cond=1e2)
+    spec = SolverSpec(method=method, maxit=maxit, window=window, d=d, s_nz=8, precond="irn")
+    kstar, _, _ = _stable_horizon(p, spec, min(maxit, 40))
+    assert kstar >= 10, kstar
+    r = solve_problem(p, spec, maxit=kstar)
+    g = _gpu_run(p, spec, maxit=kstar)
+    _compare(g, r, n_res=kstar)
+    if maxit > 100:
+        # the full 600-iteration run: same status and stop index, residual history within the oracle's own
+        # forward-stability band beyond the horizon is not asserted (reading R17); x by state injection
+        # is covered elsewhere — here the run must complete with finite, non-increasing sketched residuals
+        g = _gpu_run(p, spec, maxit=maxit)
+        assert g["info"]["k_done"] == maxit and np.all(np.isfinite(g["sketch_res"]))
+        assert np.all(np.diff(g["sketch_res"]) <= 1e-12 * g["sketch_res"][0])
+
+
+@pytest.mark.parametrize("m,n", [(3, 2), (2, 3), (1, 1), (5, 1)])
+def test_tiny_problems(m, n):
+    p = _dense_prob(m, n, seed=7 * m + n, cond=10)
+    maxit = min(m, n) + 1
+    spec = SolverSpec(method="sflsqr", maxit=maxit, window=2, d=max(maxit, 2), s_nz=1, precond="identity")
+    r = solve_problem(p, spec)
+    g = _gpu_run(p, spec)
+    assert g["status"] == r.status and g["info"]["k_x"] == r.k, (g["status"], r.status, g["info"], r.k)
+    np.testing.assert_allclose(g["x"], r.x, rtol=1e-10, atol=1e-12 * max(np.abs(r.x).max(), 1e-300))
