@@ -277,3 +277,25 @@ def test_step_from_state_reproduces_the_run(method, precond):
         np.testing.assert_array_equal(out["Hcol"], r.H[:k + 1, k - 1])
         np.testing.assert_array_equal(out["x"], r.xs[k - 1])
         assert out["r"] == r.true_res[k - 1] and out["sres"] == r.sketch_res[k - 1]
+
+
+# ---------------------------------------------------------------- P6b: Corollary (Gaussian sketch)
+def test_corollary_expected_residual_gaussian_sketch():
+    # Gaussian S (reading R21): E ||(S Q)^+ S Q_perp Q_perp^T b||^2 = k/(s-k-1) ||Q_perp^T b||^2 for a k-column
+    # orthonormal Q (HMT Prop. 10.2, which the Corollary's proof invokes), so by the
+    # identity of Theorem 2.1's proof E[r_k^2] = r_opt^2 (1 + k/(s-k-1)).  The Corollary as printed has
+    # s/(s-k-1) (paper inconsistency); the Monte Carlo mean separates the two.
+    from oracle.sketch import GaussianSketch
+    A, b, _ = _dense_problem(120, 60, 1e2, 41, noise=0.3)
+    k, s = 6, 20
+    ratios = []
+    for seed in range(300):
+        r = solve(DenseOperator(A), b, "sflsqr", maxit=k, window=k, sketch=GaussianSketch(1000 + seed, s, 120),
+                  precond="identity")
+        AZ = A @ r.Z
+        r_opt = np.linalg.norm(b - AZ @ np.linalg.lstsq(AZ, b, rcond=None)[0])
+        ratios.append(r.true_res[-1] ** 2 / r_opt ** 2 - 1.0)
+    mean, se = float(np.mean(ratios)), float(np.std(ratios) / np.sqrt(len(ratios)))
+    expect = k / (s - k - 1)                        # 0.4615
+    assert abs(mean - expect) < 4 * se + 0.02, (mean, se, expect)
+    assert abs(mean - s / (s - k - 1)) > 10 * se     # the printed constant (1.54) is rejected
