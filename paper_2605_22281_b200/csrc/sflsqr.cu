@@ -105,6 +105,7 @@ struct sflsqr {
   Prof prof;
   bool res_overlap = true;  // W-path residual on the side stream (SFLSQR_RES_OVERLAP=0/1 forces; A/B timing)
   bool res_overlap_forced = false;
+  bool lr_qr_cgs = false;   // tau_r range QR: shifted Cholesky QR (default) or one-CTA CGS2 (SFLSQR_LR_QR=cgs)
   int coop_grid = 0;     // blocks of the cooperative phase kernels (0: not available)
   bool coop_attr = true; // launch with cudaLaunchAttributeCooperative (cleared if unsupported)
 };
@@ -628,16 +629,31 @@ int launch_coop(sflsqr_t* h, void (*kern)(Params), double bytes) {
 }
 
 // a2 for the low-rank truncation: z_k = tau_r(p_k) by the randomized SVD (reading R22).
-void enqueue_lowrank(sflsqr_t* h) {
+int enqueue_lowrank(sflsqr_t* h) {
   Params& P = h->P;
   const double hw8 = 8.0 * P.lr_H * P.lr_W, l = P.lr_l;
   {
     Launch L(h, SFLSQR_KC_TAU, hw8 + 8.0 * l * (P.lr_W + P.lr_H));
     k_lr_range<<<std::min(P.lr_H, 148 * 4), 256, sizeof(double) * P.lr_W, h->stream>>>(P);
   }
-  {
+  if (h->lr_qr_cgs) {
     Launch L(h, SFLSQR_KC_TAU, 8.0 * l * P.lr_H * 2);
     k_lr_qr<<<1, 1024, kLrQrSmem, h->stream>>>(P);
+  } else {
+    // sCholQR3 on the range Y (copied into lr_Q, factored in place)
+    CU(h, cudaMemcpyAsync(P.lr_Q, P.lr_Y, sizeof(double) * P.lr_l * P.lr_H, cudaMemcpyDeviceToDevice, h->stream));
+    const int gg = (int)std::max<int64_t>(1, ((int64_t)P.lr_l * P.lr_l + 7) / 8);
+    const int gs = (int)std::max<int64_t>(1, std::min<int64_t>((P.lr_H + 255) / 256, 148 * 4));
+    for (int round = 0; round < 3; ++round) {
+      {
+        Launch L(h, SFLSQR_KC_TAU, 8.0 * l * P.lr_H);
+        k_lr_ygram<<<gg, 256, 0, h->stream>>>(P);
+      }
+      {
+        Launch L(h, SFLSQR_KC_TAU, 16.0 * l * P.lr_H);
+        k_lr_cholsolve<<<gs, 256, 0, h->stream>>>(P, round == 0 ? 1 : 0);
+      }
+    }
   }
   {
     Launch L(h, SFLSQR_KC_TAU, hw8 + 8.0 * l * (P.lr_W + P.lr_H));
@@ -663,6 +679,7 @@ void enqueue_lowrank(sflsqr_t* h) {
     Launch L(h, SFLSQR_KC_TAU, hw8 + 8.0 * l * (P.lr_W + P.lr_H));
     k_lr_recon<<<std::min(P.lr_H, 148 * 4), 256, 0, h->stream>>>(P);
   }
+  return SFLSQR_OK;
 }
 
 // One iteration k of Alg. 1 / Alg. 2, or of FLSQR /
@@ -687,7 +704,7 @@ int enqueue_iteration(sflsqr_t* h) {
     Launch L(h, SFLSQR_KC_TAU, n8 * (2 + (P.use_pring ? 1 : 0) + (P.precond ? 1 : 0)));
     k_finish_z<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P);
   }
-  if (P.precond == SFLSQR_PRECOND_LOWRANK_RND) enqueue_lowrank(h);
+  if (P.precond == SFLSQR_PRECOND_LOWRANK_RND && (rc = enqueue_lowrank(h))) return rc;
   // a3: w = A z_k  (z_k = Z[:, k-1]; all-gathered across ranks when sharded)
   if (h->world == 1) {
     enqueue_apply(h, 0, P.st, P.Z, h->n_loc, -1, P.w, SFLSQR_KC_SPMV_A);
@@ -1211,6 +1228,7 @@ int sflsqr_create(sflsqr_t** out, const sflsqr_opts* o) {
     }
   }
   if (const char* ev = std::getenv("SFLSQR_SPMV_MODE")) h->spmv_mode = std::atoi(ev);
+  if (const char* ev = std::getenv("SFLSQR_LR_QR")) h->lr_qr_cgs = std::strcmp(ev, "cgs") == 0;
   if (const char* ev = std::getenv("SFLSQR_RES_OVERLAP")) {
     h->res_overlap = ev[0] != '0';
     h->res_overlap_forced = h->res_overlap;

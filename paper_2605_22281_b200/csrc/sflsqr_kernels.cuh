@@ -1334,6 +1334,95 @@ __global__ void __launch_bounds__(1024) k_lr_qr(Params P) {
     for (int64_t e = threadIdx.x; e < (int64_t)H * l; e += 1024) P.lr_Q[e] = qs[e];
 }
 
+// Q = orth(Y) by shifted Cholesky QR, three rounds (sCholQR3): G = Y^T Y (+ shift in round 1),
+// R = chol(G), Y <- Y R^{-1}.  Same Q as Gram-Schmidt in exact arithmetic (Y = QR with R upper
+// triangular, positive diagonal), orthogonal to working precision after the third round even
+// for numerically rank-deficient Y (the shift keeps G + sI positive definite); all the work is
+// parallel: a Gram kernel (one warp per entry) and a solve kernel (one thread per row, each
+// block factors the l x l matrix redundantly in shared memory).
+__global__ void __launch_bounds__(256) k_lr_ygram(Params P) {
+  if (P.st->done) return;
+  const int H = P.lr_H, l = P.lr_l;
+  const int lane = threadIdx.x & 31;
+  for (int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wg < (int64_t)l * l;
+       wg += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int a = (int)(wg / l), b = (int)(wg % l);
+    if (b < a) continue;
+    const double* ya = P.lr_Q + (int64_t)a * H;
+    const double* yb = P.lr_Q + (int64_t)b * H;
+    double acc0 = 0.0, acc1 = 0.0;
+    int i = lane;
+    for (; i + 32 < H; i += 64) {
+      acc0 = fma(ya[i], yb[i], acc0);
+      acc1 = fma(ya[i + 32], yb[i + 32], acc1);
+    }
+    if (i < H) acc0 = fma(ya[i], yb[i], acc0);
+    const double v = warp_sum(acc0 + acc1);
+    if (lane == 0) {
+      P.lr_PB[(int64_t)a * l + b] = v;
+      P.lr_PB[(int64_t)b * l + a] = v;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_lr_cholsolve(Params P, int shifted) {
+  __shared__ double R[kLrMaxL][kLrMaxL + 1];
+  __shared__ double rinv[kLrMaxL];
+  if (P.st->done) return;
+  const int H = P.lr_H, l = P.lr_l;
+  for (int e = threadIdx.x; e < l * l; e += blockDim.x) R[e / l][e % l] = P.lr_PB[e];
+  __syncthreads();
+  if (shifted) {  // s = 11 (H l + l (l + 1)) u ||Y||_F^2 >= the sCholQR3 shift bound
+    __shared__ double shv;
+    if (threadIdx.x < 32) {
+      double tr = 0.0;
+      for (int a = threadIdx.x; a < l; a += 32) tr += R[a][a];
+      tr = warp_sum(tr);
+      if (threadIdx.x == 0) shv = 11.0 * ((double)H * l + (double)l * (l + 1)) * 1.1102230246251565e-16 * tr;
+    }
+    __syncthreads();
+    if (threadIdx.x < l) R[threadIdx.x][threadIdx.x] += shv;
+    __syncthreads();
+  }
+  // right-looking Cholesky, upper factor R (R^T R = G), the whole block on each trailing update
+  for (int c = 0; c < l; ++c) {
+    if (threadIdx.x == 0) {
+      const double d = sqrt(fmax(R[c][c], 1e-300));
+      R[c][c] = d;
+      rinv[c] = 1.0 / d;
+    }
+    __syncthreads();
+    for (int b = c + 1 + threadIdx.x; b < l; b += blockDim.x) R[c][b] *= rinv[c];
+    __syncthreads();
+    const int nr = l - c - 1;
+    for (int t = threadIdx.x; t < nr * kLrMaxL; t += blockDim.x) {
+      const int a = c + 1 + t / kLrMaxL, b = t % kLrMaxL;  // kLrMaxL is a power of two: shifts
+      if (b >= a && b < l) R[a][b] = fma(-R[c][a], R[c][b], R[a][b]);
+    }
+    __syncthreads();
+  }
+  // Y <- Y R^{-1}: for each row y, solve q R = y by forward substitution over the columns
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < H; i += (int64_t)gridDim.x * blockDim.x) {
+    double q[kLrMaxL];
+#pragma unroll
+    for (int c = 0; c < kLrMaxL; ++c)
+      if (c < l) q[c] = P.lr_Q[(int64_t)c * H + i];
+#pragma unroll
+    for (int c = 0; c < kLrMaxL; ++c) {
+      if (c < l) {
+        double v = q[c];
+#pragma unroll
+        for (int j = 0; j < kLrMaxL; ++j)
+          if (j < c) v = fma(-q[j], R[j][c], v);
+        q[c] = v * rinv[c];
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < kLrMaxL; ++c)
+      if (c < l) P.lr_Q[(int64_t)c * H + i] = q[c];
+  }
+}
+
 // B = Q^T C (l x W), split over kLrSplit chunks of image rows for parallelism: one warp per
 // (row c of B, 32 image columns, row chunk) writes a partial into lr_part; k_lr_proj_sum adds
 // the kLrSplit partials in chunk order (deterministic).
