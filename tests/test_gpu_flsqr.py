@@ -154,3 +154,14 @@ def test_graph_and_eager_agree_bitwise_flsmr():
     g1 = _gpu_run(p, spec, 25, "flsmr", use_graph=False)
     g2 = _gpu_run(p, spec, 25, "flsmr", use_graph=True)
     assert np.array_equal(g1["x"], g2["x"]) and np.array_equal(g1["proj_res"], g2["proj_res"])
+
+
+@pytest.mark.parametrize("cfg,maxit", [(3, 8), (4, 3)])
+@pytest.mark.parametrize("method", ["flsqr", "flsmr"])
+def test_full_size_first_iterations(cfg, maxit, method):
+    # BASELINE.json sizes (config 3: 1.2e8 nnz matched; config 4: 2.5e9 nnz unmatched), first iterations
+    p = make_problem(cfg)
+    spec = p.solvers[0]
+    r = solve_problem(p, spec, maxit=maxit, eta=0.0, method=method, record=False)
+    g = _gpu_run(p, spec, maxit, method)
+    _compare(g, r, maxit)

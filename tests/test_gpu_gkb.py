@@ -140,3 +140,13 @@ def test_gkb_rejects_flexible_preconditioner():
         s.set_rhs(p.b)
     assert e.value.code == B.E_INVALID
     s.close()
+
+
+@pytest.mark.parametrize("cfg,maxit", [(3, 8), (4, 3)])
+@pytest.mark.parametrize("method", ["lsqr", "lsmr"])
+def test_gkb_full_size_first_iterations(cfg, maxit, method):
+    p = make_problem(cfg)
+    spec = p.solvers[0]
+    r = solve_problem(p, spec, maxit=maxit, eta=0.0, method=method, record=False)
+    g = _gpu_run(p, spec, maxit, method)
+    _compare(g, r, method)
