@@ -690,7 +690,6 @@ int enqueue_iteration(sflsqr_t* h) {
   if (P.method >= SFLSQR_METHOD_LSQR) return enqueue_gkb_iteration(h);
   const int k = h->host_k;  // used only for the byte model
   const double n8 = 8.0 * h->n_loc, m8 = 8.0 * h->m_loc;
-  const bool sketched = P.method == SFLSQR_METHOD_SFLSQR || P.method == SFLSQR_METHOD_SFLSMR;
   int rc;
   const bool coop = use_coop(h);
   const int Jz = std::min(P.ell, k - 1), Jw = std::min(P.ell + 1, k);
@@ -756,7 +755,6 @@ int enqueue_iteration(sflsqr_t* h) {
   // FLSMR: z side of step k+1 now (column k+1 of T for T_{k+1} H_{k+1,k}, L361-367)
   if (P.method == SFLSQR_METHOD_FLSMR && (rc = enqueue_orth(h, 0, 1))) return rc;
   // a7: projected (sketched) LS (replicated on every rank: identical inputs)
-  (void)sketched;
   if (fork_ls) {
     CU(h, cudaStreamWaitEvent(h->stream, h->ev_join, 0));
   } else if ((rc = enqueue_ls(h, false))) {
