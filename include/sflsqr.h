@@ -53,7 +53,7 @@
 extern "C" {
 #endif
 
-#define SFLSQR_ABI_VERSION 2
+#define SFLSQR_ABI_VERSION 3
 
 /* return codes */
 #define SFLSQR_OK 0
@@ -164,6 +164,9 @@ typedef struct sflsqr_info {
   double beta;         /* ||b||                                                   */
   int64_t m0, m_loc;   /* this rank's rows of A / slice of m-vectors: [m0, m0+m_loc) */
   int64_t n0, n_loc;   /* this rank's slice of n-vectors: [n0, n0+n_loc)           */
+  double delta_e;      /* opts.delta_e (the discrepancy test's noise norm)         */
+  double bytes_model;  /* algorithmic HBM bytes of iteration k_done on this rank, the model of
+                          SURVEY.md §8(d) / DESIGN.md §5 (0 before the first iteration)  */
 } sflsqr_info;
 
 /* Per-kernel-class device time, recorded with CUDA events on the library stream

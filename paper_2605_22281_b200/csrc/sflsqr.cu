@@ -1744,7 +1744,21 @@ int sflsqr_get_info(sflsqr_t* h, sflsqr_info* info) {
     info->status = st.done ? st.status : SFLSQR_RUNNING;
     info->rank_flag = st.rank_flag;
     info->beta = st.beta;
+    const int k = info->k_done;
+    if (k > 0) {
+      // operators + each gathered input read once and each product written once +
+      // the windowed orthogonalisation passes + [tau needs x] x reconstruction + [history] W path
+      const double m8 = 8.0 * h->m_loc, n8 = 8.0 * h->n_loc, ell = h->P.ell;
+      double b = h->blur ? 4.0 * 16.0 * h->n_loc : 12.0 * (h->nnz_a + h->nnz_t) + 8.0 * (h->m_loc + 1) +
+                                                      8.0 * (h->t_rows + 1);
+      b += 2.0 * (m8 + n8);
+      if (h->o.method <= SFLSQR_METHOD_FLSMR) b += m8 * (2 * ell + 5) + n8 * (2 * ell + 3) + 2.0 * n8;
+      if (h->P.need_x) b += n8 * (k - 1);
+      if (h->P.want_res && h->o.method < SFLSQR_METHOD_LSQR) b += m8 * (k + 1);
+      info->bytes_model = b;
+    }
   }
+  info->delta_e = h->o.delta_e;
   return SFLSQR_OK;
 }
 

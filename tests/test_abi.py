@@ -50,7 +50,7 @@ def test_version_and_create_without_gpu(lib):
     import torch
     from paper_2605_22281_b200 import sflsqr as B
     L = B.load_library()
-    assert L.sflsqr_version() == 2
+    assert L.sflsqr_version() == 3
     if torch.cuda.is_available():
         pytest.skip("GPU present: covered by the -m gpu tests")
     with pytest.raises(B.SflsqrError) as ei:
@@ -65,3 +65,21 @@ def test_option_validation_precedes_device_use(lib):
         with pytest.raises(B.SflsqrError) as ei:
             B.SFLSQR(**kw)
         assert ei.value.code == B.E_INVALID, kw
+
+
+def test_ctypes_structs_match_header_layout(lib):
+    # the binding's ctypes mirrors of sflsqr_opts / sflsqr_info / sflsqr_profile must have the C sizes
+    # (compiled here from include/sflsqr.h with gcc, no GPU needed)
+    import ctypes
+    import os
+    import tempfile
+    from paper_2605_22281_b200 import sflsqr as B
+    inc = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include")
+    src = ('#include "sflsqr.h"\n#include <stdio.h>\nint main(void){printf("%zu %zu %zu\\n", sizeof(sflsqr_opts),'
+           ' sizeof(sflsqr_info), sizeof(sflsqr_profile)); return 0;}\n')
+    with tempfile.TemporaryDirectory() as d:
+        c, exe = os.path.join(d, "s.c"), os.path.join(d, "s")
+        open(c, "w").write(src)
+        subprocess.run(["gcc", "-I" + inc, c, "-o", exe], check=True)
+        sizes = [int(t) for t in subprocess.run([exe], capture_output=True, text=True, check=True).stdout.split()]
+    assert sizes == [ctypes.sizeof(B.Opts), ctypes.sizeof(B.Info), ctypes.sizeof(B.Profile)]

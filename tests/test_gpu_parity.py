@@ -482,3 +482,21 @@ def test_tiny_problems(m, n):
     g = _gpu_run(p, spec)
     assert g["status"] == r.status and g["info"]["k_x"] == r.k, (g["status"], r.status, g["info"], r.k)
     np.testing.assert_allclose(g["x"], r.x, rtol=1e-10, atol=1e-12 * max(np.abs(r.x).max(), 1e-300))
+
+
+def test_info_bytes_model_and_delta_e():
+    # sflsqr_get_info: the SURVEY.md §8(d) byte model of the last iteration, written out here
+    from paper_2605_22281_b200 import solver_for_problem
+    p = make_problem(3, N=96, n_angles=70, nb=137)
+    spec = p.solvers[0]                                   # NONNEG tau (x each step), history on
+    s = solver_for_problem(p, spec, maxit=7, eta=0.0)
+    s.set_rhs(p.b)
+    s.iterate(7)
+    info = s.get_info()
+    s.close()
+    m, n, ell, k = p.m, p.n, spec.window, 7
+    nnz = p.A.nnz
+    expect = (12.0 * 2 * nnz + 8.0 * (m + 1) + 8.0 * (n + 1) + 16.0 * (m + n) + 8.0 * m * (2 * ell + 5)
+              + 8.0 * n * (2 * ell + 3) + 16.0 * n + 8.0 * n * (k - 1) + 8.0 * m * (k + 1))
+    assert info["bytes_model"] == pytest.approx(expect, rel=1e-12)
+    assert info["delta_e"] == p.delta_e
