@@ -5,6 +5,7 @@
 #include <nccl.h>
 
 #include <cstring>
+#include <vector>
 
 namespace sfl {
 
@@ -57,8 +58,46 @@ NcclApi& nccl() {
 
 struct NcclComm : Comm {
   ncclComm_t comm = nullptr;
+  double* scratch = nullptr;  // one double for the barrier all-reduce
   ~NcclComm() override {
     if (comm) nccl().CommDestroy(comm);
+    cudaFree(scratch);
+  }
+  int barrier(cudaStream_t s, std::string& err) override {
+    if (!scratch && cudaMalloc(&scratch, sizeof(double)) != cudaSuccess) {
+      err = "barrier: cudaMalloc failed";
+      return -1;
+    }
+    // an all-reduce completes only after every rank's NCCL kernel ran, i.e. after all the work its
+    // stream had before it (the kernels storing into peer memory)
+    return check(nccl().AllReduce(scratch, scratch, 1, ncclDouble, ncclSum, comm, s), "ncclAllReduce(barrier)", err);
+  }
+  int share_buffer(void* local, void** peers, std::string& err) override {
+    cudaIpcMemHandle_t mine;
+    if (cudaIpcGetMemHandle(&mine, local) != cudaSuccess) {
+      cudaGetLastError();
+      err = "cudaIpcGetMemHandle failed";
+      return -1;
+    }
+    std::vector<cudaIpcMemHandle_t> all(world);
+    if (allgather_host(&mine, all.data(), sizeof(mine), err)) return -1;
+    for (int r = 0; r < world; ++r) {
+      peers[r] = nullptr;
+      if (r == rank) {
+        peers[r] = local;
+      } else if (cudaIpcOpenMemHandle(&peers[r], all[r], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        err = "cudaIpcOpenMemHandle failed (no peer access between the ranks' GPUs?)";
+        for (int q = 0; q < r; ++q)
+          if (q != rank && peers[q]) cudaIpcCloseMemHandle(peers[q]);
+        return -1;
+      }
+    }
+    return 0;
+  }
+  void unshare_buffer(void** peers) override {
+    for (int r = 0; r < world; ++r)
+      if (r != rank && peers[r]) cudaIpcCloseMemHandle(peers[r]);
   }
   int check(ncclResult_t r, const char* what, std::string& err) {
     if (r == ncclSuccess) return 0;
@@ -259,6 +298,11 @@ struct LocalComm : Comm {
       if (g->host_stage.size() < bytes * g->world) g->host_stage.resize(bytes * g->world);
     }
     return collective(4, send, recv, bytes, nullptr, err);
+  }
+  // every rank's stream waits on every rank's prior work (a zero-length collective: no kernel)
+  int barrier(cudaStream_t s, std::string& err) override { return collective(0, nullptr, nullptr, 0, s, err); }
+  int share_buffer(void* local, void** peers, std::string& err) override {
+    return allgather_host(&local, peers, sizeof(void*), err);
   }
   ~LocalComm() override { local_group_release(g); }
 };

@@ -37,6 +37,13 @@ struct Comm {
   virtual int reduce_scatter(const double* send, double* recv, size_t count, cudaStream_t s, std::string& err) = 0;
   // blocking host allgather of `bytes` per rank (setup only)
   virtual int allgather_host(const void* send, void* recv, size_t bytes, std::string& err) = 0;
+  // Stream-ordered barrier: work issued on s after it starts only when every rank's work issued
+  // before its barrier call -- including stores into peer memory -- is complete.
+  virtual int barrier(cudaStream_t s, std::string& err) = 0;
+  // Peer pointers of a buffer every rank allocated (same role, cudaMalloc base): peers[r] is rank
+  // r's buffer addressable from this device (in-process: the raw pointers; NCCL: CUDA IPC).
+  virtual int share_buffer(void* local, void** peers, std::string& err) = 0;
+  virtual void unshare_buffer(void** peers) { (void)peers; }
 };
 
 // ---------------------------------------------------------------- NCCL (dlopen)

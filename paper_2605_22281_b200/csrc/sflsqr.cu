@@ -92,6 +92,13 @@ struct sflsqr {
   Params P;
   int nslots = 0;
   double *zfull = nullptr, *wfull = nullptr, *zpart = nullptr;
+  // peer-memory collectives (SFLSQR_P2P; default on for the in-process group, opt-in for NCCL):
+  // every rank's zfull / wfull / zrecv addressable from this device
+  bool p2p = false;
+  double* zrecv = nullptr;
+  void* peer_zfull[8] = {};
+  void* peer_wfull[8] = {};
+  void* peer_zrecv[8] = {};
   double* gtmp = nullptr;  // GKB: product before the separate epilogue pass (blur / non-default SpMV)
   std::vector<void*> solve_allocs;
   std::vector<size_t> solve_sizes;
@@ -250,6 +257,14 @@ void free_solve(sflsqr_t* h) {
     cudaGraphExecDestroy(h->gexec);
     h->gexec = nullptr;
   }
+  if (h->comm) {
+    cudaStreamSynchronize(h->stream);
+    for (void** pp : {h->peer_zfull, h->peer_wfull, h->peer_zrecv}) {
+      if (pp[h->rank]) h->comm->unshare_buffer(pp);
+      for (int g = 0; g < 8; ++g) pp[g] = nullptr;
+    }
+  }
+  h->zrecv = nullptr;
   for (void* p : h->solve_allocs) cudaFree(p);
   h->solve_allocs.clear();
   h->solve_sizes.clear();
@@ -463,10 +478,35 @@ int enqueue_transpose_product(sflsqr_t* h, bool init) {
   }
   std::string e;
   if (h->tkind == T_ROWSHARD) {
-    // all-gather w_{k+1} (wsend, m_max per rank, zero padded) -> wfull; local rows of T
-    if (h->comm->allgather(P.wsend, h->wfull, h->m_max, h->stream, e))
+    // all-gather w_{k+1} (wsend, m_max per rank, zero padded) -> wfull; local rows of T.  Peer
+    // memory: k_finish_w / k_init_w1 already stored w_{k+1} into every rank's wfull; a barrier.
+    if (h->p2p) {
+      if (h->comm->barrier(h->stream, e)) return fail(h, SFLSQR_E_CUDA, "barrier(w): %s", e.c_str());
+    } else if (h->comm->allgather(P.wsend, h->wfull, h->m_max, h->stream, e)) {
       return fail(h, SFLSQR_E_CUDA, "allgather(w): %s", e.c_str());
+    }
     enqueue_apply(h, 1, P.st, h->wfull, 0, 0, P.z, SFLSQR_KC_SPMV_T);
+    return SFLSQR_OK;
+  }
+  if (h->p2p) {
+    // COLSHARD, peer memory: the product's epilogue stores each row sum into its owner's receive
+    // slot for this rank (the reduce-scatter fused into the SpMV, overlapped with it row group by
+    // row group); after a barrier every rank sums its slots in rank order.
+    SpmvEpi E = SpmvEpi();
+    E.kind = 4;
+    E.src = h->rank;
+    E.nmax = h->n_max;
+    for (int g = 0; g < 8; ++g) E.peers[g] = static_cast<double*>(h->peer_zrecv[g]);
+    {
+      const double bytes = 12.0 * h->nnz_t + 8.0 * (h->t_rows + 1) + 16.0 * h->m_loc + 8.0 * h->t_rows;
+      Launch L(h, SFLSQR_KC_SPMV_T, bytes);
+      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((h->t_rows + 31) / 32, 148 * 4));
+      k_spmv_csr_pf<16, 4, 16, true><<<grid, 512, 0, h->stream>>>(P.st, h->t_rows, h->t_rowptr, h->t_col, h->t_val,
+                                                                   P.W, ld, 0, nullptr, E);
+    }
+    if (h->comm->barrier(h->stream, e)) return fail(h, SFLSQR_E_CUDA, "barrier(z): %s", e.c_str());
+    Launch L(h, SFLSQR_KC_SPMV_T, 8.0 * (h->world + 1) * h->n_max);
+    k_reduce_recv<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P.st, h->zrecv, h->world, h->n_max, P.z);
     return SFLSQR_OK;
   }
   // COLSHARD: partial n-vector (padded layout) from the local w slice, reduce-scattered
@@ -709,8 +749,11 @@ int enqueue_iteration(sflsqr_t* h) {
     enqueue_apply(h, 0, P.st, P.Z, h->n_loc, -1, P.w, SFLSQR_KC_SPMV_A);
   } else {
     std::string e;
-    if (h->comm->allgather(P.zsend, h->zfull, h->n_max, h->stream, e))
+    if (h->p2p) {  // z_k already stored into every rank's zfull by k_finish_z: a barrier
+      if (h->comm->barrier(h->stream, e)) return fail(h, SFLSQR_E_CUDA, "barrier(z_k): %s", e.c_str());
+    } else if (h->comm->allgather(P.zsend, h->zfull, h->n_max, h->stream, e)) {
       return fail(h, SFLSQR_E_CUDA, "allgather(z): %s", e.c_str());
+    }
     enqueue_apply(h, 0, P.st, h->zfull, 0, 0, P.w, SFLSQR_KC_SPMV_A);
   }
   // a4 + a5 in one cooperative kernel (sketch of w, then the w side)
@@ -1031,6 +1074,7 @@ int alloc_solve(sflsqr_t* h) {
       if ((rc = A(&P.wsend, h->m_max)) || (rc = A(&h->wfull, (size_t)h->world * h->m_max))) return rc;
     } else {
       if ((rc = A(&h->zpart, (size_t)h->world * h->n_max))) return rc;
+      if (h->p2p && (rc = A(&h->zrecv, (size_t)h->world * h->n_max))) return rc;
     }
   }
   // Debug aid (no sanitizer on this pool): SFLSQR_DEBUG_POISON=1 fills every solve
@@ -1045,6 +1089,29 @@ int alloc_solve(sflsqr_t* h) {
   // the padded send buffers' tails are never written
   if (P.zsend) CU(h, cudaMemset(P.zsend, 0, sizeof(double) * h->n_max));
   if (P.wsend) CU(h, cudaMemset(P.wsend, 0, sizeof(double) * h->m_max));
+  if (h->p2p) {
+    // peer-memory collectives: zero the gathered buffers (padding tails stay zero) and exchange
+    // the buffer addresses (collective over the ranks)
+    std::string e;
+    CU(h, cudaMemset(h->zfull, 0, sizeof(double) * h->world * h->n_max));
+    if (h->wfull) CU(h, cudaMemset(h->wfull, 0, sizeof(double) * h->world * h->m_max));
+    CU(h, cudaDeviceSynchronize());
+    if (h->comm->share_buffer(h->zfull, h->peer_zfull, e) ||
+        (h->wfull && h->comm->share_buffer(h->wfull, h->peer_wfull, e)) ||
+        (h->zrecv && h->comm->share_buffer(h->zrecv, h->peer_zrecv, e)))
+      return fail(h, SFLSQR_E_CUDA, "peer buffers: %s", e.c_str());
+    P.p2p_z = 1;
+    P.p2p_w = h->tkind == T_ROWSHARD ? 1 : 0;
+    P.rank_id = h->rank;
+    P.n_max_p = h->n_max;
+    P.m_max_p = h->m_max;
+    for (int g = 0; g < 8; ++g) {
+      P.peer_zfull[g] = static_cast<double*>(h->peer_zfull[g]);
+      P.peer_wfull[g] = static_cast<double*>(h->peer_wfull[g]);
+    }
+    P.zsend = nullptr;  // the peer stores replace the send copies
+    P.wsend = nullptr;
+  }
   if (sketched && (rc = build_sketch(h))) return rc;
   h->bufs = true;
   return SFLSQR_OK;
@@ -1219,6 +1286,11 @@ int sflsqr_create(sflsqr_t** out, const sflsqr_opts* o) {
       h->comm = nccl_comm_create(o->nccl_id, o->rank, o->world, o->device, ce);
     else
       h->comm = local_comm_create(static_cast<LocalGroup*>(o->local_group), o->rank);
+    // peer-memory collectives: default on in-process (tested), opt-in (SFLSQR_P2P=1) across
+    // processes (CUDA IPC over NVLink: not exercisable on this single-GPU pool)
+    const char* pe = std::getenv("SFLSQR_P2P");
+    h->p2p = pe ? pe[0] == '1' : o->comm_kind == SFLSQR_COMM_LOCAL;
+    if (o->world > 8) h->p2p = false;
     if (!h->comm) {
       if (h->own_stream) cudaStreamDestroy(h->stream);
       delete h;

@@ -53,6 +53,12 @@ struct Params {
   double* scal;            // per-slot global scalars (dist)
   double* skbuf;           // d: S v of the current vector (allreduced when dist)
   double *zsend, *wsend;   // dist: fixed-address copies of z_k / w_{k+1} for the allgathers
+  // dist, peer-memory collectives (SFLSQR_P2P): z_k / w_{k+1} are stored straight into every
+  // rank's gathered buffer, the COLSHARD T product straight into its owner's receive slots
+  int p2p_z, p2p_w, rank_id;
+  int64_t n_max_p, m_max_p;
+  double* peer_zfull[8];
+  double* peer_wfull[8];
   double p_exp, eps_rel, tol, eta, delta_e, sk_scale;
   uint32_t seed_lo, seed_hi;
   // n-side vectors
@@ -430,6 +436,9 @@ __global__ void __launch_bounds__(WPB * 32, 2048 / (WPB * 32)) k_spmv_csr_rows(c
 //   kind 1 (A side):  a = 1,        c = alpha_k / beta_k   (u' = A v_k - alpha_k u_k, u_k = u'_old / beta_k)
 //   kind 2 (T side):  a = 1/beta',  c = beta'              (v' = T u_{k+1} - beta_{k+1} v_k, beta'^2 = scal[slot_in])
 //   kind 3 (T, init): a = 1/beta_1, c = 0                  (v' = T b / ||b||)
+//   kind 4 (COLSHARD T product, peer memory): row r of the padded n layout is owned by rank
+//                     g = r / nmax; the row sum is stored into peers[g][src * nmax + r - g nmax]
+//                     (reduce-scatter fused into the product; k_reduce_recv sums the slots)
 struct SpmvEpi {
   int kind;               // 0: plain y = M x
   double* aux;            // may alias y (each row reads and writes only its own entry)
@@ -438,6 +447,9 @@ struct SpmvEpi {
   double* part;           // per-block partials
   int* ctr;
   int slot_in, slot_out, ctr_idx;
+  int src;                // kind 4: this rank
+  int64_t nmax;           // kind 4: rows per rank in the padded layout
+  double* peers[8];       // kind 4: every rank's receive buffer (world x nmax)
 };
 
 __device__ __forceinline__ void epi_coefs(const SpmvEpi& E, const DevState* st, double& a, double& c) {
@@ -446,7 +458,7 @@ __device__ __forceinline__ void epi_coefs(const SpmvEpi& E, const DevState* st, 
   if (E.kind == 1) {
     const double* g = E.gk + kGkbState * (st->k & 1);
     c = g[1] > 0.0 ? g[0] / g[1] : 0.0;
-  } else if (E.kind >= 2) {
+  } else if (E.kind == 2 || E.kind == 3) {
     const double bn = sqrt(E.scal[E.slot_in]);
     a = bn > 0.0 ? 1.0 / bn : 0.0;
     c = E.kind == 2 ? bn : 0.0;
@@ -510,14 +522,19 @@ __global__ void __launch_bounds__(WPB * 32, EPI ? 2 : 2048 / (WPB * 32)) k_spmv_
 #pragma unroll
     for (int o = LANES / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
     if (sl == 0 && row < nrows) {
-      if (EPI) {
-        sum = E.kind == 3 ? sum * ea : fma(sum, ea, -ec * E.aux[row]);
-        nrm = fma(sum, sum, nrm);
+      if (EPI && E.kind == 4) {
+        const int64_t g = row / E.nmax;
+        E.peers[g][(int64_t)E.src * E.nmax + (row - g * E.nmax)] = sum;
+      } else {
+        if (EPI) {
+          sum = E.kind == 3 ? sum * ea : fma(sum, ea, -ec * E.aux[row]);
+          nrm = fma(sum, sum, nrm);
+        }
+        y[row] = sum;
       }
-      y[row] = sum;
     }
   }
-  if (EPI) {
+  if (EPI && E.kind != 4) {
     __shared__ double sh[33];
     __shared__ int s_last;
     nrm = block_sum<WPB * 32>(nrm, sh);
@@ -829,6 +846,18 @@ __global__ void __launch_bounds__(kVecThreads) k_reduce_slots(Params P, int slot
   if (threadIdx.x == 0) P.scal[slot] = v;
 }
 
+// Peer-memory reduce-scatter, second half: z[i] = sum over source ranks of recv[src * nmax + i]
+// (fixed rank order, the order of the in-process group's reduction: deterministic).
+__global__ void __launch_bounds__(kVecThreads) k_reduce_recv(const DevState* st, const double* __restrict__ recv,
+                                                             int world, int64_t nmax, double* __restrict__ z) {
+  if (st && st->done) return;
+  for (int64_t i = (int64_t)blockIdx.x * kVecThreads + threadIdx.x; i < nmax; i += (int64_t)gridDim.x * kVecThreads) {
+    double acc = recv[i];
+    for (int g = 1; g < world; ++g) acc += recv[(int64_t)g * nmax + i];
+    z[i] = acc;
+  }
+}
+
 // ------------------------------------------------------------------ init
 // beta = ||b|| (partials in slot_beta), then w_1 = b / beta (Alg. 1).
 __global__ void __launch_bounds__(kVecThreads) k_norm_partial(Params P, const double* __restrict__ v, int64_t len,
@@ -848,6 +877,11 @@ __global__ void __launch_bounds__(kVecThreads) k_init_w1(Params P) {
     const double w1 = P.b[i] / beta;
     P.W[i] = w1;
     if (P.wsend) P.wsend[i] = w1;
+    if (P.p2p_w) {
+      const int64_t o = (int64_t)P.rank_id * P.m_max_p + i;
+      for (int g = 0; g < 8; ++g)
+        if (P.peer_wfull[g]) P.peer_wfull[g][o] = w1;
+    }
   }
 }
 
@@ -1241,6 +1275,11 @@ __device__ __forceinline__ bool finish_z_body(const Params& P, DevState* st, int
     zk[i] = zi;
     if (pr) pr[i] = p;
     if (P.zsend) P.zsend[i] = zi;
+    if (P.p2p_z) {  // all-gather of z_k as direct stores into every rank's zfull (NVLink peer memory)
+      const int64_t o = (int64_t)P.rank_id * P.n_max_p + i;
+      for (int g = 0; g < 8; ++g)
+        if (P.peer_zfull[g]) P.peer_zfull[g][o] = zi;
+    }
   }
   return true;
 }
@@ -1647,6 +1686,11 @@ __device__ __forceinline__ void finish_w_body(const Params& P, DevState* st, int
     const double wv = brk ? 0.0 : P.w[i] / hn;
     wk1[i] = wv;
     if (P.wsend) P.wsend[i] = wv;
+    if (P.p2p_w) {  // ROWSHARD all-gather of w_{k+1} as direct peer stores
+      const int64_t o = (int64_t)P.rank_id * P.m_max_p + i;
+      for (int g = 0; g < 8; ++g)
+        if (P.peer_wfull[g]) P.peer_wfull[g][o] = wv;
+    }
   }
 }
 

@@ -88,3 +88,26 @@ def test_nccl_unique_id_available():
     from paper_2605_22281_b200.sflsqr import get_unique_id
     uid = get_unique_id()
     assert isinstance(uid, bytes) and len(uid) == 128 and any(uid)
+
+
+@pytest.mark.parametrize("cfg,world", [(3, 3), (4, 2)])
+def test_peer_memory_collectives_bitwise_equal_to_collectives(cfg, world, monkeypatch):
+    # SFLSQR_P2P: all-gathers as direct stores into every rank's gathered buffer and the COLSHARD
+    # reduce-scatter fused into the T product's epilogue (stores into the owner's receive slots),
+    # each followed by a barrier; the sums run in rank order as in the in-process collectives,
+    # so the two paths must agree bit for bit (config 3: COLSHARD, config 4: ROWSHARD)
+    from paper_2605_22281_b200.shard import run_local_group
+    kw = dict(N=96, n_angles=70, nb=137) if cfg == 3 else dict(N=128, n_angles=90, nb=183)
+    p = make_problem(cfg, **kw)
+    spec = p.solvers[0]
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("SFLSQR_P2P", mode)
+        x, tr, sk, infos, st, _ = run_local_group(p, spec, world, maxit=20, eta=0.0)
+        out[mode] = (x, tr, sk)
+    assert np.array_equal(out["0"][0], out["1"][0])
+    assert np.array_equal(out["0"][1], out["1"][1]) and np.array_equal(out["0"][2], out["1"][2])
+    # and the peer-memory path against the oracle
+    r = solve_problem(p, spec, maxit=12, eta=0.0)
+    x, tr, sk, _, _, _ = run_local_group(p, spec, world, maxit=12, eta=0.0)
+    _check(x, tr, sk, r, 12)
