@@ -641,8 +641,15 @@ int enqueue_ls(sflsqr_t* h, bool forked) {
 
 // The cooperative phase kernels replace the standalone a1/a2 and a4/a5 kernels on one rank
 // with the fused window orthogonalisation of a sketched method (opt-in: SFLSQR_COOP=1).
+// FLSMR (needs column k+1 of T at step k) and sFLSMR (overlaps it with the LS) run the z-side
+// orthogonalisation of step k+1 at the end of step k (and of step 1 in set_rhs); step k then
+// starts with the normalisation.  Same arithmetic, earlier in the stream.
+bool z_early(sflsqr_t* h) {
+  return h->P.method == SFLSQR_METHOD_FLSMR || h->P.method == SFLSQR_METHOD_SFLSMR;
+}
+
 bool use_coop(sflsqr_t* h) {
-  return h->coop_grid > 0 && h->world == 1 && h->P.orth_alg == ORTH_FUSED && h->P.method <= SFLSQR_METHOD_SFLSMR &&
+  return h->coop_grid > 0 && h->world == 1 && h->P.orth_alg == ORTH_FUSED && h->P.method == SFLSQR_METHOD_SFLSQR &&
          h->sk_kind == 0;
 }
 
@@ -737,7 +744,7 @@ int enqueue_iteration(sflsqr_t* h) {
   if (coop && (rc = launch_coop(h, k_zphase, n8 * (3 + 2 * Jz + (P.use_pring ? 1 : 0) + (P.precond ? 1 : 0)))))
     return rc;
   // a1: z-side windowed orthogonalisation (FLSMR: done at the end of the previous step / in set_rhs)
-  if (!coop && P.method != SFLSQR_METHOD_FLSMR && (rc = enqueue_orth(h, 0, 0))) return rc;
+  if (!coop && !z_early(h) && (rc = enqueue_orth(h, 0, 0))) return rc;
   // a1 end + a2: normalise, tau, store z_k
   if (!coop) {
     Launch L(h, SFLSQR_KC_TAU, n8 * (2 + (P.use_pring ? 1 : 0) + (P.precond ? 1 : 0)));
@@ -795,10 +802,14 @@ int enqueue_iteration(sflsqr_t* h) {
   if ((rc = enqueue_transpose_product(h, false))) return rc;
   // a4 (sFLSMR): S z -> S_TW[:, k+1]
   if (P.method == SFLSQR_METHOD_SFLSMR && (rc = enqueue_sketch(h, P.st, P.z))) return rc;
-  // FLSMR: z side of step k+1 now (column k+1 of T for T_{k+1} H_{k+1,k}, L361-367)
-  if (P.method == SFLSQR_METHOD_FLSMR && (rc = enqueue_orth(h, 0, 1))) return rc;
+  // FLSMR: z side of step k+1 now (column k+1 of T for T_{k+1} H_{k+1,k}, L361-367).
+  // sFLSMR: the same, on the main stream while the LS (which needs only S z) runs on the side
+  // stream -- the z-side dots/axpy of step k+1 depend on neither the LS nor the stop test.
+  const bool fork_ls_mr = P.method == SFLSQR_METHOD_SFLSMR && !h->prof_on && h->side;
+  if (fork_ls_mr && (rc = enqueue_ls(h, true))) return rc;
+  if (z_early(h) && (rc = enqueue_orth(h, 0, 1))) return rc;
   // a7: projected (sketched) LS (replicated on every rank: identical inputs)
-  if (fork_ls) {
+  if (fork_ls || fork_ls_mr) {
     CU(h, cudaStreamWaitEvent(h->stream, h->ev_join, 0));
   } else if ((rc = enqueue_ls(h, false))) {
     return rc;
@@ -1713,7 +1724,7 @@ int sflsqr_set_rhs(sflsqr_t* h, const double* b, int64_t len, int32_t mem_flags)
   }
   // FLSMR: the z side of step 1 (its norm is T_11) now; later steps run it one step early
   h->host_k = 1;
-  if (P.method == SFLSQR_METHOD_FLSMR && (rc = enqueue_orth(h, 0, 0))) return rc;
+  if (z_early(h) && (rc = enqueue_orth(h, 0, 0))) return rc;
   if ((rc = check_launch(h))) return rc;
   CU(h, cudaStreamSynchronize(h->stream));
   h->host_k = 1;
@@ -1932,7 +1943,22 @@ int sflsqr_debug_state(sflsqr_t* h, double* z, double* x, double* p_ring, double
     if ((rc = check_launch(h))) return rc;
     if (h->n_loc) CU(h, cudaMemcpyAsync(x, P.x, sizeof(double) * h->n_loc, cudaMemcpyDeviceToHost, h->stream));
   }
-  if (z && h->n_loc) CU(h, cudaMemcpyAsync(z, P.z, sizeof(double) * h->n_loc, cudaMemcpyDeviceToHost, h->stream));
+  if (z && h->n_loc) {
+    if (!z_early(h)) {
+      CU(h, cudaMemcpyAsync(z, P.z, sizeof(double) * h->n_loc, cudaMemcpyDeviceToHost, h->stream));
+    } else {
+      // P.z already holds the orthogonalised z of step kd+1 (z_early): form T w_{kd+1} afresh
+      if (h->world > 1) return fail(h, SFLSQR_E_UNSUPPORTED, "debug_state(z) of FLSMR / sFLSMR runs on one rank");
+      double* tz = nullptr;
+      if ((rc = dalloc(h, (void**)&tz, sizeof(double) * h->n_loc, nullptr))) return rc;
+      enqueue_apply(h, 1, nullptr, P.W + (size_t)h->m_loc * kd, 0, 0, tz, SFLSQR_KC_SPMV_T);
+      rc = check_launch(h);
+      if (!rc) cudaMemcpyAsync(z, tz, sizeof(double) * h->n_loc, cudaMemcpyDeviceToHost, h->stream);
+      cudaStreamSynchronize(h->stream);
+      cudaFree(tz);
+      if (rc) return rc;
+    }
+  }
   if (p_ring) {
     if (P.use_pring)
       CU(h, cudaMemcpyAsync(p_ring, P.Pring, sizeof(double) * h->n_loc * P.ell, cudaMemcpyDeviceToHost, h->stream));
