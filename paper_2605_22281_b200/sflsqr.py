@@ -407,3 +407,58 @@ def solver_for_problem(prob, spec, maxit=None, history=HIST_TRUE_RES, use_graph=
     else:
         s.set_precond(spec.precond, spec.p, spec.eps_rel)
     return s
+
+
+def _csr_arrays(M):
+    """(nrows, ncols, rowptr int64, col int32, val float64) of a scipy.sparse matrix or a
+    (rowptr, col, val, shape) tuple."""
+    if hasattr(M, "tocsr"):
+        C = M.tocsr()
+        return (C.shape[0], C.shape[1], np.ascontiguousarray(C.indptr, dtype=np.int64),
+                np.ascontiguousarray(C.indices, dtype=np.int32), np.ascontiguousarray(C.data, dtype=np.float64))
+    rowptr, col, val, shape = M
+    return (int(shape[0]), int(shape[1]), np.ascontiguousarray(rowptr, dtype=np.int64),
+            np.ascontiguousarray(col, dtype=np.int32), np.ascontiguousarray(val, dtype=np.float64))
+
+
+def solve(A, b, method="sflsqr", T=None, maxit=50, window=3, sketch=("sparse", None, 8, 0), precond="identity",
+          p=1.0, eps_rel=1e-3, lowrank=None, tol=0.0, eta=0.0, delta_e=0.0, orth_mode="P", device=0,
+          use_graph=True):
+    """One-call solve through the C ABI (argument marshalling only).
+
+    A: scipy.sparse matrix or (rowptr, col, val, (m, n)); T: the transpose-side operator B ~ A^T
+    in the same forms (None: A^T formed by the library).  method: sflsqr | sflsmr | flsqr | flsmr |
+    lsqr | lsmr.  sketch: ("sparse", d, s_nz, seed) or ("gaussian", d, seed); d = None -> 2 maxit + 1.
+    precond: identity | irn | nonneg | lowrank_rnd (lowrank = dict(H, W, r, oversample, seed)).
+    Returns dict(x, status, k, true_res, sketch_res, info)."""
+    m, n, rp, col, val = _csr_arrays(A)
+    s = SFLSQR(method=method, window=window, maxit=maxit, orth_mode=orth_mode, tol=tol, eta=eta, delta_e=delta_e,
+               device=device, use_graph=use_graph)
+    try:
+        if T is None:
+            s.set_operator(m, n, rp, col, val)
+        else:
+            tn, tm, trp, tcol, tval = _csr_arrays(T)
+            if (tn, tm) != (n, m):
+                raise ValueError("T must be n x m")
+            s.set_operator(m, n, rp, col, val, t=(trp, tcol, tval))
+        if method in ("sflsqr", "sflsmr"):
+            kind = sketch[0]
+            d = sketch[1] if sketch[1] is not None else 2 * maxit + 1
+            if kind == "gaussian":
+                s.set_sketch_gaussian(sketch[2] if len(sketch) > 2 else 0, d)
+            else:
+                s.set_sketch(sketch[3] if len(sketch) > 3 else 0, d, sketch[2])
+        if precond == "lowrank_rnd":
+            lr = lowrank or {}
+            s.set_precond_lowrank(lr["H"], lr["W"], lr["r"], lr.get("oversample", 10), lr.get("seed", 0))
+        else:
+            s.set_precond(precond, p, eps_rel)
+        s.set_rhs(np.ascontiguousarray(b, dtype=np.float64))
+        done, status = s.iterate(maxit)
+        tr, sk = s.get_residual_norms()
+        info = s.get_info()
+        x = s.get_x()
+    finally:
+        s.close()
+    return dict(x=x, status=status, k=info["k_x"], true_res=tr, sketch_res=sk, info=info)

@@ -500,3 +500,16 @@ def test_info_bytes_model_and_delta_e():
               + 8.0 * n * (2 * ell + 3) + 16.0 * n + 8.0 * n * (k - 1) + 8.0 * m * (k + 1))
     assert info["bytes_model"] == pytest.approx(expect, rel=1e-12)
     assert info["delta_e"] == p.delta_e
+
+
+def test_one_call_solve_api_matches_handle_path():
+    import scipy.sparse as sp
+    from paper_2605_22281_b200 import solve
+    p = make_problem(4, N=64, n_angles=45, nb=91)
+    spec = p.solvers[0]
+    A = sp.csr_matrix((p.A.val, p.A.col, p.A.rowptr), shape=(p.m, p.n))
+    B = sp.csr_matrix((p.T.val, p.T.col, p.T.rowptr), shape=(p.n, p.m))
+    out = solve(A, p.b, method="sflsqr", T=B, maxit=12, window=spec.window,
+                sketch=("sparse", spec.d, spec.s_nz, p.sketch_seed), precond="identity")
+    g = _gpu_run(p, spec, maxit=12)
+    assert np.array_equal(out["x"], g["x"]) and np.array_equal(out["true_res"], g["true_res"])
