@@ -453,6 +453,38 @@ void enqueue_apply(sflsqr_t* h, int which, const DevState* st, const double* x, 
   }
 }
 
+// Row-tile GEMV launch: RPT rows per thread, CTAs of RPT * 256 rows, at most kVecBlocks CTAs
+// (grid-stride over the tiles).
+// Measured (configs 3 and 4): 2 rows per thread (512-row tiles, grid-stride over a full grid)
+// beats 4 and 8 (fewer CTAs, less in flight); SFLSQR_GEMV_RPT=4|8 for A/B runs.
+int gemv_rpt(int64_t len) {
+  (void)len;
+  static const int forced = std::getenv("SFLSQR_GEMV_RPT") ? std::atoi(std::getenv("SFLSQR_GEMV_RPT")) : 0;
+  return (forced == 4 || forced == 8) ? forced : 2;
+}
+int gemv_grid(int64_t len, int rpt) {
+  const int64_t tile = (int64_t)rpt * kVecThreads;
+  return (int)std::max<int64_t>(1, std::min<int64_t>((len + tile - 1) / tile, kVecBlocks));
+}
+void launch_xupdate(sflsqr_t* h, int force) {
+  const int rpt = gemv_rpt(h->n_loc), g = gemv_grid(h->n_loc, rpt);
+  if (rpt == 8)
+    k_xupdate<8><<<g, kVecThreads, 0, h->stream>>>(h->P, force);
+  else if (rpt == 4)
+    k_xupdate<4><<<g, kVecThreads, 0, h->stream>>>(h->P, force);
+  else
+    k_xupdate<2><<<g, kVecThreads, 0, h->stream>>>(h->P, force);
+}
+void launch_res(sflsqr_t* h, cudaStream_t s, int fuse_stop) {
+  const int rpt = gemv_rpt(h->m_loc), g = gemv_grid(h->m_loc, rpt);
+  if (rpt == 8)
+    k_res_partial<8><<<g, kVecThreads, 0, s>>>(h->P, fuse_stop);
+  else if (rpt == 4)
+    k_res_partial<4><<<g, kVecThreads, 0, s>>>(h->P, fuse_stop);
+  else
+    k_res_partial<2><<<g, kVecThreads, 0, s>>>(h->P, fuse_stop);
+}
+
 // skbuf = S v (this rank's coordinates), allreduced over ranks.
 int enqueue_sketch(sflsqr_t* h, const DevState* st, const double* v) {
   const int64_t dim_loc = h->P.method == SFLSQR_METHOD_SFLSQR ? h->m_loc : h->n_loc;
@@ -794,7 +826,7 @@ int enqueue_iteration(sflsqr_t* h) {
     CU(h, cudaStreamWaitEvent(h->side, h->ev_w, 0));
     {
       Launch L(h, SFLSQR_KC_RES, m8 * (k + 1));
-      k_res_partial<<<kVecBlocks, kVecThreads, 0, h->side>>>(P, 0);
+      launch_res(h, h->side, 0);
     }
     CU(h, cudaEventRecord(h->ev_join, h->side));
   }
@@ -818,7 +850,7 @@ int enqueue_iteration(sflsqr_t* h) {
   if (P.need_x) {
     {
       Launch L(h, SFLSQR_KC_XUPD, n8 * (k + 1));
-      k_xupdate<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P, 0);
+      launch_xupdate(h, 0);
     }
     if ((rc = coll_allreduce(h, P.scal + P.slot_xmax, 1, true))) return rc;
   }
@@ -827,7 +859,7 @@ int enqueue_iteration(sflsqr_t* h) {
   if (P.want_res && !res_side) {
     {
       Launch L(h, SFLSQR_KC_RES, m8 * (k + 1));
-      k_res_partial<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P, fuse_stop ? 1 : 0);
+      launch_res(h, h->stream, fuse_stop ? 1 : 0);
     }
     if ((rc = coll_allreduce(h, P.scal + P.slot_res, 1, false))) return rc;
   }
@@ -1772,7 +1804,7 @@ int sflsqr_get_x(sflsqr_t* h, double* x, int64_t len, int32_t mem_flags) {
   cudaSetDevice(h->o.device);
   if (h->P.method < SFLSQR_METHOD_LSQR) {  // x_k = Z_k y_k; GKB methods update x in place
     Launch L(h, SFLSQR_KC_XUPD, 8.0 * h->n_loc);
-    k_xupdate<<<kVecBlocks, kVecThreads, 0, h->stream>>>(h->P, 1);
+    launch_xupdate(h, 1);
   }
   if ((rc = check_launch(h))) return rc;
   const bool dev = (mem_flags & SFLSQR_MEM_DEVICE) != 0;
@@ -1938,7 +1970,7 @@ int sflsqr_debug_state(sflsqr_t* h, double* z, double* x, double* p_ring, double
   if (x) {
     {
       Launch L(h, SFLSQR_KC_XUPD, 8.0 * h->n_loc);
-      k_xupdate<<<kVecBlocks, kVecThreads, 0, h->stream>>>(h->P, 1);
+      launch_xupdate(h, 1);
     }
     if ((rc = check_launch(h))) return rc;
     if (h->n_loc) CU(h, cudaMemcpyAsync(x, P.x, sizeof(double) * h->n_loc, cudaMemcpyDeviceToHost, h->stream));

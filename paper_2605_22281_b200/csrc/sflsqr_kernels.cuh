@@ -2059,8 +2059,44 @@ __device__ __forceinline__ void tsgemv_pair(const double* __restrict__ M, int64_
   }
 }
 
+// Row-tile GEMV: a CTA owns RPT * NT consecutive rows of the column-major tall-skinny M and
+// streams the kc columns in order (each column a contiguous RPT * NT * 8-byte segment: long
+// DRAM bursts), two columns and RPT rows per thread in flight; every row accumulates in
+// increasing column order (deterministic).
+template <int NT, int RPT>
+__device__ __forceinline__ void tsgemv_tile(const double* __restrict__ M, int64_t ld, int64_t r0, int64_t len,
+                                            const double* c, int kc, double (&out)[RPT]) {
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) out[u] = 0.0;
+  int j = 0;
+  for (; j + 2 <= kc; j += 2) {
+    const double c0 = c[j], c1 = c[j + 1];
+    const double* m0 = M + (int64_t)j * ld;
+    const double* m1 = m0 + ld;
+    double a[RPT], b[RPT];
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+      const int64_t r = r0 + threadIdx.x + (int64_t)u * NT;
+      a[u] = r < len ? __ldcs(m0 + r) : 0.0;
+      b[u] = r < len ? __ldcs(m1 + r) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) out[u] = fma(b[u], c1, fma(a[u], c0, out[u]));
+  }
+  if (j < kc) {
+    const double c0 = c[j];
+    const double* m0 = M + (int64_t)j * ld;
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+      const int64_t r = r0 + threadIdx.x + (int64_t)u * NT;
+      if (r < len) out[u] = fma(__ldcs(m0 + r), c0, out[u]);
+    }
+  }
+}
+
 // a8: x_k = Z_k y_k (Alg. 1 L504 / Alg. 2), plus the partial max needed by
 // tau_{k+1} (|x| for IRN, x_+ for NONNEG).  HBM-bound (0.25 flop/B).
+template <int RPT>
 __global__ void __launch_bounds__(kVecThreads) k_xupdate(Params P, int force) {
   __shared__ double sh[33];
   __shared__ double ys[kMaxD];
@@ -2071,15 +2107,17 @@ __global__ void __launch_bounds__(kVecThreads) k_xupdate(Params P, int force) {
   __syncthreads();
   double mx = -INFINITY;
   const bool absmax = P.precond == 1;
-  for (int64_t i2 = 2 * ((int64_t)blockIdx.x * kVecThreads + threadIdx.x); i2 < P.n;
-       i2 += 2 * (int64_t)gridDim.x * kVecThreads) {
-    double a0, a1;
-    tsgemv_pair(P.Z, P.n, P.n, i2, ys, kx, a0, a1);
-    P.x[i2] = a0;
-    mx = fmax(mx, absmax ? fabs(a0) : a0);
-    if (i2 + 1 < P.n) {
-      P.x[i2 + 1] = a1;
-      mx = fmax(mx, absmax ? fabs(a1) : a1);
+  constexpr int64_t tile = (int64_t)RPT * kVecThreads;
+  for (int64_t r0 = (int64_t)blockIdx.x * tile; r0 < P.n; r0 += (int64_t)gridDim.x * tile) {
+    double o[RPT];
+    tsgemv_tile<kVecThreads, RPT>(P.Z, P.n, r0, P.n, ys, kx, o);
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+      const int64_t r = r0 + threadIdx.x + (int64_t)u * kVecThreads;
+      if (r < P.n) {
+        P.x[r] = o[u];
+        mx = fmax(mx, absmax ? fabs(o[u]) : o[u]);
+      }
     }
   }
   mx = block_max<kVecThreads>(mx, sh);
@@ -2113,6 +2151,7 @@ __device__ __forceinline__ void stop_body(const Params& P, DevState* st, double 
 // (eq. FGK: A Z_k = W_{k+1} H_{k+1,k}, w_1 = b/beta).  Every block forms g in
 // shared memory from the band of H; fuse_stop (one rank): the last block also runs
 // the stop tests.
+template <int RPT>
 __global__ void __launch_bounds__(kVecThreads) k_res_partial(Params P, int fuse_stop) {
   __shared__ double sh[33];
   __shared__ double gs[kMaxD];
@@ -2127,12 +2166,12 @@ __global__ void __launch_bounds__(kVecThreads) k_res_partial(Params P, int fuse_
   }
   __syncthreads();
   double acc2 = 0.0;
-  for (int64_t i2 = 2 * ((int64_t)blockIdx.x * kVecThreads + threadIdx.x); i2 < P.m;
-       i2 += 2 * (int64_t)gridDim.x * kVecThreads) {
-    double r0, r1;
-    tsgemv_pair(P.W, P.m, P.m, i2, gs, kk, r0, r1);
-    acc2 = fma(r0, r0, acc2);
-    acc2 = fma(r1, r1, acc2);  // r1 = 0 past the end
+  constexpr int64_t tile = (int64_t)RPT * kVecThreads;
+  for (int64_t r0 = (int64_t)blockIdx.x * tile; r0 < P.m; r0 += (int64_t)gridDim.x * tile) {
+    double o[RPT];
+    tsgemv_tile<kVecThreads, RPT>(P.W, P.m, r0, P.m, gs, kk, o);
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) acc2 = fma(o[u], o[u], acc2);  // rows past the end are 0
   }
   acc2 = block_sum<kVecThreads>(acc2, sh);
   if (threadIdx.x == 0) P.part[(size_t)P.slot_res * kVecBlocks + blockIdx.x] = acc2;
