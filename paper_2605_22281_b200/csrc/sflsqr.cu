@@ -453,6 +453,16 @@ void enqueue_apply(sflsqr_t* h, int which, const DevState* st, const double* x, 
   }
 }
 
+// Grid of the fused windowed-orthogonalisation and normalisation kernels: about 8 elements per
+// thread, at least one CTA per SM, at most kVecBlocks (the partial-sum stride); short vectors
+// then pay a 148-way instead of a 592-way last-block reduction.  SFLSQR_VEC_GRID=full: always
+// kVecBlocks (A/B runs).
+int vec_grid(int64_t len) {
+  static const bool full = std::getenv("SFLSQR_VEC_GRID") && std::strcmp(std::getenv("SFLSQR_VEC_GRID"), "full") == 0;
+  if (full) return kVecBlocks;
+  return (int)std::max<int64_t>(148, std::min<int64_t>((len + 8 * kVecThreads - 1) / (8 * kVecThreads), kVecBlocks));
+}
+
 // Row-tile GEMV launch: RPT rows per thread, CTAs of RPT * 256 rows, at most kVecBlocks CTAs
 // (grid-stride over the tiles).
 // Measured (configs 3 and 4): 2 rows per thread (512-row tiles, grid-stride over a full grid)
@@ -563,12 +573,12 @@ int enqueue_orth(sflsqr_t* h, int side, int koff) {
   if (P.orth_alg == ORTH_FUSED) {
     {
       Launch L(h, SFLSQR_KC_ORTH, v8 * (1 + J));
-      k_orth_dots<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P, side, koff);
+      k_orth_dots<<<vec_grid(side == 0 ? h->n_loc : h->m_loc), kVecThreads, 0, h->stream>>>(P, side, koff);
     }
     if ((rc = coll_allreduce(h, P.scal + slot_f, kFuseAcc, false))) return rc;
     {
       Launch L(h, SFLSQR_KC_ORTH, v8 * (2 + J));
-      k_orth_axpy<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P, side, koff);
+      k_orth_axpy<<<vec_grid(side == 0 ? h->n_loc : h->m_loc), kVecThreads, 0, h->stream>>>(P, side, koff);
     }
     return coll_allreduce(h, P.scal + slot_out, 1, false);
   }
@@ -780,7 +790,7 @@ int enqueue_iteration(sflsqr_t* h) {
   // a1 end + a2: normalise, tau, store z_k
   if (!coop) {
     Launch L(h, SFLSQR_KC_TAU, n8 * (2 + (P.use_pring ? 1 : 0) + (P.precond ? 1 : 0)));
-    k_finish_z<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P);
+    k_finish_z<<<vec_grid(h->n_loc), kVecThreads, 0, h->stream>>>(P);
   }
   if (P.precond == SFLSQR_PRECOND_LOWRANK_RND && (rc = enqueue_lowrank(h))) return rc;
   // a3: w = A z_k  (z_k = Z[:, k-1]; all-gathered across ranks when sharded)
@@ -811,7 +821,7 @@ int enqueue_iteration(sflsqr_t* h) {
   if (!coop) {
     if ((rc = enqueue_orth(h, 1, 0))) return rc;
     Launch L(h, SFLSQR_KC_ORTH, 2 * m8);
-    k_finish_w<<<kVecBlocks, kVecThreads, 0, h->stream>>>(P);
+    k_finish_w<<<vec_grid(h->m_loc), kVecThreads, 0, h->stream>>>(P);
   }
   if (fork_ls && P.method == SFLSQR_METHOD_FLSQR && (rc = enqueue_ls(h, true))) return rc;
   // a9 (W-path residual) on the side stream too, after the LS and a5, overlapped with a6: it
