@@ -1190,21 +1190,40 @@ __global__ void __launch_bounds__(kVecThreads) k_cgs_update(Params P, int side, 
         P.H[(int64_t)row + (int64_t)(kk - 1) * P.ldh] = cf;
     }
   }
+  // row tiles of 2 x kVecThreads rows, two rows per thread, window vectors in order (the same
+  // per-row operation order as a one-row-per-thread loop), 4 vectors x 2 rows loads in flight
   double acc = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * kVecThreads + threadIdx.x; i < len; i += (int64_t)gridDim.x * kVecThreads) {
-    double vi = v[i];
+  constexpr int64_t tile = 2 * kVecThreads;
+  for (int64_t r0 = (int64_t)blockIdx.x * tile; r0 < len; r0 += (int64_t)gridDim.x * tile) {
+    const int64_t i0 = r0 + threadIdx.x, i1 = i0 + kVecThreads;
+    const bool ok0 = i0 < len, ok1 = i1 < len;
+    double a = ok0 ? v[i0] : 0.0, b = ok1 ? v[i1] : 0.0;
     int j = 0;
     for (; j + 4 <= J; j += 4) {
-      const double q0 = __ldg(qp[j] + i), q1 = __ldg(qp[j + 1] + i);
-      const double q2 = __ldg(qp[j + 2] + i), q3 = __ldg(qp[j + 3] + i);
-      vi = fma(-cs[j], q0, vi);
-      vi = fma(-cs[j + 1], q1, vi);
-      vi = fma(-cs[j + 2], q2, vi);
-      vi = fma(-cs[j + 3], q3, vi);
+      double qa[4], qb[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        qa[u] = ok0 ? __ldg(qp[j + u] + i0) : 0.0;
+        qb[u] = ok1 ? __ldg(qp[j + u] + i1) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a = fma(-cs[j + u], qa[u], a);
+        b = fma(-cs[j + u], qb[u], b);
+      }
     }
-    for (; j < J; ++j) vi = fma(-cs[j], __ldg(qp[j] + i), vi);
-    v[i] = vi;
-    acc = fma(vi, vi, acc);
+    for (; j < J; ++j) {
+      if (ok0) a = fma(-cs[j], __ldg(qp[j] + i0), a);
+      if (ok1) b = fma(-cs[j], __ldg(qp[j] + i1), b);
+    }
+    if (ok0) {
+      v[i0] = a;
+      acc = fma(a, a, acc);
+    }
+    if (ok1) {
+      v[i1] = b;
+      acc = fma(b, b, acc);
+    }
   }
   if (stage == 0) return;
   acc = block_sum<kVecThreads>(acc, sh);
