@@ -513,3 +513,17 @@ def test_one_call_solve_api_matches_handle_path():
                 sketch=("sparse", spec.d, spec.s_nz, p.sketch_seed), precond="identity")
     g = _gpu_run(p, spec, maxit=12)
     assert np.array_equal(out["x"], g["x"]) and np.array_equal(out["true_res"], g["true_res"])
+
+
+@pytest.mark.parametrize("method", ["sflsqr", "sflsmr"])
+def test_tol_stop_matches_oracle(method):
+    import dataclasses
+    p = make_problem(1)
+    spec = [s for s in p.solvers if s.method == method][0]
+    full = solve_problem(p, spec, eta=0.0)
+    rel = np.array(full.sketch_res) / np.linalg.norm(full.rhs)
+    spec_t = dataclasses.replace(spec, tol=float(rel[9]) * (1 + 1e-7))
+    r = solve_problem(p, spec_t, eta=0.0)
+    assert r.status == 2
+    g = _gpu_run(p, spec_t, eta=0.0)
+    _compare(g, r)

@@ -299,3 +299,18 @@ def test_corollary_expected_residual_gaussian_sketch():
     expect = k / (s - k - 1)                        # 0.4615
     assert abs(mean - expect) < 4 * se + 0.02, (mean, se, expect)
     assert abs(mean - s / (s - k - 1)) > 10 * se     # the printed constant (1.54) is rejected
+
+
+@pytest.mark.parametrize("method", ["sflsqr", "sflsmr"])
+def test_tol_stop_index(method):
+    # Alg. 1 L498 / Alg. 2 L798 (reading R3): stop at the first k with ||rhs - M y_k|| < tol ||rhs||
+    from oracle.sflsqr import TOL
+    A, b, _ = _dense_problem(120, 80, 1e4, 13, noise=0.05)
+    sk = SparseSignSketch(8, 61, 4, 120 if method == "sflsqr" else 80)
+    full = solve(DenseOperator(A), b, method, maxit=30, window=2, sketch=sk, precond="irn")
+    rel = np.array(full.sketch_res) / np.linalg.norm(full.rhs)
+    tol = float(rel[11]) * (1 + 1e-9)
+    hits = [k + 1 for k, v in enumerate(rel) if v < tol]
+    stop = solve(DenseOperator(A), b, method, maxit=30, window=2, sketch=sk, precond="irn", tol=tol)
+    assert stop.status == TOL and stop.k == hits[0]
+    np.testing.assert_array_equal(stop.x, full.xs[hits[0] - 1])
