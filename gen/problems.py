@@ -442,29 +442,35 @@ class ShardProblem:
     solvers: list
 
 
-def ct_row_nnz(config_index: int, nthreads: int = 0):
-    """Row lengths of A (and B when unmatched) for the nnz-balanced partition."""
+def _ct_geometry(cfg, N=None, n_angles=None, nb=None):
+    Nimg = N or cfg["N"]
+    tile = cfg.get("tile", 0) if Nimg % max(cfg.get("tile", 1), 1) == 0 else 0
+    return Nimg, n_angles or cfg["n_angles"], nb or cfg["nb"], tile
+
+
+def ct_row_nnz(config_index: int, nthreads: int = 0, N=None, n_angles=None, nb=None):
+    """Row lengths of A (and B when unmatched) for the nnz-balanced partition (geometry overrides
+    as in make_problem)."""
     cfg = CONFIGS[config_index]
-    tile = cfg.get("tile", 0)
-    a = row_nnz("siddon", cfg["N"], cfg["n_angles"], cfg["nb"], nthreads, tile)
-    t = None if cfg["matched"] else row_nnz("pixbp", cfg["N"], cfg["n_angles"], cfg["nb"], nthreads, tile)
+    Nimg, na, nbins, tile = _ct_geometry(cfg, N, n_angles, nb)
+    a = row_nnz("siddon", Nimg, na, nbins, nthreads, tile)
+    t = None if cfg["matched"] else row_nnz("pixbp", Nimg, na, nbins, nthreads, tile)
     return a, t
 
 
 def make_ct_shard(config_index: int, a_rows: tuple, t_rows: Optional[tuple], allreduce_sum,
-                  nthreads: int = 0) -> ShardProblem:
+                  nthreads: int = 0, N=None, n_angles=None, nb=None) -> ShardProblem:
     """The rows [a_rows) of A (and [t_rows) of B) of make_problem(config_index), and the
     matching slice of b = A x_true + e.  The same seeded streams as make_problem;
     ||A x_true|| is the allreduce of the ranks' partial squares (allreduce_sum(float))."""
     cfg = CONFIGS[config_index]
     if cfg["kind"] != "ct":
         raise ValueError("sharded generation is for the CT configs")
-    N, na, nb = cfg["N"], cfg["n_angles"], cfg["nb"]
+    N, na, nb, tile = _ct_geometry(cfg, N, n_angles, nb)
     ss = np.random.SeedSequence(MASTER_SEED + config_index)
     s_A, s_x, s_e = ss.spawn(3)
     rx, re = (np.random.Generator(np.random.PCG64(s)) for s in (s_x, s_e))
     m, n = na * nb, N * N
-    tile = cfg.get("tile", 0)
     A_loc = _rows_block("siddon", N, na, nb, a_rows[0], a_rows[1], nthreads, tile)
     T_loc = None
     t_mode = "build"

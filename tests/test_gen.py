@@ -172,3 +172,32 @@ def test_ct_recipe_reduced():
     assert p.x_true.min() >= 0 and p.x_true.max() > 0
     p4 = make_problem(4, N=48, n_angles=30, nb=69)
     assert p4.t_mode == "given" and p4.T.nrows == 48 * 48 and p4.T.ncols == 30 * 69
+
+
+@pytest.mark.parametrize("cfg,world", [(3, 2), (4, 3)])
+def test_ct_shards_reassemble_the_problem(cfg, world):
+    # the multi-GPU bench's per-rank generation (make_ct_shard) must produce exactly the rows of
+    # make_problem's operators and the matching slices of b
+    from gen.problems import ct_row_nnz, make_ct_shard
+    from paper_2605_22281_b200.shard import balanced_row_blocks
+    geo = dict(N=48, n_angles=33, nb=71)
+    p = make_problem(cfg, **geo)
+    a_cnt, t_cnt = ct_row_nnz(cfg, **geo)
+    np.testing.assert_array_equal(a_cnt, np.diff(p.A.rowptr))
+    ab = balanced_row_blocks(np.concatenate([[0], np.cumsum(a_cnt)]), world)
+    tb = None if t_cnt is None else balanced_row_blocks(np.concatenate([[0], np.cumsum(t_cnt)]), world)
+    # the ranks' all-reduce of their partial ||A x_true||^2, emulated by the global value
+    ax2 = float((p.b - p.e) @ (p.b - p.e))
+    shards = [make_ct_shard(cfg, ab[g], None if tb is None else tb[g], lambda v: ax2, **geo) for g in range(world)]
+    for g, sh in enumerate(shards):
+        r0, r1 = ab[g]
+        s, e = p.A.rowptr[r0], p.A.rowptr[r1]
+        np.testing.assert_array_equal(sh.A_loc.col, p.A.col[s:e])
+        np.testing.assert_array_equal(sh.A_loc.val, p.A.val[s:e])
+        np.testing.assert_allclose(sh.b_loc, p.b[r0:r1], rtol=1e-13, atol=1e-13 * np.abs(p.b).max())
+        assert abs(sh.delta_e - p.delta_e) <= 1e-12 * p.delta_e
+        if tb is not None:
+            t0, t1 = tb[g]
+            s, e = p.T.rowptr[t0], p.T.rowptr[t1]
+            np.testing.assert_array_equal(sh.T_loc.col, p.T.col[s:e])
+            np.testing.assert_array_equal(sh.T_loc.val, p.T.val[s:e])
