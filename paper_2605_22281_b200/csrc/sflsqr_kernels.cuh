@@ -1034,11 +1034,35 @@ __device__ __forceinline__ void orth_axpy_block(const Params& P, int side, int J
 #pragma unroll
   for (int j = 0; j < kFuseJ; ++j) q[j] = j < J ? mgs_basis(P, side, j0 + j) : nullptr;
   double acc = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < len; i += (int64_t)gridDim.x * NT) {
+  // two elements per iteration (12 independent loads in flight); the window vectors are
+  // read-only in this kernel (read through the non-coherent path, so they may be hoisted)
+  const int64_t stride = (int64_t)gridDim.x * NT;
+  int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x;
+  for (; i + stride < len; i += 2 * stride) {
+    const int64_t i1 = i + stride;
+    double a = v[i], b = v[i1];
+    double qa[kFuseJ], qb[kFuseJ];
+#pragma unroll
+    for (int j = 0; j < kFuseJ; ++j) {
+      qa[j] = j < J ? __ldg(q[j] + i) : 0.0;
+      qb[j] = j < J ? __ldg(q[j] + i1) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < kFuseJ; ++j)
+      if (j < J) {
+        a = fma(-c[j], qa[j], a);
+        b = fma(-c[j], qb[j], b);
+      }
+    v[i] = a;
+    v[i1] = b;
+    acc = fma(a, a, acc);
+    acc = fma(b, b, acc);
+  }
+  if (i < len) {
     double vi = v[i];
 #pragma unroll
     for (int j = 0; j < kFuseJ; ++j)
-      if (j < J) vi = fma(-c[j], q[j][i], vi);
+      if (j < J) vi = fma(-c[j], __ldg(q[j] + i), vi);
     v[i] = vi;
     acc = fma(vi, vi, acc);
   }
@@ -1259,8 +1283,9 @@ __device__ __forceinline__ bool finish_z_body(const Params& P, DevState* st, int
   if (mode == 3) {
     // p_k stays in P.z (and the P ring); k_lr_range .. k_lr_recon form z_k = tau_r(p_k) into Z[:, k-1]
     double* pr = P.use_pring ? P.Pring + (int64_t)((k - 1) % P.ell) * P.n : nullptr;
+    const double it = 1.0 / t;
     for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < P.n; i += (int64_t)gridDim.x * NT) {
-      const double p = P.z[i] / t;
+      const double p = P.z[i] * it;
       P.z[i] = p;
       if (pr) pr[i] = p;
     }
@@ -1279,8 +1304,9 @@ __device__ __forceinline__ bool finish_z_body(const Params& P, DevState* st, int
   }
   double* zk = P.Z + (int64_t)(k - 1) * P.n;
   double* pr = P.use_pring ? P.Pring + (int64_t)((k - 1) % P.ell) * P.n : nullptr;
+  const double it = 1.0 / t;  // one division; the elements take a multiply
   for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < P.n; i += (int64_t)gridDim.x * NT) {
-    const double p = P.z[i] / t;
+    const double p = P.z[i] * it;
     double zi = p;
     if (mode == 1) {
       const double xi = P.x[i];
@@ -1696,13 +1722,14 @@ __global__ void __launch_bounds__(256) k_lr_recon(Params P) {
 template <int NT>
 __device__ __forceinline__ void finish_w_body(const Params& P, DevState* st, int k, double hn, double win) {
   const bool brk = (hn == 0.0 || hn <= 1e-14 * win);
+  const double ihn = brk ? 0.0 : 1.0 / hn;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     st->wbreak = brk ? 1 : 0;
     P.H[(int64_t)k + (int64_t)(k - 1) * P.ldh] = brk ? 0.0 : hn;
   }
   double* wk1 = P.W + (int64_t)k * P.m;
   for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < P.m; i += (int64_t)gridDim.x * NT) {
-    const double wv = brk ? 0.0 : P.w[i] / hn;
+    const double wv = brk ? 0.0 : P.w[i] * ihn;
     wk1[i] = wv;
     if (P.wsend) P.wsend[i] = wv;
     if (P.p2p_w) {  // ROWSHARD all-gather of w_{k+1} as direct peer stores
