@@ -485,6 +485,15 @@ void launch_xupdate(sflsqr_t* h, int force) {
   else
     k_xupdate<2><<<g, kVecThreads, 0, h->stream>>>(h->P, force);
 }
+void k_xupdate_launch_side(sflsqr_t* h) {
+  const int rpt = gemv_rpt(h->n_loc), g = gemv_grid(h->n_loc, rpt);
+  if (rpt == 8)
+    k_xupdate<8><<<g, kVecThreads, 0, h->side>>>(h->P, 0);
+  else if (rpt == 4)
+    k_xupdate<4><<<g, kVecThreads, 0, h->side>>>(h->P, 0);
+  else
+    k_xupdate<2><<<g, kVecThreads, 0, h->side>>>(h->P, 0);
+}
 void launch_res(sflsqr_t* h, cudaStream_t s, int fuse_stop) {
   const int rpt = gemv_rpt(h->m_loc), g = gemv_grid(h->m_loc, rpt);
   if (rpt == 8)
@@ -686,13 +695,16 @@ int enqueue_ls(sflsqr_t* h, bool forked) {
 // FLSMR (needs column k+1 of T at step k) and sFLSMR (overlaps it with the LS) run the z-side
 // orthogonalisation of step k+1 at the end of step k (and of step 1 in set_rhs); step k then
 // starts with the normalisation.  Same arithmetic, earlier in the stream.
+// sFLSQR with an x-dependent tau on one rank does the same so that the x update runs on the
+// side stream (after the LS) while the main stream orthogonalises the next z.
 bool z_early(sflsqr_t* h) {
-  return h->P.method == SFLSQR_METHOD_FLSMR || h->P.method == SFLSQR_METHOD_SFLSMR;
+  return h->P.method == SFLSQR_METHOD_FLSMR || h->P.method == SFLSQR_METHOD_SFLSMR ||
+         (h->P.method == SFLSQR_METHOD_SFLSQR && h->P.need_x && h->world == 1 && h->side);
 }
 
 bool use_coop(sflsqr_t* h) {
   return h->coop_grid > 0 && h->world == 1 && h->P.orth_alg == ORTH_FUSED && h->P.method == SFLSQR_METHOD_SFLSQR &&
-         h->sk_kind == 0;
+         h->sk_kind == 0 && !z_early(h);
 }
 
 int launch_coop(sflsqr_t* h, void (*kern)(Params), double bytes) {
@@ -824,6 +836,16 @@ int enqueue_iteration(sflsqr_t* h) {
     k_finish_w<<<vec_grid(h->m_loc), kVecThreads, 0, h->stream>>>(P);
   }
   if (fork_ls && P.method == SFLSQR_METHOD_FLSQR && (rc = enqueue_ls(h, true))) return rc;
+  // a8 on the side stream after the LS (sFLSQR with an x-dependent tau, one rank): the main
+  // stream meanwhile runs the T product and the next z side (z_early); joined before the stop
+  const bool xupd_side = fork_ls && P.need_x && P.method == SFLSQR_METHOD_SFLSQR && z_early(h);
+  if (xupd_side) {
+    {
+      Launch L(h, SFLSQR_KC_XUPD, n8 * (k + 1));
+      k_xupdate_launch_side(h);
+    }
+    CU(h, cudaEventRecord(h->ev_join, h->side));
+  }
   // a9 (W-path residual) on the side stream too, after the LS and a5, overlapped with a6: it
   // streams W while the T product leaves HBM bandwidth unused.  The stop test then runs on the
   // main stream after the join (the T product reads st->k, which the stop test advances).
@@ -857,7 +879,7 @@ int enqueue_iteration(sflsqr_t* h) {
     return rc;
   }
   // a8: x_k = Z_k y_k (needed by tau_{k+1})
-  if (P.need_x) {
+  if (P.need_x && !xupd_side) {
     {
       Launch L(h, SFLSQR_KC_XUPD, n8 * (k + 1));
       launch_xupdate(h, 0);
