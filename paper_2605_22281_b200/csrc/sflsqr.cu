@@ -699,7 +699,8 @@ int enqueue_ls(sflsqr_t* h, bool forked) {
 // side stream (after the LS) while the main stream orthogonalises the next z.
 bool z_early(sflsqr_t* h) {
   return h->P.method == SFLSQR_METHOD_FLSMR || h->P.method == SFLSQR_METHOD_SFLSMR ||
-         (h->P.method == SFLSQR_METHOD_SFLSQR && h->P.need_x && h->world == 1 && h->side);
+         ((h->P.method == SFLSQR_METHOD_SFLSQR || h->P.method == SFLSQR_METHOD_FLSQR) && h->P.need_x &&
+          h->world == 1 && h->side);
 }
 
 bool use_coop(sflsqr_t* h) {
@@ -836,9 +837,9 @@ int enqueue_iteration(sflsqr_t* h) {
     k_finish_w<<<vec_grid(h->m_loc), kVecThreads, 0, h->stream>>>(P);
   }
   if (fork_ls && P.method == SFLSQR_METHOD_FLSQR && (rc = enqueue_ls(h, true))) return rc;
-  // a8 on the side stream after the LS (sFLSQR with an x-dependent tau, one rank): the main
+  // a8 on the side stream after the LS (sFLSQR / FLSQR with an x-dependent tau, one rank): the main
   // stream meanwhile runs the T product and the next z side (z_early); joined before the stop
-  const bool xupd_side = fork_ls && P.need_x && P.method == SFLSQR_METHOD_SFLSQR && z_early(h);
+  const bool xupd_side = fork_ls && P.need_x && z_early(h);
   if (xupd_side) {
     {
       Launch L(h, SFLSQR_KC_XUPD, n8 * (k + 1));
