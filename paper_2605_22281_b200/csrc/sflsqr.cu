@@ -742,18 +742,19 @@ int enqueue_lowrank(sflsqr_t* h) {
     Launch L(h, SFLSQR_KC_TAU, 8.0 * l * P.lr_H * 2);
     k_lr_qr<<<1, 1024, kLrQrSmem, h->stream>>>(P);
   } else {
-    // sCholQR3 on the range Y (copied into lr_Q, factored in place)
-    CU(h, cudaMemcpyAsync(P.lr_Q, P.lr_Y, sizeof(double) * P.lr_l * P.lr_H, cudaMemcpyDeviceToDevice, h->stream));
-    const int gg = (int)std::max<int64_t>(1, ((int64_t)P.lr_l * P.lr_l + 7) / 8);
-    const int gs = (int)std::max<int64_t>(1, std::min<int64_t>((P.lr_H + 255) / 256, 148 * 4));
+    // sCholQR3 on the range Y: lr_Y -> lr_Q -> lr_Y -> lr_Q
+    const int gg = (int)std::max<int64_t>(1, ((int64_t)P.lr_l * P.lr_l + kLrGramThreads / 32 - 1) / (kLrGramThreads / 32));
+    const int ga = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)P.lr_H * P.lr_l + 255) / 256, 148 * 4));
     for (int round = 0; round < 3; ++round) {
+      const double* in = (round == 1) ? P.lr_Q : P.lr_Y;
+      double* out = (round == 1) ? P.lr_Y : P.lr_Q;
       {
         Launch L(h, SFLSQR_KC_TAU, 8.0 * l * P.lr_H);
-        k_lr_ygram<<<gg, 256, 0, h->stream>>>(P);
+        k_lr_ygram<<<gg, kLrGramThreads, 0, h->stream>>>(P, in, round == 0 ? 1 : 0);
       }
       {
         Launch L(h, SFLSQR_KC_TAU, 16.0 * l * P.lr_H);
-        k_lr_cholsolve<<<gs, 256, 0, h->stream>>>(P, round == 0 ? 1 : 0);
+        k_lr_rapply<<<ga, 256, 0, h->stream>>>(P, in, out);
       }
     }
   }
@@ -770,7 +771,7 @@ int enqueue_lowrank(sflsqr_t* h) {
   }
   {
     Launch L(h, SFLSQR_KC_TAU, 16.0 * l * l);
-    k_lr_eig<<<1, 1024, kLrEigSmem, h->stream>>>(P);
+    k_lr_eig<<<1, 256, kLrEigSmem, h->stream>>>(P);
   }
   {
     Launch L(h, SFLSQR_KC_TAU, 16.0 * l * P.lr_H);

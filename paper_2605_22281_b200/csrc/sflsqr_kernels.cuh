@@ -24,7 +24,7 @@ constexpr int kFuseAcc = 1 + kFuseJ + kFuseJ * (kFuseJ - 1) / 2;  // ||v||^2, do
 constexpr int kCgsChunk = 2048;           // CGS2 dot kernel: rows of v staged in shared memory per step
 enum CounterIdx {
   CTR_BETA = 0, CTR_ZDOTS, CTR_ZAXPY, CTR_WDOTS, CTR_WAXPY, CTR_XMAX, CTR_RES, CTR_CGS,
-  CTR_GKB_A, CTR_GKB_T, CTR_GKB_UPD, CTR_COUNT
+  CTR_GKB_A, CTR_GKB_T, CTR_GKB_UPD, CTR_LRG, CTR_COUNT
 };
 constexpr int kGkbState = 24;             // carried LSQR / LSMR scalars, double-buffered by k parity
 enum OrthAlg { ORTH_FUSED = 0, ORTH_MGS = 1, ORTH_CGS2 = 2 };
@@ -1421,19 +1421,33 @@ __global__ void __launch_bounds__(1024) k_lr_qr(Params P) {
 // Q = orth(Y) by shifted Cholesky QR, three rounds (sCholQR3): G = Y^T Y (+ shift in round 1),
 // R = chol(G), Y <- Y R^{-1}.  Same Q as Gram-Schmidt in exact arithmetic (Y = QR with R upper
 // triangular, positive diagonal), orthogonal to working precision after the third round even
-// for numerically rank-deficient Y (the shift keeps G + sI positive definite); all the work is
-// parallel: a Gram kernel (one warp per entry) and a solve kernel (one thread per row, each
-// block factors the l x l matrix redundantly in shared memory).
-__global__ void __launch_bounds__(256) k_lr_ygram(Params P) {
+// for numerically rank-deficient Y (the shift keeps G + sI positive definite).  Per round two
+// kernels: k_lr_ygram (one warp per Gram entry; the last CTA to finish factors G and inverts R
+// into lr_PB[l*l .. 2*l*l)) and k_lr_rapply (Q = Y R^{-1}, one thread per entry).
+//
+// Factor + inverse in the last CTA, one barrier per pivot: symmetric Gaussian elimination
+// G = L D L^T applied to [G | I] (the right block becomes L^{-1}); R = D^{1/2} L^T is kept as the
+// scaled upper rows of S (R_cb = S[c][b], b > c; 1 / R_cc in rinv) and L^{-1} in S's strict lower
+// triangle, so R^{-1} = L^{-T} D^{-1/2}: X_ij = S[j][i] rinv[j] (i < j), X_ii = rinv[i].  Phase c
+// (row c of R final): S[a][b] -= R_ca R_cb (c < a <= b), row c+1 scaled on the fly (its new pivot
+// formed redundantly by every thread that needs it; the stale diagonal is never written), and the
+// L^{-1} rows a > c updated, W_ab -= (R_ca / R_cc) W_cb (b <= c, W_cc = 1).  Threads are a 16 x 64
+// grid: column b = tid % 64 (l <= 64), rows a = c + 1 + tid / 64 + 16 k.
+constexpr int kLrGramThreads = 1024;
+__global__ void __launch_bounds__(kLrGramThreads) k_lr_ygram(Params P, const double* __restrict__ Y, int shifted) {
+  __shared__ double S[kLrMaxL][kLrMaxL + 1];
+  __shared__ double rinv[kLrMaxL];
+  __shared__ double shv;
+  __shared__ int s_last;
   if (P.st->done) return;
   const int H = P.lr_H, l = P.lr_l;
-  const int lane = threadIdx.x & 31;
-  for (int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wg < (int64_t)l * l;
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int64_t wg = ((int64_t)blockIdx.x * blockDim.x + tid) >> 5; wg < (int64_t)l * l;
        wg += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int a = (int)(wg / l), b = (int)(wg % l);
     if (b < a) continue;
-    const double* ya = P.lr_Q + (int64_t)a * H;
-    const double* yb = P.lr_Q + (int64_t)b * H;
+    const double* ya = Y + (int64_t)a * H;
+    const double* yb = Y + (int64_t)b * H;
     double acc0 = 0.0, acc1 = 0.0;
     int i = lane;
     for (; i + 32 < H; i += 64) {
@@ -1447,63 +1461,106 @@ __global__ void __launch_bounds__(256) k_lr_ygram(Params P) {
       P.lr_PB[(int64_t)b * l + a] = v;
     }
   }
-}
-
-__global__ void __launch_bounds__(256) k_lr_cholsolve(Params P, int shifted) {
-  __shared__ double R[kLrMaxL][kLrMaxL + 1];
-  __shared__ double rinv[kLrMaxL];
-  if (P.st->done) return;
-  const int H = P.lr_H, l = P.lr_l;
-  for (int e = threadIdx.x; e < l * l; e += blockDim.x) R[e / l][e % l] = P.lr_PB[e];
+  __threadfence();
   __syncthreads();
-  if (shifted) {  // s = 11 (H l + l (l + 1)) u ||Y||_F^2 >= the sCholQR3 shift bound
-    __shared__ double shv;
-    if (threadIdx.x < 32) {
-      double tr = 0.0;
-      for (int a = threadIdx.x; a < l; a += 32) tr += R[a][a];
-      tr = warp_sum(tr);
-      if (threadIdx.x == 0) shv = 11.0 * ((double)H * l + (double)l * (l + 1)) * 1.1102230246251565e-16 * tr;
-    }
-    __syncthreads();
-    if (threadIdx.x < l) R[threadIdx.x][threadIdx.x] += shv;
-    __syncthreads();
+  if (tid == 0) s_last = (atomicAdd(P.ctr + CTR_LRG, 1) == (int)gridDim.x - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int e = tid; e < l * l; e += blockDim.x) {  // upper triangle of G; W = L^{-1} starts as I (strict lower 0)
+    const int a = e / l, b = e % l;
+    S[a][b] = a <= b ? __ldcg(P.lr_PB + e) : 0.0;
   }
-  // right-looking Cholesky, upper factor R (R^T R = G), the whole block on each trailing update
-  for (int c = 0; c < l; ++c) {
-    if (threadIdx.x == 0) {
-      const double d = sqrt(fmax(R[c][c], 1e-300));
-      R[c][c] = d;
-      rinv[c] = 1.0 / d;
+  double* X = P.lr_PB + (int64_t)l * l;  // R^{-1}, row-major l x l (zeros below the diagonal)
+  if (!shifted) {
+    // Y already nearly orthonormal (rounds 2 and 3): G = I + E with max |E_ab| <= 1e-9 has
+    // R = I + F + O(E^2), F = triu(E, 1) + diag(E) / 2, so R^{-1} = I - F to working precision,
+    // with no serial factorisation
+    __shared__ double shm[33];
+    double em = 0.0;
+    for (int e = tid; e < l * l; e += blockDim.x) {
+      const int a = e / l, b = e % l;
+      if (a <= b) em = fmax(em, fabs(S[a][b] - (a == b ? 1.0 : 0.0)));
     }
     __syncthreads();
-    for (int b = c + 1 + threadIdx.x; b < l; b += blockDim.x) R[c][b] *= rinv[c];
-    __syncthreads();
-    const int nr = l - c - 1;
-    for (int t = threadIdx.x; t < nr * kLrMaxL; t += blockDim.x) {
-      const int a = c + 1 + t / kLrMaxL, b = t % kLrMaxL;  // kLrMaxL is a power of two: shifts
-      if (b >= a && b < l) R[a][b] = fma(-R[c][a], R[c][b], R[a][b]);
+    em = block_max<kLrGramThreads>(em, shm);
+    if (em <= 1e-9) {
+      for (int e = tid; e < l * l; e += blockDim.x) {
+        const int i = e / l, j = e % l;
+        X[e] = i < j ? -S[i][j] : (i == j ? 1.5 - 0.5 * S[i][i] : 0.0);
+      }
+      if (tid == 0) P.ctr[CTR_LRG] = 0;
+      return;
     }
-    __syncthreads();
   }
-  // Y <- Y R^{-1}: for each row y, solve q R = y by forward substitution over the columns
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < H; i += (int64_t)gridDim.x * blockDim.x) {
-    double q[kLrMaxL];
+  if (tid < 32) {  // s = 11 (H l + l (l + 1)) u ||Y||_F^2 >= the sCholQR3 shift bound (round 1 only)
+    double tr = 0.0;
+    for (int a = tid; a < l; a += 32) tr += __ldcg(P.lr_PB + (int64_t)a * l + a);
+    tr = warp_sum(tr);
+    if (tid == 0) shv = shifted ? 11.0 * ((double)H * l + (double)l * (l + 1)) * 1.1102230246251565e-16 * tr : 0.0;
+  }
+  __syncthreads();
+  if (tid < l) S[tid][tid] += shv;
+  __syncthreads();
+  const int bcol = tid & 63, arow = tid >> 6;
+  {  // row 0 of R
+    const double di = rsqrt(fmax(S[0][0], 1e-300));
+    if (tid == 0) rinv[0] = di;
+    if (arow == 0 && bcol > 0 && bcol < l) S[0][bcol] *= di;
+  }
+  __syncthreads();
+  for (int c = 0; c + 1 < l; ++c) {
+    const double rcc = rinv[c];
+    // the next pivot: G^(c+1)_{c+1,c+1} = S[c+1][c+1] - R_{c,c+1}^2 (needed by row c+1 only)
+    const double dn = arow == 0 ? rsqrt(fmax(fma(-S[c][c + 1], S[c][c + 1], S[c + 1][c + 1]), 1e-300)) : 0.0;
+    const double rcb = S[c][bcol];             // R_cb (b > c) or W_cb (b < c)
+    const double wcb = bcol < c ? rcb : 1.0;   // W_cb, b <= c
 #pragma unroll
-    for (int c = 0; c < kLrMaxL; ++c)
-      if (c < l) q[c] = P.lr_Q[(int64_t)c * H + i];
-#pragma unroll
-    for (int c = 0; c < kLrMaxL; ++c) {
-      if (c < l) {
-        double v = q[c];
-#pragma unroll
-        for (int j = 0; j < kLrMaxL; ++j)
-          if (j < c) v = fma(-q[j], R[j][c], v);
-        q[c] = v * rinv[c];
+    for (int k = 0; k < kLrMaxL / 16; ++k) {   // branch-free (predicated) rows a = c + 1 + arow + 16 k
+      const int a = c + 1 + arow + 16 * k;
+      if (a < l && bcol < l) {
+        const double rca = S[c][a], sab = S[a][bcol];
+        const bool upd = bcol >= a;              // Schur complement, else L^{-1} row update (b <= c)
+        const double v = upd ? fma(-rca, rcb, sab) : fma(-rca * rcc, wcb, sab);
+        const bool first = (a == c + 1);         // row c+1 scaled into R; its diagonal never written
+        if ((upd && !(first && bcol == a)) || bcol <= c) S[a][bcol] = (first && upd) ? v * dn : v;
       }
     }
+    if (tid == 0) rinv[c + 1] = dn;
+    __syncthreads();
+  }
+  for (int e = tid; e < l * l; e += blockDim.x) {
+    const int i = e / l, j = e % l;
+    X[e] = i < j ? S[j][i] * rinv[j] : (i == j ? rinv[i] : 0.0);
+  }
+  if (tid == 0) P.ctr[CTR_LRG] = 0;
+}
+
+// Q = Y R^{-1} (H x l column-major, out of place): one thread per entry, q_ic = sum_{j<=c} y_ij X_jc
+// (eight loads in flight per thread).
+__global__ void __launch_bounds__(256) k_lr_rapply(Params P, const double* __restrict__ Y, double* __restrict__ Q) {
+  __shared__ double X[kLrMaxL * kLrMaxL];
+  if (P.st->done) return;
+  const int H = P.lr_H, l = P.lr_l;
+  for (int e = threadIdx.x; e < l * l; e += blockDim.x) X[e] = P.lr_PB[(int64_t)l * l + e];
+  __syncthreads();
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)H * l; e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e / H);
+    const int64_t i = e - (int64_t)c * H;
+    double a0 = 0.0, a1 = 0.0;
+    int j = 0;
+    for (; j + 8 <= c + 1; j += 8) {
+      double y[8];
 #pragma unroll
-    for (int c = 0; c < kLrMaxL; ++c)
-      if (c < l) P.lr_Q[(int64_t)c * H + i] = q[c];
+      for (int u = 0; u < 8; ++u) y[u] = __ldg(Y + (int64_t)(j + u) * H + i);
+#pragma unroll
+      for (int u = 0; u < 8; u += 2) {
+        a0 = fma(y[u], X[(j + u) * l + c], a0);
+        a1 = fma(y[u + 1], X[(j + u + 1) * l + c], a1);
+      }
+    }
+    for (; j <= c; ++j) a0 = fma(__ldg(Y + (int64_t)j * H + i), X[j * l + c], a0);
+    Q[e] = a0 + a1;
   }
 }
 
@@ -1576,108 +1633,127 @@ __global__ void __launch_bounds__(256) k_lr_gram(Params P) {
   }
 }
 
-// Parallel cyclic Jacobi on Mg (round-robin pairs, one warp per pair), then the top-r
-// projector Pr = U_r U_r^T (l x l) into lr_PB[l*l .. 2*l*l).  One CTA of 1024 threads.
-constexpr size_t kLrEigSmem = 2 * sizeof(double) * kLrMaxL * (kLrMaxL + 1);
-__global__ void __launch_bounds__(1024) k_lr_eig(Params P) {
-  extern __shared__ double lr_sm[];  // kLrEigSmem bytes: M then V, each kLrMaxL x (kLrMaxL + 1)
-  double(*M)[kLrMaxL + 1] = reinterpret_cast<double(*)[kLrMaxL + 1]>(lr_sm);
-  double(*V)[kLrMaxL + 1] = reinterpret_cast<double(*)[kLrMaxL + 1]>(lr_sm + kLrMaxL * (kLrMaxL + 1));
-  __shared__ double cs[kLrMaxL / 2][2];
-  __shared__ int pq[kLrMaxL / 2][2];
-  __shared__ double sh[33];
+// Top-r projector Pr = U_r U_r^T (l x l) of Mg = B B^T into lr_PB[l*l .. 2*l*l), by one-sided
+// (Hestenes) Jacobi on A = Mg: the columns a_p are orthogonalised by plane rotations, A J = U Sigma.
+// Mg is symmetric positive semi-definite, so its left singular vectors U are its eigenvectors and
+// sigma_p = lambda_p (same order): no rotation accumulation is needed and Pr = sum over the r
+// largest ||a_p|| of a_p a_p^T / ||a_p||^2.  Round-robin pairs, 8 lanes per pair (rows j, j+8, ...),
+// one barrier per step; a pair is rotated when |a_p.a_q| > sqrt(L) u ||a_p|| ||a_q||, sweeps until
+// none is.  The xor-butterfly sums are bitwise identical on every lane of a pair group, so the
+// lanes agree on the rotation without a broadcast.  One CTA of 256 threads (l <= 64).
+constexpr int kLrEigLd = kLrMaxL + 1;
+constexpr size_t kLrEigSmem = sizeof(double) * kLrMaxL * kLrEigLd;
+__global__ void __launch_bounds__(256) k_lr_eig(Params P) {
+  extern __shared__ double lr_sm[];  // kLrEigSmem bytes: A[col][row]
+  double(*A)[kLrEigLd] = reinterpret_cast<double(*)[kLrEigLd]>(lr_sm);
+  __shared__ unsigned short ptab[kLrMaxL - 1][kLrMaxL / 2];
+  __shared__ double ialpha[kLrMaxL];
   __shared__ int top[kLrMaxL];
   if (P.st->done) return;
   const int l = P.lr_l, r = P.lr_r;
-  const int L = (l + 1) & ~1;  // even number of slots for the tournament (slot l is a dummy when l is odd)
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  for (int e = tid; e < l * l; e += 1024) M[e / l][e % l] = P.lr_PB[e];
-  for (int e = tid; e < kLrMaxL * kLrMaxL; e += 1024) V[e / kLrMaxL][e % kLrMaxL] = (e / kLrMaxL == e % kLrMaxL) ? 1.0 : 0.0;
+  const int L = (l + 1) & ~1;  // even number of slots for the tournament (slot l is a zero column when l is odd)
+  const int np = L / 2;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int pr = tid >> 3, j = tid & 7;  // pair of this 8-lane group, lane in the group
+  for (int e = tid; e < L * L; e += 256) {
+    const int c = e / L, rr = e % L;
+    A[c][rr] = (c < l && rr < l) ? P.lr_PB[rr * l + c] : 0.0;
+  }
+  // round-robin tournament: slot 0 fixed, slots 1..L-1 rotate; pair w of step s is (slot w, slot L-1-w)
+  for (int e = tid; e < (L - 1) * np; e += 256) {
+    const int step = e / np, w = e % np;
+    auto slot = [&](int s2) { return s2 == 0 ? 0 : 1 + (s2 - 1 + step) % (L - 1); };
+    int p = slot(w), q = slot(L - 1 - w);
+    if (p > q) {
+      const int t = p;
+      p = q;
+      q = t;
+    }
+    ptab[step][w] = (unsigned short)(p | (q << 8));
+  }
   __syncthreads();
-  double fro = 0.0;
-  for (int e = tid; e < l * l; e += 1024) fro = fma(M[e / l][e % l], M[e / l][e % l], fro);
-  fro = block_sum<1024>(fro, sh);
-  // sweeps until the off-diagonal mass is below (1e-15)^2 ||M||_F^2 or stops shrinking
-  // (Jacobi converges quadratically; once at the rounding floor further sweeps only
-  // shuffle rounding), at most 20
-  double prev = INFINITY;
-  for (int sweep = 0; sweep < 20; ++sweep) {
-    double off = 0.0;
-    for (int e = tid; e < l * l; e += 1024)
-      if (e / l != e % l) off = fma(M[e / l][e % l], M[e / l][e % l], off);
-    off = block_sum<1024>(off, sh);
-    // converged, or at the rounding floor (off-diagonal mass tiny and no longer shrinking)
-    if (!(off > 1e-30 * fro) || (off <= 1e-24 * fro && off > 0.25 * prev)) break;
-    prev = off;
+  const double tol2 = (double)L * 1.2325951644078309e-32;  // (sqrt(L) u)^2, u = 2^-53
+  const unsigned gmask = 0xffu << (lane & ~7);
+  for (int sweep = 0; sweep < 30; ++sweep) {
+    int rotated = 0;
     for (int step = 0; step < L - 1; ++step) {
-      // round-robin tournament: slot 0 fixed, slots 1..L-1 rotate; warp w owns pair w and
-      // computes its rotation (lane-redundantly) right before applying it to the columns
-      // columns: M <- M J, V <- V J
-      for (int w = wid; w < L / 2; w += 32) {
-        auto slot = [&](int s2) { return s2 == 0 ? 0 : 1 + (s2 - 1 + step) % (L - 1); };
-        int p = slot(w), q = slot(L - 1 - w);
-        if (p > q) {
-          const int t = p;
-          p = q;
-          q = t;
+      if (pr < np) {
+        const int pqv = ptab[step][pr];
+        const int p = pqv & 255, q = pqv >> 8;
+        double ap[kLrMaxL / 8], aq[kLrMaxL / 8];
+#pragma unroll
+        for (int k = 0; k < kLrMaxL / 8; ++k) {
+          const int rr = j + 8 * k;
+          ap[k] = rr < L ? A[p][rr] : 0.0;
+          aq[k] = rr < L ? A[q][rr] : 0.0;
         }
-        double c = 1.0, s = 0.0;
-        if (q < l && M[p][q] != 0.0) {
-          // t = sgn(theta) / (|theta| + sqrt(theta^2 + 1)), theta = (M_qq - M_pp) / (2 M_pq), written as
-          // t = 2 M_pq sgn(dd) / (|dd| + sqrt(dd^2 + 4 M_pq^2)), dd = M_qq - M_pp (one div, one sqrt)
-          const double apq = M[p][q], dd = M[q][q] - M[p][p];
-          const double sg = ((dd >= 0.0) == (apq >= 0.0)) ? 1.0 : -1.0;
-          const double t = sg * 2.0 * fabs(apq) / (fabs(dd) + sqrt(fma(dd, dd, 4.0 * apq * apq)));
-          c = rsqrt(fma(t, t, 1.0));
-          s = t * c;
+        double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll
+        for (int k = 0; k < kLrMaxL / 8; ++k) {
+          al = fma(ap[k], ap[k], al);
+          be = fma(aq[k], aq[k], be);
+          ga = fma(ap[k], aq[k], ga);
         }
-        __syncwarp();
-        if (lane == 0) {
-          pq[w][0] = p;
-          pq[w][1] = q;
-          cs[w][0] = c;
-          cs[w][1] = s;
+#pragma unroll
+        for (int o = 4; o; o >>= 1) {
+          al += __shfl_xor_sync(gmask, al, o, 8);
+          be += __shfl_xor_sync(gmask, be, o, 8);
+          ga += __shfl_xor_sync(gmask, ga, o, 8);
         }
-        if (q >= l) continue;
-        for (int a = lane; a < l; a += 32) {
-          const double mp = M[a][p], mq = M[a][q], vp = V[a][p], vq = V[a][q];
-          M[a][p] = c * mp - s * mq;
-          M[a][q] = s * mp + c * mq;
-          V[a][p] = c * vp - s * vq;
-          V[a][q] = s * vp + c * vq;
-        }
-      }
-      __syncthreads();
-      // rows: M <- J^T M
-      for (int w = wid; w < L / 2; w += 32) {
-        const int p = pq[w][0], q = pq[w][1];
-        if (q >= l) continue;
-        const double c = cs[w][0], s = cs[w][1];
-        for (int b = lane; b < l; b += 32) {
-          const double mp = M[p][b], mq = M[q][b];
-          M[p][b] = c * mp - s * mq;
-          M[q][b] = s * mp + c * mq;
+        if (ga != 0.0 && ga * ga > tol2 * al * be) {
+          rotated = 1;
+          // tan(phi) = sgn 2|ga| / (|dd| + sqrt(dd^2 + 4 ga^2)), dd = be - al; with h = (dd^2 + 4 ga^2)^(-1/2):
+          // cos(phi) = sqrt(u), u = (1 + |dd| h) / 2, sin(phi) = sgn |ga| h / cos(phi) (two rsqrt, no divisions)
+          const double dd = be - al;
+          const double sg = ((dd >= 0.0) == (ga >= 0.0)) ? 1.0 : -1.0;
+          const double h = rsqrt(fma(dd, dd, 4.0 * ga * ga));
+          const double u = fma(0.5 * fabs(dd), h, 0.5);
+          const double rc = rsqrt(u);
+          const double c = u * rc, s = sg * fabs(ga) * h * rc;
+#pragma unroll
+          for (int k = 0; k < kLrMaxL / 8; ++k) {
+            const int rr = j + 8 * k;
+            if (rr < L) {
+              A[p][rr] = c * ap[k] - s * aq[k];
+              A[q][rr] = s * ap[k] + c * aq[k];
+            }
+          }
         }
       }
       __syncthreads();
     }
+    if (!__syncthreads_or(rotated)) break;
   }
-  // the r largest eigenvalues (ties by index)
+  // sigma_p^2 = ||a_p||^2; the r largest (ties by index), zero columns never selected
   if (tid < l) {
-    const double lam = M[tid][tid];
+    double a = 0.0;
+    for (int rr = 0; rr < l; ++rr) a = fma(A[tid][rr], A[tid][rr], a);
+    ialpha[tid] = a;
+  }
+  __syncthreads();
+  int sel = 0;
+  double inv = 0.0;
+  if (tid < l) {
+    const double lam = ialpha[tid];
     int rank = 0;
     for (int b = 0; b < l; ++b) {
-      const double lb = M[b][b];
+      const double lb = ialpha[b];
       rank += (lb > lam || (lb == lam && b < tid)) ? 1 : 0;
     }
-    top[tid] = rank < r ? 1 : 0;
+    sel = (rank < r && lam > 0.0) ? 1 : 0;
+    inv = sel ? 1.0 / lam : 0.0;
   }
   __syncthreads();
-  for (int e = tid; e < l * l; e += 1024) {
+  if (tid < l) {
+    top[tid] = sel;
+    ialpha[tid] = inv;
+  }
+  __syncthreads();
+  for (int e = tid; e < l * l; e += 256) {
     const int x = e / l, y = e % l;
     double acc = 0.0;
     for (int a = 0; a < l; ++a)
-      if (top[a]) acc = fma(V[x][a], V[y][a], acc);
+      if (top[a]) acc = fma(A[a][x] * ialpha[a], A[a][y], acc);
     P.lr_PB[(int64_t)l * l + e] = acc;
   }
 }
