@@ -1637,55 +1637,48 @@ __global__ void __launch_bounds__(256) k_lr_gram(Params P) {
 // (Hestenes) Jacobi on A = Mg: the columns a_p are orthogonalised by plane rotations, A J = U Sigma.
 // Mg is symmetric positive semi-definite, so its left singular vectors U are its eigenvectors and
 // sigma_p = lambda_p (same order): no rotation accumulation is needed and Pr = sum over the r
-// largest ||a_p|| of a_p a_p^T / ||a_p||^2.  Round-robin pairs, 8 lanes per pair (rows j, j+8, ...),
-// one barrier per step; a pair is rotated when |a_p.a_q| > sqrt(L) u ||a_p|| ||a_q||, sweeps until
-// none is.  The xor-butterfly sums are bitwise identical on every lane of a pair group, so the
-// lanes agree on the rotation without a broadcast.  One CTA of 256 threads (l <= 64).
-constexpr int kLrEigLd = kLrMaxL + 1;
-constexpr size_t kLrEigSmem = sizeof(double) * kLrMaxL * kLrEigLd;
+// largest ||a_p|| of a_p a_p^T / ||a_p||^2.  Round-robin (tournament) ordering with the columns
+// stored at their tournament slot: pair w is always slots (w, L-1-w) and the rotated columns are
+// written to the slots they occupy at the next step (slot 0 stays, 1 -> L-1, k -> k-1), double
+// buffered.  8 lanes per pair (rows j, j+8, ...), one barrier per step; with the slot stride
+// kLrEigLd = 8 mod 16 the two pairs of a half-warp touch opposite-parity slots, i.e. disjoint
+// halves of the shared-memory banks.  A pair is rotated when |a_p.a_q| > sqrt(L) u ||a_p|| ||a_q||;
+// sweeps until none is.  The xor-butterfly sums are bitwise identical on every lane of a group, so
+// the lanes agree on the rotation without a broadcast.  One CTA of 256 threads (l <= 64).
+constexpr int kLrEigLd = kLrMaxL + 8;
+constexpr size_t kLrEigSmem = 2 * sizeof(double) * kLrMaxL * kLrEigLd;
 __global__ void __launch_bounds__(256) k_lr_eig(Params P) {
-  extern __shared__ double lr_sm[];  // kLrEigSmem bytes: A[col][row]
-  double(*A)[kLrEigLd] = reinterpret_cast<double(*)[kLrEigLd]>(lr_sm);
-  __shared__ unsigned short ptab[kLrMaxL - 1][kLrMaxL / 2];
+  extern __shared__ double lr_sm[];  // kLrEigSmem bytes: two [slot][row] buffers
   __shared__ double ialpha[kLrMaxL];
   __shared__ int top[kLrMaxL];
   if (P.st->done) return;
   const int l = P.lr_l, r = P.lr_r;
-  const int L = (l + 1) & ~1;  // even number of slots for the tournament (slot l is a zero column when l is odd)
+  const int L = (l + 1) & ~1;  // even number of slots (slot l is a zero column when l is odd)
   const int np = L / 2;
   const int tid = threadIdx.x, lane = tid & 31;
-  const int pr = tid >> 3, j = tid & 7;  // pair of this 8-lane group, lane in the group
+  const int w = tid >> 3, j = tid & 7;  // pair of this 8-lane group, lane in the group
   for (int e = tid; e < L * L; e += 256) {
     const int c = e / L, rr = e % L;
-    A[c][rr] = (c < l && rr < l) ? P.lr_PB[rr * l + c] : 0.0;
-  }
-  // round-robin tournament: slot 0 fixed, slots 1..L-1 rotate; pair w of step s is (slot w, slot L-1-w)
-  for (int e = tid; e < (L - 1) * np; e += 256) {
-    const int step = e / np, w = e % np;
-    auto slot = [&](int s2) { return s2 == 0 ? 0 : 1 + (s2 - 1 + step) % (L - 1); };
-    int p = slot(w), q = slot(L - 1 - w);
-    if (p > q) {
-      const int t = p;
-      p = q;
-      q = t;
-    }
-    ptab[step][w] = (unsigned short)(p | (q << 8));
+    lr_sm[c * kLrEigLd + rr] = (c < l && rr < l) ? P.lr_PB[rr * l + c] : 0.0;
   }
   __syncthreads();
   const double tol2 = (double)L * 1.2325951644078309e-32;  // (sqrt(L) u)^2, u = 2^-53
   const unsigned gmask = 0xffu << (lane & ~7);
+  const int sp = w, sq = L - 1 - w;                                        // this pair's slots
+  const int np_ = sp == 0 ? 0 : (sp == 1 ? L - 1 : sp - 1), nq_ = sq == 1 ? L - 1 : sq - 1;  // next step's
+  int cur = 0;
   for (int sweep = 0; sweep < 30; ++sweep) {
     int rotated = 0;
     for (int step = 0; step < L - 1; ++step) {
-      if (pr < np) {
-        const int pqv = ptab[step][pr];
-        const int p = pqv & 255, q = pqv >> 8;
+      const double* Ac = lr_sm + cur * kLrMaxL * kLrEigLd;
+      double* An = lr_sm + (cur ^ 1) * kLrMaxL * kLrEigLd;
+      if (w < np) {
         double ap[kLrMaxL / 8], aq[kLrMaxL / 8];
 #pragma unroll
         for (int k = 0; k < kLrMaxL / 8; ++k) {
           const int rr = j + 8 * k;
-          ap[k] = rr < L ? A[p][rr] : 0.0;
-          aq[k] = rr < L ? A[q][rr] : 0.0;
+          ap[k] = rr < L ? Ac[sp * kLrEigLd + rr] : 0.0;
+          aq[k] = rr < L ? Ac[sq * kLrEigLd + rr] : 0.0;
         }
         double al = 0.0, be = 0.0, ga = 0.0;
 #pragma unroll
@@ -1700,6 +1693,7 @@ __global__ void __launch_bounds__(256) k_lr_eig(Params P) {
           be += __shfl_xor_sync(gmask, be, o, 8);
           ga += __shfl_xor_sync(gmask, ga, o, 8);
         }
+        double c = 1.0, s = 0.0;
         if (ga != 0.0 && ga * ga > tol2 * al * be) {
           rotated = 1;
           // tan(phi) = sgn 2|ga| / (|dd| + sqrt(dd^2 + 4 ga^2)), dd = be - al; with h = (dd^2 + 4 ga^2)^(-1/2):
@@ -1709,34 +1703,37 @@ __global__ void __launch_bounds__(256) k_lr_eig(Params P) {
           const double h = rsqrt(fma(dd, dd, 4.0 * ga * ga));
           const double u = fma(0.5 * fabs(dd), h, 0.5);
           const double rc = rsqrt(u);
-          const double c = u * rc, s = sg * fabs(ga) * h * rc;
+          c = u * rc;
+          s = sg * fabs(ga) * h * rc;
+        }
 #pragma unroll
-          for (int k = 0; k < kLrMaxL / 8; ++k) {
-            const int rr = j + 8 * k;
-            if (rr < L) {
-              A[p][rr] = c * ap[k] - s * aq[k];
-              A[q][rr] = s * ap[k] + c * aq[k];
-            }
+        for (int k = 0; k < kLrMaxL / 8; ++k) {
+          const int rr = j + 8 * k;
+          if (rr < L) {
+            An[np_ * kLrEigLd + rr] = c * ap[k] - s * aq[k];
+            An[nq_ * kLrEigLd + rr] = s * ap[k] + c * aq[k];
           }
         }
       }
+      cur ^= 1;
       __syncthreads();
     }
     if (!__syncthreads_or(rotated)) break;
   }
-  // sigma_p^2 = ||a_p||^2; the r largest (ties by index), zero columns never selected
-  if (tid < l) {
+  const double* Af = lr_sm + cur * kLrMaxL * kLrEigLd;
+  // sigma^2 = ||a||^2 per slot; the r largest (ties by slot), zero columns never selected
+  if (tid < L) {
     double a = 0.0;
-    for (int rr = 0; rr < l; ++rr) a = fma(A[tid][rr], A[tid][rr], a);
+    for (int rr = 0; rr < l; ++rr) a = fma(Af[tid * kLrEigLd + rr], Af[tid * kLrEigLd + rr], a);
     ialpha[tid] = a;
   }
   __syncthreads();
   int sel = 0;
   double inv = 0.0;
-  if (tid < l) {
+  if (tid < L) {
     const double lam = ialpha[tid];
     int rank = 0;
-    for (int b = 0; b < l; ++b) {
+    for (int b = 0; b < L; ++b) {
       const double lb = ialpha[b];
       rank += (lb > lam || (lb == lam && b < tid)) ? 1 : 0;
     }
@@ -1744,7 +1741,7 @@ __global__ void __launch_bounds__(256) k_lr_eig(Params P) {
     inv = sel ? 1.0 / lam : 0.0;
   }
   __syncthreads();
-  if (tid < l) {
+  if (tid < L) {
     top[tid] = sel;
     ialpha[tid] = inv;
   }
@@ -1752,8 +1749,8 @@ __global__ void __launch_bounds__(256) k_lr_eig(Params P) {
   for (int e = tid; e < l * l; e += 256) {
     const int x = e / l, y = e % l;
     double acc = 0.0;
-    for (int a = 0; a < l; ++a)
-      if (top[a]) acc = fma(A[a][x] * ialpha[a], A[a][y], acc);
+    for (int a = 0; a < L; ++a)
+      if (top[a]) acc = fma(Af[a * kLrEigLd + x] * ialpha[a], Af[a * kLrEigLd + y], acc);
     P.lr_PB[(int64_t)l * l + e] = acc;
   }
 }
