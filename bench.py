@@ -318,7 +318,8 @@ def main():
     ms, launches, _, clk, done, status = timed_region(False)
     # (2) the same K iterations again with CUDA events around every launch (per-kernel times)
     ms_prof, _, prof, clk2, _, _ = (timed_region(True) if not args.no_profile else (None, None, {}, None, None, None))
-    k_done = s.get_info()["k_done"]
+    info_end = s.get_info()
+    k_done = info_end["k_done"]
     # sharded: the ranks cooperate on one solve (iterations/s of the job); replicas: independent solves
     value = (K if sharded else K * world) / (ms / 1e3)
 
@@ -337,9 +338,15 @@ def main():
         d = prof[dom]
         bpl = d["bytes"] / d["launches"]
         ach = bpl / (d["ms"] / d["launches"] / 1e3) / 1e9
-        tr = _traffic(prob.name, dom)
-        kname = {"spmv_A": "k_spmv_csr (A z)", "spmv_T": "k_spmv_csr (T w)"}.get(dom, dom)
+        inf = s.get_info()
+        fmt = {"spmv_A": "pair-CSR" if inf["a_pairs"] else "CSR", "spmv_T": "pair-CSR" if inf["t_pairs"] else "CSR"}
+        tr = _traffic(prob.name, dom + ("_pcsr" if fmt.get(dom) == "pair-CSR" else ""))
+        kname = {"spmv_A": f"k_spmv_csr_pf, {fmt['spmv_A']} (A z)",
+                 "spmv_T": f"k_spmv_csr_pf, {fmt['spmv_T']} (T w)"}.get(dom, dom)
         roof = {"bound": "hbm", "kernel": kname, "achieved": ach, "peak": peak,
+                "bytes_basis": "bytes of the format the product runs on: CSR 12 B/nnz (int32 col + fp64 value), "
+                               "pair-CSR 20 B per adjacent-column pair + 12 B per singleton, + row pointers and "
+                               "vectors (DESIGN.md §5)",
                 "unit": "GB/s", "frac": ach / peak, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": bpl, "traffic": tr}
     step_bytes = sum(d["bytes"] for d in prof.values())
@@ -376,6 +383,9 @@ def main():
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": prob.name, "method": spec.method, "m": prob.m, "n": prob.n,
                        "nnz_A": nnz_A, "nnz_T": nnz_T,
+                       "spmv_format": {"A": "pair-CSR" if info_end["a_pairs"] else "CSR",
+                                       "T": "pair-CSR" if info_end["t_pairs"] else "CSR",
+                                       "pairs_A": info_end["a_pairs"], "pairs_T": info_end["t_pairs"]},
                        "ell": spec.window, "d": spec.d, "s": spec.s_nz, "tau": spec.precond, "maxit": maxit,
                        "iterations_timed": f"{W + 1}..{W + K}", "history": "true residual (W path) on",
                        "l2": "inputs larger than L2 (operators ~30 GB vs 126 MB L2); no flush",

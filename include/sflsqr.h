@@ -53,7 +53,7 @@
 extern "C" {
 #endif
 
-#define SFLSQR_ABI_VERSION 3
+#define SFLSQR_ABI_VERSION 4
 
 /* return codes */
 #define SFLSQR_OK 0
@@ -167,6 +167,9 @@ typedef struct sflsqr_info {
   double delta_e;      /* opts.delta_e (the discrepancy test's noise norm)         */
   double bytes_model;  /* algorithmic HBM bytes of iteration k_done on this rank, the model of
                           SURVEY.md §8(d) / DESIGN.md §5 (0 before the first iteration)  */
+  int64_t a_pairs, t_pairs; /* adjacent-column pairs of the pair-CSR copy the A / T products
+                          run on (SpMV mode 16: 10 instead of 12 bytes per paired nonzero);
+                          0 = plain CSR                                                  */
 } sflsqr_info;
 
 /* Per-kernel-class device time, recorded with CUDA events on the library stream
@@ -335,8 +338,12 @@ int sflsqr_debug_state(sflsqr_t *h, double *z, double *x, double *p_ring, double
  * row-group CSR (rows per CTA x chunks in flight: 16x4, 8x4, 32x4, 32x2);
  * 8 = 64 half-warp rows per CTA; 11, 12, 13, 14 = software-pipelined row-group
  * CSR (next chunks' indices/values loaded ahead of the gathers; 14 = half-warp
- * rows, 32 rows per 512-thread CTA = the default).  band_shift is reserved (8..30).
- * Invalidates a captured graph (rebuilt at the next set_rhs). */
+ * rows, 32 rows per 512-thread CTA = the default); 15 = CSR-16 (16-bit column
+ * offsets per 16-entry chunk, built on request; falls back to 14 when a chunk
+ * spans > 65536 columns); 16 = pair-CSR (every row's runs of consecutive columns
+ * stored as (column, two values) pairs plus a singleton CSR: 10 instead of 12
+ * bytes per paired nonzero; built on request, on the device).  band_shift is
+ * reserved (8..30).  Invalidates a captured graph (rebuilt at the next set_rhs). */
 int sflsqr_debug_set_tuning(sflsqr_t *h, int32_t spmv_mode, int32_t band_shift);
 
 /* Profiling: on = 1 launches kernels eagerly (no graph) with CUDA events around

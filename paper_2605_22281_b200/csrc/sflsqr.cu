@@ -43,6 +43,17 @@ enum TKind { T_FULL = 0, T_ROWSHARD = 1, T_COLSHARD = 2 };
 
 // CSR-16 copy of an operator's column indices (k_spmv_c16): per-chunk int32 base,
 // 16-bit offsets, chunk pointer per row.  ok = false: the operator stays int32 CSR.
+struct PCSR {  // pair-CSR copy of an operator (k_pcsr_rows): pairs + singleton CSR
+  bool ok = false;
+  int64_t npairs = 0, nsingles = 0;
+  int64_t* prp = nullptr;
+  int* pcol = nullptr;
+  double2* pval = nullptr;
+  int64_t* srp = nullptr;
+  int* scol = nullptr;
+  double* sval = nullptr;
+};
+
 struct C16 {
   bool ok = false;
   int64_t nchunks = 0;
@@ -76,7 +87,9 @@ struct sflsqr {
   int bH = 0, bW = 0, brad = 0;
   double* taps = nullptr;
   double* blur_tmp = nullptr;
-  C16 ca, ct;           // CSR-16 index copies of A and T (default SpMV format when ok)
+  C16 ca, ct;           // CSR-16 index copies of A and T (SpMV mode 15, on request)
+  PCSR pa, pt;          // pair-CSR copies of A and T (SpMV mode 16)
+  int pcsr_unroll = 4;  // pairs in flight per lane in the mode-16 kernel (4 or 2; SFLSQR_PCSR_UNROLL)
   // sketch
   bool sk_set = false;
   int sk_kind = 0;  // 0 sparse-sign (R5/R6), 1 dense Gaussian (R21)
@@ -274,6 +287,16 @@ void free_solve(sflsqr_t* h) {
   h->rhs_set = false;
 }
 
+void free_pcsr(PCSR& p) {
+  cudaFree(p.prp);
+  cudaFree(p.pcol);
+  cudaFree(p.pval);
+  cudaFree(p.srp);
+  cudaFree(p.scol);
+  cudaFree(p.sval);
+  p = PCSR();
+}
+
 void free_op(sflsqr_t* h) {
   if (h->a_owned) {
     cudaFree(h->a_rowptr);
@@ -293,6 +316,8 @@ void free_op(sflsqr_t* h) {
     cudaFree(c->off);
     *c = C16();
   }
+  free_pcsr(h->pa);
+  free_pcsr(h->pt);
   h->a_rowptr = h->t_rowptr = nullptr;
   h->a_col = h->t_col = nullptr;
   h->a_val = h->t_val = h->taps = h->blur_tmp = nullptr;
@@ -409,8 +434,25 @@ void enqueue_apply(sflsqr_t* h, int which, const DevState* st, const double* x, 
     return (int)std::max<int64_t>(1, std::min<int64_t>(want, 148 * per_sm));
   };
   const C16& cc = which == 0 ? h->ca : h->ct;
-  int mode = h->spmv_mode >= 0 ? h->spmv_mode : select_spmv_mode(nnz, nrows);
+  const PCSR& pc = which == 0 ? h->pa : h->pt;
+  int mode = h->spmv_mode >= 0 ? h->spmv_mode : (pc.ok ? 16 : select_spmv_mode(nnz, nrows));
   if (mode == 15 && !cc.ok) mode = 14;
+  if (mode == 16 && !pc.ok) mode = 14;
+  if (mode == 16) {
+    // pair-CSR: 20 bytes per pair of nonzeros, 12 per singleton, two row pointer arrays
+    L.bytes_override(20.0 * pc.npairs + 12.0 * pc.nsingles + 16.0 * (nrows + 1) + 8.0 * xlen + 8.0 * nrows);
+    PairPart PP;
+    PP.rowptr = pc.prp;
+    PP.col = pc.pcol;
+    PP.val = pc.pval;
+    if (h->pcsr_unroll == 4)
+      k_spmv_csr_pf<16, 4, 16, false, 4><<<grid_for(32, 2), 512, 0, h->stream>>>(
+          st, nrows, pc.srp, pc.scol, pc.sval, x, x_ld, x_koff, y, SpmvEpi(), PP);
+    else
+      k_spmv_csr_pf<16, 4, 16, false, 2><<<grid_for(32, 2), 512, 0, h->stream>>>(
+          st, nrows, pc.srp, pc.scol, pc.sval, x, x_ld, x_koff, y, SpmvEpi(), PP);
+    return;
+  }
   if (mode == 15) {
     // CSR-16: 8 (value) + 2 (offset) bytes per nonzero + 4 per 16-entry chunk + chunk pointers
     L.bytes_override(10.0 * nnz + 4.0 * cc.nchunks + 16.0 * (nrows + 1) + 8.0 * xlen + 8.0 * nrows);
@@ -973,6 +1015,83 @@ int build_c16_all(sflsqr_t* h) {
   return build_c16(h, h->t_rows, h->t_rowptr, h->t_col, h->nnz_t, h->ct);
 }
 
+int check_launch(sflsqr_t* h);
+
+// Pair-CSR copy of one operator (k_pcsr_rows): counts, two exclusive scans, fill.
+int build_pcsr(sflsqr_t* h, int64_t nrows, const int64_t* rp, const int32_t* col, const double* val, PCSR& p) {
+  free_pcsr(p);
+  if (nrows < 1) return SFLSQR_OK;
+  int64_t *cp = nullptr, *cs = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  int rc;
+  auto cleanup = [&]() {
+    cudaFree(cp);
+    cudaFree(cs);
+    cudaFree(tmp);
+  };
+  if ((rc = dalloc(h, (void**)&cp, sizeof(int64_t) * (nrows + 1), nullptr)) ||
+      (rc = dalloc(h, (void**)&cs, sizeof(int64_t) * (nrows + 1), nullptr)) ||
+      (rc = dalloc(h, (void**)&p.prp, sizeof(int64_t) * (nrows + 1), nullptr)) ||
+      (rc = dalloc(h, (void**)&p.srp, sizeof(int64_t) * (nrows + 1), nullptr))) {
+    cleanup();
+    free_pcsr(p);
+    return rc;
+  }
+  CU(h, cudaMemsetAsync(cp + nrows, 0, sizeof(int64_t), h->stream));
+  CU(h, cudaMemsetAsync(cs + nrows, 0, sizeof(int64_t), h->stream));
+  const int g = (int)std::min<int64_t>((nrows + 7) / 8, 148 * 64);
+  k_pcsr_rows<false><<<g, 256, 0, h->stream>>>(nrows, rp, col, val, cp, cs, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                               nullptr);
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cp, p.prp, nrows + 1, h->stream);
+  if ((rc = dalloc(h, &tmp, tmp_bytes, nullptr))) {
+    cleanup();
+    free_pcsr(p);
+    return rc;
+  }
+  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cp, p.prp, nrows + 1, h->stream);
+  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cs, p.srp, nrows + 1, h->stream);
+  CU(h, cudaMemcpyAsync(&p.npairs, p.prp + nrows, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+  CU(h, cudaMemcpyAsync(&p.nsingles, p.srp + nrows, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+  CU(h, cudaStreamSynchronize(h->stream));
+  if ((rc = dalloc(h, (void**)&p.pcol, sizeof(int) * std::max<int64_t>(p.npairs, 1), nullptr)) ||
+      (rc = dalloc(h, (void**)&p.pval, sizeof(double2) * std::max<int64_t>(p.npairs, 1), nullptr)) ||
+      (rc = dalloc(h, (void**)&p.scol, sizeof(int) * std::max<int64_t>(p.nsingles, 1), nullptr)) ||
+      (rc = dalloc(h, (void**)&p.sval, sizeof(double) * std::max<int64_t>(p.nsingles, 1), nullptr))) {
+    cleanup();
+    free_pcsr(p);
+    return rc;
+  }
+  k_pcsr_rows<true><<<g, 256, 0, h->stream>>>(nrows, rp, col, val, nullptr, nullptr, p.prp, p.srp, p.pcol, p.pval,
+                                              p.scol, p.sval);
+  CU(h, cudaStreamSynchronize(h->stream));
+  cleanup();
+  if ((rc = check_launch(h))) {
+    free_pcsr(p);
+    return rc;
+  }
+  p.ok = true;
+  return SFLSQR_OK;
+}
+
+// Auxiliary SpMV formats the selected mode needs (built after every operator upload).
+int build_formats(sflsqr_t* h) {
+  if (h->blur) return SFLSQR_OK;
+  if (h->spmv_mode == 15) return build_c16_all(h);
+  int rc;
+  if (h->spmv_mode == 16) {
+    if (!h->pa.ok && (rc = build_pcsr(h, h->m_loc, h->a_rowptr, h->a_col, h->a_val, h->pa))) return rc;
+    if (!h->pt.ok && (rc = build_pcsr(h, h->t_rows, h->t_rowptr, h->t_col, h->t_val, h->pt))) return rc;
+  } else if (h->spmv_mode < 0 && !h->pt.ok && h->nnz_t > 0) {
+    // default rule: the transpose-side operator runs as pair-CSR when at least 75 % of its
+    // nonzeros pair up (>= 12.5 % fewer bytes; the pixel-driven B of config 4: 100 %); the
+    // forward Siddon product is L1-gather bound and gains nothing
+    if ((rc = build_pcsr(h, h->t_rows, h->t_rowptr, h->t_col, h->t_val, h->pt))) return rc;
+    if (2.0 * h->pt.npairs < 0.75 * (double)h->nnz_t) free_pcsr(h->pt);
+  }
+  return SFLSQR_OK;
+}
+
 int check_launch(sflsqr_t* h) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(h, SFLSQR_E_CUDA, "kernel launch: %s", cudaGetErrorString(e));
@@ -1375,6 +1494,7 @@ int sflsqr_create(sflsqr_t** out, const sflsqr_opts* o) {
     }
   }
   if (const char* ev = std::getenv("SFLSQR_SPMV_MODE")) h->spmv_mode = std::atoi(ev);
+  if (const char* ev = std::getenv("SFLSQR_PCSR_UNROLL")) h->pcsr_unroll = std::atoi(ev) == 2 ? 2 : 4;
   if (const char* ev = std::getenv("SFLSQR_LR_QR")) h->lr_qr_cgs = std::strcmp(ev, "cgs") == 0;
   if (const char* ev = std::getenv("SFLSQR_RES_OVERLAP")) {
     h->res_overlap = ev[0] != '0';
@@ -1523,7 +1643,7 @@ int sflsqr_set_operator_shard(sflsqr_t* h, int64_t m, int64_t n, int64_t a_row0,
     rc = upload_csr(h, h->t_rows, trp.data(), tcol.data(), tval.data(), &h->t_rowptr, &h->t_col, &h->t_val,
                     &h->nnz_t);
   }
-  if (rc || (h->spmv_mode == 15 && (rc = build_c16_all(h)))) {
+  if (rc || (rc = build_formats(h))) {
     free_op(h);
     return rc;
   }
@@ -1593,7 +1713,7 @@ int sflsqr_set_operator(sflsqr_t* h, int64_t m, int64_t n, const int64_t* a_rowp
       return rc;
     }
   }
-  if (h->spmv_mode == 15 && (rc0 = build_c16_all(h))) {
+  if ((rc0 = build_formats(h))) {
     free_op(h);
     return rc0;
   }
@@ -1908,6 +2028,10 @@ int sflsqr_get_info(sflsqr_t* h, sflsqr_info* info) {
     }
   }
   info->delta_e = h->o.delta_e;
+  const int mode_a = h->spmv_mode >= 0 ? h->spmv_mode : (h->pa.ok ? 16 : 14);
+  const int mode_t = h->spmv_mode >= 0 ? h->spmv_mode : (h->pt.ok ? 16 : 14);
+  info->a_pairs = (mode_a == 16 && h->pa.ok) ? h->pa.npairs : 0;
+  info->t_pairs = (mode_t == 16 && h->pt.ok) ? h->pt.npairs : 0;
   return SFLSQR_OK;
 }
 
@@ -2046,12 +2170,12 @@ int sflsqr_debug_state(sflsqr_t* h, double* z, double* x, double* p_ring, double
 int sflsqr_debug_set_tuning(sflsqr_t* h, int32_t spmv_mode, int32_t band_shift) {
   if (!h) return fail(nullptr, SFLSQR_E_INVALID, "NULL handle");
   const bool ok_mode = spmv_mode == -1 || spmv_mode == 0 || spmv_mode == 1 || spmv_mode == 2 || spmv_mode == 3 ||
-                       spmv_mode == 8 || (spmv_mode >= 10 && spmv_mode <= 15);
+                       spmv_mode == 8 || (spmv_mode >= 10 && spmv_mode <= 16);
   if (!ok_mode || band_shift < 8 || band_shift > 30) return fail(h, SFLSQR_E_INVALID, "bad tuning values");
   h->spmv_mode = spmv_mode;
   h->band_shift = band_shift;
-  if (spmv_mode == 15 && h->op_set) {
-    int rc = build_c16_all(h);
+  if (h->op_set) {
+    int rc = build_formats(h);
     if (rc) return rc;
   }
   if (h->gexec) {

@@ -465,13 +465,25 @@ __device__ __forceinline__ void epi_coefs(const SpmvEpi& E, const DevState* st, 
   }
 }
 
-template <int WPB, int UNR, int LANES, bool EPI = false>
-__global__ void __launch_bounds__(WPB * 32, EPI ? 2 : 2048 / (WPB * 32)) k_spmv_csr_pf(const DevState* st, int64_t nrows,
+// Pair part of a pair-CSR operator (see k_pcsr_rows): entry q stands for the two nonzeros
+// (row, pcol[q]) = pval[q].x and (row, pcol[q] + 1) = pval[q].y.
+struct PairPart {
+  const int64_t* rowptr = nullptr;
+  const int* col = nullptr;
+  const double2* val = nullptr;
+};
+
+// PAIRS = 0: plain CSR; 2 or 4: pair-CSR with that many pairs in flight per lane (64
+// registers: 2 CTAs of 512 threads per SM).
+template <int WPB, int UNR, int LANES, bool EPI = false, int PAIRS = 0>
+__global__ void __launch_bounds__(WPB * 32, (EPI || PAIRS) ? 2 : 2048 / (WPB * 32))
+    k_spmv_csr_pf(const DevState* st, int64_t nrows,
                                                             const int64_t* __restrict__ rowptr,
                                                             const int* __restrict__ col,
                                                             const double* __restrict__ val,
                                                             const double* __restrict__ x_base, int64_t x_ld,
-                                                            int x_koff, double* y, SpmvEpi E = SpmvEpi()) {
+                                                            int x_koff, double* y, SpmvEpi E = SpmvEpi(),
+                                                            PairPart PP = PairPart()) {
   if (st && st->done) return;
   double ea = 1.0, ec = 0.0, nrm = 0.0;
   if (EPI) epi_coefs(E, st, ea, ec);
@@ -487,6 +499,51 @@ __global__ void __launch_bounds__(WPB * 32, EPI ? 2 : 2048 / (WPB * 32)) k_spmv_
       e = rowptr[row + 1];
     }
     double sum = 0.0;
+    if (PAIRS) {
+      // the row's adjacent-column pairs first: 4 B index + 16 B values per two nonzeros
+      int64_t ps = 0, pe = 0;
+      if (row < nrows) {
+        ps = PP.rowptr[row];
+        pe = PP.rowptr[row + 1];
+      }
+      int64_t q = ps + sl;
+      constexpr int PU = PAIRS > 0 ? PAIRS : 1;
+      int cn[PU];
+      double2 vn[PU];
+#pragma unroll
+      for (int u = 0; u < PU; ++u) {
+        const int64_t t = q + (int64_t)LANES * u;
+        cn[u] = t < pe ? ld_stream_i(PP.col + t) : 0;
+        vn[u] = t < pe ? ld_stream_d2(PP.val + t) : make_double2(0.0, 0.0);
+      }
+      while (__any_sync(0xffffffffu, q < pe)) {
+        int c[PU];
+        double2 v[PU];
+#pragma unroll
+        for (int u = 0; u < PU; ++u) {
+          c[u] = cn[u];
+          v[u] = vn[u];
+        }
+        const int64_t qn = q + (int64_t)LANES * PU;
+#pragma unroll
+        for (int u = 0; u < PU; ++u) {
+          const int64_t t = qn + (int64_t)LANES * u;
+          cn[u] = t < pe ? ld_stream_i(PP.col + t) : 0;
+          vn[u] = t < pe ? ld_stream_d2(PP.val + t) : make_double2(0.0, 0.0);
+        }
+        double x0[PU], x1[PU];
+#pragma unroll
+        for (int u = 0; u < PU; ++u) {
+          const bool ok = q + (int64_t)LANES * u < pe;
+          x0[u] = ok ? __ldg(x + c[u]) : 0.0;
+          x1[u] = ok ? __ldg(x + c[u] + 1) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < PU; ++u)
+          if (q + (int64_t)LANES * u < pe) sum = fma(v[u].y, x1[u], fma(v[u].x, x0[u], sum));
+        q = qn;
+      }
+    }
     int64_t p = s + sl;
     int cn[UNR];
     double vn[UNR];
@@ -552,6 +609,71 @@ __global__ void __launch_bounds__(WPB * 32, EPI ? 2 : 2048 / (WPB * 32)) k_spmv_
     if (threadIdx.x == 0) {
       E.scal[E.slot_out] = v;
       E.ctr[E.ctr_idx] = 0;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ pair-CSR (setup)
+// Splits every CSR row into adjacent-column pairs and singletons: each maximal run of
+// consecutive column indices c, c+1, ..., c+L-1 in a row gives floor(L/2) pairs (c, c+1),
+// (c+2, c+3), ... and, when L is odd, one singleton (its last entry).  Pairs are stored as
+// (pcol, double2 values), singletons as plain CSR; the row sum is then the pairs' sum plus the
+// singletons' sum.  One warp per row, 32 entries per step: run starts by ballot, the position
+// of each entry in its run from the last start at or below it (carried across steps).
+// FILL = false: per-row counts into np_cnt / ns_cnt; FILL = true: the entries, at the rows'
+// offsets prp / srp.
+template <bool FILL>
+__global__ void __launch_bounds__(256) k_pcsr_rows(int64_t nrows, const int64_t* __restrict__ rp,
+                                                   const int* __restrict__ col, const double* __restrict__ val,
+                                                   int64_t* np_cnt, int64_t* ns_cnt, const int64_t* __restrict__ prp,
+                                                   const int64_t* __restrict__ srp, int* pcol, double2* pval, int* scol,
+                                                   double* sval) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < nrows;
+       row += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t s = rp[row], e = rp[row + 1];
+    int64_t np = 0, ns = 0;
+    int carry_pos = 0, carry_col = 0;
+    for (int64_t k0 = s; k0 < e; k0 += 32) {
+      const int64_t k = k0 + lane;
+      const bool valid = k < e;
+      const int c = valid ? col[k] : 0;
+      const double v = (FILL && valid) ? val[k] : 0.0;
+      int cprev = __shfl_up_sync(0xffffffffu, c, 1);
+      if (lane == 0) cprev = carry_col;
+      const bool cont = valid && k > s && c == cprev + 1;            // continues the run of entry k-1
+      const unsigned starts = __ballot_sync(0xffffffffu, valid && !cont);
+      const unsigned m = starts & (lt | (1u << lane));
+      const int pos = m ? lane - (31 - __clz(m)) : carry_pos + 1 + lane;
+      const bool ncont = __shfl_down_sync(0xffffffffu, cont, 1);
+      const bool has_next = valid && (lane < 31 ? ncont : (k + 1 < e && col[k + 1] == c + 1));
+      const bool head = valid && !(pos & 1) && has_next;
+      const bool single = valid && !(pos & 1) && !has_next;
+      const unsigned hm = __ballot_sync(0xffffffffu, head), sm = __ballot_sync(0xffffffffu, single);
+      if (FILL) {
+        double v1 = __shfl_down_sync(0xffffffffu, v, 1);
+        if (head && lane == 31) v1 = val[k + 1];
+        if (head) {
+          const int64_t o = prp[row] + np + __popc(hm & lt);
+          pcol[o] = c;
+          pval[o] = make_double2(v, v1);
+        }
+        if (single) {
+          const int64_t o = srp[row] + ns + __popc(sm & lt);
+          scol[o] = c;
+          sval[o] = v;
+        }
+      }
+      np += __popc(hm);
+      ns += __popc(sm);
+      const int last = (int)(e - 1 - k0 < 31 ? e - 1 - k0 : 31);
+      carry_pos = __shfl_sync(0xffffffffu, pos, last);
+      carry_col = __shfl_sync(0xffffffffu, c, last);
+    }
+    if (!FILL && lane == 0) {
+      np_cnt[row] = np;
+      ns_cnt[row] = ns;
     }
   }
 }

@@ -50,7 +50,7 @@ def test_version_and_create_without_gpu(lib):
     import torch
     from paper_2605_22281_b200 import sflsqr as B
     L = B.load_library()
-    assert L.sflsqr_version() == 3
+    assert L.sflsqr_version() == 4
     if torch.cuda.is_available():
         pytest.skip("GPU present: covered by the -m gpu tests")
     with pytest.raises(B.SflsqrError) as ei:

@@ -424,6 +424,65 @@ def test_csr16_bitwise_equal_to_int32_csr_and_oracle():
     s.close()
 
 
+# ------------------------------------------------------------------ pair-CSR (SpMV mode 16)
+def _runs_csr(seed, m, n):
+    """Rows made of runs of consecutive columns (lengths 1..9, odd and even, some rows empty,
+    some longer than 32 entries so runs straddle the kernel's 32-entry steps)."""
+    rng = np.random.default_rng(seed)
+    rows = []
+    for i in range(m):
+        cols, c = [], int(rng.integers(0, 5))
+        target = 0 if i % 17 == 0 else int(rng.integers(1, 120))
+        while len(cols) < target and c < n - 10:
+            L = int(rng.integers(1, 10))
+            cols.extend(range(c, min(c + L, n)))
+            c += L + int(rng.integers(1, 4))
+        rows.append(np.array(cols[:target], dtype=np.int64))
+    rowptr = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.int64)
+    col = np.concatenate(rows).astype(np.int32) if rowptr[-1] else np.zeros(0, np.int32)
+    return rowptr, col, rng.standard_normal(col.size)
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_pair_csr_matches_oracle_matvec(seed):
+    from paper_2605_22281_b200 import SFLSQR
+    m, n = 700, 2000
+    rp, col, val = _runs_csr(seed, m, n)
+    A = OracleCSR(m, n, rp, col, val)
+    At = A.transpose()
+    s = SFLSQR(maxit=4)
+    s.set_operator(m, n, rp, col, val)                       # T = A^T built by the library
+    rng = np.random.default_rng(10 + seed)
+    x, w = rng.standard_normal(n), rng.standard_normal(m)
+    s.debug_set_tuning(16)
+    ya, yt = s.debug_apply(0, x), s.debug_apply(1, w)
+    ra, rt = A.matvec(x), At.matvec(w)
+    absa = OracleCSR(m, n, rp, col, np.abs(val))
+    # each entry within a few ulp of the row's absolute sum (summation order differs)
+    assert np.all(np.abs(ya - ra) <= 1e-14 * absa.matvec(np.abs(x)) + 1e-300)
+    assert np.all(np.abs(yt - rt) <= 1e-14 * absa.transpose().matvec(np.abs(w)) + 1e-300)
+    s.close()
+
+
+def test_pair_csr_solver_parity_unmatched_ct():
+    # sFLSQR on a reduced config-4 problem (pixel-driven B: all pairs; Siddon A: mixed) with
+    # SpMV mode 16 against the oracle, same bar as the mode-14 runs
+    from paper_2605_22281_b200 import solver_for_problem
+    p = make_problem(4, N=96, n_angles=61, nb=137)
+    spec = p.solvers[0]
+    r = solve_problem(p, spec, maxit=12, eta=0.0)
+    s = solver_for_problem(p, spec, maxit=12, eta=0.0)
+    s.debug_set_tuning(16)
+    s.set_rhs(p.b)
+    s.iterate(12)
+    tr, sk = s.get_residual_norms()
+    x = s.get_x()
+    s.close()
+    assert np.max(np.abs(tr - np.array(r.true_res)) / np.array(r.true_res)) < 1e-9
+    assert np.max(np.abs(sk - np.array(r.sketch_res)) / np.array(r.sketch_res)) < 1e-9
+    assert np.linalg.norm(x - r.x) / np.linalg.norm(r.x) < 1e-6
+
+
 def test_csr16_overflow_falls_back_to_int32():
     # a 16-entry chunk spanning > 65536 columns cannot be offset-encoded: the operator stays int32 CSR
     from gen.problems import CSR
