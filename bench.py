@@ -339,8 +339,9 @@ def main():
         bpl = d["bytes"] / d["launches"]
         ach = bpl / (d["ms"] / d["launches"] / 1e3) / 1e9
         inf = s.get_info()
-        fmt = {"spmv_A": "pair-CSR" if inf["a_pairs"] else "CSR", "spmv_T": "pair-CSR" if inf["t_pairs"] else "CSR"}
-        tr = _traffic(prob.name, dom + ("_pcsr" if fmt.get(dom) == "pair-CSR" else ""))
+        fnames = {0: "CSR", 1: "pair-CSR", 2: "aligned pair-CSR"}
+        fmt = {"spmv_A": fnames[inf["a_fmt"]], "spmv_T": fnames[inf["t_fmt"]]}
+        tr = _traffic(prob.name, dom + {"CSR": "", "pair-CSR": "_pcsr", "aligned pair-CSR": "_apcsr"}[fmt.get(dom, "CSR")])
         kname = {"spmv_A": f"k_spmv_csr_pf, {fmt['spmv_A']} (A z)",
                  "spmv_T": f"k_spmv_csr_pf, {fmt['spmv_T']} (T w)"}.get(dom, dom)
         roof = {"bound": "hbm", "kernel": kname, "achieved": ach, "peak": peak,
@@ -383,8 +384,8 @@ def main():
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": prob.name, "method": spec.method, "m": prob.m, "n": prob.n,
                        "nnz_A": nnz_A, "nnz_T": nnz_T,
-                       "spmv_format": {"A": "pair-CSR" if info_end["a_pairs"] else "CSR",
-                                       "T": "pair-CSR" if info_end["t_pairs"] else "CSR",
+                       "spmv_format": {"A": ["CSR", "pair-CSR", "aligned pair-CSR"][info_end["a_fmt"]],
+                                       "T": ["CSR", "pair-CSR", "aligned pair-CSR"][info_end["t_fmt"]],
                                        "pairs_A": info_end["a_pairs"], "pairs_T": info_end["t_pairs"]},
                        "ell": spec.window, "d": spec.d, "s": spec.s_nz, "tau": spec.precond, "maxit": maxit,
                        "iterations_timed": f"{W + 1}..{W + K}", "history": "true residual (W path) on",

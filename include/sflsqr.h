@@ -168,8 +168,9 @@ typedef struct sflsqr_info {
   double bytes_model;  /* algorithmic HBM bytes of iteration k_done on this rank, the model of
                           SURVEY.md §8(d) / DESIGN.md §5 (0 before the first iteration)  */
   int64_t a_pairs, t_pairs; /* adjacent-column pairs of the pair-CSR copy the A / T products
-                          run on (SpMV mode 16: 10 instead of 12 bytes per paired nonzero);
-                          0 = plain CSR                                                  */
+                          run on (10 instead of 12 bytes per paired nonzero); 0 = plain CSR */
+  int32_t a_fmt, t_fmt; /* SpMV format of the A / T products: 0 CSR, 1 pair-CSR (any adjacent
+                          pair), 2 aligned pair-CSR (pairs at even columns, 16-byte gathers)  */
 } sflsqr_info;
 
 /* Per-kernel-class device time, recorded with CUDA events on the library stream

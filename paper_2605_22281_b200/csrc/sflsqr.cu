@@ -45,6 +45,7 @@ enum TKind { T_FULL = 0, T_ROWSHARD = 1, T_COLSHARD = 2 };
 // 16-bit offsets, chunk pointer per row.  ok = false: the operator stays int32 CSR.
 struct PCSR {  // pair-CSR copy of an operator (k_pcsr_rows): pairs + singleton CSR
   bool ok = false;
+  bool aligned = false;  // pairs only at even columns (gathered as one 16-byte load)
   int64_t npairs = 0, nsingles = 0;
   int64_t* prp = nullptr;
   int* pcol = nullptr;
@@ -437,15 +438,20 @@ void enqueue_apply(sflsqr_t* h, int which, const DevState* st, const double* x, 
   const PCSR& pc = which == 0 ? h->pa : h->pt;
   int mode = h->spmv_mode >= 0 ? h->spmv_mode : (pc.ok ? 16 : select_spmv_mode(nnz, nrows));
   if (mode == 15 && !cc.ok) mode = 14;
-  if (mode == 16 && !pc.ok) mode = 14;
-  if (mode == 16) {
+  if ((mode == 16 || mode == 17) && !pc.ok) mode = 14;
+  if (mode == 16 || mode == 17) {
     // pair-CSR: 20 bytes per pair of nonzeros, 12 per singleton, two row pointer arrays
     L.bytes_override(20.0 * pc.npairs + 12.0 * pc.nsingles + 16.0 * (nrows + 1) + 8.0 * xlen + 8.0 * nrows);
     PairPart PP;
     PP.rowptr = pc.prp;
     PP.col = pc.pcol;
     PP.val = pc.pval;
-    if (h->pcsr_unroll == 4)
+    // aligned pairs gather one 16-byte value pair: needs x (any k-relative column) 16-byte aligned
+    const bool x16 = ((uintptr_t)x % 16 == 0) && (x_ld % 2 == 0);
+    if (pc.aligned && x16)
+      k_spmv_csr_pf<16, 4, 16, false, 5><<<grid_for(32, 2), 512, 0, h->stream>>>(
+          st, nrows, pc.srp, pc.scol, pc.sval, x, x_ld, x_koff, y, SpmvEpi(), PP);
+    else if (h->pcsr_unroll == 4)
       k_spmv_csr_pf<16, 4, 16, false, 4><<<grid_for(32, 2), 512, 0, h->stream>>>(
           st, nrows, pc.srp, pc.scol, pc.sval, x, x_ld, x_koff, y, SpmvEpi(), PP);
     else
@@ -1018,7 +1024,10 @@ int build_c16_all(sflsqr_t* h) {
 int check_launch(sflsqr_t* h);
 
 // Pair-CSR copy of one operator (k_pcsr_rows): counts, two exclusive scans, fill.
-int build_pcsr(sflsqr_t* h, int64_t nrows, const int64_t* rp, const int32_t* col, const double* val, PCSR& p) {
+// min_frac: leave the operator plain (p.ok = false) unless at least that fraction of its nonzeros
+// pairs up (decided after the count pass, before any fill).
+int build_pcsr(sflsqr_t* h, int64_t nrows, const int64_t* rp, const int32_t* col, const double* val, PCSR& p,
+               bool aligned = false, double min_frac = 0.0) {
   free_pcsr(p);
   if (nrows < 1) return SFLSQR_OK;
   int64_t *cp = nullptr, *cs = nullptr;
@@ -1041,8 +1050,12 @@ int build_pcsr(sflsqr_t* h, int64_t nrows, const int64_t* rp, const int32_t* col
   CU(h, cudaMemsetAsync(cp + nrows, 0, sizeof(int64_t), h->stream));
   CU(h, cudaMemsetAsync(cs + nrows, 0, sizeof(int64_t), h->stream));
   const int g = (int)std::min<int64_t>((nrows + 7) / 8, 148 * 64);
-  k_pcsr_rows<false><<<g, 256, 0, h->stream>>>(nrows, rp, col, val, cp, cs, nullptr, nullptr, nullptr, nullptr, nullptr,
-                                               nullptr);
+  if (aligned)
+    k_pcsr_rows<false, true><<<g, 256, 0, h->stream>>>(nrows, rp, col, val, cp, cs, nullptr, nullptr, nullptr, nullptr,
+                                                       nullptr, nullptr);
+  else
+    k_pcsr_rows<false><<<g, 256, 0, h->stream>>>(nrows, rp, col, val, cp, cs, nullptr, nullptr, nullptr, nullptr,
+                                                 nullptr, nullptr);
   cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cp, p.prp, nrows + 1, h->stream);
   if ((rc = dalloc(h, &tmp, tmp_bytes, nullptr))) {
     cleanup();
@@ -1054,6 +1067,11 @@ int build_pcsr(sflsqr_t* h, int64_t nrows, const int64_t* rp, const int32_t* col
   CU(h, cudaMemcpyAsync(&p.npairs, p.prp + nrows, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
   CU(h, cudaMemcpyAsync(&p.nsingles, p.srp + nrows, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
   CU(h, cudaStreamSynchronize(h->stream));
+  if (2.0 * p.npairs < min_frac * (double)(2 * p.npairs + p.nsingles)) {
+    cleanup();
+    free_pcsr(p);
+    return SFLSQR_OK;
+  }
   if ((rc = dalloc(h, (void**)&p.pcol, sizeof(int) * std::max<int64_t>(p.npairs, 1), nullptr)) ||
       (rc = dalloc(h, (void**)&p.pval, sizeof(double2) * std::max<int64_t>(p.npairs, 1), nullptr)) ||
       (rc = dalloc(h, (void**)&p.scol, sizeof(int) * std::max<int64_t>(p.nsingles, 1), nullptr)) ||
@@ -1062,8 +1080,12 @@ int build_pcsr(sflsqr_t* h, int64_t nrows, const int64_t* rp, const int32_t* col
     free_pcsr(p);
     return rc;
   }
-  k_pcsr_rows<true><<<g, 256, 0, h->stream>>>(nrows, rp, col, val, nullptr, nullptr, p.prp, p.srp, p.pcol, p.pval,
-                                              p.scol, p.sval);
+  if (aligned)
+    k_pcsr_rows<true, true><<<g, 256, 0, h->stream>>>(nrows, rp, col, val, nullptr, nullptr, p.prp, p.srp, p.pcol,
+                                                      p.pval, p.scol, p.sval);
+  else
+    k_pcsr_rows<true><<<g, 256, 0, h->stream>>>(nrows, rp, col, val, nullptr, nullptr, p.prp, p.srp, p.pcol, p.pval,
+                                                p.scol, p.sval);
   CU(h, cudaStreamSynchronize(h->stream));
   cleanup();
   if ((rc = check_launch(h))) {
@@ -1071,6 +1093,7 @@ int build_pcsr(sflsqr_t* h, int64_t nrows, const int64_t* rp, const int32_t* col
     return rc;
   }
   p.ok = true;
+  p.aligned = aligned;
   return SFLSQR_OK;
 }
 
@@ -1079,15 +1102,30 @@ int build_formats(sflsqr_t* h) {
   if (h->blur) return SFLSQR_OK;
   if (h->spmv_mode == 15) return build_c16_all(h);
   int rc;
-  if (h->spmv_mode == 16) {
-    if (!h->pa.ok && (rc = build_pcsr(h, h->m_loc, h->a_rowptr, h->a_col, h->a_val, h->pa))) return rc;
-    if (!h->pt.ok && (rc = build_pcsr(h, h->t_rows, h->t_rowptr, h->t_col, h->t_val, h->pt))) return rc;
-  } else if (h->spmv_mode < 0 && !h->pt.ok && h->nnz_t > 0) {
-    // default rule: the transpose-side operator runs as pair-CSR when at least 75 % of its
-    // nonzeros pair up (>= 12.5 % fewer bytes; the pixel-driven B of config 4: 100 %); the
-    // forward Siddon product is L1-gather bound and gains nothing
-    if ((rc = build_pcsr(h, h->t_rows, h->t_rowptr, h->t_col, h->t_val, h->pt))) return rc;
-    if (2.0 * h->pt.npairs < 0.75 * (double)h->nnz_t) free_pcsr(h->pt);
+  if (h->spmv_mode == 16 || h->spmv_mode == 17) {
+    const bool al = h->spmv_mode == 17;
+    if ((!h->pa.ok || h->pa.aligned != al) &&
+        (rc = build_pcsr(h, h->m_loc, h->a_rowptr, h->a_col, h->a_val, h->pa, al)))
+      return rc;
+    if ((!h->pt.ok || h->pt.aligned != al) &&
+        (rc = build_pcsr(h, h->t_rows, h->t_rowptr, h->t_col, h->t_val, h->pt, al)))
+      return rc;
+  } else if (h->spmv_mode < 0 && h->o.method < SFLSQR_METHOD_LSQR) {
+    // default rule per operator: pair-CSR when at least 75 % of the nonzeros pair
+    // up (>= 12.5 % fewer bytes for the DRAM-bound product; the pixel-driven B of config 4: 100 %),
+    // else aligned pair-CSR when at least 40 % sit in even-column pairs (16-byte gathers: fewer L1
+    // wavefronts for the gather-bound Siddon products, ~50 %), else plain CSR.  The GKB methods run
+    // fused-epilogue CSR kernels and keep plain CSR.
+    auto pick = [&](int64_t nrows, const int64_t* rp, const int32_t* col, const double* val, int64_t nnz,
+                    PCSR& p) -> int {
+      if (p.ok || nnz <= 0) return SFLSQR_OK;
+      int r;
+      if ((r = build_pcsr(h, nrows, rp, col, val, p, false, 0.75))) return r;
+      if (p.ok) return SFLSQR_OK;
+      return build_pcsr(h, nrows, rp, col, val, p, true, 0.40);
+    };
+    if ((rc = pick(h->m_loc, h->a_rowptr, h->a_col, h->a_val, h->nnz_a, h->pa))) return rc;
+    if ((rc = pick(h->t_rows, h->t_rowptr, h->t_col, h->t_val, h->nnz_t, h->pt))) return rc;
   }
   return SFLSQR_OK;
 }
@@ -2030,8 +2068,10 @@ int sflsqr_get_info(sflsqr_t* h, sflsqr_info* info) {
   info->delta_e = h->o.delta_e;
   const int mode_a = h->spmv_mode >= 0 ? h->spmv_mode : (h->pa.ok ? 16 : 14);
   const int mode_t = h->spmv_mode >= 0 ? h->spmv_mode : (h->pt.ok ? 16 : 14);
-  info->a_pairs = (mode_a == 16 && h->pa.ok) ? h->pa.npairs : 0;
-  info->t_pairs = (mode_t == 16 && h->pt.ok) ? h->pt.npairs : 0;
+  info->a_pairs = ((mode_a == 16 || mode_a == 17) && h->pa.ok) ? h->pa.npairs : 0;
+  info->t_pairs = ((mode_t == 16 || mode_t == 17) && h->pt.ok) ? h->pt.npairs : 0;
+  info->a_fmt = info->a_pairs ? (h->pa.aligned ? 2 : 1) : 0;
+  info->t_fmt = info->t_pairs ? (h->pt.aligned ? 2 : 1) : 0;
   return SFLSQR_OK;
 }
 
@@ -2170,7 +2210,7 @@ int sflsqr_debug_state(sflsqr_t* h, double* z, double* x, double* p_ring, double
 int sflsqr_debug_set_tuning(sflsqr_t* h, int32_t spmv_mode, int32_t band_shift) {
   if (!h) return fail(nullptr, SFLSQR_E_INVALID, "NULL handle");
   const bool ok_mode = spmv_mode == -1 || spmv_mode == 0 || spmv_mode == 1 || spmv_mode == 2 || spmv_mode == 3 ||
-                       spmv_mode == 8 || (spmv_mode >= 10 && spmv_mode <= 16);
+                       spmv_mode == 8 || (spmv_mode >= 10 && spmv_mode <= 17);
   if (!ok_mode || band_shift < 8 || band_shift > 30) return fail(h, SFLSQR_E_INVALID, "bad tuning values");
   h->spmv_mode = spmv_mode;
   h->band_shift = band_shift;

@@ -474,7 +474,8 @@ struct PairPart {
 };
 
 // PAIRS = 0: plain CSR; 2 or 4: pair-CSR with that many pairs in flight per lane (64
-// registers: 2 CTAs of 512 threads per SM).
+// registers: 2 CTAs of 512 threads per SM); 5: 4 in flight, aligned pairs (c even) gathered as
+// one 16-byte load (x must be 16-byte aligned).
 template <int WPB, int UNR, int LANES, bool EPI = false, int PAIRS = 0>
 __global__ void __launch_bounds__(WPB * 32, (EPI || PAIRS) ? 2 : 2048 / (WPB * 32))
     k_spmv_csr_pf(const DevState* st, int64_t nrows,
@@ -507,7 +508,7 @@ __global__ void __launch_bounds__(WPB * 32, (EPI || PAIRS) ? 2 : 2048 / (WPB * 3
         pe = PP.rowptr[row + 1];
       }
       int64_t q = ps + sl;
-      constexpr int PU = PAIRS > 0 ? PAIRS : 1;
+      constexpr int PU = PAIRS == 5 ? 4 : (PAIRS > 0 ? PAIRS : 1);
       int cn[PU];
       double2 vn[PU];
 #pragma unroll
@@ -535,8 +536,14 @@ __global__ void __launch_bounds__(WPB * 32, (EPI || PAIRS) ? 2 : 2048 / (WPB * 3
 #pragma unroll
         for (int u = 0; u < PU; ++u) {
           const bool ok = q + (int64_t)LANES * u < pe;
-          x0[u] = ok ? __ldg(x + c[u]) : 0.0;
-          x1[u] = ok ? __ldg(x + c[u] + 1) : 0.0;
+          if (PAIRS == 5) {
+            const double2 xx = ok ? __ldg(reinterpret_cast<const double2*>(x + c[u])) : make_double2(0.0, 0.0);
+            x0[u] = xx.x;
+            x1[u] = xx.y;
+          } else {
+            x0[u] = ok ? __ldg(x + c[u]) : 0.0;
+            x1[u] = ok ? __ldg(x + c[u] + 1) : 0.0;
+          }
         }
 #pragma unroll
         for (int u = 0; u < PU; ++u)
@@ -622,7 +629,9 @@ __global__ void __launch_bounds__(WPB * 32, (EPI || PAIRS) ? 2 : 2048 / (WPB * 3
 // of each entry in its run from the last start at or below it (carried across steps).
 // FILL = false: per-row counts into np_cnt / ns_cnt; FILL = true: the entries, at the rows'
 // offsets prp / srp.
-template <bool FILL>
+// ALIGNED: pairs only at even columns (c even, c+1): a pair's two gathered values are then one
+// 16-byte load; every other entry is a singleton.
+template <bool FILL, bool ALIGNED = false>
 __global__ void __launch_bounds__(256) k_pcsr_rows(int64_t nrows, const int64_t* __restrict__ rp,
                                                    const int* __restrict__ col, const double* __restrict__ val,
                                                    int64_t* np_cnt, int64_t* ns_cnt, const int64_t* __restrict__ prp,
@@ -648,8 +657,8 @@ __global__ void __launch_bounds__(256) k_pcsr_rows(int64_t nrows, const int64_t*
       const int pos = m ? lane - (31 - __clz(m)) : carry_pos + 1 + lane;
       const bool ncont = __shfl_down_sync(0xffffffffu, cont, 1);
       const bool has_next = valid && (lane < 31 ? ncont : (k + 1 < e && col[k + 1] == c + 1));
-      const bool head = valid && !(pos & 1) && has_next;
-      const bool single = valid && !(pos & 1) && !has_next;
+      const bool head = ALIGNED ? (valid && !(c & 1) && has_next) : (valid && !(pos & 1) && has_next);
+      const bool single = ALIGNED ? (valid && !head && !((c & 1) && cont)) : (valid && !(pos & 1) && !has_next);
       const unsigned hm = __ballot_sync(0xffffffffu, head), sm = __ballot_sync(0xffffffffu, single);
       if (FILL) {
         double v1 = __shfl_down_sync(0xffffffffu, v, 1);

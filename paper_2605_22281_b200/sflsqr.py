@@ -63,7 +63,8 @@ class Info(ctypes.Structure):
                 ("nnz_a", ctypes.c_int64), ("nnz_t", ctypes.c_int64), ("launches", ctypes.c_int64),
                 ("beta", ctypes.c_double), ("m0", ctypes.c_int64), ("m_loc", ctypes.c_int64),
                 ("n0", ctypes.c_int64), ("n_loc", ctypes.c_int64), ("delta_e", ctypes.c_double),
-                ("bytes_model", ctypes.c_double), ("a_pairs", ctypes.c_int64), ("t_pairs", ctypes.c_int64)]
+                ("bytes_model", ctypes.c_double), ("a_pairs", ctypes.c_int64), ("t_pairs", ctypes.c_int64),
+                ("a_fmt", ctypes.c_int32), ("t_fmt", ctypes.c_int32)]
 
 
 class Profile(ctypes.Structure):

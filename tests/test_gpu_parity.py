@@ -443,8 +443,9 @@ def _runs_csr(seed, m, n):
     return rowptr, col, rng.standard_normal(col.size)
 
 
+@pytest.mark.parametrize("mode", [16, 17])   # 17: pairs only at even columns, 16-byte gathers
 @pytest.mark.parametrize("seed", [0, 1])
-def test_pair_csr_matches_oracle_matvec(seed):
+def test_pair_csr_matches_oracle_matvec(seed, mode):
     from paper_2605_22281_b200 import SFLSQR
     m, n = 700, 2000
     rp, col, val = _runs_csr(seed, m, n)
@@ -454,7 +455,7 @@ def test_pair_csr_matches_oracle_matvec(seed):
     s.set_operator(m, n, rp, col, val)                       # T = A^T built by the library
     rng = np.random.default_rng(10 + seed)
     x, w = rng.standard_normal(n), rng.standard_normal(m)
-    s.debug_set_tuning(16)
+    s.debug_set_tuning(mode)
     ya, yt = s.debug_apply(0, x), s.debug_apply(1, w)
     ra, rt = A.matvec(x), At.matvec(w)
     absa = OracleCSR(m, n, rp, col, np.abs(val))
@@ -464,15 +465,16 @@ def test_pair_csr_matches_oracle_matvec(seed):
     s.close()
 
 
-def test_pair_csr_solver_parity_unmatched_ct():
+@pytest.mark.parametrize("mode", [16, 17])
+def test_pair_csr_solver_parity_unmatched_ct(mode):
     # sFLSQR on a reduced config-4 problem (pixel-driven B: all pairs; Siddon A: mixed) with
-    # SpMV mode 16 against the oracle, same bar as the mode-14 runs
+    # SpMV mode 16 / 17 against the oracle, same bar as the mode-14 runs
     from paper_2605_22281_b200 import solver_for_problem
     p = make_problem(4, N=96, n_angles=61, nb=137)
     spec = p.solvers[0]
     r = solve_problem(p, spec, maxit=12, eta=0.0)
     s = solver_for_problem(p, spec, maxit=12, eta=0.0)
-    s.debug_set_tuning(16)
+    s.debug_set_tuning(mode)
     s.set_rhs(p.b)
     s.iterate(12)
     tr, sk = s.get_residual_norms()
@@ -481,6 +483,23 @@ def test_pair_csr_solver_parity_unmatched_ct():
     assert np.max(np.abs(tr - np.array(r.true_res)) / np.array(r.true_res)) < 1e-9
     assert np.max(np.abs(sk - np.array(r.sketch_res)) / np.array(r.sketch_res)) < 1e-9
     assert np.linalg.norm(x - r.x) / np.linalg.norm(r.x) < 1e-6
+
+
+def test_default_spmv_format_rule():
+    # >= 75 % adjacent pairs -> pair-CSR (the pixel-driven B), else >= 40 % even-column
+    # pairs -> aligned pair-CSR (Siddon), else CSR; the GKB methods keep CSR
+    from paper_2605_22281_b200 import solver_for_problem
+    p = make_problem(4, N=96, n_angles=61, nb=137)
+    spec = p.solvers[0]
+    s = solver_for_problem(p, spec, maxit=3, eta=0.0)
+    inf = s.get_info()
+    s.close()
+    assert inf["t_fmt"] == 1 and inf["t_pairs"] == p.T.nnz // 2 or inf["t_pairs"] >= 0.375 * p.T.nnz
+    assert inf["a_fmt"] == 2 and inf["a_pairs"] >= 0.2 * p.A.nnz
+    s = solver_for_problem(p, spec, maxit=3, eta=0.0, method="lsqr")
+    inf = s.get_info()
+    s.close()
+    assert inf["a_fmt"] == 0 and inf["t_fmt"] == 0 and inf["a_pairs"] == 0 and inf["t_pairs"] == 0
 
 
 def test_csr16_overflow_falls_back_to_int32():
