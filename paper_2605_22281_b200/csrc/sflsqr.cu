@@ -404,6 +404,9 @@ int select_spmv_mode(int64_t nnz, int64_t nrows) {
   return 14;
 }
 
+bool launch_pairs_epi(sflsqr_t* h, int which, const double* x, int64_t x_ld, double* y, const SpmvEpi& E, int cls,
+                      double extra, int grid);
+
 // y = A x (which 0) or y = T x (which 1) for this rank's shard; x may be a
 // k-relative column (x_ld != 0).
 void enqueue_apply(sflsqr_t* h, int which, const DevState* st, const double* x, int64_t x_ld, int x_koff, double* y,
@@ -596,10 +599,10 @@ int enqueue_transpose_product(sflsqr_t* h, bool init) {
     E.src = h->rank;
     E.nmax = h->n_max;
     for (int g = 0; g < 8; ++g) E.peers[g] = static_cast<double*>(h->peer_zrecv[g]);
-    {
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((h->t_rows + 31) / 32, 148 * 4));
+    if (!launch_pairs_epi(h, 1, P.W, ld, nullptr, E, SFLSQR_KC_SPMV_T, 0.0, grid)) {
       const double bytes = 12.0 * h->nnz_t + 8.0 * (h->t_rows + 1) + 16.0 * h->m_loc + 8.0 * h->t_rows;
       Launch L(h, SFLSQR_KC_SPMV_T, bytes);
-      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((h->t_rows + 31) / 32, 148 * 4));
       k_spmv_csr_pf<16, 4, 16, true><<<grid, 512, 0, h->stream>>>(P.st, h->t_rows, h->t_rowptr, h->t_col, h->t_val,
                                                                    P.W, ld, 0, nullptr, E);
     }
@@ -671,6 +674,30 @@ int enqueue_orth(sflsqr_t* h, int side, int koff) {
 
 // GKB product with its epilogue (methods 4 / 5): fused into the default CSR kernel, or a
 // plain product followed by k_epi_vec (blur operator / a forced SpMV variant).
+// Fused-epilogue product on the operator's pair-CSR copy (if it has one): returns false when
+// the operator runs as plain CSR (the caller launches the CSR kernel).  extra: epilogue bytes.
+bool launch_pairs_epi(sflsqr_t* h, int which, const double* x, int64_t x_ld, double* y, const SpmvEpi& E, int cls,
+                      double extra, int grid) {
+  const PCSR& pc = which == 0 ? h->pa : h->pt;
+  const int mode = h->spmv_mode >= 0 ? h->spmv_mode : (pc.ok ? 16 : 14);
+  if (h->blur || !pc.ok || (mode != 16 && mode != 17)) return false;
+  const int64_t nrows = which == 0 ? h->m_loc : h->t_rows;
+  const int64_t xlen = which == 0 ? (h->world > 1 ? h->world * h->n_max : h->n)
+                                  : (h->tkind == T_ROWSHARD ? h->world * h->m_max : h->m_loc);
+  Launch L(h, cls, 20.0 * pc.npairs + 12.0 * pc.nsingles + 16.0 * (nrows + 1) + 8.0 * xlen + 8.0 * nrows + extra);
+  PairPart PP;
+  PP.rowptr = pc.prp;
+  PP.col = pc.pcol;
+  PP.val = pc.pval;
+  if (pc.aligned && (uintptr_t)x % 16 == 0 && x_ld % 2 == 0)
+    k_spmv_csr_pf<16, 4, 16, true, 5><<<grid, 512, 0, h->stream>>>(h->P.st, nrows, pc.srp, pc.scol, pc.sval, x, x_ld,
+                                                                    0, y, E, PP);
+  else
+    k_spmv_csr_pf<16, 4, 16, true, 4><<<grid, 512, 0, h->stream>>>(h->P.st, nrows, pc.srp, pc.scol, pc.sval, x, x_ld,
+                                                                    0, y, E, PP);
+  return true;
+}
+
 void enqueue_apply_gkb(sflsqr_t* h, int which, const double* x, double* y, int kind, int slot_in, int slot_out,
                        int ctr_idx) {
   Params& P = h->P;
@@ -687,6 +714,9 @@ void enqueue_apply_gkb(sflsqr_t* h, int which, const double* x, double* y, int k
   const int64_t nrows = which == 0 ? h->m_loc : h->t_rows;
   const int mode = h->spmv_mode >= 0 ? h->spmv_mode : 14;
   const int cls = which == 0 ? SFLSQR_KC_SPMV_A : SFLSQR_KC_SPMV_T;
+  if (launch_pairs_epi(h, which, x, 0, y, E, cls, kind == 3 ? 0.0 : 8.0 * nrows,
+                       (int)std::max<int64_t>(1, std::min<int64_t>((nrows + 31) / 32, 148 * 4))))
+    return;
   if (!h->blur && mode == 14) {
     const int64_t nnz = which == 0 ? h->nnz_a : h->nnz_t;
     const int64_t xlen = which == 0 ? h->n : h->m;
@@ -1110,12 +1140,11 @@ int build_formats(sflsqr_t* h) {
     if ((!h->pt.ok || h->pt.aligned != al) &&
         (rc = build_pcsr(h, h->t_rows, h->t_rowptr, h->t_col, h->t_val, h->pt, al)))
       return rc;
-  } else if (h->spmv_mode < 0 && h->o.method < SFLSQR_METHOD_LSQR) {
+  } else if (h->spmv_mode < 0) {
     // default rule per operator: pair-CSR when at least 75 % of the nonzeros pair
     // up (>= 12.5 % fewer bytes for the DRAM-bound product; the pixel-driven B of config 4: 100 %),
     // else aligned pair-CSR when at least 40 % sit in even-column pairs (16-byte gathers: fewer L1
-    // wavefronts for the gather-bound Siddon products, ~50 %), else plain CSR.  The GKB methods run
-    // fused-epilogue CSR kernels and keep plain CSR.
+    // wavefronts for the gather-bound Siddon products, ~50 %), else plain CSR.
     auto pick = [&](int64_t nrows, const int64_t* rp, const int32_t* col, const double* val, int64_t nnz,
                     PCSR& p) -> int {
       if (p.ok || nnz <= 0) return SFLSQR_OK;

@@ -487,7 +487,7 @@ def test_pair_csr_solver_parity_unmatched_ct(mode):
 
 def test_default_spmv_format_rule():
     # >= 75 % adjacent pairs -> pair-CSR (the pixel-driven B), else >= 40 % even-column
-    # pairs -> aligned pair-CSR (Siddon), else CSR; the GKB methods keep CSR
+    # pairs -> aligned pair-CSR (Siddon), else CSR; the same for the GKB methods (fused epilogues)
     from paper_2605_22281_b200 import solver_for_problem
     p = make_problem(4, N=96, n_angles=61, nb=137)
     spec = p.solvers[0]
@@ -497,6 +497,11 @@ def test_default_spmv_format_rule():
     assert inf["t_fmt"] == 1 and inf["t_pairs"] == p.T.nnz // 2 or inf["t_pairs"] >= 0.375 * p.T.nnz
     assert inf["a_fmt"] == 2 and inf["a_pairs"] >= 0.2 * p.A.nnz
     s = solver_for_problem(p, spec, maxit=3, eta=0.0, method="lsqr")
+    inf = s.get_info()
+    s.close()
+    assert inf["a_fmt"] == 2 and inf["t_fmt"] == 1
+    s = solver_for_problem(p, spec, maxit=3, eta=0.0)
+    s.debug_set_tuning(14)                                 # forced plain CSR
     inf = s.get_info()
     s.close()
     assert inf["a_fmt"] == 0 and inf["t_fmt"] == 0 and inf["a_pairs"] == 0 and inf["t_pairs"] == 0
