@@ -1143,15 +1143,18 @@ int build_formats(sflsqr_t* h) {
   } else if (h->spmv_mode < 0) {
     // default rule per operator: pair-CSR when at least 75 % of the nonzeros pair
     // up (>= 12.5 % fewer bytes for the DRAM-bound product; the pixel-driven B of config 4: 100 %),
-    // else aligned pair-CSR when at least 40 % sit in even-column pairs (16-byte gathers: fewer L1
-    // wavefronts for the gather-bound Siddon products, ~50 %), else plain CSR.
+    // else aligned pair-CSR when at least 20 % sit in even-column pairs (16-byte gathers: fewer L1
+    // wavefronts; Siddon A: 50 %, Siddon A^T: 21 %), else plain CSR; rows of >= 64 nonzeros on
+    // average only.
     auto pick = [&](int64_t nrows, const int64_t* rp, const int32_t* col, const double* val, int64_t nnz,
                     PCSR& p) -> int {
-      if (p.ok || nnz <= 0) return SFLSQR_OK;
+      // short rows (< 64 nonzeros on average, e.g. the 5 x 5 stencil rows of config 8) lose more to
+      // the second loop and the 64-register kernel than the pairs save (measured): plain CSR
+      if (p.ok || nnz <= 0 || nnz < 64 * nrows) return SFLSQR_OK;
       int r;
       if ((r = build_pcsr(h, nrows, rp, col, val, p, false, 0.75))) return r;
       if (p.ok) return SFLSQR_OK;
-      return build_pcsr(h, nrows, rp, col, val, p, true, 0.40);
+      return build_pcsr(h, nrows, rp, col, val, p, true, 0.20);
     };
     if ((rc = pick(h->m_loc, h->a_rowptr, h->a_col, h->a_val, h->nnz_a, h->pa))) return rc;
     if ((rc = pick(h->t_rows, h->t_rowptr, h->t_col, h->t_val, h->nnz_t, h->pt))) return rc;

@@ -486,7 +486,7 @@ def test_pair_csr_solver_parity_unmatched_ct(mode):
 
 
 def test_default_spmv_format_rule():
-    # >= 75 % adjacent pairs -> pair-CSR (the pixel-driven B), else >= 40 % even-column
+    # >= 75 % adjacent pairs -> pair-CSR (the pixel-driven B), else >= 20 % even-column
     # pairs -> aligned pair-CSR (Siddon), else CSR; the same for the GKB methods (fused epilogues)
     from paper_2605_22281_b200 import solver_for_problem
     p = make_problem(4, N=96, n_angles=61, nb=137)
