@@ -70,7 +70,11 @@ struct sflsqr {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   cudaStream_t side = nullptr;  // second stream: the projected LS overlaps the T product (fork/join)
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_w = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_w = nullptr, ev_sk = nullptr;
+  bool axpy_wait_sk = false;  // enqueue_orth(side 1): wait for ev_sk (sketch on the side stream) before writing w
+  // sFLSQR's sketch of A z on the side stream beside the w-side dots (SFLSQR_SKETCH_SIDE=0: main
+  // stream): config 1 +6 %, config 2 +1 %, config 3 +2 %, config 4 unchanged (same box)
+  bool sketch_side = true;
   std::string err;
   // distribution
   int rank = 0, world = 1;
@@ -562,17 +566,18 @@ void launch_res(sflsqr_t* h, cudaStream_t s, int fuse_stop) {
 }
 
 // skbuf = S v (this rank's coordinates), allreduced over ranks.
-int enqueue_sketch(sflsqr_t* h, const DevState* st, const double* v) {
+int enqueue_sketch(sflsqr_t* h, const DevState* st, const double* v, cudaStream_t strm = nullptr) {
   const int64_t dim_loc = h->P.method == SFLSQR_METHOD_SFLSQR ? h->m_loc : h->n_loc;
+  cudaStream_t ss = strm ? strm : h->stream;
   if (h->sk_kind == 1) {
     Launch L(h, SFLSQR_KC_SKETCH, 8.0 * h->d * dim_loc + 8.0 * dim_loc + 8.0 * h->d);
-    k_sketch_dense<<<std::min(h->d, 148 * 8), 256, 0, h->stream>>>(st, h->P.sk_dense, dim_loc, v, h->d, h->P.skbuf);
+    k_sketch_dense<<<std::min(h->d, 148 * 8), 256, 0, ss>>>(st, h->P.sk_dense, dim_loc, v, h->d, h->P.skbuf);
   } else {
     Launch L(h, SFLSQR_KC_SKETCH, 12.0 * h->s_nz * dim_loc + 8.0 * (h->d + 1) + 8.0 * h->d);
     const int grid = std::min(h->d, 148 * 8);
-    k_sketch_apply<<<grid, kSkApplyThreads, 0, h->stream>>>(st, h->P.sk_rp, h->P.sk_ent, v, h->d, h->P.sk_scale,
-                                                            h->P.skbuf);
+    k_sketch_apply<<<grid, kSkApplyThreads, 0, ss>>>(st, h->P.sk_rp, h->P.sk_ent, v, h->d, h->P.sk_scale, h->P.skbuf);
   }
+  if (strm) return SFLSQR_OK;  // one rank only (no collective on the side stream)
   return coll_allreduce(h, h->P.skbuf, h->d, false);
 }
 
@@ -642,12 +647,14 @@ int enqueue_orth(sflsqr_t* h, int side, int koff) {
       k_orth_dots<<<vec_grid(side == 0 ? h->n_loc : h->m_loc), kVecThreads, 0, h->stream>>>(P, side, koff);
     }
     if ((rc = coll_allreduce(h, P.scal + slot_f, kFuseAcc, false))) return rc;
+    if (side == 1 && h->axpy_wait_sk) CU(h, cudaStreamWaitEvent(h->stream, h->ev_sk, 0));
     {
       Launch L(h, SFLSQR_KC_ORTH, v8 * (2 + J));
       k_orth_axpy<<<vec_grid(side == 0 ? h->n_loc : h->m_loc), kVecThreads, 0, h->stream>>>(P, side, koff);
     }
     return coll_allreduce(h, P.scal + slot_out, 1, false);
   }
+  if (side == 1 && h->axpy_wait_sk) CU(h, cudaStreamWaitEvent(h->stream, h->ev_sk, 0));
   if (P.orth_alg == ORTH_CGS2) {
     const size_t sm_dots = sizeof(double) * (kCgsChunk + P.ldc), sm_upd = sizeof(double) * 2 * P.ldc;
     for (int stage = 0; stage < 2; ++stage) {
@@ -907,8 +914,19 @@ int enqueue_iteration(sflsqr_t* h) {
   if (coop && (rc = launch_coop(h, k_wphase,
                                 m8 * (4 + 2 * Jw) + (P.method == SFLSQR_METHOD_SFLSQR ? 12.0 * h->s_nz * h->m_loc : 0.0))))
     return rc;
-  // a4 (sFLSQR): S_AZ[:, k] = S w
-  if (!coop && P.method == SFLSQR_METHOD_SFLSQR && (rc = enqueue_sketch(h, P.st, P.w))) return rc;
+  // a4 (sFLSQR): S_AZ[:, k] = S w -- on the side stream (one rank), beside the w-side dots; the
+  // in-place w update waits for it (SFLSQR_SKETCH_SIDE)
+  const bool sk_side = h->sketch_side && !coop && P.method == SFLSQR_METHOD_SFLSQR && h->world == 1 && h->side &&
+                       !h->prof_on;
+  if (sk_side) {
+    CU(h, cudaEventRecord(h->ev_fork, h->stream));
+    CU(h, cudaStreamWaitEvent(h->side, h->ev_fork, 0));
+    if ((rc = enqueue_sketch(h, P.st, P.w, h->side))) return rc;
+    CU(h, cudaEventRecord(h->ev_sk, h->side));
+    h->axpy_wait_sk = true;
+  } else if (!coop && P.method == SFLSQR_METHOD_SFLSQR && (rc = enqueue_sketch(h, P.st, P.w))) {
+    return rc;
+  }
   // a7 can start now for sFLSQR (it needs only S A Z_k) / after a5 for FLSQR (it needs
   // H_{:,k}): it runs on the side stream, overlapped with the T product (a6), and is
   // joined before a8.  Sequential when profiling (clean per-kernel events).
@@ -917,7 +935,9 @@ int enqueue_iteration(sflsqr_t* h) {
   if (fork_ls && P.method == SFLSQR_METHOD_SFLSQR && (rc = enqueue_ls(h, true))) return rc;
   // a5: w-side windowed orthogonalisation and normalisation
   if (!coop) {
-    if ((rc = enqueue_orth(h, 1, 0))) return rc;
+    rc = enqueue_orth(h, 1, 0);
+    h->axpy_wait_sk = false;
+    if (rc) return rc;
     Launch L(h, SFLSQR_KC_ORTH, 2 * m8);
     k_finish_w<<<vec_grid(h->m_loc), kVecThreads, 0, h->stream>>>(P);
   }
@@ -1570,6 +1590,7 @@ int sflsqr_create(sflsqr_t** out, const sflsqr_opts* o) {
     }
   }
   if (const char* ev = std::getenv("SFLSQR_SPMV_MODE")) h->spmv_mode = std::atoi(ev);
+  if (const char* ev = std::getenv("SFLSQR_SKETCH_SIDE")) h->sketch_side = std::atoi(ev) != 0;
   if (const char* ev = std::getenv("SFLSQR_SPMV_GRID_DELTA")) h->spmv_grid_delta = std::max(0, std::min(100, std::atoi(ev)));
   if (const char* ev = std::getenv("SFLSQR_PCSR_UNROLL")) h->pcsr_unroll = std::atoi(ev) == 2 ? 2 : 4;
   if (const char* ev = std::getenv("SFLSQR_LR_QR")) h->lr_qr_cgs = std::strcmp(ev, "cgs") == 0;
@@ -1593,7 +1614,8 @@ int sflsqr_create(sflsqr_t** out, const sflsqr_opts* o) {
   if (cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&h->ev_w, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&h->ev_w, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_sk, cudaEventDisableTiming) != cudaSuccess) {
     cudaGetLastError();
     h->side = nullptr;  // no overlap; the LS runs on the main stream
   }
@@ -2296,6 +2318,7 @@ void sflsqr_destroy(sflsqr_t* h) {
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
   if (h->ev_w) cudaEventDestroy(h->ev_w);
+  if (h->ev_sk) cudaEventDestroy(h->ev_sk);
   if (h->own_stream) cudaStreamDestroy(h->stream);
   delete h;
 }
