@@ -71,7 +71,7 @@ struct sflsqr {
   bool own_stream = false;
   cudaStream_t side = nullptr;  // second stream: the projected LS overlaps the T product (fork/join)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_w = nullptr, ev_sk = nullptr;
-  bool axpy_wait_sk = false;  // enqueue_orth(side 1): wait for ev_sk (sketch on the side stream) before writing w
+  int axpy_wait_sk = -1;  // enqueue_orth(this side): wait for ev_sk (sketch on the side stream) before the in-place update
   // sFLSQR's sketch of A z on the side stream beside the w-side dots (SFLSQR_SKETCH_SIDE=0: main
   // stream): config 1 +6 %, config 2 +1 %, config 3 +2 %, config 4 unchanged (same box)
   bool sketch_side = true;
@@ -647,14 +647,14 @@ int enqueue_orth(sflsqr_t* h, int side, int koff) {
       k_orth_dots<<<vec_grid(side == 0 ? h->n_loc : h->m_loc), kVecThreads, 0, h->stream>>>(P, side, koff);
     }
     if ((rc = coll_allreduce(h, P.scal + slot_f, kFuseAcc, false))) return rc;
-    if (side == 1 && h->axpy_wait_sk) CU(h, cudaStreamWaitEvent(h->stream, h->ev_sk, 0));
+    if (side == h->axpy_wait_sk) CU(h, cudaStreamWaitEvent(h->stream, h->ev_sk, 0));
     {
       Launch L(h, SFLSQR_KC_ORTH, v8 * (2 + J));
       k_orth_axpy<<<vec_grid(side == 0 ? h->n_loc : h->m_loc), kVecThreads, 0, h->stream>>>(P, side, koff);
     }
     return coll_allreduce(h, P.scal + slot_out, 1, false);
   }
-  if (side == 1 && h->axpy_wait_sk) CU(h, cudaStreamWaitEvent(h->stream, h->ev_sk, 0));
+  if (side == h->axpy_wait_sk) CU(h, cudaStreamWaitEvent(h->stream, h->ev_sk, 0));
   if (P.orth_alg == ORTH_CGS2) {
     const size_t sm_dots = sizeof(double) * (kCgsChunk + P.ldc), sm_upd = sizeof(double) * 2 * P.ldc;
     for (int stage = 0; stage < 2; ++stage) {
@@ -923,7 +923,7 @@ int enqueue_iteration(sflsqr_t* h) {
     CU(h, cudaStreamWaitEvent(h->side, h->ev_fork, 0));
     if ((rc = enqueue_sketch(h, P.st, P.w, h->side))) return rc;
     CU(h, cudaEventRecord(h->ev_sk, h->side));
-    h->axpy_wait_sk = true;
+    h->axpy_wait_sk = 1;
   } else if (!coop && P.method == SFLSQR_METHOD_SFLSQR && (rc = enqueue_sketch(h, P.st, P.w))) {
     return rc;
   }
@@ -936,7 +936,7 @@ int enqueue_iteration(sflsqr_t* h) {
   // a5: w-side windowed orthogonalisation and normalisation
   if (!coop) {
     rc = enqueue_orth(h, 1, 0);
-    h->axpy_wait_sk = false;
+    h->axpy_wait_sk = -1;
     if (rc) return rc;
     Launch L(h, SFLSQR_KC_ORTH, 2 * m8);
     k_finish_w<<<vec_grid(h->m_loc), kVecThreads, 0, h->stream>>>(P);
@@ -970,14 +970,28 @@ int enqueue_iteration(sflsqr_t* h) {
   }
   // a6: z = T w_{k+1}  (w_{k+1} = W[:, k])
   if ((rc = enqueue_transpose_product(h, false))) return rc;
-  // a4 (sFLSMR): S z -> S_TW[:, k+1]
-  if (P.method == SFLSQR_METHOD_SFLSMR && (rc = enqueue_sketch(h, P.st, P.z))) return rc;
   // FLSMR: z side of step k+1 now (column k+1 of T for T_{k+1} H_{k+1,k}, L361-367).
   // sFLSMR: the same, on the main stream while the LS (which needs only S z) runs on the side
   // stream -- the z-side dots/axpy of step k+1 depend on neither the LS nor the stop test.
   const bool fork_ls_mr = P.method == SFLSQR_METHOD_SFLSMR && !h->prof_on && h->side;
+  // a4 (sFLSMR): S z -> S_TW[:, k+1]; on one rank on the side stream (then the LS), beside the
+  // z-side dots of step k+1, whose in-place update waits for it
+  const bool sk_side_mr = fork_ls_mr && h->sketch_side && h->world == 1 && z_early(h);
+  if (sk_side_mr) {
+    CU(h, cudaEventRecord(h->ev_fork, h->stream));
+    CU(h, cudaStreamWaitEvent(h->side, h->ev_fork, 0));
+    if ((rc = enqueue_sketch(h, P.st, P.z, h->side))) return rc;
+    CU(h, cudaEventRecord(h->ev_sk, h->side));
+    h->axpy_wait_sk = 0;
+  } else if (P.method == SFLSQR_METHOD_SFLSMR && (rc = enqueue_sketch(h, P.st, P.z))) {
+    return rc;
+  }
   if (fork_ls_mr && (rc = enqueue_ls(h, true))) return rc;
-  if (z_early(h) && (rc = enqueue_orth(h, 0, 1))) return rc;
+  if (z_early(h)) {
+    rc = enqueue_orth(h, 0, 1);
+    h->axpy_wait_sk = -1;
+    if (rc) return rc;
+  }
   // a7: projected (sketched) LS (replicated on every rank: identical inputs)
   if (fork_ls || fork_ls_mr) {
     CU(h, cudaStreamWaitEvent(h->stream, h->ev_join, 0));
