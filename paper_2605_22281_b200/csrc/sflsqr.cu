@@ -1191,10 +1191,21 @@ int build_formats(sflsqr_t* h) {
       // short rows (< 64 nonzeros on average, e.g. the 5 x 5 stencil rows of config 8) lose more to
       // the second loop and the 64-register kernel than the pairs save (measured): plain CSR
       if (p.ok || nnz <= 0 || nnz < 64 * nrows) return SFLSQR_OK;
-      int r;
-      if ((r = build_pcsr(h, nrows, rp, col, val, p, false, 0.75))) return r;
-      if (p.ok) return SFLSQR_OK;
-      return build_pcsr(h, nrows, rp, col, val, p, true, 0.20);
+      // a copy costs up to 10 B per nonzero + 16 B per row: only when it leaves the solve's
+      // buffers room (>= 4 GB and >= 10 % of the device free afterwards); an allocation failure
+      // leaves the operator plain CSR rather than failing the upload
+      size_t fr = 0, tot = 0;
+      cudaMemGetInfo(&fr, &tot);
+      const double need = 10.0 * nnz + 32.0 * (nrows + 1);
+      if ((double)fr < need + std::max(4.0e9, 0.1 * (double)tot)) return SFLSQR_OK;
+      int r = build_pcsr(h, nrows, rp, col, val, p, false, 0.75);
+      if (!r && !p.ok) r = build_pcsr(h, nrows, rp, col, val, p, true, 0.20);
+      if (r == SFLSQR_E_OOM) {
+        free_pcsr(p);
+        cudaGetLastError();
+        return SFLSQR_OK;
+      }
+      return r;
     };
     if ((rc = pick(h->m_loc, h->a_rowptr, h->a_col, h->a_val, h->nnz_a, h->pa))) return rc;
     if ((rc = pick(h->t_rows, h->t_rowptr, h->t_col, h->t_val, h->nnz_t, h->pt))) return rc;
