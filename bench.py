@@ -339,15 +339,16 @@ def main():
         bpl = d["bytes"] / d["launches"]
         ach = bpl / (d["ms"] / d["launches"] / 1e3) / 1e9
         inf = s.get_info()
-        fnames = {0: "CSR", 1: "pair-CSR", 2: "aligned pair-CSR"}
+        fnames = {0: "CSR", 1: "pair-CSR", 2: "aligned pair-CSR", 3: "interpolation pair-CSR"}
         fmt = {"spmv_A": fnames[inf["a_fmt"]], "spmv_T": fnames[inf["t_fmt"]]}
-        tr = _traffic(prob.name, dom + {"CSR": "", "pair-CSR": "_pcsr", "aligned pair-CSR": "_apcsr"}[fmt.get(dom, "CSR")])
+        tr = _traffic(prob.name, dom + {"CSR": "", "pair-CSR": "_pcsr", "aligned pair-CSR": "_apcsr",
+                                        "interpolation pair-CSR": "_ipcsr"}[fmt.get(dom, "CSR")])
         kname = {"spmv_A": f"k_spmv_csr_pf, {fmt['spmv_A']} (A z)",
                  "spmv_T": f"k_spmv_csr_pf, {fmt['spmv_T']} (T w)"}.get(dom, dom)
         roof = {"bound": "hbm", "kernel": kname, "achieved": ach, "peak": peak,
                 "bytes_basis": "bytes of the format the product runs on: CSR 12 B/nnz (int32 col + fp64 value), "
-                               "pair-CSR 20 B per adjacent-column pair + 12 B per singleton, + row pointers and "
-                               "vectors (DESIGN.md §5)",
+                               "pair-CSR 20 B per adjacent-column pair (interpolation pairs 12 B) + 12 B per "
+                               "singleton, + row pointers and vectors (DESIGN.md §5)",
                 "unit": "GB/s", "frac": ach / peak, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": bpl, "traffic": tr}
     step_bytes = sum(d["bytes"] for d in prof.values())
@@ -384,8 +385,8 @@ def main():
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": prob.name, "method": spec.method, "m": prob.m, "n": prob.n,
                        "nnz_A": nnz_A, "nnz_T": nnz_T,
-                       "spmv_format": {"A": ["CSR", "pair-CSR", "aligned pair-CSR"][info_end["a_fmt"]],
-                                       "T": ["CSR", "pair-CSR", "aligned pair-CSR"][info_end["t_fmt"]],
+                       "spmv_format": {"A": ["CSR", "pair-CSR", "aligned pair-CSR", "interpolation pair-CSR"][info_end["a_fmt"]],
+                                       "T": ["CSR", "pair-CSR", "aligned pair-CSR", "interpolation pair-CSR"][info_end["t_fmt"]],
                                        "pairs_A": info_end["a_pairs"], "pairs_T": info_end["t_pairs"]},
                        "ell": spec.window, "d": spec.d, "s": spec.s_nz, "tau": spec.precond, "maxit": maxit,
                        "iterations_timed": f"{W + 1}..{W + K}", "history": "true residual (W path) on",

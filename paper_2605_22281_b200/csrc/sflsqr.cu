@@ -46,6 +46,7 @@ enum TKind { T_FULL = 0, T_ROWSHARD = 1, T_COLSHARD = 2 };
 struct PCSR {  // pair-CSR copy of an operator (k_pcsr_rows): pairs + singleton CSR
   bool ok = false;
   bool aligned = false;  // pairs only at even columns (gathered as one 16-byte load)
+  double* f = nullptr;   // interpolation pairs: second values only (first = 1 - f bitwise), pval freed
   int64_t npairs = 0, nsingles = 0;
   int64_t* prp = nullptr;
   int* pcol = nullptr;
@@ -95,6 +96,7 @@ struct sflsqr {
   C16 ca, ct;           // CSR-16 index copies of A and T (SpMV mode 15, on request)
   PCSR pa, pt;          // pair-CSR copies of A and T (SpMV mode 16)
   int pcsr_unroll = 4;  // pairs in flight per lane in the mode-16 kernel (4 or 2; SFLSQR_PCSR_UNROLL)
+  bool pcsr_interp = true;  // interpolation pairs when every pair qualifies (SFLSQR_PCSR_INTERP=0: off)
   // sketch
   bool sk_set = false;
   int sk_kind = 0;  // 0 sparse-sign (R5/R6), 1 dense Gaussian (R21)
@@ -299,6 +301,7 @@ void free_solve(sflsqr_t* h) {
 }
 
 void free_pcsr(PCSR& p) {
+  cudaFree(p.f);
   cudaFree(p.prp);
   cudaFree(p.pcol);
   cudaFree(p.pval);
@@ -459,9 +462,14 @@ void enqueue_apply(sflsqr_t* h, int which, const DevState* st, const double* x, 
     PP.rowptr = pc.prp;
     PP.col = pc.pcol;
     PP.val = pc.pval;
+    PP.f = pc.f;
+    if (pc.f) L.bytes_override(12.0 * pc.npairs + 12.0 * pc.nsingles + 16.0 * (nrows + 1) + 8.0 * xlen + 8.0 * nrows);
     // aligned pairs gather one 16-byte value pair: needs x (any k-relative column) 16-byte aligned
     const bool x16 = ((uintptr_t)x % 16 == 0) && (x_ld % 2 == 0);
-    if (pc.aligned && x16)
+    if (pc.f)
+      k_spmv_csr_pf<16, 4, 16, false, 6><<<grid_for(32, 2), 512, 0, h->stream>>>(
+          st, nrows, pc.srp, pc.scol, pc.sval, x, x_ld, x_koff, y, SpmvEpi(), PP);
+    else if (pc.aligned && x16)
       k_spmv_csr_pf<16, 4, 16, false, 5><<<grid_for(32, 2), 512, 0, h->stream>>>(
           st, nrows, pc.srp, pc.scol, pc.sval, x, x_ld, x_koff, y, SpmvEpi(), PP);
     else if (h->pcsr_unroll == 4)
@@ -697,12 +705,17 @@ bool launch_pairs_epi(sflsqr_t* h, int which, const double* x, int64_t x_ld, dou
   const int64_t nrows = which == 0 ? h->m_loc : h->t_rows;
   const int64_t xlen = which == 0 ? (h->world > 1 ? h->world * h->n_max : h->n)
                                   : (h->tkind == T_ROWSHARD ? h->world * h->m_max : h->m_loc);
-  Launch L(h, cls, 20.0 * pc.npairs + 12.0 * pc.nsingles + 16.0 * (nrows + 1) + 8.0 * xlen + 8.0 * nrows + extra);
+  Launch L(h, cls, (pc.f ? 12.0 : 20.0) * pc.npairs + 12.0 * pc.nsingles + 16.0 * (nrows + 1) + 8.0 * xlen + 8.0 * nrows +
+                       extra);
   PairPart PP;
   PP.rowptr = pc.prp;
   PP.col = pc.pcol;
   PP.val = pc.pval;
-  if (pc.aligned && (uintptr_t)x % 16 == 0 && x_ld % 2 == 0)
+  PP.f = pc.f;
+  if (pc.f)
+    k_spmv_csr_pf<16, 4, 16, true, 6><<<grid, 512, 0, h->stream>>>(h->P.st, nrows, pc.srp, pc.scol, pc.sval, x, x_ld,
+                                                                    0, y, E, PP);
+  else if (pc.aligned && (uintptr_t)x % 16 == 0 && x_ld % 2 == 0)
     k_spmv_csr_pf<16, 4, 16, true, 5><<<grid, 512, 0, h->stream>>>(h->P.st, nrows, pc.srp, pc.scol, pc.sval, x, x_ld,
                                                                     0, y, E, PP);
   else
@@ -1167,6 +1180,30 @@ int build_pcsr(sflsqr_t* h, int64_t nrows, const int64_t* rp, const int32_t* col
   return SFLSQR_OK;
 }
 
+// Interpolation pairs (PAIRS == 6): when every pair of a pair-CSR copy has first value
+// 1 - second value bitwise (linear-interpolation weights), keep only the second values:
+// 12 instead of 20 bytes per pair, the same operator bit for bit.
+int try_interp(sflsqr_t* h, PCSR& p) {
+  if (!p.ok || p.aligned || p.f || p.npairs < 1) return SFLSQR_OK;
+  int* flag = nullptr;
+  int rc;
+  if ((rc = dalloc(h, (void**)&flag, sizeof(int), nullptr))) return rc;
+  CU(h, cudaMemsetAsync(flag, 0, sizeof(int), h->stream));
+  const int g = (int)std::min<int64_t>((p.npairs + 255) / 256, 148 * 16);
+  k_pcsr_interp<<<g, 256, 0, h->stream>>>(p.npairs, p.pval, nullptr, flag);
+  int bad = 0;
+  CU(h, cudaMemcpyAsync(&bad, flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CU(h, cudaStreamSynchronize(h->stream));
+  cudaFree(flag);
+  if (bad) return SFLSQR_OK;
+  if ((rc = dalloc(h, (void**)&p.f, sizeof(double) * p.npairs, nullptr))) return rc;
+  k_pcsr_interp<<<g, 256, 0, h->stream>>>(p.npairs, p.pval, p.f, nullptr);
+  CU(h, cudaStreamSynchronize(h->stream));
+  cudaFree(p.pval);
+  p.pval = nullptr;
+  return check_launch(h);
+}
+
 // Auxiliary SpMV formats the selected mode needs (built after every operator upload).
 int build_formats(sflsqr_t* h) {
   if (h->blur) return SFLSQR_OK;
@@ -1199,6 +1236,7 @@ int build_formats(sflsqr_t* h) {
       const double need = 10.0 * nnz + 32.0 * (nrows + 1);
       if ((double)fr < need + std::max(4.0e9, 0.1 * (double)tot)) return SFLSQR_OK;
       int r = build_pcsr(h, nrows, rp, col, val, p, false, 0.75);
+      if (!r && p.ok && h->pcsr_interp) r = try_interp(h, p);
       if (!r && !p.ok) r = build_pcsr(h, nrows, rp, col, val, p, true, 0.20);
       if (r == SFLSQR_E_OOM) {
         free_pcsr(p);
@@ -1616,6 +1654,7 @@ int sflsqr_create(sflsqr_t** out, const sflsqr_opts* o) {
   }
   if (const char* ev = std::getenv("SFLSQR_SPMV_MODE")) h->spmv_mode = std::atoi(ev);
   if (const char* ev = std::getenv("SFLSQR_SKETCH_SIDE")) h->sketch_side = std::atoi(ev) != 0;
+  if (const char* ev = std::getenv("SFLSQR_PCSR_INTERP")) h->pcsr_interp = std::atoi(ev) != 0;
   if (const char* ev = std::getenv("SFLSQR_SPMV_GRID_DELTA")) h->spmv_grid_delta = std::max(0, std::min(100, std::atoi(ev)));
   if (const char* ev = std::getenv("SFLSQR_PCSR_UNROLL")) h->pcsr_unroll = std::atoi(ev) == 2 ? 2 : 4;
   if (const char* ev = std::getenv("SFLSQR_LR_QR")) h->lr_qr_cgs = std::strcmp(ev, "cgs") == 0;
@@ -2156,8 +2195,8 @@ int sflsqr_get_info(sflsqr_t* h, sflsqr_info* info) {
   const int mode_t = h->spmv_mode >= 0 ? h->spmv_mode : (h->pt.ok ? 16 : 14);
   info->a_pairs = ((mode_a == 16 || mode_a == 17) && h->pa.ok) ? h->pa.npairs : 0;
   info->t_pairs = ((mode_t == 16 || mode_t == 17) && h->pt.ok) ? h->pt.npairs : 0;
-  info->a_fmt = info->a_pairs ? (h->pa.aligned ? 2 : 1) : 0;
-  info->t_fmt = info->t_pairs ? (h->pt.aligned ? 2 : 1) : 0;
+  info->a_fmt = info->a_pairs ? (h->pa.aligned ? 2 : (h->pa.f ? 3 : 1)) : 0;
+  info->t_fmt = info->t_pairs ? (h->pt.aligned ? 2 : (h->pt.f ? 3 : 1)) : 0;
   return SFLSQR_OK;
 }
 

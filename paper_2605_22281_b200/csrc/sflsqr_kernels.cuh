@@ -471,11 +471,13 @@ struct PairPart {
   const int64_t* rowptr = nullptr;
   const int* col = nullptr;
   const double2* val = nullptr;
+  const double* f = nullptr;  // PAIRS == 6: interpolation pairs, values (1 - f[q], f[q]) exactly
 };
 
 // PAIRS = 0: plain CSR; 2 or 4: pair-CSR with that many pairs in flight per lane (64
 // registers: 2 CTAs of 512 threads per SM); 5: 4 in flight, aligned pairs (c even) gathered as
-// one 16-byte load (x must be 16-byte aligned).
+// one 16-byte load (x must be 16-byte aligned); 6: 4 in flight, interpolation pairs (only f
+// stored, the pair's values are 1 - f and f, bitwise those of the stored operator).
 template <int WPB, int UNR, int LANES, bool EPI = false, int PAIRS = 0>
 __global__ void __launch_bounds__(WPB * 32, (EPI || PAIRS) ? 2 : 2048 / (WPB * 32))
     k_spmv_csr_pf(const DevState* st, int64_t nrows,
@@ -508,14 +510,21 @@ __global__ void __launch_bounds__(WPB * 32, (EPI || PAIRS) ? 2 : 2048 / (WPB * 3
         pe = PP.rowptr[row + 1];
       }
       int64_t q = ps + sl;
-      constexpr int PU = PAIRS == 5 ? 4 : (PAIRS > 0 ? PAIRS : 1);
+      constexpr int PU = PAIRS >= 5 ? 4 : (PAIRS > 0 ? PAIRS : 1);
       int cn[PU];
       double2 vn[PU];
+      auto ldv = [&](int64_t t) -> double2 {
+        if (PAIRS == 6) {
+          const double fq = ld_stream_d(PP.f + t);
+          return make_double2(1.0 - fq, fq);
+        }
+        return ld_stream_d2(PP.val + t);
+      };
 #pragma unroll
       for (int u = 0; u < PU; ++u) {
         const int64_t t = q + (int64_t)LANES * u;
         cn[u] = t < pe ? ld_stream_i(PP.col + t) : 0;
-        vn[u] = t < pe ? ld_stream_d2(PP.val + t) : make_double2(0.0, 0.0);
+        vn[u] = t < pe ? ldv(t) : make_double2(0.0, 0.0);
       }
       while (__any_sync(0xffffffffu, q < pe)) {
         int c[PU];
@@ -530,7 +539,7 @@ __global__ void __launch_bounds__(WPB * 32, (EPI || PAIRS) ? 2 : 2048 / (WPB * 3
         for (int u = 0; u < PU; ++u) {
           const int64_t t = qn + (int64_t)LANES * u;
           cn[u] = t < pe ? ld_stream_i(PP.col + t) : 0;
-          vn[u] = t < pe ? ld_stream_d2(PP.val + t) : make_double2(0.0, 0.0);
+          vn[u] = t < pe ? ldv(t) : make_double2(0.0, 0.0);
         }
         double x0[PU], x1[PU];
 #pragma unroll
@@ -684,6 +693,17 @@ __global__ void __launch_bounds__(256) k_pcsr_rows(int64_t nrows, const int64_t*
       np_cnt[row] = np;
       ns_cnt[row] = ns;
     }
+  }
+}
+
+// Interpolation pairs: every pair's first value is 1 - (its second value), bitwise (a linear-
+// interpolation backprojector's weights: L1646).  flag <- 1 if some pair is not; f <- second values.
+__global__ void __launch_bounds__(256) k_pcsr_interp(int64_t npairs, const double2* __restrict__ pval, double* f,
+                                                     int* flag) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < npairs; q += (int64_t)gridDim.x * blockDim.x) {
+    const double2 v = pval[q];
+    if (f) f[q] = v.y;
+    else if (!(v.x == 1.0 - v.y) || __double_as_longlong(v.x) != __double_as_longlong(1.0 - v.y)) *flag = 1;
   }
 }
 

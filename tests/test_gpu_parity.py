@@ -494,17 +494,46 @@ def test_default_spmv_format_rule():
     s = solver_for_problem(p, spec, maxit=3, eta=0.0)
     inf = s.get_info()
     s.close()
-    assert inf["t_fmt"] == 1 and inf["t_pairs"] == p.T.nnz // 2 or inf["t_pairs"] >= 0.375 * p.T.nnz
+    assert inf["t_fmt"] == 3 and inf["t_pairs"] >= 0.375 * p.T.nnz    # B: interpolation pairs (1 - f, f)
     assert inf["a_fmt"] == 2 and inf["a_pairs"] >= 0.2 * p.A.nnz
     s = solver_for_problem(p, spec, maxit=3, eta=0.0, method="lsqr")
     inf = s.get_info()
     s.close()
-    assert inf["a_fmt"] == 2 and inf["t_fmt"] == 1
+    assert inf["a_fmt"] == 2 and inf["t_fmt"] == 3
     s = solver_for_problem(p, spec, maxit=3, eta=0.0)
     s.debug_set_tuning(14)                                 # forced plain CSR
     inf = s.get_info()
     s.close()
     assert inf["a_fmt"] == 0 and inf["t_fmt"] == 0 and inf["a_pairs"] == 0 and inf["t_pairs"] == 0
+
+
+def test_interpolation_pairs_bitwise_equal_to_pair_csr(monkeypatch):
+    # config 4's pixel-driven B: every pair is (1 - f, f) bitwise, so only f is stored (12 instead
+    # of 20 bytes per pair); the reconstructed values and the summation order are those of the
+    # pair-CSR kernel, so the products agree bit for bit
+    from paper_2605_22281_b200 import SFLSQR
+    p = make_problem(4, N=96, n_angles=61, nb=137)
+    rng = np.random.default_rng(5)
+    w, x = rng.standard_normal(p.m), rng.standard_normal(p.n)
+    out = {}
+    for interp in ("0", "1"):
+        monkeypatch.setenv("SFLSQR_PCSR_INTERP", interp)
+        s = SFLSQR(maxit=4)
+        s.set_operator(p.A.nrows, p.A.ncols, p.A.rowptr, p.A.col, p.A.val, t=(p.T.rowptr, p.T.col, p.T.val))
+        out[interp] = (s.get_info()["t_fmt"], s.debug_apply(1, w), s.debug_apply(0, x))
+        s.close()
+    assert out["0"][0] == 1 and out["1"][0] == 3
+    assert np.array_equal(out["0"][1], out["1"][1]) and np.array_equal(out["0"][2], out["1"][2])
+    B = OracleCSR(p.T.nrows, p.T.ncols, p.T.rowptr, p.T.col, p.T.val)
+    ref = B.matvec(w)
+    assert np.max(np.abs(out["1"][1] - ref)) <= 1e-13 * np.max(np.abs(ref))
+    # an operator whose pairs are not interpolation weights keeps the full pair values
+    m, n = 700, 2000
+    rp, col, val = _runs_csr(3, m, n)
+    s = SFLSQR(maxit=4)
+    s.set_operator(m, n, rp, col, val, t=(rp, col, val) if m == n else None)
+    assert s.get_info()["a_fmt"] in (0, 1, 2)
+    s.close()
 
 
 def test_csr16_overflow_falls_back_to_int32():
