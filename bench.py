@@ -341,8 +341,10 @@ def main():
         inf = s.get_info()
         fnames = {0: "CSR", 1: "pair-CSR", 2: "aligned pair-CSR", 3: "interpolation pair-CSR"}
         fmt = {"spmv_A": fnames[inf["a_fmt"]], "spmv_T": fnames[inf["t_fmt"]]}
-        tr = _traffic(prob.name, dom + {"CSR": "", "pair-CSR": "_pcsr", "aligned pair-CSR": "_apcsr",
-                                        "interpolation pair-CSR": "_ipcsr"}[fmt.get(dom, "CSR")])
+        tkey = dom + {"CSR": "", "pair-CSR": "_pcsr", "aligned pair-CSR": "_apcsr",
+                      "interpolation pair-CSR": "_ipcsr"}[fmt.get(dom, "CSR")]
+        tr = _traffic(prob.name, tkey)
+        l1 = _traffic(prob.name, tkey + "_l1_wavefronts_pct")
         kname = {"spmv_A": f"k_spmv_csr_pf, {fmt['spmv_A']} (A z)",
                  "spmv_T": f"k_spmv_csr_pf, {fmt['spmv_T']} (T w)"}.get(dom, dom)
         roof = {"bound": "hbm", "kernel": kname, "achieved": ach, "peak": peak,
@@ -350,7 +352,10 @@ def main():
                                "pair-CSR 20 B per adjacent-column pair (interpolation pairs 12 B) + 12 B per "
                                "singleton, + row pointers and vectors (DESIGN.md §5)",
                 "unit": "GB/s", "frac": ach / peak, "peak_source": peak_src,
-                "algorithmic_bytes_per_launch": bpl, "traffic": tr}
+                "algorithmic_bytes_per_launch": bpl, "traffic": tr,
+                "l1_wavefronts_pct_of_peak": l1,
+                "note": "the pair formats move fewer HBM bytes than CSR; the interpolation pair-CSR product is bound "
+                        "by its L1 gather wavefronts (ncu l1_wavefronts_pct_of_peak), not HBM (DESIGN.md §5)"}
     step_bytes = sum(d["bytes"] for d in prof.values())
     step_gbs = step_bytes / (ms / 1e3) / 1e9 if step_bytes else None   # algorithmic bytes of the step / production time
 
