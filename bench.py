@@ -116,6 +116,9 @@ def _barrier(world):
         dist.barrier()
 
 
+FMT_NAMES = ["CSR", "pair-CSR", "aligned pair-CSR", "interpolation pair-CSR", "sliced-ELL interpolation pairs"]
+
+
 def _traffic(workload, kernel):
     p = os.path.join(ROOT, "profiles", f"traffic_{workload}.json")
     try:
@@ -339,10 +342,11 @@ def main():
         bpl = d["bytes"] / d["launches"]
         ach = bpl / (d["ms"] / d["launches"] / 1e3) / 1e9
         inf = s.get_info()
-        fnames = {0: "CSR", 1: "pair-CSR", 2: "aligned pair-CSR", 3: "interpolation pair-CSR"}
+        fnames = {0: "CSR", 1: "pair-CSR", 2: "aligned pair-CSR", 3: "interpolation pair-CSR",
+                  4: "sliced-ELL interpolation pairs"}
         fmt = {"spmv_A": fnames[inf["a_fmt"]], "spmv_T": fnames[inf["t_fmt"]]}
         tkey = dom + {"CSR": "", "pair-CSR": "_pcsr", "aligned pair-CSR": "_apcsr",
-                      "interpolation pair-CSR": "_ipcsr"}[fmt.get(dom, "CSR")]
+                      "interpolation pair-CSR": "_ipcsr", "sliced-ELL interpolation pairs": "_sell"}[fmt.get(dom, "CSR")]
         tr = _traffic(prob.name, tkey)
         l1 = _traffic(prob.name, tkey + "_l1_wavefronts_pct")
         kname = {"spmv_A": f"k_spmv_csr_pf, {fmt['spmv_A']} (A z)",
@@ -390,8 +394,7 @@ def main():
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": prob.name, "method": spec.method, "m": prob.m, "n": prob.n,
                        "nnz_A": nnz_A, "nnz_T": nnz_T,
-                       "spmv_format": {"A": ["CSR", "pair-CSR", "aligned pair-CSR", "interpolation pair-CSR"][info_end["a_fmt"]],
-                                       "T": ["CSR", "pair-CSR", "aligned pair-CSR", "interpolation pair-CSR"][info_end["t_fmt"]],
+                       "spmv_format": {"A": FMT_NAMES[info_end["a_fmt"]], "T": FMT_NAMES[info_end["t_fmt"]],
                                        "pairs_A": info_end["a_pairs"], "pairs_T": info_end["t_pairs"]},
                        "ell": spec.window, "d": spec.d, "s": spec.s_nz, "tau": spec.precond, "maxit": maxit,
                        "iterations_timed": f"{W + 1}..{W + K}", "history": "true residual (W path) on",

@@ -171,7 +171,8 @@ typedef struct sflsqr_info {
                           run on (10 instead of 12 bytes per paired nonzero); 0 = plain CSR */
   int32_t a_fmt, t_fmt; /* SpMV format of the A / T products: 0 CSR, 1 pair-CSR (any adjacent
                           pair), 2 aligned pair-CSR (pairs at even columns, 16-byte gathers),
-                          3 interpolation pair-CSR (every pair (1 - f, f) bitwise: only f stored) */
+                          3 interpolation pair-CSR (every pair (1 - f, f) bitwise: only f stored),
+                          4 the same pairs as sliced ELL, 32 rows per slice, one row per lane    */
 } sflsqr_info;
 
 /* Per-kernel-class device time, recorded with CUDA events on the library stream

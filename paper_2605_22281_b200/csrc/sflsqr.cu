@@ -47,6 +47,12 @@ struct PCSR {  // pair-CSR copy of an operator (k_pcsr_rows): pairs + singleton 
   bool ok = false;
   bool aligned = false;  // pairs only at even columns (gathered as one 16-byte load)
   double* f = nullptr;   // interpolation pairs: second values only (first = 1 - f bitwise), pval freed
+  // sliced-ELL copy of the interpolation pairs (k_spmv_sell_ip): slice offsets, per-row counts
+  int64_t* soff = nullptr;
+  int* rcnt = nullptr;
+  int* ecol = nullptr;
+  double* ef = nullptr;
+  int64_t sell_entries = 0;
   int64_t npairs = 0, nsingles = 0;
   int64_t* prp = nullptr;
   int* pcol = nullptr;
@@ -97,6 +103,7 @@ struct sflsqr {
   PCSR pa, pt;          // pair-CSR copies of A and T (SpMV mode 16)
   int pcsr_unroll = 4;  // pairs in flight per lane in the mode-16 kernel (4 or 2; SFLSQR_PCSR_UNROLL)
   bool pcsr_interp = true;  // interpolation pairs when every pair qualifies (SFLSQR_PCSR_INTERP=0: off)
+  bool sell = true;         // sliced-ELL (row per lane) copy of interpolation pairs (SFLSQR_SELL=0: off)
   // sketch
   bool sk_set = false;
   int sk_kind = 0;  // 0 sparse-sign (R5/R6), 1 dense Gaussian (R21)
@@ -301,6 +308,10 @@ void free_solve(sflsqr_t* h) {
 }
 
 void free_pcsr(PCSR& p) {
+  cudaFree(p.soff);
+  cudaFree(p.rcnt);
+  cudaFree(p.ecol);
+  cudaFree(p.ef);
   cudaFree(p.f);
   cudaFree(p.prp);
   cudaFree(p.pcol);
@@ -466,7 +477,14 @@ void enqueue_apply(sflsqr_t* h, int which, const DevState* st, const double* x, 
     if (pc.f) L.bytes_override(12.0 * pc.npairs + 12.0 * pc.nsingles + 16.0 * (nrows + 1) + 8.0 * xlen + 8.0 * nrows);
     // aligned pairs gather one 16-byte value pair: needs x (any k-relative column) 16-byte aligned
     const bool x16 = ((uintptr_t)x % 16 == 0) && (x_ld % 2 == 0);
-    if (pc.f)
+    if (pc.f && pc.ecol) {
+      L.bytes_override(12.0 * pc.sell_entries + 12.0 * pc.nsingles + 4.0 * nrows + 16.0 * (nrows + 1) + 8.0 * xlen +
+                       8.0 * nrows);
+      const int64_t nsl = (nrows + kSellC - 1) / kSellC;
+      const int g = (int)std::max<int64_t>(1, std::min<int64_t>((nsl + 15) / 16, 148 * 2 - h->spmv_grid_delta));
+      k_spmv_sell_ip<4><<<g, 512, 0, h->stream>>>(st, nrows, pc.soff, pc.rcnt, pc.ecol, pc.ef, pc.srp, pc.scol, pc.sval,
+                                                   x, x_ld, x_koff, y);
+    } else if (pc.f)
       k_spmv_csr_pf<16, 4, 16, false, 6><<<grid_for(32, 2), 512, 0, h->stream>>>(
           st, nrows, pc.srp, pc.scol, pc.sval, x, x_ld, x_koff, y, SpmvEpi(), PP);
     else if (pc.aligned && x16)
@@ -1204,6 +1222,54 @@ int try_interp(sflsqr_t* h, PCSR& p) {
   return check_launch(h);
 }
 
+// Sliced-ELL copy of an interpolation pair-CSR operator (row per lane, k_spmv_sell_ip), kept only
+// when the slices' padding costs at most 10 % more entries.
+int build_sell(sflsqr_t* h, int64_t nrows, PCSR& p) {
+  if (!p.ok || !p.f || nrows < 1) return SFLSQR_OK;
+  const int64_t nsl = (nrows + kSellC - 1) / kSellC;
+  int64_t* len = nullptr;
+  void* tmp = nullptr;
+  size_t tb = 0;
+  int rc;
+  if ((rc = dalloc(h, (void**)&len, sizeof(int64_t) * (nsl + 1), nullptr)) ||
+      (rc = dalloc(h, (void**)&p.soff, sizeof(int64_t) * (nsl + 1), nullptr))) {
+    cudaFree(len);
+    return rc;
+  }
+  CU(h, cudaMemsetAsync(len + nsl, 0, sizeof(int64_t), h->stream));
+  k_sell_len<<<(int)std::min<int64_t>((nsl + 255) / 256, 148 * 16), 256, 0, h->stream>>>(nrows, p.prp, len);
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, len, p.soff, nsl + 1, h->stream);
+  if ((rc = dalloc(h, &tmp, tb, nullptr))) {
+    cudaFree(len);
+    return rc;
+  }
+  cub::DeviceScan::ExclusiveSum(tmp, tb, len, p.soff, nsl + 1, h->stream);
+  CU(h, cudaMemcpyAsync(&p.sell_entries, p.soff + nsl, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+  CU(h, cudaStreamSynchronize(h->stream));
+  cudaFree(len);
+  cudaFree(tmp);
+  if ((double)p.sell_entries > 1.1 * (double)p.npairs ||
+      (rc = dalloc(h, (void**)&p.rcnt, sizeof(int) * nrows, nullptr)) ||
+      (rc = dalloc(h, (void**)&p.ecol, sizeof(int) * std::max<int64_t>(p.sell_entries, 1), nullptr)) ||
+      (rc = dalloc(h, (void**)&p.ef, sizeof(double) * std::max<int64_t>(p.sell_entries, 1), nullptr))) {
+    cudaFree(p.soff);
+    cudaFree(p.rcnt);
+    cudaFree(p.ecol);
+    p.soff = nullptr;
+    p.rcnt = p.ecol = nullptr;
+    p.ef = nullptr;
+    cudaGetLastError();
+    return SFLSQR_OK;
+  }
+  // padding entries are never loaded (masked by the row counts); zero them anyway
+  CU(h, cudaMemsetAsync(p.ecol, 0, sizeof(int) * p.sell_entries, h->stream));
+  CU(h, cudaMemsetAsync(p.ef, 0, sizeof(double) * p.sell_entries, h->stream));
+  k_sell_fill<<<(int)std::min<int64_t>((nrows + 255) / 256, 148 * 16), 256, 0, h->stream>>>(nrows, p.prp, p.pcol, p.f,
+                                                                                          p.soff, p.rcnt, p.ecol, p.ef);
+  CU(h, cudaStreamSynchronize(h->stream));
+  return check_launch(h);
+}
+
 // Auxiliary SpMV formats the selected mode needs (built after every operator upload).
 int build_formats(sflsqr_t* h) {
   if (h->blur) return SFLSQR_OK;
@@ -1237,6 +1303,7 @@ int build_formats(sflsqr_t* h) {
       if ((double)fr < need + std::max(4.0e9, 0.1 * (double)tot)) return SFLSQR_OK;
       int r = build_pcsr(h, nrows, rp, col, val, p, false, 0.75);
       if (!r && p.ok && h->pcsr_interp) r = try_interp(h, p);
+      if (!r && p.ok && p.f && h->sell) r = build_sell(h, nrows, p);
       if (!r && !p.ok) r = build_pcsr(h, nrows, rp, col, val, p, true, 0.20);
       if (r == SFLSQR_E_OOM) {
         free_pcsr(p);
@@ -1655,6 +1722,7 @@ int sflsqr_create(sflsqr_t** out, const sflsqr_opts* o) {
   if (const char* ev = std::getenv("SFLSQR_SPMV_MODE")) h->spmv_mode = std::atoi(ev);
   if (const char* ev = std::getenv("SFLSQR_SKETCH_SIDE")) h->sketch_side = std::atoi(ev) != 0;
   if (const char* ev = std::getenv("SFLSQR_PCSR_INTERP")) h->pcsr_interp = std::atoi(ev) != 0;
+  if (const char* ev = std::getenv("SFLSQR_SELL")) h->sell = std::atoi(ev) != 0;
   if (const char* ev = std::getenv("SFLSQR_SPMV_GRID_DELTA")) h->spmv_grid_delta = std::max(0, std::min(100, std::atoi(ev)));
   if (const char* ev = std::getenv("SFLSQR_PCSR_UNROLL")) h->pcsr_unroll = std::atoi(ev) == 2 ? 2 : 4;
   if (const char* ev = std::getenv("SFLSQR_LR_QR")) h->lr_qr_cgs = std::strcmp(ev, "cgs") == 0;
@@ -2195,8 +2263,8 @@ int sflsqr_get_info(sflsqr_t* h, sflsqr_info* info) {
   const int mode_t = h->spmv_mode >= 0 ? h->spmv_mode : (h->pt.ok ? 16 : 14);
   info->a_pairs = ((mode_a == 16 || mode_a == 17) && h->pa.ok) ? h->pa.npairs : 0;
   info->t_pairs = ((mode_t == 16 || mode_t == 17) && h->pt.ok) ? h->pt.npairs : 0;
-  info->a_fmt = info->a_pairs ? (h->pa.aligned ? 2 : (h->pa.f ? 3 : 1)) : 0;
-  info->t_fmt = info->t_pairs ? (h->pt.aligned ? 2 : (h->pt.f ? 3 : 1)) : 0;
+  info->a_fmt = info->a_pairs ? (h->pa.aligned ? 2 : (h->pa.f ? (h->pa.ecol ? 4 : 3) : 1)) : 0;
+  info->t_fmt = info->t_pairs ? (h->pt.aligned ? 2 : (h->pt.f ? (h->pt.ecol ? 4 : 3) : 1)) : 0;
   return SFLSQR_OK;
 }
 

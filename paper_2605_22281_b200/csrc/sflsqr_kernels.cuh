@@ -707,6 +707,98 @@ __global__ void __launch_bounds__(256) k_pcsr_interp(int64_t npairs, const doubl
   }
 }
 
+// ------------------------------------------------------------------ sliced-ELL pairs (row per lane)
+// Slices of 32 consecutive rows; entry k of the slice's rows is stored at soff[s] + 32 k + lane
+// (k < the row's pair count; the slice is as long as its longest row).  A warp takes a slice,
+// lane = row: the 32 lanes load 32 consecutive columns / values (coalesced) and gather for 32
+// NEIGHBOURING rows at the same k -- for the pixel-driven B (rows = pixels in 4x4 tiles, pair k =
+// angle k) neighbouring pixels project onto neighbouring detector bins, so one gather instruction
+// touches one or two lines instead of 32.  Each lane sums its own row in k order (deterministic).
+// Interpolation pairs only (values 1 - f, f); singletons of the row (if any) from the singleton CSR.
+constexpr int kSellC = 32;
+template <int UNR>
+__global__ void __launch_bounds__(512, 2) k_spmv_sell_ip(const DevState* st, int64_t nrows, const int64_t* __restrict__ soff,
+                                                       const int* __restrict__ rcnt, const int* __restrict__ scol,
+                                                       const double* __restrict__ sf, const int64_t* __restrict__ srp,
+                                                       const int* __restrict__ s1col, const double* __restrict__ s1val,
+                                                       const double* __restrict__ x_base, int64_t x_ld, int x_koff,
+                                                       double* y) {
+  if (st && st->done) return;
+  const double* __restrict__ x = kvec(st, x_base, x_ld, x_koff);
+  const int lane = threadIdx.x & 31;
+  const int64_t nslices = (nrows + kSellC - 1) / kSellC;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t sl = gw; sl < nslices; sl += nw) {
+    const int64_t row = sl * kSellC + lane;
+    const int cnt = row < nrows ? rcnt[row] : 0;
+    const int L = __reduce_max_sync(0xffffffffu, cnt);
+    const int64_t base = soff[sl] + lane;
+    double sum = 0.0;
+    int cn[UNR];
+    double fn[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      cn[u] = u < cnt ? ld_stream_i(scol + base + (int64_t)kSellC * u) : 0;
+      fn[u] = u < cnt ? ld_stream_d(sf + base + (int64_t)kSellC * u) : 0.0;
+    }
+    for (int k = 0; k < L; k += UNR) {
+      int c[UNR];
+      double fv[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        c[u] = cn[u];
+        fv[u] = fn[u];
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int kk = k + UNR + u;
+        cn[u] = kk < cnt ? ld_stream_i(scol + base + (int64_t)kSellC * kk) : 0;
+        fn[u] = kk < cnt ? ld_stream_d(sf + base + (int64_t)kSellC * kk) : 0.0;
+      }
+      double x0[UNR], x1[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const bool ok = k + u < cnt;
+        x0[u] = ok ? __ldg(x + c[u]) : 0.0;
+        x1[u] = ok ? __ldg(x + c[u] + 1) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u)
+        if (k + u < cnt) sum = fma(fv[u], x1[u], fma(1.0 - fv[u], x0[u], sum));
+    }
+    if (row < nrows) {
+      for (int64_t p = srp[row]; p < srp[row + 1]; ++p) sum = fma(s1val[p], __ldg(x + s1col[p]), sum);
+      y[row] = sum;
+    }
+  }
+}
+
+// Sliced-ELL build from an interpolation pair-CSR copy: thread per row scatters its pairs.
+__global__ void __launch_bounds__(256) k_sell_fill(int64_t nrows, const int64_t* __restrict__ prp,
+                                                   const int* __restrict__ pcol, const double* __restrict__ pf,
+                                                   const int64_t* __restrict__ soff, int* rcnt, int* scol, double* sf) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s0 = prp[r], n = prp[r + 1] - s0;
+    rcnt[r] = (int)n;
+    const int64_t base = soff[r / kSellC] + (r % kSellC);
+    for (int64_t k = 0; k < n; ++k) {
+      scol[base + kSellC * k] = pcol[s0 + k];
+      sf[base + kSellC * k] = pf[s0 + k];
+    }
+  }
+}
+
+// Slice lengths (max pair count of the slice's rows) x kSellC -> sl_len.
+__global__ void __launch_bounds__(256) k_sell_len(int64_t nrows, const int64_t* __restrict__ prp, int64_t* sl_len) {
+  const int64_t nslices = (nrows + kSellC - 1) / kSellC;
+  for (int64_t sl = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; sl < nslices; sl += (int64_t)gridDim.x * blockDim.x) {
+    int64_t mx = 0;
+    for (int64_t r = sl * kSellC; r < min(nrows, (sl + 1) * kSellC); ++r) mx = max(mx, prp[r + 1] - prp[r]);
+    sl_len[sl] = mx * kSellC;
+  }
+}
+
 // ------------------------------------------------------------------ a3 / a6: CSR-16 (compressed column indices)
 // Same traversal as k_spmv_csr_pf<WPB, UNR, 16> (half-warp rows, 16-entry lane-strided
 // chunks, next UNR chunks prefetched), but the int32 column index of entry q of row i

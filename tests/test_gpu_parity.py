@@ -494,12 +494,12 @@ def test_default_spmv_format_rule():
     s = solver_for_problem(p, spec, maxit=3, eta=0.0)
     inf = s.get_info()
     s.close()
-    assert inf["t_fmt"] == 3 and inf["t_pairs"] >= 0.375 * p.T.nnz    # B: interpolation pairs (1 - f, f)
+    assert inf["t_fmt"] == 4 and inf["t_pairs"] >= 0.375 * p.T.nnz    # B: interpolation pairs (1 - f, f), sliced ELL
     assert inf["a_fmt"] == 2 and inf["a_pairs"] >= 0.2 * p.A.nnz
     s = solver_for_problem(p, spec, maxit=3, eta=0.0, method="lsqr")
     inf = s.get_info()
     s.close()
-    assert inf["a_fmt"] == 2 and inf["t_fmt"] == 3
+    assert inf["a_fmt"] == 2 and inf["t_fmt"] == 4
     s = solver_for_problem(p, spec, maxit=3, eta=0.0)
     s.debug_set_tuning(14)                                 # forced plain CSR
     inf = s.get_info()
@@ -516,17 +516,20 @@ def test_interpolation_pairs_bitwise_equal_to_pair_csr(monkeypatch):
     rng = np.random.default_rng(5)
     w, x = rng.standard_normal(p.m), rng.standard_normal(p.n)
     out = {}
-    for interp in ("0", "1"):
+    for interp, sell in (("0", "0"), ("1", "0"), ("1", "1")):
         monkeypatch.setenv("SFLSQR_PCSR_INTERP", interp)
+        monkeypatch.setenv("SFLSQR_SELL", sell)
         s = SFLSQR(maxit=4)
         s.set_operator(p.A.nrows, p.A.ncols, p.A.rowptr, p.A.col, p.A.val, t=(p.T.rowptr, p.T.col, p.T.val))
-        out[interp] = (s.get_info()["t_fmt"], s.debug_apply(1, w), s.debug_apply(0, x))
+        out[interp + sell] = (s.get_info()["t_fmt"], s.debug_apply(1, w), s.debug_apply(0, x))
         s.close()
-    assert out["0"][0] == 1 and out["1"][0] == 3
-    assert np.array_equal(out["0"][1], out["1"][1]) and np.array_equal(out["0"][2], out["1"][2])
+    assert out["00"][0] == 1 and out["10"][0] == 3 and out["11"][0] == 4
+    assert np.array_equal(out["00"][1], out["10"][1]) and np.array_equal(out["00"][2], out["10"][2])
     B = OracleCSR(p.T.nrows, p.T.ncols, p.T.rowptr, p.T.col, p.T.val)
     ref = B.matvec(w)
-    assert np.max(np.abs(out["1"][1] - ref)) <= 1e-13 * np.max(np.abs(ref))
+    absref = OracleCSR(p.T.nrows, p.T.ncols, p.T.rowptr, p.T.col, np.abs(p.T.val)).matvec(np.abs(w))
+    for key in ("10", "11"):   # the sliced-ELL copy sums each row in its own (k) order
+        assert np.all(np.abs(out[key][1] - ref) <= 1e-14 * absref + 1e-300)
     # an operator whose pairs are not interpolation weights keeps the full pair values
     m, n = 700, 2000
     rp, col, val = _runs_csr(3, m, n)
