@@ -116,7 +116,8 @@ def _barrier(world):
         dist.barrier()
 
 
-FMT_NAMES = ["CSR", "pair-CSR", "aligned pair-CSR", "interpolation pair-CSR", "sliced-ELL interpolation pairs"]
+FMT_NAMES = ["CSR", "pair-CSR", "aligned pair-CSR", "interpolation pair-CSR", "sliced-ELL interpolation pairs",
+             "sliced-ELL CSR"]
 
 
 def _traffic(workload, kernel):
@@ -342,11 +343,11 @@ def main():
         bpl = d["bytes"] / d["launches"]
         ach = bpl / (d["ms"] / d["launches"] / 1e3) / 1e9
         inf = s.get_info()
-        fnames = {0: "CSR", 1: "pair-CSR", 2: "aligned pair-CSR", 3: "interpolation pair-CSR",
-                  4: "sliced-ELL interpolation pairs"}
+        fnames = dict(enumerate(FMT_NAMES))
         fmt = {"spmv_A": fnames[inf["a_fmt"]], "spmv_T": fnames[inf["t_fmt"]]}
         tkey = dom + {"CSR": "", "pair-CSR": "_pcsr", "aligned pair-CSR": "_apcsr",
-                      "interpolation pair-CSR": "_ipcsr", "sliced-ELL interpolation pairs": "_sell"}[fmt.get(dom, "CSR")]
+                      "interpolation pair-CSR": "_ipcsr", "sliced-ELL interpolation pairs": "_sell",
+                      "sliced-ELL CSR": "_sellcsr"}[fmt.get(dom, "CSR")]
         tr = _traffic(prob.name, tkey)
         l1 = _traffic(prob.name, tkey + "_l1_wavefronts_pct")
         kname = {"spmv_A": f"k_spmv_csr_pf, {fmt['spmv_A']} (A z)",

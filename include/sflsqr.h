@@ -172,7 +172,8 @@ typedef struct sflsqr_info {
   int32_t a_fmt, t_fmt; /* SpMV format of the A / T products: 0 CSR, 1 pair-CSR (any adjacent
                           pair), 2 aligned pair-CSR (pairs at even columns, 16-byte gathers),
                           3 interpolation pair-CSR (every pair (1 - f, f) bitwise: only f stored),
-                          4 the same pairs as sliced ELL, 32 rows per slice, one row per lane    */
+                          4 the same pairs as sliced ELL, 32 rows per slice, one row per lane,
+                          5 plain CSR as sliced ELL (opt-in, SFLSQR_SELL_A=1 for A)              */
 } sflsqr_info;
 
 /* Per-kernel-class device time, recorded with CUDA events on the library stream

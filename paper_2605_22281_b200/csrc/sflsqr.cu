@@ -62,6 +62,15 @@ struct PCSR {  // pair-CSR copy of an operator (k_pcsr_rows): pairs + singleton 
   double* sval = nullptr;
 };
 
+struct SELL {  // sliced-ELL copy of a plain CSR operator (k_spmv_sell_csr)
+  bool ok = false;
+  int64_t entries = 0;
+  int64_t* soff = nullptr;
+  int* rcnt = nullptr;
+  int* ecol = nullptr;
+  double* ev = nullptr;
+};
+
 struct C16 {
   bool ok = false;
   int64_t nchunks = 0;
@@ -101,9 +110,11 @@ struct sflsqr {
   double* blur_tmp = nullptr;
   C16 ca, ct;           // CSR-16 index copies of A and T (SpMV mode 15, on request)
   PCSR pa, pt;          // pair-CSR copies of A and T (SpMV mode 16)
+  SELL ea, et;          // sliced-ELL copies of A and T (plain values)
   int pcsr_unroll = 4;  // pairs in flight per lane in the mode-16 kernel (4 or 2; SFLSQR_PCSR_UNROLL)
   bool pcsr_interp = true;  // interpolation pairs when every pair qualifies (SFLSQR_PCSR_INTERP=0: off)
   bool sell = true;         // sliced-ELL (row per lane) copy of interpolation pairs (SFLSQR_SELL=0: off)
+  bool sell_a = false;      // sliced-ELL copy of the forward operator A (SFLSQR_SELL_A=1)
   // sketch
   bool sk_set = false;
   int sk_kind = 0;  // 0 sparse-sign (R5/R6), 1 dense Gaussian (R21)
@@ -307,6 +318,14 @@ void free_solve(sflsqr_t* h) {
   h->rhs_set = false;
 }
 
+void free_sell(SELL& e) {
+  cudaFree(e.soff);
+  cudaFree(e.rcnt);
+  cudaFree(e.ecol);
+  cudaFree(e.ev);
+  e = SELL();
+}
+
 void free_pcsr(PCSR& p) {
   cudaFree(p.soff);
   cudaFree(p.rcnt);
@@ -343,6 +362,8 @@ void free_op(sflsqr_t* h) {
   }
   free_pcsr(h->pa);
   free_pcsr(h->pt);
+  free_sell(h->ea);
+  free_sell(h->et);
   h->a_rowptr = h->t_rowptr = nullptr;
   h->a_col = h->t_col = nullptr;
   h->a_val = h->t_val = h->taps = h->blur_tmp = nullptr;
@@ -463,6 +484,14 @@ void enqueue_apply(sflsqr_t* h, int which, const DevState* st, const double* x, 
   };
   const C16& cc = which == 0 ? h->ca : h->ct;
   const PCSR& pc = which == 0 ? h->pa : h->pt;
+  const SELL& es = which == 0 ? h->ea : h->et;
+  if (h->spmv_mode < 0 && es.ok) {
+    L.bytes_override(12.0 * es.entries + 4.0 * nrows + 8.0 * (nrows / kSellC + 1) + 8.0 * xlen + 8.0 * nrows);
+    const int64_t nsl = (nrows + kSellC - 1) / kSellC;
+    const int g = (int)std::max<int64_t>(1, std::min<int64_t>((nsl + 15) / 16, 148 * 2 - h->spmv_grid_delta));
+    k_spmv_sell_csr<4><<<g, 512, 0, h->stream>>>(st, nrows, es.soff, es.rcnt, es.ecol, es.ev, x, x_ld, x_koff, y);
+    return;
+  }
   int mode = h->spmv_mode >= 0 ? h->spmv_mode : (pc.ok ? 16 : select_spmv_mode(nnz, nrows));
   if (mode == 15 && !cc.ok) mode = 14;
   if ((mode == 16 || mode == 17) && !pc.ok) mode = 14;
@@ -1270,6 +1299,57 @@ int build_sell(sflsqr_t* h, int64_t nrows, PCSR& p) {
   return check_launch(h);
 }
 
+// Sliced-ELL copy of a plain CSR operator (k_sell_len / k_sell_fill on rowptr, col, val), kept when
+// the slices' padding costs at most max_pad more entries.
+int build_sell_csr(sflsqr_t* h, int64_t nrows, const int64_t* rp, const int32_t* col, const double* val, int64_t nnz,
+                   SELL& e, double max_pad) {
+  free_sell(e);
+  if (nrows < 1 || nnz < 1) return SFLSQR_OK;
+  const int64_t nsl = (nrows + kSellC - 1) / kSellC;
+  int64_t* len = nullptr;
+  void* tmp = nullptr;
+  size_t tb = 0;
+  int rc;
+  if ((rc = dalloc(h, (void**)&len, sizeof(int64_t) * (nsl + 1), nullptr)) ||
+      (rc = dalloc(h, (void**)&e.soff, sizeof(int64_t) * (nsl + 1), nullptr))) {
+    cudaFree(len);
+    free_sell(e);
+    return rc;
+  }
+  CU(h, cudaMemsetAsync(len + nsl, 0, sizeof(int64_t), h->stream));
+  k_sell_len<<<(int)std::min<int64_t>((nsl + 255) / 256, 148 * 16), 256, 0, h->stream>>>(nrows, rp, len);
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, len, e.soff, nsl + 1, h->stream);
+  if ((rc = dalloc(h, &tmp, tb, nullptr))) {
+    cudaFree(len);
+    free_sell(e);
+    return rc;
+  }
+  cub::DeviceScan::ExclusiveSum(tmp, tb, len, e.soff, nsl + 1, h->stream);
+  CU(h, cudaMemcpyAsync(&e.entries, e.soff + nsl, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+  CU(h, cudaStreamSynchronize(h->stream));
+  cudaFree(len);
+  cudaFree(tmp);
+  if ((double)e.entries > (1.0 + max_pad) * (double)nnz ||
+      (rc = dalloc(h, (void**)&e.rcnt, sizeof(int) * nrows, nullptr)) ||
+      (rc = dalloc(h, (void**)&e.ecol, sizeof(int) * std::max<int64_t>(e.entries, 1), nullptr)) ||
+      (rc = dalloc(h, (void**)&e.ev, sizeof(double) * std::max<int64_t>(e.entries, 1), nullptr))) {
+    free_sell(e);
+    cudaGetLastError();
+    return SFLSQR_OK;
+  }
+  CU(h, cudaMemsetAsync(e.ecol, 0, sizeof(int) * e.entries, h->stream));
+  CU(h, cudaMemsetAsync(e.ev, 0, sizeof(double) * e.entries, h->stream));
+  k_sell_fill<<<(int)std::min<int64_t>((nrows + 255) / 256, 148 * 16), 256, 0, h->stream>>>(nrows, rp, col, val, e.soff,
+                                                                                          e.rcnt, e.ecol, e.ev);
+  CU(h, cudaStreamSynchronize(h->stream));
+  if ((rc = check_launch(h))) {
+    free_sell(e);
+    return rc;
+  }
+  e.ok = true;
+  return SFLSQR_OK;
+}
+
 // Auxiliary SpMV formats the selected mode needs (built after every operator upload).
 int build_formats(sflsqr_t* h) {
   if (h->blur) return SFLSQR_OK;
@@ -1312,7 +1392,10 @@ int build_formats(sflsqr_t* h) {
       }
       return r;
     };
-    if ((rc = pick(h->m_loc, h->a_rowptr, h->a_col, h->a_val, h->nnz_a, h->pa))) return rc;
+    if (h->sell_a && h->nnz_a >= 64 * h->m_loc) {
+      if ((rc = build_sell_csr(h, h->m_loc, h->a_rowptr, h->a_col, h->a_val, h->nnz_a, h->ea, 0.10))) return rc;
+    }
+    if (!h->ea.ok && (rc = pick(h->m_loc, h->a_rowptr, h->a_col, h->a_val, h->nnz_a, h->pa))) return rc;
     if ((rc = pick(h->t_rows, h->t_rowptr, h->t_col, h->t_val, h->nnz_t, h->pt))) return rc;
   }
   return SFLSQR_OK;
@@ -1723,6 +1806,7 @@ int sflsqr_create(sflsqr_t** out, const sflsqr_opts* o) {
   if (const char* ev = std::getenv("SFLSQR_SKETCH_SIDE")) h->sketch_side = std::atoi(ev) != 0;
   if (const char* ev = std::getenv("SFLSQR_PCSR_INTERP")) h->pcsr_interp = std::atoi(ev) != 0;
   if (const char* ev = std::getenv("SFLSQR_SELL")) h->sell = std::atoi(ev) != 0;
+  if (const char* ev = std::getenv("SFLSQR_SELL_A")) h->sell_a = std::atoi(ev) != 0;
   if (const char* ev = std::getenv("SFLSQR_SPMV_GRID_DELTA")) h->spmv_grid_delta = std::max(0, std::min(100, std::atoi(ev)));
   if (const char* ev = std::getenv("SFLSQR_PCSR_UNROLL")) h->pcsr_unroll = std::atoi(ev) == 2 ? 2 : 4;
   if (const char* ev = std::getenv("SFLSQR_LR_QR")) h->lr_qr_cgs = std::strcmp(ev, "cgs") == 0;
@@ -2263,8 +2347,8 @@ int sflsqr_get_info(sflsqr_t* h, sflsqr_info* info) {
   const int mode_t = h->spmv_mode >= 0 ? h->spmv_mode : (h->pt.ok ? 16 : 14);
   info->a_pairs = ((mode_a == 16 || mode_a == 17) && h->pa.ok) ? h->pa.npairs : 0;
   info->t_pairs = ((mode_t == 16 || mode_t == 17) && h->pt.ok) ? h->pt.npairs : 0;
-  info->a_fmt = info->a_pairs ? (h->pa.aligned ? 2 : (h->pa.f ? (h->pa.ecol ? 4 : 3) : 1)) : 0;
-  info->t_fmt = info->t_pairs ? (h->pt.aligned ? 2 : (h->pt.f ? (h->pt.ecol ? 4 : 3) : 1)) : 0;
+  info->a_fmt = info->a_pairs ? (h->pa.aligned ? 2 : (h->pa.f ? (h->pa.ecol ? 4 : 3) : 1)) : ((h->spmv_mode < 0 && h->ea.ok) ? 5 : 0);
+  info->t_fmt = info->t_pairs ? (h->pt.aligned ? 2 : (h->pt.f ? (h->pt.ecol ? 4 : 3) : 1)) : ((h->spmv_mode < 0 && h->et.ok) ? 5 : 0);
   return SFLSQR_OK;
 }
 

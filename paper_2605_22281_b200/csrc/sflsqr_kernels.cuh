@@ -774,6 +774,57 @@ __global__ void __launch_bounds__(512, 2) k_spmv_sell_ip(const DevState* st, int
   }
 }
 
+// Plain-CSR sliced ELL (same layout, one value per entry): for the Siddon A, lane = ray and the
+// 32 rays of a slice are neighbouring bins of one angle, so their k-th crossed pixels are close.
+template <int UNR>
+__global__ void __launch_bounds__(512, 2) k_spmv_sell_csr(const DevState* st, int64_t nrows, const int64_t* __restrict__ soff,
+                                                        const int* __restrict__ rcnt, const int* __restrict__ ecol,
+                                                        const double* __restrict__ ev, const double* __restrict__ x_base,
+                                                        int64_t x_ld, int x_koff, double* y) {
+  if (st && st->done) return;
+  const double* __restrict__ x = kvec(st, x_base, x_ld, x_koff);
+  const int lane = threadIdx.x & 31;
+  const int64_t nslices = (nrows + kSellC - 1) / kSellC;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t sl = gw; sl < nslices; sl += nw) {
+    const int64_t row = sl * kSellC + lane;
+    const int cnt = row < nrows ? rcnt[row] : 0;
+    const int L = __reduce_max_sync(0xffffffffu, cnt);
+    const int64_t base = soff[sl] + lane;
+    double sum = 0.0;
+    int cn[UNR];
+    double vn[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      cn[u] = u < cnt ? ld_stream_i(ecol + base + (int64_t)kSellC * u) : 0;
+      vn[u] = u < cnt ? ld_stream_d(ev + base + (int64_t)kSellC * u) : 0.0;
+    }
+    for (int k = 0; k < L; k += UNR) {
+      int c[UNR];
+      double v[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        c[u] = cn[u];
+        v[u] = vn[u];
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int kk = k + UNR + u;
+        cn[u] = kk < cnt ? ld_stream_i(ecol + base + (int64_t)kSellC * kk) : 0;
+        vn[u] = kk < cnt ? ld_stream_d(ev + base + (int64_t)kSellC * kk) : 0.0;
+      }
+      double xv[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) xv[u] = (k + u < cnt) ? __ldg(x + c[u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < UNR; ++u)
+        if (k + u < cnt) sum = fma(v[u], xv[u], sum);
+    }
+    if (row < nrows) y[row] = sum;
+  }
+}
+
 // Sliced-ELL build from an interpolation pair-CSR copy: thread per row scatters its pairs.
 __global__ void __launch_bounds__(256) k_sell_fill(int64_t nrows, const int64_t* __restrict__ prp,
                                                    const int* __restrict__ pcol, const double* __restrict__ pf,
