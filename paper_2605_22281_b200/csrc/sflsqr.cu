@@ -752,6 +752,16 @@ bool launch_pairs_epi(sflsqr_t* h, int which, const double* x, int64_t x_ld, dou
   const int64_t nrows = which == 0 ? h->m_loc : h->t_rows;
   const int64_t xlen = which == 0 ? (h->world > 1 ? h->world * h->n_max : h->n)
                                   : (h->tkind == T_ROWSHARD ? h->world * h->m_max : h->m_loc);
+  if (pc.f && pc.ecol) {  // sliced-ELL interpolation pairs with the fused epilogue
+    Launch L(h, cls, 12.0 * pc.sell_entries + 12.0 * pc.nsingles + 4.0 * nrows + 16.0 * (nrows + 1) + 8.0 * xlen +
+                         8.0 * nrows + extra);
+    const int64_t nsl = (nrows + kSellC - 1) / kSellC;
+    const int g = (int)std::max<int64_t>(1, std::min<int64_t>((nsl + 15) / 16, 148 * 2 - h->spmv_grid_delta));
+    k_spmv_sell_ip<4, true><<<g, 512, 0, h->stream>>>(h->P.st, nrows, pc.soff, pc.rcnt, pc.ecol, pc.ef, pc.srp, pc.scol,
+                                                       pc.sval, x, x_ld, 0, y, E);
+    return true;
+  }
+  (void)grid;
   Launch L(h, cls, (pc.f ? 12.0 : 20.0) * pc.npairs + 12.0 * pc.nsingles + 16.0 * (nrows + 1) + 8.0 * xlen + 8.0 * nrows +
                        extra);
   PairPart PP;

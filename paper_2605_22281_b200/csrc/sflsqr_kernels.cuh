@@ -716,14 +716,17 @@ __global__ void __launch_bounds__(256) k_pcsr_interp(int64_t npairs, const doubl
 // touches one or two lines instead of 32.  Each lane sums its own row in k order (deterministic).
 // Interpolation pairs only (values 1 - f, f); singletons of the row (if any) from the singleton CSR.
 constexpr int kSellC = 32;
-template <int UNR>
+// EPI: the fused epilogues of k_spmv_csr_pf (GKB kinds 1-3, peer reduce-scatter kind 4).
+template <int UNR, bool EPI = false>
 __global__ void __launch_bounds__(512, 2) k_spmv_sell_ip(const DevState* st, int64_t nrows, const int64_t* __restrict__ soff,
                                                        const int* __restrict__ rcnt, const int* __restrict__ scol,
                                                        const double* __restrict__ sf, const int64_t* __restrict__ srp,
                                                        const int* __restrict__ s1col, const double* __restrict__ s1val,
                                                        const double* __restrict__ x_base, int64_t x_ld, int x_koff,
-                                                       double* y) {
+                                                       double* y, SpmvEpi E = SpmvEpi()) {
   if (st && st->done) return;
+  double ea = 1.0, ec = 0.0, nrm = 0.0;
+  if (EPI) epi_coefs(E, st, ea, ec);
   const double* __restrict__ x = kvec(st, x_base, x_ld, x_koff);
   const int lane = threadIdx.x & 31;
   const int64_t nslices = (nrows + kSellC - 1) / kSellC;
@@ -769,7 +772,36 @@ __global__ void __launch_bounds__(512, 2) k_spmv_sell_ip(const DevState* st, int
     }
     if (row < nrows) {
       for (int64_t p = srp[row]; p < srp[row + 1]; ++p) sum = fma(s1val[p], __ldg(x + s1col[p]), sum);
-      y[row] = sum;
+      if (EPI && E.kind == 4) {
+        const int64_t g = row / E.nmax;
+        E.peers[g][(int64_t)E.src * E.nmax + (row - g * E.nmax)] = sum;
+      } else {
+        if (EPI) {
+          sum = E.kind == 3 ? sum * ea : fma(sum, ea, -ec * E.aux[row]);
+          nrm = fma(sum, sum, nrm);
+        }
+        y[row] = sum;
+      }
+    }
+  }
+  if (EPI && E.kind != 4) {
+    __shared__ double sh[33];
+    __shared__ int s_last;
+    nrm = block_sum<512>(nrm, sh);
+    if (threadIdx.x == 0) E.part[(size_t)E.slot_out * kVecBlocks + blockIdx.x] = nrm;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(E.ctr + E.ctr_idx, 1) == (int)gridDim.x - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const double* pp = E.part + (size_t)E.slot_out * kVecBlocks;
+    double v = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += 512) v += __ldcg(pp + b);
+    v = block_sum<512>(v, sh);
+    if (threadIdx.x == 0) {
+      E.scal[E.slot_out] = v;
+      E.ctr[E.ctr_idx] = 0;
     }
   }
 }
