@@ -359,8 +359,10 @@ def main():
                 "unit": "GB/s", "frac": ach / peak, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": bpl, "traffic": tr,
                 "l1_wavefronts_pct_of_peak": l1,
-                "note": "the pair formats move fewer HBM bytes than CSR; the interpolation pair-CSR product is bound "
-                        "by its L1 gather wavefronts (ncu l1_wavefronts_pct_of_peak), not HBM (DESIGN.md §5)"}
+                "note": ("bytes of the format the product runs on (DESIGN.md §5); this product's gathers keep the L1 "
+                         "data pipe at l1_wavefronts_pct_of_peak (ncu), so inside the power-capped loop it follows "
+                         "the SM clock" if (l1 or 0) > 70 else
+                         "bytes of the format the product runs on (DESIGN.md §5); HBM bound")}
     step_bytes = sum(d["bytes"] for d in prof.values())
     step_gbs = step_bytes / (ms / 1e3) / 1e9 if step_bytes else None   # algorithmic bytes of the step / production time
 
