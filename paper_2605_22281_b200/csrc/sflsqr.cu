@@ -115,6 +115,7 @@ struct sflsqr {
   bool pcsr_interp = true;  // interpolation pairs when every pair qualifies (SFLSQR_PCSR_INTERP=0: off)
   bool sell = true;         // sliced-ELL (row per lane) copy of interpolation pairs (SFLSQR_SELL=0: off)
   bool sell_a = false;      // sliced-ELL copy of the forward operator A (SFLSQR_SELL_A=1)
+  bool cgs_selective = true;  // CGS2 second pass only when needed (one rank; SFLSQR_CGS_SELECTIVE=0: always)
   // sketch
   bool sk_set = false;
   int sk_kind = 0;  // 0 sparse-sign (R5/R6), 1 dense Gaussian (R21)
@@ -1627,6 +1628,7 @@ int alloc_solve(sflsqr_t* h) {
     P.zsend = nullptr;  // the peer stores replace the send copies
     P.wsend = nullptr;
   }
+  P.cgs_selective = (h->cgs_selective && h->world == 1) ? 1 : 0;
   if (sketched && (rc = build_sketch(h))) return rc;
   h->bufs = true;
   return SFLSQR_OK;
@@ -1817,6 +1819,7 @@ int sflsqr_create(sflsqr_t** out, const sflsqr_opts* o) {
   if (const char* ev = std::getenv("SFLSQR_PCSR_INTERP")) h->pcsr_interp = std::atoi(ev) != 0;
   if (const char* ev = std::getenv("SFLSQR_SELL")) h->sell = std::atoi(ev) != 0;
   if (const char* ev = std::getenv("SFLSQR_SELL_A")) h->sell_a = std::atoi(ev) != 0;
+  if (const char* ev = std::getenv("SFLSQR_CGS_SELECTIVE")) h->cgs_selective = std::atoi(ev) != 0;
   if (const char* ev = std::getenv("SFLSQR_SPMV_GRID_DELTA")) h->spmv_grid_delta = std::max(0, std::min(100, std::atoi(ev)));
   if (const char* ev = std::getenv("SFLSQR_PCSR_UNROLL")) h->pcsr_unroll = std::atoi(ev) == 2 ? 2 : 4;
   if (const char* ev = std::getenv("SFLSQR_LR_QR")) h->lr_qr_cgs = std::strcmp(ev, "cgs") == 0;

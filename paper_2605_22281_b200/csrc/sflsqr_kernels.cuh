@@ -71,6 +71,7 @@ struct Params {
   double* part;
   int slot_zin, slot_z0, slot_win, slot_w0, slot_xmax, slot_res, slot_beta;
   int orth_alg;            // OrthAlg: fused (window <= kFuseJ vectors), literal MGS passes, or CGS2
+  int cgs_selective;        // CGS2: skip the second pass when ||v'|| >= ||v|| / sqrt(2) (one rank)
   int slot_zf, slot_zout, slot_wf, slot_wout;  // fused orthogonalisation slots (kFuseAcc + 1 per side)
   int* ctr;                // last-block arrival counters (one per reduction site)
   unsigned int* bar;       // grid barrier of the cooperative phase kernels (count, generation)
@@ -1439,12 +1440,22 @@ __device__ __forceinline__ void cgs_window(const Params& P, int side, int kk, in
   j0 = max(1, kk - P.ell);
 }
 
+// Kahan's "twice is enough" criterion: after the first classical Gram-Schmidt pass, a second one
+// is needed only when the pass removed more than half of ||v||^2 (||v'||^2 < ||v||^2 / 2); the
+// first pass then already leaves v' orthogonal to the window to working precision.
+__device__ __forceinline__ bool cgs_skip_second(const Params& P, int side) {
+  if (!P.cgs_selective) return false;
+  const double vin = P.scal[side == 0 ? P.slot_zf : P.slot_wf], vout = P.scal[side == 0 ? P.slot_zout : P.slot_wout];
+  return vout >= 0.5 * vin;
+}
+
 __global__ void __launch_bounds__(kVecThreads) k_cgs_dots(Params P, int side, int stage, int koff) {
   extern __shared__ double cg_sm[];
   double* vs = cg_sm;                 // kCgsChunk
   double* acc = cg_sm + kCgsChunk;    // J + 1 (ldc)
   const DevState* st = P.st;
   if (st->done) return;
+  if (stage == 1 && cgs_skip_second(P, side)) return;
   int J, j0;
   cgs_window(P, side, st->k + koff, J, j0);
   const double* __restrict__ v = side == 0 ? P.z : P.w;
@@ -1524,8 +1535,9 @@ __global__ void __launch_bounds__(kVecThreads) k_cgs_update(Params P, int side, 
   double* __restrict__ v = side == 0 ? P.z : P.w;
   const int64_t len = side == 0 ? P.n : P.m;
   const double* c = P.cscal + (size_t)stage * P.ldc;
+  const bool skip = stage == 1 && cgs_skip_second(P, side);  // ||v'||^2 of the first pass stays in slot_out
   for (int j = threadIdx.x; j < J; j += kVecThreads) {
-    cs[j] = c[j];
+    cs[j] = skip ? 0.0 : c[j];
     qp[j] = mgs_basis(P, side, j0 + j);
   }
   __syncthreads();
@@ -1533,13 +1545,14 @@ __global__ void __launch_bounds__(kVecThreads) k_cgs_update(Params P, int side, 
     const double* c1 = P.cscal;
     for (int j = threadIdx.x; j < J; j += kVecThreads) {
       const int row = j0 - 1 + j;
-      const double cf = c1[j] + cs[j];
+      const double cf = skip ? c1[j] : c1[j] + cs[j];
       if (side == 0)
         P.Tm[(int64_t)row + (int64_t)(kk - 1) * P.ldtm] = cf;
       else
         P.H[(int64_t)row + (int64_t)(kk - 1) * P.ldh] = cf;
     }
   }
+  if (skip) return;
   // row tiles of 2 x kVecThreads rows, two rows per thread, window vectors in order (the same
   // per-row operation order as a one-row-per-thread loop), 4 vectors x 2 rows loads in flight
   double acc = 0.0;
@@ -1575,9 +1588,9 @@ __global__ void __launch_bounds__(kVecThreads) k_cgs_update(Params P, int side, 
       acc = fma(b, b, acc);
     }
   }
-  if (stage == 0) return;
+  if (stage == 0 && !P.cgs_selective) return;
   acc = block_sum<kVecThreads>(acc, sh);
-  const int so = side == 0 ? P.slot_zout : P.slot_wout;
+  const int so = side == 0 ? P.slot_zout : P.slot_wout;  // stage 0 (selective): ||v'||^2 for the criterion
   if (threadIdx.x == 0) P.part[(size_t)so * kVecBlocks + blockIdx.x] = acc;
   last_block_reduce(P, so, 1, CTR_CGS, false);
 }
