@@ -539,6 +539,59 @@ def test_interpolation_pairs_bitwise_equal_to_pair_csr(monkeypatch):
     s.close()
 
 
+def _interp_csr(seed, nrows, ncols, singles=True):
+    """Rows of (1 - f, f) pairs at adjacent columns (the interpolation structure), ragged lengths
+    (64..200 pairs, some rows far shorter than their slice's longest), optional singleton tails."""
+    rng = np.random.default_rng(seed)
+    rows_c, rows_v = [], []
+    for i in range(nrows):
+        npair = int(rng.integers(140, 161)) if i % 97 else int(rng.integers(0, 5))
+        base = np.sort(rng.choice(np.arange(0, ncols - 4, 3), size=npair, replace=False))
+        f = rng.uniform(0.0, 1.0, npair)
+        c = np.empty(2 * npair, np.int64)
+        v = np.empty(2 * npair)
+        c[0::2], c[1::2] = base, base + 1
+        v[0::2], v[1::2] = 1.0 - f, f
+        if singles and i % 5 == 0 and npair > 0:     # a singleton after the last pair
+            c = np.concatenate([c, [base[-1] + 3]])      # not adjacent to base[-1] + 1
+            v = np.concatenate([v, [rng.standard_normal()]])
+        rows_c.append(c)
+        rows_v.append(v)
+    rowptr = np.concatenate([[0], np.cumsum([len(c) for c in rows_c])]).astype(np.int64)
+    return rowptr, np.concatenate(rows_c).astype(np.int32), np.concatenate(rows_v)
+
+
+@pytest.mark.parametrize("singles", [False, True])
+def test_sliced_ell_interpolation_pairs_ragged(singles):
+    # T given as a ragged interpolation operator (n rows not a multiple of the 32-row slices, rows of
+    # very different lengths in one slice, optional singletons): the sliced-ELL kernel, the
+    # interpolation pair-CSR kernel and plain CSR all match the oracle product
+    from paper_2605_22281_b200 import SFLSQR
+    m, n = 1500, 1000 + 13
+    trp, tcol, tval = _interp_csr(7, n, m, singles)
+    T = OracleCSR(n, m, trp, tcol, tval)
+    A = T.transpose()                                    # any A with the right shape
+    rng = np.random.default_rng(8)
+    w = rng.standard_normal(m)
+    ref = T.matvec(w)
+    absref = OracleCSR(n, m, trp, tcol, np.abs(tval)).matvec(np.abs(w))
+    fmts = set()
+    for tune in (-1, 14):
+        s = SFLSQR(maxit=4)
+        s.set_operator(m, n, A.rowptr, A.col, A.val, t=(trp, tcol, tval))
+        if tune == 14:
+            s.debug_set_tuning(14)
+        fmts.add(s.get_info()["t_fmt"])
+        got = s.debug_apply(1, w)
+        s.close()
+        assert np.all(np.abs(got - ref) <= 1e-14 * absref + 1e-300), tune
+    # the sliced-ELL copy is kept when its padding is <= 10 % (here about 8 %): format 4
+    npairs = np.array([(np.diff(trp)[r] // 2) for r in range(n)])
+    slices = [npairs[i:i + 32] for i in range(0, n, 32)]
+    pad = sum(len(sl) * sl.max() for sl in slices) / npairs.sum() - 1.0
+    assert pad <= 0.10 and fmts == {4, 0}, (pad, fmts)
+
+
 def test_csr16_overflow_falls_back_to_int32():
     # a 16-entry chunk spanning > 65536 columns cannot be offset-encoded: the operator stays int32 CSR
     from gen.problems import CSR
