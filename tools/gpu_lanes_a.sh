@@ -1,0 +1,5 @@
+for r in 1 2; do
+for v in 16 32; do
+SFLSQR_PAIR_LANES_A=$v timeout 900 python bench.py --config 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_c3_pa$v.$r.log 2>&1
+SFLSQR_PAIR_LANES_A=$v timeout 900 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_c4_pa$v.$r.log 2>&1
+done; done
