@@ -440,10 +440,11 @@ int reduce_slots(sflsqr_t* h, int slot0, int ns, bool is_max) {
   return coll_allreduce(h, h->P.scal + slot0, ns, is_max);
 }
 
-// Default SpMV variant (measured on configs 3-4, tools/spmv_tune.py):
+// Plain-CSR SpMV variant (measured on configs 3-4, tools/spmv_tune.py):
 // half-warp rows, 32 adjacent rows per 512-thread CTA, 4 CTAs per SM, the next
 // 4 chunks' indices/values loaded before the current gathers (mode 14).  Fixed,
-// so results are reproducible run to run.
+// so results are reproducible run to run.  Operators with a pair-CSR or sliced-ELL copy
+// (build_formats, the default rule of DESIGN.md §5) run on that copy instead.
 int select_spmv_mode(int64_t nnz, int64_t nrows) {
   (void)nnz;
   (void)nrows;
