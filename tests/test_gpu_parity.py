@@ -592,6 +592,28 @@ def test_sliced_ell_interpolation_pairs_ragged(singles):
     assert pad <= 0.10 and fmts == {4, 0}, (pad, fmts)
 
 
+def test_pair_formats_odd_dimensions():
+    # odd n (97^2 pixels, row-major order) and odd m: the columns of Z / W are 16-byte aligned only
+    # for every other k, so the aligned pair kernel alternates with its two-load fallback; the
+    # sliced-ELL backprojector does not depend on alignment.  Same bar as the other solver runs.
+    from paper_2605_22281_b200 import solver_for_problem
+    p = make_problem(4, N=97, n_angles=61, nb=139)
+    assert p.n % 2 == 1 and p.m % 2 == 1
+    spec = p.solvers[0]
+    r = solve_problem(p, spec, maxit=10, eta=0.0)
+    s = solver_for_problem(p, spec, maxit=10, eta=0.0)
+    inf = s.get_info()
+    s.set_rhs(p.b)
+    s.iterate(10)
+    tr, sk = s.get_residual_norms()
+    x = s.get_x()
+    s.close()
+    assert inf["a_fmt"] == 2 and inf["t_fmt"] == 4, (inf["a_fmt"], inf["t_fmt"])
+    assert np.max(np.abs(tr - np.array(r.true_res)) / np.array(r.true_res)) < 1e-9
+    assert np.max(np.abs(sk - np.array(r.sketch_res)) / np.array(r.sketch_res)) < 1e-9
+    assert np.linalg.norm(x - r.x) / np.linalg.norm(r.x) < 1e-6
+
+
 def test_csr16_overflow_falls_back_to_int32():
     # a 16-entry chunk spanning > 65536 columns cannot be offset-encoded: the operator stays int32 CSR
     from gen.problems import CSR
