@@ -152,6 +152,7 @@ struct sflsqr {
   // fixed share of rows finishes last.  One CTA fewer keeps every CTA resident from the start:
   // config 4 190 -> 201 it/s (same box), config 3 unchanged.
   int spmv_grid_delta = 1;
+  bool pdl = true;  // programmatic dependent launch of the main-stream kernels (SFLSQR_PDL=0: off)
   int band_shift = 16;   // reserved
   bool prof_on = false;
   Prof prof;
@@ -440,6 +441,25 @@ int reduce_slots(sflsqr_t* h, int slot0, int ns, bool is_max) {
   return coll_allreduce(h, h->P.scal + slot0, ns, is_max);
 }
 
+// Launch with programmatic stream serialization (PDL) when enabled: the kernel may become
+// resident while its predecessor in the stream drains (every kernel launched this way starts with
+// pdl_wait()).  SFLSQR_PDL=0: plain launches.
+template <typename... KArgs, typename... Args>
+void launch_pdl(sflsqr_t* h, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = h->pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 // Plain-CSR SpMV variant (measured on configs 3-4, tools/spmv_tune.py):
 // half-warp rows, 32 adjacent rows per 512-thread CTA, 4 CTAs per SM, the next
 // 4 chunks' indices/values loaded before the current gathers (mode 14).  Fixed,
@@ -513,14 +533,16 @@ void enqueue_apply(sflsqr_t* h, int which, const DevState* st, const double* x, 
                        8.0 * nrows);
       const int64_t nsl = (nrows + kSellC - 1) / kSellC;
       const int g = (int)std::max<int64_t>(1, std::min<int64_t>((nsl + 15) / 16, 148 * 2 - h->spmv_grid_delta));
-      k_spmv_sell_ip<4><<<g, 512, 0, h->stream>>>(st, nrows, pc.soff, pc.rcnt, pc.ecol, pc.ef, pc.srp, pc.scol, pc.sval,
-                                                   x, x_ld, x_koff, y);
+      launch_pdl(h, k_spmv_sell_ip<4, false>, g, 512, 0, h->stream, st, nrows, (const int64_t*)pc.soff,
+                 (const int*)pc.rcnt, (const int*)pc.ecol, (const double*)pc.ef, (const int64_t*)pc.srp,
+                 (const int*)pc.scol, (const double*)pc.sval, x, x_ld, x_koff, y, SpmvEpi());
     } else if (pc.f)
       k_spmv_csr_pf<16, 4, 16, false, 6><<<grid_for(32, 2), 512, 0, h->stream>>>(
           st, nrows, pc.srp, pc.scol, pc.sval, x, x_ld, x_koff, y, SpmvEpi(), PP);
     else if (pc.aligned && x16)
-      k_spmv_csr_pf<16, 4, 16, false, 5><<<grid_for(32, 2), 512, 0, h->stream>>>(
-          st, nrows, pc.srp, pc.scol, pc.sval, x, x_ld, x_koff, y, SpmvEpi(), PP);
+      launch_pdl(h, k_spmv_csr_pf<16, 4, 16, false, 5>, grid_for(32, 2), 512, 0, h->stream, st, nrows,
+                 (const int64_t*)pc.srp, (const int*)pc.scol, (const double*)pc.sval, x, x_ld, x_koff, y, SpmvEpi(),
+                 PP);
     else if (h->pcsr_unroll == 4)
       k_spmv_csr_pf<16, 4, 16, false, 4><<<grid_for(32, 2), 512, 0, h->stream>>>(
           st, nrows, pc.srp, pc.scol, pc.sval, x, x_ld, x_koff, y, SpmvEpi(), PP);
@@ -563,7 +585,8 @@ void enqueue_apply(sflsqr_t* h, int which, const DevState* st, const double* x, 
       k_spmv_csr_pf<16, 4, 32><<<grid_for(16, 4), 512, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
       break;
     case 14:
-      k_spmv_csr_pf<16, 4, 16><<<grid_for(32, 4), 512, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
+      launch_pdl(h, k_spmv_csr_pf<16, 4, 16>, grid_for(32, 4), 512, 0, h->stream, st, nrows, rp, (const int*)col, val,
+                 x, x_ld, x_koff, y, SpmvEpi(), PairPart());
       break;
     default:  // 3
       k_spmv_csr_rows<32, 4><<<grid_for(32, 2), 1024, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
@@ -615,11 +638,11 @@ void k_xupdate_launch_side(sflsqr_t* h) {
 void launch_res(sflsqr_t* h, cudaStream_t s, int fuse_stop) {
   const int rpt = gemv_rpt(h->m_loc), g = gemv_grid(h->m_loc, rpt);
   if (rpt == 8)
-    k_res_partial<8><<<g, kVecThreads, 0, s>>>(h->P, fuse_stop);
+    launch_pdl(h, k_res_partial<8>, g, kVecThreads, 0, s, h->P, fuse_stop);
   else if (rpt == 4)
-    k_res_partial<4><<<g, kVecThreads, 0, s>>>(h->P, fuse_stop);
+    launch_pdl(h, k_res_partial<4>, g, kVecThreads, 0, s, h->P, fuse_stop);
   else
-    k_res_partial<2><<<g, kVecThreads, 0, s>>>(h->P, fuse_stop);
+    launch_pdl(h, k_res_partial<2>, g, kVecThreads, 0, s, h->P, fuse_stop);
 }
 
 // skbuf = S v (this rank's coordinates), allreduced over ranks.
@@ -701,13 +724,13 @@ int enqueue_orth(sflsqr_t* h, int side, int koff) {
   if (P.orth_alg == ORTH_FUSED) {
     {
       Launch L(h, SFLSQR_KC_ORTH, v8 * (1 + J));
-      k_orth_dots<<<vec_grid(side == 0 ? h->n_loc : h->m_loc), kVecThreads, 0, h->stream>>>(P, side, koff);
+      launch_pdl(h, k_orth_dots, vec_grid(side == 0 ? h->n_loc : h->m_loc), kVecThreads, 0, h->stream, P, side, koff);
     }
     if ((rc = coll_allreduce(h, P.scal + slot_f, kFuseAcc, false))) return rc;
     if (side == h->axpy_wait_sk) CU(h, cudaStreamWaitEvent(h->stream, h->ev_sk, 0));
     {
       Launch L(h, SFLSQR_KC_ORTH, v8 * (2 + J));
-      k_orth_axpy<<<vec_grid(side == 0 ? h->n_loc : h->m_loc), kVecThreads, 0, h->stream>>>(P, side, koff);
+      launch_pdl(h, k_orth_axpy, vec_grid(side == 0 ? h->n_loc : h->m_loc), kVecThreads, 0, h->stream, P, side, koff);
     }
     return coll_allreduce(h, P.scal + slot_out, 1, false);
   }
@@ -967,7 +990,7 @@ int enqueue_iteration(sflsqr_t* h) {
   // a1 end + a2: normalise, tau, store z_k
   if (!coop) {
     Launch L(h, SFLSQR_KC_TAU, n8 * (2 + (P.use_pring ? 1 : 0) + (P.precond ? 1 : 0)));
-    k_finish_z<<<vec_grid(h->n_loc), kVecThreads, 0, h->stream>>>(P);
+    launch_pdl(h, k_finish_z, vec_grid(h->n_loc), kVecThreads, 0, h->stream, P);
   }
   if (P.precond == SFLSQR_PRECOND_LOWRANK_RND && (rc = enqueue_lowrank(h))) return rc;
   // a3: w = A z_k  (z_k = Z[:, k-1]; all-gathered across ranks when sharded)
@@ -1011,7 +1034,7 @@ int enqueue_iteration(sflsqr_t* h) {
     h->axpy_wait_sk = -1;
     if (rc) return rc;
     Launch L(h, SFLSQR_KC_ORTH, 2 * m8);
-    k_finish_w<<<vec_grid(h->m_loc), kVecThreads, 0, h->stream>>>(P);
+    launch_pdl(h, k_finish_w, vec_grid(h->m_loc), kVecThreads, 0, h->stream, P);
   }
   if (fork_ls && P.method == SFLSQR_METHOD_FLSQR && (rc = enqueue_ls(h, true))) return rc;
   // a8 on the side stream after the LS (sFLSQR / FLSQR with an x-dependent tau, one rank): the main
@@ -1089,7 +1112,7 @@ int enqueue_iteration(sflsqr_t* h) {
   }
   if (!fuse_stop) {
     Launch L(h, SFLSQR_KC_STOP, 0.0);
-    k_stop<<<1, 32, 0, h->stream>>>(P);
+    launch_pdl(h, k_stop, 1, 32, 0, h->stream, P);
   }
   return SFLSQR_OK;
 }
@@ -1816,6 +1839,7 @@ int sflsqr_create(sflsqr_t** out, const sflsqr_opts* o) {
     }
   }
   if (const char* ev = std::getenv("SFLSQR_SPMV_MODE")) h->spmv_mode = std::atoi(ev);
+  if (const char* ev = std::getenv("SFLSQR_PDL")) h->pdl = std::atoi(ev) != 0;
   if (const char* ev = std::getenv("SFLSQR_SKETCH_SIDE")) h->sketch_side = std::atoi(ev) != 0;
   if (const char* ev = std::getenv("SFLSQR_PCSR_INTERP")) h->pcsr_interp = std::atoi(ev) != 0;
   if (const char* ev = std::getenv("SFLSQR_SELL")) h->sell = std::atoi(ev) != 0;

@@ -204,6 +204,12 @@ __device__ __forceinline__ bool last_block_reduce(const Params& P, int s0, int n
 }
 
 // Streaming (read-once) loads: bypass L1 allocation so L1 keeps the gathered vector.
+// Programmatic dependent launch: a kernel launched with the programmatic-serialization attribute
+// may become resident while its predecessor in the stream drains; griddepcontrol.wait blocks until
+// the predecessor has completed and its memory is visible.  A no-op for normal launches.  Every
+// kernel that can be launched that way calls it before its first global memory access.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ int4 ld_stream_i4(const int4* p) {
   int4 r;
   asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.s32 {%0,%1,%2,%3}, [%4];"
@@ -488,6 +494,7 @@ __global__ void __launch_bounds__(WPB * 32, (EPI || PAIRS) ? 2 : 2048 / (WPB * 3
                                                             const double* __restrict__ x_base, int64_t x_ld,
                                                             int x_koff, double* y, SpmvEpi E = SpmvEpi(),
                                                             PairPart PP = PairPart()) {
+  pdl_wait();
   if (st && st->done) return;
   double ea = 1.0, ec = 0.0, nrm = 0.0;
   if (EPI) epi_coefs(E, st, ea, ec);
@@ -725,6 +732,7 @@ __global__ void __launch_bounds__(512, 2) k_spmv_sell_ip(const DevState* st, int
                                                        const int* __restrict__ s1col, const double* __restrict__ s1val,
                                                        const double* __restrict__ x_base, int64_t x_ld, int x_koff,
                                                        double* y, SpmvEpi E = SpmvEpi()) {
+  pdl_wait();
   if (st && st->done) return;
   double ea = 1.0, ec = 0.0, nrm = 0.0;
   if (EPI) epi_coefs(E, st, ea, ec);
@@ -1398,6 +1406,7 @@ __device__ __forceinline__ void orth_axpy_block(const Params& P, int side, int J
 }
 
 __global__ void __launch_bounds__(kVecThreads, 4) k_orth_dots(Params P, int side, int koff) {
+  pdl_wait();
   const DevState* st = P.st;
   if (st->done) return;
   const int k = st->k + koff;
@@ -1409,6 +1418,7 @@ __global__ void __launch_bounds__(kVecThreads, 4) k_orth_dots(Params P, int side
 }
 
 __global__ void __launch_bounds__(kVecThreads) k_orth_axpy(Params P, int side, int koff) {
+  pdl_wait();
   const DevState* st = P.st;
   if (st->done) return;
   const int k = st->k + koff;
@@ -1669,6 +1679,7 @@ __device__ __forceinline__ bool finish_z_body(const Params& P, DevState* st, int
 }
 
 __global__ void __launch_bounds__(kVecThreads) k_finish_z(Params P) {
+  pdl_wait();
   __shared__ double sh[33];
   DevState* st = P.st;
   if (st->done) return;
@@ -2153,6 +2164,7 @@ __device__ __forceinline__ void finish_w_body(const Params& P, DevState* st, int
 }
 
 __global__ void __launch_bounds__(kVecThreads) k_finish_w(Params P) {
+  pdl_wait();
   __shared__ double sh[33];
   DevState* st = P.st;
   if (st->done) return;
@@ -2611,6 +2623,7 @@ __device__ __forceinline__ void stop_body(const Params& P, DevState* st, double 
 // the stop tests.
 template <int RPT>
 __global__ void __launch_bounds__(kVecThreads) k_res_partial(Params P, int fuse_stop) {
+  pdl_wait();
   __shared__ double sh[33];
   __shared__ double gs[kMaxD];
   DevState* st = P.st;
@@ -2639,6 +2652,7 @@ __global__ void __launch_bounds__(kVecThreads) k_res_partial(Params P, int fuse_
 
 // a9 without the fused residual (no history, or several ranks: after the allreduce).
 __global__ void __launch_bounds__(32) k_stop(Params P) {
+  pdl_wait();
   DevState* st = P.st;
   if (st->done || threadIdx.x != 0) return;
   stop_body(P, st, P.want_res ? sqrt(P.scal[P.slot_res]) : NAN);
