@@ -614,6 +614,30 @@ def test_pair_formats_odd_dimensions():
     assert np.linalg.norm(x - r.x) / np.linalg.norm(r.x) < 1e-6
 
 
+@pytest.mark.parametrize("knob", ["SFLSQR_PDL", "SFLSQR_SKETCH_SIDE", "SFLSQR_SPMV_GRID_DELTA"])
+def test_scheduling_knobs_bitwise_neutral(monkeypatch, knob):
+    # launch scheduling (programmatic dependent launch, the sketch on the side stream, the SpMV grid
+    # size) changes no arithmetic: the same solve bit for bit with the knob off
+    from paper_2605_22281_b200 import solver_for_problem
+    p = make_problem(4, N=96, n_angles=61, nb=137)
+    spec = p.solvers[0]
+    out = []
+    for val in ("0", None):
+        if val is None:
+            monkeypatch.delenv(knob, raising=False)
+        else:
+            monkeypatch.setenv(knob, val)
+        s = solver_for_problem(p, spec, maxit=12, eta=0.0)
+        s.set_rhs(p.b)
+        s.iterate(12)
+        tr, sk = s.get_residual_norms()
+        out.append((s.get_x(), tr, sk))
+        s.close()
+    # (SFLSQR_SPMV_GRID_DELTA changes which CTA takes which rows, not any row's summation order)
+    for a, b in zip(out[0], out[1]):
+        assert np.array_equal(a, b)
+
+
 def test_csr16_overflow_falls_back_to_int32():
     # a 16-entry chunk spanning > 65536 columns cannot be offset-encoded: the operator stays int32 CSR
     from gen.problems import CSR
