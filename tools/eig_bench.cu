@@ -776,6 +776,201 @@ void run_oss(const double* dG, int l, int r, double* dP, int* dsw, const std::ve
          cudaGetErrorString(cudaGetLastError()));
 }
 
+// ---------------------------------------------------------------- mixed precision (fp32 start)
+// Phase 1: fp32 one-sided Jacobi on float(G) (slot-stored, as eig_oss); phase 2: V = normalised
+// fp32 columns in fp64, re-orthonormalised by Newton-Schulz V <- V (3I - V^T V) / 2; phase 3:
+// G' = V^T G V; phase 4: fp64 one-sided Jacobi on G' (nearly diagonal: few sweeps); phase 5:
+// P = (V A_top D^-1)(...)^T.  Even l only (no dummy slot).
+constexpr int kLdM = kMaxL + 1;
+template <typename T>
+__device__ int jacobi_os(T* buf, int L, int np, double tol2) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 3, j = tid & 7;
+  const unsigned gmask = 0xffu << (lane & ~7);
+  const int sp = w, sq = L - 1 - w;
+  const int np_ = sp == 0 ? 0 : (sp == 1 ? L - 1 : sp - 1), nq_ = sq == 1 ? L - 1 : sq - 1;
+  int cur = 0, sweep = 0;
+  for (; sweep < 30; ++sweep) {
+    int rotated = 0;
+    for (int step = 0; step < L - 1; ++step) {
+      const T* Ac = buf + cur * kMaxL * kLdS;
+      T* An = buf + (cur ^ 1) * kMaxL * kLdS;
+      if (w < np) {
+        T ap[kMaxL / 8], aq[kMaxL / 8];
+#pragma unroll
+        for (int k = 0; k < kMaxL / 8; ++k) {
+          const int rr = j + 8 * k;
+          ap[k] = rr < L ? Ac[sp * kLdS + rr] : T(0);
+          aq[k] = rr < L ? Ac[sq * kLdS + rr] : T(0);
+        }
+        T al = 0, be = 0, ga = 0;
+#pragma unroll
+        for (int k = 0; k < kMaxL / 8; ++k) {
+          al = fma(ap[k], ap[k], al);
+          be = fma(aq[k], aq[k], be);
+          ga = fma(ap[k], aq[k], ga);
+        }
+#pragma unroll
+        for (int o = 4; o; o >>= 1) {
+          al += __shfl_xor_sync(gmask, al, o, 8);
+          be += __shfl_xor_sync(gmask, be, o, 8);
+          ga += __shfl_xor_sync(gmask, ga, o, 8);
+        }
+        T c = 1, sn = 0;
+        if (ga != T(0) && (double)ga * ga > tol2 * (double)al * be) {
+          rotated = 1;
+          const T dd = be - al;
+          const T sg = ((dd >= T(0)) == (ga >= T(0))) ? T(1) : T(-1);
+          const T h = rsqrt(fma(dd, dd, T(4) * ga * ga));
+          const T u = fma(T(0.5) * fabs(dd), h, T(0.5));
+          const T rc = rsqrt(u);
+          c = u * rc;
+          sn = sg * fabs(ga) * h * rc;
+        }
+#pragma unroll
+        for (int k = 0; k < kMaxL / 8; ++k) {
+          const int rr = j + 8 * k;
+          if (rr < L) {
+            An[np_ * kLdS + rr] = c * ap[k] - sn * aq[k];
+            An[nq_ * kLdS + rr] = sn * ap[k] + c * aq[k];
+          }
+        }
+      }
+      cur ^= 1;
+      __syncthreads();
+    }
+    if (!__syncthreads_or(rotated)) break;
+  }
+  return cur | (sweep << 1);
+}
+
+// C (L x L, ld kLdM) = op(A) op(B): tA / tB transpose flags; 256 threads
+__device__ void gemm_small(double (*C)[kLdM], double (*A)[kLdM], bool tA, double (*B)[kLdM], bool tB, int L) {
+  for (int e = threadIdx.x; e < L * L; e += 256) {
+    const int i = e / L, jj = e % L;
+    double acc = 0.0;
+    for (int k = 0; k < L; ++k) acc = fma(tA ? A[k][i] : A[i][k], tB ? B[jj][k] : B[k][jj], acc);
+    C[i][jj] = acc;
+  }
+}
+
+__global__ void __launch_bounds__(256) eig_mix(const double* G, int l, int r, double* Pout, int* sweeps_out, long long* clk) {
+  extern __shared__ double sm[];
+  double* A64 = sm;                                   // 2 x kMaxL x kLdS doubles (phase 4)
+  float* A32 = reinterpret_cast<float*>(sm);          // aliases A64 during phase 1
+  double(*V)[kLdM] = reinterpret_cast<double(*)[kLdM]>(sm + 2 * kMaxL * kLdS);
+  double(*Wm)[kLdM] = reinterpret_cast<double(*)[kLdM]>(sm + 2 * kMaxL * kLdS + kMaxL * kLdM);
+  double(*Gs)[kLdM] = reinterpret_cast<double(*)[kLdM]>(sm + 2 * kMaxL * kLdS + 2 * kMaxL * kLdM);
+  __shared__ double nrm[kMaxL];
+  __shared__ int top[kMaxL];
+  const int L = l, np = L / 2, tid = threadIdx.x;
+  for (int e = tid; e < L * L; e += 256) {
+    const int c = e / L, rr = e % L;
+    A32[c * kLdS + rr] = (float)G[rr * l + c];
+    Gs[rr][c] = G[rr * l + c];
+  }
+  __syncthreads();
+  const int r1 = jacobi_os<float>(A32, L, np, (double)L * 3.55e-15);  // (sqrt(L) 2^-24)^2
+  const float* Af = A32 + (r1 & 1) * kMaxL * kLdS;
+  // V[:, p] = a_p / ||a_p|| (fp64)
+  if (tid < L) {
+    double a = 0.0;
+    for (int rr = 0; rr < L; ++rr) a = fma((double)Af[tid * kLdS + rr], (double)Af[tid * kLdS + rr], a);
+    nrm[tid] = a > 0.0 ? rsqrt(a) : 0.0;
+  }
+  __syncthreads();
+  for (int e = tid; e < L * L; e += 256) {
+    const int rr = e / L, c = e % L;
+    V[rr][c] = (double)Af[c * kLdS + rr] * nrm[c];
+  }
+  __syncthreads();
+  // Newton-Schulz: V <- V (3I - V^T V) / 2, three times
+  for (int it = 0; it < 3; ++it) {
+    gemm_small(Wm, V, true, V, false, L);  // W = V^T V
+    __syncthreads();
+    for (int e = tid; e < L * L; e += 256) {
+      const int i = e / L, jj = e % L;
+      Wm[i][jj] = (i == jj ? 1.5 : 0.0) - 0.5 * Wm[i][jj];
+    }
+    __syncthreads();
+    // V <- V W  (via A64 region as scratch)
+    double(*Tm)[kLdM] = reinterpret_cast<double(*)[kLdM]>(A64);
+    gemm_small(Tm, V, false, Wm, false, L);
+    __syncthreads();
+    for (int e = tid; e < L * L; e += 256) V[e / L][e % L] = Tm[e / L][e % L];
+    __syncthreads();
+  }
+  // G' = V^T G V into the fp64 slot buffer 0 (column c of G' at slot c)
+  gemm_small(Wm, Gs, false, V, false, L);  // W = G V
+  __syncthreads();
+  {
+    double(*Tm)[kLdM] = reinterpret_cast<double(*)[kLdM]>(Gs);  // reuse Gs for G'
+    gemm_small(Tm, V, true, Wm, false, L);
+    __syncthreads();
+    for (int e = tid; e < L * L; e += 256) {
+      const int c = e / L, rr = e % L;
+      A64[c * kLdS + rr] = Tm[rr][c];
+    }
+  }
+  __syncthreads();
+  const int r2 = jacobi_os<double>(A64, L, np, (double)L * 1.2325951644078309e-32);
+  const double* Ad = A64 + (r2 & 1) * kMaxL * kLdS;
+  if (tid == 0) *sweeps_out = (r1 >> 1) * 100 + (r2 >> 1);
+  if (tid < L) {
+    double a = 0.0;
+    for (int rr = 0; rr < L; ++rr) a = fma(Ad[tid * kLdS + rr], Ad[tid * kLdS + rr], a);
+    nrm[tid] = a;
+  }
+  __syncthreads();
+  if (tid < L) {
+    const double lam = nrm[tid];
+    int rank = 0;
+    for (int b = 0; b < L; ++b) rank += (nrm[b] > lam || (nrm[b] == lam && b < tid)) ? 1 : 0;
+    top[tid] = (rank < r && lam > 0.0) ? 1 : 0;
+  }
+  __syncthreads();
+  // U = V A_top D^-1/2 (columns), P = U U^T
+  for (int e = tid; e < L * L; e += 256) {
+    const int rr = e / L, c = e % L;  // Wm[rr][c] = (V a_c)[rr] / ||a_c|| for top c else 0
+    double acc = 0.0;
+    if (top[c]) {
+      for (int k = 0; k < L; ++k) acc = fma(V[rr][k], Ad[c * kLdS + k], acc);
+      acc *= rsqrt(nrm[c]);
+    }
+    Wm[rr][c] = acc;
+  }
+  __syncthreads();
+  for (int e = tid; e < L * L; e += 256) {
+    const int x = e / L, y = e % L;
+    double acc = 0.0;
+    for (int k = 0; k < L; ++k) acc = fma(Wm[x][k], Wm[y][k], acc);
+    Pout[e] = acc;
+  }
+}
+
+void run_mix(const double* dG, int l, int r, double* dP, int* dsw, const std::vector<double>& Pref, long long* dclk) {
+  const size_t smem = sizeof(double) * (2 * kMaxL * kLdS + 3 * kMaxL * kLdM);
+  cudaFuncSetAttribute(eig_mix, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  eig_mix<<<1, 256, smem>>>(dG, l, r, dP, dsw, dclk);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  const int reps = 20;
+  for (int i = 0; i < reps; ++i) eig_mix<<<1, 256, smem>>>(dG, l, r, dP, dsw, dclk);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  std::vector<double> P(l * l);
+  int sw;
+  cudaMemcpy(P.data(), dP, sizeof(double) * l * l, cudaMemcpyDeviceToHost);
+  cudaMemcpy(&sw, dsw, sizeof(int), cudaMemcpyDeviceToHost);
+  double err = 0;
+  for (int i = 0; i < l * l; ++i) err = fmax(err, fabs(P[i] - Pref[i]));
+  printf("mixed fp32/fp64: %.1f us  sweeps fp32 %d fp64 %d  max|P-Pref| %.3e  (%s, smem %zu)\n", 1000.0 * ms / reps,
+         sw / 100, sw % 100, err, cudaGetErrorString(cudaGetLastError()), smem);
+}
+
 int main(int argc, char** argv) {
   const char* path = argc > 1 ? argv[1] : "tools/eig_case_c8.bin";
   FILE* f = fopen(path, "rb");
@@ -798,5 +993,6 @@ int main(int argc, char** argv) {
   printf("l %d r %d\n", l, r);
   run_osT<8, 256>(dG, l, r, dP, dsw, Pref, dclk);
   run_oss(dG, l, r, dP, dsw, Pref, dclk);
+  run_mix(dG, l, r, dP, dsw, Pref, dclk);
   return 0;
 }
