@@ -143,8 +143,24 @@ def _spec_for(prob, method):
     raise SystemExit(f"unknown method {method}")
 
 
-def run_cpu_baseline(prob, spec, budget_s=25.0):
-    """The oracle as it stands (single thread), first iterations of the same workload."""
+def _host_cpu():
+    """CPU model and usable core count of the host the line was measured on."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(),
+            "affinity": len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else None}
+
+
+def run_cpu_baseline(prob, spec, budget_s=40.0, min_its=5):
+    """The oracle as it stands (single thread), first iterations of the same workload: at least
+    min_its iterations beyond the first (more when they fit the budget)."""
     from threadpoolctl import threadpool_limits
     from oracle.operators import operator_from_problem
     from oracle.sflsqr import solve_problem
@@ -156,15 +172,17 @@ def run_cpu_baseline(prob, spec, budget_s=25.0):
         t0 = time.perf_counter()
         solve_problem(prob, spec, op=op, maxit=1, record=False)
         t1 = time.perf_counter() - t0
-        k = int(max(2, min(spec.maxit, budget_s // max(t1, 1e-6)))) if t1 * 2 < budget_s else 1
+        k = int(max(min_its + 1, min(spec.maxit, budget_s // max(t1, 1e-6))))
         t0 = time.perf_counter()
         solve_problem(prob, spec, op=op, maxit=k, record=False)
         tk = time.perf_counter() - t0
     per_it = max((tk - t1) / max(k - 1, 1), 1e-9) if k > 1 else t1
-    return {"value": 1.0 / per_it, "unit": UNIT, "cores": 1, "kind": "oracle",
+    return {"value": 1.0 / per_it, "unit": UNIT, "cores": 1, "kind": "oracle", "host": _host_cpu(),
+            "iterations": k - 1,
             "sample": (f"oracle (NumPy + plain C CSR, 1 thread) on the full {prob.name} problem: solve with "
-                       f"maxit={k} minus maxit=1, per iteration (init + per-iteration cost separated); "
-                       f"{per_it:.3g} s/iteration, init+1st iteration {t1:.3g} s, operator setup {t_op:.3g} s")}
+                       f"maxit={k} minus maxit=1, i.e. iterations 2..{k} ({k - 1} iterations; init + first "
+                       f"iteration separated); {per_it:.3g} s/iteration, init+1st iteration {t1:.3g} s, "
+                       f"operator setup {t_op:.3g} s")}
 
 
 def bench_reference(args, prob, spec, world, rank):
@@ -194,7 +212,7 @@ def bench_reference(args, prob, spec, world, rank):
                        "nnz_T": prob.T.nnz if prob.T is not None else (prob.A.nnz if prob.A is not None else None),
                        "ell": spec.window, "d": spec.d,
                        "s": spec.s_nz, "tau": spec.precond},
-            "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "host": _host_cpu(),
                              "sample": f"{k} oracle iterations after init+1 (time budget {budget:.0f} s)"},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -214,6 +232,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-profile", action="store_true", help="graph replay without per-kernel events")
     ap.add_argument("--N", type=int, default=None, help="override grid size (debug)")
+    ap.add_argument("--no-windows", action="store_true", help="skip the late-window and full-solve timings")
     args = ap.parse_args()
 
     world, rank, local = _dist()
@@ -297,10 +316,12 @@ def main():
         nnz_T = prob.T.nnz if prob.T is not None else nnz_A
         parallelism = "replicas" if world > 1 else "single"
     stream = torch.cuda.current_stream()
-    def timed_region(profiled):
+
+    def timed_region(profiled, W=W, K=K):
         """W untimed iterations, then exactly K timed ones between barrier + synchronize."""
         s.set_rhs(b_host)                              # (re)start the solve
         s.iterate(W)                                   # untimed warm-up
+        b_w = s.get_info()["bytes_model"]              # SURVEY.md §8(d) bytes of iteration W
         s.set_profiling(profiled)
         s.reset_profile()
         l0 = s.get_info()["launches"]
@@ -316,33 +337,65 @@ def main():
         t_ms = _max_over_ranks(e0.elapsed_time(e1), world)
         pr = s.get_profile()
         s.set_profiling(False)
-        return t_ms, s.get_info()["launches"] - l0, pr, ck, dn, stt
+        inf = s.get_info()
+        if inf["k_done"] != W + K:
+            # a stop inside the window would leave launches that return early: refuse the number
+            raise SystemExit(f"bench: the solve stopped at k = {inf['k_done']} inside the timed window "
+                             f"{W + 1}..{W + K} (status {inf['status']})")
+        # §8(d) bytes are affine in k: the sum over k = W+1..W+K from iterations W and W+K
+        b_k = inf["bytes_model"]
+        s8d = K * (b_w + (b_k - b_w) / K + b_k) / 2.0 if W >= 1 else K * b_k
+        return dict(ms=t_ms, launches=inf["launches"] - l0, prof=pr, clk=ck, done=dn, status=stt, s8d_bytes=s8d,
+                    rank_flag=inf["rank_flag"])
 
     # (1) production timing: one CUDA graph per iteration (single rank) / eager with NCCL (sharded)
-    ms, launches, _, clk, done, status = timed_region(False)
+    R1 = timed_region(False)
+    ms, launches, clk, done, status = R1["ms"], R1["launches"], R1["clk"], R1["done"], R1["status"]
     # (2) the same K iterations again with CUDA events around every launch (per-kernel times)
-    ms_prof, _, prof, clk2, _, _ = (timed_region(True) if not args.no_profile else (None, None, {}, None, None, None))
+    R2 = timed_region(True) if not args.no_profile else None
+    ms_prof, prof, clk2 = (R2["ms"], R2["prof"], R2["clk"]) if R2 else (None, {}, None)
+    # (3) costs that grow with k (x reconstruction, W-path residual): the last 20 iterations of the
+    #     maxit solve, and the whole solve averaged (iterations 1..maxit), same launch mode as (1)
+    windows = {}
+    if not args.no_windows and maxit > 20:
+        RL = timed_region(False, W=maxit - 20, K=20)
+        RF = timed_region(False, W=1, K=maxit - 1)
+        for nm, R, lo, hi in (("late", RL, maxit - 19, maxit), ("full_solve", RF, 2, maxit)):
+            kk = hi - lo + 1
+            windows[nm] = {"iterations": f"{lo}..{hi}", "value": (kk if sharded else kk * world) / (R["ms"] / 1e3),
+                           "ms_per_step": R["ms"] / kk, "step_gbs_s8d": R["s8d_bytes"] / (R["ms"] / 1e3) / 1e9,
+                           "clocks": R["clk"].summary()}
     info_end = s.get_info()
     k_done = info_end["k_done"]
     # sharded: the ranks cooperate on one solve (iterations/s of the job); replicas: independent solves
     value = (K if sharded else K * world) / (ms / 1e3)
 
-    # roofline of the dominant kernel (HBM-bound CSR SpMV)
+    # roofline of the dominant kernel (HBM-bound SpMV), on two byte bases:
+    #   s8d:    SURVEY.md §8(d)'s per-unit figure, 12 B per stored nonzero of the CSR operator + int64 row
+    #           pointers + one read of the gathered vector + one write of the product (the contract's basis)
+    #   format: the bytes of the storage format the product actually runs on (pair formats are smaller)
     peak, peak_src = _peaks()
     roof = None
     kernels = {}
+    inf = s.get_info()
     for nm, d in prof.items():
         if d["launches"]:
             kernels[nm] = {"ms_total": d["ms"], "launches": d["launches"],
                            "ms_per_launch": d["ms"] / d["launches"],
                            "algo_gbs": d["bytes"] / (d["ms"] / 1e3) / 1e9 if d["ms"] > 0 else None,
                            "share": d["ms"] / ms_prof}
+    s8d_per_launch = {}
+    if inf["nnz_a"]:
+        s8d_per_launch["spmv_A"] = 12.0 * inf["nnz_a"] + 8.0 * (inf["m_loc"] + 1) + 8.0 * inf["n"] + 8.0 * inf["m_loc"]
+        s8d_per_launch["spmv_T"] = 12.0 * inf["nnz_t"] + 8.0 * (inf["n_loc"] + 1) + 8.0 * inf["m"] + 8.0 * inf["n_loc"]
     if kernels:
         dom = max(kernels, key=lambda k2: kernels[k2]["ms_total"])
         d = prof[dom]
+        t_launch = d["ms"] / d["launches"] / 1e3
         bpl = d["bytes"] / d["launches"]
-        ach = bpl / (d["ms"] / d["launches"] / 1e3) / 1e9
-        inf = s.get_info()
+        ach_fmt = bpl / t_launch / 1e9
+        b8 = s8d_per_launch.get(dom, bpl)
+        ach = b8 / t_launch / 1e9
         fnames = dict(enumerate(FMT_NAMES))
         fmt = {"spmv_A": fnames[inf["a_fmt"]], "spmv_T": fnames[inf["t_fmt"]]}
         tkey = dom + {"CSR": "", "pair-CSR": "_pcsr", "aligned pair-CSR": "_apcsr",
@@ -352,19 +405,31 @@ def main():
         l1 = _traffic(prob.name, tkey + "_l1_wavefronts_pct")
         kname = {"spmv_A": f"k_spmv_csr_pf, {fmt['spmv_A']} (A z)",
                  "spmv_T": f"k_spmv_csr_pf, {fmt['spmv_T']} (T w)"}.get(dom, dom)
-        roof = {"bound": "hbm", "kernel": kname, "achieved": ach, "peak": peak,
-                "bytes_basis": "bytes of the format the product runs on: CSR 12 B/nnz (int32 col + fp64 value), "
-                               "pair-CSR 20 B per adjacent-column pair (interpolation pairs 12 B) + 12 B per "
-                               "singleton, + row pointers and vectors (DESIGN.md §5)",
-                "unit": "GB/s", "frac": ach / peak, "peak_source": peak_src,
-                "algorithmic_bytes_per_launch": bpl, "traffic": tr,
+        roof = {"bound": "hbm", "kernel": kname, "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                "bytes_basis": "SURVEY.md §8(d): 12 B per stored nonzero (int32 col + fp64 value) of the CSR "
+                               "operator + 8 B int64 row pointers + one read of the gathered vector + one write "
+                               "of the product",
+                "algorithmic_bytes_per_launch": b8,
+                "format_bytes_per_launch": bpl, "achieved_format_bytes": ach_fmt, "frac_format_bytes": ach_fmt / peak,
+                "format_bytes_basis": f"bytes of the format the product runs on ({fmt.get(dom, 'CSR')}): CSR 12 B/nnz, "
+                                      "pair-CSR 20 B per adjacent-column pair (interpolation pairs 12 B) + 12 B per "
+                                      "singleton, + row pointers and vectors (DESIGN.md §5)",
+                "peak_source": peak_src, "launch_ms": t_launch * 1e3, "traffic": tr,
+                "traffic_note": "ncu dram__bytes_read.sum + dram__bytes_write.sum of one launch (profiles/)",
                 "l1_wavefronts_pct_of_peak": l1,
-                "note": ("bytes of the format the product runs on (DESIGN.md §5); this product's gathers keep the L1 "
-                         "data pipe at l1_wavefronts_pct_of_peak (ncu), so inside the power-capped loop it follows "
-                         "the SM clock" if (l1 or 0) > 70 else
-                         "bytes of the format the product runs on (DESIGN.md §5); HBM bound")}
-    step_bytes = sum(d["bytes"] for d in prof.values())
-    step_gbs = step_bytes / (ms / 1e3) / 1e9 if step_bytes else None   # algorithmic bytes of the step / production time
+                "note": ("this product's gathers keep the L1 data pipe at l1_wavefronts_pct_of_peak (ncu), so inside "
+                         "the power-capped loop it follows the SM clock" if (l1 or 0) > 70 else "HBM bound")}
+    fmt_step_bytes = sum(d["bytes"] for d in prof.values())
+    # step throughput on both bases, over the production-timed region (1)
+    step = {"s8d_gbs": R1["s8d_bytes"] / (ms / 1e3) / 1e9,
+            "format_gbs": (fmt_step_bytes / (ms / 1e3) / 1e9) if fmt_step_bytes else None}
+    step["s8d_frac_of_peak"] = step["s8d_gbs"] / peak
+    step["s8d_frac_of_8TBs"] = step["s8d_gbs"] / CONTRACT_PEAK_GBS
+    step["format_frac_of_peak"] = step["format_gbs"] / peak if step["format_gbs"] else None
+    step["note"] = ("s8d: SURVEY.md §8(d)'s byte model of the whole step (CSR operators at 12 B/nnz, vectors, "
+                    "x reconstruction, W-path residual) over the production time; it can exceed the copy peak "
+                    "because the products run on lossless smaller formats (format: the bytes those formats and "
+                    "the other kernels actually move, from the per-kernel model of DESIGN.md §5)")
 
     # e2e through the public API: host b -> set_rhs, K iterations, x + histories back to host
     e2e = None
@@ -407,13 +472,16 @@ def main():
                        "per_kernel_timing": "second timed region of K iterations, eager launches with CUDA events "
                                             "on the library stream (ms_per_step_profiled)"},
             "roofline": roof,
-            "step_algorithmic_gbs": step_gbs,
-            "step_frac_of_8TBs": step_gbs / CONTRACT_PEAK_GBS if step_gbs else None,
-            "step_frac_of_peak": step_gbs / peak if step_gbs else None,
+            "step": step,
+            "windows": windows,
             "ms_per_step_profiled": (ms_prof / K) if ms_prof else None,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
             "clocks_profiled_region": clk2.summary() if clk2 else None,
-            "kernels": kernels, "status": {"done": done, "status": status, "k_done": k_done},
+            "kernels": kernels,
+            "status": {"done": done, "status": status, "k_done": k_done, "rank_flag": R1["rank_flag"],
+                       "rank_flag_note": "1: a projected problem had |R_kk| < 1e-14 max|R_jj| (reading R14); the "
+                                         "timed iterations then run on a numerically rank-deficient sketched basis"},
+            "host": _host_cpu(),
             "setup_s": {"generate": t_gen, "upload": t_up},
         }
         print(json.dumps(line), flush=True)

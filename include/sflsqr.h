@@ -122,6 +122,7 @@ extern "C" {
 #define SFLSQR_MEM_HOST 0   /* pointers are host memory (copied)                    */
 #define SFLSQR_MEM_DEVICE 1 /* pointers are device memory                           */
 #define SFLSQR_MEM_BORROW 2 /* OR with SFLSQR_MEM_DEVICE: keep the caller's arrays */
+#define SFLSQR_X_GATHERED 4 /* sflsqr_get_x only: the whole x (length n) on every rank  */
 
 /* opts.history bits */
 #define SFLSQR_HIST_TRUE_RES 1 /* record ||b - A x_k|| every iteration              */
@@ -303,9 +304,12 @@ int sflsqr_set_rhs(sflsqr_t *h, const double *b, int64_t len, int32_t mem_flags)
  * Blocks until the issued work is complete. */
 int sflsqr_iterate(sflsqr_t *h, int32_t k, int32_t *done, int32_t *status);
 
-/* x_{k_x} = Z_{k_x} y_{k_x} (Alg. 1 L504 / Alg. 2) into x (length n; with
- * world > 1 this rank's slice [n0, n0+n_loc)), host or device per mem_flags;
- * caller owns the buffer.  x_0 = 0. */
+/* x_{k_x} = Z_{k_x} y_{k_x} (Alg. 1 L504 / Alg. 2) into x, host or device per
+ * mem_flags; caller owns the buffer.  x_0 = 0.  where: with world > 1, x is this rank's
+ * slice [n0, n0+n_loc) (len = n_loc), or with SFLSQR_X_GATHERED OR'ed into mem_flags the
+ * whole x (len = n), all-gathered over the ranks (a collective: every rank must call it;
+ * identical bits on every rank).  With world = 1 both forms are the whole x.
+ * len mismatch -> SFLSQR_E_DIM. */
 int sflsqr_get_x(sflsqr_t *h, double *x, int64_t len, int32_t mem_flags);
 
 /* Per-iteration histories (host buffers, either may be NULL):

@@ -66,6 +66,7 @@ class OracleResult:
     sketch_cols: np.ndarray = None   # M_k columns (sFLSQR) / [S_TW, S z] (sFLSMR)
     rhs: np.ndarray = None
     rank_ratio: list = field(default_factory=list)
+    method: str = ""                 # bookkeeping: which algorithm produced the run
 
 
 def tau_apply(kind, p_k, x_prev, k, p_exp=1.0, eps_rel=1e-3, fixed=None):
@@ -251,7 +252,7 @@ def solve(op, b, method="sflsqr", maxit=10, window=2, sketch=None, sketch_seed=0
             sketch = SparseSignSketch(sketch_seed, d, s_nz, m if method == "sflsqr" else n)
         S = sketch.apply
     st = init_state(op, b, method, maxit, S)
-    res = OracleResult(x=np.zeros(n), k=0, status=RUNNING, rhs=st.rhs)
+    res = OracleResult(x=np.zeros(n), k=0, status=RUNNING, rhs=st.rhs, method=method)
     k_done = 0
     for k in range(1, maxit + 1):
         out = fgk_step(op, st, k, ell, S, precond, p_exp, eps_rel, fixed_diag, orth_mode)

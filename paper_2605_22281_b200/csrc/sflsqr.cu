@@ -97,6 +97,7 @@ struct sflsqr {
   Comm* comm = nullptr;
   int tkind = T_FULL;
   int64_t m0 = 0, m_loc = 0, n0 = 0, n_loc = 0, m_max = 0, n_max = 0;
+  std::vector<int64_t> nst;  // n-partition: rank g owns [nst[g], nst[g+1]) (world + 1 entries)
   // operator (this rank's shard)
   bool op_set = false, blur = false;
   int64_t m = 0, n = 0, nnz_a = 0, nnz_t = 0;
@@ -1933,6 +1934,7 @@ int sflsqr_set_operator_shard(sflsqr_t* h, int64_t m, int64_t n, int64_t a_row0,
   h->m_loc = mst[h->rank + 1] - mst[h->rank];
   h->n0 = nst[h->rank];
   h->n_loc = nst[h->rank + 1] - nst[h->rank];
+  h->nst = nst;
   h->m_max = h->n_max = 0;
   for (int g = 0; g < R; ++g) {
     h->m_max = std::max(h->m_max, mst[g + 1] - mst[g]);
@@ -2306,8 +2308,9 @@ int sflsqr_iterate(sflsqr_t* h, int32_t k, int32_t* done, int32_t* status) {
 int sflsqr_get_x(sflsqr_t* h, double* x, int64_t len, int32_t mem_flags) {
   int rc;
   if ((rc = ensure_ready(h, true))) return rc;
+  const bool gathered = (mem_flags & SFLSQR_X_GATHERED) != 0 && h->world > 1;
   if (!x && len) return fail(h, SFLSQR_E_INVALID, "NULL x");
-  if (len != h->n_loc) return fail(h, SFLSQR_E_DIM, "len(x) != local n");
+  if (len != (gathered ? h->n : h->n_loc)) return fail(h, SFLSQR_E_DIM, gathered ? "len(x) != n" : "len(x) != local n");
   cudaSetDevice(h->o.device);
   if (h->P.method < SFLSQR_METHOD_LSQR) {  // x_k = Z_k y_k; GKB methods update x in place
     Launch L(h, SFLSQR_KC_XUPD, 8.0 * h->n_loc);
@@ -2315,10 +2318,38 @@ int sflsqr_get_x(sflsqr_t* h, double* x, int64_t len, int32_t mem_flags) {
   }
   if ((rc = check_launch(h))) return rc;
   const bool dev = (mem_flags & SFLSQR_MEM_DEVICE) != 0;
-  if (len)
-    CU(h, cudaMemcpyAsync(x, h->P.x, sizeof(double) * len, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
-                          h->stream));
-  CU(h, cudaStreamSynchronize(h->stream));
+  const cudaMemcpyKind kind = dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  if (gathered) {
+    // all-gather of the n-slices (padded to n_max per rank), then each rank's slice to its place
+    const int R = h->world;
+    double *send = nullptr, *all = nullptr;
+    if ((rc = dalloc(h, (void**)&send, sizeof(double) * h->n_max, nullptr))) return rc;
+    if ((rc = dalloc(h, (void**)&all, sizeof(double) * R * h->n_max, nullptr))) {
+      cudaFree(send);
+      return rc;
+    }
+    std::string e;
+    rc = SFLSQR_OK;
+    if (cudaMemsetAsync(send, 0, sizeof(double) * h->n_max, h->stream) != cudaSuccess ||
+        (h->n_loc && cudaMemcpyAsync(send, h->P.x, sizeof(double) * h->n_loc, cudaMemcpyDeviceToDevice,
+                                     h->stream) != cudaSuccess))
+      rc = fail(h, SFLSQR_E_CUDA, "get_x: staging copy failed");
+    else if (h->comm->allgather(send, all, h->n_max, h->stream, e))
+      rc = fail(h, SFLSQR_E_CUDA, "allgather(x): %s", e.c_str());
+    for (int g = 0; g < R && rc == SFLSQR_OK; ++g) {
+      const int64_t len_g = h->nst[g + 1] - h->nst[g];
+      if (len_g && cudaMemcpyAsync(x + h->nst[g], all + (int64_t)g * h->n_max, sizeof(double) * len_g, kind,
+                                   h->stream) != cudaSuccess)
+        rc = fail(h, SFLSQR_E_CUDA, "get_x: gather copy failed");
+    }
+    cudaStreamSynchronize(h->stream);
+    cudaFree(send);
+    cudaFree(all);
+    if (rc) return rc;
+  } else {
+    if (len) CU(h, cudaMemcpyAsync(x, h->P.x, sizeof(double) * len, kind, h->stream));
+    CU(h, cudaStreamSynchronize(h->stream));
+  }
   if (h->prof_on) prof_collect(h);
   return SFLSQR_OK;
 }

@@ -30,6 +30,7 @@ RUNNING, MAXIT, TOL, DISCREPANCY, BREAKDOWN = 0, 1, 2, 3, 4
 PRECOND_IDENTITY, PRECOND_IRN, PRECOND_NONNEG, PRECOND_LOWRANK_RND = 0, 1, 2, 3
 T_BUILD, T_GIVEN = 0, 1
 MEM_HOST, MEM_DEVICE, MEM_BORROW = 0, 1, 2
+X_GATHERED = 4          # sflsqr_get_x: the whole x, all-gathered over the ranks
 HIST_TRUE_RES = 1
 KC_NAMES = ["spmv_A", "spmv_T", "orth", "tau", "sketch", "ls", "xupd", "res", "stop"]
 
@@ -241,6 +242,7 @@ class SFLSQR:
         inf = self.get_info()
         self.m_glob, self.n_glob = int(m), int(n)
         self.m, self.n = inf["m_loc"], inf["n_loc"]
+        self.n_global = inf["n"]
 
     def set_operator_blur(self, H, W, sigma, radius):
         self._check(self.lib.sflsqr_set_operator_blur(self.h, int(H), int(W), float(sigma), int(radius)))
@@ -275,11 +277,15 @@ class SFLSQR:
         self._check(self.lib.sflsqr_iterate(self.h, int(k), ctypes.byref(done), ctypes.byref(status)))
         return bool(done.value), int(status.value)
 
-    def get_x(self, out=None):
+    def get_x(self, out=None, gathered=False):
+        """This rank's slice of x_k (the whole x on one rank); gathered=True: the whole x on every
+        rank (a collective over the group)."""
+        n = getattr(self, "n_global", self.n) if gathered else self.n
         if out is None:
-            out = np.empty(self.n)
+            out = np.empty(n)
         p, dev, _ = _ptr(out)
-        self._check(self.lib.sflsqr_get_x(self.h, p, int(self.n), MEM_DEVICE if dev else MEM_HOST))
+        flags = (MEM_DEVICE if dev else MEM_HOST) | (X_GATHERED if gathered else 0)
+        self._check(self.lib.sflsqr_get_x(self.h, p, int(n), flags))
         return out
 
     def get_residual_norms(self):

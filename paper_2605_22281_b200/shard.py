@@ -81,9 +81,10 @@ def run_local_group(prob, spec, world: int, maxit=None, device=0, eta=None, hist
             done, status = s.iterate(mx)
             tr, sk = s.get_residual_norms()
             x = s.get_x()
+            xg = s.get_x(gathered=True)
             info = s.get_info()
             s.close()
-            out[r] = (x, tr, sk, info, done, status)
+            out[r] = (x, tr, sk, info, done, status, xg)
         except Exception as exc:  # surfaced to the caller below
             err[r] = exc
 

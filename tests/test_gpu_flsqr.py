@@ -15,6 +15,8 @@ from gen.problems import SolverSpec
 from oracle.operators import operator_from_problem
 from oracle.sflsqr import solve_problem
 
+from horizons import horizon
+
 pytestmark = pytest.mark.gpu
 
 RES_TOL = 1e-9
@@ -44,21 +46,6 @@ def _gpu_run(prob, spec, maxit, method, eta=0.0, orth_kernel="auto", use_graph=T
     return dict(done=done, status=status, true_res=tr, proj_res=pr, x=x, info=info, basis=basis)
 
 
-def _stable_horizon(p, spec, maxit, method, thresh=1e-11):
-    """Last k up to which the oracle itself is forward-stable (reading R17)."""
-    op = operator_from_problem(p)
-    r0 = solve_problem(p, spec, op=op, maxit=maxit, eta=0.0, method=method)
-    b0 = p.b
-    p.b = b0 * (1 + 1e-15 * np.random.default_rng(0).standard_normal(b0.size))
-    try:
-        r1 = solve_problem(p, spec, op=op, maxit=maxit, eta=0.0, method=method)
-    finally:
-        p.b = b0
-    dev = np.abs(np.array(r1.true_res) - np.array(r0.true_res)) / np.array(r0.true_res)
-    bad = np.flatnonzero(dev > thresh)
-    return (int(bad[0]) if bad.size else len(dev)), r0
-
-
 def _compare(g, r, n_res):
     kk = len(r.true_res)
     assert g["info"]["k_done"] == kk and g["status"] == r.status and g["info"]["k_x"] == r.k
@@ -76,8 +63,7 @@ def _compare(g, r, n_res):
 def test_config1_flsqr_flsmr(method):
     p = make_problem(1)
     spec = p.solvers[0]                               # IRN-l1, 40 iterations
-    kstar, r = _stable_horizon(p, spec, 40, method)
-    assert kstar >= 20, kstar
+    kstar, r = horizon(f"flsqr/c1/{method}", p)
     g = _gpu_run(p, spec, 40, method)
     r40 = r
     # strict bar up to the oracle's stable horizon; identical status and stop index at 40
@@ -91,8 +77,7 @@ def test_config1_flsqr_flsmr(method):
 def test_config3_reduced_flsqr_flsmr(method):
     p = make_problem(3, N=128, n_angles=90, nb=183)   # Siddon, NONNEG tau
     spec = p.solvers[0]
-    kstar, _ = _stable_horizon(p, spec, 60, method)
-    assert kstar >= 15, kstar
+    kstar, _ = horizon(f"flsqr/c3r128/{method}", p)
     r = solve_problem(p, spec, maxit=kstar, eta=0.0, method=method)
     g = _gpu_run(p, spec, kstar, method)
     _compare(g, r, kstar)
@@ -105,8 +90,7 @@ def test_config3_reduced_flsqr_flsmr(method):
 def test_config4_reduced_unmatched(method):
     p = make_problem(4, N=160, n_angles=113, nb=227)  # unmatched B, identity tau
     spec = p.solvers[0]
-    kstar, _ = _stable_horizon(p, spec, 50, method)
-    assert kstar >= 10, kstar
+    kstar, _ = horizon(f"flsqr/c4r160/{method}", p)
     r = solve_problem(p, spec, maxit=kstar, eta=0.0, method=method)
     g = _gpu_run(p, spec, kstar, method)
     _compare(g, r, kstar)
@@ -116,8 +100,7 @@ def test_config4_reduced_unmatched(method):
 def test_config2_blur(method):
     p = make_problem(2)
     spec = p.solvers[0]
-    kstar, _ = _stable_horizon(p, spec, 40, method)
-    assert kstar >= 15, kstar
+    kstar, _ = horizon(f"flsqr/c2/{method}", p)
     r = solve_problem(p, spec, maxit=kstar, eta=0.0, method=method)
     g = _gpu_run(p, spec, kstar, method)
     _compare(g, r, kstar)

@@ -16,6 +16,8 @@ from oracle.operators import operator_from_problem
 from oracle.sflsqr import solve_problem
 from oracle.sketch import gaussian_table
 
+from horizons import horizon
+
 pytestmark = pytest.mark.gpu
 
 RES_TOL = 1e-9
@@ -57,27 +59,12 @@ def _gpu_run(prob, spec, maxit):
     return dict(status=status, true_res=tr, sketch_res=sk, x=x, info=info)
 
 
-def _horizon(p, spec, maxit, thresh=1e-11):
-    op = operator_from_problem(p)
-    r0 = solve_problem(p, spec, op=op, maxit=maxit, eta=0.0)
-    b0 = p.b
-    p.b = b0 * (1 + 1e-15 * np.random.default_rng(0).standard_normal(b0.size))
-    try:
-        r1 = solve_problem(p, spec, op=op, maxit=maxit, eta=0.0)
-    finally:
-        p.b = b0
-    dev = np.abs(np.array(r1.true_res) - np.array(r0.true_res)) / np.array(r0.true_res)
-    bad = np.flatnonzero(dev > thresh)
-    return int(bad[0]) if bad.size else len(dev)
-
-
 @pytest.mark.parametrize("cfg", [6, 7])
 @pytest.mark.parametrize("method", ["sflsqr", "sflsmr"])
 def test_decay_family(cfg, method):
     p = make_problem(cfg)
     spec = [s for s in p.solvers if s.method == method][0]
-    kstar = _horizon(p, spec, spec.maxit)
-    assert kstar >= 15, kstar
+    kstar, _ = horizon(f"gauss/c{cfg}/{method}", p)
     r = solve_problem(p, spec, maxit=kstar, eta=0.0)
     g = _gpu_run(p, spec, kstar)
     assert g["info"]["k_done"] == len(r.true_res) and g["status"] == r.status
@@ -91,8 +78,7 @@ def test_gaussian_sketch_on_ct():
     import dataclasses
     p = make_problem(3, N=96, n_angles=70, nb=137)
     spec = dataclasses.replace(p.solvers[0], sketch="gaussian", maxit=40, d=81)
-    kstar = _horizon(p, spec, 40)
-    assert kstar >= 15, kstar
+    kstar, _ = horizon("gauss/ct", p)
     r = solve_problem(p, spec, maxit=kstar, eta=0.0)
     g = _gpu_run(p, spec, kstar)
     rt = np.abs(g["true_res"] - np.array(r.true_res)) / np.array(r.true_res)

@@ -14,6 +14,8 @@ from gen import make_problem
 from oracle.operators import operator_from_problem
 from oracle.sflsqr import solve_problem
 
+from horizons import horizon
+
 pytestmark = pytest.mark.gpu
 
 RES_TOL = 1e-9
@@ -43,36 +45,6 @@ def _gpu_run(prob, spec, maxit, method, eta=0.0, use_graph=True, spmv_mode=None)
     return dict(done=done, status=status, res=res, nres=nres, x=x, info=info)
 
 
-class _Noisy:
-    """The oracle's operator with a rounding-level relative perturbation (2^-53 scale, fresh every
-    product) of each result: models the different summation order of another implementation."""
-
-    def __init__(self, op, seed=0):
-        self.op, self.m, self.n = op, op.m, op.n
-        self.rng = np.random.default_rng(seed)
-
-    def matvec(self, v):
-        y = self.op.matvec(v)
-        return y * (1 + 2.0 ** -53 * self.rng.standard_normal(y.size))
-
-    def tmatvec(self, w):
-        y = self.op.tmatvec(w)
-        return y * (1 + 2.0 ** -53 * self.rng.standard_normal(y.size))
-
-
-def _horizon(p, spec, maxit, method, thresh=1e-11):
-    """Last k up to which the oracle is forward-stable under rounding-level perturbations of
-    every product (short recurrences amplify them once orthogonality is lost, reading R17)."""
-    op = operator_from_problem(p)
-    r0 = solve_problem(p, spec, op=op, maxit=maxit, eta=0.0, method=method)
-    r1 = solve_problem(p, spec, op=_Noisy(op), maxit=maxit, eta=0.0, method=method)
-    dev = np.abs(np.array(r1.est_res) - np.array(r0.est_res)) / np.array(r0.est_res)
-    if method == "lsmr":                                   # ||T r|| is the more sensitive history
-        dev = np.maximum(dev, np.abs(np.array(r1.est_nres) - np.array(r0.est_nres)) / np.array(r0.est_nres))
-    bad = np.flatnonzero(dev > thresh)
-    return int(bad[0]) if bad.size else len(dev)
-
-
 def _compare(g, r, method):
     kk = len(r.est_res)
     assert g["info"]["k_done"] == kk and g["status"] == r.status and g["info"]["k_x"] == r.k
@@ -90,17 +62,16 @@ def _compare(g, r, method):
 
 
 @pytest.mark.parametrize("method", ["lsqr", "lsmr"])
-@pytest.mark.parametrize("cfg,kw,maxit", [
-    (1, {}, 40),                                          # dense, sigma_min 1e-6
-    (2, {}, 60),                                          # matrix-free blur (separate epilogue pass)
-    (3, dict(N=128, n_angles=90, nb=183), 80),            # Siddon, matched A^T
-    (4, dict(N=160, n_angles=113, nb=227), 80),           # unmatched B ("LSQR ignoring A# != A^T")
+@pytest.mark.parametrize("cfg,kw,tag", [
+    (1, {}, "c1"),                                        # dense, sigma_min 1e-6
+    (2, {}, "c2"),                                        # matrix-free blur (separate epilogue pass)
+    (3, dict(N=128, n_angles=90, nb=183), "c3r128"),      # Siddon, matched A^T
+    (4, dict(N=160, n_angles=113, nb=227), "c4r160"),     # unmatched B ("LSQR ignoring A# != A^T")
 ])
-def test_gkb_parity(method, cfg, kw, maxit):
+def test_gkb_parity(method, cfg, kw, tag):
     p = make_problem(cfg, **kw)
     spec = p.solvers[0]
-    kstar = _horizon(p, spec, maxit, method)
-    assert kstar >= 10, kstar
+    kstar, _ = horizon(f"gkb/{tag}/{method}", p)
     r = solve_problem(p, spec, maxit=kstar, eta=0.0, method=method)
     g = _gpu_run(p, spec, kstar, method)
     _compare(g, r, method)

@@ -13,6 +13,8 @@ from oracle.lowrank import rnd_omega, tau_lowrank_rnd
 from oracle.operators import operator_from_problem
 from oracle.sflsqr import solve_problem
 
+from horizons import horizon
+
 pytestmark = pytest.mark.gpu
 
 RES_TOL = 1e-9
@@ -39,21 +41,6 @@ def _gpu(prob, spec, maxit, method=None):
     return out
 
 
-def _horizon(p, spec, maxit, method=None, thresh=1e-11):
-    op = operator_from_problem(p)
-    kw = {} if method is None else dict(method=method)
-    r0 = solve_problem(p, spec, op=op, maxit=maxit, eta=0.0, **kw)
-    b0 = p.b
-    p.b = b0 * (1 + 1e-15 * np.random.default_rng(0).standard_normal(b0.size))
-    try:
-        r1 = solve_problem(p, spec, op=op, maxit=maxit, eta=0.0, **kw)
-    finally:
-        p.b = b0
-    dev = np.abs(np.array(r1.true_res) - np.array(r0.true_res)) / np.array(r0.true_res)
-    bad = np.flatnonzero(dev > thresh)
-    return int(bad[0]) if bad.size else len(dev)
-
-
 def test_first_basis_vector_is_rnd_truncation():
     p = make_problem(8, N=128)
     spec = p.solvers[0]
@@ -72,9 +59,7 @@ def test_first_basis_vector_is_rnd_truncation():
 def test_deblur_inpaint_rnd(N, method):
     p = make_problem(8, N=N)
     spec = [s for s in p.solvers if s.method == method][0]
-    maxit = 20 if N == 512 else 50
-    kstar = _horizon(p, spec, maxit)
-    assert kstar >= 8, kstar
+    kstar, _ = horizon(f"lowrank/{'c8' if N == 512 else 'c8r128'}/{method}", p)
     r = solve_problem(p, spec, maxit=kstar, eta=0.0)
     g = _gpu(p, spec, kstar)
     rt = np.abs(g["true_res"] - np.array(r.true_res)) / np.array(r.true_res)
@@ -86,8 +71,7 @@ def test_deblur_inpaint_rnd(N, method):
 def test_flsqr_rnd():
     p = make_problem(8, N=128)
     spec = dataclasses.replace(p.solvers[0], maxit=30)
-    kstar = _horizon(p, spec, 30, method="flsqr")
-    assert kstar >= 8, kstar
+    kstar, _ = horizon("lowrank/c8r128/flsqr", p)
     r = solve_problem(p, spec, maxit=kstar, eta=0.0, method="flsqr")
     g = _gpu(p, spec, kstar, method="flsqr")
     rt = np.abs(g["true_res"] - np.array(r.true_res)) / np.array(r.true_res)

@@ -20,6 +20,12 @@ def _lib():
     build_library()
 
 
+def _check_gathered(x, out):
+    # sflsqr_get_x(..., SFLSQR_X_GATHERED): the whole x on every rank, bit for bit the slices' concatenation
+    for o in out:
+        assert np.array_equal(o[6], x)
+
+
 def _check(x, tr, sk, r, n_res, res_tol=1e-9, x_tol=1e-6):
     n = min(n_res, len(r.true_res))
     rt = np.abs(tr[:n] - np.array(r.true_res[:n])) / np.array(r.true_res[:n])
@@ -37,10 +43,34 @@ def test_colshard_config3_reduced(world, method):
     p = make_problem(3, N=128, n_angles=90, nb=183)
     spec = [s for s in p.solvers if s.method == method][0]
     r = solve_problem(p, spec, maxit=60, eta=0.0)
-    x, tr, sk, infos, st, _ = run_local_group(p, spec, world, maxit=60, eta=0.0)
+    x, tr, sk, infos, st, out = run_local_group(p, spec, world, maxit=60, eta=0.0)
     assert all(s == (True, 1) for s in st)
     assert sum(i["m_loc"] for i in infos) == p.m and sum(i["n_loc"] for i in infos) == p.n
     _check(x, tr, sk, r, 60)
+    _check_gathered(x, out)
+
+
+@pytest.fixture(scope="module")
+def c5_reduced():
+    from horizons import C5R
+    return make_problem(5, **C5R)
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("method", ["sflsqr", "sflsmr"])
+def test_colshard_config5_reduced(c5_reduced, world, method):
+    # BASELINE configs[4]'s recipe (Siddon, A^T column-sharded and built per rank, IRN-l1, ell = 5,
+    # d = 600, s = 8) on a 256^2 grid, 40 iterations (inside the oracle's horizon, tests/horizons.py)
+    from paper_2605_22281_b200.shard import run_local_group
+    p = c5_reduced
+    spec = [s for s in p.solvers if s.method == method][0]
+    K = 40
+    r = solve_problem(p, spec, maxit=K, eta=0.0)
+    x, tr, sk, infos, st, out = run_local_group(p, spec, world, maxit=K, eta=0.0)
+    assert all(s == (True, 1) for s in st)
+    assert [i["n0"] for i in infos] == sorted(i["n0"] for i in infos)
+    _check(x, tr, sk, r, K)
+    _check_gathered(x, out)
 
 
 @pytest.mark.parametrize("world", [2, 4])
@@ -50,8 +80,9 @@ def test_rowshard_config4_reduced(world):
     spec = p.solvers[0]
     K = 12   # inside the oracle's forward-stable horizon for this unmatched problem (test_gpu_parity)
     r = solve_problem(p, spec, maxit=K, eta=0.0)
-    x, tr, sk, infos, st, _ = run_local_group(p, spec, world, maxit=K, eta=0.0)
+    x, tr, sk, infos, st, out = run_local_group(p, spec, world, maxit=K, eta=0.0)
     _check(x, tr, sk, r, K)
+    _check_gathered(x, out)
 
 
 def test_dense_config1_world2_discrepancy_stop():
