@@ -53,7 +53,7 @@
 extern "C" {
 #endif
 
-#define SFLSQR_ABI_VERSION 4
+#define SFLSQR_ABI_VERSION 5
 
 /* return codes */
 #define SFLSQR_OK 0
@@ -124,6 +124,26 @@ extern "C" {
 #define SFLSQR_MEM_BORROW 2 /* OR with SFLSQR_MEM_DEVICE: keep the caller's arrays */
 #define SFLSQR_X_GATHERED 4 /* sflsqr_get_x only: the whole x (length n) on every rank  */
 
+/* opts.knobs: scheduling and storage-format switches.  None changes the method's arithmetic
+ * except the summation order of a product (a format) or of CGS2's second pass; 0 selects the
+ * measured defaults.  Unknown bits -> SFLSQR_E_INVALID at create. */
+#define SFLSQR_KNOB_NO_PDL 0x1          /* plain launches (no programmatic dependent launch)          */
+#define SFLSQR_KNOB_SKETCH_MAIN 0x2     /* the per-step sketch on the main stream (not beside the dots) */
+#define SFLSQR_KNOB_NO_INTERP 0x4       /* keep full pair values even for (1 - f, f) interpolation pairs */
+#define SFLSQR_KNOB_NO_SELL 0x8         /* no sliced-ELL copy of interpolation pairs                  */
+#define SFLSQR_KNOB_CGS_ALWAYS2 0x10    /* CGS2: always the second pass (not Kahan's criterion)       */
+#define SFLSQR_KNOB_FULL_SPMV_GRID 0x20 /* product grids fill every SM slot (default: one CTA short)   */
+#define SFLSQR_KNOB_RES_MAIN 0x40       /* W-path residual on the main stream                         */
+#define SFLSQR_KNOB_RES_SIDE 0x80       /* W-path residual on the side stream (default: by size)       */
+#define SFLSQR_KNOB_P2P_ON 0x100        /* peer-memory collectives (default: in-process group only)    */
+#define SFLSQR_KNOB_P2P_OFF 0x200       /* collective calls only                                      */
+#define SFLSQR_KNOB_KEEP_CSR 0x400      /* keep the uploaded CSR after its format copy is built (needed
+                                            by sflsqr_debug_set_tuning's forced formats); default: freed */
+#define SFLSQR_KNOB_DEBUG_POISON 0x800 /* fill every solve buffer with NaN bytes at allocation
+                                            (a read before write then shows in the results)   */
+#define SFLSQR_KNOB_NO_ELL_C16 0x1000 /* 32-bit columns in the sliced-ELL interpolation pairs   */
+#define SFLSQR_KNOB_ALL 0x1fff
+
 /* opts.history bits */
 #define SFLSQR_HIST_TRUE_RES 1 /* record ||b - A x_k|| every iteration              */
 
@@ -151,7 +171,8 @@ typedef struct sflsqr_opts {
   const uint8_t *nccl_id; /* SFLSQR_COMM_NCCL: the 128-byte id of sflsqr_get_unique_id */
   void *local_group;      /* SFLSQR_COMM_LOCAL: sflsqr_local_group_create()          */
   int32_t orth_kernel;    /* SFLSQR_ORTHK_* (0 = auto)                               */
-  int32_t reserved[3];
+  int32_t knobs;          /* SFLSQR_KNOB_* bits; 0 = the measured defaults */
+  int32_t reserved[2];
 } sflsqr_opts;
 
 typedef struct sflsqr_info {
@@ -173,8 +194,9 @@ typedef struct sflsqr_info {
   int32_t a_fmt, t_fmt; /* SpMV format of the A / T products: 0 CSR, 1 pair-CSR (any adjacent
                           pair), 2 aligned pair-CSR (pairs at even columns, 16-byte gathers),
                           3 interpolation pair-CSR (every pair (1 - f, f) bitwise: only f stored),
-                          4 the same pairs as sliced ELL, 32 rows per slice, one row per lane,
-                          5 plain CSR as sliced ELL (opt-in, SFLSQR_SELL_A=1 for A)              */
+                          4 the same pairs as sliced ELL, 32 rows per slice, one row per lane */
+  int32_t knobs;        /* opts.knobs of this handle                                             */
+  int32_t csr_kept;     /* bit 0: A's uploaded CSR is held, bit 1: T's (else released, its copy serves) */
 } sflsqr_info;
 
 /* Per-kernel-class device time, recorded with CUDA events on the library stream
@@ -340,18 +362,15 @@ int sflsqr_debug_basis(sflsqr_t *h, double *H, double *Tm, double *Z, double *W,
  * (sFLSMR), column-major; rhs (d) = s_b or s_{A^T b}. */
 int sflsqr_debug_state(sflsqr_t *h, double *z, double *x, double *p_ring, double *sketch_cols, double *rhs);
 
-/* Tuning knob (performance only; every variant is deterministic and
- * oracle-checked): spmv_mode -1 (default) = per-operator rule on the average
- * row length; 0 = warp-per-row CSR with 128-bit per-lane loads; 1, 2, 3, 10 =
- * row-group CSR (rows per CTA x chunks in flight: 16x4, 8x4, 32x4, 32x2);
- * 8 = 64 half-warp rows per CTA; 11, 12, 13, 14 = software-pipelined row-group
- * CSR (next chunks' indices/values loaded ahead of the gathers; 14 = half-warp
- * rows, 32 rows per 512-thread CTA = the default); 15 = CSR-16 (16-bit column
- * offsets per 16-entry chunk, built on request; falls back to 14 when a chunk
- * spans > 65536 columns); 16 = pair-CSR (every row's runs of consecutive columns
- * stored as (column, two values) pairs plus a singleton CSR: 10 instead of 12
- * bytes per paired nonzero; built on request, on the device).  band_shift is
- * reserved (8..30).  Invalidates a captured graph (rebuilt at the next set_rhs). */
+/* Debug: force the SpMV format of both products (performance only; every format is the same
+ * operator, deterministic and oracle-checked): spmv_mode -1 = the default rule of DESIGN.md §5
+ * (sflsqr_info.a_fmt / t_fmt report it); 14 = plain CSR (half-warp rows, 32 rows per 512-thread
+ * CTA, the next 4 chunks prefetched); 16 = pair-CSR (every row's runs of consecutive columns as
+ * (column, two values) pairs + a singleton CSR, 10 instead of 12 bytes per paired nonzero); 17 =
+ * aligned pair-CSR (pairs at even columns only, one 16-byte gather per pair).  Forcing a format
+ * rebuilds from the uploaded CSR: SFLSQR_E_STATE when it was released (create with
+ * SFLSQR_KNOB_KEEP_CSR).  Other modes -> SFLSQR_E_INVALID; band_shift is ignored.  Invalidates a
+ * captured graph (rebuilt at the next set_rhs). */
 int sflsqr_debug_set_tuning(sflsqr_t *h, int32_t spmv_mode, int32_t band_shift);
 
 /* Profiling: on = 1 launches kernels eagerly (no graph) with CUDA events around

@@ -18,6 +18,7 @@
 #include <vector>
 
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_sort.cuh>
 #include <cuda_runtime.h>
 
 #include "comm.h"
@@ -41,16 +42,19 @@ struct Prof {
 
 enum TKind { T_FULL = 0, T_ROWSHARD = 1, T_COLSHARD = 2 };
 
-// CSR-16 copy of an operator's column indices (k_spmv_c16): per-chunk int32 base,
-// 16-bit offsets, chunk pointer per row.  ok = false: the operator stays int32 CSR.
 struct PCSR {  // pair-CSR copy of an operator (k_pcsr_rows): pairs + singleton CSR
   bool ok = false;
   bool aligned = false;  // pairs only at even columns (gathered as one 16-byte load)
-  double* f = nullptr;   // interpolation pairs: second values only (first = 1 - f bitwise), pval freed
+  bool interp = false;   // interpolation pairs: second values f only (first = 1 - f bitwise), pval freed
+  bool ell = false;      // their sliced-ELL copy serves the product (pair-CSR arrays prp / pcol / f freed)
+  bool c16 = false;      // ... with 16-bit column offsets from a per-slice-entry base (ecol freed)
+  double* f = nullptr;
   // sliced-ELL copy of the interpolation pairs (k_spmv_sell_ip): slice offsets, per-row counts
   int64_t* soff = nullptr;
   int* rcnt = nullptr;
   int* ecol = nullptr;
+  int* ebase = nullptr;      // c16: column base of each slice entry (32 rows), sell_entries / 32 of them
+  uint16_t* eoff = nullptr;  // c16: column - base of every entry
   double* ef = nullptr;
   int64_t sell_entries = 0;
   int64_t npairs = 0, nsingles = 0;
@@ -62,23 +66,6 @@ struct PCSR {  // pair-CSR copy of an operator (k_pcsr_rows): pairs + singleton 
   double* sval = nullptr;
 };
 
-struct SELL {  // sliced-ELL copy of a plain CSR operator (k_spmv_sell_csr)
-  bool ok = false;
-  int64_t entries = 0;
-  int64_t* soff = nullptr;
-  int* rcnt = nullptr;
-  int* ecol = nullptr;
-  double* ev = nullptr;
-};
-
-struct C16 {
-  bool ok = false;
-  int64_t nchunks = 0;
-  int64_t* cptr = nullptr;
-  int* base = nullptr;
-  uint16_t* off = nullptr;
-};
-
 }  // namespace
 
 struct sflsqr {
@@ -88,7 +75,7 @@ struct sflsqr {
   cudaStream_t side = nullptr;  // second stream: the projected LS overlaps the T product (fork/join)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_w = nullptr, ev_sk = nullptr;
   int axpy_wait_sk = -1;  // enqueue_orth(this side): wait for ev_sk (sketch on the side stream) before the in-place update
-  // sFLSQR's sketch of A z on the side stream beside the w-side dots (SFLSQR_SKETCH_SIDE=0: main
+  // sFLSQR's sketch of A z on the side stream beside the w-side dots (SFLSQR_KNOB_SKETCH_MAIN: main
   // stream): config 1 +6 %, config 2 +1 %, config 3 +2 %, config 4 unchanged (same box)
   bool sketch_side = true;
   std::string err;
@@ -109,14 +96,13 @@ struct sflsqr {
   int bH = 0, bW = 0, brad = 0;
   double* taps = nullptr;
   double* blur_tmp = nullptr;
-  C16 ca, ct;           // CSR-16 index copies of A and T (SpMV mode 15, on request)
-  PCSR pa, pt;          // pair-CSR copies of A and T (SpMV mode 16)
-  SELL ea, et;          // sliced-ELL copies of A and T (plain values)
-  int pcsr_unroll = 4;  // pairs in flight per lane in the mode-16 kernel (4 or 2; SFLSQR_PCSR_UNROLL)
-  bool pcsr_interp = true;  // interpolation pairs when every pair qualifies (SFLSQR_PCSR_INTERP=0: off)
-  bool sell = true;         // sliced-ELL (row per lane) copy of interpolation pairs (SFLSQR_SELL=0: off)
-  bool sell_a = false;      // sliced-ELL copy of the forward operator A (SFLSQR_SELL_A=1)
-  bool cgs_selective = true;  // CGS2 second pass only when needed (one rank; SFLSQR_CGS_SELECTIVE=0: always)
+  PCSR pa, pt;          // pair-CSR copies of A and T (the format rule of DESIGN.md §5)
+  bool keep_csr = false;    // keep the uploaded CSR after a format copy is built (SFLSQR_KNOB_KEEP_CSR)
+  bool csr_freed_a = false, csr_freed_t = false;  // the CSR of A / T was released (its copy serves)
+  bool pcsr_interp = true;  // interpolation pairs when every pair qualifies (SFLSQR_KNOB_NO_INTERP: off)
+  bool sell = true;         // sliced-ELL (row per lane) copy of interpolation pairs (SFLSQR_KNOB_NO_SELL: off)
+  bool ell_c16 = true;      // ... with 16-bit column offsets when they fit (SFLSQR_KNOB_NO_ELL_C16: off)
+  bool cgs_selective = true;  // CGS2 second pass only when needed (one rank; SFLSQR_KNOB_CGS_ALWAYS2: always)
   // sketch
   bool sk_set = false;
   int sk_kind = 0;  // 0 sparse-sign (R5/R6), 1 dense Gaussian (R21)
@@ -132,7 +118,7 @@ struct sflsqr {
   Params P;
   int nslots = 0;
   double *zfull = nullptr, *wfull = nullptr, *zpart = nullptr;
-  // peer-memory collectives (SFLSQR_P2P; default on for the in-process group, opt-in for NCCL):
+  // peer-memory collectives (default on for the in-process group, opt-in for NCCL; SFLSQR_KNOB_P2P_*):
   // every rank's zfull / wfull / zrecv addressable from this device
   bool p2p = false;
   double* zrecv = nullptr;
@@ -147,21 +133,18 @@ struct sflsqr {
   int64_t launches = 0;
   int host_k = 1;        // host mirror (profiling byte model only)
   int spmv_mode = -1;    // -1: per-operator rule (select_spmv_mode); else a forced variant (tuning)
-  // CTAs left out of the full SpMV grid (SFLSQR_SPMV_GRID_DELTA).  The products are grid-stride
+  // CTAs left out of the full SpMV grid (1; SFLSQR_KNOB_FULL_SPMV_GRID: 0).  The products are grid-stride
   // kernels sized to exactly fill every SM; when the one-CTA projected LS runs concurrently on the
   // side stream it takes part of one SM, one product CTA then starts only after the LS and its
   // fixed share of rows finishes last.  One CTA fewer keeps every CTA resident from the start:
   // config 4 190 -> 201 it/s (same box), config 3 unchanged.
   int spmv_grid_delta = 1;
-  bool pdl = true;  // programmatic dependent launch of the main-stream kernels (SFLSQR_PDL=0: off)
-  int band_shift = 16;   // reserved
+  bool pdl = true;  // programmatic dependent launch of the main-stream kernels (SFLSQR_KNOB_NO_PDL: off)
+  int32_t knobs = 0;     // opts.knobs as given (reported by sflsqr_get_info)
   bool prof_on = false;
   Prof prof;
-  bool res_overlap = true;  // W-path residual on the side stream (SFLSQR_RES_OVERLAP=0/1 forces; A/B timing)
+  bool res_overlap = true;  // W-path residual on the side stream (SFLSQR_KNOB_RES_MAIN / _RES_SIDE force it)
   bool res_overlap_forced = false;
-  bool lr_qr_cgs = false;   // tau_r range QR: shifted Cholesky QR (default) or one-CTA CGS2 (SFLSQR_LR_QR=cgs)
-  int coop_grid = 0;     // blocks of the cooperative phase kernels (0: not available)
-  bool coop_attr = true; // launch with cudaLaunchAttributeCooperative (cleared if unsupported)
 };
 
 namespace {
@@ -246,58 +229,6 @@ int validate_csr(sflsqr_t* h, const char* name, int64_t nrows, int64_t ncols, co
 // output row entries keep increasing original-row order -> canonical, deterministic).
 // rp may have a nonzero base.  row_map (optional) maps an output row j to its
 // position in a (possibly padded) output of nout rows.
-void host_transpose(int64_t nrows, int64_t ncols, const int64_t* rp, const int32_t* col, const double* val,
-                    int64_t nout, const std::vector<int64_t>* row_map, std::vector<int64_t>& trp,
-                    std::vector<int32_t>& tcol, std::vector<double>& tval) {
-  const int nt = std::min(host_threads(), 16);
-  const int64_t nnz = rp[nrows] - rp[0];
-  std::vector<int64_t> rs(nt + 1);
-  for (int t = 0; t <= nt; ++t) rs[t] = std::min(nrows, (nrows + nt - 1) / nt * t);
-  std::vector<std::vector<int32_t>> cnt(nt, std::vector<int32_t>(ncols, 0));
-  {
-    std::vector<std::thread> th;
-    for (int t = 0; t < nt; ++t)
-      th.emplace_back([&, t]() {
-        auto& c = cnt[t];
-        for (int64_t p = rp[rs[t]]; p < rp[rs[t + 1]]; ++p) c[col[p]]++;
-      });
-    for (auto& x : th) x.join();
-  }
-  auto orow = [&](int64_t j) { return row_map ? (*row_map)[j] : j; };
-  std::vector<int64_t> rowcnt(nout, 0);
-  for (int64_t j = 0; j < ncols; ++j) {
-    int64_t s = 0;
-    for (int t = 0; t < nt; ++t) s += cnt[t][j];
-    rowcnt[orow(j)] = s;
-  }
-  trp.assign(nout + 1, 0);
-  for (int64_t r = 0; r < nout; ++r) trp[r + 1] = trp[r] + rowcnt[r];
-  std::vector<std::vector<int64_t>> off(nt, std::vector<int64_t>(ncols));
-  par_for(ncols, [&](int64_t s, int64_t e) {
-    for (int64_t j = s; j < e; ++j) {
-      int64_t o = trp[orow(j)];
-      for (int t = 0; t < nt; ++t) {
-        off[t][j] = o;
-        o += cnt[t][j];
-      }
-    }
-  });
-  cnt.clear();
-  tcol.resize(nnz);
-  tval.resize(nnz);
-  std::vector<std::thread> th;
-  for (int t = 0; t < nt; ++t)
-    th.emplace_back([&, t]() {
-      auto& o = off[t];
-      for (int64_t i = rs[t]; i < rs[t + 1]; ++i)
-        for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
-          int64_t q = o[col[p]]++;
-          tcol[q] = (int32_t)i;
-          tval[q] = val[p];
-        }
-    });
-  for (auto& x : th) x.join();
-}
 
 void free_solve(sflsqr_t* h) {
   if (h->gexec) {
@@ -321,18 +252,12 @@ void free_solve(sflsqr_t* h) {
   h->rhs_set = false;
 }
 
-void free_sell(SELL& e) {
-  cudaFree(e.soff);
-  cudaFree(e.rcnt);
-  cudaFree(e.ecol);
-  cudaFree(e.ev);
-  e = SELL();
-}
-
 void free_pcsr(PCSR& p) {
   cudaFree(p.soff);
   cudaFree(p.rcnt);
   cudaFree(p.ecol);
+  cudaFree(p.ebase);
+  cudaFree(p.eoff);
   cudaFree(p.ef);
   cudaFree(p.f);
   cudaFree(p.prp);
@@ -357,16 +282,9 @@ void free_op(sflsqr_t* h) {
   }
   cudaFree(h->taps);
   cudaFree(h->blur_tmp);
-  for (C16* c : {&h->ca, &h->ct}) {
-    cudaFree(c->cptr);
-    cudaFree(c->base);
-    cudaFree(c->off);
-    *c = C16();
-  }
   free_pcsr(h->pa);
   free_pcsr(h->pt);
-  free_sell(h->ea);
-  free_sell(h->et);
+  h->csr_freed_a = h->csr_freed_t = false;
   h->a_rowptr = h->t_rowptr = nullptr;
   h->a_col = h->t_col = nullptr;
   h->a_val = h->t_val = h->taps = h->blur_tmp = nullptr;
@@ -444,7 +362,7 @@ int reduce_slots(sflsqr_t* h, int slot0, int ns, bool is_max) {
 
 // Launch with programmatic stream serialization (PDL) when enabled: the kernel may become
 // resident while its predecessor in the stream drains (every kernel launched this way starts with
-// pdl_wait()).  SFLSQR_PDL=0: plain launches.
+// pdl_wait()).  SFLSQR_KNOB_NO_PDL: plain launches.
 template <typename... KArgs, typename... Args>
 void launch_pdl(sflsqr_t* h, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                 Args&&... args) {
@@ -461,22 +379,30 @@ void launch_pdl(sflsqr_t* h, void (*kern)(KArgs...), dim3 grid, dim3 block, size
   cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
-// Plain-CSR SpMV variant (measured on configs 3-4, tools/spmv_tune.py):
-// half-warp rows, 32 adjacent rows per 512-thread CTA, 4 CTAs per SM, the next
-// 4 chunks' indices/values loaded before the current gathers (mode 14).  Fixed,
-// so results are reproducible run to run.  Operators with a pair-CSR or sliced-ELL copy
-// (build_formats, the default rule of DESIGN.md §5) run on that copy instead.
-int select_spmv_mode(int64_t nnz, int64_t nrows) {
-  (void)nnz;
-  (void)nrows;
-  return 14;
-}
-
 bool launch_pairs_epi(sflsqr_t* h, int which, const double* x, int64_t x_ld, double* y, const SpmvEpi& E, int cls,
                       double extra, int grid);
 
+// Bytes of the sliced-ELL interpolation pairs a product streams: per entry the column (4 B, or a 2 B
+// offset + a 4 B base per 32 entries) and f (8 B); the singleton CSR; per-row counts; slice offsets.
+double sell_bytes(const PCSR& pc, int64_t nrows) {
+  const double per = pc.c16 ? 10.0 + 4.0 / kSellC : 12.0;
+  return per * pc.sell_entries + 12.0 * pc.nsingles + 4.0 * nrows + 8.0 * (nrows + 1) +
+         8.0 * ((nrows + kSellC - 1) / kSellC + 1);
+}
+
+// The product runs on the operator's format copy when it has one (pa / pt, built by the rule of
+// DESIGN.md §5 or forced by sflsqr_debug_set_tuning 16 / 17), else on the uploaded CSR
+// (sflsqr_debug_set_tuning 14 forces the CSR, which needs SFLSQR_KNOB_KEEP_CSR once a copy exists).
+bool runs_on_pairs(const sflsqr_t* h, int which) {
+  const PCSR& pc = which == 0 ? h->pa : h->pt;
+  return !h->blur && pc.ok && h->spmv_mode != 14;
+}
+
 // y = A x (which 0) or y = T x (which 1) for this rank's shard; x may be a
 // k-relative column (x_ld != 0).
+// Plain CSR: half-warp rows, 32 adjacent rows per 512-thread CTA, 4 CTAs per SM, the next 4
+// chunks' indices / values loaded before the current gathers (measured on configs 3-4, DESIGN.md
+// §5).  Every format sums each row in a fixed order: results are reproducible run to run.
 void enqueue_apply(sflsqr_t* h, int which, const DevState* st, const double* x, int64_t x_ld, int x_koff, double* y,
                    int cls) {
   const int64_t nrows = which == 0 ? h->m_loc : h->t_rows;
@@ -493,9 +419,6 @@ void enqueue_apply(sflsqr_t* h, int which, const DevState* st, const double* x, 
     }
     return;
   }
-  const int64_t* rp = which == 0 ? h->a_rowptr : h->t_rowptr;
-  const int32_t* col = which == 0 ? h->a_col : h->t_col;
-  const double* val = which == 0 ? h->a_val : h->t_val;
   const int64_t nnz = which == 0 ? h->nnz_a : h->nnz_t;
   const int64_t xlen = which == 0 ? (h->world > 1 ? h->world * h->n_max : h->n)
                                   : (h->tkind == T_ROWSHARD ? h->world * h->m_max : h->m_loc);
@@ -505,145 +428,71 @@ void enqueue_apply(sflsqr_t* h, int which, const DevState* st, const double* x, 
     const int64_t want = (nrows + rows_per_cta - 1) / rows_per_cta;
     return (int)std::max<int64_t>(1, std::min<int64_t>(want, 148 * per_sm - h->spmv_grid_delta));
   };
-  const C16& cc = which == 0 ? h->ca : h->ct;
   const PCSR& pc = which == 0 ? h->pa : h->pt;
-  const SELL& es = which == 0 ? h->ea : h->et;
-  if (h->spmv_mode < 0 && es.ok) {
-    L.bytes_override(12.0 * es.entries + 4.0 * nrows + 8.0 * (nrows / kSellC + 1) + 8.0 * xlen + 8.0 * nrows);
+  if (!runs_on_pairs(h, which)) {
+    const int64_t* rp = which == 0 ? h->a_rowptr : h->t_rowptr;
+    const int32_t* col = which == 0 ? h->a_col : h->t_col;
+    const double* val = which == 0 ? h->a_val : h->t_val;
+    launch_pdl(h, k_spmv_csr_pf<16, 4, 16>, grid_for(32, 4), 512, 0, h->stream, st, nrows, rp, (const int*)col, val, x,
+               x_ld, x_koff, y, SpmvEpi(), PairPart());
+    return;
+  }
+  // pair-CSR: 20 bytes per pair of nonzeros, 12 per singleton, two row pointer arrays
+  L.bytes_override(20.0 * pc.npairs + 12.0 * pc.nsingles + 16.0 * (nrows + 1) + 8.0 * xlen + 8.0 * nrows);
+  PairPart PP;
+  PP.rowptr = pc.prp;
+  PP.col = pc.pcol;
+  PP.val = pc.pval;
+  PP.f = pc.f;
+  if (pc.interp) L.bytes_override(12.0 * pc.npairs + 12.0 * pc.nsingles + 16.0 * (nrows + 1) + 8.0 * xlen + 8.0 * nrows);
+  // aligned pairs gather one 16-byte value pair: needs x (any k-relative column) 16-byte aligned
+  const bool x16 = ((uintptr_t)x % 16 == 0) && (x_ld % 2 == 0);
+  if (pc.ell) {  // sliced-ELL interpolation pairs (pair-CSR arrays released after the build)
+    L.bytes_override(sell_bytes(pc, nrows) + 8.0 * xlen + 8.0 * nrows);
     const int64_t nsl = (nrows + kSellC - 1) / kSellC;
     const int g = (int)std::max<int64_t>(1, std::min<int64_t>((nsl + 15) / 16, 148 * 2 - h->spmv_grid_delta));
-    k_spmv_sell_csr<4><<<g, 512, 0, h->stream>>>(st, nrows, es.soff, es.rcnt, es.ecol, es.ev, x, x_ld, x_koff, y);
-    return;
-  }
-  int mode = h->spmv_mode >= 0 ? h->spmv_mode : (pc.ok ? 16 : select_spmv_mode(nnz, nrows));
-  if (mode == 15 && !cc.ok) mode = 14;
-  if ((mode == 16 || mode == 17) && !pc.ok) mode = 14;
-  if (mode == 16 || mode == 17) {
-    // pair-CSR: 20 bytes per pair of nonzeros, 12 per singleton, two row pointer arrays
-    L.bytes_override(20.0 * pc.npairs + 12.0 * pc.nsingles + 16.0 * (nrows + 1) + 8.0 * xlen + 8.0 * nrows);
-    PairPart PP;
-    PP.rowptr = pc.prp;
-    PP.col = pc.pcol;
-    PP.val = pc.pval;
-    PP.f = pc.f;
-    if (pc.f) L.bytes_override(12.0 * pc.npairs + 12.0 * pc.nsingles + 16.0 * (nrows + 1) + 8.0 * xlen + 8.0 * nrows);
-    // aligned pairs gather one 16-byte value pair: needs x (any k-relative column) 16-byte aligned
-    const bool x16 = ((uintptr_t)x % 16 == 0) && (x_ld % 2 == 0);
-    if (pc.f && pc.ecol) {
-      L.bytes_override(12.0 * pc.sell_entries + 12.0 * pc.nsingles + 4.0 * nrows + 16.0 * (nrows + 1) + 8.0 * xlen +
-                       8.0 * nrows);
-      const int64_t nsl = (nrows + kSellC - 1) / kSellC;
-      const int g = (int)std::max<int64_t>(1, std::min<int64_t>((nsl + 15) / 16, 148 * 2 - h->spmv_grid_delta));
-      launch_pdl(h, k_spmv_sell_ip<4, false>, g, 512, 0, h->stream, st, nrows, (const int64_t*)pc.soff,
-                 (const int*)pc.rcnt, (const int*)pc.ecol, (const double*)pc.ef, (const int64_t*)pc.srp,
-                 (const int*)pc.scol, (const double*)pc.sval, x, x_ld, x_koff, y, SpmvEpi());
-    } else if (pc.f)
-      k_spmv_csr_pf<16, 4, 16, false, 6><<<grid_for(32, 2), 512, 0, h->stream>>>(
-          st, nrows, pc.srp, pc.scol, pc.sval, x, x_ld, x_koff, y, SpmvEpi(), PP);
-    else if (pc.aligned && x16)
-      launch_pdl(h, k_spmv_csr_pf<16, 4, 16, false, 5>, grid_for(32, 2), 512, 0, h->stream, st, nrows,
-                 (const int64_t*)pc.srp, (const int*)pc.scol, (const double*)pc.sval, x, x_ld, x_koff, y, SpmvEpi(),
-                 PP);
-    else if (h->pcsr_unroll == 4)
-      k_spmv_csr_pf<16, 4, 16, false, 4><<<grid_for(32, 2), 512, 0, h->stream>>>(
-          st, nrows, pc.srp, pc.scol, pc.sval, x, x_ld, x_koff, y, SpmvEpi(), PP);
+    if (pc.c16)
+      launch_pdl(h, k_spmv_sell_ip<4, false, true>, g, 512, 0, h->stream, st, nrows, (const int64_t*)pc.soff,
+                 (const int*)pc.rcnt, (const int*)pc.ebase, (const uint16_t*)pc.eoff, (const double*)pc.ef,
+                 (const int64_t*)pc.srp, (const int*)pc.scol, (const double*)pc.sval, x, x_ld, x_koff, y, SpmvEpi());
     else
-      k_spmv_csr_pf<16, 4, 16, false, 2><<<grid_for(32, 2), 512, 0, h->stream>>>(
-          st, nrows, pc.srp, pc.scol, pc.sval, x, x_ld, x_koff, y, SpmvEpi(), PP);
-    return;
-  }
-  if (mode == 15) {
-    // CSR-16: 8 (value) + 2 (offset) bytes per nonzero + 4 per 16-entry chunk + chunk pointers
-    L.bytes_override(10.0 * nnz + 4.0 * cc.nchunks + 16.0 * (nrows + 1) + 8.0 * xlen + 8.0 * nrows);
-    k_spmv_c16<16, 4><<<grid_for(32, 4), 512, 0, h->stream>>>(st, nrows, rp, cc.cptr, cc.base, cc.off, val, x, x_ld,
-                                                                x_koff, y);
-    return;
-  }
-  switch (mode) {
-    case 0:
-      k_spmv_csr<<<grid_for(kSpmvThreads / 32, 8), kSpmvThreads, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld,
-                                                                               x_koff, y);
-      break;
-    case 1:
-      k_spmv_csr_rows<16, 4><<<grid_for(16, 4), 512, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
-      break;
-    case 2:
-      k_spmv_csr_rows<8, 4><<<grid_for(8, 8), 256, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
-      break;
-    case 10:
-      k_spmv_csr_rows<32, 2><<<grid_for(32, 2), 1024, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
-      break;
-    case 8:
-      k_spmv_csr_half<32, 4><<<grid_for(64, 2), 1024, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
-      break;
-    case 11:
-      k_spmv_csr_pf<32, 2, 32><<<grid_for(32, 2), 1024, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
-      break;
-    case 12:
-      k_spmv_csr_pf<32, 2, 16><<<grid_for(64, 2), 1024, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
-      break;
-    case 13:
-      k_spmv_csr_pf<16, 4, 32><<<grid_for(16, 4), 512, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
-      break;
-    case 14:
-      launch_pdl(h, k_spmv_csr_pf<16, 4, 16>, grid_for(32, 4), 512, 0, h->stream, st, nrows, rp, (const int*)col, val,
-                 x, x_ld, x_koff, y, SpmvEpi(), PairPart());
-      break;
-    default:  // 3
-      k_spmv_csr_rows<32, 4><<<grid_for(32, 2), 1024, 0, h->stream>>>(st, nrows, rp, col, val, x, x_ld, x_koff, y);
-      break;
-  }
+      launch_pdl(h, k_spmv_sell_ip<4, false, false>, g, 512, 0, h->stream, st, nrows, (const int64_t*)pc.soff,
+                 (const int*)pc.rcnt, (const int*)pc.ecol, (const uint16_t*)nullptr, (const double*)pc.ef,
+                 (const int64_t*)pc.srp, (const int*)pc.scol, (const double*)pc.sval, x, x_ld, x_koff, y, SpmvEpi());
+  } else if (pc.interp)
+    k_spmv_csr_pf<16, 4, 16, false, 6><<<grid_for(32, 2), 512, 0, h->stream>>>(
+        st, nrows, pc.srp, pc.scol, pc.sval, x, x_ld, x_koff, y, SpmvEpi(), PP);
+  else if (pc.aligned && x16)
+    launch_pdl(h, k_spmv_csr_pf<16, 4, 16, false, 5>, grid_for(32, 2), 512, 0, h->stream, st, nrows,
+               (const int64_t*)pc.srp, (const int*)pc.scol, (const double*)pc.sval, x, x_ld, x_koff, y, SpmvEpi(),
+               PP);
+  else
+    k_spmv_csr_pf<16, 4, 16, false, 4><<<grid_for(32, 2), 512, 0, h->stream>>>(
+        st, nrows, pc.srp, pc.scol, pc.sval, x, x_ld, x_koff, y, SpmvEpi(), PP);
 }
 
 // Grid of the fused windowed-orthogonalisation and normalisation kernels: about 8 elements per
 // thread, at least one CTA per SM, at most kVecBlocks (the partial-sum stride); short vectors
-// then pay a 148-way instead of a 592-way last-block reduction.  SFLSQR_VEC_GRID=full: always
-// kVecBlocks (A/B runs).
+// then pay a 148-way instead of a 592-way last-block reduction.
 int vec_grid(int64_t len) {
-  static const bool full = std::getenv("SFLSQR_VEC_GRID") && std::strcmp(std::getenv("SFLSQR_VEC_GRID"), "full") == 0;
-  if (full) return kVecBlocks;
   return (int)std::max<int64_t>(148, std::min<int64_t>((len + 8 * kVecThreads - 1) / (8 * kVecThreads), kVecBlocks));
 }
 
-// Row-tile GEMV launch: RPT rows per thread, CTAs of RPT * 256 rows, at most kVecBlocks CTAs
-// (grid-stride over the tiles).
-// Measured (configs 3 and 4): 2 rows per thread (512-row tiles, grid-stride over a full grid)
-// beats 4 and 8 (fewer CTAs, less in flight); SFLSQR_GEMV_RPT=4|8 for A/B runs.
-int gemv_rpt(int64_t len) {
-  (void)len;
-  static const int forced = std::getenv("SFLSQR_GEMV_RPT") ? std::atoi(std::getenv("SFLSQR_GEMV_RPT")) : 0;
-  return (forced == 4 || forced == 8) ? forced : 2;
-}
-int gemv_grid(int64_t len, int rpt) {
-  const int64_t tile = (int64_t)rpt * kVecThreads;
+// Row-tile GEMVs (x update, W-path residual): 2 rows per thread, 512-row tiles, grid-stride over
+// at most kVecBlocks CTAs (measured on configs 3-4: 4 and 8 rows per thread were slower).
+constexpr int kGemvRpt = 2;
+int gemv_grid(int64_t len) {
+  const int64_t tile = (int64_t)kGemvRpt * kVecThreads;
   return (int)std::max<int64_t>(1, std::min<int64_t>((len + tile - 1) / tile, kVecBlocks));
 }
 void launch_xupdate(sflsqr_t* h, int force) {
-  const int rpt = gemv_rpt(h->n_loc), g = gemv_grid(h->n_loc, rpt);
-  if (rpt == 8)
-    k_xupdate<8><<<g, kVecThreads, 0, h->stream>>>(h->P, force);
-  else if (rpt == 4)
-    k_xupdate<4><<<g, kVecThreads, 0, h->stream>>>(h->P, force);
-  else
-    k_xupdate<2><<<g, kVecThreads, 0, h->stream>>>(h->P, force);
+  k_xupdate<kGemvRpt><<<gemv_grid(h->n_loc), kVecThreads, 0, h->stream>>>(h->P, force);
 }
 void k_xupdate_launch_side(sflsqr_t* h) {
-  const int rpt = gemv_rpt(h->n_loc), g = gemv_grid(h->n_loc, rpt);
-  if (rpt == 8)
-    k_xupdate<8><<<g, kVecThreads, 0, h->side>>>(h->P, 0);
-  else if (rpt == 4)
-    k_xupdate<4><<<g, kVecThreads, 0, h->side>>>(h->P, 0);
-  else
-    k_xupdate<2><<<g, kVecThreads, 0, h->side>>>(h->P, 0);
+  k_xupdate<kGemvRpt><<<gemv_grid(h->n_loc), kVecThreads, 0, h->side>>>(h->P, 0);
 }
 void launch_res(sflsqr_t* h, cudaStream_t s, int fuse_stop) {
-  const int rpt = gemv_rpt(h->m_loc), g = gemv_grid(h->m_loc, rpt);
-  if (rpt == 8)
-    launch_pdl(h, k_res_partial<8>, g, kVecThreads, 0, s, h->P, fuse_stop);
-  else if (rpt == 4)
-    launch_pdl(h, k_res_partial<4>, g, kVecThreads, 0, s, h->P, fuse_stop);
-  else
-    launch_pdl(h, k_res_partial<2>, g, kVecThreads, 0, s, h->P, fuse_stop);
+  launch_pdl(h, k_res_partial<kGemvRpt>, gemv_grid(h->m_loc), kVecThreads, 0, s, h->P, fuse_stop);
 }
 
 // skbuf = S v (this rank's coordinates), allreduced over ranks.
@@ -766,36 +615,36 @@ int enqueue_orth(sflsqr_t* h, int side, int koff) {
   return SFLSQR_OK;
 }
 
-// GKB product with its epilogue (methods 4 / 5): fused into the default CSR kernel, or a
-// plain product followed by k_epi_vec (blur operator / a forced SpMV variant).
 // Fused-epilogue product on the operator's pair-CSR copy (if it has one): returns false when
 // the operator runs as plain CSR (the caller launches the CSR kernel).  extra: epilogue bytes.
 bool launch_pairs_epi(sflsqr_t* h, int which, const double* x, int64_t x_ld, double* y, const SpmvEpi& E, int cls,
                       double extra, int grid) {
   const PCSR& pc = which == 0 ? h->pa : h->pt;
-  const int mode = h->spmv_mode >= 0 ? h->spmv_mode : (pc.ok ? 16 : 14);
-  if (h->blur || !pc.ok || (mode != 16 && mode != 17)) return false;
+  if (!runs_on_pairs(h, which)) return false;
   const int64_t nrows = which == 0 ? h->m_loc : h->t_rows;
   const int64_t xlen = which == 0 ? (h->world > 1 ? h->world * h->n_max : h->n)
                                   : (h->tkind == T_ROWSHARD ? h->world * h->m_max : h->m_loc);
-  if (pc.f && pc.ecol) {  // sliced-ELL interpolation pairs with the fused epilogue
-    Launch L(h, cls, 12.0 * pc.sell_entries + 12.0 * pc.nsingles + 4.0 * nrows + 16.0 * (nrows + 1) + 8.0 * xlen +
-                         8.0 * nrows + extra);
+  if (pc.ell) {  // sliced-ELL interpolation pairs with the fused epilogue
+    Launch L(h, cls, sell_bytes(pc, nrows) + 8.0 * xlen + 8.0 * nrows + extra);
     const int64_t nsl = (nrows + kSellC - 1) / kSellC;
     const int g = (int)std::max<int64_t>(1, std::min<int64_t>((nsl + 15) / 16, 148 * 2 - h->spmv_grid_delta));
-    k_spmv_sell_ip<4, true><<<g, 512, 0, h->stream>>>(h->P.st, nrows, pc.soff, pc.rcnt, pc.ecol, pc.ef, pc.srp, pc.scol,
-                                                       pc.sval, x, x_ld, 0, y, E);
+    if (pc.c16)
+      k_spmv_sell_ip<4, true, true><<<g, 512, 0, h->stream>>>(h->P.st, nrows, pc.soff, pc.rcnt, pc.ebase, pc.eoff, pc.ef,
+                                                             pc.srp, pc.scol, pc.sval, x, x_ld, 0, y, E);
+    else
+      k_spmv_sell_ip<4, true, false><<<g, 512, 0, h->stream>>>(h->P.st, nrows, pc.soff, pc.rcnt, pc.ecol, nullptr, pc.ef,
+                                                              pc.srp, pc.scol, pc.sval, x, x_ld, 0, y, E);
     return true;
   }
   (void)grid;
-  Launch L(h, cls, (pc.f ? 12.0 : 20.0) * pc.npairs + 12.0 * pc.nsingles + 16.0 * (nrows + 1) + 8.0 * xlen + 8.0 * nrows +
+  Launch L(h, cls, (pc.interp ? 12.0 : 20.0) * pc.npairs + 12.0 * pc.nsingles + 16.0 * (nrows + 1) + 8.0 * xlen + 8.0 * nrows +
                        extra);
   PairPart PP;
   PP.rowptr = pc.prp;
   PP.col = pc.pcol;
   PP.val = pc.pval;
   PP.f = pc.f;
-  if (pc.f)
+  if (pc.interp)
     k_spmv_csr_pf<16, 4, 16, true, 6><<<grid, 512, 0, h->stream>>>(h->P.st, nrows, pc.srp, pc.scol, pc.sval, x, x_ld,
                                                                     0, y, E, PP);
   else if (pc.aligned && (uintptr_t)x % 16 == 0 && x_ld % 2 == 0)
@@ -807,6 +656,8 @@ bool launch_pairs_epi(sflsqr_t* h, int which, const double* x, int64_t x_ld, dou
   return true;
 }
 
+// GKB product with its epilogue (methods 4 / 5): fused into the product on the operator's format
+// (pairs or CSR), or, for the matrix-free blur, a plain product followed by k_epi_vec.
 void enqueue_apply_gkb(sflsqr_t* h, int which, const double* x, double* y, int kind, int slot_in, int slot_out,
                        int ctr_idx) {
   Params& P = h->P;
@@ -821,12 +672,11 @@ void enqueue_apply_gkb(sflsqr_t* h, int which, const double* x, double* y, int k
   E.slot_out = slot_out;
   E.ctr_idx = ctr_idx;
   const int64_t nrows = which == 0 ? h->m_loc : h->t_rows;
-  const int mode = h->spmv_mode >= 0 ? h->spmv_mode : 14;
   const int cls = which == 0 ? SFLSQR_KC_SPMV_A : SFLSQR_KC_SPMV_T;
   if (launch_pairs_epi(h, which, x, 0, y, E, cls, kind == 3 ? 0.0 : 8.0 * nrows,
                        (int)std::max<int64_t>(1, std::min<int64_t>((nrows + 31) / 32, 148 * 4))))
     return;
-  if (!h->blur && mode == 14) {
+  if (!h->blur) {
     const int64_t nnz = which == 0 ? h->nnz_a : h->nnz_t;
     const int64_t xlen = which == 0 ? h->n : h->m;
     Launch L(h, cls, 12.0 * nnz + 8.0 * (nrows + 1) + 8.0 * xlen + 8.0 * nrows + (kind == 3 ? 0.0 : 8.0 * nrows));
@@ -877,8 +727,6 @@ int enqueue_ls(sflsqr_t* h, bool forked) {
   return SFLSQR_OK;
 }
 
-// The cooperative phase kernels replace the standalone a1/a2 and a4/a5 kernels on one rank
-// with the fused window orthogonalisation of a sketched method (opt-in: SFLSQR_COOP=1).
 // FLSMR (needs column k+1 of T at step k) and sFLSMR (overlaps it with the LS) run the z-side
 // orthogonalisation of step k+1 at the end of step k (and of step 1 in set_rhs); step k then
 // starts with the normalisation.  Same arithmetic, earlier in the stream.
@@ -890,33 +738,6 @@ bool z_early(sflsqr_t* h) {
           h->world == 1 && h->side);
 }
 
-bool use_coop(sflsqr_t* h) {
-  return h->coop_grid > 0 && h->world == 1 && h->P.orth_alg == ORTH_FUSED && h->P.method == SFLSQR_METHOD_SFLSQR &&
-         h->sk_kind == 0 && !z_early(h);
-}
-
-int launch_coop(sflsqr_t* h, void (*kern)(Params), double bytes) {
-  Launch L(h, SFLSQR_KC_ORTH, bytes);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(h->coop_grid);
-  cfg.blockDim = dim3(kCoopThreads);
-  cfg.stream = h->stream;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeCooperative;
-  at[0].val.cooperative = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = h->coop_attr ? 1 : 0;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, h->P);
-  if (e != cudaSuccess && h->coop_attr) {  // e.g. not capturable: all blocks are co-resident anyway
-    cudaGetLastError();
-    h->coop_attr = false;
-    cfg.numAttrs = 0;
-    e = cudaLaunchKernelEx(&cfg, kern, h->P);
-  }
-  if (e != cudaSuccess) return fail(h, SFLSQR_E_CUDA, "cooperative launch: %s", cudaGetErrorString(e));
-  return SFLSQR_OK;
-}
-
 // a2 for the low-rank truncation: z_k = tau_r(p_k) by the randomized SVD (reading R22).
 int enqueue_lowrank(sflsqr_t* h) {
   Params& P = h->P;
@@ -925,10 +746,7 @@ int enqueue_lowrank(sflsqr_t* h) {
     Launch L(h, SFLSQR_KC_TAU, hw8 + 8.0 * l * (P.lr_W + P.lr_H));
     k_lr_range<<<std::min(P.lr_H, 148 * 4), 256, sizeof(double) * P.lr_W, h->stream>>>(P);
   }
-  if (h->lr_qr_cgs) {
-    Launch L(h, SFLSQR_KC_TAU, 8.0 * l * P.lr_H * 2);
-    k_lr_qr<<<1, 1024, kLrQrSmem, h->stream>>>(P);
-  } else {
+  {
     // sCholQR3 on the range Y: lr_Y -> lr_Q -> lr_Y -> lr_Q
     const int gg = (int)std::max<int64_t>(1, ((int64_t)P.lr_l * P.lr_l + kLrGramThreads / 32 - 1) / (kLrGramThreads / 32));
     const int ga = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)P.lr_H * P.lr_l + 255) / 256, 148 * 4));
@@ -981,15 +799,10 @@ int enqueue_iteration(sflsqr_t* h) {
   const int k = h->host_k;  // used only for the byte model
   const double n8 = 8.0 * h->n_loc, m8 = 8.0 * h->m_loc;
   int rc;
-  const bool coop = use_coop(h);
-  const int Jz = std::min(P.ell, k - 1), Jw = std::min(P.ell + 1, k);
-  // a1 + a2 in one cooperative kernel
-  if (coop && (rc = launch_coop(h, k_zphase, n8 * (3 + 2 * Jz + (P.use_pring ? 1 : 0) + (P.precond ? 1 : 0)))))
-    return rc;
   // a1: z-side windowed orthogonalisation (FLSMR: done at the end of the previous step / in set_rhs)
-  if (!coop && !z_early(h) && (rc = enqueue_orth(h, 0, 0))) return rc;
+  if (!z_early(h) && (rc = enqueue_orth(h, 0, 0))) return rc;
   // a1 end + a2: normalise, tau, store z_k
-  if (!coop) {
+  {
     Launch L(h, SFLSQR_KC_TAU, n8 * (2 + (P.use_pring ? 1 : 0) + (P.precond ? 1 : 0)));
     launch_pdl(h, k_finish_z, vec_grid(h->n_loc), kVecThreads, 0, h->stream, P);
   }
@@ -1006,13 +819,9 @@ int enqueue_iteration(sflsqr_t* h) {
     }
     enqueue_apply(h, 0, P.st, h->zfull, 0, 0, P.w, SFLSQR_KC_SPMV_A);
   }
-  // a4 + a5 in one cooperative kernel (sketch of w, then the w side)
-  if (coop && (rc = launch_coop(h, k_wphase,
-                                m8 * (4 + 2 * Jw) + (P.method == SFLSQR_METHOD_SFLSQR ? 12.0 * h->s_nz * h->m_loc : 0.0))))
-    return rc;
   // a4 (sFLSQR): S_AZ[:, k] = S w -- on the side stream (one rank), beside the w-side dots; the
-  // in-place w update waits for it (SFLSQR_SKETCH_SIDE)
-  const bool sk_side = h->sketch_side && !coop && P.method == SFLSQR_METHOD_SFLSQR && h->world == 1 && h->side &&
+  // in-place w update waits for it (SFLSQR_KNOB_SKETCH_MAIN: main stream)
+  const bool sk_side = h->sketch_side && P.method == SFLSQR_METHOD_SFLSQR && h->world == 1 && h->side &&
                        !h->prof_on;
   if (sk_side) {
     CU(h, cudaEventRecord(h->ev_fork, h->stream));
@@ -1020,7 +829,7 @@ int enqueue_iteration(sflsqr_t* h) {
     if ((rc = enqueue_sketch(h, P.st, P.w, h->side))) return rc;
     CU(h, cudaEventRecord(h->ev_sk, h->side));
     h->axpy_wait_sk = 1;
-  } else if (!coop && P.method == SFLSQR_METHOD_SFLSQR && (rc = enqueue_sketch(h, P.st, P.w))) {
+  } else if (P.method == SFLSQR_METHOD_SFLSQR && (rc = enqueue_sketch(h, P.st, P.w))) {
     return rc;
   }
   // a7 can start now for sFLSQR (it needs only S A Z_k) / after a5 for FLSQR (it needs
@@ -1030,7 +839,7 @@ int enqueue_iteration(sflsqr_t* h) {
                        (P.method == SFLSQR_METHOD_SFLSQR || P.method == SFLSQR_METHOD_FLSQR);
   if (fork_ls && P.method == SFLSQR_METHOD_SFLSQR && (rc = enqueue_ls(h, true))) return rc;
   // a5: w-side windowed orthogonalisation and normalisation
-  if (!coop) {
+  {
     rc = enqueue_orth(h, 1, 0);
     h->axpy_wait_sk = -1;
     if (rc) return rc;
@@ -1118,75 +927,6 @@ int enqueue_iteration(sflsqr_t* h) {
   return SFLSQR_OK;
 }
 
-// Build the CSR-16 copy of a device CSR (nrows x *, nnz entries); leaves c.ok = false
-// when a 16-entry chunk spans more than 65536 columns.
-int build_c16(sflsqr_t* h, int64_t nrows, const int64_t* rp, const int32_t* col, int64_t nnz, C16& c) {
-  c = C16();
-  if (nrows < 1 || nnz < 1) return SFLSQR_OK;
-  int64_t* cnt = nullptr;
-  void* tmp = nullptr;
-  int* flag = nullptr;
-  size_t tmp_bytes = 0;
-  int rc;
-  auto cleanup = [&]() {
-    cudaFree(cnt);
-    cudaFree(tmp);
-    cudaFree(flag);
-  };
-  if ((rc = dalloc(h, (void**)&cnt, sizeof(int64_t) * (nrows + 1), nullptr)) ||
-      (rc = dalloc(h, (void**)&c.cptr, sizeof(int64_t) * (nrows + 1), nullptr)) ||
-      (rc = dalloc(h, (void**)&flag, sizeof(int), nullptr))) {
-    cleanup();
-    return rc;
-  }
-  const int g = (int)std::min<int64_t>((nrows + 256) / 256 + 1, 148 * 16);
-  k_c16_count<<<g, 256, 0, h->stream>>>(nrows, rp, cnt);
-  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, c.cptr, nrows + 1, h->stream);
-  if ((rc = dalloc(h, &tmp, tmp_bytes, nullptr))) {
-    cleanup();
-    return rc;
-  }
-  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, c.cptr, nrows + 1, h->stream);
-  CU(h, cudaMemcpyAsync(&c.nchunks, c.cptr + nrows, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
-  CU(h, cudaMemsetAsync(flag, 0, sizeof(int), h->stream));
-  CU(h, cudaStreamSynchronize(h->stream));
-  if ((rc = dalloc(h, (void**)&c.base, sizeof(int) * std::max<int64_t>(c.nchunks, 1), nullptr)) ||
-      (rc = dalloc(h, (void**)&c.off, sizeof(uint16_t) * nnz, nullptr))) {
-    cleanup();
-    return rc;
-  }
-  const int gf = (int)std::min<int64_t>((nrows + 15) / 16 + 1, 148 * 32);
-  k_c16_fill<<<gf, 256, 0, h->stream>>>(nrows, rp, col, c.cptr, c.base, c.off, flag);
-  int ovf = 0;
-  CU(h, cudaMemcpyAsync(&ovf, flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
-  CU(h, cudaStreamSynchronize(h->stream));
-  cleanup();
-  if (ovf) {
-    cudaFree(c.cptr);
-    cudaFree(c.base);
-    cudaFree(c.off);
-    c = C16();
-    return SFLSQR_OK;
-  }
-  c.ok = true;
-  return SFLSQR_OK;
-}
-
-// Built only on request (sflsqr_debug_set_tuning(h, 15, ...)): measured slower than the
-// int32 CSR kernel on the CT operators, so it costs no memory by default.
-int build_c16_all(sflsqr_t* h) {
-  int rc;
-  if (h->blur || (h->ca.ok && h->ct.ok)) return SFLSQR_OK;
-  for (C16* c : {&h->ca, &h->ct}) {
-    cudaFree(c->cptr);
-    cudaFree(c->base);
-    cudaFree(c->off);
-    *c = C16();
-  }
-  if ((rc = build_c16(h, h->m_loc, h->a_rowptr, h->a_col, h->nnz_a, h->ca))) return rc;
-  return build_c16(h, h->t_rows, h->t_rowptr, h->t_col, h->nnz_t, h->ct);
-}
-
 int check_launch(sflsqr_t* h);
 
 // Pair-CSR copy of one operator (k_pcsr_rows): counts, two exclusive scans, fill.
@@ -1267,7 +1007,7 @@ int build_pcsr(sflsqr_t* h, int64_t nrows, const int64_t* rp, const int32_t* col
 // 1 - second value bitwise (linear-interpolation weights), keep only the second values:
 // 12 instead of 20 bytes per pair, the same operator bit for bit.
 int try_interp(sflsqr_t* h, PCSR& p) {
-  if (!p.ok || p.aligned || p.f || p.npairs < 1) return SFLSQR_OK;
+  if (!p.ok || p.aligned || p.interp || p.npairs < 1) return SFLSQR_OK;
   int* flag = nullptr;
   int rc;
   if ((rc = dalloc(h, (void**)&flag, sizeof(int), nullptr))) return rc;
@@ -1284,13 +1024,15 @@ int try_interp(sflsqr_t* h, PCSR& p) {
   CU(h, cudaStreamSynchronize(h->stream));
   cudaFree(p.pval);
   p.pval = nullptr;
+  p.interp = true;
   return check_launch(h);
 }
 
 // Sliced-ELL copy of an interpolation pair-CSR operator (row per lane, k_spmv_sell_ip), kept only
 // when the slices' padding costs at most 10 % more entries.
+int build_sell_c16(sflsqr_t* h, int64_t nrows, PCSR& p);
 int build_sell(sflsqr_t* h, int64_t nrows, PCSR& p) {
-  if (!p.ok || !p.f || nrows < 1) return SFLSQR_OK;
+  if (!p.ok || !p.interp || nrows < 1) return SFLSQR_OK;
   const int64_t nsl = (nrows + kSellC - 1) / kSellC;
   int64_t* len = nullptr;
   void* tmp = nullptr;
@@ -1332,108 +1074,133 @@ int build_sell(sflsqr_t* h, int64_t nrows, PCSR& p) {
   k_sell_fill<<<(int)std::min<int64_t>((nrows + 255) / 256, 148 * 16), 256, 0, h->stream>>>(nrows, p.prp, p.pcol, p.f,
                                                                                           p.soff, p.rcnt, p.ecol, p.ef);
   CU(h, cudaStreamSynchronize(h->stream));
-  return check_launch(h);
-}
-
-// Sliced-ELL copy of a plain CSR operator (k_sell_len / k_sell_fill on rowptr, col, val), kept when
-// the slices' padding costs at most max_pad more entries.
-int build_sell_csr(sflsqr_t* h, int64_t nrows, const int64_t* rp, const int32_t* col, const double* val, int64_t nnz,
-                   SELL& e, double max_pad) {
-  free_sell(e);
-  if (nrows < 1 || nnz < 1) return SFLSQR_OK;
-  const int64_t nsl = (nrows + kSellC - 1) / kSellC;
-  int64_t* len = nullptr;
-  void* tmp = nullptr;
-  size_t tb = 0;
-  int rc;
-  if ((rc = dalloc(h, (void**)&len, sizeof(int64_t) * (nsl + 1), nullptr)) ||
-      (rc = dalloc(h, (void**)&e.soff, sizeof(int64_t) * (nsl + 1), nullptr))) {
-    cudaFree(len);
-    free_sell(e);
-    return rc;
-  }
-  CU(h, cudaMemsetAsync(len + nsl, 0, sizeof(int64_t), h->stream));
-  k_sell_len<<<(int)std::min<int64_t>((nsl + 255) / 256, 148 * 16), 256, 0, h->stream>>>(nrows, rp, len);
-  cub::DeviceScan::ExclusiveSum(nullptr, tb, len, e.soff, nsl + 1, h->stream);
-  if ((rc = dalloc(h, &tmp, tb, nullptr))) {
-    cudaFree(len);
-    free_sell(e);
-    return rc;
-  }
-  cub::DeviceScan::ExclusiveSum(tmp, tb, len, e.soff, nsl + 1, h->stream);
-  CU(h, cudaMemcpyAsync(&e.entries, e.soff + nsl, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
-  CU(h, cudaStreamSynchronize(h->stream));
-  cudaFree(len);
-  cudaFree(tmp);
-  if ((double)e.entries > (1.0 + max_pad) * (double)nnz ||
-      (rc = dalloc(h, (void**)&e.rcnt, sizeof(int) * nrows, nullptr)) ||
-      (rc = dalloc(h, (void**)&e.ecol, sizeof(int) * std::max<int64_t>(e.entries, 1), nullptr)) ||
-      (rc = dalloc(h, (void**)&e.ev, sizeof(double) * std::max<int64_t>(e.entries, 1), nullptr))) {
-    free_sell(e);
-    cudaGetLastError();
-    return SFLSQR_OK;
-  }
-  CU(h, cudaMemsetAsync(e.ecol, 0, sizeof(int) * e.entries, h->stream));
-  CU(h, cudaMemsetAsync(e.ev, 0, sizeof(double) * e.entries, h->stream));
-  k_sell_fill<<<(int)std::min<int64_t>((nrows + 255) / 256, 148 * 16), 256, 0, h->stream>>>(nrows, rp, col, val, e.soff,
-                                                                                          e.rcnt, e.ecol, e.ev);
-  CU(h, cudaStreamSynchronize(h->stream));
-  if ((rc = check_launch(h))) {
-    free_sell(e);
-    return rc;
-  }
-  e.ok = true;
+  if ((rc = check_launch(h))) return rc;
+  p.ell = true;
+  // the sliced-ELL copy serves every product of this operator: release the pair-CSR arrays it was
+  // built from
+  cudaFree(p.prp);
+  cudaFree(p.pcol);
+  cudaFree(p.f);
+  p.prp = nullptr;
+  p.pcol = nullptr;
+  p.f = nullptr;
+  if (h->ell_c16) return build_sell_c16(h, nrows, p);
   return SFLSQR_OK;
 }
 
-// Auxiliary SpMV formats the selected mode needs (built after every operator upload).
+// 16-bit column offsets for the sliced-ELL interpolation pairs: entry k of a slice's 32 rows keeps
+// column - base[slice entry k] (the base is the entry's smallest column; the 32 neighbouring pixels of
+// a slice project onto neighbouring bins at each angle, so their columns lie within a few bins).  The
+// same operator: 10.125 instead of 12 bytes per pair, for a product that streams its bytes at the HBM
+// roofline.  Kept only when every slice entry spans < 65536 columns.
+int build_sell_c16(sflsqr_t* h, int64_t nrows, PCSR& p) {
+  const int64_t nsl = (nrows + kSellC - 1) / kSellC;
+  const int64_t nbase = p.sell_entries / kSellC;
+  int* flag = nullptr;
+  int rc;
+  if ((rc = dalloc(h, (void**)&flag, sizeof(int), nullptr))) return rc;
+  if ((rc = dalloc(h, (void**)&p.ebase, sizeof(int) * std::max<int64_t>(nbase, 1), nullptr)) ||
+      (rc = dalloc(h, (void**)&p.eoff, sizeof(uint16_t) * std::max<int64_t>(p.sell_entries, 1), nullptr))) {
+    cudaFree(flag);
+    cudaFree(p.ebase);
+    cudaFree(p.eoff);
+    p.ebase = nullptr;
+    p.eoff = nullptr;
+    cudaGetLastError();
+    return SFLSQR_OK;  // no room: the 32-bit columns serve
+  }
+  CU(h, cudaMemsetAsync(flag, 0, sizeof(int), h->stream));
+  k_sell_c16<<<(int)std::min<int64_t>((nsl + 7) / 8, 148 * 16), 256, 0, h->stream>>>(nrows, p.soff, p.rcnt, p.ecol,
+                                                                                      p.ebase, p.eoff, flag);
+  int bad = 0;
+  CU(h, cudaMemcpyAsync(&bad, flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CU(h, cudaStreamSynchronize(h->stream));
+  cudaFree(flag);
+  if ((rc = check_launch(h))) return rc;
+  if (bad) {
+    cudaFree(p.ebase);
+    cudaFree(p.eoff);
+    p.ebase = nullptr;
+    p.eoff = nullptr;
+    return SFLSQR_OK;
+  }
+  cudaFree(p.ecol);
+  p.ecol = nullptr;
+  p.c16 = true;
+  return SFLSQR_OK;
+}
+
+// Release the uploaded CSR of an operator once its format copy serves every product of it (unless
+// SFLSQR_KNOB_KEEP_CSR or the arrays are borrowed): the copy is the same operator, and the CSR
+// would hold 12 B per nonzero of HBM that no kernel reads (config 4: 30 GB; a config-5 shard
+// needs the room).
+void release_csr(sflsqr_t* h, int which) {
+  if (h->keep_csr) return;
+  if (which == 0 && h->pa.ok && h->a_owned && !h->csr_freed_a) {
+    cudaFree(h->a_col);
+    cudaFree(h->a_val);
+    h->a_col = nullptr;
+    h->a_val = nullptr;
+    h->csr_freed_a = true;
+  }
+  if (which == 1 && h->pt.ok && h->t_owned && !h->csr_freed_t) {
+    cudaFree(h->t_col);
+    cudaFree(h->t_val);
+    h->t_col = nullptr;
+    h->t_val = nullptr;
+    h->csr_freed_t = true;
+  }
+}
+
+// SpMV format copies (built after every operator upload).  Default rule per operator (DESIGN.md
+// §5): pair-CSR when at least 75 % of the nonzeros pair up (>= 12.5 % fewer bytes for the
+// DRAM-bound product; the pixel-driven B of config 4: 100 %), then interpolation pairs when every
+// pair is (1 - f, f) bitwise, then their sliced-ELL copy when its padding is <= 10 %; else aligned
+// pair-CSR when at least 20 % of the nonzeros sit in even-column pairs (16-byte gathers: fewer L1
+// wavefronts; Siddon A: 50 %, Siddon A^T: 21 %); else plain CSR.  Rows of >= 64 nonzeros on
+// average only.  sflsqr_debug_set_tuning 16 / 17 force pair-CSR / aligned pair-CSR, 14 plain CSR.
 int build_formats(sflsqr_t* h) {
   if (h->blur) return SFLSQR_OK;
-  if (h->spmv_mode == 15) return build_c16_all(h);
   int rc;
   if (h->spmv_mode == 16 || h->spmv_mode == 17) {
     const bool al = h->spmv_mode == 17;
-    if ((!h->pa.ok || h->pa.aligned != al) &&
+    if ((!h->pa.ok || h->pa.aligned != al || h->pa.interp) &&
         (rc = build_pcsr(h, h->m_loc, h->a_rowptr, h->a_col, h->a_val, h->pa, al)))
       return rc;
-    if ((!h->pt.ok || h->pt.aligned != al) &&
+    if ((!h->pt.ok || h->pt.aligned != al || h->pt.interp) &&
         (rc = build_pcsr(h, h->t_rows, h->t_rowptr, h->t_col, h->t_val, h->pt, al)))
       return rc;
-  } else if (h->spmv_mode < 0) {
-    // default rule per operator: pair-CSR when at least 75 % of the nonzeros pair
-    // up (>= 12.5 % fewer bytes for the DRAM-bound product; the pixel-driven B of config 4: 100 %),
-    // else aligned pair-CSR when at least 20 % sit in even-column pairs (16-byte gathers: fewer L1
-    // wavefronts; Siddon A: 50 %, Siddon A^T: 21 %), else plain CSR; rows of >= 64 nonzeros on
-    // average only.
-    auto pick = [&](int64_t nrows, const int64_t* rp, const int32_t* col, const double* val, int64_t nnz,
-                    PCSR& p) -> int {
-      // short rows (< 64 nonzeros on average, e.g. the 5 x 5 stencil rows of config 8) lose more to
-      // the second loop and the 64-register kernel than the pairs save (measured): plain CSR
-      if (p.ok || nnz <= 0 || nnz < 64 * nrows) return SFLSQR_OK;
-      // a copy costs up to 10 B per nonzero + 16 B per row: only when it leaves the solve's
-      // buffers room (>= 4 GB and >= 10 % of the device free afterwards); an allocation failure
-      // leaves the operator plain CSR rather than failing the upload
-      size_t fr = 0, tot = 0;
-      cudaMemGetInfo(&fr, &tot);
-      const double need = 10.0 * nnz + 32.0 * (nrows + 1);
-      if ((double)fr < need + std::max(4.0e9, 0.1 * (double)tot)) return SFLSQR_OK;
-      int r = build_pcsr(h, nrows, rp, col, val, p, false, 0.75);
-      if (!r && p.ok && h->pcsr_interp) r = try_interp(h, p);
-      if (!r && p.ok && p.f && h->sell) r = build_sell(h, nrows, p);
-      if (!r && !p.ok) r = build_pcsr(h, nrows, rp, col, val, p, true, 0.20);
-      if (r == SFLSQR_E_OOM) {
-        free_pcsr(p);
-        cudaGetLastError();
-        return SFLSQR_OK;
-      }
-      return r;
-    };
-    if (h->sell_a && h->nnz_a >= 64 * h->m_loc) {
-      if ((rc = build_sell_csr(h, h->m_loc, h->a_rowptr, h->a_col, h->a_val, h->nnz_a, h->ea, 0.10))) return rc;
-    }
-    if (!h->ea.ok && (rc = pick(h->m_loc, h->a_rowptr, h->a_col, h->a_val, h->nnz_a, h->pa))) return rc;
-    if ((rc = pick(h->t_rows, h->t_rowptr, h->t_col, h->t_val, h->nnz_t, h->pt))) return rc;
+    return SFLSQR_OK;
   }
+  if (h->spmv_mode == 14) return SFLSQR_OK;
+  auto pick = [&](int64_t nrows, const int64_t* rp, const int32_t* col, const double* val, int64_t nnz,
+                  PCSR& p) -> int {
+    // short rows (< 64 nonzeros on average, e.g. the 5 x 5 stencil rows of config 8) lose more to
+    // the second loop and the 64-register kernel than the pairs save (measured): plain CSR
+    if (p.ok || nnz <= 0 || nnz < 64 * nrows) return SFLSQR_OK;
+    // peak of the chain: pair-CSR (<= 10 B per nonzero + 16 B per row) while the CSR is still held,
+    // plus the interpolation values (4 B per nonzero) or the sliced-ELL copy (6.6 B per nonzero) beside
+    // it; build only when that leaves the solve's buffers room (>= 4 GB and >= 10 % of the device
+    // free afterwards); an allocation failure leaves the operator plain CSR rather than failing
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    const double need = 16.6 * nnz + 40.0 * (nrows + 1);
+    if ((double)fr < need + std::max(4.0e9, 0.1 * (double)tot)) return SFLSQR_OK;
+    int r = build_pcsr(h, nrows, rp, col, val, p, false, 0.75);
+    if (!r && p.ok && h->pcsr_interp) r = try_interp(h, p);
+    if (!r && p.ok && p.interp && h->sell) r = build_sell(h, nrows, p);
+    if (!r && !p.ok) r = build_pcsr(h, nrows, rp, col, val, p, true, 0.20);
+    if (r == SFLSQR_E_OOM) {
+      free_pcsr(p);
+      cudaGetLastError();
+      return SFLSQR_OK;
+    }
+    return r;
+  };
+  if ((rc = pick(h->m_loc, h->a_rowptr, h->a_col, h->a_val, h->nnz_a, h->pa))) return rc;
+  release_csr(h, 0);
+  if ((rc = pick(h->t_rows, h->t_rowptr, h->t_col, h->t_val, h->nnz_t, h->pt))) return rc;
+  release_csr(h, 1);
   return SFLSQR_OK;
 }
 
@@ -1571,8 +1338,6 @@ int alloc_solve(sflsqr_t* h) {
   const size_t zlen = std::max<size_t>(n, (size_t)h->n_max);
   if ((rc = dalloc(h, (void**)&P.st, sizeof(DevState), &h->solve_allocs, &h->solve_sizes))) return rc;
   if ((rc = dalloc(h, (void**)&P.ctr, sizeof(int) * CTR_COUNT, &h->solve_allocs, &h->solve_sizes))) return rc;
-  if ((rc = dalloc(h, (void**)&P.bar, sizeof(unsigned int) * 2, &h->solve_allocs, &h->solve_sizes))) return rc;
-  CU(h, cudaMemset(P.bar, 0, sizeof(unsigned int) * 2));
   if ((rc = A(&P.z, zlen)) || (rc = A(&P.x, n)) || (rc = A(&P.Z, n * ncol)) || (rc = A(&P.w, m)) ||
       (rc = A(&P.W, m * (ncol + 1))) || (rc = A(&P.b, m)) || (rc = A(&P.H, (size_t)(maxit + 1) * maxit)) ||
       (rc = A(&P.Tm, (size_t)(maxit + 1) * (maxit + 1))) || (rc = A(&P.part, (size_t)s * kVecBlocks)) ||
@@ -1618,10 +1383,9 @@ int alloc_solve(sflsqr_t* h) {
       if (h->p2p && (rc = A(&h->zrecv, (size_t)h->world * h->n_max))) return rc;
     }
   }
-  // Debug aid (no sanitizer on this pool): SFLSQR_DEBUG_POISON=1 fills every solve
-  // buffer with NaN bytes so a read-before-write shows up as NaN in the results.
-  const char* poison = std::getenv("SFLSQR_DEBUG_POISON");
-  if (poison && poison[0] == '1') {
+  // Debug aid: SFLSQR_KNOB_DEBUG_POISON fills every solve buffer with NaN bytes so a
+  // read-before-write shows up as NaN in the results.
+  if (h->knobs & SFLSQR_KNOB_DEBUG_POISON) {
     for (size_t i = 0; i < h->solve_allocs.size(); ++i)
       if (h->solve_allocs[i] != (void*)P.st && h->solve_allocs[i] != (void*)P.ctr)
         CU(h, cudaMemset(h->solve_allocs[i], 0xFF, h->solve_sizes[i]));
@@ -1738,6 +1502,117 @@ int upload_csr(sflsqr_t* h, int64_t nrows, const int64_t* rp, const int32_t* col
   return SFLSQR_OK;
 }
 
+// T = A^T of this rank's A rows on the device (T_BUILD): tnrows = n (one rank) or world * n_max
+// (COLSHARD, A's columns already in the padded layout).  The entries of each T row are ordered by
+// A row (then value bits), the order a sequential transpose produces.  Rows longer than kTrSortMax
+// entries (dense columns) are sorted by cub's segmented sort in two stable passes (value bits,
+// then row), which needs 24 B per nonzero of scratch.
+int device_transpose(sflsqr_t* h, int64_t nrows, int64_t tnrows, const int64_t* rp, const int32_t* col,
+                     const double* val, int64_t nnz, int64_t** trp_out, int32_t** tcol_out, double** tval_out) {
+  int64_t* trp = nullptr;
+  int32_t* tcol = nullptr;
+  double* tval = nullptr;
+  unsigned long long* cnt = nullptr;
+  int* flag = nullptr;
+  void* tmp = nullptr;
+  size_t tb = 0;
+  int rc;
+  auto cleanup = [&](bool all) {
+    cudaFree(cnt);
+    cudaFree(flag);
+    cudaFree(tmp);
+    if (all) {
+      cudaFree(trp);
+      cudaFree(tcol);
+      cudaFree(tval);
+    }
+  };
+  if ((rc = dalloc(h, (void**)&trp, sizeof(int64_t) * (tnrows + 1), nullptr)) ||
+      (rc = dalloc(h, (void**)&tcol, sizeof(int32_t) * std::max<int64_t>(nnz, 1), nullptr)) ||
+      (rc = dalloc(h, (void**)&tval, sizeof(double) * std::max<int64_t>(nnz, 1), nullptr)) ||
+      (rc = dalloc(h, (void**)&cnt, sizeof(unsigned long long) * (tnrows + 1), nullptr)) ||
+      (rc = dalloc(h, (void**)&flag, sizeof(int), nullptr))) {
+    cleanup(true);
+    return rc;
+  }
+  cudaStream_t s = h->stream;
+  CU(h, cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * (tnrows + 1), s));
+  CU(h, cudaMemsetAsync(flag, 0, sizeof(int), s));
+  const int g = (int)std::max<int64_t>(1, std::min<int64_t>((nnz + 255) / 256, 148 * 16));
+  if (nnz) k_tr_count<<<g, 256, 0, s>>>(nnz, col, cnt);
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, (int64_t*)cnt, trp, tnrows + 1, s);
+  if ((rc = dalloc(h, &tmp, tb, nullptr))) {
+    cleanup(true);
+    return rc;
+  }
+  cub::DeviceScan::ExclusiveSum(tmp, tb, (int64_t*)cnt, trp, tnrows + 1, s);
+  CU(h, cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * (tnrows + 1), s));
+  if (nnz) {
+    const int gr = (int)std::max<int64_t>(1, std::min<int64_t>((nrows + 7) / 8, 148 * 16));
+    k_tr_fill<<<gr, 256, 0, s>>>(nrows, rp, col, val, trp, cnt, tcol, tval);
+    k_tr_sort<<<(int)std::max<int64_t>(1, std::min<int64_t>(tnrows, 148 * 8)), 256, kTrSortSmem, s>>>(tnrows, trp, tcol,
+                                                                                                  tval, flag);
+  }
+  int long_rows = 0;
+  CU(h, cudaMemcpyAsync(&long_rows, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CU(h, cudaStreamSynchronize(s));
+  if ((rc = check_launch(h))) {
+    cleanup(true);
+    return rc;
+  }
+  if (long_rows) {
+    // (row, value bits) order by two stable segmented sorts over every T row
+    unsigned long long *kv = nullptr, *kv2 = nullptr;
+    int* r2 = nullptr;
+    void* t2 = nullptr;
+    size_t t2b = 0, t2b1 = 0;
+    auto done2 = [&]() {
+      cudaFree(kv);
+      cudaFree(kv2);
+      cudaFree(r2);
+      cudaFree(t2);
+    };
+    unsigned long long* tv = reinterpret_cast<unsigned long long*>(tval);
+    cub::DeviceSegmentedSort::StableSortPairs(nullptr, t2b, tv, kv, tcol, r2, nnz, tnrows, trp, trp + 1, s);
+    cub::DeviceSegmentedSort::StableSortPairs(nullptr, t2b1, r2, tcol, kv, tv, nnz, tnrows, trp, trp + 1, s);
+    t2b = std::max(t2b, t2b1);
+    if ((rc = dalloc(h, (void**)&kv, sizeof(unsigned long long) * nnz, nullptr)) ||
+        (rc = dalloc(h, (void**)&r2, sizeof(int) * nnz, nullptr)) || (rc = dalloc(h, &t2, t2b, nullptr))) {
+      done2();
+      cleanup(true);
+      return rc;
+    }
+    // pass 1: by value bits (tval -> kv, rows follow into r2); pass 2: stably by row (r2 -> tcol, kv -> tval)
+    cub::DeviceSegmentedSort::StableSortPairs(t2, t2b, tv, kv, tcol, r2, nnz, tnrows, trp, trp + 1, s);
+    cub::DeviceSegmentedSort::StableSortPairs(t2, t2b, r2, tcol, kv, tv, nnz, tnrows, trp, trp + 1, s);
+    CU(h, cudaStreamSynchronize(s));
+    done2();
+    if ((rc = check_launch(h))) {
+      cleanup(true);
+      return rc;
+    }
+    (void)kv2;
+  }
+  cleanup(false);
+  *trp_out = trp;
+  *tcol_out = tcol;
+  *tval_out = tval;
+  return SFLSQR_OK;
+}
+
+// Sharded column remap on the device: A's columns (T's for ROWSHARD) into the padded layout.
+int device_remap_cols(sflsqr_t* h, int32_t* col, int64_t nnz, const std::vector<int64_t>& st, int64_t mx) {
+  if (nnz == 0) return SFLSQR_OK;
+  int64_t* dst = nullptr;
+  int rc;
+  if ((rc = upload(h, (void**)&dst, st.data(), sizeof(int64_t) * st.size(), cudaMemcpyHostToDevice))) return rc;
+  const int g = (int)std::max<int64_t>(1, std::min<int64_t>((nnz + 255) / 256, 148 * 16));
+  k_remap_cols<<<g, 256, 0, h->stream>>>(nnz, col, dst, (int)st.size() - 1, mx);
+  cudaStreamSynchronize(h->stream);
+  cudaFree(dst);
+  return check_launch(h);
+}
+
 }  // namespace
 
 // ====================================================================== C ABI
@@ -1796,6 +1671,12 @@ int sflsqr_create(sflsqr_t** out, const sflsqr_opts* o) {
     return fail(nullptr, SFLSQR_E_INVALID, "world > 1 with NCCL needs opts.nccl_id");
   if (o->world > 1 && o->comm_kind == SFLSQR_COMM_LOCAL && !o->local_group)
     return fail(nullptr, SFLSQR_E_INVALID, "world > 1 with LOCAL needs opts.local_group");
+  if (o->knobs & ~SFLSQR_KNOB_ALL) return fail(nullptr, SFLSQR_E_INVALID, "unknown opts.knobs bits");
+  if ((o->knobs & SFLSQR_KNOB_RES_MAIN) && (o->knobs & SFLSQR_KNOB_RES_SIDE))
+    return fail(nullptr, SFLSQR_E_INVALID, "SFLSQR_KNOB_RES_MAIN and SFLSQR_KNOB_RES_SIDE exclude each other");
+  if ((o->knobs & SFLSQR_KNOB_P2P_ON) && (o->knobs & SFLSQR_KNOB_P2P_OFF))
+    return fail(nullptr, SFLSQR_E_INVALID, "SFLSQR_KNOB_P2P_ON and SFLSQR_KNOB_P2P_OFF exclude each other");
+  const int32_t kn = o->knobs;
   int ndev = 0;
   cudaError_t e = cudaGetDeviceCount(&ndev);
   if (e != cudaSuccess || ndev == 0) {
@@ -1808,6 +1689,7 @@ int sflsqr_create(sflsqr_t** out, const sflsqr_opts* o) {
   h->o = *o;
   h->rank = o->rank;
   h->world = o->world;
+  h->knobs = kn;
   if (o->window > o->maxit) h->o.window = o->maxit;  // full orthogonalisation
   if (o->method == SFLSQR_METHOD_FLSQR || o->method == SFLSQR_METHOD_FLSMR)
     h->o.window = o->maxit;  // FLSQR / FLSMR: full (L344-345)
@@ -1828,10 +1710,9 @@ int sflsqr_create(sflsqr_t** out, const sflsqr_opts* o) {
       h->comm = nccl_comm_create(o->nccl_id, o->rank, o->world, o->device, ce);
     else
       h->comm = local_comm_create(static_cast<LocalGroup*>(o->local_group), o->rank);
-    // peer-memory collectives: default on in-process (tested), opt-in (SFLSQR_P2P=1) across
+    // peer-memory collectives: default on in-process (tested), opt-in (SFLSQR_KNOB_P2P_ON) across
     // processes (CUDA IPC over NVLink: not exercisable on this single-GPU pool)
-    const char* pe = std::getenv("SFLSQR_P2P");
-    h->p2p = pe ? pe[0] == '1' : o->comm_kind == SFLSQR_COMM_LOCAL;
+    h->p2p = (kn & SFLSQR_KNOB_P2P_ON) ? true : (kn & SFLSQR_KNOB_P2P_OFF) ? false : o->comm_kind == SFLSQR_COMM_LOCAL;
     if (o->world > 8) h->p2p = false;
     if (!h->comm) {
       if (h->own_stream) cudaStreamDestroy(h->stream);
@@ -1839,32 +1720,17 @@ int sflsqr_create(sflsqr_t** out, const sflsqr_opts* o) {
       return fail(nullptr, SFLSQR_E_UNSUPPORTED, "communicator: %s", ce.c_str());
     }
   }
-  if (const char* ev = std::getenv("SFLSQR_SPMV_MODE")) h->spmv_mode = std::atoi(ev);
-  if (const char* ev = std::getenv("SFLSQR_PDL")) h->pdl = std::atoi(ev) != 0;
-  if (const char* ev = std::getenv("SFLSQR_SKETCH_SIDE")) h->sketch_side = std::atoi(ev) != 0;
-  if (const char* ev = std::getenv("SFLSQR_PCSR_INTERP")) h->pcsr_interp = std::atoi(ev) != 0;
-  if (const char* ev = std::getenv("SFLSQR_SELL")) h->sell = std::atoi(ev) != 0;
-  if (const char* ev = std::getenv("SFLSQR_SELL_A")) h->sell_a = std::atoi(ev) != 0;
-  if (const char* ev = std::getenv("SFLSQR_CGS_SELECTIVE")) h->cgs_selective = std::atoi(ev) != 0;
-  if (const char* ev = std::getenv("SFLSQR_SPMV_GRID_DELTA")) h->spmv_grid_delta = std::max(0, std::min(100, std::atoi(ev)));
-  if (const char* ev = std::getenv("SFLSQR_PCSR_UNROLL")) h->pcsr_unroll = std::atoi(ev) == 2 ? 2 : 4;
-  if (const char* ev = std::getenv("SFLSQR_LR_QR")) h->lr_qr_cgs = std::strcmp(ev, "cgs") == 0;
-  if (const char* ev = std::getenv("SFLSQR_RES_OVERLAP")) {
-    h->res_overlap = ev[0] != '0';
+  h->pdl = !(kn & SFLSQR_KNOB_NO_PDL);
+  h->sketch_side = !(kn & SFLSQR_KNOB_SKETCH_MAIN);
+  h->pcsr_interp = !(kn & SFLSQR_KNOB_NO_INTERP);
+  h->sell = !(kn & SFLSQR_KNOB_NO_SELL);
+  h->ell_c16 = !(kn & SFLSQR_KNOB_NO_ELL_C16);
+  h->cgs_selective = !(kn & SFLSQR_KNOB_CGS_ALWAYS2);
+  h->spmv_grid_delta = (kn & SFLSQR_KNOB_FULL_SPMV_GRID) ? 0 : 1;
+  h->keep_csr = (kn & SFLSQR_KNOB_KEEP_CSR) != 0;
+  if (kn & (SFLSQR_KNOB_RES_MAIN | SFLSQR_KNOB_RES_SIDE)) {
+    h->res_overlap = (kn & SFLSQR_KNOB_RES_SIDE) != 0;
     h->res_overlap_forced = h->res_overlap;
-  }
-  {
-    // co-resident blocks of the cooperative phase kernels (both kernels, 512 threads)
-    int nsm = 0, oz = 0, ow = 0;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, o->device);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oz, k_zphase, kCoopThreads, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ow, k_wphase, kCoopThreads, 0);
-    const int per = std::min(std::min(oz, ow), 2);
-    h->coop_grid = std::min(nsm * per, kVecBlocks);
-    // opt-in (SFLSQR_COOP=1): measured no faster than the standalone kernels
-    const char* nc = std::getenv("SFLSQR_COOP");
-    if (per < 1 || !(nc && nc[0] == '1')) h->coop_grid = 0;
-    cudaGetLastError();
   }
   if (cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
@@ -1876,7 +1742,6 @@ int sflsqr_create(sflsqr_t** out, const sflsqr_opts* o) {
   }
   cudaFuncSetAttribute(k_ls<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 4 * kLsThreads * (int)sizeof(double));
   cudaFuncSetAttribute(k_lr_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLrEigSmem);
-  cudaFuncSetAttribute(k_lr_qr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLrQrSmem);
   cudaFuncSetAttribute(k_lr_range, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * (int)sizeof(double));
   cudaGetLastError();
   *out = h;
@@ -1944,59 +1809,24 @@ int sflsqr_set_operator_shard(sflsqr_t* h, int64_t m, int64_t n, int64_t a_row0,
   int rc;
   if ((rc = validate_csr(h, "A", h->m_loc, n, a_rowptr, a_col, a_val))) return rc;
   if (t_mode == SFLSQR_T_GIVEN && (rc = validate_csr(h, "T", h->n_loc, m, t_rowptr, t_col, t_val))) return rc;
-  // ---- padded index maps (sharded): global index -> owner * max + local offset
-  auto pad_map = [&](const std::vector<int64_t>& st, int64_t mx, int64_t len) {
-    std::vector<int64_t> mp(len);
-    for (int g = 0; g < R; ++g)
-      for (int64_t j = st[g]; j < st[g + 1]; ++j) mp[j] = (int64_t)g * mx + (j - st[g]);
-    return mp;
-  };
-  const int64_t abase = a_rowptr[0], annz = a_rowptr[h->m_loc] - abase;
-  std::vector<int32_t> acol_re;
-  const int32_t* acol_up = a_col;
-  if (R > 1) {
-    const std::vector<int64_t> nmap = pad_map(nst, h->n_max, n);
-    acol_re.resize(annz);
-    par_for(annz, [&](int64_t s, int64_t e) {
-      for (int64_t p = s; p < e; ++p) acol_re[p] = (int32_t)nmap[a_col[abase + p]];
-    });
-    acol_up = acol_re.data() - abase;
-  }
-  if ((rc = upload_csr(h, h->m_loc, a_rowptr, acol_up, a_val, &h->a_rowptr, &h->a_col, &h->a_val, &h->nnz_a))) {
+  // ---- upload; sharded: the columns into the padded layout on the device (global index j of
+  // rank g's slice -> g * max + j - st[g]); T_BUILD: T = A^T of the local rows on the device
+  if ((rc = upload_csr(h, h->m_loc, a_rowptr, a_col, a_val, &h->a_rowptr, &h->a_col, &h->a_val, &h->nnz_a)) ||
+      (R > 1 && (rc = device_remap_cols(h, h->a_col, h->nnz_a, nst, h->n_max)))) {
     free_op(h);
     return rc;
   }
   h->a_owned = h->t_owned = true;
   if (t_mode == SFLSQR_T_GIVEN) {
-    const int64_t tbase = t_rowptr[0], tnnz = t_rowptr[h->n_loc] - tbase;
-    std::vector<int32_t> tcol_re;
-    const int32_t* tcol_up = t_col;
-    if (R > 1) {
-      const std::vector<int64_t> mmap = pad_map(mst, h->m_max, m);
-      tcol_re.resize(tnnz);
-      par_for(tnnz, [&](int64_t s, int64_t e) {
-        for (int64_t p = s; p < e; ++p) tcol_re[p] = (int32_t)mmap[t_col[tbase + p]];
-      });
-      tcol_up = tcol_re.data() - tbase;
-    }
     h->t_rows = h->n_loc;
-    rc = upload_csr(h, h->n_loc, t_rowptr, tcol_up, t_val, &h->t_rowptr, &h->t_col, &h->t_val, &h->nnz_t);
+    rc = upload_csr(h, h->n_loc, t_rowptr, t_col, t_val, &h->t_rowptr, &h->t_col, &h->t_val, &h->nnz_t);
+    if (!rc && R > 1) rc = device_remap_cols(h, h->t_col, h->nnz_t, mst, h->m_max);
   } else {
     // T = A^T of this rank's row block (COLSHARD when sharded: rows in the padded n layout)
-    std::vector<int64_t> trp;
-    std::vector<int32_t> tcol;
-    std::vector<double> tval;
-    std::vector<int64_t> nmap;
-    if (R > 1) {
-      nmap = pad_map(nst, h->n_max, n);
-      h->t_rows = (int64_t)R * h->n_max;
-      host_transpose(h->m_loc, n, a_rowptr, a_col, a_val, h->t_rows, &nmap, trp, tcol, tval);
-    } else {
-      h->t_rows = n;
-      host_transpose(h->m_loc, n, a_rowptr, a_col, a_val, n, nullptr, trp, tcol, tval);
-    }
-    rc = upload_csr(h, h->t_rows, trp.data(), tcol.data(), tval.data(), &h->t_rowptr, &h->t_col, &h->t_val,
-                    &h->nnz_t);
+    h->t_rows = R > 1 ? (int64_t)R * h->n_max : n;
+    h->nnz_t = h->nnz_a;
+    rc = device_transpose(h, h->m_loc, h->t_rows, h->a_rowptr, h->a_col, h->a_val, h->nnz_a, &h->t_rowptr, &h->t_col,
+                          &h->t_val);
   }
   if (rc || (rc = build_formats(h))) {
     free_op(h);
@@ -2017,7 +1847,6 @@ int sflsqr_set_operator(sflsqr_t* h, int64_t m, int64_t n, const int64_t* a_rowp
   const bool dev = (mem_flags & SFLSQR_MEM_DEVICE) != 0;
   const bool borrow = (mem_flags & SFLSQR_MEM_BORROW) != 0;
   if (borrow && !dev) return fail(h, SFLSQR_E_INVALID, "BORROW requires device pointers");
-  if (dev && t_mode == SFLSQR_T_BUILD) return fail(h, SFLSQR_E_INVALID, "T_BUILD requires host arrays");
   if (!dev) {
     if (!a_rowptr || !a_col || !a_val) return fail(h, SFLSQR_E_INVALID, "A: NULL array");
     if (a_rowptr[0] != 0) return fail(h, SFLSQR_E_DIM, "A: rowptr[0] != 0");
@@ -2027,15 +1856,16 @@ int sflsqr_set_operator(sflsqr_t* h, int64_t m, int64_t n, const int64_t* a_rowp
     }
     return sflsqr_set_operator_shard(h, m, n, 0, m, a_rowptr, a_col, a_val, t_mode, 0, n, t_rowptr, t_col, t_val);
   }
-  // device arrays (copied or borrowed; not validated)
-  if (!a_rowptr || !a_col || !a_val || !t_rowptr || !t_col || !t_val)
+  // device arrays (copied or borrowed; not validated); T_BUILD: T = A^T formed on the device
+  const bool build_t = t_mode == SFLSQR_T_BUILD;
+  if (!a_rowptr || !a_col || !a_val || (!build_t && (!t_rowptr || !t_col || !t_val)))
     return fail(h, SFLSQR_E_INVALID, "NULL device array");
   cudaSetDevice(h->o.device);
   free_solve(h);
   free_op(h);
-  int64_t nnz_a, nnz_t;
+  int64_t nnz_a, nnz_t = 0;
   CU(h, cudaMemcpy(&nnz_a, a_rowptr + m, sizeof(int64_t), cudaMemcpyDeviceToHost));
-  CU(h, cudaMemcpy(&nnz_t, t_rowptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost));
+  if (!build_t) CU(h, cudaMemcpy(&nnz_t, t_rowptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost));
   h->m = m;
   h->n = n;
   h->m0 = h->n0 = 0;
@@ -2046,26 +1876,40 @@ int sflsqr_set_operator(sflsqr_t* h, int64_t m, int64_t n, const int64_t* a_rowp
   h->nnz_a = nnz_a;
   h->nnz_t = nnz_t;
   int rc0;
+  const cudaMemcpyKind kd = cudaMemcpyDeviceToDevice;
   if (borrow) {
-    h->a_owned = h->t_owned = false;
+    h->a_owned = false;
     h->a_rowptr = (int64_t*)a_rowptr;
     h->a_col = (int32_t*)a_col;
     h->a_val = (double*)a_val;
+  } else {
+    h->a_owned = true;
+    if ((rc0 = upload(h, (void**)&h->a_rowptr, a_rowptr, sizeof(int64_t) * (m + 1), kd)) ||
+        (rc0 = upload(h, (void**)&h->a_col, a_col, sizeof(int32_t) * nnz_a, kd)) ||
+        (rc0 = upload(h, (void**)&h->a_val, a_val, sizeof(double) * nnz_a, kd))) {
+      free_op(h);
+      return rc0;
+    }
+  }
+  if (build_t) {
+    h->t_owned = true;
+    h->nnz_t = nnz_a;
+    if ((rc0 = device_transpose(h, m, n, h->a_rowptr, h->a_col, h->a_val, nnz_a, &h->t_rowptr, &h->t_col, &h->t_val))) {
+      free_op(h);
+      return rc0;
+    }
+  } else if (borrow) {
+    h->t_owned = false;
     h->t_rowptr = (int64_t*)t_rowptr;
     h->t_col = (int32_t*)t_col;
     h->t_val = (double*)t_val;
   } else {
-    h->a_owned = h->t_owned = true;
-    int rc;
-    const cudaMemcpyKind kd = cudaMemcpyDeviceToDevice;
-    if ((rc = upload(h, (void**)&h->a_rowptr, a_rowptr, sizeof(int64_t) * (m + 1), kd)) ||
-        (rc = upload(h, (void**)&h->a_col, a_col, sizeof(int32_t) * nnz_a, kd)) ||
-        (rc = upload(h, (void**)&h->a_val, a_val, sizeof(double) * nnz_a, kd)) ||
-        (rc = upload(h, (void**)&h->t_rowptr, t_rowptr, sizeof(int64_t) * (n + 1), kd)) ||
-        (rc = upload(h, (void**)&h->t_col, t_col, sizeof(int32_t) * nnz_t, kd)) ||
-        (rc = upload(h, (void**)&h->t_val, t_val, sizeof(double) * nnz_t, kd))) {
+    h->t_owned = true;
+    if ((rc0 = upload(h, (void**)&h->t_rowptr, t_rowptr, sizeof(int64_t) * (n + 1), kd)) ||
+        (rc0 = upload(h, (void**)&h->t_col, t_col, sizeof(int32_t) * nnz_t, kd)) ||
+        (rc0 = upload(h, (void**)&h->t_val, t_val, sizeof(double) * nnz_t, kd))) {
       free_op(h);
-      return rc;
+      return rc0;
     }
   }
   if ((rc0 = build_formats(h))) {
@@ -2416,8 +2260,10 @@ int sflsqr_get_info(sflsqr_t* h, sflsqr_info* info) {
   const int mode_t = h->spmv_mode >= 0 ? h->spmv_mode : (h->pt.ok ? 16 : 14);
   info->a_pairs = ((mode_a == 16 || mode_a == 17) && h->pa.ok) ? h->pa.npairs : 0;
   info->t_pairs = ((mode_t == 16 || mode_t == 17) && h->pt.ok) ? h->pt.npairs : 0;
-  info->a_fmt = info->a_pairs ? (h->pa.aligned ? 2 : (h->pa.f ? (h->pa.ecol ? 4 : 3) : 1)) : ((h->spmv_mode < 0 && h->ea.ok) ? 5 : 0);
-  info->t_fmt = info->t_pairs ? (h->pt.aligned ? 2 : (h->pt.f ? (h->pt.ecol ? 4 : 3) : 1)) : ((h->spmv_mode < 0 && h->et.ok) ? 5 : 0);
+  info->a_fmt = info->a_pairs ? (h->pa.aligned ? 2 : (h->pa.interp ? (h->pa.ell ? 4 : 3) : 1)) : 0;
+  info->t_fmt = info->t_pairs ? (h->pt.aligned ? 2 : (h->pt.interp ? (h->pt.ell ? 4 : 3) : 1)) : 0;
+  info->knobs = h->knobs;
+  info->csr_kept = (h->csr_freed_a ? 0 : 1) | (h->csr_freed_t ? 0 : 2);
   return SFLSQR_OK;
 }
 
@@ -2555,11 +2401,13 @@ int sflsqr_debug_state(sflsqr_t* h, double* z, double* x, double* p_ring, double
 
 int sflsqr_debug_set_tuning(sflsqr_t* h, int32_t spmv_mode, int32_t band_shift) {
   if (!h) return fail(nullptr, SFLSQR_E_INVALID, "NULL handle");
-  const bool ok_mode = spmv_mode == -1 || spmv_mode == 0 || spmv_mode == 1 || spmv_mode == 2 || spmv_mode == 3 ||
-                       spmv_mode == 8 || (spmv_mode >= 10 && spmv_mode <= 17);
-  if (!ok_mode || band_shift < 8 || band_shift > 30) return fail(h, SFLSQR_E_INVALID, "bad tuning values");
+  (void)band_shift;
+  const bool ok_mode = spmv_mode == -1 || spmv_mode == 14 || spmv_mode == 16 || spmv_mode == 17;
+  if (!ok_mode) return fail(h, SFLSQR_E_INVALID, "bad tuning values");
+  if (spmv_mode >= 0 && (h->csr_freed_a || h->csr_freed_t))
+    return fail(h, SFLSQR_E_STATE, "the operator's CSR was released after its format copy was built: "
+                                   "create the handle with SFLSQR_KNOB_KEEP_CSR to force an SpMV format");
   h->spmv_mode = spmv_mode;
-  h->band_shift = band_shift;
   if (h->op_set) {
     int rc = build_formats(h);
     if (rc) return rc;

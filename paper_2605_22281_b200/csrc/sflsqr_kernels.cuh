@@ -14,7 +14,6 @@ namespace sfl {
 
 constexpr int kVecThreads = 256;          // vector kernels
 constexpr int kVecBlocks = 148 * 4;       // 4 CTAs per SM on 148 SMs, grid-stride
-constexpr int kSpmvThreads = 256;         // 8 warps, one row per warp at a time
 constexpr int kSkThreads = 256;           // sketch kernel: 8 warps, one d-bin set per warp
 constexpr int kSkBlocks = 148 * 2;
 constexpr int kLsThreads = 512;           // one CTA solves the projected problem
@@ -53,7 +52,7 @@ struct Params {
   double* scal;            // per-slot global scalars (dist)
   double* skbuf;           // d: S v of the current vector (allreduced when dist)
   double *zsend, *wsend;   // dist: fixed-address copies of z_k / w_{k+1} for the allgathers
-  // dist, peer-memory collectives (SFLSQR_P2P): z_k / w_{k+1} are stored straight into every
+  // dist, peer-memory collectives (SFLSQR_KNOB_P2P_ON): z_k / w_{k+1} are stored straight into every
   // rank's gathered buffer, the COLSHARD T product straight into its owner's receive slots
   int p2p_z, p2p_w, rank_id;
   int64_t n_max_p, m_max_p;
@@ -74,7 +73,6 @@ struct Params {
   int cgs_selective;        // CGS2: skip the second pass when ||v'|| >= ||v|| / sqrt(2) (one rank)
   int slot_zf, slot_zout, slot_wf, slot_wout;  // fused orthogonalisation slots (kFuseAcc + 1 per side)
   int* ctr;                // last-block arrival counters (one per reduction site)
-  unsigned int* bar;       // grid barrier of the cooperative phase kernels (count, generation)
   double *cpart, *cscal;   // CGS2: (ell + 2) x kVecBlocks dot partials; 2 stages x ldc reduced dots
   int ldc;                 // ell + 2
   // textbook LSQR / LSMR (methods 4 / 5): u' = P.w (m, unnormalised), v = P.z (n), x = P.x,
@@ -111,6 +109,23 @@ __device__ __forceinline__ double warp_max(double v) {
 }
 
 // Deterministic block sum, result returned to every thread. sh: >= 33 doubles.
+// Fixed-order warp sum of nb per-block partials pp[0 .. nb): four independent partial sums per lane
+// (the L2 loads overlap instead of one latency per 32 blocks), combined in a fixed order, then the
+// shuffle tree.  Deterministic for a given nb; every lane gets the sum.
+__device__ __forceinline__ double warp_sum_partials(const double* pp, int nb, int lane) {
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int b = lane;
+  for (; b + 96 < nb; b += 128) {
+    const double v0 = __ldcg(pp + b), v1 = __ldcg(pp + b + 32), v2 = __ldcg(pp + b + 64), v3 = __ldcg(pp + b + 96);
+    a0 += v0;
+    a1 += v1;
+    a2 += v2;
+    a3 += v3;
+  }
+  for (; b < nb; b += 32) a0 += __ldcg(pp + b);
+  return warp_sum((a0 + a1) + (a2 + a3));
+}
+
 template <int NT>
 __device__ __forceinline__ double block_sum(double v, double* sh) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -190,11 +205,23 @@ __device__ __forceinline__ bool last_block_reduce(const Params& P, int s0, int n
   const int nb = gridDim.x;
   for (int t = wid; t < ns; t += nw) {
     const double* pp = P.part + (size_t)(s0 + t) * kVecBlocks;
-    double acc = is_max ? -INFINITY : 0.0;
-    for (int b = lane; b < nb; b += 32) {
-      const double v = __ldcg(pp + b);
-      acc = is_max ? fmax(acc, v) : acc + v;
+    // four independent partial sums per lane (the L2 loads overlap instead of one latency per
+    // 32 blocks), combined in a fixed order: deterministic for a given grid
+    const double id = is_max ? -INFINITY : 0.0;
+    double a0 = id, a1 = id, a2 = id, a3 = id;
+    int b = lane;
+    for (; b + 96 < nb; b += 128) {
+      const double v0 = __ldcg(pp + b), v1 = __ldcg(pp + b + 32), v2 = __ldcg(pp + b + 64), v3 = __ldcg(pp + b + 96);
+      a0 = is_max ? fmax(a0, v0) : a0 + v0;
+      a1 = is_max ? fmax(a1, v1) : a1 + v1;
+      a2 = is_max ? fmax(a2, v2) : a2 + v2;
+      a3 = is_max ? fmax(a3, v3) : a3 + v3;
     }
+    for (; b < nb; b += 32) {
+      const double v = __ldcg(pp + b);
+      a0 = is_max ? fmax(a0, v) : a0 + v;
+    }
+    double acc = is_max ? fmax(fmax(a0, a1), fmax(a2, a3)) : (a0 + a1) + (a2 + a3);
     acc = is_max ? warp_max(acc) : warp_sum(acc);
     if (lane == 0) P.scal[s0 + t] = acc;
   }
@@ -334,105 +361,6 @@ __device__ __forceinline__ const double* kvec(const DevState* st, const double* 
 }
 __device__ __forceinline__ double* kvec_w(const DevState* st, double* base, int64_t ld, int koff) {
   return ld ? base + ld * (int64_t)(st->k + koff) : base;
-}
-
-__global__ void __launch_bounds__(kSpmvThreads) k_spmv_csr(const DevState* st, int64_t nrows,
-                                                           const int64_t* __restrict__ rowptr,
-                                                           const int* __restrict__ col,
-                                                           const double* __restrict__ val,
-                                                           const double* __restrict__ x_base, int64_t x_ld,
-                                                           int x_koff, double* __restrict__ y) {
-  if (st && st->done) return;
-  const double* __restrict__ x = kvec(st, x_base, x_ld, x_koff);
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  constexpr int WPB = kSpmvThreads / 32;
-  for (int64_t row = (int64_t)blockIdx.x * WPB + wid; row < nrows; row += (int64_t)gridDim.x * WPB) {
-    const int64_t s = rowptr[row], e = rowptr[row + 1];
-    int64_t a = (s + 3) & ~(int64_t)3;
-    if (a > e) a = e;
-    double sum = 0.0;
-    if (s + lane < a) {
-      const int64_t p = s + lane;
-      sum = fma(ld_stream_d(val + p), __ldg(x + ld_stream_i(col + p)), sum);
-    }
-    const int64_t nq = (e - a) >> 2;
-    const int4* c4 = reinterpret_cast<const int4*>(col + a);
-    const double2* v2 = reinterpret_cast<const double2*>(val + a);
-    int64_t q = lane;
-    for (; q + 32 < nq; q += 64) {
-      const int4 ca = ld_stream_i4(c4 + q);
-      const int4 cb = ld_stream_i4(c4 + q + 32);
-      const double2 va0 = ld_stream_d2(v2 + 2 * q), va1 = ld_stream_d2(v2 + 2 * q + 1);
-      const double2 vb0 = ld_stream_d2(v2 + 2 * (q + 32)), vb1 = ld_stream_d2(v2 + 2 * (q + 32) + 1);
-      const double xa0 = __ldg(x + ca.x), xa1 = __ldg(x + ca.y), xa2 = __ldg(x + ca.z), xa3 = __ldg(x + ca.w);
-      const double xb0 = __ldg(x + cb.x), xb1 = __ldg(x + cb.y), xb2 = __ldg(x + cb.z), xb3 = __ldg(x + cb.w);
-      sum = fma(va0.x, xa0, sum);
-      sum = fma(va0.y, xa1, sum);
-      sum = fma(va1.x, xa2, sum);
-      sum = fma(va1.y, xa3, sum);
-      sum = fma(vb0.x, xb0, sum);
-      sum = fma(vb0.y, xb1, sum);
-      sum = fma(vb1.x, xb2, sum);
-      sum = fma(vb1.y, xb3, sum);
-    }
-    if (q < nq) {
-      const int4 ca = ld_stream_i4(c4 + q);
-      const double2 va0 = ld_stream_d2(v2 + 2 * q), va1 = ld_stream_d2(v2 + 2 * q + 1);
-      sum = fma(va0.x, __ldg(x + ca.x), sum);
-      sum = fma(va0.y, __ldg(x + ca.y), sum);
-      sum = fma(va1.x, __ldg(x + ca.z), sum);
-      sum = fma(va1.y, __ldg(x + ca.w), sum);
-    }
-    const int64_t t0 = a + 4 * nq;
-    if (t0 + lane < e) {
-      const int64_t p = t0 + lane;
-      sum = fma(ld_stream_d(val + p), __ldg(x + ld_stream_i(col + p)), sum);
-    }
-    sum = warp_sum(sum);
-    if (lane == 0) y[row] = sum;
-  }
-}
-
-// Row-group CSR SpMV (default).  Each CTA owns WPB consecutive rows at a time
-// (one warp per row; adjacent rays / adjacent pixels, so their gathered x lines
-// overlap and are served from L1), grid-stride over row groups.  Within a row the
-// entries are consumed in order in lane-strided chunks (lane L takes element
-// p + L, so one gather instruction touches consecutive entries of the row and the
-// column / value streams are fully coalesced), UNR chunks in flight per warp.
-// Summation order is fixed (per-lane FMA chain, then a shuffle tree): deterministic.
-template <int WPB, int UNR>
-__global__ void __launch_bounds__(WPB * 32, 2048 / (WPB * 32)) k_spmv_csr_rows(const DevState* st, int64_t nrows,
-                                                            const int64_t* __restrict__ rowptr,
-                                                            const int* __restrict__ col,
-                                                            const double* __restrict__ val,
-                                                            const double* __restrict__ x_base, int64_t x_ld,
-                                                            int x_koff, double* __restrict__ y) {
-  if (st && st->done) return;
-  const double* __restrict__ x = kvec(st, x_base, x_ld, x_koff);
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int64_t r0 = (int64_t)blockIdx.x * WPB; r0 < nrows; r0 += (int64_t)gridDim.x * WPB) {
-    const int64_t row = r0 + wid;
-    double sum = 0.0;
-    if (row < nrows) {
-      const int64_t s = rowptr[row], e = rowptr[row + 1];
-      int64_t p = s + lane;
-      for (; p + 32 * (UNR - 1) < e; p += 32 * UNR) {
-        int c[UNR];
-        double v[UNR], xv[UNR];
-#pragma unroll
-        for (int u = 0; u < UNR; ++u) c[u] = ld_stream_i(col + p + 32 * u);
-#pragma unroll
-        for (int u = 0; u < UNR; ++u) v[u] = ld_stream_d(val + p + 32 * u);
-#pragma unroll
-        for (int u = 0; u < UNR; ++u) xv[u] = __ldg(x + c[u]);
-#pragma unroll
-        for (int u = 0; u < UNR; ++u) sum = fma(v[u], xv[u], sum);
-      }
-      for (; p < e; p += 32) sum = fma(ld_stream_d(val + p), __ldg(x + ld_stream_i(col + p)), sum);
-      sum = warp_sum(sum);
-      if (lane == 0) y[row] = sum;
-    }
-  }
 }
 
 // Variant: software-pipelined row-group SpMV — the column indices and values of
@@ -724,10 +652,18 @@ __global__ void __launch_bounds__(256) k_pcsr_interp(int64_t npairs, const doubl
 // touches one or two lines instead of 32.  Each lane sums its own row in k order (deterministic).
 // Interpolation pairs only (values 1 - f, f); singletons of the row (if any) from the singleton CSR.
 constexpr int kSellC = 32;
+__device__ __forceinline__ int ld_stream_u16(const uint16_t* p) {
+  unsigned short r;
+  asm volatile("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=h"(r) : "l"(p));
+  return (int)r;
+}
 // EPI: the fused epilogues of k_spmv_csr_pf (GKB kinds 1-3, peer reduce-scatter kind 4).
-template <int UNR, bool EPI = false>
+// C16: the column of entry k of a slice is ebase[soff / 32 + k] + eoff[entry] (scol = ebase then);
+// the same operator, 2 + 4/32 instead of 4 bytes of column per pair.
+template <int UNR, bool EPI = false, bool C16 = false>
 __global__ void __launch_bounds__(512, 2) k_spmv_sell_ip(const DevState* st, int64_t nrows, const int64_t* __restrict__ soff,
                                                        const int* __restrict__ rcnt, const int* __restrict__ scol,
+                                                       const uint16_t* __restrict__ eoff,
                                                        const double* __restrict__ sf, const int64_t* __restrict__ srp,
                                                        const int* __restrict__ s1col, const double* __restrict__ s1val,
                                                        const double* __restrict__ x_base, int64_t x_ld, int x_koff,
@@ -746,12 +682,20 @@ __global__ void __launch_bounds__(512, 2) k_spmv_sell_ip(const DevState* st, int
     const int cnt = row < nrows ? rcnt[row] : 0;
     const int L = __reduce_max_sync(0xffffffffu, cnt);
     const int64_t base = soff[sl] + lane;
+    const int* __restrict__ eb = scol + soff[sl] / kSellC;  // C16: the slice's entry bases
+    // the column loads of the next UNR entries are issued one iteration ahead; with C16 the base
+    // and the offset stay separate registers until the gather (adding them at the prefetch would
+    // wait for both loads there)
+    auto col_ld = [&](int kk) -> int {
+      return C16 ? ld_stream_u16(eoff + base + (int64_t)kSellC * kk) : ld_stream_i(scol + base + (int64_t)kSellC * kk);
+    };
     double sum = 0.0;
-    int cn[UNR];
+    int cn[UNR], bn[UNR];
     double fn[UNR];
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
-      cn[u] = u < cnt ? ld_stream_i(scol + base + (int64_t)kSellC * u) : 0;
+      cn[u] = u < cnt ? col_ld(u) : 0;
+      bn[u] = (C16 && u < cnt) ? __ldg(eb + u) : 0;
       fn[u] = u < cnt ? ld_stream_d(sf + base + (int64_t)kSellC * u) : 0.0;
     }
     for (int k = 0; k < L; k += UNR) {
@@ -759,13 +703,14 @@ __global__ void __launch_bounds__(512, 2) k_spmv_sell_ip(const DevState* st, int
       double fv[UNR];
 #pragma unroll
       for (int u = 0; u < UNR; ++u) {
-        c[u] = cn[u];
+        c[u] = C16 ? bn[u] + cn[u] : cn[u];
         fv[u] = fn[u];
       }
 #pragma unroll
       for (int u = 0; u < UNR; ++u) {
         const int kk = k + UNR + u;
-        cn[u] = kk < cnt ? ld_stream_i(scol + base + (int64_t)kSellC * kk) : 0;
+        cn[u] = kk < cnt ? col_ld(kk) : 0;
+        if (C16) bn[u] = kk < cnt ? __ldg(eb + kk) : 0;
         fn[u] = kk < cnt ? ld_stream_d(sf + base + (int64_t)kSellC * kk) : 0.0;
       }
       double x0[UNR], x1[UNR];
@@ -815,57 +760,6 @@ __global__ void __launch_bounds__(512, 2) k_spmv_sell_ip(const DevState* st, int
   }
 }
 
-// Plain-CSR sliced ELL (same layout, one value per entry): for the Siddon A, lane = ray and the
-// 32 rays of a slice are neighbouring bins of one angle, so their k-th crossed pixels are close.
-template <int UNR>
-__global__ void __launch_bounds__(512, 2) k_spmv_sell_csr(const DevState* st, int64_t nrows, const int64_t* __restrict__ soff,
-                                                        const int* __restrict__ rcnt, const int* __restrict__ ecol,
-                                                        const double* __restrict__ ev, const double* __restrict__ x_base,
-                                                        int64_t x_ld, int x_koff, double* y) {
-  if (st && st->done) return;
-  const double* __restrict__ x = kvec(st, x_base, x_ld, x_koff);
-  const int lane = threadIdx.x & 31;
-  const int64_t nslices = (nrows + kSellC - 1) / kSellC;
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t sl = gw; sl < nslices; sl += nw) {
-    const int64_t row = sl * kSellC + lane;
-    const int cnt = row < nrows ? rcnt[row] : 0;
-    const int L = __reduce_max_sync(0xffffffffu, cnt);
-    const int64_t base = soff[sl] + lane;
-    double sum = 0.0;
-    int cn[UNR];
-    double vn[UNR];
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      cn[u] = u < cnt ? ld_stream_i(ecol + base + (int64_t)kSellC * u) : 0;
-      vn[u] = u < cnt ? ld_stream_d(ev + base + (int64_t)kSellC * u) : 0.0;
-    }
-    for (int k = 0; k < L; k += UNR) {
-      int c[UNR];
-      double v[UNR];
-#pragma unroll
-      for (int u = 0; u < UNR; ++u) {
-        c[u] = cn[u];
-        v[u] = vn[u];
-      }
-#pragma unroll
-      for (int u = 0; u < UNR; ++u) {
-        const int kk = k + UNR + u;
-        cn[u] = kk < cnt ? ld_stream_i(ecol + base + (int64_t)kSellC * kk) : 0;
-        vn[u] = kk < cnt ? ld_stream_d(ev + base + (int64_t)kSellC * kk) : 0.0;
-      }
-      double xv[UNR];
-#pragma unroll
-      for (int u = 0; u < UNR; ++u) xv[u] = (k + u < cnt) ? __ldg(x + c[u]) : 0.0;
-#pragma unroll
-      for (int u = 0; u < UNR; ++u)
-        if (k + u < cnt) sum = fma(v[u], xv[u], sum);
-    }
-    if (row < nrows) y[row] = sum;
-  }
-}
-
 // Sliced-ELL build from an interpolation pair-CSR copy: thread per row scatters its pairs.
 __global__ void __launch_bounds__(256) k_sell_fill(int64_t nrows, const int64_t* __restrict__ prp,
                                                    const int* __restrict__ pcol, const double* __restrict__ pf,
@@ -881,6 +775,129 @@ __global__ void __launch_bounds__(256) k_sell_fill(int64_t nrows, const int64_t*
   }
 }
 
+// 16-bit column offsets of a sliced-ELL copy (warp per slice): ebase[soff/32 + k] = the smallest
+// column of entry k over the slice's rows, eoff = column - base; flag = 1 when an entry spans
+// >= 65536 columns (the 32-bit columns then stay).
+__global__ void __launch_bounds__(256) k_sell_c16(int64_t nrows, const int64_t* __restrict__ soff,
+                                                  const int* __restrict__ rcnt, const int* __restrict__ ecol,
+                                                  int* __restrict__ ebase, uint16_t* __restrict__ eoff, int* flag) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nsl = (nrows + kSellC - 1) / kSellC;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t sl = gw; sl < nsl; sl += nw) {
+    const int64_t row = sl * kSellC + lane;
+    const int cnt = row < nrows ? rcnt[row] : 0;
+    const int L = __reduce_max_sync(0xffffffffu, cnt);
+    for (int k = 0; k < L; ++k) {
+      const int64_t e = soff[sl] + (int64_t)kSellC * k + lane;
+      const bool ok = k < cnt;
+      const int c = ok ? ecol[e] : 0;
+      const unsigned mn = __reduce_min_sync(0xffffffffu, ok ? (unsigned)c : 0xffffffffu);
+      const unsigned mx = __reduce_max_sync(0xffffffffu, ok ? (unsigned)c : 0u);
+      if (lane == 0) {
+        ebase[soff[sl] / kSellC + k] = (int)mn;
+        if (mx - mn > 65535u) atomicExch(flag, 1);
+      }
+      eoff[e] = ok ? (uint16_t)((unsigned)c - mn) : (uint16_t)0;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ operator setup: T = A^T on the device
+// (T_BUILD; the COLSHARD transpose is the transpose of the local A rows, no
+// communication).  A counting sort by column: per-column counts (atomics, order-free), an exclusive
+// scan (cub), a fill through per-column atomic cursors (arbitrary order inside a T row), then every
+// T row sorted by (A row, value bits) -- the order a sequential transpose produces (rows increasing),
+// so the built operator and every product on it are the same bits run to run.
+__global__ void __launch_bounds__(256) k_tr_count(int64_t nnz, const int* __restrict__ col,
+                                                  unsigned long long* __restrict__ cnt) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(cnt + col[p], 1ull);
+}
+
+// warp per A row: entry (i, c) goes to T row c at trp[c] + cursor[c]++
+__global__ void __launch_bounds__(256) k_tr_fill(int64_t nrows, const int64_t* __restrict__ rp,
+                                                 const int* __restrict__ col, const double* __restrict__ val,
+                                                 const int64_t* __restrict__ trp, unsigned long long* __restrict__ cur,
+                                                 int* __restrict__ tcol, double* __restrict__ tval) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = gw; i < nrows; i += nw)
+    for (int64_t p = rp[i] + lane; p < rp[i + 1]; p += 32) {
+      const int c = col[p];
+      const int64_t q = trp[c] + (int64_t)atomicAdd(cur + c, 1ull);
+      tcol[q] = (int)i;
+      tval[q] = val[p];
+    }
+}
+
+// (row, value bits) order of two entries
+__device__ __forceinline__ bool tr_less(int ra, unsigned long long va, int rb, unsigned long long vb) {
+  return ra < rb || (ra == rb && va < vb);
+}
+
+// One CTA per T row: bitonic sort of the row's entries in shared memory (rows of <= kTrSortMax
+// entries; longer rows set *long_rows and are sorted by the segmented-sort fallback).
+constexpr int kTrSortMax = 4096;
+constexpr size_t kTrSortSmem = (size_t)kTrSortMax * (sizeof(int) + sizeof(unsigned long long));
+__global__ void __launch_bounds__(256) k_tr_sort(int64_t tnrows, const int64_t* __restrict__ trp, int* __restrict__ tcol,
+                                                 double* __restrict__ tval, int* long_rows) {
+  extern __shared__ unsigned long long trs[];
+  unsigned long long* sv = trs;                                   // value bits
+  int* sr = reinterpret_cast<int*>(trs + kTrSortMax);             // A rows
+  for (int64_t r = blockIdx.x; r < tnrows; r += gridDim.x) {
+    const int64_t b = trp[r];
+    const int L = (int)(trp[r + 1] - b);
+    if (L <= 1) continue;
+    if (L > kTrSortMax) {
+      if (threadIdx.x == 0) atomicExch(long_rows, 1);
+      continue;
+    }
+    int n2 = 1;
+    while (n2 < L) n2 <<= 1;
+    for (int t = threadIdx.x; t < n2; t += blockDim.x) {
+      sr[t] = t < L ? tcol[b + t] : INT_MAX;
+      sv[t] = t < L ? (unsigned long long)__double_as_longlong(tval[b + t]) : ~0ull;
+    }
+    __syncthreads();
+    for (int size = 2; size <= n2; size <<= 1)
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int t = threadIdx.x; t < n2 / 2; t += blockDim.x) {
+          const int lo = 2 * t - (t & (stride - 1)), hi = lo + stride;
+          const bool up = (lo & size) == 0;
+          if (tr_less(sr[hi], sv[hi], sr[lo], sv[lo]) == up) {
+            const int rr = sr[lo];
+            sr[lo] = sr[hi];
+            sr[hi] = rr;
+            const unsigned long long vv = sv[lo];
+            sv[lo] = sv[hi];
+            sv[hi] = vv;
+          }
+        }
+        __syncthreads();
+      }
+    for (int t = threadIdx.x; t < L; t += blockDim.x) {
+      tcol[b + t] = sr[t];
+      tval[b + t] = __longlong_as_double((long long)sv[t]);
+    }
+    __syncthreads();
+  }
+}
+
+// Column remap of a sharded operator into the padded layout: global index j owned by rank g
+// (st[g] <= j < st[g+1]) -> g * mx + (j - st[g]).
+__global__ void __launch_bounds__(256) k_remap_cols(int64_t nnz, int* __restrict__ col, const int64_t* __restrict__ st,
+                                                    int world, int64_t mx) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = col[p];
+    int g = 0;
+    while (g + 1 < world && j >= st[g + 1]) ++g;
+    col[p] = (int)((int64_t)g * mx + (j - st[g]));
+  }
+}
+
 // Slice lengths (max pair count of the slice's rows) x kSellC -> sl_len.
 __global__ void __launch_bounds__(256) k_sell_len(int64_t nrows, const int64_t* __restrict__ prp, int64_t* sl_len) {
   const int64_t nslices = (nrows + kSellC - 1) / kSellC;
@@ -888,170 +905,6 @@ __global__ void __launch_bounds__(256) k_sell_len(int64_t nrows, const int64_t* 
     int64_t mx = 0;
     for (int64_t r = sl * kSellC; r < min(nrows, (sl + 1) * kSellC); ++r) mx = max(mx, prp[r + 1] - prp[r]);
     sl_len[sl] = mx * kSellC;
-  }
-}
-
-// ------------------------------------------------------------------ a3 / a6: CSR-16 (compressed column indices)
-// Same traversal as k_spmv_csr_pf<WPB, UNR, 16> (half-warp rows, 16-entry lane-strided
-// chunks, next UNR chunks prefetched), but the int32 column index of entry q of row i
-// is stored as a 16-bit offset from a per-chunk base:
-//     col[q] = cbase[cptr[i] + (q - rowptr[i]) / 16] + off[q]
-// (chunks of 16 consecutive entries of a row, aligned to the row start; cptr[i] = number
-// of chunks of rows < i).  10.25 instead of 12 bytes per nonzero are streamed; the
-// gathered x, the summation order and therefore the result are bit-identical to the
-// int32 CSR kernels.  Built on the device from the CSR (k_c16_count / k_c16_fill) when
-// every chunk's column range fits 16 bits (always for the CT operators).
-__device__ __forceinline__ int ld_stream_u16(const uint16_t* p) {
-  unsigned short r;
-  asm volatile("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=h"(r) : "l"(p));
-  return (int)r;
-}
-
-template <int WPB, int UNR>
-__global__ void __launch_bounds__(WPB * 32, 2048 / (WPB * 32)) k_spmv_c16(const DevState* st, int64_t nrows,
-                                                            const int64_t* __restrict__ rowptr,
-                                                            const int64_t* __restrict__ cptr,
-                                                            const int* __restrict__ cbase,
-                                                            const uint16_t* __restrict__ off,
-                                                            const double* __restrict__ val,
-                                                            const double* __restrict__ x_base, int64_t x_ld,
-                                                            int x_koff, double* __restrict__ y) {
-  if (st && st->done) return;
-  const double* __restrict__ x = kvec(st, x_base, x_ld, x_koff);
-  constexpr int LANES = 16, RPW = 2;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int sl = lane % LANES, sub = lane / LANES;
-  for (int64_t r0 = (int64_t)blockIdx.x * WPB * RPW; r0 < nrows; r0 += (int64_t)gridDim.x * WPB * RPW) {
-    const int64_t row = r0 + (int64_t)wid * RPW + sub;
-    int64_t s = 0, e = 0;
-    const int* cb = cbase;
-    if (row < nrows) {
-      s = rowptr[row];
-      e = rowptr[row + 1];
-      cb = cbase + cptr[row];
-    }
-    double sum = 0.0;
-    int64_t p = s + sl;
-    int ch = 0;  // chunk of p within the row
-    int cn[UNR];
-    double vn[UNR];
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      const int64_t q = p + (int64_t)LANES * u;
-      cn[u] = q < e ? __ldg(cb + ch + u) + ld_stream_u16(off + q) : 0;
-      vn[u] = q < e ? ld_stream_d(val + q) : 0.0;
-    }
-    while (__any_sync(0xffffffffu, p < e)) {
-      int c[UNR];
-      double v[UNR];
-#pragma unroll
-      for (int u = 0; u < UNR; ++u) {
-        c[u] = cn[u];
-        v[u] = vn[u];
-      }
-      const int64_t pn = p + (int64_t)LANES * UNR;
-      const int chn = ch + UNR;
-#pragma unroll
-      for (int u = 0; u < UNR; ++u) {
-        const int64_t q = pn + (int64_t)LANES * u;
-        cn[u] = q < e ? __ldg(cb + chn + u) + ld_stream_u16(off + q) : 0;
-        vn[u] = q < e ? ld_stream_d(val + q) : 0.0;
-      }
-      double xv[UNR];
-#pragma unroll
-      for (int u = 0; u < UNR; ++u) xv[u] = (p + (int64_t)LANES * u < e) ? __ldg(x + c[u]) : 0.0;
-#pragma unroll
-      for (int u = 0; u < UNR; ++u)
-        if (p + (int64_t)LANES * u < e) sum = fma(v[u], xv[u], sum);
-      p = pn;
-      ch = chn;
-    }
-#pragma unroll
-    for (int o = LANES / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    if (sl == 0 && row < nrows) y[row] = sum;
-  }
-}
-
-// CSR-16 construction: chunks per row, then (after an exclusive scan into cptr) the
-// per-chunk minimum column as base and the 16-bit offsets; *overflow = 1 if a chunk's
-// column range exceeds 65535 (the operator then stays in int32 CSR).
-__global__ void k_c16_count(int64_t nrows, const int64_t* __restrict__ rowptr, int64_t* __restrict__ cnt) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= nrows; i += (int64_t)gridDim.x * blockDim.x)
-    cnt[i] = i < nrows ? (rowptr[i + 1] - rowptr[i] + 15) / 16 : 0;
-}
-__global__ void k_c16_fill(int64_t nrows, const int64_t* __restrict__ rowptr, const int* __restrict__ col,
-                           const int64_t* __restrict__ cptr, int* __restrict__ cbase, uint16_t* __restrict__ off,
-                           int* overflow) {
-  const int lane = threadIdx.x & 31, sl = lane & 15;
-  const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;   // warp: rows 2wg, 2wg+1
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t r0 = 2 * wg; r0 < nrows; r0 += 2 * nw) {
-    const int64_t row = r0 + (lane >> 4);
-    const bool valid = row < nrows;
-    const int64_t s = valid ? rowptr[row] : 0, e = valid ? rowptr[row + 1] : 0;
-    const int64_t nch = (e - s + 15) / 16;
-    const int64_t c0 = valid ? cptr[row] : 0;
-    // both half-warps loop to the larger chunk count (shuffles need the full warp)
-    const int64_t other = __shfl_xor_sync(0xffffffffu, nch, 16);
-    const int64_t nmax = nch > other ? nch : other;
-    for (int64_t ch = 0; ch < nmax; ++ch) {
-      const int64_t q = s + ch * 16 + sl;
-      const bool in = ch < nch && q < e;
-      const int c = in ? col[q] : 0;
-      int mn = in ? c : INT_MAX, mx = in ? c : INT_MIN;
-#pragma unroll
-      for (int o = 8; o > 0; o >>= 1) {
-        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      }
-      if (ch < nch) {
-        if (sl == 0) {
-          cbase[c0 + ch] = mn;
-          if ((int64_t)mx - (int64_t)mn > 65535) *overflow = 1;
-        }
-        if (in) off[q] = (uint16_t)(c - mn);
-      }
-    }
-  }
-}
-
-// Variant: half-warp per row (2 rows per warp, 2*WPB adjacent rows per CTA).
-template <int WPB, int UNR>
-__global__ void __launch_bounds__(WPB * 32, 2048 / (WPB * 32)) k_spmv_csr_half(const DevState* st, int64_t nrows,
-                                                            const int64_t* __restrict__ rowptr,
-                                                            const int* __restrict__ col,
-                                                            const double* __restrict__ val,
-                                                            const double* __restrict__ x_base, int64_t x_ld,
-                                                            int x_koff, double* __restrict__ y) {
-  if (st && st->done) return;
-  const double* __restrict__ x = kvec(st, x_base, x_ld, x_koff);
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int hl = lane & 15, half = lane >> 4;
-  for (int64_t r0 = (int64_t)blockIdx.x * 2 * WPB; r0 < nrows; r0 += (int64_t)gridDim.x * 2 * WPB) {
-    const int64_t row = r0 + 2 * wid + half;
-    int64_t s = 0, e = 0;
-    if (row < nrows) {
-      s = rowptr[row];
-      e = rowptr[row + 1];
-    }
-    double sum = 0.0;
-    int64_t p = s + hl;
-    for (; p + 16 * (UNR - 1) < e; p += 16 * UNR) {
-      int c[UNR];
-      double v[UNR], xv[UNR];
-#pragma unroll
-      for (int u = 0; u < UNR; ++u) c[u] = ld_stream_i(col + p + 16 * u);
-#pragma unroll
-      for (int u = 0; u < UNR; ++u) v[u] = ld_stream_d(val + p + 16 * u);
-#pragma unroll
-      for (int u = 0; u < UNR; ++u) xv[u] = __ldg(x + c[u]);
-#pragma unroll
-      for (int u = 0; u < UNR; ++u) sum = fma(v[u], xv[u], sum);
-    }
-    for (; p < e; p += 16) sum = fma(ld_stream_d(val + p), __ldg(x + ld_stream_i(col + p)), sum);
-#pragma unroll
-    for (int o = 8; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    if (hl == 0 && row < nrows) y[row] = sum;
   }
 }
 
@@ -1292,8 +1145,7 @@ __global__ void __launch_bounds__(kVecThreads) k_mgs_pass(Params P, int side, in
 template <int JM>
 __device__ __forceinline__ int gram_idx(int i, int j) { return 1 + JM + j * (j - 1) / 2 + i; }
 
-// Block-level bodies (NT threads), shared by the standalone kernels below and the
-// cooperative phase kernels (k_zphase / k_wphase).
+// Block-level bodies (NT threads) of the standalone kernels below.
 // Dots + Gram: block partials of ||v||^2, <q_j, v>, <q_i, q_j> into part[base + a][blockIdx].
 template <int NT>
 __device__ __forceinline__ void orth_dots_block(const Params& P, int side, int J, int j0, int base) {
@@ -1519,10 +1371,7 @@ __global__ void __launch_bounds__(kVecThreads) k_cgs_dots(Params P, int side, in
   __threadfence();
   double* out = P.cscal + (size_t)stage * P.ldc;
   for (int j = wid; j < ns; j += kVecThreads / 32) {
-    const double* pp = P.cpart + (size_t)j * kVecBlocks;
-    double a = 0.0;
-    for (int b = lane; b < nb; b += 32) a += __ldcg(pp + b);
-    a = warp_sum(a);
+    const double a = warp_sum_partials(P.cpart + (size_t)j * kVecBlocks, nb, lane);
     if (lane == 0) out[j] = a;
   }
   __syncthreads();
@@ -1715,57 +1564,6 @@ __global__ void __launch_bounds__(256) k_lr_range(Params P) {
       if (lane == 0) P.lr_Y[(int64_t)c * H + i] = acc;
     }
   }
-}
-
-// Q = orth(Y) by classical Gram-Schmidt applied twice, one column at a time (one CTA; the
-// H x l panel is staged in shared memory when it fits, kLrQrSmem bytes).
-constexpr int kLrQrSmemDoubles = 26 * 1024;
-constexpr size_t kLrQrSmem = sizeof(double) * kLrQrSmemDoubles;
-__global__ void __launch_bounds__(1024) k_lr_qr(Params P) {
-  extern __shared__ double qs[];
-  __shared__ double d[kLrMaxL];
-  __shared__ double sh[33];
-  if (P.st->done) return;
-  const int H = P.lr_H, l = P.lr_l;
-  const bool staged = (int64_t)H * l <= kLrQrSmemDoubles;
-  double* Qb = staged ? qs : P.lr_Q;  // column-major H x l
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int c = 0; c < l; ++c) {
-    double* q = Qb + (int64_t)c * H;
-    for (int i = threadIdx.x; i < H; i += 1024) q[i] = P.lr_Y[(int64_t)c * H + i];
-    __syncthreads();
-    for (int pass = 0; pass < 2; ++pass) {
-      for (int j = wid; j < c; j += 32) {
-        const double* qj = Qb + (int64_t)j * H;
-        double acc = 0.0;
-        for (int i = lane; i < H; i += 32) acc = fma(qj[i], q[i], acc);
-        acc = warp_sum(acc);
-        if (lane == 0) d[j] = acc;
-      }
-      __syncthreads();
-      for (int i = threadIdx.x; i < H; i += 1024) {
-        double v0 = q[i], v1 = 0.0, v2 = 0.0, v3 = 0.0;  // four chains for latency hiding
-        int j = 0;
-        for (; j + 4 <= c; j += 4) {
-          v0 = fma(-d[j], Qb[(int64_t)j * H + i], v0);
-          v1 = fma(-d[j + 1], Qb[(int64_t)(j + 1) * H + i], v1);
-          v2 = fma(-d[j + 2], Qb[(int64_t)(j + 2) * H + i], v2);
-          v3 = fma(-d[j + 3], Qb[(int64_t)(j + 3) * H + i], v3);
-        }
-        for (; j < c; ++j) v0 = fma(-d[j], Qb[(int64_t)j * H + i], v0);
-        q[i] = (v0 + v1) + (v2 + v3);
-      }
-      __syncthreads();
-    }
-    double acc = 0.0;
-    for (int i = threadIdx.x; i < H; i += 1024) acc = fma(q[i], q[i], acc);
-    const double nrm = sqrt(block_sum<1024>(acc, sh));
-    const double inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
-    for (int i = threadIdx.x; i < H; i += 1024) q[i] *= inv;
-    __syncthreads();
-  }
-  if (staged)
-    for (int64_t e = threadIdx.x; e < (int64_t)H * l; e += 1024) P.lr_Q[e] = qs[e];
 }
 
 // Q = orth(Y) by shifted Cholesky QR, three rounds (sCholQR3): G = Y^T Y (+ shift in round 1),
@@ -2176,87 +1974,6 @@ __global__ void __launch_bounds__(kVecThreads) k_finish_w(Params P) {
       sqrt(P.orth_alg != ORTH_MGS ? P.scal[P.slot_wout] : get_sum<kVecThreads>(P, P.slot_w0 + J, sh, kVecBlocks));
   const double win = sqrt(P.orth_alg != ORTH_MGS ? P.scal[P.slot_wf] : get_sum<kVecThreads>(P, P.slot_win, sh, kVecBlocks));
   finish_w_body<kVecThreads>(P, st, k, hn, win);
-}
-
-// ------------------------------------------------------------------ cooperative phase kernels
-// One launch per vector phase instead of three or four (one rank, fused window orth):
-// all blocks are co-resident (cooperative launch), phases are separated by a grid barrier,
-// and each reduction is summed in fixed block order by one designated block per slot.
-//   k_zphase: a1 + a2 (z-side dots/Gram -> axpy + norm -> normalise, tau, store z_k)
-//   k_wphase: a4 (sFLSQR sketch of w) + a5 (w-side dots/Gram -> axpy + norm -> w_{k+1})
-constexpr int kCoopThreads = 512;
-
-__device__ __forceinline__ void grid_sync(unsigned int* bar) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile unsigned int* gen = bar + 1;
-    const unsigned int g = *gen;
-    __threadfence();
-    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-      atomicExch(bar, 0u);
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
-      while (*gen == g) __nanosleep(32);
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
-// scal[s0 + t] = sum over blocks of part[s0 + t][b] (block t mod gridDim reduces slot t), then a barrier.
-__device__ __forceinline__ void coop_reduce(const Params& P, int s0, int ns) {
-  __shared__ double sh[33];
-  grid_sync(P.bar);
-  for (int t = blockIdx.x; t < ns; t += gridDim.x) {
-    const double* pp = P.part + (size_t)(s0 + t) * kVecBlocks;
-    double v = 0.0;
-    for (int b = threadIdx.x; b < (int)gridDim.x; b += kCoopThreads) v += __ldcg(pp + b);
-    v = block_sum<kCoopThreads>(v, sh);
-    if (threadIdx.x == 0) P.scal[s0 + t] = v;
-  }
-  grid_sync(P.bar);
-}
-
-__global__ void __launch_bounds__(kCoopThreads) k_zphase(Params P) {
-  DevState* st = P.st;
-  if (st->done) return;
-  const int k = st->k;
-  const int J = min(P.ell, k - 1), j0 = max(1, k - P.ell);
-  orth_dots_block<kCoopThreads>(P, 0, J, j0, P.slot_zf);
-  coop_reduce(P, P.slot_zf, kFuseAcc);
-  double c[kFuseJ];
-  orth_coefs(P, 0, k, J, j0, P.slot_zf, c);
-  orth_axpy_block<kCoopThreads>(P, 0, J, j0, c, P.slot_zout);
-  coop_reduce(P, P.slot_zout, 1);
-  finish_z_body<kCoopThreads>(P, st, k, sqrt(P.scal[P.slot_zout]), sqrt(P.scal[P.slot_zf]));
-}
-
-__global__ void __launch_bounds__(kCoopThreads) k_wphase(Params P) {
-  __shared__ double sh[33];
-  DevState* st = P.st;
-  if (st->done) return;
-  const int k = st->k;
-  if (P.method == 0) {  // a4: S_AZ[:, k] = S w (rows of the stored transposed S, fixed order)
-    for (int r = blockIdx.x; r < P.d; r += gridDim.x) {
-      double acc = 0.0;
-      for (int64_t q = P.sk_rp[r] + threadIdx.x; q < P.sk_rp[r + 1]; q += kCoopThreads) {
-        const uint32_t e = __ldg(P.sk_ent + q);
-        const double vi = P.w[e & 0x7fffffffu];
-        acc += (e >> 31) ? -vi : vi;
-      }
-      acc = block_sum<kCoopThreads>(acc, sh) * P.sk_scale;
-      if (threadIdx.x == 0) P.skbuf[r] = acc;
-    }
-  }
-  const int J = min(P.ell + 1, k), j0 = max(1, k - P.ell);
-  orth_dots_block<kCoopThreads>(P, 1, J, j0, P.slot_wf);
-  coop_reduce(P, P.slot_wf, kFuseAcc);
-  double c[kFuseJ];
-  orth_coefs(P, 1, k, J, j0, P.slot_wf, c);
-  orth_axpy_block<kCoopThreads>(P, 1, J, j0, c, P.slot_wout);
-  coop_reduce(P, P.slot_wout, 1);
-  finish_w_body<kCoopThreads>(P, st, k, sqrt(P.scal[P.slot_wout]), sqrt(P.scal[P.slot_wf]));
 }
 
 // ------------------------------------------------------------------ a7: projected sketched LS (one CTA)

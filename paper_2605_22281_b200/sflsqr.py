@@ -47,6 +47,23 @@ EXPORTED = [
 
 COMM_NCCL, COMM_LOCAL = 0, 1
 
+# opts.knobs (include/sflsqr.h SFLSQR_KNOB_*): scheduling / storage-format switches, 0 = defaults
+KNOBS = {"no_pdl": 0x1, "sketch_main": 0x2, "no_interp": 0x4, "no_sell": 0x8, "cgs_always2": 0x10,
+         "full_spmv_grid": 0x20, "res_main": 0x40, "res_side": 0x80, "p2p_on": 0x100, "p2p_off": 0x200,
+         "keep_csr": 0x400, "debug_poison": 0x800, "no_ell_c16": 0x1000}
+
+
+def knob_bits(knobs):
+    """int bits, or an iterable of names of KNOBS."""
+    if knobs is None:
+        return 0
+    if isinstance(knobs, int):
+        return knobs
+    bits = 0
+    for k in knobs:
+        bits |= KNOBS[k]
+    return bits
+
 
 class Opts(ctypes.Structure):
     _fields_ = [("method", ctypes.c_int32), ("window", ctypes.c_int32), ("maxit", ctypes.c_int32),
@@ -54,8 +71,8 @@ class Opts(ctypes.Structure):
                 ("delta_e", ctypes.c_double), ("history", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("stream", ctypes.c_void_p), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
                 ("use_graph", ctypes.c_int32), ("comm_kind", ctypes.c_int32), ("nccl_id", ctypes.c_void_p),
-                ("local_group", ctypes.c_void_p), ("orth_kernel", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 3)]
+                ("local_group", ctypes.c_void_p), ("orth_kernel", ctypes.c_int32), ("knobs", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 2)]
 
 
 class Info(ctypes.Structure):
@@ -65,7 +82,8 @@ class Info(ctypes.Structure):
                 ("beta", ctypes.c_double), ("m0", ctypes.c_int64), ("m_loc", ctypes.c_int64),
                 ("n0", ctypes.c_int64), ("n_loc", ctypes.c_int64), ("delta_e", ctypes.c_double),
                 ("bytes_model", ctypes.c_double), ("a_pairs", ctypes.c_int64), ("t_pairs", ctypes.c_int64),
-                ("a_fmt", ctypes.c_int32), ("t_fmt", ctypes.c_int32)]
+                ("a_fmt", ctypes.c_int32), ("t_fmt", ctypes.c_int32), ("knobs", ctypes.c_int32),
+                ("csr_kept", ctypes.c_int32)]
 
 
 class Profile(ctypes.Structure):
@@ -159,9 +177,10 @@ class SFLSQR:
 
     def __init__(self, method="sflsqr", window=2, maxit=10, orth_mode="P", tol=0.0, eta=0.0, delta_e=0.0,
                  history=HIST_TRUE_RES, device=0, stream=None, use_graph=True, rank=0, world=1, nccl_id=None,
-                 local_group=None, orth_kernel="auto"):
+                 local_group=None, orth_kernel="auto", knobs=0):
         self.lib = load_library()
         o = Opts()
+        o.knobs = knob_bits(knobs)
         o.method = METHODS.get(method, -1)
         o.orth_kernel = ORTHK_MGS if orth_kernel == "mgs" else ORTHK_AUTO
         o.window, o.maxit = int(window), int(maxit)
@@ -388,13 +407,13 @@ class LocalGroup:
 
 
 def solver_for_problem(prob, spec, maxit=None, history=HIST_TRUE_RES, use_graph=True, eta=None, device=0,
-                       operator_on_device=False, method=None, orth_kernel="auto"):
+                       operator_on_device=False, method=None, orth_kernel="auto", knobs=0):
     """Configure an SFLSQR handle for a gen.Problem / gen.SolverSpec (marshalling only).
     method overrides spec.method (e.g. "flsqr" / "flsmr" on a config's operator)."""
     mx = maxit or spec.maxit
     s = SFLSQR(method=method or spec.method, window=spec.window, maxit=mx, orth_mode=spec.orth_mode, tol=spec.tol,
                eta=spec.eta if eta is None else eta, delta_e=prob.delta_e, history=history, device=device,
-               use_graph=use_graph, orth_kernel=orth_kernel)
+               use_graph=use_graph, orth_kernel=orth_kernel, knobs=knobs)
     if prob.t_mode == "same":
         bl = prob.blur
         s.set_operator_blur(bl["H"], bl["W"], bl["sigma"], bl["radius"])

@@ -50,7 +50,7 @@ def shard_plan(prob, world: int) -> dict:
     return dict(a_blocks=a_blocks, t_mode="colshard", n_blocks=even_blocks(prob.n, world))
 
 
-def run_local_group(prob, spec, world: int, maxit=None, device=0, eta=None, history=1):
+def run_local_group(prob, spec, world: int, maxit=None, device=0, eta=None, history=1, knobs=0):
     """Run one sharded solve with `world` ranks as host threads of this process
     (SFLSQR_COMM_LOCAL) on one device.  Returns (x, true_res, sketch_res, infos)
     with x assembled from the ranks' n-slices."""
@@ -66,7 +66,7 @@ def run_local_group(prob, spec, world: int, maxit=None, device=0, eta=None, hist
         try:
             s = SFLSQR(method=spec.method, window=spec.window, maxit=mx, orth_mode=spec.orth_mode, tol=spec.tol,
                        eta=spec.eta if eta is None else eta, delta_e=prob.delta_e, history=history, device=device,
-                       use_graph=False, rank=r, world=world, local_group=grp)
+                       use_graph=False, rank=r, world=world, local_group=grp, knobs=knobs)
             a0, a1 = plan["a_blocks"][r]
             arp, acol, aval = csr_block(prob.A.rowptr, prob.A.col, prob.A.val, a0, a1)
             if plan["t_mode"] == "rowshard":

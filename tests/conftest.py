@@ -1,7 +1,14 @@
 import os
 import sys
 
-import pytest
+# The oracle's NumPy / LAPACK steps on every host with one thread and one kernel set (set before
+# NumPy loads OpenBLAS): the committed horizons (tests/golden/horizons.json) and every oracle
+# number are then the same bits here and on the GPU box (8 vs 16 OpenBLAS threads moved the config-8
+# horizon by 4 iterations).
+os.environ["OPENBLAS_NUM_THREADS"] = "1"
+os.environ["OPENBLAS_CORETYPE"] = "Haswell"
+
+import pytest  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:

@@ -11,9 +11,10 @@ move by < 1e-11 relative under
   * "products": a 2^-53 relative perturbation of every operator product (short recurrences).
 
 The numbers in tests/golden/horizons.json were written by tools/compute_horizons.py, which calls
-only gen/ and oracle/.  Each test recomputes k* on the box and asserts it equals the committed
-value within +-1 (BLAS kernels differ between hosts at rounding level), so a regression that
-shrinks a strict window shows up as a failure, not as a silently shorter window.
+only gen/ and oracle/.  Each test recomputes k* on the box, asserts it is the committed value
+within +-2 (BLAS kernels differ between hosts at rounding level) and holds the GPU to the strict
+bar over min(k*, committed) iterations, so a change that shrinks a strict window shows up as a
+failure, not as a silently shorter window.
 """
 import json
 import os
@@ -191,16 +192,20 @@ def truncate(r, k):
         sketch_cols=None if r.sketch_cols is None else r.sketch_cols[:, :ncols])
 
 
-def horizon(key, p=None, op=None):
-    """Recompute k* for a committed case on this host and assert it is the committed value +-1.
+def horizon(key, p=None, op=None, slack=2):
+    """Recompute k* for a committed case on this host and check it against the committed value.
 
-    The oracle runs to min(case maxit, committed + 2), enough to tell whether k* lies within +-1 of
-    the committed value.  Returns (k*, the unperturbed oracle run truncated to k*)."""
+    The oracle runs to min(case maxit, committed + slack + 1).  Its BLAS / LAPACK kernels differ
+    between hosts at rounding level, which moves k* by an iteration or two (measured: config 8
+    reduced, 23 here, 25 on the GPU box), so |k* - committed| <= slack is asserted.  The strict
+    window is min(k*, committed): never longer than what was committed, never beyond where this
+    host's oracle is stable.  Returns (window, the unperturbed oracle run truncated to it)."""
     p, spec, maxit, meth, mode = _resolve(key, p)
     want = committed(key)
-    run_to = min(maxit, want + 2)
+    run_to = min(maxit, want + slack + 1)
     kstar, r0 = stable_horizon(p, spec, run_to, meth, mode, op=op)
     print(f"horizon {key}: k* = {kstar} (committed {want}, run to {run_to})")
-    assert abs(kstar - want) <= 1, (key, kstar, want)
+    assert abs(kstar - want) <= slack, (key, kstar, want)
+    window = min(kstar, want)
     from oracle.sflsqr import OracleResult
-    return kstar, (truncate(r0, kstar) if isinstance(r0, OracleResult) else r0)
+    return window, (truncate(r0, window) if isinstance(r0, OracleResult) else r0)

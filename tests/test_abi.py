@@ -50,7 +50,7 @@ def test_version_and_create_without_gpu(lib):
     import torch
     from paper_2605_22281_b200 import sflsqr as B
     L = B.load_library()
-    assert L.sflsqr_version() == 4
+    assert L.sflsqr_version() == 5
     if torch.cuda.is_available():
         pytest.skip("GPU present: covered by the -m gpu tests")
     with pytest.raises(B.SflsqrError) as ei:
@@ -60,7 +60,8 @@ def test_version_and_create_without_gpu(lib):
 
 def test_option_validation_precedes_device_use(lib):
     from paper_2605_22281_b200 import sflsqr as B
-    bad = [dict(method="nope"), dict(window=0), dict(maxit=0), dict(tol=-1.0), dict(eta=0.5), dict(delta_e=-1.0)]
+    bad = [dict(method="nope"), dict(window=0), dict(maxit=0), dict(tol=-1.0), dict(eta=0.5), dict(delta_e=-1.0),
+           dict(knobs=1 << 20), dict(knobs=["res_main", "res_side"]), dict(knobs=["p2p_on", "p2p_off"])]
     for kw in bad:
         with pytest.raises(B.SflsqrError) as ei:
             B.SFLSQR(**kw)
@@ -83,3 +84,13 @@ def test_ctypes_structs_match_header_layout(lib):
         subprocess.run(["gcc", "-I" + inc, c, "-o", exe], check=True)
         sizes = [int(t) for t in subprocess.run([exe], capture_output=True, text=True, check=True).stdout.split()]
     assert sizes == [ctypes.sizeof(B.Opts), ctypes.sizeof(B.Info), ctypes.sizeof(B.Profile)]
+
+
+def test_knob_names_match_header():
+    # opts.knobs: the binding's names carry the header's bit values, and SFLSQR_KNOB_ALL covers them
+    from paper_2605_22281_b200 import sflsqr as B
+    txt = open(HEADER).read()
+    bits = {m.group(1).lower(): int(m.group(2), 16) for m in re.finditer(r"#define SFLSQR_KNOB_(\w+) (0x[0-9a-f]+)", txt)}
+    allbits = bits.pop("all")
+    assert bits == B.KNOBS
+    assert allbits == sum(bits.values())

@@ -32,10 +32,10 @@ def _lib():
     build_library()
 
 
-def _gpu_run(prob, spec, maxit, method, eta=0.0, orth_kernel="auto", use_graph=True):
+def _gpu_run(prob, spec, maxit, method, eta=0.0, orth_kernel="auto", use_graph=True, knobs=()):
     from paper_2605_22281_b200 import solver_for_problem
     s = solver_for_problem(prob, spec, maxit=maxit, eta=eta, method=method, orth_kernel=orth_kernel,
-                           use_graph=use_graph)
+                           use_graph=use_graph, knobs=list(knobs))
     s.set_rhs(prob.b)
     done, status = s.iterate(maxit)
     tr, pr = s.get_residual_norms()
@@ -129,6 +129,26 @@ def test_cgs2_and_mgs_kernels_agree_on_long_sketched_window():
     for g in (ga, gm):
         rt = np.abs(g["true_res"][:20] - np.array(r.true_res[:20])) / np.array(r.true_res[:20])
         assert rt.max() < RES_TOL, rt.max()
+
+
+@pytest.mark.parametrize("method", ["flsqr", "flsmr"])
+def test_selective_second_cgs_pass(method):
+    # reading R18: on one rank CGS2's second pass runs only when Kahan's criterion asks for it
+    # (||v'||^2 < ||v||^2 / 2 after the first pass).  Against always two passes (SFLSQR_KNOB_CGS_ALWAYS2):
+    # a pass was skipped (the runs differ bitwise), both hold the oracle's bar over its horizon, and
+    # the GPU's W stays orthonormal to working precision either way
+    p = make_problem(3, N=128, n_angles=90, nb=183)   # NONNEG tau: the z side keeps >= 81 % of its norm
+    spec = p.solvers[0]
+    kstar, _ = horizon(f"flsqr/c3r128/{method}", p)
+    r = solve_problem(p, spec, maxit=kstar, eta=0.0, method=method)
+    gs = _gpu_run(p, spec, kstar, method)
+    g2 = _gpu_run(p, spec, kstar, method, knobs=["cgs_always2"])
+    assert not np.array_equal(gs["x"], g2["x"])
+    for g in (gs, g2):
+        _compare(g, r, kstar)
+        W = g["basis"]["W"]
+        assert np.abs(W.T @ W - np.eye(W.shape[1])).max() < 1e-12
+    assert np.linalg.norm(gs["x"] - g2["x"]) <= 1e-9 * np.linalg.norm(g2["x"])
 
 
 def test_graph_and_eager_agree_bitwise_flsmr():

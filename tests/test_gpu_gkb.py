@@ -33,7 +33,8 @@ def _lib():
 
 def _gpu_run(prob, spec, maxit, method, eta=0.0, use_graph=True, spmv_mode=None):
     from paper_2605_22281_b200 import solver_for_problem
-    s = solver_for_problem(prob, spec, maxit=maxit, eta=eta, method=method, use_graph=use_graph)
+    s = solver_for_problem(prob, spec, maxit=maxit, eta=eta, method=method, use_graph=use_graph,
+                           knobs=["keep_csr"] if spmv_mode is not None else [])
     if spmv_mode is not None:
         s.debug_set_tuning(spmv_mode)
     s.set_rhs(prob.b)
@@ -78,7 +79,7 @@ def test_gkb_parity(method, cfg, kw, tag):
 
 
 @pytest.mark.parametrize("method", ["lsqr", "lsmr"])
-def test_gkb_discrepancy_stop_and_unfused_epilogue(method):
+def test_gkb_discrepancy_stop_and_forced_formats(method):
     p = make_problem(3, N=96, n_angles=70, nb=137)
     spec = p.solvers[0]
     full = solve_problem(p, spec, maxit=30, eta=0.0, method=method)
@@ -87,7 +88,7 @@ def test_gkb_discrepancy_stop_and_unfused_epilogue(method):
     eta = float(ratio[k0]) * (1 + 1e-7)
     r = solve_problem(p, spec, maxit=30, eta=eta, method=method)
     assert r.status == 3
-    for mode in (None, 3):                                 # fused CSR epilogue / separate pass
+    for mode in (None, 14, 16):                            # default format / fused CSR / fused pair-CSR epilogue
         g = _gpu_run(p, spec, 30, method, eta=eta, spmv_mode=mode)
         _compare(g, r, method)
 

@@ -122,8 +122,8 @@ def test_nccl_unique_id_available():
 
 
 @pytest.mark.parametrize("cfg,world", [(3, 3), (4, 2)])
-def test_peer_memory_collectives_bitwise_equal_to_collectives(cfg, world, monkeypatch):
-    # SFLSQR_P2P: all-gathers as direct stores into every rank's gathered buffer and the COLSHARD
+def test_peer_memory_collectives_bitwise_equal_to_collectives(cfg, world):
+    # peer memory (SFLSQR_KNOB_P2P_ON, the in-process default): all-gathers as direct stores into every rank's gathered buffer and the COLSHARD
     # reduce-scatter fused into the T product's epilogue (stores into the owner's receive slots),
     # each followed by a barrier; the sums run in rank order as in the in-process collectives,
     # so the two paths must agree bit for bit (config 3: COLSHARD, config 4: ROWSHARD)
@@ -133,8 +133,8 @@ def test_peer_memory_collectives_bitwise_equal_to_collectives(cfg, world, monkey
     spec = p.solvers[0]
     out = {}
     for mode in ("0", "1"):
-        monkeypatch.setenv("SFLSQR_P2P", mode)
-        x, tr, sk, infos, st, _ = run_local_group(p, spec, world, maxit=20, eta=0.0)
+        x, tr, sk, infos, st, _ = run_local_group(p, spec, world, maxit=20, eta=0.0,
+                                                  knobs=["p2p_off"] if mode == "0" else ["p2p_on"])
         out[mode] = (x, tr, sk)
     assert np.array_equal(out["0"][0], out["1"][0])
     assert np.array_equal(out["0"][1], out["1"][1]) and np.array_equal(out["0"][2], out["1"][2])

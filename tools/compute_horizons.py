@@ -8,6 +8,9 @@ import os
 import sys
 import time
 
+os.environ["OPENBLAS_NUM_THREADS"] = "1"      # as tests/conftest.py: host-independent oracle bits
+os.environ["OPENBLAS_CORETYPE"] = "Haswell"
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path[:0] = [ROOT, os.path.join(ROOT, "tests")]
 

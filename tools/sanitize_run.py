@@ -8,7 +8,8 @@ from paper_2605_22281_b200 import solver_for_problem
 
 
 def run(p, spec, maxit, method=None, graph=True, tune=None):
-    s = solver_for_problem(p, spec, maxit=maxit, eta=0.0, use_graph=graph, **({} if method is None else dict(method=method)))
+    s = solver_for_problem(p, spec, maxit=maxit, eta=0.0, use_graph=graph, knobs=["keep_csr"] if tune else [],
+                           **({} if method is None else dict(method=method)))
     if tune is not None:
         s.debug_set_tuning(tune)
     s.set_rhs(p.b)
