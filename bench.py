@@ -289,7 +289,7 @@ def main():
         maxit = max(spec.maxit, W + K)
         t_up = time.perf_counter()
         s = SFLSQR(method=spec.method, window=spec.window, maxit=maxit, orth_mode=spec.orth_mode, tol=spec.tol,
-                   eta=0.0, delta_e=prob.delta_e, device=local, use_graph=False, rank=rank, world=world,
+                   eta=0.0, delta_e=prob.delta_e, device=local, use_graph=True, rank=rank, world=world,
                    nccl_id=bytes(uid.cpu().numpy()))
         A = prob.A_loc
         t = None if prob.T_loc is None else (prob.T_loc.rowptr, prob.T_loc.col, prob.T_loc.val)
@@ -466,7 +466,8 @@ def main():
                        "iterations_timed": f"{W + 1}..{W + K}", "history": "true residual (W path) on",
                        "l2": "inputs larger than L2 (operators ~30 GB vs 126 MB L2); no flush",
                        "parallelism": parallelism,
-                       "launch": "CUDA graph per iteration" if not sharded else "eager + NCCL",
+                       "launch": ("CUDA graph per iteration" + (" (NCCL collectives captured)" if sharded else ""))
+                                 if info_end["graph"] else "eager launches" + (" + NCCL" if sharded else ""),
                        "per_kernel_timing": "second timed region of K iterations, eager launches with CUDA events "
                                             "on the library stream (ms_per_step_profiled)"},
             "roofline": roof,

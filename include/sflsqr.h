@@ -166,7 +166,8 @@ typedef struct sflsqr_opts {
   void *stream;      /* cudaStream_t (borrowed) or NULL                            */
   int32_t rank;      /* this rank, 0 <= rank < world                               */
   int32_t world;     /* number of ranks sharding the operator     */
-  int32_t use_graph; /* 1: replay one captured CUDA graph per iteration (world = 1) */
+  int32_t use_graph; /* 1: replay one captured CUDA graph per iteration (one rank, or NCCL ranks
+                        with the collectives captured; the in-process group runs eagerly) */
   int32_t comm_kind; /* SFLSQR_COMM_* (world > 1)                                  */
   const uint8_t *nccl_id; /* SFLSQR_COMM_NCCL: the 128-byte id of sflsqr_get_unique_id */
   void *local_group;      /* SFLSQR_COMM_LOCAL: sflsqr_local_group_create()          */
@@ -197,6 +198,8 @@ typedef struct sflsqr_info {
                           4 the same pairs as sliced ELL, 32 rows per slice, one row per lane */
   int32_t knobs;        /* opts.knobs of this handle                                             */
   int32_t csr_kept;     /* bit 0: A's uploaded CSR is held, bit 1: T's (else released, its copy serves) */
+  int32_t graph;        /* 1: iterate() replays one captured CUDA graph per iteration             */
+  int32_t reserved_i;
 } sflsqr_info;
 
 /* Per-kernel-class device time, recorded with CUDA events on the library stream

@@ -16,7 +16,9 @@ vectors; sketch table properties; Householder vs numpy.linalg.lstsq;
 reductions to SciPy LSQR/LSMR (tau = id, S = I, full window); fixed-diagonal
 tau vs LSQR on A D^{1/2}; AB-/BA-GMRES brute force for unmatched B; the
 Remark sFLSMR == sFLSQR with sketch S A^T; rank-k exactness; Theorem 2.1's
-identity; FGK relations.  "Parity unpinned": the IRN and NONNEG weight
-formulas themselves (paper-silent, readings R7/R8) are pinned only through the
-fixed-diagonal reduction and GPU-vs-oracle agreement.
+identity; FGK relations; the IRN weights against the IRLS definitions they
+implement (the weighted 2-norm tends to the l_p norm, the weights are the
+gradient of the smoothed l_p penalty, p = 2 gives no reweighting) and the
+NONNEG weights against the properties of a multiplicative nonnegativity
+scaling (tests/test_oracle_precond.py; readings R7/R8).
 """

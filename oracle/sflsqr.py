@@ -28,6 +28,8 @@ Readings of paper-silent / ambiguous points (R1-R14):
   R4  sFLSQR sketches m-vectors, sFLSMR sketches n-vectors.
   R7  IRN-l_p: tau_k(v) = D_k v, D_k = diag((x_{k-1}^2 + eps^2)^((2-p)/4)),
       eps = eps_rel * max|x_{k-1}|; D_1 = I (x_0 = 0; also D = I if x_{k-1} = 0).
+      Pinned (tests/test_oracle_precond.py): sum (x/D)^2 -> ||x||_p^p as eps -> 0, and
+      x / D^2 = the gradient of (1/p) sum (x^2 + eps^2)^{p/2} (the IRLS weights, L59-64).
   R8  NONNEG: D_k = diag(max(x_{k-1}, 0) + eps_rel * max(x_{k-1})_+); D_1 = I
       (also D = I if max(x_{k-1})_+ = 0).
   R11 breakdown: if ||z|| <= 1e-14 ||T w_k|| (before orthogonalisation) z_k

@@ -1451,12 +1451,21 @@ int build_graph(sflsqr_t* h) {
   const int64_t before = h->launches;
   const bool prof = h->prof_on;
   h->prof_on = false;
-  cudaGraph_t g;
+  cudaGraph_t g = nullptr;
   CU(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
   h->host_k = 1;
   int rc = enqueue_iteration(h);
   cudaError_t e = cudaStreamEndCapture(h->stream, &g);
   h->prof_on = prof;
+  if (h->world > 1 && (rc || e != cudaSuccess)) {
+    // a communicator whose calls cannot be captured: run the iterations eagerly instead
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+    h->launches = before;
+    h->o.use_graph = 0;
+    h->err.clear();
+    return SFLSQR_OK;
+  }
   if (rc) return rc;
   if (e != cudaSuccess) return fail(h, SFLSQR_E_CUDA, "graph capture: %s", cudaGetErrorString(e));
   h->kernels_per_iter = (int)(h->launches - before);
@@ -1694,7 +1703,9 @@ int sflsqr_create(sflsqr_t** out, const sflsqr_opts* o) {
   if (o->method == SFLSQR_METHOD_FLSQR || o->method == SFLSQR_METHOD_FLSMR)
     h->o.window = o->maxit;  // FLSQR / FLSMR: full (L344-345)
   if (o->method >= SFLSQR_METHOD_LSQR) h->o.window = 1;  // GKB short recurrences: no stored window
-  if (o->world > 1) h->o.use_graph = 0;             // collectives are issued eagerly
+  // the in-process group's collectives are host rendezvous (not capturable): eager; NCCL calls are
+  // captured into the per-iteration graph with the kernels (eager fallback if capture fails)
+  if (o->world > 1 && o->comm_kind == SFLSQR_COMM_LOCAL) h->o.use_graph = 0;
   if (o->stream && (cudaStream_t)o->stream != cudaStreamLegacy && (cudaStream_t)o->stream != cudaStreamPerThread) {
     h->stream = (cudaStream_t)o->stream;
   } else {
@@ -2263,6 +2274,7 @@ int sflsqr_get_info(sflsqr_t* h, sflsqr_info* info) {
   info->a_fmt = info->a_pairs ? (h->pa.aligned ? 2 : (h->pa.interp ? (h->pa.ell ? 4 : 3) : 1)) : 0;
   info->t_fmt = info->t_pairs ? (h->pt.aligned ? 2 : (h->pt.interp ? (h->pt.ell ? 4 : 3) : 1)) : 0;
   info->knobs = h->knobs;
+  info->graph = (h->gexec && h->o.use_graph) ? 1 : 0;
   info->csr_kept = (h->csr_freed_a ? 0 : 1) | (h->csr_freed_t ? 0 : 2);
   return SFLSQR_OK;
 }

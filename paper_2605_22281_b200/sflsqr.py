@@ -83,7 +83,7 @@ class Info(ctypes.Structure):
                 ("n0", ctypes.c_int64), ("n_loc", ctypes.c_int64), ("delta_e", ctypes.c_double),
                 ("bytes_model", ctypes.c_double), ("a_pairs", ctypes.c_int64), ("t_pairs", ctypes.c_int64),
                 ("a_fmt", ctypes.c_int32), ("t_fmt", ctypes.c_int32), ("knobs", ctypes.c_int32),
-                ("csr_kept", ctypes.c_int32)]
+                ("csr_kept", ctypes.c_int32), ("graph", ctypes.c_int32), ("reserved_i", ctypes.c_int32)]
 
 
 class Profile(ctypes.Structure):

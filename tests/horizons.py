@@ -11,10 +11,10 @@ move by < 1e-11 relative under
   * "products": a 2^-53 relative perturbation of every operator product (short recurrences).
 
 The numbers in tests/golden/horizons.json were written by tools/compute_horizons.py, which calls
-only gen/ and oracle/.  Each test recomputes k* on the box, asserts it is the committed value
-within +-2 (BLAS kernels differ between hosts at rounding level) and holds the GPU to the strict
-bar over min(k*, committed) iterations, so a change that shrinks a strict window shows up as a
-failure, not as a silently shorter window.
+only gen/ and oracle/.  Each test recomputes k* on the box, asserts it is not shorter than the
+committed value by more than 3 (host-to-host rounding of NumPy's reductions) and holds the GPU to
+the strict bar over min(k*, committed) iterations, so a change that shrinks a strict window shows
+up as a failure, not as a silently shorter window.
 """
 import json
 import os
@@ -192,20 +192,21 @@ def truncate(r, k):
         sketch_cols=None if r.sketch_cols is None else r.sketch_cols[:, :ncols])
 
 
-def horizon(key, p=None, op=None, slack=2):
+def horizon(key, p=None, op=None, slack=3):
     """Recompute k* for a committed case on this host and check it against the committed value.
 
-    The oracle runs to min(case maxit, committed + slack + 1).  Its BLAS / LAPACK kernels differ
-    between hosts at rounding level, which moves k* by an iteration or two (measured: config 8
-    reduced, 23 here, 25 on the GPU box), so |k* - committed| <= slack is asserted.  The strict
-    window is min(k*, committed): never longer than what was committed, never beyond where this
-    host's oracle is stable.  Returns (window, the unperturbed oracle run truncated to it)."""
+    The oracle runs to min(case maxit, committed + 1).  Its arithmetic is host-independent up to
+    NumPy's CPU-dispatched SIMD reductions (OpenBLAS is pinned in conftest.py), which move k* by up
+    to 3 iterations between this container and the GPU box (measured: config 5 reduced 96 / 99,
+    config 8 reduced 19 / 22).  The check is one-sided -- k* >= committed - slack: a change that
+    shortens the oracle's stable window fails, a host on which it is longer passes.  The strict
+    window is min(k*, committed).  Returns (window, the unperturbed oracle run truncated to it)."""
     p, spec, maxit, meth, mode = _resolve(key, p)
     want = committed(key)
-    run_to = min(maxit, want + slack + 1)
+    run_to = min(maxit, want + 1)
     kstar, r0 = stable_horizon(p, spec, run_to, meth, mode, op=op)
     print(f"horizon {key}: k* = {kstar} (committed {want}, run to {run_to})")
-    assert abs(kstar - want) <= slack, (key, kstar, want)
+    assert kstar >= want - slack, (key, kstar, want)
     window = min(kstar, want)
     from oracle.sflsqr import OracleResult
     return window, (truncate(r0, window) if isinstance(r0, OracleResult) else r0)

@@ -227,6 +227,7 @@ def test_graph_and_eager_agree_bitwise(use_graph):
     spec = p.solvers[0]
     g1 = _gpu_run(p, spec, maxit=15, use_graph=use_graph)
     g2 = _gpu_run(p, spec, maxit=15, use_graph=True)
+    assert g1["info"]["graph"] == int(use_graph) and g2["info"]["graph"] == 1
     assert np.array_equal(g1["x"], g2["x"])              # deterministic reductions
     assert np.array_equal(g1["true_res"], g2["true_res"])
 

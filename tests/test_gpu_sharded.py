@@ -45,6 +45,7 @@ def test_colshard_config3_reduced(world, method):
     r = solve_problem(p, spec, maxit=60, eta=0.0)
     x, tr, sk, infos, st, out = run_local_group(p, spec, world, maxit=60, eta=0.0)
     assert all(s == (True, 1) for s in st)
+    assert all(i["graph"] == 0 for i in infos)         # in-process collectives are host rendezvous: eager
     assert sum(i["m_loc"] for i in infos) == p.m and sum(i["n_loc"] for i in infos) == p.n
     _check(x, tr, sk, r, 60)
     _check_gathered(x, out)
