@@ -116,7 +116,8 @@ def _barrier(world):
         dist.barrier()
 
 
-FMT_NAMES = ["CSR", "pair-CSR", "aligned pair-CSR", "interpolation pair-CSR", "sliced-ELL interpolation pairs"]
+FMT_NAMES = ["CSR", "pair-CSR", "aligned pair-CSR", "interpolation pair-CSR", "sliced-ELL interpolation pairs",
+             "IC16 aligned pairs"]
 
 
 def _traffic(workload, kernel):
@@ -232,6 +233,7 @@ def main():
     ap.add_argument("--no-profile", action="store_true", help="graph replay without per-kernel events")
     ap.add_argument("--N", type=int, default=None, help="override grid size (debug)")
     ap.add_argument("--no-windows", action="store_true", help="skip the late-window and full-solve timings")
+    ap.add_argument("--knobs", default="", help="comma-separated opts.knobs names (A/B runs; default: none)")
     args = ap.parse_args()
 
     world, rank, local = _dist()
@@ -262,6 +264,7 @@ def main():
     _barrier(world)
 
     W, K = args.warmup, args.steps
+    knobs = [k for k in args.knobs.split(",") if k]
     sharded = world > 1 and CONFIGS[args.config]["kind"] == "ct" and not args.N
     t_gen = time.perf_counter()
     if sharded:
@@ -290,7 +293,7 @@ def main():
         t_up = time.perf_counter()
         s = SFLSQR(method=spec.method, window=spec.window, maxit=maxit, orth_mode=spec.orth_mode, tol=spec.tol,
                    eta=0.0, delta_e=prob.delta_e, device=local, use_graph=True, rank=rank, world=world,
-                   nccl_id=bytes(uid.cpu().numpy()))
+                   nccl_id=bytes(uid.cpu().numpy()), knobs=knobs)
         A = prob.A_loc
         t = None if prob.T_loc is None else (prob.T_loc.rowptr, prob.T_loc.col, prob.T_loc.val)
         s.set_operator_shard(prob.m, prob.n, prob.a_rows[0], prob.a_rows[1], A.rowptr, A.col, A.val, t=t,
@@ -308,7 +311,7 @@ def main():
         t_gen = time.perf_counter() - t_gen
         maxit = max(spec.maxit, W + K)
         t_up = time.perf_counter()
-        s = solver_for_problem(prob, spec, maxit=maxit, eta=0.0, device=local, use_graph=True)
+        s = solver_for_problem(prob, spec, maxit=maxit, eta=0.0, device=local, use_graph=True, knobs=knobs)
         t_up = time.perf_counter() - t_up
         b_host = prob.b
         nnz_A = prob.A.nnz if prob.A is not None else None
@@ -398,7 +401,8 @@ def main():
         fnames = dict(enumerate(FMT_NAMES))
         fmt = {"spmv_A": fnames[inf["a_fmt"]], "spmv_T": fnames[inf["t_fmt"]]}
         tkey = dom + {"CSR": "", "pair-CSR": "_pcsr", "aligned pair-CSR": "_apcsr",
-                      "interpolation pair-CSR": "_ipcsr", "sliced-ELL interpolation pairs": "_sell"}[fmt.get(dom, "CSR")]
+                      "interpolation pair-CSR": "_ipcsr", "sliced-ELL interpolation pairs": "_sell",
+                      "IC16 aligned pairs": "_ic16"}[fmt.get(dom, "CSR")]
         tr = _traffic(prob.name, tkey)
         l1 = _traffic(prob.name, tkey + "_l1_wavefronts_pct")
         kname = {"spmv_A": f"k_spmv_csr_pf, {fmt['spmv_A']} (A z)",
@@ -465,7 +469,7 @@ def main():
                        "ell": spec.window, "d": spec.d, "s": spec.s_nz, "tau": spec.precond, "maxit": maxit,
                        "iterations_timed": f"{W + 1}..{W + K}", "history": "true residual (W path) on",
                        "l2": "inputs larger than L2 (operators ~30 GB vs 126 MB L2); no flush",
-                       "parallelism": parallelism,
+                       "parallelism": parallelism, "knobs": knobs,
                        "launch": ("CUDA graph per iteration" + (" (NCCL collectives captured)" if sharded else ""))
                                  if info_end["graph"] else "eager launches" + (" + NCCL" if sharded else ""),
                        "per_kernel_timing": "second timed region of K iterations, eager launches with CUDA events "
