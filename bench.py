@@ -116,8 +116,7 @@ def _barrier(world):
         dist.barrier()
 
 
-FMT_NAMES = ["CSR", "pair-CSR", "aligned pair-CSR", "interpolation pair-CSR", "sliced-ELL interpolation pairs",
-             "IC16 aligned pairs"]
+FMT_NAMES = ["CSR", "pair-CSR", "aligned pair-CSR", "interpolation pair-CSR", "sliced-ELL interpolation pairs"]
 
 
 def _traffic(workload, kernel):
@@ -401,8 +400,7 @@ def main():
         fnames = dict(enumerate(FMT_NAMES))
         fmt = {"spmv_A": fnames[inf["a_fmt"]], "spmv_T": fnames[inf["t_fmt"]]}
         tkey = dom + {"CSR": "", "pair-CSR": "_pcsr", "aligned pair-CSR": "_apcsr",
-                      "interpolation pair-CSR": "_ipcsr", "sliced-ELL interpolation pairs": "_sell",
-                      "IC16 aligned pairs": "_ic16"}[fmt.get(dom, "CSR")]
+                      "interpolation pair-CSR": "_ipcsr", "sliced-ELL interpolation pairs": "_sell"}[fmt.get(dom, "CSR")]
         tr = _traffic(prob.name, tkey)
         l1 = _traffic(prob.name, tkey + "_l1_wavefronts_pct")
         kname = {"spmv_A": f"k_spmv_csr_pf, {fmt['spmv_A']} (A z)",

@@ -142,8 +142,7 @@ extern "C" {
 #define SFLSQR_KNOB_DEBUG_POISON 0x800 /* fill every solve buffer with NaN bytes at allocation
                                             (a read before write then shows in the results)   */
 #define SFLSQR_KNOB_NO_ELL_C16 0x1000 /* 32-bit columns in the sliced-ELL interpolation pairs   */
-#define SFLSQR_KNOB_NO_IC16 0x2000   /* aligned pairs stay pair-CSR (no IC16 re-layout)             */
-#define SFLSQR_KNOB_ALL 0x3fff
+#define SFLSQR_KNOB_ALL 0x1fff
 
 /* opts.history bits */
 #define SFLSQR_HIST_TRUE_RES 1 /* record ||b - A x_k|| every iteration              */
@@ -196,9 +195,7 @@ typedef struct sflsqr_info {
   int32_t a_fmt, t_fmt; /* SpMV format of the A / T products: 0 CSR, 1 pair-CSR (any adjacent
                           pair), 2 aligned pair-CSR (pairs at even columns, 16-byte gathers),
                           3 interpolation pair-CSR (every pair (1 - f, f) bitwise: only f stored),
-                          4 the same pairs as sliced ELL, 32 rows per slice, one row per lane,
-                          5 aligned pair-CSR re-laid as IC16: 64-entry chunks interleaved per lane,
-                            16-bit column offsets from a base per 16 entries          */
+                          4 the same pairs as sliced ELL, 32 rows per slice, one row per lane */
   int32_t knobs;        /* opts.knobs of this handle                                             */
   int32_t csr_kept;     /* bit 0: A's uploaded CSR is held, bit 1: T's (else released, its copy serves) */
   int32_t graph;        /* 1: iterate() replays one captured CUDA graph per iteration             */

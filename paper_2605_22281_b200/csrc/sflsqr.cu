@@ -48,16 +48,6 @@ struct PCSR {  // pair-CSR copy of an operator (k_pcsr_rows): pairs + singleton 
   bool interp = false;   // interpolation pairs: second values f only (first = 1 - f bitwise), pval freed
   bool ell = false;      // their sliced-ELL copy serves the product (pair-CSR arrays prp / pcol / f freed)
   bool c16 = false;      // ... with 16-bit column offsets from a per-slice-entry base (ecol freed)
-  bool ic = false;       // aligned pairs re-laid as IC16 (interleaved chunks, 16-bit columns; pcol / pval /
-                         // scol / sval freed, prp / srp kept for the counts)
-  int64_t ic_pent = 0, ic_sent = 0, ic_pgr = 0, ic_sgr = 0;  // IC16 stream entries and group bases
-  int64_t *ic_pstart = nullptr, *ic_pbst = nullptr, *ic_sstart = nullptr, *ic_sbst = nullptr;
-  uint16_t *ic_poff = nullptr, *ic_soff = nullptr;
-  int *ic_pbase = nullptr, *ic_sbase = nullptr;
-  int *ic_pesc = nullptr, *ic_sesc = nullptr;  // escaped groups (span >= 65536 columns): int32 columns
-  int64_t ic_nesc = 0;
-  double2* ic_pval = nullptr;
-  double* ic_sval = nullptr;
   double* f = nullptr;
   // sliced-ELL copy of the interpolation pairs (k_spmv_sell_ip): slice offsets, per-row counts
   int64_t* soff = nullptr;
@@ -112,7 +102,6 @@ struct sflsqr {
   bool pcsr_interp = true;  // interpolation pairs when every pair qualifies (SFLSQR_KNOB_NO_INTERP: off)
   bool sell = true;         // sliced-ELL (row per lane) copy of interpolation pairs (SFLSQR_KNOB_NO_SELL: off)
   bool ell_c16 = true;      // ... with 16-bit column offsets when they fit (SFLSQR_KNOB_NO_ELL_C16: off)
-  bool ic16 = true;         // aligned pairs re-laid as IC16 (SFLSQR_KNOB_NO_IC16: off)
   bool cgs_selective = true;  // CGS2 second pass only when needed (one rank; SFLSQR_KNOB_CGS_ALWAYS2: always)
   // sketch
   bool sk_set = false;
@@ -266,10 +255,6 @@ void free_solve(sflsqr_t* h) {
 void free_pcsr(PCSR& p) {
   cudaFree(p.soff);
   cudaFree(p.rcnt);
-  for (void* q : {(void*)p.ic_pstart, (void*)p.ic_pbst, (void*)p.ic_sstart, (void*)p.ic_sbst, (void*)p.ic_poff,
-                  (void*)p.ic_soff, (void*)p.ic_pbase, (void*)p.ic_sbase, (void*)p.ic_pval, (void*)p.ic_sval,
-                  (void*)p.ic_pesc, (void*)p.ic_sesc})
-    cudaFree(q);
   cudaFree(p.ecol);
   cudaFree(p.ebase);
   cudaFree(p.eoff);
@@ -405,30 +390,6 @@ double sell_bytes(const PCSR& pc, int64_t nrows) {
          8.0 * ((nrows + kSellC - 1) / kSellC + 1);
 }
 
-// Bytes of an IC16 operator a product streams: pairs 2 B offset + 16 B values, singletons
-// 2 B + 8 B, 4 B per 16-entry group base, padding to 4 entries, per-row starts / counts.
-double ic_bytes(const PCSR& pc, int64_t nrows) {
-  return 18.0 * pc.ic_pent + 10.0 * pc.ic_sent + 4.0 * (pc.ic_pgr + pc.ic_sgr) + 64.0 * pc.ic_nesc + 48.0 * (nrows + 1);
-}
-ICPart ic_part(const PCSR& pc) {
-  ICPart P;
-  P.pstart = pc.ic_pstart;
-  P.pbst = pc.ic_pbst;
-  P.prp = pc.prp;
-  P.poff = pc.ic_poff;
-  P.pbase = pc.ic_pbase;
-  P.pesc = pc.ic_pesc;
-  P.pval = pc.ic_pval;
-  P.sstart = pc.ic_sstart;
-  P.sbst = pc.ic_sbst;
-  P.srp = pc.srp;
-  P.soff = pc.ic_soff;
-  P.sbase = pc.ic_sbase;
-  P.sesc = pc.ic_sesc;
-  P.sval = pc.ic_sval;
-  return P;
-}
-
 // The product runs on the operator's format copy when it has one (pa / pt, built by the rule of
 // DESIGN.md §5 or forced by sflsqr_debug_set_tuning 16 / 17), else on the uploaded CSR
 // (sflsqr_debug_set_tuning 14 forces the CSR, which needs SFLSQR_KNOB_KEEP_CSR once a copy exists).
@@ -486,15 +447,7 @@ void enqueue_apply(sflsqr_t* h, int which, const DevState* st, const double* x, 
   if (pc.interp) L.bytes_override(12.0 * pc.npairs + 12.0 * pc.nsingles + 16.0 * (nrows + 1) + 8.0 * xlen + 8.0 * nrows);
   // aligned pairs gather one 16-byte value pair: needs x (any k-relative column) 16-byte aligned
   const bool x16 = ((uintptr_t)x % 16 == 0) && (x_ld % 2 == 0);
-  if (pc.ic) {  // IC16 aligned pairs
-    L.bytes_override(ic_bytes(pc, nrows) + 8.0 * xlen + 8.0 * nrows);
-    if (x16)
-      launch_pdl(h, k_spmv_ic16<false, true>, grid_for(32, 2), 512, 0, h->stream, st, nrows, ic_part(pc), x, x_ld,
-                 x_koff, y, SpmvEpi());
-    else
-      launch_pdl(h, k_spmv_ic16<false, false>, grid_for(32, 2), 512, 0, h->stream, st, nrows, ic_part(pc), x, x_ld,
-                 x_koff, y, SpmvEpi());
-  } else if (pc.ell) {  // sliced-ELL interpolation pairs (pair-CSR arrays released after the build)
+  if (pc.ell) {  // sliced-ELL interpolation pairs (pair-CSR arrays released after the build)
     L.bytes_override(sell_bytes(pc, nrows) + 8.0 * xlen + 8.0 * nrows);
     const int64_t nsl = (nrows + kSellC - 1) / kSellC;
     const int g = (int)std::max<int64_t>(1, std::min<int64_t>((nsl + 15) / 16, 148 * 2 - h->spmv_grid_delta));
@@ -672,14 +625,6 @@ bool launch_pairs_epi(sflsqr_t* h, int which, const double* x, int64_t x_ld, dou
   const int64_t nrows = which == 0 ? h->m_loc : h->t_rows;
   const int64_t xlen = which == 0 ? (h->world > 1 ? h->world * h->n_max : h->n)
                                   : (h->tkind == T_ROWSHARD ? h->world * h->m_max : h->m_loc);
-  if (pc.ic) {  // IC16 aligned pairs with the fused epilogue
-    Launch L(h, cls, ic_bytes(pc, nrows) + 8.0 * xlen + 8.0 * nrows + extra);
-    if ((uintptr_t)x % 16 == 0 && x_ld % 2 == 0)
-      k_spmv_ic16<true, true><<<grid, 512, 0, h->stream>>>(h->P.st, nrows, ic_part(pc), x, x_ld, 0, y, E);
-    else
-      k_spmv_ic16<true, false><<<grid, 512, 0, h->stream>>>(h->P.st, nrows, ic_part(pc), x, x_ld, 0, y, E);
-    return true;
-  }
   if (pc.ell) {  // sliced-ELL interpolation pairs with the fused epilogue
     Launch L(h, cls, sell_bytes(pc, nrows) + 8.0 * xlen + 8.0 * nrows + extra);
     const int64_t nsl = (nrows + kSellC - 1) / kSellC;
@@ -1087,121 +1032,6 @@ int try_interp(sflsqr_t* h, PCSR& p) {
 // Sliced-ELL copy of an interpolation pair-CSR operator (row per lane, k_spmv_sell_ip), kept only
 // when the slices' padding costs at most 10 % more entries.
 int build_sell_c16(sflsqr_t* h, int64_t nrows, PCSR& p);
-
-// IC16 copy of an aligned pair-CSR operator: per-row stream lengths and group-base
-// counts, four exclusive scans, the fill (k_ic_fill; groups spanning >= 65536 columns escaped to
-// int32 columns); kept when the copy fits beside the pair-CSR arrays it replaces (freed afterwards).
-int build_ic(sflsqr_t* h, int64_t nrows, PCSR& p) {
-  if (!p.ok || !p.aligned || p.interp || nrows < 1) return SFLSQR_OK;
-  int64_t *len[4] = {nullptr, nullptr, nullptr, nullptr};
-  int64_t* outp[4] = {nullptr, nullptr, nullptr, nullptr};
-  void* tmp = nullptr;
-  int* flag = nullptr;
-  size_t tb = 0;
-  int rc;
-  auto drop = [&](bool all) {
-    for (int i = 0; i < 4; ++i) cudaFree(len[i]);
-    cudaFree(tmp);
-    cudaFree(flag);
-    if (all) {
-      for (int i = 0; i < 4; ++i) cudaFree(outp[i]);
-      for (void* q : {(void*)p.ic_poff, (void*)p.ic_soff, (void*)p.ic_pbase, (void*)p.ic_sbase, (void*)p.ic_pval,
-                      (void*)p.ic_sval})
-        cudaFree(q);
-      p.ic_poff = p.ic_soff = nullptr;
-      p.ic_pbase = p.ic_sbase = nullptr;
-      p.ic_pval = nullptr;
-      p.ic_sval = nullptr;
-      cudaGetLastError();
-    }
-  };
-  for (int i = 0; i < 4; ++i)
-    if ((rc = dalloc(h, (void**)&len[i], sizeof(int64_t) * (nrows + 1), nullptr)) ||
-        (rc = dalloc(h, (void**)&outp[i], sizeof(int64_t) * (nrows + 1), nullptr))) {
-      drop(true);
-      return SFLSQR_OK;
-    }
-  cudaStream_t s = h->stream;
-  for (int i = 0; i < 4; ++i) CU(h, cudaMemsetAsync(len[i] + nrows, 0, sizeof(int64_t), s));
-  const int g = (int)std::min<int64_t>((nrows + 255) / 256, 148 * 16);
-  k_ic_len<<<g, 256, 0, s>>>(nrows, p.prp, p.srp, len[0], len[1], len[2], len[3]);
-  cub::DeviceScan::ExclusiveSum(nullptr, tb, len[0], outp[0], nrows + 1, s);
-  if ((rc = dalloc(h, &tmp, tb, nullptr))) {
-    drop(true);
-    return SFLSQR_OK;
-  }
-  for (int i = 0; i < 4; ++i) cub::DeviceScan::ExclusiveSum(tmp, tb, len[i], outp[i], nrows + 1, s);
-  int64_t tot[4];
-  for (int i = 0; i < 4; ++i) CU(h, cudaMemcpyAsync(&tot[i], outp[i] + nrows, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  CU(h, cudaStreamSynchronize(s));
-  if ((rc = dalloc(h, (void**)&flag, sizeof(int), nullptr)) ||
-      (rc = dalloc(h, (void**)&p.ic_poff, sizeof(uint16_t) * std::max<int64_t>(tot[0], 1), nullptr)) ||
-      (rc = dalloc(h, (void**)&p.ic_pval, sizeof(double2) * std::max<int64_t>(tot[0], 1), nullptr)) ||
-      (rc = dalloc(h, (void**)&p.ic_pbase, sizeof(int) * std::max<int64_t>(tot[1], 4), nullptr)) ||
-      (rc = dalloc(h, (void**)&p.ic_soff, sizeof(uint16_t) * std::max<int64_t>(tot[2], 1), nullptr)) ||
-      (rc = dalloc(h, (void**)&p.ic_sval, sizeof(double) * std::max<int64_t>(tot[2], 1), nullptr)) ||
-      (rc = dalloc(h, (void**)&p.ic_sbase, sizeof(int) * std::max<int64_t>(tot[3], 4), nullptr))) {
-    drop(true);
-    return SFLSQR_OK;  // no room: the pair-CSR arrays serve
-  }
-  CU(h, cudaMemsetAsync(flag, 0, sizeof(int), s));  // escape-slot counter
-  // padding entries are never read (counts); zero them anyway
-  CU(h, cudaMemsetAsync(p.ic_poff, 0, sizeof(uint16_t) * tot[0], s));
-  CU(h, cudaMemsetAsync(p.ic_pval, 0, sizeof(double2) * tot[0], s));
-  CU(h, cudaMemsetAsync(p.ic_soff, 0, sizeof(uint16_t) * tot[2], s));
-  CU(h, cudaMemsetAsync(p.ic_sval, 0, sizeof(double) * tot[2], s));
-  const int gw = (int)std::min<int64_t>((nrows + 7) / 8, 148 * 64);
-  // pass 1 counts the escaped groups of both streams; pass 2 (only if there are any) writes them
-  int nesc[2] = {0, 0};
-  for (int pass = 0; pass < 2; ++pass) {
-    int* pe = pass ? p.ic_pesc : nullptr;
-    int* se = pass ? p.ic_sesc : nullptr;
-    CU(h, cudaMemsetAsync(flag, 0, sizeof(int), s));
-    k_ic_fill<true><<<gw, 256, 0, s>>>(nrows, p.prp, p.pcol, p.pval, outp[0], outp[1], p.ic_poff, p.ic_pbase, p.ic_pval,
-                                       flag, pe);
-    CU(h, cudaMemcpyAsync(&nesc[0], flag, sizeof(int), cudaMemcpyDeviceToHost, s));
-    CU(h, cudaMemsetAsync(flag, 0, sizeof(int), s));
-    k_ic_fill<false><<<gw, 256, 0, s>>>(nrows, p.srp, p.scol, p.sval, outp[2], outp[3], p.ic_soff, p.ic_sbase,
-                                        p.ic_sval, flag, se);
-    CU(h, cudaMemcpyAsync(&nesc[1], flag, sizeof(int), cudaMemcpyDeviceToHost, s));
-    CU(h, cudaStreamSynchronize(s));
-    if ((rc = check_launch(h))) {
-      drop(true);
-      return rc;
-    }
-    if (pass == 1 || (nesc[0] == 0 && nesc[1] == 0)) break;
-    if ((rc = dalloc(h, (void**)&p.ic_pesc, sizeof(int) * 16 * std::max(nesc[0], 1), nullptr)) ||
-        (rc = dalloc(h, (void**)&p.ic_sesc, sizeof(int) * 16 * std::max(nesc[1], 1), nullptr))) {
-      cudaFree(p.ic_pesc);
-      cudaFree(p.ic_sesc);
-      p.ic_pesc = p.ic_sesc = nullptr;
-      drop(true);
-      return SFLSQR_OK;
-    }
-  }
-  p.ic_nesc = (int64_t)nesc[0] + nesc[1];
-  drop(false);
-  p.ic_pstart = outp[0];
-  p.ic_pbst = outp[1];
-  p.ic_sstart = outp[2];
-  p.ic_sbst = outp[3];
-  p.ic_pent = tot[0];
-  p.ic_pgr = tot[1];
-  p.ic_sent = tot[2];
-  p.ic_sgr = tot[3];
-  // the IC16 streams replace the pair-CSR columns and values (prp / srp stay: the row counts)
-  cudaFree(p.pcol);
-  cudaFree(p.pval);
-  cudaFree(p.scol);
-  cudaFree(p.sval);
-  p.pcol = nullptr;
-  p.pval = nullptr;
-  p.scol = nullptr;
-  p.sval = nullptr;
-  p.ic = true;
-  return SFLSQR_OK;
-}
-
 int build_sell(sflsqr_t* h, int64_t nrows, PCSR& p) {
   if (!p.ok || !p.interp || nrows < 1) return SFLSQR_OK;
   const int64_t nsl = (nrows + kSellC - 1) / kSellC;
@@ -1335,10 +1165,10 @@ int build_formats(sflsqr_t* h) {
   int rc;
   if (h->spmv_mode == 16 || h->spmv_mode == 17) {
     const bool al = h->spmv_mode == 17;
-    if ((!h->pa.ok || h->pa.aligned != al || h->pa.interp || h->pa.ic) &&
+    if ((!h->pa.ok || h->pa.aligned != al || h->pa.interp) &&
         (rc = build_pcsr(h, h->m_loc, h->a_rowptr, h->a_col, h->a_val, h->pa, al)))
       return rc;
-    if ((!h->pt.ok || h->pt.aligned != al || h->pt.interp || h->pt.ic) &&
+    if ((!h->pt.ok || h->pt.aligned != al || h->pt.interp) &&
         (rc = build_pcsr(h, h->t_rows, h->t_rowptr, h->t_col, h->t_val, h->pt, al)))
       return rc;
     return SFLSQR_OK;
@@ -1360,10 +1190,7 @@ int build_formats(sflsqr_t* h) {
     int r = build_pcsr(h, nrows, rp, col, val, p, false, 0.75);
     if (!r && p.ok && h->pcsr_interp) r = try_interp(h, p);
     if (!r && p.ok && p.interp && h->sell) r = build_sell(h, nrows, p);
-    if (!r && !p.ok) {
-      r = build_pcsr(h, nrows, rp, col, val, p, true, 0.20);
-      if (!r && p.ok && h->ic16) r = build_ic(h, nrows, p);
-    }
+    if (!r && !p.ok) r = build_pcsr(h, nrows, rp, col, val, p, true, 0.20);
     if (r == SFLSQR_E_OOM) {
       free_pcsr(p);
       cudaGetLastError();
@@ -1910,7 +1737,6 @@ int sflsqr_create(sflsqr_t** out, const sflsqr_opts* o) {
   h->pcsr_interp = !(kn & SFLSQR_KNOB_NO_INTERP);
   h->sell = !(kn & SFLSQR_KNOB_NO_SELL);
   h->ell_c16 = !(kn & SFLSQR_KNOB_NO_ELL_C16);
-  h->ic16 = !(kn & SFLSQR_KNOB_NO_IC16);
   h->cgs_selective = !(kn & SFLSQR_KNOB_CGS_ALWAYS2);
   h->spmv_grid_delta = (kn & SFLSQR_KNOB_FULL_SPMV_GRID) ? 0 : 1;
   h->keep_csr = (kn & SFLSQR_KNOB_KEEP_CSR) != 0;
@@ -2446,8 +2272,8 @@ int sflsqr_get_info(sflsqr_t* h, sflsqr_info* info) {
   const int mode_t = h->spmv_mode >= 0 ? h->spmv_mode : (h->pt.ok ? 16 : 14);
   info->a_pairs = ((mode_a == 16 || mode_a == 17) && h->pa.ok) ? h->pa.npairs : 0;
   info->t_pairs = ((mode_t == 16 || mode_t == 17) && h->pt.ok) ? h->pt.npairs : 0;
-  info->a_fmt = info->a_pairs ? (h->pa.aligned ? (h->pa.ic ? 5 : 2) : (h->pa.interp ? (h->pa.ell ? 4 : 3) : 1)) : 0;
-  info->t_fmt = info->t_pairs ? (h->pt.aligned ? (h->pt.ic ? 5 : 2) : (h->pt.interp ? (h->pt.ell ? 4 : 3) : 1)) : 0;
+  info->a_fmt = info->a_pairs ? (h->pa.aligned ? 2 : (h->pa.interp ? (h->pa.ell ? 4 : 3) : 1)) : 0;
+  info->t_fmt = info->t_pairs ? (h->pt.aligned ? 2 : (h->pt.interp ? (h->pt.ell ? 4 : 3) : 1)) : 0;
   info->knobs = h->knobs;
   info->graph = (h->gexec && h->o.use_graph) ? 1 : 0;
   info->csr_kept = (h->csr_freed_a ? 0 : 1) | (h->csr_freed_t ? 0 : 2);

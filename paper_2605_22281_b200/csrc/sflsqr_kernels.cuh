@@ -664,255 +664,6 @@ __global__ void __launch_bounds__(256) k_pcsr_rows(int64_t nrows, const int64_t*
   }
 }
 
-// ------------------------------------------------------------------ IC16: interleaved chunks, 16-bit columns
-// The streams of an aligned pair-CSR operator (pairs: column + two values; singletons: column +
-// value) re-laid for the half-warp-per-row product: a row's stream is cut into chunks of 64 entries
-// = 4 gather steps of 16 lanes.  Entry e = 64 c + 16 u + L of a full chunk c is stored at
-// start + 64 c + 4 L + u, so lane L fetches the 4 entries it gathers in the chunk with one 8-byte
-// load of 16-bit column offsets and one (singletons) or two (pairs) 32-byte value loads; the gather
-// step u of the chunk still covers 16 consecutive entries of the ray (the gather locality and the
-// per-lane summation order of the plain layout: the same row sums bit for bit).  Column = base of
-// the entry's 16-entry group (one int32 per group, the group's smallest column) + offset; a group
-// spanning more than 65535 columns (a sparse stream: e.g. the pairs of a near-vertical ray, rows
-// sorted by column) is escaped: its base is -(slot + 1) and its 16 columns are plain int32 in
-// esc[slot + lane] (config 3: 0.8 % of A's groups, 6 % of A^T's).  The tail
-// of a row (its last cnt mod 64 entries) keeps the plain order; every row's stream starts at a
-// multiple of 4 entries.  10 B (singletons) / 18 B (pairs) + 4 B per 16 entries instead of 12 / 20 B,
-// and 1 + 1 (+1) load instructions per lane per 4 entries instead of 4 + 4.
-struct ICPart {
-  const int64_t* pstart = nullptr;  // per row: first pair entry (multiple of 4)
-  const int64_t* pbst = nullptr;    // per row: first pair group base
-  const int64_t* prp = nullptr;     // pair counts: prp[r + 1] - prp[r]
-  const uint16_t* poff = nullptr;
-  const int* pbase = nullptr;
-  const int* pesc = nullptr;        // escaped groups' int32 columns
-  const double2* pval = nullptr;
-  const int64_t* sstart = nullptr;
-  const int64_t* sbst = nullptr;
-  const int64_t* srp = nullptr;
-  const uint16_t* soff = nullptr;
-  const int* sbase = nullptr;
-  const int* sesc = nullptr;
-  const double* sval = nullptr;
-};
-
-__device__ __forceinline__ uint2 ld_stream_u16x4(const uint16_t* p) {
-  uint2 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
-  return r;
-}
-__device__ __forceinline__ void ld_stream_d4(const double* p, double* v) {
-  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.f64 {%0,%1,%2,%3}, [%4];"
-               : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
-               : "l"(p));
-}
-__device__ __forceinline__ int u16_of(uint2 o, int u) {
-  const unsigned w = u < 2 ? o.x : o.y;
-  return (int)((u & 1) ? (w >> 16) : (w & 0xffffu));
-}
-
-// One IC16 stream of one row into sum (lane sl of the row's half-warp).  PAIR: value pairs at
-// columns (c, c + 1), gathered as one 16-byte load when X16 (x 16-byte aligned).
-template <bool PAIR, bool X16>
-__device__ __forceinline__ double ic_stream(int64_t st, int cnt, int64_t bst, const uint16_t* __restrict__ off,
-                                            const int* __restrict__ base, const int* __restrict__ esc,
-                                            const void* __restrict__ vals, const double* __restrict__ x, int sl,
-                                            double sum) {
-  // column of lane sl's entry in a group with base b: b + offset, or the escaped group's int32
-  auto colof = [&](int b, int o) -> int { return b >= 0 ? b + o : __ldg(esc + (-(int64_t)b - 1) + sl); };
-  const int nfull = cnt >> 6;
-  const double* __restrict__ dv = reinterpret_cast<const double*>(vals);
-  constexpr int VW = PAIR ? 8 : 4;  // doubles per lane per chunk
-  auto gather = [&](int col, double v0, double v1) {
-    if (PAIR) {
-      double x0, x1;
-      if (X16) {
-        const double2 xx = __ldg(reinterpret_cast<const double2*>(x + col));
-        x0 = xx.x;
-        x1 = xx.y;
-      } else {
-        x0 = __ldg(x + col);
-        x1 = __ldg(x + col + 1);
-      }
-      sum = fma(v1, x1, fma(v0, x0, sum));
-    } else {
-      sum = fma(v0, __ldg(x + col), sum);
-    }
-  };
-  if (nfull > 0) {
-    int4 bn = __ldg(reinterpret_cast<const int4*>(base + bst));
-    uint2 on = ld_stream_u16x4(off + st + 4 * sl);
-    double vn[VW];
-    ld_stream_d4(dv + (PAIR ? 2 : 1) * (st + 4 * sl), vn);
-    if (PAIR) ld_stream_d4(dv + 2 * (st + 4 * sl) + 4, vn + 4);
-    for (int c = 0; c < nfull; ++c) {
-      const int4 b = bn;
-      const uint2 o = on;
-      double v[VW];
-#pragma unroll
-      for (int i = 0; i < VW; ++i) v[i] = vn[i];
-      if (c + 1 < nfull) {  // the next chunk's streams in flight during this chunk's gathers
-        const int64_t e1 = st + 64 * (int64_t)(c + 1) + 4 * sl;
-        bn = __ldg(reinterpret_cast<const int4*>(base + bst + 4 * (c + 1)));
-        on = ld_stream_u16x4(off + e1);
-        ld_stream_d4(dv + (PAIR ? 2 : 1) * e1, vn);
-        if (PAIR) ld_stream_d4(dv + 2 * e1 + 4, vn + 4);
-      }
-      const int bb[4] = {b.x, b.y, b.z, b.w};
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int col = colof(bb[u], u16_of(o, u));
-        if (PAIR)
-          gather(col, v[2 * u], v[2 * u + 1]);
-        else
-          gather(col, v[u], 0.0);
-      }
-    }
-  }
-  const int t = cnt - 64 * nfull;
-  if (t > 0) {
-    const int64_t e0 = st + 64 * (int64_t)nfull;
-    const int* __restrict__ tb = base + bst + 4 * nfull;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int e = 16 * u + sl;
-      if (e < t) {
-        const int col = colof(__ldg(tb + u), (int)off[e0 + e]);
-        if (PAIR) {
-          const double2 v = ld_stream_d2(reinterpret_cast<const double2*>(vals) + e0 + e);
-          gather(col, v.x, v.y);
-        } else {
-          gather(col, ld_stream_d(dv + e0 + e), 0.0);
-        }
-      }
-    }
-  }
-  return sum;
-}
-
-// y = M x on an IC16 operator: half a warp per row, 32 adjacent rows per 512-thread CTA (as
-// k_spmv_csr_pf<16, 4, 16, EPI, 5>), the row's pairs then its singletons; the EPI epilogues of
-// k_spmv_csr_pf (GKB kinds 1-3, peer reduce-scatter kind 4).  X16: the gathered vector is 16-byte
-// aligned (pairs gathered as one 16-byte load; else two 8-byte loads).
-template <bool EPI = false, bool X16 = true>
-__global__ void __launch_bounds__(512, 2) k_spmv_ic16(const DevState* st, int64_t nrows, ICPart IC,
-                                                      const double* __restrict__ x_base, int64_t x_ld, int x_koff,
-                                                      double* y, SpmvEpi E = SpmvEpi()) {
-  pdl_wait();
-  if (st && st->done) return;
-  double ea = 1.0, ec = 0.0, nrm = 0.0;
-  if (EPI) epi_coefs(E, st, ea, ec);
-  const double* __restrict__ x = kvec(st, x_base, x_ld, x_koff);
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int sl = lane & 15, sub = lane >> 4;
-  for (int64_t r0 = (int64_t)blockIdx.x * 32; r0 < nrows; r0 += (int64_t)gridDim.x * 32) {
-    const int64_t row = r0 + (int64_t)wid * 2 + sub;
-    double sum = 0.0;
-    if (row < nrows) {
-      const int np = (int)(IC.prp[row + 1] - IC.prp[row]);
-      const int ns = (int)(IC.srp[row + 1] - IC.srp[row]);
-      sum = ic_stream<true, X16>(IC.pstart[row], np, IC.pbst[row], IC.poff, IC.pbase, IC.pesc, IC.pval, x, sl, sum);
-      sum = ic_stream<false, false>(IC.sstart[row], ns, IC.sbst[row], IC.soff, IC.sbase, IC.sesc, IC.sval, x, sl, sum);
-    }
-#pragma unroll
-    for (int o = 8; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    if (sl == 0 && row < nrows) {
-      if (EPI && E.kind == 4) {
-        const int64_t g = row / E.nmax;
-        E.peers[g][(int64_t)E.src * E.nmax + (row - g * E.nmax)] = sum;
-      } else {
-        if (EPI) {
-          sum = E.kind == 3 ? sum * ea : fma(sum, ea, -ec * E.aux[row]);
-          nrm = fma(sum, sum, nrm);
-        }
-        y[row] = sum;
-      }
-    }
-  }
-  if (EPI && E.kind != 4) {
-    __shared__ double sh[33];
-    __shared__ int s_last;
-    nrm = block_sum<512>(nrm, sh);
-    if (threadIdx.x == 0) E.part[(size_t)E.slot_out * kVecBlocks + blockIdx.x] = nrm;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = (atomicAdd(E.ctr + E.ctr_idx, 1) == (int)gridDim.x - 1);
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    const double* pp = E.part + (size_t)E.slot_out * kVecBlocks;
-    double v = 0.0;
-    for (int b = threadIdx.x; b < (int)gridDim.x; b += 512) v += __ldcg(pp + b);
-    v = block_sum<512>(v, sh);
-    if (threadIdx.x == 0) {
-      E.scal[E.slot_out] = v;
-      E.ctr[E.ctr_idx] = 0;
-    }
-  }
-}
-
-// IC16 build, pass 1: per row the padded stream length (multiple of 4) and the group-base count
-// (4 per started chunk of 64) of the pair and singleton streams.
-__global__ void __launch_bounds__(256) k_ic_len(int64_t nrows, const int64_t* __restrict__ prp,
-                                                const int64_t* __restrict__ srp, int64_t* plen, int64_t* pbl,
-                                                int64_t* slen, int64_t* sbl) {
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t np = prp[r + 1] - prp[r], ns = srp[r + 1] - srp[r];
-    plen[r] = (np + 3) & ~(int64_t)3;
-    pbl[r] = 4 * ((np + 63) / 64);
-    slen[r] = (ns + 3) & ~(int64_t)3;
-    sbl[r] = 4 * ((ns + 63) / 64);
-  }
-}
-
-// IC16 build, pass 2 (warp per row, one stream): each half-warp takes a 16-entry group, the group
-// base is its smallest column, entries go to their interleaved (full chunks) or plain (tail)
-// position.  A group spanning >= 65536 columns takes an escape slot (*nesc counts them; with esc
-// given, its columns go to esc[16 slot + lane] and its base is -(16 slot + 1)).
-template <bool PAIR>
-__global__ void __launch_bounds__(256) k_ic_fill(int64_t nrows, const int64_t* __restrict__ rp,
-                                                 const int* __restrict__ col, const void* __restrict__ val,
-                                                 const int64_t* __restrict__ start, const int64_t* __restrict__ bst,
-                                                 uint16_t* off, int* base, void* oval, int* nesc, int* esc) {
-  const int lane = threadIdx.x & 31, hl = lane & 15, half = lane >> 4;
-  for (int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < nrows;
-       row += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int64_t s0 = rp[row];
-    const int cnt = (int)(rp[row + 1] - s0);
-    const int nfull = cnt >> 6;
-    const int ngroups = (cnt + 15) >> 4;
-    for (int g0 = 0; g0 < ngroups; g0 += 2) {
-      const int g = g0 + half;
-      const int e = 16 * g + hl;
-      const bool ok = g < ngroups && e < cnt;
-      const int c = ok ? col[s0 + e] : 0;
-      unsigned mn = ok ? (unsigned)c : 0xffffffffu, mx = ok ? (unsigned)c : 0u;
-#pragma unroll
-      for (int o = 8; o > 0; o >>= 1) {
-        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      }
-      const bool wide = mx > mn && mx - mn > 65535u;
-      int slot = 0;
-      if (g < ngroups && hl == 0) {
-        if (wide) slot = atomicAdd(nesc, 1);
-        base[bst[row] + g] = wide ? -(16 * slot + 1) : (int)mn;
-      }
-      slot = __shfl_sync(0xffffffffu, slot, half << 4);
-      if (wide && esc && ok) esc[16 * (int64_t)slot + hl] = c;
-      if (ok) {
-        const int ch = e >> 6;
-        const int64_t pos = start[row] + (ch < nfull ? 64 * (int64_t)ch + 4 * (e & 15) + ((e >> 4) & 3) : (int64_t)e);
-        off[pos] = (uint16_t)((unsigned)c - mn);
-        if (PAIR)
-          reinterpret_cast<double2*>(oval)[pos] = reinterpret_cast<const double2*>(val)[s0 + e];
-        else
-          reinterpret_cast<double*>(oval)[pos] = reinterpret_cast<const double*>(val)[s0 + e];
-      }
-    }
-  }
-}
-
 // Interpolation pairs: every pair's first value is 1 - (its second value), bitwise (a linear-
 // interpolation backprojector's weights: L1646).  flag <- 1 if some pair is not; f <- second values.
 __global__ void __launch_bounds__(256) k_pcsr_interp(int64_t npairs, const double2* __restrict__ pval, double* f,

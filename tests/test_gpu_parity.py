@@ -588,11 +588,11 @@ def test_default_spmv_format_rule():
     inf = s.get_info()
     s.close()
     assert inf["t_fmt"] == 4 and inf["t_pairs"] >= 0.375 * p.T.nnz    # B: interpolation pairs (1 - f, f), sliced ELL
-    assert inf["a_fmt"] == 5 and inf["a_pairs"] >= 0.2 * p.A.nnz      # A: aligned pairs, re-laid as IC16
+    assert inf["a_fmt"] == 2 and inf["a_pairs"] >= 0.2 * p.A.nnz
     s = solver_for_problem(p, spec, maxit=3, eta=0.0, method="lsqr")
     inf = s.get_info()
     s.close()
-    assert inf["a_fmt"] == 5 and inf["t_fmt"] == 4
+    assert inf["a_fmt"] == 2 and inf["t_fmt"] == 4
     assert inf["csr_kept"] == 0                            # both copies serve: the uploaded CSR is released
     s = solver_for_problem(p, spec, maxit=3, eta=0.0)
     with pytest.raises(SflsqrError) as e:                  # forcing a format needs the CSR
@@ -636,56 +636,6 @@ def test_interpolation_pairs_bitwise_equal_to_pair_csr():
     s.set_operator(m, n, rp, col, val, t=(rp, col, val) if m == n else None)
     assert s.get_info()["a_fmt"] in (0, 1, 2)
     s.close()
-
-
-def _ic_csr(seed, m, n, wide=False):
-    """Rows of 0..300 entries (lengths around the 64-entry chunks: 0, 1, 15, 16, 63, 64, 65, 127, 128,
-    129, ...) made of short column runs (aligned pairs mixed with singletons); wide: rows whose 16-entry
-    groups span more than 65535 columns (escaped groups: int32 columns)."""
-    rng = np.random.default_rng(seed)
-    special = [0, 1, 15, 16, 17, 63, 64, 65, 127, 128, 129, 191, 192, 255, 256, 300]
-    rows = []
-    for i in range(m):
-        L = special[i % len(special)] if i < 4 * len(special) else int(rng.integers(60, 300))
-        cols, c = [], int(rng.integers(0, 50))
-        while len(cols) < L:
-            run = int(rng.choice([1, 1, 1, 2, 2, 3]))
-            cols.extend(range(c, c + run))
-            c += run + int(rng.integers(1, 40))
-        cols = [cc % n for cc in cols[:L]]
-        rows.append(np.array(cols, dtype=np.int64))
-    if wide:
-        rows[5] = np.array([0, 70000] + list(range(100, 162)), dtype=np.int64)          # first full-chunk group
-        rows[6] = np.array(list(range(1000, 1080, 3)) + [99000], dtype=np.int64)        # tail group
-        rows[7] = np.array([2 * i * 5000 for i in range(20)], dtype=np.int64) % n        # every group
-    rowptr = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.int64)
-    col = np.concatenate(rows).astype(np.int32)
-    return rowptr, col, rng.standard_normal(col.size)
-
-
-@pytest.mark.parametrize("wide", [False, True])
-def test_ic16_bitwise_equal_to_aligned_pairs(wide):
-    # IC16 re-lays the aligned pair-CSR streams (interleaved 64-entry chunks, 16-bit offsets); every
-    # lane sums the same entries in the same order, so the products agree bit for bit with the plain
-    # aligned-pair kernel (SFLSQR_KNOB_NO_IC16), and with the oracle to rounding (the odd-alignment
-    # gathers run in the solver tests with odd n: test_pair_formats_odd_dimensions)
-    from paper_2605_22281_b200 import SFLSQR
-    m, n = 1200, 100003
-    rp, col, val = _ic_csr(21, m, n, wide)
-    A = OracleCSR(m, n, rp, col, val)
-    rng = np.random.default_rng(22)
-    x = rng.standard_normal(n + 1)
-    out = {}
-    for kn in ([], ["no_ic16"]):
-        s = SFLSQR(maxit=4, knobs=kn)
-        s.set_operator(m, n, rp, col, val)
-        out[tuple(kn)] = (s.get_info()["a_fmt"], s.debug_apply(0, x[:n]), s.debug_apply(0, x[1:]))
-        s.close()
-    assert out[("no_ic16",)][0] == 2 and out[()][0] == 5
-    for i in (1, 2):
-        assert np.array_equal(out[()][i], out[("no_ic16",)][i])
-    absref = OracleCSR(m, n, rp, col, np.abs(val)).matvec(np.abs(x[:n]))
-    assert np.all(np.abs(out[()][1] - A.matvec(x[:n])) <= 1e-14 * absref + 1e-300)
 
 
 def _interp_csr(seed, nrows, ncols, singles=True):
@@ -757,7 +707,7 @@ def test_pair_formats_odd_dimensions():
     tr, sk = s.get_residual_norms()
     x = s.get_x()
     s.close()
-    assert inf["a_fmt"] == 5 and inf["t_fmt"] == 4, (inf["a_fmt"], inf["t_fmt"])
+    assert inf["a_fmt"] == 2 and inf["t_fmt"] == 4, (inf["a_fmt"], inf["t_fmt"])
     assert np.max(np.abs(tr - np.array(r.true_res)) / np.array(r.true_res)) < 1e-9
     assert np.max(np.abs(sk - np.array(r.sketch_res)) / np.array(r.sketch_res)) < 1e-9
     assert np.linalg.norm(x - r.x) / np.linalg.norm(r.x) < 1e-6
