@@ -142,8 +142,7 @@ extern "C" {
 #define SFLSQR_KNOB_DEBUG_POISON 0x800 /* fill every solve buffer with NaN bytes at allocation
                                             (a read before write then shows in the results)   */
 #define SFLSQR_KNOB_NO_ELL_C16 0x1000 /* 32-bit columns in the sliced-ELL interpolation pairs   */
-#define SFLSQR_KNOB_NO_FUSED_DOTS 0x2000 /* window dots by k_orth_dots, not in the product's epilogue */
-#define SFLSQR_KNOB_ALL 0x3fff
+#define SFLSQR_KNOB_ALL 0x1fff
 
 /* opts.history bits */
 #define SFLSQR_HIST_TRUE_RES 1 /* record ||b - A x_k|| every iteration              */

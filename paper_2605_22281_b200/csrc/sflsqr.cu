@@ -145,9 +145,6 @@ struct sflsqr {
   Prof prof;
   bool res_overlap = true;  // W-path residual on the side stream (SFLSQR_KNOB_RES_MAIN / _RES_SIDE force it)
   bool res_overlap_forced = false;
-  // the window dots of the next z-side orthogonalisation were taken in the epilogue of the T
-  // product that formed z (FuseDots, side 0): its k_orth_dots launch is skipped
-  bool z_dots_fused = false;
 };
 
 namespace {
@@ -384,8 +381,6 @@ void launch_pdl(sflsqr_t* h, void (*kern)(KArgs...), dim3 grid, dim3 block, size
 
 bool launch_pairs_epi(sflsqr_t* h, int which, const double* x, int64_t x_ld, double* y, const SpmvEpi& E, int cls,
                       double extra, int grid);
-bool enqueue_apply(sflsqr_t* h, int which, const DevState* st, const double* x, int64_t x_ld, int x_koff, double* y,
-                   int cls, const FuseDots* fd = nullptr);
 
 // Bytes of the sliced-ELL interpolation pairs a product streams: per entry the column (4 B, or a 2 B
 // offset + a 4 B base per 32 entries) and f (8 B); the singleton CSR; per-row counts; slice offsets.
@@ -408,8 +403,8 @@ bool runs_on_pairs(const sflsqr_t* h, int which) {
 // Plain CSR: half-warp rows, 32 adjacent rows per 512-thread CTA, 4 CTAs per SM, the next 4
 // chunks' indices / values loaded before the current gathers (measured on configs 3-4, DESIGN.md
 // §5).  Every format sums each row in a fixed order: results are reproducible run to run.
-bool enqueue_apply(sflsqr_t* h, int which, const DevState* st, const double* x, int64_t x_ld, int x_koff, double* y,
-                   int cls, const FuseDots* fd) {
+void enqueue_apply(sflsqr_t* h, int which, const DevState* st, const double* x, int64_t x_ld, int x_koff, double* y,
+                   int cls) {
   const int64_t nrows = which == 0 ? h->m_loc : h->t_rows;
   if (h->blur) {
     const int64_t nn = (int64_t)h->bH * h->bW;
@@ -422,50 +417,34 @@ bool enqueue_apply(sflsqr_t* h, int which, const DevState* st, const double* x, 
       Launch L(h, cls, 16.0 * nn);
       k_blur_cols<<<grid, 256, 0, h->stream>>>(st, h->bH, h->bW, h->brad, h->taps, h->blur_tmp, y);
     }
-    return false;
+    return;
   }
   const int64_t nnz = which == 0 ? h->nnz_a : h->nnz_t;
   const int64_t xlen = which == 0 ? (h->world > 1 ? h->world * h->n_max : h->n)
                                   : (h->tkind == T_ROWSHARD ? h->world * h->m_max : h->m_loc);
-  const PCSR& pc = which == 0 ? h->pa : h->pt;
-  const bool fuse = fd && !(runs_on_pairs(h, which) && pc.ell);
-  // the fused dots read the window vectors at the product's rows (at most ell + 1 of them)
-  const double epi = fuse ? 8.0 * (h->P.ell + 1) * nrows : 0.0;
-  const double bytes = 12.0 * nnz + 8.0 * (nrows + 1) + 8.0 * xlen + 8.0 * nrows + epi;
+  const double bytes = 12.0 * nnz + 8.0 * (nrows + 1) + 8.0 * xlen + 8.0 * nrows;
   Launch L(h, cls, bytes);
   auto grid_for = [&](int rows_per_cta, int per_sm) {
     const int64_t want = (nrows + rows_per_cta - 1) / rows_per_cta;
     return (int)std::max<int64_t>(1, std::min<int64_t>(want, 148 * per_sm - h->spmv_grid_delta));
   };
-  SpmvEpi E = SpmvEpi();
-  if (fuse) {
-    E.part = h->P.part;
-    E.scal = h->P.scal;
-    E.ctr = h->P.ctr;
-    E.ctr_idx = fd->side == 0 ? CTR_ZDOTS : CTR_WDOTS;
-    E.fd = *fd;
-  }
+  const PCSR& pc = which == 0 ? h->pa : h->pt;
   if (!runs_on_pairs(h, which)) {
     const int64_t* rp = which == 0 ? h->a_rowptr : h->t_rowptr;
     const int32_t* col = which == 0 ? h->a_col : h->t_col;
     const double* val = which == 0 ? h->a_val : h->t_val;
-    if (fuse)
-      launch_pdl(h, k_spmv_csr_pf<16, 4, 16, 2>, grid_for(32, 2), 512, 0, h->stream, st, nrows, rp, (const int*)col, val,
-                 x, x_ld, x_koff, y, E, PairPart());
-    else
-      launch_pdl(h, k_spmv_csr_pf<16, 4, 16>, grid_for(32, 4), 512, 0, h->stream, st, nrows, rp, (const int*)col, val, x,
-                 x_ld, x_koff, y, SpmvEpi(), PairPart());
-    return fuse;
+    launch_pdl(h, k_spmv_csr_pf<16, 4, 16>, grid_for(32, 4), 512, 0, h->stream, st, nrows, rp, (const int*)col, val, x,
+               x_ld, x_koff, y, SpmvEpi(), PairPart());
+    return;
   }
   // pair-CSR: 20 bytes per pair of nonzeros, 12 per singleton, two row pointer arrays
-  L.bytes_override(20.0 * pc.npairs + 12.0 * pc.nsingles + 16.0 * (nrows + 1) + 8.0 * xlen + 8.0 * nrows + epi);
+  L.bytes_override(20.0 * pc.npairs + 12.0 * pc.nsingles + 16.0 * (nrows + 1) + 8.0 * xlen + 8.0 * nrows);
   PairPart PP;
   PP.rowptr = pc.prp;
   PP.col = pc.pcol;
   PP.val = pc.pval;
   PP.f = pc.f;
-  if (pc.interp)
-    L.bytes_override(12.0 * pc.npairs + 12.0 * pc.nsingles + 16.0 * (nrows + 1) + 8.0 * xlen + 8.0 * nrows + epi);
+  if (pc.interp) L.bytes_override(12.0 * pc.npairs + 12.0 * pc.nsingles + 16.0 * (nrows + 1) + 8.0 * xlen + 8.0 * nrows);
   // aligned pairs gather one 16-byte value pair: needs x (any k-relative column) 16-byte aligned
   const bool x16 = ((uintptr_t)x % 16 == 0) && (x_ld % 2 == 0);
   if (pc.ell) {  // sliced-ELL interpolation pairs (pair-CSR arrays released after the build)
@@ -480,35 +459,16 @@ bool enqueue_apply(sflsqr_t* h, int which, const DevState* st, const double* x, 
       launch_pdl(h, k_spmv_sell_ip<4, false, false>, g, 512, 0, h->stream, st, nrows, (const int64_t*)pc.soff,
                  (const int*)pc.rcnt, (const int*)pc.ecol, (const uint16_t*)nullptr, (const double*)pc.ef,
                  (const int64_t*)pc.srp, (const int*)pc.scol, (const double*)pc.sval, x, x_ld, x_koff, y, SpmvEpi());
-    return false;
-  }
-  const int g2 = grid_for(32, 2);
-  const int64_t* srp = pc.srp;
-  const int* scol = pc.scol;
-  const double* sval = pc.sval;
-  if (pc.interp) {
-    if (fuse)
-      launch_pdl(h, k_spmv_csr_pf<16, 4, 16, 2, 6>, g2, 512, 0, h->stream, st, nrows, srp, scol, sval, x, x_ld, x_koff, y,
-                 E, PP);
-    else
-      launch_pdl(h, k_spmv_csr_pf<16, 4, 16, 0, 6>, g2, 512, 0, h->stream, st, nrows, srp, scol, sval, x, x_ld, x_koff, y,
-                 SpmvEpi(), PP);
-  } else if (pc.aligned && x16) {
-    if (fuse)
-      launch_pdl(h, k_spmv_csr_pf<16, 4, 16, 2, 5>, g2, 512, 0, h->stream, st, nrows, srp, scol, sval, x, x_ld, x_koff, y,
-                 E, PP);
-    else
-      launch_pdl(h, k_spmv_csr_pf<16, 4, 16, 0, 5>, g2, 512, 0, h->stream, st, nrows, srp, scol, sval, x, x_ld, x_koff, y,
-                 SpmvEpi(), PP);
-  } else {
-    if (fuse)
-      launch_pdl(h, k_spmv_csr_pf<16, 4, 16, 2, 4>, g2, 512, 0, h->stream, st, nrows, srp, scol, sval, x, x_ld, x_koff, y,
-                 E, PP);
-    else
-      launch_pdl(h, k_spmv_csr_pf<16, 4, 16, 0, 4>, g2, 512, 0, h->stream, st, nrows, srp, scol, sval, x, x_ld, x_koff, y,
-                 SpmvEpi(), PP);
-  }
-  return fuse;
+  } else if (pc.interp)
+    k_spmv_csr_pf<16, 4, 16, false, 6><<<grid_for(32, 2), 512, 0, h->stream>>>(
+        st, nrows, pc.srp, pc.scol, pc.sval, x, x_ld, x_koff, y, SpmvEpi(), PP);
+  else if (pc.aligned && x16)
+    launch_pdl(h, k_spmv_csr_pf<16, 4, 16, false, 5>, grid_for(32, 2), 512, 0, h->stream, st, nrows,
+               (const int64_t*)pc.srp, (const int*)pc.scol, (const double*)pc.sval, x, x_ld, x_koff, y, SpmvEpi(),
+               PP);
+  else
+    k_spmv_csr_pf<16, 4, 16, false, 4><<<grid_for(32, 2), 512, 0, h->stream>>>(
+        st, nrows, pc.srp, pc.scol, pc.sval, x, x_ld, x_koff, y, SpmvEpi(), PP);
 }
 
 // Grid of the fused windowed-orthogonalisation and normalisation kernels: about 8 elements per
@@ -536,27 +496,6 @@ void launch_res(sflsqr_t* h, cudaStream_t s, int fuse_stop) {
   launch_pdl(h, k_res_partial<kGemvRpt>, gemv_grid(h->m_loc), kVecThreads, 0, s, h->P, fuse_stop);
 }
 
-// The window dots of side `side` for iteration st->k + koff, to be fused into the product forming
-// that side's vector (reading R10): only with the one-pass fused orthogonalisation and a product
-// whose result is complete on this rank (not the COLSHARD partial T product); NULL otherwise.
-const FuseDots* fuse_dots(sflsqr_t* h, int side, int koff, FuseDots& F) {
-  const Params& P = h->P;
-  if (P.orth_alg != ORTH_FUSED || P.method >= SFLSQR_METHOD_LSQR || h->blur) return nullptr;
-  if (h->knobs & SFLSQR_KNOB_NO_FUSED_DOTS) return nullptr;
-  if (side == 0 && h->tkind == T_COLSHARD) return nullptr;
-  F.W = P.W;
-  F.Pring = P.Pring;
-  F.Z = P.Z;
-  F.m = h->m_loc;
-  F.n = h->n_loc;
-  F.ell = P.ell;
-  F.use_pring = P.use_pring;
-  F.side = side;
-  F.koff = koff;
-  F.base = side == 0 ? P.slot_zf : P.slot_wf;
-  return &F;
-}
-
 // skbuf = S v (this rank's coordinates), allreduced over ranks.
 int enqueue_sketch(sflsqr_t* h, const DevState* st, const double* v, cudaStream_t strm = nullptr) {
   const int64_t dim_loc = h->P.method == SFLSQR_METHOD_SFLSQR ? h->m_loc : h->n_loc;
@@ -577,13 +516,8 @@ int enqueue_sketch(sflsqr_t* h, const DevState* st, const double* v, cudaStream_
 int enqueue_transpose_product(sflsqr_t* h, bool init) {
   Params& P = h->P;
   const int64_t ld = init ? 0 : h->m_loc;
-  // the z-side window dots of the step that consumes z: st->k + 1 (at init st->k is still 0 --
-  // k_init_rhs sets it to 1 after this product -- so that is step 1 too)
-  FuseDots F;
-  const FuseDots* fd = fuse_dots(h, 0, 1, F);
-  h->z_dots_fused = false;
   if (h->tkind == T_FULL) {
-    h->z_dots_fused = enqueue_apply(h, 1, P.st, P.W, ld, 0, P.z, SFLSQR_KC_SPMV_T, fd);
+    enqueue_apply(h, 1, P.st, P.W, ld, 0, P.z, SFLSQR_KC_SPMV_T);
     return SFLSQR_OK;
   }
   std::string e;
@@ -595,7 +529,7 @@ int enqueue_transpose_product(sflsqr_t* h, bool init) {
     } else if (h->comm->allgather(P.wsend, h->wfull, h->m_max, h->stream, e)) {
       return fail(h, SFLSQR_E_CUDA, "allgather(w): %s", e.c_str());
     }
-    h->z_dots_fused = enqueue_apply(h, 1, P.st, h->wfull, 0, 0, P.z, SFLSQR_KC_SPMV_T, fd);
+    enqueue_apply(h, 1, P.st, h->wfull, 0, 0, P.z, SFLSQR_KC_SPMV_T);
     return SFLSQR_OK;
   }
   if (h->p2p) {
@@ -630,7 +564,7 @@ int enqueue_transpose_product(sflsqr_t* h, bool init) {
 // (side 1, Alg. 1 L476-480 / Alg. 2) for iteration st->k + koff, by the
 // handle's algorithm (fused dots+Gram / literal MGS passes / CGS2), leaving ||v||^2
 // where k_finish_z / k_finish_w (and FLSMR's k_ls) read it.
-int enqueue_orth(sflsqr_t* h, int side, int koff, bool dots_done) {
+int enqueue_orth(sflsqr_t* h, int side, int koff) {
   Params& P = h->P;
   const int k = h->host_k + koff;  // used only for the byte model
   const double v8 = 8.0 * (side == 0 ? h->n_loc : h->m_loc);
@@ -639,7 +573,7 @@ int enqueue_orth(sflsqr_t* h, int side, int koff, bool dots_done) {
   const int slot_f = side == 0 ? P.slot_zf : P.slot_wf, slot_out = side == 0 ? P.slot_zout : P.slot_wout;
   int rc;
   if (P.orth_alg == ORTH_FUSED) {
-    if (!dots_done) {  // else taken in the epilogue of the product that formed the vector
+    {
       Launch L(h, SFLSQR_KC_ORTH, v8 * (1 + J));
       launch_pdl(h, k_orth_dots, vec_grid(side == 0 ? h->n_loc : h->m_loc), kVecThreads, 0, h->stream, P, side, koff);
     }
@@ -867,20 +801,16 @@ int enqueue_iteration(sflsqr_t* h) {
   const double n8 = 8.0 * h->n_loc, m8 = 8.0 * h->m_loc;
   int rc;
   // a1: z-side windowed orthogonalisation (FLSMR: done at the end of the previous step / in set_rhs)
-  if (!z_early(h) && (rc = enqueue_orth(h, 0, 0, h->z_dots_fused))) return rc;
+  if (!z_early(h) && (rc = enqueue_orth(h, 0, 0))) return rc;
   // a1 end + a2: normalise, tau, store z_k
   {
     Launch L(h, SFLSQR_KC_TAU, n8 * (2 + (P.use_pring ? 1 : 0) + (P.precond ? 1 : 0)));
     launch_pdl(h, k_finish_z, vec_grid(h->n_loc), kVecThreads, 0, h->stream, P);
   }
   if (P.precond == SFLSQR_PRECOND_LOWRANK_RND && (rc = enqueue_lowrank(h))) return rc;
-  // a3: w = A z_k  (z_k = Z[:, k-1]; all-gathered across ranks when sharded), with the w-side
-  // window dots (a5's first pass) in its epilogue when the format has one
-  FuseDots Fw;
-  const FuseDots* fdw = fuse_dots(h, 1, 0, Fw);
-  bool w_dots_fused = false;
+  // a3: w = A z_k  (z_k = Z[:, k-1]; all-gathered across ranks when sharded)
   if (h->world == 1) {
-    w_dots_fused = enqueue_apply(h, 0, P.st, P.Z, h->n_loc, -1, P.w, SFLSQR_KC_SPMV_A, fdw);
+    enqueue_apply(h, 0, P.st, P.Z, h->n_loc, -1, P.w, SFLSQR_KC_SPMV_A);
   } else {
     std::string e;
     if (h->p2p) {  // z_k already stored into every rank's zfull by k_finish_z: a barrier
@@ -888,7 +818,7 @@ int enqueue_iteration(sflsqr_t* h) {
     } else if (h->comm->allgather(P.zsend, h->zfull, h->n_max, h->stream, e)) {
       return fail(h, SFLSQR_E_CUDA, "allgather(z): %s", e.c_str());
     }
-    w_dots_fused = enqueue_apply(h, 0, P.st, h->zfull, 0, 0, P.w, SFLSQR_KC_SPMV_A, fdw);
+    enqueue_apply(h, 0, P.st, h->zfull, 0, 0, P.w, SFLSQR_KC_SPMV_A);
   }
   // a4 (sFLSQR): S_AZ[:, k] = S w -- on the side stream (one rank), beside the w-side dots; the
   // in-place w update waits for it (SFLSQR_KNOB_SKETCH_MAIN: main stream)
@@ -911,7 +841,7 @@ int enqueue_iteration(sflsqr_t* h) {
   if (fork_ls && P.method == SFLSQR_METHOD_SFLSQR && (rc = enqueue_ls(h, true))) return rc;
   // a5: w-side windowed orthogonalisation and normalisation
   {
-    rc = enqueue_orth(h, 1, 0, w_dots_fused);
+    rc = enqueue_orth(h, 1, 0);
     h->axpy_wait_sk = -1;
     if (rc) return rc;
     Launch L(h, SFLSQR_KC_ORTH, 2 * m8);
@@ -964,7 +894,7 @@ int enqueue_iteration(sflsqr_t* h) {
   }
   if (fork_ls_mr && (rc = enqueue_ls(h, true))) return rc;
   if (z_early(h)) {
-    rc = enqueue_orth(h, 0, 1, h->z_dots_fused);
+    rc = enqueue_orth(h, 0, 1);
     h->axpy_wait_sk = -1;
     if (rc) return rc;
   }
@@ -2191,7 +2121,7 @@ int sflsqr_set_rhs(sflsqr_t* h, const double* b, int64_t len, int32_t mem_flags)
   }
   // FLSMR: the z side of step 1 (its norm is T_11) now; later steps run it one step early
   h->host_k = 1;
-  if (z_early(h) && (rc = enqueue_orth(h, 0, 0, h->z_dots_fused))) return rc;
+  if (z_early(h) && (rc = enqueue_orth(h, 0, 0))) return rc;
   if ((rc = check_launch(h))) return rc;
   CU(h, cudaStreamSynchronize(h->stream));
   h->host_k = 1;

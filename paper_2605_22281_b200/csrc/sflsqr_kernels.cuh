@@ -21,9 +21,6 @@ constexpr int kLsThreads = 512;           // one CTA solves the projected proble
 constexpr int kMaxD = 2048;               // sketch rows supported by the one-CTA LS
 constexpr int kFuseJ = 6;                 // fused orthogonalisation for windows of up to 6 vectors
 constexpr int kFuseAcc = 1 + kFuseJ + kFuseJ * (kFuseJ - 1) / 2;  // ||v||^2, dots, Gram pairs
-// slot of the Gram entry <q_i, q_j> (i < j) among the kFuseAcc one-pass sums (after ||v||^2 and the dots)
-template <int JM>
-__device__ __forceinline__ int gram_idx(int i, int j) { return 1 + JM + j * (j - 1) / 2 + i; }
 constexpr int kCgsChunk = 2048;           // CGS2 dot kernel: rows of v staged in shared memory per step
 enum CounterIdx {
   CTR_BETA = 0, CTR_ZDOTS, CTR_ZAXPY, CTR_WDOTS, CTR_WAXPY, CTR_XMAX, CTR_RES, CTR_CGS,
@@ -409,24 +406,6 @@ __device__ __forceinline__ double* kvec_w(const DevState* st, double* base, int6
 //   kind 4 (COLSHARD T product, peer memory): row r of the padded n layout is owned by rank
 //                     g = r / nmax; the row sum is stored into peers[g][src * nmax + r - g nmax]
 //                     (reduce-scatter fused into the product; k_reduce_recv sums the slots)
-// Window dots fused into a product (EPI == 2, reading R10): the one-pass sums of the windowed
-// orthogonalisation of v = M x -- ||v||^2, <q_j, v>, <q_i, q_j> in the slots of gram_idx -- taken as
-// each row's sum is formed, so the standalone k_orth_dots pass over v and the window is not needed
-// (k_orth_axpy then reads the reduced sums as before).  The window q_j (j = j0 .. j0+J-1) of
-// iteration st->k + koff on side 0 (z: P ring or Z) or 1 (w: W), as mgs_basis.
-struct FuseDots {
-  const double* W = nullptr;
-  const double* Pring = nullptr;
-  const double* Z = nullptr;
-  int64_t m = 0, n = 0;
-  int ell = 0, use_pring = 0, side = 0, koff = 0, base = 0;
-};
-__device__ __forceinline__ const double* fuse_q(const FuseDots& F, int j /*1-based*/) {
-  if (F.side == 1) return F.W + (int64_t)(j - 1) * F.m;
-  if (F.use_pring) return F.Pring + (int64_t)((j - 1) % F.ell) * F.n;
-  return F.Z + (int64_t)(j - 1) * F.n;
-}
-
 struct SpmvEpi {
   int kind;               // 0: plain y = M x
   double* aux;            // may alias y (each row reads and writes only its own entry)
@@ -438,7 +417,6 @@ struct SpmvEpi {
   int src;                // kind 4: this rank
   int64_t nmax;           // kind 4: rows per rank in the padded layout
   double* peers[8];       // kind 4: every rank's receive buffer (world x nmax)
-  FuseDots fd;            // EPI == 2: the window dots (slots fd.base ..; counter ctr_idx)
 };
 
 __device__ __forceinline__ void epi_coefs(const SpmvEpi& E, const DevState* st, double& a, double& c) {
@@ -467,8 +445,7 @@ struct PairPart {
 // registers: 2 CTAs of 512 threads per SM); 5: 4 in flight, aligned pairs (c even) gathered as
 // one 16-byte load (x must be 16-byte aligned); 6: 4 in flight, interpolation pairs (only f
 // stored, the pair's values are 1 - f and f, bitwise those of the stored operator).
-// EPI: 0 plain, 1 the GKB / peer epilogues of SpmvEpi, 2 the fused window dots (FuseDots).
-template <int WPB, int UNR, int LANES, int EPI = 0, int PAIRS = 0>
+template <int WPB, int UNR, int LANES, bool EPI = false, int PAIRS = 0>
 __global__ void __launch_bounds__(WPB * 32, (EPI || PAIRS) ? 2 : 2048 / (WPB * 32))
     k_spmv_csr_pf(const DevState* st, int64_t nrows,
                                                             const int64_t* __restrict__ rowptr,
@@ -480,44 +457,9 @@ __global__ void __launch_bounds__(WPB * 32, (EPI || PAIRS) ? 2 : 2048 / (WPB * 3
   pdl_wait();
   if (st && st->done) return;
   double ea = 1.0, ec = 0.0, nrm = 0.0;
-  if (EPI == 1) epi_coefs(E, st, ea, ec);
+  if (EPI) epi_coefs(E, st, ea, ec);
   const double* __restrict__ x = kvec(st, x_base, x_ld, x_koff);
   constexpr int RPW = 32 / LANES;  // rows per warp
-  // EPI == 2: quantity idx (< nfd) of the window sums = product of operands fqa[idx], fqb[idx]
-  // (a window vector, or NULL for v itself); lane l of a row's half-warp accumulates idx = l, l + 16
-  __shared__ const double* fqa[kFuseAcc];
-  __shared__ const double* fqb[kFuseAcc];
-  __shared__ int fslot[kFuseAcc];
-  int nfd = 0;
-  double fa0 = 0.0, fa1 = 0.0;
-  if (EPI == 2) {
-    const FuseDots& F = E.fd;
-    const int k = st->k + F.koff;
-    const int J = F.side == 0 ? min(F.ell, k - 1) : min(F.ell + 1, k);
-    const int j0 = max(1, k - F.ell);
-    nfd = 1 + J + J * (J - 1) / 2;
-    if (threadIdx.x < nfd) {
-      const int idx = threadIdx.x;
-      int a = -1, b = -1, slot = 0;
-      if (idx >= 1 && idx <= J) {
-        slot = idx;
-        b = idx - 1;
-      } else if (idx > J) {
-        int t = idx - 1 - J, j = 1;
-        while (t >= j) {
-          t -= j;
-          ++j;
-        }
-        a = t;
-        b = j;
-        slot = gram_idx<kFuseJ>(t, j);
-      }
-      fqa[idx] = a < 0 ? nullptr : fuse_q(F, j0 + a);
-      fqb[idx] = b < 0 ? nullptr : fuse_q(F, j0 + b);
-      fslot[idx] = slot;
-    }
-    __syncthreads();
-  }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int sl = lane % LANES, sub = lane / LANES;
   for (int64_t r0 = (int64_t)blockIdx.x * WPB * RPW; r0 < nrows; r0 += (int64_t)gridDim.x * WPB * RPW) {
@@ -620,24 +562,12 @@ __global__ void __launch_bounds__(WPB * 32, (EPI || PAIRS) ? 2 : 2048 / (WPB * 3
     }
 #pragma unroll
     for (int o = LANES / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    if (EPI == 2 && row < nrows) {  // every lane of the half-warp holds the row sum
-      if (sl < nfd) {
-        const double* pa = fqa[sl];
-        const double* pb = fqb[sl];
-        fa0 = fma(pa ? __ldg(pa + row) : sum, pb ? __ldg(pb + row) : sum, fa0);
-      }
-      if (sl + LANES < nfd) {
-        const double* pa = fqa[sl + LANES];
-        const double* pb = fqb[sl + LANES];
-        fa1 = fma(pa ? __ldg(pa + row) : sum, pb ? __ldg(pb + row) : sum, fa1);
-      }
-    }
     if (sl == 0 && row < nrows) {
-      if (EPI == 1 && E.kind == 4) {
+      if (EPI && E.kind == 4) {
         const int64_t g = row / E.nmax;
         E.peers[g][(int64_t)E.src * E.nmax + (row - g * E.nmax)] = sum;
       } else {
-        if (EPI == 1) {
+        if (EPI) {
           sum = E.kind == 3 ? sum * ea : fma(sum, ea, -ec * E.aux[row]);
           nrm = fma(sum, sum, nrm);
         }
@@ -645,22 +575,7 @@ __global__ void __launch_bounds__(WPB * 32, (EPI || PAIRS) ? 2 : 2048 / (WPB * 3
       }
     }
   }
-  if (EPI == 2) {
-    // per-CTA sums of the row-group accumulators in fixed order, then the grid reduction
-    constexpr int NG = WPB * 32 / LANES;  // row groups (half-warps) per CTA
-    __shared__ double fred[NG][kFuseAcc];
-    const int grp = threadIdx.x / LANES;
-    if (sl < nfd) fred[grp][sl] = fa0;
-    if (sl + LANES < nfd) fred[grp][sl + LANES] = fa1;
-    __syncthreads();
-    if ((int)threadIdx.x < nfd) {  // slots no quantity maps to are never read (orth_coefs)
-      double t = 0.0;
-      for (int g = 0; g < NG; ++g) t += fred[g][threadIdx.x];
-      E.part[(size_t)(E.fd.base + fslot[threadIdx.x]) * kVecBlocks + blockIdx.x] = t;
-    }
-    grid_reduce(E.part + (size_t)E.fd.base * kVecBlocks, kFuseAcc, E.scal + E.fd.base, E.ctr + E.ctr_idx, false);
-  }
-  if (EPI == 1 && E.kind != 4) {
+  if (EPI && E.kind != 4) {
     __shared__ double sh[33];
     __shared__ int s_last;
     nrm = block_sum<WPB * 32>(nrm, sh);
@@ -1259,6 +1174,8 @@ __global__ void __launch_bounds__(kVecThreads) k_mgs_pass(Params P, int side, in
 // pass applies v -= sum_j c_j q_j (in window order) with the MGS coefficients
 // c_j = d_j - sum_{i<j} c_i G_ij — exactly the coefficients of the literal MGS
 // loop (Alg. 1 L464-467 / L476-480) in exact arithmetic — and accumulates ||v||^2.
+template <int JM>
+__device__ __forceinline__ int gram_idx(int i, int j) { return 1 + JM + j * (j - 1) / 2 + i; }
 
 // Block-level bodies (NT threads) of the standalone kernels below.
 // Dots + Gram: block partials of ||v||^2, <q_j, v>, <q_i, q_j> into part[base + a][blockIdx].

@@ -735,23 +735,6 @@ def test_scheduling_knobs_bitwise_neutral(knob):
         assert np.array_equal(a, b)
 
 
-@pytest.mark.parametrize("cfg,method", [(3, "sflsqr"), (3, "sflsmr"), (4, "sflsqr"), (1, "sflsmr")])
-def test_fused_window_dots_match_standalone(cfg, method):
-    # reading R10: the window dots taken in the product's epilogue (FuseDots) are the same one-pass
-    # sums as k_orth_dots in another summation order: the runs agree to rounding, and both hold the
-    # oracle's bar (configs 3 / 1: both products fused; config 4: A z fused, the ELL B w not)
-    kw = {3: dict(N=128, n_angles=90, nb=183), 4: dict(N=96, n_angles=61, nb=137), 1: {}}[cfg]
-    p = make_problem(cfg, **kw)
-    spec = [s for s in p.solvers if s.method == method][0]
-    K = 12
-    r = solve_problem(p, spec, maxit=K, eta=0.0)
-    g_f = _gpu_run(p, spec, maxit=K, eta=0.0)
-    g_s = _gpu_run(p, spec, maxit=K, eta=0.0, knobs=["no_fused_dots"])
-    assert np.max(np.abs(g_f["true_res"] - g_s["true_res"]) / g_s["true_res"]) < 1e-11
-    for g in (g_f, g_s):
-        _compare(g, r, n_res=K)
-
-
 def test_wide_column_range_rows_match_oracle():
     # short rows whose columns span 200 000 columns (random, sorted): plain CSR, built transpose
     from paper_2605_22281_b200 import SFLSQR
