@@ -8,7 +8,6 @@
 
 #include <climits>
 #include <cstdint>
-#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 namespace sfl {
@@ -197,59 +196,35 @@ __device__ __forceinline__ double get_max(const Params& P, int slot, double* sh,
 // Fixed-order reduction of per-block partials over the grid: part[t * kVecBlocks + b] (t < ns)
 // holds block b's partial of quantity t; out[t] receives their sum (or max) in block order.
 // The last block to arrive (arrival counter, no waiting) folds them, four independent partial
-// folds per lane so the L2 loads overlap.  Grids launched in thread-block clusters reduce in two
-// levels: after a cluster barrier each cluster's rank-0 CTA folds its cluster's partials into its
-// own slot, then the last rank-0 CTA folds the cluster partials (measured on the vector kernels:
-// clusters of 8 over 592 CTAs were slower than 148 plain CTAs -- config 3 orthogonalisation
-// 12.9 -> 15.9 us a launch -- so no kernel is launched in clusters).
-// Deterministic for a given grid.  Returns true in the CTA that wrote out[].
-constexpr int kRedCluster = 8;
+// folds per lane so the L2 loads overlap.  (Measured: 592 CTAs in clusters of 8 with a two-level
+// cluster fold were slower than 148 plain CTAs on the vector kernels -- config 3 orthogonalisation
+// 12.9 -> 15.9 us a launch.)  Deterministic for a given grid.  Returns true in the
+// CTA that wrote out[].
 __device__ __forceinline__ bool grid_reduce(double* part, int ns, double* out, int* ctr, bool is_max) {
-  namespace cg = cooperative_groups;
   __shared__ int s_last;
   const double id = is_max ? -INFINITY : 0.0;
-  auto op = [is_max](double a, double b) { return is_max ? fmax(a, b) : a + b; };
-  cg::cluster_group cl = cg::this_cluster();
-  const int C = (int)cl.num_blocks();
   __threadfence();
-  if (C > 1) {
-    cl.sync();  // release / acquire at cluster scope: the cluster's partials are visible
-    if (cl.block_rank() != 0) return false;
-    const int b0 = blockIdx.x;  // rank 0 of a 1-D cluster: the cluster's first block
-    for (int t = threadIdx.x; t < ns; t += blockDim.x) {
-      double* pp = part + (size_t)t * kVecBlocks + b0;
-      double v[kRedCluster];
-#pragma unroll
-      for (int r = 0; r < kRedCluster; ++r) v[r] = r < C ? __ldcg(pp + r) : id;
-      double a = v[0];
-#pragma unroll
-      for (int r = 1; r < kRedCluster; ++r) a = op(a, v[r]);
-      pp[0] = a;
-    }
-    __threadfence();
-  }
   __syncthreads();
-  const int narrive = (int)gridDim.x / C;
-  if (threadIdx.x == 0) s_last = (atomicAdd(ctr, 1) == narrive - 1);
+  if (threadIdx.x == 0) s_last = (atomicAdd(ctr, 1) == (int)gridDim.x - 1);
   __syncthreads();
   if (!s_last) return false;
   __threadfence();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int nb = gridDim.x;
   for (int t = wid; t < ns; t += nw) {
     const double* pp = part + (size_t)t * kVecBlocks;
-    // four independent partial folds per lane (the L2 loads overlap), combined in a fixed order
     double a0 = id, a1 = id, a2 = id, a3 = id;
     int c = lane;
-    for (; c + 96 < narrive; c += 128) {
-      const double v0 = __ldcg(pp + (size_t)c * C), v1 = __ldcg(pp + (size_t)(c + 32) * C);
-      const double v2 = __ldcg(pp + (size_t)(c + 64) * C), v3 = __ldcg(pp + (size_t)(c + 96) * C);
-      a0 = op(a0, v0);
-      a1 = op(a1, v1);
-      a2 = op(a2, v2);
-      a3 = op(a3, v3);
+    for (; c + 96 < nb; c += 128) {
+      const double v0 = __ldcg(pp + c), v1 = __ldcg(pp + c + 32), v2 = __ldcg(pp + c + 64), v3 = __ldcg(pp + c + 96);
+      if (is_max) {
+        a0 = fmax(a0, v0), a1 = fmax(a1, v1), a2 = fmax(a2, v2), a3 = fmax(a3, v3);
+      } else {
+        a0 += v0, a1 += v1, a2 += v2, a3 += v3;
+      }
     }
-    for (; c < narrive; c += 32) a0 = op(a0, __ldcg(pp + (size_t)c * C));
-    double acc = op(op(a0, a1), op(a2, a3));
+    for (; c < nb; c += 32) a0 = is_max ? fmax(a0, __ldcg(pp + c)) : a0 + __ldcg(pp + c);
+    double acc = is_max ? fmax(fmax(a0, a1), fmax(a2, a3)) : (a0 + a1) + (a2 + a3);
     acc = is_max ? warp_max(acc) : warp_sum(acc);
     if (lane == 0) out[t] = acc;
   }
@@ -1177,46 +1152,100 @@ __global__ void __launch_bounds__(kVecThreads) k_mgs_pass(Params P, int side, in
 template <int JM>
 __device__ __forceinline__ int gram_idx(int i, int j) { return 1 + JM + j * (j - 1) / 2 + i; }
 
-// Block-level bodies (NT threads) of the standalone kernels below.
-// Dots + Gram: block partials of ||v||^2, <q_j, v>, <q_i, q_j> into part[base + a][blockIdx].
-template <int NT>
-__device__ __forceinline__ void orth_dots_block(const Params& P, int side, int J, int j0, int base) {
-  __shared__ double red[NT / 32][kFuseAcc + 1];
+// Dots + Gram for a window of exactly JJ vectors (registers: 1 + JJ + JJ(JJ-1)/2 accumulators, so
+// small windows leave room for 16-byte loads of element pairs): block partials into
+// part[base + slot][blockIdx] in the slots of gram_idx.  V2: v and every q_j 16-byte aligned (the
+// pairs (2i, 2i+1) are loaded as one double2; len odd: the last element in block 0).  Every
+// thread sums its elements in a fixed order, then warp / block / grid reductions in fixed orders
+// (deterministic for a given grid).
+template <int NT, int JJ, bool V2>
+__device__ __forceinline__ void orth_dots_j(const Params& P, int side, int j0, int base) {
+  constexpr int NA = 1 + JJ + JJ * (JJ - 1) / 2;
+  __shared__ double red[NT / 32][NA + 1];
   const double* __restrict__ v = side == 0 ? P.z : P.w;
   const int64_t len = side == 0 ? P.n : P.m;
-  const double* q[kFuseJ];
+  const double* q[JJ > 0 ? JJ : 1];
 #pragma unroll
-  for (int j = 0; j < kFuseJ; ++j) q[j] = j < J ? mgs_basis(P, side, j0 + j) : nullptr;
-  double acc[kFuseAcc];
+  for (int j = 0; j < JJ; ++j) q[j] = mgs_basis(P, side, j0 + j);
+  double acc[NA];
 #pragma unroll
-  for (int a = 0; a < kFuseAcc; ++a) acc[a] = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < len; i += (int64_t)gridDim.x * NT) {
-    const double vi = v[i];
+  for (int a = 0; a < NA; ++a) acc[a] = 0.0;
+  auto add = [&](double vi, const double* qv) {
     acc[0] = fma(vi, vi, acc[0]);
-    double qv[kFuseJ];
 #pragma unroll
-    for (int j = 0; j < kFuseJ; ++j) {
-      qv[j] = j < J ? q[j][i] : 0.0;
-      acc[1 + j] = fma(qv[j], vi, acc[1 + j]);
+    for (int j = 0; j < JJ; ++j) acc[1 + j] = fma(qv[j], vi, acc[1 + j]);
+    int a = 1 + JJ;
+#pragma unroll
+    for (int j = 1; j < JJ; ++j)
+#pragma unroll
+      for (int i2 = 0; i2 < j; ++i2) {
+        acc[a] = fma(qv[i2], qv[j], acc[a]);
+        ++a;
+      }
+  };
+  const int64_t stride = (int64_t)gridDim.x * NT;
+  if (V2) {
+    const int64_t len2 = len >> 1;
+    for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < len2; i += stride) {
+      const double2 vv = __ldcg(reinterpret_cast<const double2*>(v) + i);
+      double qx[JJ > 0 ? JJ : 1], qy[JJ > 0 ? JJ : 1];
+#pragma unroll
+      for (int j = 0; j < JJ; ++j) {
+        const double2 t = __ldg(reinterpret_cast<const double2*>(q[j]) + i);
+        qx[j] = t.x;
+        qy[j] = t.y;
+      }
+      add(vv.x, qx);
+      add(vv.y, qy);
     }
+    if ((len & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+      double qv[JJ > 0 ? JJ : 1];
 #pragma unroll
-    for (int j = 1; j < kFuseJ; ++j)
+      for (int j = 0; j < JJ; ++j) qv[j] = q[j][len - 1];
+      add(v[len - 1], qv);
+    }
+  } else {
+    for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < len; i += stride) {
+      double qv[JJ > 0 ? JJ : 1];
 #pragma unroll
-      for (int i2 = 0; i2 < j; ++i2) acc[gram_idx<kFuseJ>(i2, j)] = fma(qv[i2], qv[j], acc[gram_idx<kFuseJ>(i2, j)]);
+      for (int j = 0; j < JJ; ++j) qv[j] = q[j][i];
+      add(v[i], qv);
+    }
   }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
-  for (int a = 0; a < kFuseAcc; ++a) {
+  for (int a = 0; a < NA; ++a) {
     const double t = warp_sum(acc[a]);
     if (lane == 0) red[wid][a] = t;
   }
   __syncthreads();
-  if (threadIdx.x < kFuseAcc) {
+  if (threadIdx.x < NA) {
     double t = 0.0;
 #pragma unroll
     for (int w = 0; w < NT / 32; ++w) t += red[w][threadIdx.x];
-    P.part[(size_t)(base + threadIdx.x) * kVecBlocks + blockIdx.x] = t;
+    // accumulator a -> slot: 0 (||v||^2), 1 + j (dots), gram_idx<kFuseJ>(i, j) (pairs, j-major)
+    int slot = threadIdx.x;
+    if (slot > JJ) {
+      int t2 = slot - 1 - JJ, j = 1;
+      while (t2 >= j) {
+        t2 -= j;
+        ++j;
+      }
+      slot = gram_idx<kFuseJ>(t2, j);
+    }
+    P.part[(size_t)(base + slot) * kVecBlocks + blockIdx.x] = t;
   }
+}
+
+template <int NT, int JJ>
+__device__ __forceinline__ void orth_dots_jv(const Params& P, int side, int j0, int base) {
+  const double* v = side == 0 ? P.z : P.w;
+  bool al = JJ <= 4 && ((uintptr_t)v & 15) == 0;  // 5 window vectors in pairs would spill (64 registers)
+  for (int j = 0; j < JJ; ++j) al = al && (((uintptr_t)mgs_basis(P, side, j0 + j) & 15) == 0);
+  if (JJ <= 4 && al)
+    orth_dots_j<NT, JJ, (JJ <= 4)>(P, side, j0, base);
+  else
+    orth_dots_j<NT, JJ, false>(P, side, j0, base);
 }
 
 // MGS coefficients from the reduced dots / Gram (scal[base ..]): c_j = d_j - sum_{i<j} c_i G_ij;
@@ -1243,52 +1272,6 @@ __device__ __forceinline__ void orth_coefs(const Params& P, int side, int k, int
   }
 }
 
-// v -= sum_j c_j q_j (window order); block partial of ||v||^2 into part[so][blockIdx].
-template <int NT>
-__device__ __forceinline__ void orth_axpy_block(const Params& P, int side, int J, int j0, const double* c, int so) {
-  __shared__ double sh[33];
-  double* __restrict__ v = side == 0 ? P.z : P.w;
-  const int64_t len = side == 0 ? P.n : P.m;
-  const double* q[kFuseJ];
-#pragma unroll
-  for (int j = 0; j < kFuseJ; ++j) q[j] = j < J ? mgs_basis(P, side, j0 + j) : nullptr;
-  double acc = 0.0;
-  // two elements per iteration (12 independent loads in flight); the window vectors are
-  // read-only in this kernel (read through the non-coherent path, so they may be hoisted)
-  const int64_t stride = (int64_t)gridDim.x * NT;
-  int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x;
-  for (; i + stride < len; i += 2 * stride) {
-    const int64_t i1 = i + stride;
-    double a = v[i], b = v[i1];
-    double qa[kFuseJ], qb[kFuseJ];
-#pragma unroll
-    for (int j = 0; j < kFuseJ; ++j) {
-      qa[j] = j < J ? __ldg(q[j] + i) : 0.0;
-      qb[j] = j < J ? __ldg(q[j] + i1) : 0.0;
-    }
-#pragma unroll
-    for (int j = 0; j < kFuseJ; ++j)
-      if (j < J) {
-        a = fma(-c[j], qa[j], a);
-        b = fma(-c[j], qb[j], b);
-      }
-    v[i] = a;
-    v[i1] = b;
-    acc = fma(a, a, acc);
-    acc = fma(b, b, acc);
-  }
-  if (i < len) {
-    double vi = v[i];
-#pragma unroll
-    for (int j = 0; j < kFuseJ; ++j)
-      if (j < J) vi = fma(-c[j], __ldg(q[j] + i), vi);
-    v[i] = vi;
-    acc = fma(vi, vi, acc);
-  }
-  acc = block_sum<NT>(acc, sh);
-  if (threadIdx.x == 0) P.part[(size_t)so * kVecBlocks + blockIdx.x] = acc;
-}
-
 __global__ void __launch_bounds__(kVecThreads, 4) k_orth_dots(Params P, int side, int koff) {
   pdl_wait();
   const DevState* st = P.st;
@@ -1297,11 +1280,87 @@ __global__ void __launch_bounds__(kVecThreads, 4) k_orth_dots(Params P, int side
   const int J = side == 0 ? min(P.ell, k - 1) : min(P.ell + 1, k);
   const int j0 = max(1, k - P.ell);
   const int base = side == 0 ? P.slot_zf : P.slot_wf;
-  orth_dots_block<kVecThreads>(P, side, J, j0, base);
+  switch (J) {  // window size at compile time: registers for 16-byte loads of element pairs
+    case 0: orth_dots_jv<kVecThreads, 0>(P, side, j0, base); break;
+    case 1: orth_dots_jv<kVecThreads, 1>(P, side, j0, base); break;
+    case 2: orth_dots_jv<kVecThreads, 2>(P, side, j0, base); break;
+    case 3: orth_dots_jv<kVecThreads, 3>(P, side, j0, base); break;
+    case 4: orth_dots_jv<kVecThreads, 4>(P, side, j0, base); break;
+    case 5: orth_dots_jv<kVecThreads, 5>(P, side, j0, base); break;
+    default: orth_dots_jv<kVecThreads, kFuseJ>(P, side, j0, base); break;  // J == kFuseJ
+  }
   last_block_reduce(P, base, kFuseAcc, side == 0 ? CTR_ZDOTS : CTR_WDOTS, false);
 }
 
-__global__ void __launch_bounds__(kVecThreads) k_orth_axpy(Params P, int side, int koff) {
+// v -= sum_j c_j q_j for a window of exactly JJ vectors (coefficients and pointers in registers),
+// block partial of ||v||^2 into part[so][blockIdx].  V2: v and every q_j 16-byte aligned (element
+// pairs as one double2); the window is subtracted in order (j = 0 .. JJ-1).
+template <int NT, int JJ, bool V2>
+__device__ __forceinline__ void orth_axpy_j(const Params& P, int side, int j0, const double* c, int so) {
+  __shared__ double sh[33];
+  double* __restrict__ v = side == 0 ? P.z : P.w;
+  const int64_t len = side == 0 ? P.n : P.m;
+  const double* q[JJ > 0 ? JJ : 1];
+  double cc[JJ > 0 ? JJ : 1];
+#pragma unroll
+  for (int j = 0; j < JJ; ++j) {
+    q[j] = mgs_basis(P, side, j0 + j);
+    cc[j] = c[j];
+  }
+  double acc = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * NT;
+  if (V2) {
+    const int64_t len2 = len >> 1;
+    double2* __restrict__ v2 = reinterpret_cast<double2*>(v);
+    for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < len2; i += stride) {
+      double2 a = v2[i];
+      double2 qv[JJ > 0 ? JJ : 1];
+#pragma unroll
+      for (int j = 0; j < JJ; ++j) qv[j] = __ldg(reinterpret_cast<const double2*>(q[j]) + i);
+#pragma unroll
+      for (int j = 0; j < JJ; ++j) {
+        a.x = fma(-cc[j], qv[j].x, a.x);
+        a.y = fma(-cc[j], qv[j].y, a.y);
+      }
+      v2[i] = a;
+      acc = fma(a.x, a.x, acc);
+      acc = fma(a.y, a.y, acc);
+    }
+    if ((len & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+      double a = v[len - 1];
+#pragma unroll
+      for (int j = 0; j < JJ; ++j) a = fma(-cc[j], q[j][len - 1], a);
+      v[len - 1] = a;
+      acc = fma(a, a, acc);
+    }
+  } else {
+    for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < len; i += stride) {
+      double a = v[i];
+      double qv[JJ > 0 ? JJ : 1];
+#pragma unroll
+      for (int j = 0; j < JJ; ++j) qv[j] = __ldg(q[j] + i);
+#pragma unroll
+      for (int j = 0; j < JJ; ++j) a = fma(-cc[j], qv[j], a);
+      v[i] = a;
+      acc = fma(a, a, acc);
+    }
+  }
+  acc = block_sum<NT>(acc, sh);
+  if (threadIdx.x == 0) P.part[(size_t)so * kVecBlocks + blockIdx.x] = acc;
+}
+
+template <int NT, int JJ>
+__device__ __forceinline__ void orth_axpy_jv(const Params& P, int side, int j0, const double* c, int so) {
+  const double* v = side == 0 ? P.z : P.w;
+  bool al = ((uintptr_t)v & 15) == 0;
+  for (int j = 0; j < JJ; ++j) al = al && (((uintptr_t)mgs_basis(P, side, j0 + j) & 15) == 0);
+  if (al)
+    orth_axpy_j<NT, JJ, true>(P, side, j0, c, so);
+  else
+    orth_axpy_j<NT, JJ, false>(P, side, j0, c, so);
+}
+
+__global__ void __launch_bounds__(kVecThreads, 4) k_orth_axpy(Params P, int side, int koff) {
   pdl_wait();
   const DevState* st = P.st;
   if (st->done) return;
@@ -1312,7 +1371,15 @@ __global__ void __launch_bounds__(kVecThreads) k_orth_axpy(Params P, int side, i
   double c[kFuseJ];
   orth_coefs(P, side, k, J, j0, base, c);
   const int so = side == 0 ? P.slot_zout : P.slot_wout;
-  orth_axpy_block<kVecThreads>(P, side, J, j0, c, so);
+  switch (J) {  // window size at compile time: coefficients / pointers in registers, 16-byte pairs
+    case 0: orth_axpy_jv<kVecThreads, 0>(P, side, j0, c, so); break;
+    case 1: orth_axpy_jv<kVecThreads, 1>(P, side, j0, c, so); break;
+    case 2: orth_axpy_jv<kVecThreads, 2>(P, side, j0, c, so); break;
+    case 3: orth_axpy_jv<kVecThreads, 3>(P, side, j0, c, so); break;
+    case 4: orth_axpy_jv<kVecThreads, 4>(P, side, j0, c, so); break;
+    case 5: orth_axpy_jv<kVecThreads, 5>(P, side, j0, c, so); break;
+    default: orth_axpy_jv<kVecThreads, kFuseJ>(P, side, j0, c, so); break;  // J == kFuseJ
+  }
   last_block_reduce(P, so, 1, side == 0 ? CTR_ZAXPY : CTR_WAXPY, false);
 }
 
@@ -2231,52 +2298,52 @@ __global__ void __launch_bounds__(kLsThreads) k_ls(Params P) {
 }
 
 // ------------------------------------------------------------------ a8 / a9: tall-skinny GEMVs
-// (a0, a1) = sum_{j < kc} M[j*ld + i2 + {0, 1}] * c[j]: rows i2, i2+1 of a column-major
-// tall-skinny matrix times a short vector in shared memory.  16-byte loads of row
-// pairs, four columns in flight per step; summation in increasing j (deterministic).
-__device__ __forceinline__ void tsgemv_pair(const double* __restrict__ M, int64_t ld, int64_t len, int64_t i2,
-                                            const double* c, int kc, double& a0, double& a1) {
-  a0 = 0.0;
-  a1 = 0.0;
-  if (i2 + 1 < len && (ld & 1) == 0) {
-    const double* p = M + i2;
-    int j = 0;
-    for (; j + 4 <= kc; j += 4) {
-      const double2 v0 = __ldg(reinterpret_cast<const double2*>(p + (int64_t)j * ld));
-      const double2 v1 = __ldg(reinterpret_cast<const double2*>(p + (int64_t)(j + 1) * ld));
-      const double2 v2 = __ldg(reinterpret_cast<const double2*>(p + (int64_t)(j + 2) * ld));
-      const double2 v3 = __ldg(reinterpret_cast<const double2*>(p + (int64_t)(j + 3) * ld));
-      a0 = fma(v0.x, c[j], a0);
-      a1 = fma(v0.y, c[j], a1);
-      a0 = fma(v1.x, c[j + 1], a0);
-      a1 = fma(v1.y, c[j + 1], a1);
-      a0 = fma(v2.x, c[j + 2], a0);
-      a1 = fma(v2.y, c[j + 2], a1);
-      a0 = fma(v3.x, c[j + 3], a0);
-      a1 = fma(v3.y, c[j + 3], a1);
-    }
-    for (; j < kc; ++j) {
-      const double2 v = __ldg(reinterpret_cast<const double2*>(p + (int64_t)j * ld));
-      a0 = fma(v.x, c[j], a0);
-      a1 = fma(v.y, c[j], a1);
-    }
-  } else {
-    for (int j = 0; j < kc; ++j) {
-      a0 = fma(__ldg(M + (int64_t)j * ld + i2), c[j], a0);
-      if (i2 + 1 < len) a1 = fma(__ldg(M + (int64_t)j * ld + i2 + 1), c[j], a1);
-    }
-  }
-}
-
 // Row-tile GEMV: a CTA owns RPT * NT consecutive rows of the column-major tall-skinny M and
 // streams the kc columns in order (each column a contiguous RPT * NT * 8-byte segment: long
-// DRAM bursts), two columns and RPT rows per thread in flight; every row accumulates in
-// increasing column order (deterministic).
+// DRAM bursts); every row accumulates in increasing column order (deterministic).  row[u] is the
+// row of out[u].  Even ld (every column 16-byte aligned) and RPT == 2: thread t owns the adjacent
+// rows r0 + 2t, r0 + 2t + 1 and loads them as one 16-byte pair, four columns in flight (64 B per
+// thread; the two-column scalar form kept ~30 % of the bytes the HBM roofline needs in flight:
+// config 4's W-path residual ran at ~65 % of the copy peak); otherwise rows r0 + t + u NT.
 template <int NT, int RPT>
 __device__ __forceinline__ void tsgemv_tile(const double* __restrict__ M, int64_t ld, int64_t r0, int64_t len,
-                                            const double* c, int kc, double (&out)[RPT]) {
+                                            const double* c, int kc, double (&out)[RPT], int64_t (&row)[RPT]) {
 #pragma unroll
   for (int u = 0; u < RPT; ++u) out[u] = 0.0;
+  if (RPT == 2 && (ld & 1) == 0) {
+    const int64_t r = r0 + 2 * (int64_t)threadIdx.x;
+    row[0] = r;
+    row[RPT - 1] = r + 1;
+    if (r >= len) return;
+    if (r + 1 < len) {  // both rows: 16-byte loads
+      const double2* __restrict__ p = reinterpret_cast<const double2*>(M + r);
+      const int64_t ld2 = ld / 2;
+      double a0 = 0.0, a1 = 0.0;
+      int j = 0;
+      for (; j + 4 <= kc; j += 4) {
+        const double2 v0 = __ldcs(p + (int64_t)j * ld2), v1 = __ldcs(p + (int64_t)(j + 1) * ld2);
+        const double2 v2 = __ldcs(p + (int64_t)(j + 2) * ld2), v3 = __ldcs(p + (int64_t)(j + 3) * ld2);
+        a0 = fma(v1.x, c[j + 1], fma(v0.x, c[j], a0));
+        a1 = fma(v1.y, c[j + 1], fma(v0.y, c[j], a1));
+        a0 = fma(v3.x, c[j + 3], fma(v2.x, c[j + 2], a0));
+        a1 = fma(v3.y, c[j + 3], fma(v2.y, c[j + 2], a1));
+      }
+      for (; j < kc; ++j) {
+        const double2 v = __ldcs(p + (int64_t)j * ld2);
+        a0 = fma(v.x, c[j], a0);
+        a1 = fma(v.y, c[j], a1);
+      }
+      out[0] = a0;
+      out[RPT - 1] = a1;
+    } else {  // the last odd row
+      double a0 = 0.0;
+      for (int j = 0; j < kc; ++j) a0 = fma(__ldcs(M + (int64_t)j * ld + r), c[j], a0);
+      out[0] = a0;
+    }
+    return;
+  }
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) row[u] = r0 + threadIdx.x + (int64_t)u * NT;
   int j = 0;
   for (; j + 2 <= kc; j += 2) {
     const double c0 = c[j], c1 = c[j + 1];
@@ -2285,7 +2352,7 @@ __device__ __forceinline__ void tsgemv_tile(const double* __restrict__ M, int64_
     double a[RPT], b[RPT];
 #pragma unroll
     for (int u = 0; u < RPT; ++u) {
-      const int64_t r = r0 + threadIdx.x + (int64_t)u * NT;
+      const int64_t r = row[u];
       a[u] = r < len ? __ldcs(m0 + r) : 0.0;
       b[u] = r < len ? __ldcs(m1 + r) : 0.0;
     }
@@ -2297,7 +2364,7 @@ __device__ __forceinline__ void tsgemv_tile(const double* __restrict__ M, int64_
     const double* m0 = M + (int64_t)j * ld;
 #pragma unroll
     for (int u = 0; u < RPT; ++u) {
-      const int64_t r = r0 + threadIdx.x + (int64_t)u * NT;
+      const int64_t r = row[u];
       if (r < len) out[u] = fma(__ldcs(m0 + r), c0, out[u]);
     }
   }
@@ -2319,10 +2386,11 @@ __global__ void __launch_bounds__(kVecThreads) k_xupdate(Params P, int force) {
   constexpr int64_t tile = (int64_t)RPT * kVecThreads;
   for (int64_t r0 = (int64_t)blockIdx.x * tile; r0 < P.n; r0 += (int64_t)gridDim.x * tile) {
     double o[RPT];
-    tsgemv_tile<kVecThreads, RPT>(P.Z, P.n, r0, P.n, ys, kx, o);
+    int64_t rw[RPT];
+    tsgemv_tile<kVecThreads, RPT>(P.Z, P.n, r0, P.n, ys, kx, o, rw);
 #pragma unroll
     for (int u = 0; u < RPT; ++u) {
-      const int64_t r = r0 + threadIdx.x + (int64_t)u * kVecThreads;
+      const int64_t r = rw[u];
       if (r < P.n) {
         P.x[r] = o[u];
         mx = fmax(mx, absmax ? fabs(o[u]) : o[u]);
@@ -2379,7 +2447,8 @@ __global__ void __launch_bounds__(kVecThreads) k_res_partial(Params P, int fuse_
   constexpr int64_t tile = (int64_t)RPT * kVecThreads;
   for (int64_t r0 = (int64_t)blockIdx.x * tile; r0 < P.m; r0 += (int64_t)gridDim.x * tile) {
     double o[RPT];
-    tsgemv_tile<kVecThreads, RPT>(P.W, P.m, r0, P.m, gs, kk, o);
+    int64_t rw[RPT];
+    tsgemv_tile<kVecThreads, RPT>(P.W, P.m, r0, P.m, gs, kk, o, rw);
 #pragma unroll
     for (int u = 0; u < RPT; ++u) acc2 = fma(o[u], o[u], acc2);  // rows past the end are 0
   }
