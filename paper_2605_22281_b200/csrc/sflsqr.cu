@@ -46,6 +46,7 @@ struct PCSR {  // pair-CSR copy of an operator (k_pcsr_rows): pairs + singleton 
   bool ok = false;
   bool aligned = false;  // pairs only at even columns (gathered as one 16-byte load)
   bool interp = false;   // interpolation pairs: second values f only (first = 1 - f bitwise), pval freed
+  bool warp_rows = false;  // aligned pairs of short rows with dense pairing: a full warp per row
   bool ell = false;      // their sliced-ELL copy serves the product (pair-CSR arrays prp / pcol / f freed)
   bool c16 = false;      // ... with 16-bit column offsets from a per-slice-entry base (ecol freed)
   double* f = nullptr;
@@ -462,6 +463,10 @@ void enqueue_apply(sflsqr_t* h, int which, const DevState* st, const double* x, 
   } else if (pc.interp)
     k_spmv_csr_pf<16, 4, 16, false, 6><<<grid_for(32, 2), 512, 0, h->stream>>>(
         st, nrows, pc.srp, pc.scol, pc.sval, x, x_ld, x_koff, y, SpmvEpi(), PP);
+  else if (pc.aligned && x16 && pc.warp_rows)  // a full warp per (short, ray-like) row: 16 rows per CTA
+    launch_pdl(h, k_spmv_csr_pf<16, 4, 32, 0, 5>, grid_for(16, 2), 512, 0, h->stream, st, nrows,
+               (const int64_t*)pc.srp, (const int*)pc.scol, (const double*)pc.sval, x, x_ld, x_koff, y, SpmvEpi(),
+               PP);
   else if (pc.aligned && x16)
     launch_pdl(h, k_spmv_csr_pf<16, 4, 16, false, 5>, grid_for(32, 2), 512, 0, h->stream, st, nrows,
                (const int64_t*)pc.srp, (const int*)pc.scol, (const double*)pc.sval, x, x_ld, x_koff, y, SpmvEpi(),
@@ -648,6 +653,9 @@ bool launch_pairs_epi(sflsqr_t* h, int which, const double* x, int64_t x_ld, dou
   if (pc.interp)
     k_spmv_csr_pf<16, 4, 16, true, 6><<<grid, 512, 0, h->stream>>>(h->P.st, nrows, pc.srp, pc.scol, pc.sval, x, x_ld,
                                                                     0, y, E, PP);
+  else if (pc.aligned && (uintptr_t)x % 16 == 0 && x_ld % 2 == 0 && pc.warp_rows)  // 16 rows per CTA
+    k_spmv_csr_pf<16, 4, 32, true, 5><<<(int)std::max<int64_t>(1, std::min<int64_t>((nrows + 15) / 16, 148 * 4)), 512, 0,
+                                        h->stream>>>(h->P.st, nrows, pc.srp, pc.scol, pc.sval, x, x_ld, 0, y, E, PP);
   else if (pc.aligned && (uintptr_t)x % 16 == 0 && x_ld % 2 == 0)
     k_spmv_csr_pf<16, 4, 16, true, 5><<<grid, 512, 0, h->stream>>>(h->P.st, nrows, pc.srp, pc.scol, pc.sval, x, x_ld,
                                                                     0, y, E, PP);
@@ -1190,7 +1198,16 @@ int build_formats(sflsqr_t* h) {
     int r = build_pcsr(h, nrows, rp, col, val, p, false, 0.75);
     if (!r && p.ok && h->pcsr_interp) r = try_interp(h, p);
     if (!r && p.ok && p.interp && h->sell) r = build_sell(h, nrows, p);
-    if (!r && !p.ok) r = build_pcsr(h, nrows, rp, col, val, p, true, 0.20);
+    if (!r && !p.ok) {
+      r = build_pcsr(h, nrows, rp, col, val, p, true, 0.20);
+      // a full warp per row when rows are short (< 600 nonzeros on average) and ray-like (>= 40 % of
+      // the nonzeros in even-column pairs: consecutive entries are neighbouring pixels): config 3's
+      // Siddon A (460, 50 %) but not its A^T (460, 21 %: a full warp's 32 scattered sinogram gathers
+      // cost more) nor config 4's A (920 nonzeros a row).  SFLSQR_KNOB_HALF_WARP_ROWS: always 16 lanes
+      if (!r && p.ok && !(h->knobs & SFLSQR_KNOB_HALF_WARP_ROWS) && nnz < 600 * nrows &&
+          2.0 * p.npairs >= 0.4 * (double)nnz)
+        p.warp_rows = true;
+    }
     if (r == SFLSQR_E_OOM) {
       free_pcsr(p);
       cudaGetLastError();

@@ -735,6 +735,30 @@ def test_scheduling_knobs_bitwise_neutral(knob):
         assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("cfg", [3, 5])
+def test_full_warp_rows_match_half_warp(cfg):
+    # short ray-like rows (config 3's and config 5-reduced's Siddon A) run a full warp
+    # per row; another summation order than the half-warp kernel (SFLSQR_KNOB_HALF_WARP_ROWS): the
+    # products agree to rounding and both solves hold the oracle's bar
+    from paper_2605_22281_b200 import SFLSQR
+    kw = dict(N=128, n_angles=90, nb=183) if cfg == 3 else C5R
+    p = make_problem(cfg, **kw)
+    spec = p.solvers[0]
+    z = np.random.default_rng(31).standard_normal(p.n)
+    prods = []
+    for kn in ([], ["half_warp_rows"]):
+        s = SFLSQR(maxit=4, knobs=kn)
+        s.set_operator(p.A.nrows, p.A.ncols, p.A.rowptr, p.A.col, p.A.val)
+        prods.append(s.debug_apply(0, z))
+        s.close()
+    absref = OracleCSR(p.A.nrows, p.A.ncols, p.A.rowptr, p.A.col, np.abs(p.A.val)).matvec(np.abs(z))
+    assert np.all(np.abs(prods[0] - prods[1]) <= 1e-14 * absref + 1e-300)
+    K = 12
+    r = solve_problem(p, spec, maxit=K, eta=0.0)
+    for kn in ([], ["half_warp_rows"]):
+        _compare(_gpu_run(p, spec, maxit=K, eta=0.0, knobs=kn), r, n_res=K)
+
+
 def test_wide_column_range_rows_match_oracle():
     # short rows whose columns span 200 000 columns (random, sorted): plain CSR, built transpose
     from paper_2605_22281_b200 import SFLSQR
