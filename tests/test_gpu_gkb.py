@@ -31,10 +31,10 @@ def _lib():
     build_library()
 
 
-def _gpu_run(prob, spec, maxit, method, eta=0.0, use_graph=True, spmv_mode=None):
+def _gpu_run(prob, spec, maxit, method, eta=0.0, use_graph=True, spmv_mode=None, knobs=()):
     from paper_2605_22281_b200 import solver_for_problem
     s = solver_for_problem(prob, spec, maxit=maxit, eta=eta, method=method, use_graph=use_graph,
-                           knobs=["keep_csr"] if spmv_mode is not None else [])
+                           knobs=(["keep_csr"] if spmv_mode is not None else []) + list(knobs))
     if spmv_mode is not None:
         s.debug_set_tuning(spmv_mode)
     s.set_rhs(prob.b)
@@ -91,6 +91,20 @@ def test_gkb_discrepancy_stop_and_forced_formats(method):
     for mode in (None, 14, 16):                            # default format / fused CSR / fused pair-CSR epilogue
         g = _gpu_run(p, spec, 30, method, eta=eta, spmv_mode=mode)
         _compare(g, r, method)
+
+
+@pytest.mark.parametrize("method", ["lsqr", "lsmr"])
+def test_gkb_full_and_half_warp_rows(method):
+    # the fused-epilogue A product on short ray-like rows runs a full warp per row by default
+    # (DESIGN.md §5); SFLSQR_KNOB_HALF_WARP_ROWS selects the half-warp kernel; both hold the bar
+    p = make_problem(3, N=128, n_angles=90, nb=183)
+    spec = p.solvers[0]
+    kstar, _ = horizon(f"gkb/c3r128/{method}", p)
+    r = solve_problem(p, spec, maxit=kstar, eta=0.0, method=method)
+    g = [_gpu_run(p, spec, kstar, method, knobs=kn) for kn in ([], ["half_warp_rows"])]
+    for gi in g:
+        _compare(gi, r, method)
+    assert np.max(np.abs(g[0]["res"][:kstar] - g[1]["res"][:kstar]) / g[1]["res"][:kstar]) < 1e-10
 
 
 def test_gkb_graph_and_eager_agree_bitwise():
