@@ -653,9 +653,6 @@ bool launch_pairs_epi(sflsqr_t* h, int which, const double* x, int64_t x_ld, dou
   if (pc.interp)
     k_spmv_csr_pf<16, 4, 16, true, 6><<<grid, 512, 0, h->stream>>>(h->P.st, nrows, pc.srp, pc.scol, pc.sval, x, x_ld,
                                                                     0, y, E, PP);
-  else if (pc.aligned && (uintptr_t)x % 16 == 0 && x_ld % 2 == 0 && pc.warp_rows)  // 16 rows per CTA
-    k_spmv_csr_pf<16, 4, 32, true, 5><<<(int)std::max<int64_t>(1, std::min<int64_t>((nrows + 15) / 16, 148 * 4)), 512, 0,
-                                        h->stream>>>(h->P.st, nrows, pc.srp, pc.scol, pc.sval, x, x_ld, 0, y, E, PP);
   else if (pc.aligned && (uintptr_t)x % 16 == 0 && x_ld % 2 == 0)
     k_spmv_csr_pf<16, 4, 16, true, 5><<<grid, 512, 0, h->stream>>>(h->P.st, nrows, pc.srp, pc.scol, pc.sval, x, x_ld,
                                                                     0, y, E, PP);

@@ -93,20 +93,6 @@ def test_gkb_discrepancy_stop_and_forced_formats(method):
         _compare(g, r, method)
 
 
-@pytest.mark.parametrize("method", ["lsqr", "lsmr"])
-def test_gkb_full_and_half_warp_rows(method):
-    # the fused-epilogue A product on short ray-like rows runs a full warp per row by default
-    # (DESIGN.md §5); SFLSQR_KNOB_HALF_WARP_ROWS selects the half-warp kernel; both hold the bar
-    p = make_problem(3, N=128, n_angles=90, nb=183)
-    spec = p.solvers[0]
-    kstar, _ = horizon(f"gkb/c3r128/{method}", p)
-    r = solve_problem(p, spec, maxit=kstar, eta=0.0, method=method)
-    g = [_gpu_run(p, spec, kstar, method, knobs=kn) for kn in ([], ["half_warp_rows"])]
-    for gi in g:
-        _compare(gi, r, method)
-    assert np.max(np.abs(g[0]["res"][:kstar] - g[1]["res"][:kstar]) / g[1]["res"][:kstar]) < 1e-10
-
-
 def test_gkb_graph_and_eager_agree_bitwise():
     p = make_problem(1)
     spec = p.solvers[0]
