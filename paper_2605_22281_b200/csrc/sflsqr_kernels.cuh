@@ -445,6 +445,23 @@ __global__ void __launch_bounds__(WPB * 32, (EPI || PAIRS) ? 2 : 2048 / (WPB * 3
       e = rowptr[row + 1];
     }
     double sum = 0.0;
+    // HOIST (a full warp per row, the short ray-like rows of DESIGN.md §5): the singletons' first
+    // UNR chunks are requested before the pair pipeline runs (they depend only on the row
+    // pointers), so their latency overlaps the pairs' instead of following it.  Measured: config 3
+    // A z -2.5 %, 1601 -> 1619 it/s; half-warp rows (config 4's A) gain nothing (-0.3 %).
+    constexpr bool HOIST = LANES == 32;
+    int64_t p = s + sl;
+    int cn[UNR];
+    double vn[UNR];
+    auto first_chunks = [&]() {
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int64_t q = p + (int64_t)LANES * u;
+        cn[u] = q < e ? ld_stream_i(col + q) : 0;
+        vn[u] = q < e ? ld_stream_d(val + q) : 0.0;
+      }
+    };
+    if (HOIST) first_chunks();
     if (PAIRS) {
       // the row's adjacent-column pairs first: 4 B index + 16 B values per two nonzeros
       int64_t ps = 0, pe = 0;
@@ -454,8 +471,8 @@ __global__ void __launch_bounds__(WPB * 32, (EPI || PAIRS) ? 2 : 2048 / (WPB * 3
       }
       int64_t q = ps + sl;
       constexpr int PU = PAIRS >= 5 ? 4 : (PAIRS > 0 ? PAIRS : 1);
-      int cn[PU];
-      double2 vn[PU];
+      int pcn[PU];
+      double2 pvn[PU];
       auto ldv = [&](int64_t t) -> double2 {
         if (PAIRS == 6) {
           const double fq = ld_stream_d(PP.f + t);
@@ -466,23 +483,23 @@ __global__ void __launch_bounds__(WPB * 32, (EPI || PAIRS) ? 2 : 2048 / (WPB * 3
 #pragma unroll
       for (int u = 0; u < PU; ++u) {
         const int64_t t = q + (int64_t)LANES * u;
-        cn[u] = t < pe ? ld_stream_i(PP.col + t) : 0;
-        vn[u] = t < pe ? ldv(t) : make_double2(0.0, 0.0);
+        pcn[u] = t < pe ? ld_stream_i(PP.col + t) : 0;
+        pvn[u] = t < pe ? ldv(t) : make_double2(0.0, 0.0);
       }
       while (__any_sync(0xffffffffu, q < pe)) {
         int c[PU];
         double2 v[PU];
 #pragma unroll
         for (int u = 0; u < PU; ++u) {
-          c[u] = cn[u];
-          v[u] = vn[u];
+          c[u] = pcn[u];
+          v[u] = pvn[u];
         }
         const int64_t qn = q + (int64_t)LANES * PU;
 #pragma unroll
         for (int u = 0; u < PU; ++u) {
           const int64_t t = qn + (int64_t)LANES * u;
-          cn[u] = t < pe ? ld_stream_i(PP.col + t) : 0;
-          vn[u] = t < pe ? ldv(t) : make_double2(0.0, 0.0);
+          pcn[u] = t < pe ? ld_stream_i(PP.col + t) : 0;
+          pvn[u] = t < pe ? ldv(t) : make_double2(0.0, 0.0);
         }
         double x0[PU], x1[PU];
 #pragma unroll
@@ -503,15 +520,7 @@ __global__ void __launch_bounds__(WPB * 32, (EPI || PAIRS) ? 2 : 2048 / (WPB * 3
         q = qn;
       }
     }
-    int64_t p = s + sl;
-    int cn[UNR];
-    double vn[UNR];
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      const int64_t q = p + (int64_t)LANES * u;
-      cn[u] = q < e ? ld_stream_i(col + q) : 0;
-      vn[u] = q < e ? ld_stream_d(val + q) : 0.0;
-    }
+    if (!HOIST) first_chunks();
     while (__any_sync(0xffffffffu, p < e)) {
       int c[UNR];
       double v[UNR];
