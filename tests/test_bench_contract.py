@@ -36,3 +36,22 @@ def test_method_switch():
         s = b._spec_for(p, m)
         assert s.method == m and s.maxit == p.solvers[0].maxit
     assert b._spec_for(p, None) is p.solvers[0]
+
+
+def test_reference_arm_under_torchrun_world2():
+    # N > 1 (the driver's launch): rank 0 alone runs the oracle arm and prints the one JSON line,
+    # the other rank exits 0 without work
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, SFLSQR_REF_BUDGET_S="5")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"), "--impl", "reference",
+           "--config", "1", "--gpus", "2", "--steps", "3", "--warmup", "3"]
+    out = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["warmup"] == 3 and d["value"] > 0
