@@ -144,7 +144,11 @@ extern "C" {
 #define SFLSQR_KNOB_NO_ELL_C16 0x1000 /* 32-bit columns in the sliced-ELL interpolation pairs   */
 #define SFLSQR_KNOB_HALF_WARP_ROWS 0x2000 /* half a warp per row for every aligned-pair product (default:
                                             a full warp for short ray-like rows)        */
-#define SFLSQR_KNOB_ALL 0x3fff
+#define SFLSQR_KNOB_TMA 0x4000 /* aligned pair-CSR products with their column / value streams staged by TMA
+                                    bulk copies (cp.async.bulk + mbarrier ring per warp), a full warp per
+                                    row, bitwise equal to the full-warp register kernel; opt-in: measured
+                                    slower on configs 3-4                      */
+#define SFLSQR_KNOB_ALL 0x7fff
 
 /* opts.history bits */
 #define SFLSQR_HIST_TRUE_RES 1 /* record ||b - A x_k|| every iteration              */

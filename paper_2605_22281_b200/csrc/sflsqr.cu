@@ -231,11 +231,13 @@ int validate_csr(sflsqr_t* h, const char* name, int64_t nrows, int64_t ncols, co
 // rp may have a nonzero base.  row_map (optional) maps an output row j to its
 // position in a (possibly padded) output of nout rows.
 
+void destroy_graphs(sflsqr_t* h) {
+  if (h->gexec) cudaGraphExecDestroy(h->gexec);
+  h->gexec = nullptr;
+}
+
 void free_solve(sflsqr_t* h) {
-  if (h->gexec) {
-    cudaGraphExecDestroy(h->gexec);
-    h->gexec = nullptr;
-  }
+  destroy_graphs(h);
   if (h->comm) {
     cudaStreamSynchronize(h->stream);
     for (void** pp : {h->peer_zfull, h->peer_wfull, h->peer_zrecv}) {
@@ -463,7 +465,11 @@ void enqueue_apply(sflsqr_t* h, int which, const DevState* st, const double* x, 
   } else if (pc.interp)
     k_spmv_csr_pf<16, 4, 16, false, 6><<<grid_for(32, 2), 512, 0, h->stream>>>(
         st, nrows, pc.srp, pc.scol, pc.sval, x, x_ld, x_koff, y, SpmvEpi(), PP);
-  else if (pc.aligned && x16 && pc.warp_rows)  // a full warp per (short, ray-like) row: 16 rows per CTA
+  else if (pc.aligned && x16 && (h->knobs & SFLSQR_KNOB_TMA)) {  // TMA-staged streams, a full warp per row
+    launch_pdl(h, k_spmv_tma<8, 4, 2>, 148 * 2, 256, tma_smem_bytes<8, 4>(), h->stream, st, nrows,
+               (const int64_t*)pc.prp, (const int*)pc.pcol, (const double2*)pc.pval, (const int64_t*)pc.srp,
+               (const int*)pc.scol, (const double*)pc.sval, x, x_ld, x_koff, y);
+  } else if (pc.aligned && x16 && pc.warp_rows)  // a full warp per (short, ray-like) row: 16 rows per CTA
     launch_pdl(h, k_spmv_csr_pf<16, 4, 32, 0, 5>, grid_for(16, 2), 512, 0, h->stream, st, nrows,
                (const int64_t*)pc.srp, (const int*)pc.scol, (const double*)pc.sval, x, x_ld, x_koff, y, SpmvEpi(),
                PP);
@@ -938,6 +944,7 @@ int check_launch(sflsqr_t* h);
 // Pair-CSR copy of one operator (k_pcsr_rows): counts, two exclusive scans, fill.
 // min_frac: leave the operator plain (p.ok = false) unless at least that fraction of its nonzeros
 // pairs up (decided after the count pass, before any fill).
+constexpr int64_t kStreamPad = 16;
 int build_pcsr(sflsqr_t* h, int64_t nrows, const int64_t* rp, const int32_t* col, const double* val, PCSR& p,
                bool aligned = false, double min_frac = 0.0) {
   free_pcsr(p);
@@ -984,10 +991,11 @@ int build_pcsr(sflsqr_t* h, int64_t nrows, const int64_t* rp, const int32_t* col
     free_pcsr(p);
     return SFLSQR_OK;
   }
-  if ((rc = dalloc(h, (void**)&p.pcol, sizeof(int) * std::max<int64_t>(p.npairs, 1), nullptr)) ||
-      (rc = dalloc(h, (void**)&p.pval, sizeof(double2) * std::max<int64_t>(p.npairs, 1), nullptr)) ||
-      (rc = dalloc(h, (void**)&p.scol, sizeof(int) * std::max<int64_t>(p.nsingles, 1), nullptr)) ||
-      (rc = dalloc(h, (void**)&p.sval, sizeof(double) * std::max<int64_t>(p.nsingles, 1), nullptr))) {
+  // + kStreamPad entries: the TMA-staged product widens its copy ranges to 16-byte boundaries
+  if ((rc = dalloc(h, (void**)&p.pcol, sizeof(int) * (p.npairs + kStreamPad), nullptr)) ||
+      (rc = dalloc(h, (void**)&p.pval, sizeof(double2) * (p.npairs + kStreamPad), nullptr)) ||
+      (rc = dalloc(h, (void**)&p.scol, sizeof(int) * (p.nsingles + kStreamPad), nullptr)) ||
+      (rc = dalloc(h, (void**)&p.sval, sizeof(double) * (p.nsingles + kStreamPad), nullptr))) {
     cleanup();
     free_pcsr(p);
     return rc;
@@ -1459,10 +1467,7 @@ int zero_solve_state(sflsqr_t* h) {
 }
 
 int build_graph(sflsqr_t* h) {
-  if (h->gexec) {
-    cudaGraphExecDestroy(h->gexec);
-    h->gexec = nullptr;
-  }
+  destroy_graphs(h);
   const int64_t before = h->launches;
   const bool prof = h->prof_on;
   h->prof_on = false;
@@ -1753,6 +1758,8 @@ int sflsqr_create(sflsqr_t** out, const sflsqr_opts* o) {
   h->ell_c16 = !(kn & SFLSQR_KNOB_NO_ELL_C16);
   h->cgs_selective = !(kn & SFLSQR_KNOB_CGS_ALWAYS2);
   h->spmv_grid_delta = (kn & SFLSQR_KNOB_FULL_SPMV_GRID) ? 0 : 1;
+  if (kn & SFLSQR_KNOB_TMA)
+    cudaFuncSetAttribute(k_spmv_tma<8, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tma_smem_bytes<8, 4>());
   h->keep_csr = (kn & SFLSQR_KNOB_KEEP_CSR) != 0;
   if (kn & (SFLSQR_KNOB_RES_MAIN | SFLSQR_KNOB_RES_SIDE)) {
     h->res_overlap = (kn & SFLSQR_KNOB_RES_SIDE) != 0;
@@ -2439,10 +2446,7 @@ int sflsqr_debug_set_tuning(sflsqr_t* h, int32_t spmv_mode, int32_t band_shift) 
     int rc = build_formats(h);
     if (rc) return rc;
   }
-  if (h->gexec) {
-    cudaGraphExecDestroy(h->gexec);
-    h->gexec = nullptr;
-  }
+  destroy_graphs(h);
   return SFLSQR_OK;
 }
 

@@ -581,6 +581,230 @@ __global__ void __launch_bounds__(WPB * 32, (EPI || PAIRS) ? 2 : 2048 / (WPB * 3
   }
 }
 
+// ------------------------------------------------------------------ a3 / a6: TMA-staged pair-CSR
+// The aligned pair-CSR product (PAIRS == 5 above) with its streams -- the columns and values of
+// the row's pairs, then of its singletons -- moved by the Tensor Memory Accelerator's 1-D bulk
+// copies (cp.async.bulk, SASS UBLKCP) into a ring of NST shared-memory stages per warp, each
+// behind one mbarrier (expect_tx / complete_tx); the lanes read a stage with shared loads and
+// gather x from global memory, so the LSU's global path carries only the gathers.  A full warp
+// per row; a stage holds one kTmaCh-entry chunk of one stream, lane l taking entries l, l + 32,
+// ... of it: the per-lane FMA order and the shuffle tree of k_spmv_csr_pf<16, 4, 32, 0, 5>, so the
+// two products are bitwise equal.  Lane 0 refills a stage with the chunk NST ahead once the warp
+// has read it.  Source ranges are widened to 16-byte boundaries (the format arrays are padded).
+constexpr int kTmaCh = 128;
+struct alignas(16) TmaStage {
+  int col[kTmaCh + 8];         // columns of entries [e0 & ~3, (e0 + cnt + 3) & ~3)
+  double val[2 * kTmaCh + 8];  // pairs: kTmaCh double2; singletons: [e0 & ~1, (e0 + cnt + 1) & ~1)
+};
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n TMA_WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra TMA_WAIT_%=;\n}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(b))
+               : "memory");
+}
+
+// One warp's position in its chunk sequence: row, its pair / singleton ranges, chunk c of nc.
+struct TmaCur {
+  int64_t row, ps, np, ss, ns;
+  int c, nc;
+};
+__device__ __forceinline__ void tma_row(TmaCur& u, int64_t row, int64_t nrows, const int64_t* __restrict__ prp,
+                                        const int64_t* __restrict__ srp) {
+  u.row = row;
+  u.c = 0;
+  if (row >= nrows) {
+    u.nc = 0;
+    return;
+  }
+  u.ps = prp[row];
+  u.np = prp[row + 1] - u.ps;
+  u.ss = srp[row];
+  u.ns = srp[row + 1] - u.ss;
+  const int n = (int)((u.np + kTmaCh - 1) / kTmaCh + (u.ns + kTmaCh - 1) / kTmaCh);
+  u.nc = n > 0 ? n : 1;  // an empty row still takes one (empty) chunk: its y entry is written
+}
+__device__ __forceinline__ void tma_geom(const TmaCur& u, bool& pair, int64_t& e0, int& cnt) {
+  const int cp = (int)((u.np + kTmaCh - 1) / kTmaCh);
+  pair = u.c < cp;
+  const int64_t off = (int64_t)(pair ? u.c : u.c - cp) * kTmaCh;
+  e0 = (pair ? u.ps : u.ss) + off;
+  const int64_t left = (pair ? u.np : u.ns) - off;
+  cnt = (int)(left < kTmaCh ? (left > 0 ? left : 0) : kTmaCh);
+}
+
+// Per-lane registers of one chunk between its shared loads and its FMAs: the values and the
+// gathered x of entries lane + 32 u (pairs: both halves; singletons: .x only).
+struct TmaRegs {
+  double2 v[4], xx[4];
+  int cnt;
+  bool pair, last;
+  int64_t row;
+};
+
+template <int NW, int NST, int MINB>
+__global__ void __launch_bounds__(NW * 32, MINB) k_spmv_tma(const DevState* st, int64_t nrows,
+                                                           const int64_t* __restrict__ prp,
+                                                           const int* __restrict__ pcol,
+                                                           const double2* __restrict__ pval,
+                                                           const int64_t* __restrict__ srp,
+                                                           const int* __restrict__ scol,
+                                                           const double* __restrict__ sval,
+                                                           const double* __restrict__ x_base, int64_t x_ld,
+                                                           int x_koff, double* y) {
+  extern __shared__ __align__(16) unsigned char tma_sm[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  TmaStage* stg = reinterpret_cast<TmaStage*>(tma_sm) + wid * NST;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(tma_sm + sizeof(TmaStage) * NW * NST) + wid * NST;
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < NST; ++s) mbar_init(bar + s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncwarp();
+  pdl_wait();
+  if (st && st->done) return;
+  const double* __restrict__ x = kvec(st, x_base, x_ld, x_koff);
+  const int64_t rstride = (int64_t)gridDim.x * NW;
+  auto issue = [&](const TmaCur& u, int s) {  // lane 0: chunk u.c of u.row into stage s
+    bool pair;
+    int64_t e0;
+    int cnt;
+    tma_geom(u, pair, e0, cnt);
+    if (cnt == 0) {
+      mbar_expect_tx(bar + s, 0u);
+      return;
+    }
+    const int64_t a = e0 & ~(int64_t)3, b = (e0 + cnt + 3) & ~(int64_t)3;
+    const unsigned bc = (unsigned)(4 * (b - a));
+    if (pair) {
+      const unsigned bv = 16u * (unsigned)cnt;
+      mbar_expect_tx(bar + s, bc + bv);
+      bulk_g2s(stg[s].col, pcol + a, bc, bar + s);
+      bulk_g2s(stg[s].val, pval + e0, bv, bar + s);
+    } else {
+      const int64_t a2 = e0 & ~(int64_t)1, b2 = (e0 + cnt + 1) & ~(int64_t)1;
+      const unsigned bv = (unsigned)(8 * (b2 - a2));
+      mbar_expect_tx(bar + s, bc + bv);
+      bulk_g2s(stg[s].col, scol + a, bc, bar + s);
+      bulk_g2s(stg[s].val, sval + a2, bv, bar + s);
+    }
+  };
+  auto advance = [&](TmaCur& u) {
+    if (++u.c >= u.nc) tma_row(u, u.row + rstride, nrows, prp, srp);
+  };
+  TmaCur P, C;
+  tma_row(P, (int64_t)blockIdx.x * NW + wid, nrows, prp, srp);
+  C = P;
+  for (int s = 0; s < NST && P.nc > 0; ++s) {
+    if (lane == 0) issue(P, s);
+    advance(P);
+  }
+  // chunk t (consumer cursor C): wait for its stage, read it into registers, issue its gathers,
+  // hand the stage back to the producer (refilled with the chunk NST ahead), advance C
+  uint32_t t = 0;
+  auto load = [&](TmaRegs& R) {
+    const int s = (int)(t % NST);
+    mbar_wait(bar + s, (t / NST) & 1u);
+    int64_t e0;
+    tma_geom(C, R.pair, e0, R.cnt);
+    R.row = C.row;
+    R.last = C.c + 1 >= C.nc;
+    const TmaStage& S = stg[s];
+    const int oc = (int)(e0 & 3);
+    int c[4];
+    if (R.pair) {
+      const double2* sv = reinterpret_cast<const double2*>(S.val);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = lane + 32 * u;
+        c[u] = i < R.cnt ? S.col[oc + i] : 0;
+        R.v[u] = i < R.cnt ? sv[i] : make_double2(0.0, 0.0);
+      }
+    } else {
+      const int ov = (int)(e0 & 1);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = lane + 32 * u;
+        c[u] = i < R.cnt ? S.col[oc + i] : 0;
+        R.v[u] = make_double2(i < R.cnt ? S.val[ov + i] : 0.0, 0.0);
+      }
+    }
+    __syncwarp();
+    if (P.nc > 0) {
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(P, s);
+      }
+      advance(P);
+    }
+    if (R.pair) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        R.xx[u] = lane + 32 * u < R.cnt ? __ldg(reinterpret_cast<const double2*>(x + c[u])) : make_double2(0.0, 0.0);
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) R.xx[u] = make_double2(lane + 32 * u < R.cnt ? __ldg(x + c[u]) : 0.0, 0.0);
+    }
+    advance(C);
+    ++t;
+  };
+  double sum = 0.0;
+  auto consume = [&](const TmaRegs& R) {
+    if (R.pair) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (lane + 32 * u < R.cnt) sum = fma(R.v[u].y, R.xx[u].y, fma(R.v[u].x, R.xx[u].x, sum));
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (lane + 32 * u < R.cnt) sum = fma(R.v[u].x, R.xx[u].x, sum);
+    }
+    if (R.last) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      if (lane == 0) y[R.row] = sum;
+      sum = 0.0;
+    }
+  };
+  // two chunks in registers: the gathers of the next are in flight while the current is summed
+  TmaRegs A, B;
+  if (C.nc == 0) return;
+  load(A);
+  while (true) {
+    if (C.nc == 0) {
+      consume(A);
+      break;
+    }
+    load(B);
+    consume(A);
+    if (C.nc == 0) {
+      consume(B);
+      break;
+    }
+    load(A);
+    consume(B);
+  }
+}
+template <int NW, int NST>
+constexpr size_t tma_smem_bytes() {
+  return (sizeof(TmaStage) + sizeof(uint64_t)) * NW * NST;
+}
+
 // ------------------------------------------------------------------ pair-CSR (setup)
 // Splits every CSR row into adjacent-column pairs and singletons: each maximal run of
 // consecutive column indices c, c+1, ..., c+L-1 in a row gives floor(L/2) pairs (c, c+1),
