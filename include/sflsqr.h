@@ -148,7 +148,9 @@ extern "C" {
                                     bulk copies (cp.async.bulk + mbarrier ring per warp), a full warp per
                                     row, bitwise equal to the full-warp register kernel; opt-in: measured
                                     slower on configs 3-4                      */
-#define SFLSQR_KNOB_ALL 0x7fff
+#define SFLSQR_KNOB_WNORM_SEP 0x8000 /* the w normalisation as its own kernel (default on one rank: fused into the
+                                        transpose product, which then gathers the unnormalised w) */
+#define SFLSQR_KNOB_ALL 0xffff
 
 /* opts.history bits */
 #define SFLSQR_HIST_TRUE_RES 1 /* record ||b - A x_k|| every iteration              */

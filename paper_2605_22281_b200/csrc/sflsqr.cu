@@ -523,10 +523,43 @@ int enqueue_sketch(sflsqr_t* h, const DevState* st, const double* v, cudaStream_
   return coll_allreduce(h, h->P.skbuf, h->d, false);
 }
 
-// z = T w for w = W[:, k] (k-relative) or W[:, 0] (init).
-int enqueue_transpose_product(sflsqr_t* h, bool init) {
+// a5 end fused into a6 (one rank, full T, fused windowed orthogonalisation, T on a format with the
+// epilogue kernels): the product gathers the unnormalised w' and scales each row sum by 1 / ||w'||,
+// and its threads store w_{k+1} = w' / ||w'|| into W[:, k] and ||w'|| into H_{k+1,k} (SpmvEpi
+// kind 5) -- k_finish_w's pass without its launch and grid-wide dependency.  SFLSQR_KNOB_WNORM_SEP:
+// the separate normalisation kernel.
+bool wnorm_fused(const sflsqr_t* h) {
+  return h->world == 1 && h->tkind == T_FULL && !h->blur && h->P.orth_alg == ORTH_FUSED &&
+         !(h->knobs & SFLSQR_KNOB_WNORM_SEP) && !(runs_on_pairs(h, 1) && h->pt.warp_rows) &&
+         (runs_on_pairs(h, 1) || h->t_rowptr);
+}
+
+// z = T w for w = W[:, k] (k-relative) or W[:, 0] (init); wnorm: z = T (w' / ||w'||) with the
+// normalisation fused (wnorm_fused).
+int enqueue_transpose_product(sflsqr_t* h, bool init, bool wnorm = false) {
   Params& P = h->P;
   const int64_t ld = init ? 0 : h->m_loc;
+  if (h->tkind == T_FULL && wnorm) {
+    SpmvEpi E = SpmvEpi();
+    E.kind = 5;
+    E.aux = P.w;
+    E.scal = P.scal;
+    E.slot_in = P.slot_wout;
+    E.slot_in2 = P.slot_wf;
+    E.W = P.W;
+    E.m = h->m_loc;
+    E.H = P.H;
+    E.ldh = P.ldh;
+    const int64_t nrows = h->t_rows;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nrows + 31) / 32, 148 * 2 - h->spmv_grid_delta));
+    if (!launch_pairs_epi(h, 1, P.w, 0, P.z, E, SFLSQR_KC_SPMV_T, 16.0 * h->m_loc, grid)) {
+      Launch L(h, SFLSQR_KC_SPMV_T, 12.0 * h->nnz_t + 8.0 * (nrows + 1) + 8.0 * h->m_loc + 8.0 * nrows + 16.0 * h->m_loc);
+      launch_pdl(h, k_spmv_csr_pf<16, 4, 16, true>, grid, 512, 0, h->stream, P.st, nrows, (const int64_t*)h->t_rowptr,
+                 (const int*)h->t_col, (const double*)h->t_val, (const double*)P.w, (int64_t)0, 0, P.z, E,
+                 PairPart());
+    }
+    return SFLSQR_OK;
+  }
   if (h->tkind == T_FULL) {
     enqueue_apply(h, 1, P.st, P.W, ld, 0, P.z, SFLSQR_KC_SPMV_T);
     return SFLSQR_OK;
@@ -641,11 +674,15 @@ bool launch_pairs_epi(sflsqr_t* h, int which, const double* x, int64_t x_ld, dou
     const int64_t nsl = (nrows + kSellC - 1) / kSellC;
     const int g = (int)std::max<int64_t>(1, std::min<int64_t>((nsl + 15) / 16, 148 * 2 - h->spmv_grid_delta));
     if (pc.c16)
-      k_spmv_sell_ip<4, true, true><<<g, 512, 0, h->stream>>>(h->P.st, nrows, pc.soff, pc.rcnt, pc.ebase, pc.eoff, pc.ef,
-                                                             pc.srp, pc.scol, pc.sval, x, x_ld, 0, y, E);
+      launch_pdl(h, k_spmv_sell_ip<4, true, true>, g, 512, 0, h->stream, (const DevState*)h->P.st, nrows,
+                 (const int64_t*)pc.soff, (const int*)pc.rcnt, (const int*)pc.ebase, (const uint16_t*)pc.eoff,
+                 (const double*)pc.ef, (const int64_t*)pc.srp, (const int*)pc.scol, (const double*)pc.sval, x, x_ld, 0,
+                 y, E);
     else
-      k_spmv_sell_ip<4, true, false><<<g, 512, 0, h->stream>>>(h->P.st, nrows, pc.soff, pc.rcnt, pc.ecol, nullptr, pc.ef,
-                                                              pc.srp, pc.scol, pc.sval, x, x_ld, 0, y, E);
+      launch_pdl(h, k_spmv_sell_ip<4, true, false>, g, 512, 0, h->stream, (const DevState*)h->P.st, nrows,
+                 (const int64_t*)pc.soff, (const int*)pc.rcnt, (const int*)pc.ecol, (const uint16_t*)nullptr,
+                 (const double*)pc.ef, (const int64_t*)pc.srp, (const int*)pc.scol, (const double*)pc.sval, x, x_ld, 0,
+                 y, E);
     return true;
   }
   (void)grid;
@@ -656,15 +693,19 @@ bool launch_pairs_epi(sflsqr_t* h, int which, const double* x, int64_t x_ld, dou
   PP.col = pc.pcol;
   PP.val = pc.pval;
   PP.f = pc.f;
+  const DevState* st = h->P.st;
+  const int64_t* srp = pc.srp;
+  const int* scol = pc.scol;
+  const double* sval = pc.sval;
   if (pc.interp)
-    k_spmv_csr_pf<16, 4, 16, true, 6><<<grid, 512, 0, h->stream>>>(h->P.st, nrows, pc.srp, pc.scol, pc.sval, x, x_ld,
-                                                                    0, y, E, PP);
+    launch_pdl(h, k_spmv_csr_pf<16, 4, 16, true, 6>, grid, 512, 0, h->stream, st, nrows, srp, scol, sval, x, x_ld, 0, y,
+               E, PP);
   else if (pc.aligned && (uintptr_t)x % 16 == 0 && x_ld % 2 == 0)
-    k_spmv_csr_pf<16, 4, 16, true, 5><<<grid, 512, 0, h->stream>>>(h->P.st, nrows, pc.srp, pc.scol, pc.sval, x, x_ld,
-                                                                    0, y, E, PP);
+    launch_pdl(h, k_spmv_csr_pf<16, 4, 16, true, 5>, grid, 512, 0, h->stream, st, nrows, srp, scol, sval, x, x_ld, 0, y,
+               E, PP);
   else
-    k_spmv_csr_pf<16, 4, 16, true, 4><<<grid, 512, 0, h->stream>>>(h->P.st, nrows, pc.srp, pc.scol, pc.sval, x, x_ld,
-                                                                    0, y, E, PP);
+    launch_pdl(h, k_spmv_csr_pf<16, 4, 16, true, 4>, grid, 512, 0, h->stream, st, nrows, srp, scol, sval, x, x_ld, 0, y,
+               E, PP);
   return true;
 }
 
@@ -850,13 +891,17 @@ int enqueue_iteration(sflsqr_t* h) {
   const bool fork_ls = !h->prof_on && h->side &&
                        (P.method == SFLSQR_METHOD_SFLSQR || P.method == SFLSQR_METHOD_FLSQR);
   if (fork_ls && P.method == SFLSQR_METHOD_SFLSQR && (rc = enqueue_ls(h, true))) return rc;
-  // a5: w-side windowed orthogonalisation and normalisation
+  // a5: w-side windowed orthogonalisation and normalisation (the latter fused into a6 when
+  // wnorm_fused)
+  const bool wn_fused = wnorm_fused(h);
   {
     rc = enqueue_orth(h, 1, 0);
     h->axpy_wait_sk = -1;
     if (rc) return rc;
-    Launch L(h, SFLSQR_KC_ORTH, 2 * m8);
-    launch_pdl(h, k_finish_w, vec_grid(h->m_loc), kVecThreads, 0, h->stream, P);
+    if (!wn_fused) {
+      Launch L(h, SFLSQR_KC_ORTH, 2 * m8);
+      launch_pdl(h, k_finish_w, vec_grid(h->m_loc), kVecThreads, 0, h->stream, P);
+    }
   }
   if (fork_ls && P.method == SFLSQR_METHOD_FLSQR && (rc = enqueue_ls(h, true))) return rc;
   // a8 on the side stream after the LS (sFLSQR / FLSQR with an x-dependent tau, one rank): the main
@@ -876,7 +921,7 @@ int enqueue_iteration(sflsqr_t* h) {
   // and the concurrent stream lowers the SM clock (-0.5 %), so large operators keep it serial.
   const bool res_side = fork_ls && P.want_res && h->world == 1 && h->res_overlap &&
                         (h->res_overlap_forced || h->nnz_a + h->nnz_t < (int64_t)1000000000);
-  if (res_side) {
+  auto fork_res = [&]() -> int {
     CU(h, cudaEventRecord(h->ev_w, h->stream));
     CU(h, cudaStreamWaitEvent(h->side, h->ev_w, 0));
     {
@@ -884,9 +929,13 @@ int enqueue_iteration(sflsqr_t* h) {
       launch_res(h, h->side, 0);
     }
     CU(h, cudaEventRecord(h->ev_join, h->side));
-  }
-  // a6: z = T w_{k+1}  (w_{k+1} = W[:, k])
-  if ((rc = enqueue_transpose_product(h, false))) return rc;
+    return SFLSQR_OK;
+  };
+  if (res_side && !wn_fused && (rc = fork_res())) return rc;
+  // a6: z = T w_{k+1}  (w_{k+1} = W[:, k]; with wn_fused the product also stores w_{k+1} and H_{k+1,k},
+  // so the residual's fork follows it)
+  if ((rc = enqueue_transpose_product(h, false, wn_fused))) return rc;
+  if (res_side && wn_fused && (rc = fork_res())) return rc;
   // FLSMR: z side of step k+1 now (column k+1 of T for T_{k+1} H_{k+1,k}, L361-367).
   // sFLSMR: the same, on the main stream while the LS (which needs only S z) runs on the side
   // stream -- the z-side dots/axpy of step k+1 depend on neither the LS nor the stop test.

@@ -381,6 +381,12 @@ __device__ __forceinline__ double* kvec_w(const DevState* st, double* base, int6
 //   kind 4 (COLSHARD T product, peer memory): row r of the padded n layout is owned by rank
 //                     g = r / nmax; the row sum is stored into peers[g][src * nmax + r - g nmax]
 //                     (reduce-scatter fused into the product; k_reduce_recv sums the slots)
+//   kind 5 (T side, w normalisation fused, one rank): x = w' (the orthogonalised w, unnormalised),
+//                     beta = ||w'|| = sqrt(scal[slot_in]), w_in = sqrt(scal[slot_in2]); breakdown
+//                     when beta <= 1e-14 w_in (reading R11), a = breakdown ? 0 : 1 / beta:
+//                     y = a (T w') = T w_{k+1} up to rounding, and the kernel's threads also write
+//                     w_{k+1} = a w' into W[:, k] and beta into H_{k+1,k} (k_finish_w's work, Alg. 1
+//                     L483 / Alg. 2) -- one phase fewer on the critical path.
 struct SpmvEpi {
   int kind;               // 0: plain y = M x
   double* aux;            // may alias y (each row reads and writes only its own entry)
@@ -392,6 +398,11 @@ struct SpmvEpi {
   int src;                // kind 4: this rank
   int64_t nmax;           // kind 4: rows per rank in the padded layout
   double* peers[8];       // kind 4: every rank's receive buffer (world x nmax)
+  int slot_in2;           // kind 5: ||w||^2 before the orthogonalisation (breakdown threshold)
+  double* W;              // kind 5: W (m x (maxit + 1)), column k receives w_{k+1}
+  int64_t m;              // kind 5: length of w
+  double* H;              // kind 5: H, H_{k+1,k} = beta
+  int64_t ldh;
 };
 
 __device__ __forceinline__ void epi_coefs(const SpmvEpi& E, const DevState* st, double& a, double& c) {
@@ -404,6 +415,25 @@ __device__ __forceinline__ void epi_coefs(const SpmvEpi& E, const DevState* st, 
     const double bn = sqrt(E.scal[E.slot_in]);
     a = bn > 0.0 ? 1.0 / bn : 0.0;
     c = E.kind == 2 ? bn : 0.0;
+  } else if (E.kind == 5) {
+    const double hn = sqrt(E.scal[E.slot_in]), win = sqrt(E.scal[E.slot_in2]);
+    const bool brk = hn == 0.0 || hn <= 1e-14 * win;
+    a = brk ? 0.0 : 1.0 / hn;
+  }
+}
+
+// kind 5 prologue (every thread of the product's grid): w_{k+1} = a w' into W[:, k], and by one
+// thread H_{k+1,k} = beta (0 on breakdown) and the breakdown flag -- k_finish_w's stores.
+__device__ __forceinline__ void epi_wnorm(const SpmvEpi& E, const DevState* st, double a) {
+  const int k = st->k;
+  double* wk1 = E.W + (int64_t)k * E.m;
+  const double* __restrict__ w = E.aux;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < E.m; i += (int64_t)gridDim.x * blockDim.x)
+    wk1[i] = a == 0.0 ? 0.0 : w[i] * a;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    DevState* sw = const_cast<DevState*>(st);
+    sw->wbreak = a == 0.0 ? 1 : 0;
+    E.H[(int64_t)k + (int64_t)(k - 1) * E.ldh] = a == 0.0 ? 0.0 : sqrt(E.scal[E.slot_in]);
   }
 }
 
@@ -433,6 +463,7 @@ __global__ void __launch_bounds__(WPB * 32, (EPI || PAIRS) ? 2 : 2048 / (WPB * 3
   if (st && st->done) return;
   double ea = 1.0, ec = 0.0, nrm = 0.0;
   if (EPI) epi_coefs(E, st, ea, ec);
+  if (EPI && E.kind == 5) epi_wnorm(E, st, ea);
   const double* __restrict__ x = kvec(st, x_base, x_ld, x_koff);
   constexpr int RPW = 32 / LANES;  // rows per warp
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -552,14 +583,14 @@ __global__ void __launch_bounds__(WPB * 32, (EPI || PAIRS) ? 2 : 2048 / (WPB * 3
         E.peers[g][(int64_t)E.src * E.nmax + (row - g * E.nmax)] = sum;
       } else {
         if (EPI) {
-          sum = E.kind == 3 ? sum * ea : fma(sum, ea, -ec * E.aux[row]);
+          sum = (E.kind == 3 || E.kind == 5) ? sum * ea : fma(sum, ea, -ec * E.aux[row]);
           nrm = fma(sum, sum, nrm);
         }
         y[row] = sum;
       }
     }
   }
-  if (EPI && E.kind != 4) {
+  if (EPI && E.kind != 4 && E.kind != 5) {
     __shared__ double sh[33];
     __shared__ int s_last;
     nrm = block_sum<WPB * 32>(nrm, sh);
@@ -912,6 +943,7 @@ __global__ void __launch_bounds__(512, 2) k_spmv_sell_ip(const DevState* st, int
   if (st && st->done) return;
   double ea = 1.0, ec = 0.0, nrm = 0.0;
   if (EPI) epi_coefs(E, st, ea, ec);
+  if (EPI && E.kind == 5) epi_wnorm(E, st, ea);
   const double* __restrict__ x = kvec(st, x_base, x_ld, x_koff);
   const int lane = threadIdx.x & 31;
   const int64_t nslices = (nrows + kSellC - 1) / kSellC;
@@ -971,14 +1003,14 @@ __global__ void __launch_bounds__(512, 2) k_spmv_sell_ip(const DevState* st, int
         E.peers[g][(int64_t)E.src * E.nmax + (row - g * E.nmax)] = sum;
       } else {
         if (EPI) {
-          sum = E.kind == 3 ? sum * ea : fma(sum, ea, -ec * E.aux[row]);
+          sum = (E.kind == 3 || E.kind == 5) ? sum * ea : fma(sum, ea, -ec * E.aux[row]);
           nrm = fma(sum, sum, nrm);
         }
         y[row] = sum;
       }
     }
   }
-  if (EPI && E.kind != 4) {
+  if (EPI && E.kind != 4 && E.kind != 5) {
     __shared__ double sh[33];
     __shared__ int s_last;
     nrm = block_sum<512>(nrm, sh);

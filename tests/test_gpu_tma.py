@@ -116,3 +116,24 @@ def test_tma_config4_reduced_against_oracle():
     g = _gpu_run(p, spec, maxit=K, eta=0.0, knobs=["tma"])
     assert g["info"]["a_fmt"] == 2
     _compare(g, r, n_res=K)
+
+
+@pytest.mark.parametrize("cfg,method", [(3, "sflsqr"), (3, "sflsmr"), (4, "sflsqr"), (1, "sflsmr")])
+def test_wnorm_fused_into_transpose_product(cfg, method):
+    # one rank: the w normalisation (k_finish_w) runs inside the transpose product (SpmvEpi kind 5:
+    # gathers of the unnormalised w', row sums scaled by 1/||w'||, W[:, k] and H_{k+1,k} stored by
+    # the product's threads); SFLSQR_KNOB_WNORM_SEP keeps the separate kernel.  Both solves hold the
+    # oracle's bar, and the bases agree to rounding
+    import dataclasses
+    kw = {3: dict(N=128, n_angles=90, nb=183), 4: dict(N=96, n_angles=61, nb=137), 1: {}}[cfg]
+    p = make_problem(cfg, **kw)
+    spec = dataclasses.replace(p.solvers[0], method=method)
+    K = 12
+    r = solve_problem(p, spec, maxit=K, eta=0.0)
+    runs = {}
+    for kn in ([], ["wnorm_sep"]):
+        g = _gpu_run(p, spec, maxit=K, eta=0.0, knobs=kn)
+        _compare(g, r, n_res=K)
+        runs[bool(kn)] = g
+    a, b = runs[False], runs[True]
+    assert np.max(np.abs(a["x"] - b["x"])) <= 1e-8 * np.max(np.abs(b["x"]))
