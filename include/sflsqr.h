@@ -150,10 +150,7 @@ extern "C" {
                                     slower on configs 3-4                      */
 #define SFLSQR_KNOB_WNORM_SEP 0x8000 /* the w normalisation as its own kernel (default on one rank: fused into the
                                         transpose product, which then gathers the unnormalised w) */
-#define SFLSQR_KNOB_STOP_INLINE 0x10000 /* the residual and stop tests of iteration k at its end (default on one rank
-                                          for sFLSQR / sFLSMR with the residual history: during iteration
-                                          k + 1, beside its z side and A z; bitwise the same results)    */
-#define SFLSQR_KNOB_ALL 0x1ffff
+#define SFLSQR_KNOB_ALL 0xffff
 
 /* opts.history bits */
 #define SFLSQR_HIST_TRUE_RES 1 /* record ||b - A x_k|| every iteration              */

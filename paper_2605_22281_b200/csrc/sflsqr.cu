@@ -74,7 +74,7 @@ struct sflsqr {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   cudaStream_t side = nullptr;  // second stream: the projected LS overlaps the T product (fork/join)
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_w = nullptr, ev_sk = nullptr, ev_z = nullptr, ev_stop = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_w = nullptr, ev_sk = nullptr;
   int axpy_wait_sk = -1;  // enqueue_orth(this side): wait for ev_sk (sketch on the side stream) before the in-place update
   // sFLSQR's sketch of A z on the side stream beside the w-side dots (SFLSQR_KNOB_SKETCH_MAIN: main
   // stream): config 1 +6 %, config 2 +1 %, config 3 +2 %, config 4 unchanged (same box)
@@ -843,23 +843,6 @@ int enqueue_lowrank(sflsqr_t* h) {
   return SFLSQR_OK;
 }
 
-// Deferred stop (one rank, sFLSQR / sFLSMR with the W-path residual, a side stream): the residual
-// and stop tests of iteration k run on the side stream during iteration k + 1, beside its z side
-// and A z_{k+1} -- the L1-bound product leaves HBM bandwidth the residual's GEMV over W_{k+1} uses.
-// The z side and A z_{k+1} only write vectors a stop at k discards (z, Z[:, k], P ring, w), and the
-// main stream waits for the stop test before anything else of iteration k + 1, so every result
-// (x, histories, status, stop index) is bitwise that of the inline order (SFLSQR_KNOB_STOP_INLINE).
-// iterate() takes the last iteration's tests after its final launch.
-bool defer_stop(const sflsqr_t* h) {
-  const int me = h->P.method;
-  return h->world == 1 && h->P.want_res && h->side && !(h->knobs & SFLSQR_KNOB_STOP_INLINE) &&
-         (me == SFLSQR_METHOD_SFLSQR || me == SFLSQR_METHOD_SFLSMR);
-}
-void enqueue_deferred_res(sflsqr_t* h, cudaStream_t s) {
-  Launch L(h, SFLSQR_KC_RES, 8.0 * h->m_loc * std::max(1, h->host_k));
-  launch_pdl(h, k_res_partial<kGemvRpt>, gemv_grid(h->m_loc), kVecThreads, 0, s, h->P, 2);
-}
-
 // One iteration k of Alg. 1 / Alg. 2, or of FLSQR /
 // FLSMR (full window, no sketch; FLSMR runs the z side of step k+1 before its
 // projected problem, which needs column k+1 of T).
@@ -869,34 +852,12 @@ int enqueue_iteration(sflsqr_t* h) {
   const int k = h->host_k;  // used only for the byte model
   const double n8 = 8.0 * h->n_loc, m8 = 8.0 * h->m_loc;
   int rc;
-  const bool dstop = defer_stop(h);
-  const bool dside = dstop && !h->prof_on;  // the deferred tests on the side stream (else in line)
-  // deferred a9 of iteration k-1: its W-path residual beside this iteration's z side and A z_k
-  if (dside) {
-    CU(h, cudaEventRecord(h->ev_fork, h->stream));
-    CU(h, cudaStreamWaitEvent(h->side, h->ev_fork, 0));
-    enqueue_deferred_res(h, h->side);
-  } else if (dstop) {
-    enqueue_deferred_res(h, h->stream);
-  }
   // a1: z-side windowed orthogonalisation (FLSMR: done at the end of the previous step / in set_rhs)
   if (!z_early(h) && (rc = enqueue_orth(h, 0, 0))) return rc;
   // a1 end + a2: normalise, tau, store z_k
   {
     Launch L(h, SFLSQR_KC_TAU, n8 * (2 + (P.use_pring ? 1 : 0) + (P.precond ? 1 : 0)));
     launch_pdl(h, k_finish_z, vec_grid(h->n_loc), kVecThreads, 0, h->stream, P);
-  }
-  // deferred a9: the stop tests of iteration k-1 (they also see this iteration's z-side breakdown)
-  if (dstop) {
-    Launch L(h, SFLSQR_KC_STOP, 0.0);
-    if (dside) {
-      CU(h, cudaEventRecord(h->ev_z, h->stream));
-      CU(h, cudaStreamWaitEvent(h->side, h->ev_z, 0));
-      k_stop_deferred<<<1, 32, 0, h->side>>>(P);
-      CU(h, cudaEventRecord(h->ev_stop, h->side));
-    } else {
-      k_stop_deferred<<<1, 32, 0, h->stream>>>(P);
-    }
   }
   if (P.precond == SFLSQR_PRECOND_LOWRANK_RND && (rc = enqueue_lowrank(h))) return rc;
   // a3: w = A z_k  (z_k = Z[:, k-1]; all-gathered across ranks when sharded)
@@ -911,9 +872,6 @@ int enqueue_iteration(sflsqr_t* h) {
     }
     enqueue_apply(h, 0, P.st, h->zfull, 0, 0, P.w, SFLSQR_KC_SPMV_A);
   }
-  // nothing past A z_k before the deferred stop test has decided (the side stream's order holds
-  // the sketch, LS and x update behind it)
-  if (dside) CU(h, cudaStreamWaitEvent(h->stream, h->ev_stop, 0));
   // a4 (sFLSQR): S_AZ[:, k] = S w -- on the side stream (one rank), beside the w-side dots; the
   // in-place w update waits for it (SFLSQR_KNOB_SKETCH_MAIN: main stream)
   const bool sk_side = h->sketch_side && P.method == SFLSQR_METHOD_SFLSQR && h->world == 1 && h->side &&
@@ -961,7 +919,7 @@ int enqueue_iteration(sflsqr_t* h) {
   // main stream after the join (the T product reads st->k, which the stop test advances).
   // Measured: +3 % on config 3; on config 4 (2.5e9 nnz) the board is power capped
   // and the concurrent stream lowers the SM clock (-0.5 %), so large operators keep it serial.
-  const bool res_side = !dstop && fork_ls && P.want_res && h->world == 1 && h->res_overlap &&
+  const bool res_side = fork_ls && P.want_res && h->world == 1 && h->res_overlap &&
                         (h->res_overlap_forced || h->nnz_a + h->nnz_t < (int64_t)1000000000);
   auto fork_res = [&]() -> int {
     CU(h, cudaEventRecord(h->ev_w, h->stream));
@@ -1013,11 +971,6 @@ int enqueue_iteration(sflsqr_t* h) {
       launch_xupdate(h, 0);
     }
     if ((rc = coll_allreduce(h, P.scal + P.slot_xmax, 1, true))) return rc;
-  }
-  if (dstop) {  // a9 of this iteration runs during the next one (or after iterate()'s last launch)
-    Launch L(h, SFLSQR_KC_STOP, 0.0);
-    launch_pdl(h, k_advance, 1, 32, 0, h->stream, P);
-    return SFLSQR_OK;
   }
   // a9: true residual (W path) and stop tests (fused into the residual kernel on one rank)
   const bool fuse_stop = P.want_res && h->world == 1 && !h->prof_on && !res_side;
@@ -1417,7 +1370,6 @@ int alloc_solve(sflsqr_t* h) {
   P.s_nz = h->s_nz;
   P.dist = h->world > 1 ? 1 : 0;
   P.want_res = ((h->o.history & SFLSQR_HIST_TRUE_RES) || h->o.eta > 0.0) ? 1 : 0;
-  P.defer_stop = defer_stop(h) ? 1 : 0;  // reads P.method and P.want_res (set above)
   P.need_x = (h->pkind == SFLSQR_PRECOND_IRN || h->pkind == SFLSQR_PRECOND_NONNEG) ? 1 : 0;
   P.use_pring = (h->o.orth_mode == SFLSQR_ORTH_P && h->pkind != SFLSQR_PRECOND_IDENTITY) ? 1 : 0;
   P.p_exp = h->p_exp;
@@ -1866,9 +1818,7 @@ int sflsqr_create(sflsqr_t** out, const sflsqr_opts* o) {
       cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_w, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&h->ev_sk, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&h->ev_z, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&h->ev_stop, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&h->ev_sk, cudaEventDisableTiming) != cudaSuccess) {
     cudaGetLastError();
     h->side = nullptr;  // no overlap; the LS runs on the main stream
   }
@@ -2272,11 +2222,6 @@ int sflsqr_iterate(sflsqr_t* h, int32_t k, int32_t* done, int32_t* status) {
     }
     h->host_k++;
   }
-  if (todo > 0 && defer_stop(h)) {  // the last iteration's deferred residual and stop tests
-    enqueue_deferred_res(h, h->stream);
-    Launch L(h, SFLSQR_KC_STOP, 0.0);
-    k_stop_deferred<<<1, 32, 0, h->stream>>>(h->P);
-  }
   if ((rc = check_launch(h))) return rc;
   CU(h, cudaMemcpyAsync(&st, h->P.st, sizeof(st), cudaMemcpyDeviceToHost, h->stream));
   CU(h, cudaStreamSynchronize(h->stream));
@@ -2587,8 +2532,6 @@ void sflsqr_destroy(sflsqr_t* h) {
   if (h->ev_join) cudaEventDestroy(h->ev_join);
   if (h->ev_w) cudaEventDestroy(h->ev_w);
   if (h->ev_sk) cudaEventDestroy(h->ev_sk);
-  if (h->ev_z) cudaEventDestroy(h->ev_z);
-  if (h->ev_stop) cudaEventDestroy(h->ev_stop);
   if (h->own_stream) cudaStreamDestroy(h->stream);
   delete h;
 }

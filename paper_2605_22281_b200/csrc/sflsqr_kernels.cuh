@@ -36,8 +36,7 @@ struct DevState {
   int k_x;        // iterate held in y (x_{k_x} = Z_{k_x} y)
   int wbreak;     // w-side breakdown in the current iteration (reading R11)
   int rank_flag;  // R14
-  int zbreak;     // deferred stop: z-side breakdown of the current iteration (reading R11)
-  int pad1;
+  int pad0, pad1;
   double beta;    // ||b||
   double rhs_norm;
 };
@@ -47,7 +46,6 @@ struct Params {
   DevState* st;
   int64_t m, n;
   int ell, maxit, method, orth_mode, precond, d, s_nz, want_res, need_x, use_pring;
-  int defer_stop;  // a9 of iteration k taken during iteration k + 1 (sflsqr.cu defer_stop)
   int ldh;                 // leading dimension of H = maxit + 1
   int ldtm;                // leading dimension of Tm = maxit + 1 (FLSMR forms column maxit+1)
   int dist;                // world > 1: reductions come from scal[] (allreduced), not from part[]
@@ -1821,16 +1819,11 @@ __device__ __forceinline__ bool finish_z_body(const Params& P, DevState* st, int
   if (t == 0.0 || t <= 1e-14 * zin) {
     __syncthreads();
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-      if (P.defer_stop) {
-        st->zbreak = 1;  // the deferred stop test of iteration k - 1 ends the solve there
-      } else {
-        st->done = 1;
-        st->status = 4;  // SFLSQR_BREAKDOWN; y still holds y_{k-1}
-      }
+      st->done = 1;
+      st->status = 4;  // SFLSQR_BREAKDOWN; y still holds y_{k-1}
     }
     return false;
   }
-  if (P.defer_stop && blockIdx.x == 0 && threadIdx.x == 0) st->zbreak = 0;
   if (blockIdx.x == 0 && threadIdx.x == 0) P.Tm[(int64_t)(k - 1) + (int64_t)(k - 1) * P.ldtm] = t;
   // tau weights need x_{k-1} (computed by k_xupdate at the end of iteration k-1)
   int mode = P.precond;  // 0 identity, 1 IRN, 2 NONNEG, 3 low-rank (tau applied by the k_lr_* kernels)
@@ -2700,18 +2693,14 @@ __device__ __forceinline__ void stop_body(const Params& P, DevState* st, double 
 // (eq. FGK: A Z_k = W_{k+1} H_{k+1,k}, w_1 = b/beta).  Every block forms g in
 // shared memory from the band of H; fuse_stop (one rank): the last block also runs
 // the stop tests.
-// mode 0: iteration st->k; 1: the same with the stop tests fused; 2 (deferred stop): iteration
-// st->k - 1 (nothing before the first iteration).
 template <int RPT>
-__global__ void __launch_bounds__(kVecThreads) k_res_partial(Params P, int mode) {
+__global__ void __launch_bounds__(kVecThreads) k_res_partial(Params P, int fuse_stop) {
   pdl_wait();
   __shared__ double sh[33];
   __shared__ double gs[kMaxD];
   DevState* st = P.st;
   if (st->done) return;
-  const int k = mode == 2 ? st->k - 1 : st->k, kk = k + 1;  // columns of W_{k+1}
-  if (k < 1) return;
-  const bool fuse_stop = mode == 1;
+  const int k = st->k, kk = k + 1;  // columns of W_{k+1}
   for (int i = threadIdx.x; i <= k; i += kVecThreads) {
     double acc = (i == 0) ? st->beta : 0.0;
     const int jlo = max(0, i - 1), jhi = min(k - 1, i + P.ell);  // band: H_ij != 0 for j - ell <= i <= j + 1
@@ -2732,42 +2721,6 @@ __global__ void __launch_bounds__(kVecThreads) k_res_partial(Params P, int mode)
   if (threadIdx.x == 0) P.part[(size_t)P.slot_res * kVecBlocks + blockIdx.x] = acc2;
   const bool last = last_block_reduce(P, P.slot_res, 1, CTR_RES, false);
   if (fuse_stop && last && threadIdx.x == 0) stop_body(P, st, sqrt(P.scal[P.slot_res]));
-}
-
-// Deferred a9 (one rank, sflsqr.cu defer_stop): the stop tests of iteration k - 1 = st->k - 1, taken
-// during iteration k after its z side (k_finish_z) and before anything of iteration k that a stop
-// at k - 1 must not see (the LS overwriting y, the x update, the w-side breakdown flag); st->k is
-// advanced by k_advance at the end of every iteration.  Same tests in the same order as
-// stop_body, then the z-side breakdown of iteration k (which also ends the solve at k - 1: y still
-// holds y_{k-1}, reading R11).  Before the first iteration only the z-side breakdown can apply.
-__global__ void __launch_bounds__(32) k_stop_deferred(Params P) {
-  DevState* st = P.st;
-  if (threadIdx.x != 0 || st->done) return;
-  const int k = st->k - 1;
-  int status = 0;
-  if (k >= 1) {
-    const double r = sqrt(P.scal[P.slot_res]);
-    P.hist_true[k - 1] = r;
-    const double sres = P.hist_sk[k - 1];
-    if (st->wbreak)
-      status = 4;
-    else if (P.tol > 0.0 && sres < P.tol * st->rhs_norm)
-      status = 2;
-    else if (P.eta > 0.0 && r <= P.eta * P.delta_e)
-      status = 3;
-    else if (k >= P.maxit)
-      status = 1;
-  }
-  if (!status && st->zbreak) status = 4;
-  if (status) {
-    st->status = status;
-    st->done = 1;
-  }
-}
-// End of an iteration under the deferred stop: k advances unless the solve has stopped.
-__global__ void __launch_bounds__(32) k_advance(Params P) {
-  pdl_wait();
-  if (threadIdx.x == 0 && !P.st->done) P.st->k += 1;
 }
 
 // a9 without the fused residual (no history, or several ranks: after the allreduce).
@@ -3009,7 +2962,6 @@ __global__ void k_init_rhs(Params P) {
     P.st->status = 0;
     P.st->k_x = 0;
     P.st->wbreak = 0;
-    P.st->zbreak = 0;
     P.st->rank_flag = 0;
   }
 }

@@ -51,7 +51,7 @@ COMM_NCCL, COMM_LOCAL = 0, 1
 KNOBS = {"no_pdl": 0x1, "sketch_main": 0x2, "no_interp": 0x4, "no_sell": 0x8, "cgs_always2": 0x10,
          "full_spmv_grid": 0x20, "res_main": 0x40, "res_side": 0x80, "p2p_on": 0x100, "p2p_off": 0x200,
          "keep_csr": 0x400, "debug_poison": 0x800, "no_ell_c16": 0x1000, "half_warp_rows": 0x2000,
-         "tma": 0x4000, "wnorm_sep": 0x8000, "stop_inline": 0x10000}
+         "tma": 0x4000, "wnorm_sep": 0x8000}
 
 
 def knob_bits(knobs):

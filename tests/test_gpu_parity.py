@@ -714,7 +714,7 @@ def test_pair_formats_odd_dimensions():
 
 
 @pytest.mark.parametrize("knob", ["no_pdl", "sketch_main", "full_spmv_grid", "res_main", "res_side", "keep_csr",
-                                  "debug_poison", "stop_inline"])
+                                  "debug_poison"])
 def test_scheduling_knobs_bitwise_neutral(knob):
     # launch scheduling (programmatic dependent launch, the sketch and the W-path residual on the side
     # or main stream, the SpMV grid size), keeping the uploaded CSR and NaN-poisoned solve buffers
