@@ -1,0 +1,15 @@
+# Round-2 final captures after the TMA experiment and the fused w normalisation (same recipe as r2q)
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/r2x_build.log 2>&1 || { tail gpurun_out/r2x_build.log; exit 1; }
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,driver_version --format=csv > gpurun_out/r2x_gpu.txt
+timeout -s KILL 2400 python -m pytest tests -m gpu -q > gpurun_out/r2x_pytest.log 2>&1
+echo "pytest rc=$?"; tail -3 gpurun_out/r2x_pytest.log
+timeout -s KILL 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/r2x_smoke.log 2>&1; echo "smoke rc=$?"
+timeout -s KILL 900 python bench.py > gpurun_out/r2x_bench_default.log 2>&1; echo "default rc=$?"
+timeout -s KILL 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/r2x_bench_reference.log 2>&1; echo "ref rc=$?"
+for a in "--config 3" "--config 3 --method sflsmr" "--config 3 --method flsqr" "--config 3 --method lsqr" "--config 4 --method sflsmr" "--config 4 --method flsqr" "--config 4 --method lsqr" "--config 2 --steps 95" "--config 1 --steps 35" "--config 8 --steps 45" "--config 6 --steps 45 --warmup 3" "--config 7 --steps 45 --warmup 3"; do
+  tag=$(echo "$a" | tr -d ' -')
+  timeout -s KILL 600 python bench.py $a --no-cpu-baseline --no-e2e > gpurun_out/r2x_bench_$tag.log 2>&1
+done
+bash tools/ncu_capture.sh r2x_c4 "k_spmv|k_orth|k_finish|k_res|k_sketch_apply|k_ls" 40 16 --config 4 --steps 5 --warmup 3
+bash tools/ncu_capture.sh r2x_c3 "k_spmv|k_orth|k_finish|k_res|k_sketch_apply|k_ls|k_xupdate" 20 16 --config 3 --steps 5 --warmup 5
+echo done
