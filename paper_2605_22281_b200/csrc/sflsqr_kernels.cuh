@@ -463,7 +463,6 @@ __global__ void __launch_bounds__(WPB * 32, (EPI || PAIRS) ? 2 : 2048 / (WPB * 3
   if (st && st->done) return;
   double ea = 1.0, ec = 0.0, nrm = 0.0;
   if (EPI) epi_coefs(E, st, ea, ec);
-  if (EPI && E.kind == 5) epi_wnorm(E, st, ea);
   const double* __restrict__ x = kvec(st, x_base, x_ld, x_koff);
   constexpr int RPW = 32 / LANES;  // rows per warp
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -590,6 +589,9 @@ __global__ void __launch_bounds__(WPB * 32, (EPI || PAIRS) ? 2 : 2048 / (WPB * 3
       }
     }
   }
+  // kind 5: the w normalisation after this CTA's rows (nothing in the product reads it), so CTAs
+  // that finish their rows early fill the product's tail with it
+  if (EPI && E.kind == 5) epi_wnorm(E, st, ea);
   if (EPI && E.kind != 4 && E.kind != 5) {
     __shared__ double sh[33];
     __shared__ int s_last;
@@ -943,7 +945,6 @@ __global__ void __launch_bounds__(512, 2) k_spmv_sell_ip(const DevState* st, int
   if (st && st->done) return;
   double ea = 1.0, ec = 0.0, nrm = 0.0;
   if (EPI) epi_coefs(E, st, ea, ec);
-  if (EPI && E.kind == 5) epi_wnorm(E, st, ea);
   const double* __restrict__ x = kvec(st, x_base, x_ld, x_koff);
   const int lane = threadIdx.x & 31;
   const int64_t nslices = (nrows + kSellC - 1) / kSellC;
@@ -1010,6 +1011,9 @@ __global__ void __launch_bounds__(512, 2) k_spmv_sell_ip(const DevState* st, int
       }
     }
   }
+  // kind 5: the w normalisation after this CTA's rows (nothing in the product reads it), so CTAs
+  // that finish their rows early fill the product's tail with it
+  if (EPI && E.kind == 5) epi_wnorm(E, st, ea);
   if (EPI && E.kind != 4 && E.kind != 5) {
     __shared__ double sh[33];
     __shared__ int s_last;

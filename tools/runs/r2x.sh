@@ -13,3 +13,12 @@ done
 bash tools/ncu_capture.sh r2x_c4 "k_spmv|k_orth|k_finish|k_res|k_sketch_apply|k_ls" 40 16 --config 4 --steps 5 --warmup 3
 bash tools/ncu_capture.sh r2x_c3 "k_spmv|k_orth|k_finish|k_res|k_sketch_apply|k_ls|k_xupdate" 20 16 --config 3 --steps 5 --warmup 5
 echo done
+# summaries on the box (the .ncu-rep files exceed gpurun's 64 MiB return limit)
+for c in c4 c3; do
+  python tools/ncu_summary.py launches gpurun_out/r2x_${c}_launches.csv > gpurun_out/r2x_launch_share_${c}.md 2>&1
+  python tools/ncu_summary.py full gpurun_out/r2x_${c}.ncu-rep > gpurun_out/r2x_ncu_full_${c}_key_metrics.csv 2>&1
+  ncu -i gpurun_out/r2x_${c}.ncu-rep --page raw --csv > gpurun_out/r2x_ncu_full_${c}_raw.csv 2>/dev/null
+  gzip -f gpurun_out/r2x_ncu_full_${c}_raw.csv
+  rm -f gpurun_out/r2x_${c}.ncu-rep
+done
+du -sh gpurun_out
