@@ -528,8 +528,13 @@ int enqueue_sketch(sflsqr_t* h, const DevState* st, const double* v, cudaStream_
 // and its threads store w_{k+1} = w' / ||w'|| into W[:, k] and ||w'|| into H_{k+1,k} (SpmvEpi
 // kind 5) -- k_finish_w's pass without its launch and grid-wide dependency.  SFLSQR_KNOB_WNORM_SEP:
 // the separate normalisation kernel.
+// Only for sFLSQR (whose LS needs no H) and sFLSMR (whose LS is forked after the product): FLSQR's
+// LS is forked right after the w normalisation and reads H_{k+1,k} (FLSQR with maxit + 1 <= kFuseJ
+// takes the fused orthogonalisation).
 bool wnorm_fused(const sflsqr_t* h) {
+  const int me = h->P.method;
   return h->world == 1 && h->tkind == T_FULL && !h->blur && h->P.orth_alg == ORTH_FUSED &&
+         (me == SFLSQR_METHOD_SFLSQR || me == SFLSQR_METHOD_SFLSMR) &&
          !(h->knobs & SFLSQR_KNOB_WNORM_SEP) && !(runs_on_pairs(h, 1) && h->pt.warp_rows) &&
          (runs_on_pairs(h, 1) || h->t_rowptr);
 }
