@@ -168,3 +168,18 @@ def test_full_size_first_iterations(cfg, maxit, method):
     r = solve_problem(p, spec, maxit=maxit, eta=0.0, method=method, record=False)
     g = _gpu_run(p, spec, maxit, method)
     _compare(g, r, maxit)
+
+
+@pytest.mark.parametrize("cfg", [3, 4])
+@pytest.mark.parametrize("method", ["flsqr", "flsmr"])
+def test_short_full_window_runs_take_the_fused_orthogonalisation(cfg, method):
+    # maxit + 1 <= 6: FLSQR / FLSMR's full window fits the fused orthogonalisation kernels; FLSQR forks
+    # its LS right after the w normalisation (which therefore stays its own kernel: the fused-into-T
+    # form is for sFLSQR / sFLSMR only) -- the oracle's bar on reduced configs 3 and 4
+    kw = dict(N=128, n_angles=90, nb=183) if cfg == 3 else dict(N=96, n_angles=61, nb=137)
+    p = make_problem(cfg, **kw)
+    spec = p.solvers[0]
+    for maxit in (3, 5):
+        r = solve_problem(p, spec, maxit=maxit, eta=0.0, method=method, record=False)
+        g = _gpu_run(p, spec, maxit, method)
+        _compare(g, r, maxit)
