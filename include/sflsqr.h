@@ -160,6 +160,9 @@ typedef struct sflsqr sflsqr_t;
 /* opts.comm_kind (world > 1) */
 #define SFLSQR_COMM_NCCL 0  /* one process per GPU, NCCL (libnccl.so.2 loaded at run time) */
 #define SFLSQR_COMM_LOCAL 1 /* ranks are host threads of one process sharing opts.local_group */
+#define SFLSQR_COMM_IPC 2   /* one process per rank on one node, no NCCL: host rendezvous in the POSIX
+                               shared-memory segment named by opts.nccl_id, data through CUDA-IPC peer
+                               memory (also runs several ranks on one device)                */
 
 typedef struct sflsqr_opts {
   int32_t method;    /* SFLSQR_METHOD_*                                            */
@@ -177,7 +180,9 @@ typedef struct sflsqr_opts {
   int32_t use_graph; /* 1: replay one captured CUDA graph per iteration (one rank, or NCCL ranks
                         with the collectives captured; the in-process group runs eagerly) */
   int32_t comm_kind; /* SFLSQR_COMM_* (world > 1)                                  */
-  const uint8_t *nccl_id; /* SFLSQR_COMM_NCCL: the 128-byte id of sflsqr_get_unique_id */
+  const uint8_t *nccl_id; /* SFLSQR_COMM_NCCL: the 128-byte id of sflsqr_get_unique_id;
+                             SFLSQR_COMM_IPC: a NUL-terminated POSIX shm name ("/name", <= 100
+                             chars) unique to this group, the same on every rank          */
   void *local_group;      /* SFLSQR_COMM_LOCAL: sflsqr_local_group_create()          */
   int32_t orth_kernel;    /* SFLSQR_ORTHK_* (0 = auto)                               */
   int32_t knobs;          /* SFLSQR_KNOB_* bits; 0 = the measured defaults */
@@ -235,8 +240,10 @@ int sflsqr_version(void);
  * method, window >= 1, maxit >= 1, tol >= 0, eta == 0 or eta > 1,
  * delta_e >= 0, 1 <= world, 0 <= rank < world -> else SFLSQR_E_INVALID.
  * world > 1: NCCL comm from opts.nccl_id (collective over the ranks: every rank
- * must call it) or the in-process group opts.local_group; SFLSQR_E_UNSUPPORTED
- * when NCCL cannot be loaded.  Selects opts.device; fails with SFLSQR_E_CUDA when
+ * must call it), the in-process group opts.local_group, or the CUDA-IPC process
+ * group named by opts.nccl_id (SFLSQR_COMM_IPC; collective too, a rank that never
+ * arrives fails the others after 180 s); SFLSQR_E_UNSUPPORTED when the communicator
+ * cannot be set up (NCCL not loadable, shared memory or CUDA IPC unavailable).  Selects opts.device; fails with SFLSQR_E_CUDA when
  * no CUDA device exists. */
 int sflsqr_create(sflsqr_t **h, const sflsqr_opts *opts);
 

@@ -2,12 +2,45 @@
 #include "comm.h"
 
 #include <dlfcn.h>
+#include <fcntl.h>
 #include <nccl.h>
+#include <sched.h>
+#include <sys/mman.h>
+#include <unistd.h>
 
+#include <atomic>
+#include <chrono>
 #include <cstring>
 #include <vector>
 
 namespace sfl {
+
+// CUDA IPC exchange of one cudaMalloc'ed buffer per rank (the peer-memory collectives of the
+// process transports): `gather` is the transport's blocking host all-gather.
+template <class Gather>
+static int ipc_share(int rank, int world, void* local, void** peers, Gather gather, std::string& err) {
+  cudaIpcMemHandle_t mine;
+  if (cudaIpcGetMemHandle(&mine, local) != cudaSuccess) {
+    cudaGetLastError();
+    err = "cudaIpcGetMemHandle failed";
+    return -1;
+  }
+  std::vector<cudaIpcMemHandle_t> all(world);
+  if (gather(&mine, all.data(), sizeof(mine))) return -1;
+  for (int r = 0; r < world; ++r) {
+    peers[r] = nullptr;
+    if (r == rank) {
+      peers[r] = local;
+    } else if (cudaIpcOpenMemHandle(&peers[r], all[r], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      err = "cudaIpcOpenMemHandle failed (no peer access between the ranks' GPUs?)";
+      for (int q = 0; q < r; ++q)
+        if (q != rank && peers[q]) cudaIpcCloseMemHandle(peers[q]);
+      return -1;
+    }
+  }
+  return 0;
+}
 
 // ====================================================================== NCCL
 namespace {
@@ -73,31 +106,16 @@ struct NcclComm : Comm {
     return check(nccl().AllReduce(scratch, scratch, 1, ncclDouble, ncclSum, comm, s), "ncclAllReduce(barrier)", err);
   }
   int share_buffer(void* local, void** peers, std::string& err) override {
-    cudaIpcMemHandle_t mine;
-    if (cudaIpcGetMemHandle(&mine, local) != cudaSuccess) {
-      cudaGetLastError();
-      err = "cudaIpcGetMemHandle failed";
-      return -1;
-    }
-    std::vector<cudaIpcMemHandle_t> all(world);
-    if (allgather_host(&mine, all.data(), sizeof(mine), err)) return -1;
-    for (int r = 0; r < world; ++r) {
-      peers[r] = nullptr;
-      if (r == rank) {
-        peers[r] = local;
-      } else if (cudaIpcOpenMemHandle(&peers[r], all[r], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
-        cudaGetLastError();
-        err = "cudaIpcOpenMemHandle failed (no peer access between the ranks' GPUs?)";
-        for (int q = 0; q < r; ++q)
-          if (q != rank && peers[q]) cudaIpcCloseMemHandle(peers[q]);
-        return -1;
-      }
-    }
-    return 0;
+    return ipc_share(rank, world, local, peers,
+                     [&](const void* a, void* b, size_t n) { return allgather_host(a, b, n, err); }, err);
   }
   void unshare_buffer(void** peers) override {
     for (int r = 0; r < world; ++r)
       if (r != rank && peers[r]) cudaIpcCloseMemHandle(peers[r]);
+  }
+  void release_fence() override {
+    std::string e;
+    if (!barrier(nullptr, e)) cudaStreamSynchronize(nullptr);
   }
   int check(ncclResult_t r, const char* what, std::string& err) {
     if (r == ncclSuccess) return 0;
@@ -357,6 +375,210 @@ Comm* local_comm_create(LocalGroup* g, int rank) {
   c->g = g;
   c->rank = rank;
   c->world = g->world;
+  return c;
+}
+
+
+// ====================================================================== processes + CUDA IPC
+// World processes of one node (one GPU each, or several on one GPU): host rendezvous through a
+// POSIX shared-memory segment, data through CUDA-IPC peer memory.  Every collective stages its
+// input in a per-rank device buffer the peers opened with cudaIpcOpenMemHandle, meets the other
+// ranks on the host after a stream synchronise, and reduces the peers' buffers in fixed rank order
+// with one kernel (the same order as the in-process group: identical bits).  No kernel waits on
+// another rank.  A peer that never arrives fails the call after kIpcTimeoutS instead of hanging.
+namespace {
+
+constexpr int kIpcTimeoutS = 180;
+constexpr size_t kIpcStage = 4096;
+
+struct ShmHdr {
+  std::atomic<int> arrived;
+  std::atomic<unsigned> gen;
+  char stage[kMaxLocal][kIpcStage];
+};
+
+__global__ void k_ipc_allreduce(PtrSet p, int world, size_t count, int is_max, double* out) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
+    double acc = p.in[0][i];
+    for (int r = 1; r < world; ++r) acc = is_max ? fmax(acc, p.in[r][i]) : acc + p.in[r][i];
+    out[i] = acc;
+  }
+}
+__global__ void k_ipc_allgather(PtrSet p, int world, size_t count, double* out) {
+  const size_t total = count * world;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const int q = (int)(i / count);
+    out[i] = p.in[q][i - q * count];
+  }
+}
+__global__ void k_ipc_reduce_scatter(PtrSet p, int world, size_t count, int rank, double* out) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
+    double acc = p.in[0][rank * count + i];
+    for (int q = 1; q < world; ++q) acc += p.in[q][rank * count + i];
+    out[i] = acc;
+  }
+}
+
+struct IpcComm : Comm {
+  ShmHdr* shm = nullptr;
+  std::string name;
+  double* stg = nullptr;  // this rank's staging buffer (peers read it)
+  size_t cap = 0;         // bytes
+  void* peers[kMaxLocal] = {};
+
+  ~IpcComm() override {
+    if (stg) {
+      std::string e;
+      host_barrier(e);  // nobody still reads a peer's staging buffer
+      unshare_buffer(peers);
+      host_barrier(e);
+      cudaFree(stg);
+    }
+    if (shm) munmap(shm, sizeof(ShmHdr));
+  }
+  int host_barrier(std::string& err) {
+    const unsigned my = shm->gen.load(std::memory_order_acquire);
+    if (shm->arrived.fetch_add(1, std::memory_order_acq_rel) + 1 == world) {
+      shm->arrived.store(0, std::memory_order_relaxed);
+      shm->gen.fetch_add(1, std::memory_order_release);
+      return 0;
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    for (unsigned spin = 0; shm->gen.load(std::memory_order_acquire) == my; ++spin) {
+      if ((spin & 1023) == 1023) {
+        sched_yield();
+        if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(kIpcTimeoutS)) {
+          err = "ipc communicator: a rank did not reach the rendezvous within the timeout";
+          return -1;
+        }
+      }
+    }
+    return 0;
+  }
+  int allgather_host(const void* send, void* recv, size_t bytes, std::string& err) override {
+    if (bytes > kIpcStage) {
+      err = "ipc communicator: host all-gather larger than its stage";
+      return -1;
+    }
+    std::memcpy(shm->stage[rank], send, bytes);
+    if (host_barrier(err)) return -1;
+    for (int r = 0; r < world; ++r) std::memcpy(static_cast<char*>(recv) + r * bytes, shm->stage[r], bytes);
+    return host_barrier(err);
+  }
+  int share_buffer(void* local, void** out, std::string& err) override {
+    return ipc_share(rank, world, local, out,
+                     [&](const void* a, void* b, size_t n) { return allgather_host(a, b, n, err); }, err);
+  }
+  void unshare_buffer(void** ps) override {
+    for (int r = 0; r < world; ++r)
+      if (r != rank && ps[r]) cudaIpcCloseMemHandle(ps[r]);
+  }
+  void release_fence() override {
+    std::string e;
+    host_barrier(e);
+  }
+  // every rank calls every collective with the same count, so the staging buffers grow together
+  int ensure(size_t bytes, std::string& err) {
+    if (bytes <= cap) return 0;
+    if (stg) {
+      if (host_barrier(err)) return -1;
+      unshare_buffer(peers);
+      if (host_barrier(err)) return -1;
+      cudaFree(stg);
+      stg = nullptr;
+      cap = 0;
+    }
+    const size_t want = std::max<size_t>(bytes + bytes / 2, (size_t)2 << 20);  // its own driver block
+    if (cudaMalloc(&stg, want) != cudaSuccess) {
+      cudaGetLastError();
+      err = "ipc communicator: staging cudaMalloc failed";
+      return -1;
+    }
+    if (share_buffer(stg, peers, err)) return -1;
+    cap = want;
+    return 0;
+  }
+  // kind: 0 sum, 1 max, 2 all-gather, 3 reduce-scatter
+  int collective(int kind, const double* send, double* recv, size_t count, cudaStream_t s, std::string& err) {
+    const size_t in_count = kind == 3 ? count * world : count;
+    if (ensure(in_count * sizeof(double), err)) return -1;
+    if (in_count) cudaMemcpyAsync(stg, send, in_count * sizeof(double), cudaMemcpyDeviceToDevice, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess) {
+      err = "ipc communicator: stream failed before a collective";
+      return -1;
+    }
+    if (host_barrier(err)) return -1;  // every rank's input is staged
+    if (in_count) {
+      PtrSet p;
+      for (int r = 0; r < world; ++r) {
+        p.in[r] = static_cast<const double*>(peers[r]);
+        p.out[r] = nullptr;
+      }
+      const size_t total = kind == 2 ? count * world : count;
+      const int grid = (int)std::min<size_t>((total + 255) / 256, 148 * 4);
+      if (kind <= 1)
+        k_ipc_allreduce<<<grid, 256, 0, s>>>(p, world, count, kind == 1, recv);
+      else if (kind == 2)
+        k_ipc_allgather<<<grid, 256, 0, s>>>(p, world, count, recv);
+      else
+        k_ipc_reduce_scatter<<<grid, 256, 0, s>>>(p, world, count, rank, recv);
+      if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess) {
+        err = "ipc communicator: collective kernel failed";
+        return -1;
+      }
+    }
+    return host_barrier(err);  // every rank has read every staging buffer
+  }
+  int allreduce(double* buf, size_t count, bool is_max, cudaStream_t s, std::string& err) override {
+    return collective(is_max ? 1 : 0, buf, buf, count, s, err);
+  }
+  int allgather(const double* send, double* recv, size_t count, cudaStream_t s, std::string& err) override {
+    return collective(2, send, recv, count, s, err);
+  }
+  int reduce_scatter(const double* send, double* recv, size_t count, cudaStream_t s, std::string& err) override {
+    return collective(3, send, recv, count, s, err);
+  }
+  int barrier(cudaStream_t s, std::string& err) override {
+    if (cudaStreamSynchronize(s) != cudaSuccess) {
+      err = "ipc communicator: stream failed before a barrier";
+      return -1;
+    }
+    return host_barrier(err);
+  }
+};
+
+}  // namespace
+
+Comm* ipc_comm_create(const char* shm_name, int rank, int world, int device, std::string& err) {
+  if (world < 1 || world > kMaxLocal || !shm_name || shm_name[0] != '/' || std::strlen(shm_name) > 100) {
+    err = "ipc communicator: world must be 1..8 and the name a POSIX shm name ('/...', <= 100 chars)";
+    return nullptr;
+  }
+  cudaSetDevice(device);
+  // every rank creates-or-opens the segment; a new segment is zero-filled, which is the initial state
+  const int fd = shm_open(shm_name, O_CREAT | O_RDWR, 0600);
+  if (fd < 0 || ftruncate(fd, sizeof(ShmHdr)) != 0) {
+    if (fd >= 0) close(fd);
+    err = "ipc communicator: shm_open / ftruncate failed";
+    return nullptr;
+  }
+  void* m = mmap(nullptr, sizeof(ShmHdr), PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  close(fd);
+  if (m == MAP_FAILED) {
+    err = "ipc communicator: mmap failed";
+    return nullptr;
+  }
+  IpcComm* c = new IpcComm();
+  c->rank = rank;
+  c->world = world;
+  c->name = shm_name;
+  c->shm = static_cast<ShmHdr*>(m);
+  // all ranks have mapped the segment after this rendezvous: the name can go
+  if (c->host_barrier(err)) {
+    delete c;
+    return nullptr;
+  }
+  if (rank == 0) shm_unlink(shm_name);
   return c;
 }
 

@@ -1,6 +1,6 @@
 // Collectives used by the sharded sketched flexible Golub-Kahan step.
 //
-// Two implementations of one interface:
+// Three implementations of one interface (IpcComm, below, is the third):
 //   * NcclComm   — one process per GPU, NCCL over NVLink/NVSwitch.  libnccl is
 //                  dlopen'ed on first use (the already-loaded libnccl.so.2, e.g.
 //                  PyTorch's, else the system one), so single-GPU use needs no NCCL.
@@ -11,6 +11,10 @@
 //                  arriving rank makes a comm stream wait for all of them, reduces in
 //                  fixed rank order with one kernel, and every rank's stream waits on
 //                  the completion event.  No kernel ever waits on another rank.
+//   * IpcComm    — one process per rank on one node, host rendezvous in POSIX shared memory and
+//                  CUDA-IPC peer memory for the data: the cross-process peer-memory path
+//                  without NCCL (NCCL refuses two ranks on one device), used to run the sharded
+//                  path and its fused peer-memory collectives across real processes on one GPU.
 // All collectives are on fp64 device buffers and are deterministic (fixed
 // reduction order; identical bits on every rank).
 #pragma once
@@ -44,11 +48,20 @@ struct Comm {
   // r's buffer addressable from this device (in-process: the raw pointers; NCCL: CUDA IPC).
   virtual int share_buffer(void* local, void** peers, std::string& err) = 0;
   virtual void unshare_buffer(void** peers) { (void)peers; }
+  // Host rendezvous around the release of shared buffers (process transports that map peer
+  // memory; a no-op where the ranks share an address space or NCCL orders the teardown).
+  virtual void release_fence() {}
 };
 
 // ---------------------------------------------------------------- NCCL (dlopen)
 int nccl_get_unique_id(uint8_t id[128], std::string& err);
 Comm* nccl_comm_create(const uint8_t id[128], int rank, int world, int device, std::string& err);
+
+// ---------------------------------------------------------------- processes + CUDA IPC
+// World processes of one node: host rendezvous in the POSIX shared-memory segment `shm_name`
+// (created by whichever rank comes first, unlinked once every rank mapped it), data through
+// CUDA-IPC peer memory.  Collective over the ranks.
+Comm* ipc_comm_create(const char* shm_name, int rank, int world, int device, std::string& err);
 
 // ---------------------------------------------------------------- in-process group
 struct LocalGroup;  // shared by the R handles of one group

@@ -240,10 +240,15 @@ void free_solve(sflsqr_t* h) {
   destroy_graphs(h);
   if (h->comm) {
     cudaStreamSynchronize(h->stream);
+    const bool shared = h->peer_zfull[h->rank] != nullptr;
+    // process ranks: no peer still stores into this rank's buffers, and every peer has closed its
+    // mapping of them before they are freed below
+    if (shared) h->comm->release_fence();
     for (void** pp : {h->peer_zfull, h->peer_wfull, h->peer_zrecv}) {
       if (pp[h->rank]) h->comm->unshare_buffer(pp);
       for (int g = 0; g < 8; ++g) pp[g] = nullptr;
     }
+    if (shared) h->comm->release_fence();
   }
   h->zrecv = nullptr;
   for (void* p : h->solve_allocs) cudaFree(p);
@@ -1409,6 +1414,12 @@ int alloc_solve(sflsqr_t* h) {
   auto A = [&](double** p, size_t count) {
     return dalloc(h, (void**)p, count * sizeof(double), &h->solve_allocs, &h->solve_sizes);
   };
+  // buffers opened by the peers through CUDA IPC: at least 2 MiB, so each has its own driver block
+  // (smaller cudaMalloc's are sub-allocated from a shared one, which an IPC handle would expose whole)
+  auto AS = [&](double** p, size_t count) {
+    return dalloc(h, (void**)p, std::max(count * sizeof(double), (size_t)2 << 20), &h->solve_allocs,
+                  &h->solve_sizes);
+  };
   int rc;
   const size_t n = (size_t)h->n_loc, m = (size_t)h->m_loc;
   // z receives the reduce-scatter (n_max) when sharded by columns
@@ -1452,12 +1463,12 @@ int alloc_solve(sflsqr_t* h) {
       ((rc = A(&P.cpart, (size_t)P.ldc * kVecBlocks)) || (rc = A(&P.cscal, (size_t)2 * P.ldc))))
     return rc;
   if (h->world > 1) {
-    if ((rc = A(&P.zsend, h->n_max)) || (rc = A(&h->zfull, (size_t)h->world * h->n_max))) return rc;
+    if ((rc = A(&P.zsend, h->n_max)) || (rc = AS(&h->zfull, (size_t)h->world * h->n_max))) return rc;
     if (h->tkind == T_ROWSHARD) {
-      if ((rc = A(&P.wsend, h->m_max)) || (rc = A(&h->wfull, (size_t)h->world * h->m_max))) return rc;
+      if ((rc = A(&P.wsend, h->m_max)) || (rc = AS(&h->wfull, (size_t)h->world * h->m_max))) return rc;
     } else {
       if ((rc = A(&h->zpart, (size_t)h->world * h->n_max))) return rc;
-      if (h->p2p && (rc = A(&h->zrecv, (size_t)h->world * h->n_max))) return rc;
+      if (h->p2p && (rc = AS(&h->zrecv, (size_t)h->world * h->n_max))) return rc;
     }
   }
   // Debug aid: SFLSQR_KNOB_DEBUG_POISON fills every solve buffer with NaN bytes so a
@@ -1748,9 +1759,10 @@ int sflsqr_create(sflsqr_t** out, const sflsqr_opts* o) {
   if (!(o->delta_e >= 0.0) || !std::isfinite(o->delta_e))
     return fail(nullptr, SFLSQR_E_INVALID, "delta_e must be >= 0");
   if (o->world < 1 || o->rank < 0 || o->rank >= o->world) return fail(nullptr, SFLSQR_E_INVALID, "bad rank/world");
-  if (o->world > 1 && o->comm_kind != SFLSQR_COMM_NCCL && o->comm_kind != SFLSQR_COMM_LOCAL)
+  if (o->world > 1 && o->comm_kind != SFLSQR_COMM_NCCL && o->comm_kind != SFLSQR_COMM_LOCAL &&
+      o->comm_kind != SFLSQR_COMM_IPC)
     return fail(nullptr, SFLSQR_E_INVALID, "bad comm_kind");
-  if (o->world > 1 && o->comm_kind == SFLSQR_COMM_NCCL && !o->nccl_id)
+  if (o->world > 1 && o->comm_kind != SFLSQR_COMM_LOCAL && !o->nccl_id)
     return fail(nullptr, SFLSQR_E_INVALID, "world > 1 with NCCL needs opts.nccl_id");
   if (o->world > 1 && o->comm_kind == SFLSQR_COMM_LOCAL && !o->local_group)
     return fail(nullptr, SFLSQR_E_INVALID, "world > 1 with LOCAL needs opts.local_group");
@@ -1779,7 +1791,7 @@ int sflsqr_create(sflsqr_t** out, const sflsqr_opts* o) {
   if (o->method >= SFLSQR_METHOD_LSQR) h->o.window = 1;  // GKB short recurrences: no stored window
   // the in-process group's collectives are host rendezvous (not capturable): eager; NCCL calls are
   // captured into the per-iteration graph with the kernels (eager fallback if capture fails)
-  if (o->world > 1 && o->comm_kind == SFLSQR_COMM_LOCAL) h->o.use_graph = 0;
+  if (o->world > 1 && o->comm_kind != SFLSQR_COMM_NCCL) h->o.use_graph = 0;
   if (o->stream && (cudaStream_t)o->stream != cudaStreamLegacy && (cudaStream_t)o->stream != cudaStreamPerThread) {
     h->stream = (cudaStream_t)o->stream;
   } else {
@@ -1793,11 +1805,13 @@ int sflsqr_create(sflsqr_t** out, const sflsqr_opts* o) {
     std::string ce;
     if (o->comm_kind == SFLSQR_COMM_NCCL)
       h->comm = nccl_comm_create(o->nccl_id, o->rank, o->world, o->device, ce);
+    else if (o->comm_kind == SFLSQR_COMM_IPC)
+      h->comm = ipc_comm_create(reinterpret_cast<const char*>(o->nccl_id), o->rank, o->world, o->device, ce);
     else
       h->comm = local_comm_create(static_cast<LocalGroup*>(o->local_group), o->rank);
     // peer-memory collectives: default on in-process (tested), opt-in (SFLSQR_KNOB_P2P_ON) across
     // processes (CUDA IPC over NVLink: not exercisable on this single-GPU pool)
-    h->p2p = (kn & SFLSQR_KNOB_P2P_ON) ? true : (kn & SFLSQR_KNOB_P2P_OFF) ? false : o->comm_kind == SFLSQR_COMM_LOCAL;
+    h->p2p = (kn & SFLSQR_KNOB_P2P_ON) ? true : (kn & SFLSQR_KNOB_P2P_OFF) ? false : o->comm_kind != SFLSQR_COMM_NCCL;
     if (o->world > 8) h->p2p = false;
     if (!h->comm) {
       if (h->own_stream) cudaStreamDestroy(h->stream);

@@ -45,7 +45,7 @@ EXPORTED = [
 ]
 
 
-COMM_NCCL, COMM_LOCAL = 0, 1
+COMM_NCCL, COMM_LOCAL, COMM_IPC = 0, 1, 2
 
 # opts.knobs (include/sflsqr.h SFLSQR_KNOB_*): scheduling / storage-format switches, 0 = defaults
 KNOBS = {"no_pdl": 0x1, "sketch_main": 0x2, "no_interp": 0x4, "no_sell": 0x8, "cgs_always2": 0x10,
@@ -178,7 +178,7 @@ class SFLSQR:
 
     def __init__(self, method="sflsqr", window=2, maxit=10, orth_mode="P", tol=0.0, eta=0.0, delta_e=0.0,
                  history=HIST_TRUE_RES, device=0, stream=None, use_graph=True, rank=0, world=1, nccl_id=None,
-                 local_group=None, orth_kernel="auto", knobs=0):
+                 local_group=None, orth_kernel="auto", knobs=0, ipc_name=None):
         self.lib = load_library()
         o = Opts()
         o.knobs = knob_bits(knobs)
@@ -195,6 +195,11 @@ class SFLSQR:
         if int(world) > 1:
             if local_group is not None:
                 o.comm_kind, o.local_group = COMM_LOCAL, local_group.ptr
+            elif ipc_name is not None:
+                # SFLSQR_COMM_IPC: process ranks, POSIX shm rendezvous + CUDA-IPC peer memory
+                o.comm_kind = COMM_IPC
+                self._id_buf = ctypes.create_string_buffer(str(ipc_name).encode(), 128)
+                o.nccl_id = ctypes.addressof(self._id_buf)
             else:
                 o.comm_kind = COMM_NCCL
                 self._id_buf = ctypes.create_string_buffer(bytes(nccl_id), 128)
