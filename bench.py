@@ -93,6 +93,9 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+_DIST_DEV = "cuda"   # "cpu" under --comm ipc (gloo process group)
+
+
 def _dist():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -105,7 +108,7 @@ def _max_over_ranks(v, world):
         return v
     import torch
     import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    t = torch.tensor([v], dtype=torch.float64, device=_DIST_DEV)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -236,6 +239,11 @@ def main():
     ap.add_argument("--no-profile", action="store_true", help="graph replay without per-kernel events")
     ap.add_argument("--N", type=int, default=None, help="override grid size (debug)")
     ap.add_argument("--no-windows", action="store_true", help="skip the late-window and full-solve timings")
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "ipc"],
+                    help="N > 1 transport: nccl (one GPU per rank, the measured configuration) or ipc (process ranks "
+                         "over CUDA-IPC peer memory with a host rendezvous, ranks mapped round-robin onto the visible "
+                         "devices: runs the sharded branch on fewer GPUs than ranks, a functional check, not a "
+                         "scaling number)")
     ap.add_argument("--knobs", default="", help="comma-separated opts.knobs names (A/B runs; default: none)")
     args = ap.parse_args()
 
@@ -254,12 +262,19 @@ def main():
     if not torch.cuda.is_available():
         print(json.dumps({"metric": METRIC, "error": "no CUDA device"}))
         sys.exit(1)
+    if args.comm == "ipc":
+        global _DIST_DEV
+        _DIST_DEV = "cpu"
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     # a dedicated non-default stream: the library issues on it and the CUDA events below record on it
     torch.cuda.set_stream(torch.cuda.Stream())
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.comm == "ipc":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2605_22281_b200 import solver_for_problem
     from paper_2605_22281_b200._build import build_library
     if rank == 0:
@@ -278,7 +293,7 @@ def main():
         import torch.distributed as dist
 
         def allreduce_sum(v):
-            t = torch.tensor([v], dtype=torch.float64, device="cuda")
+            t = torch.tensor([v], dtype=torch.float64, device=_DIST_DEV)
             dist.all_reduce(t)
             return float(t.item())
 
@@ -288,15 +303,21 @@ def main():
         prob = make_ct_shard(args.config, ab[rank], None if tb is None else tb[rank], allreduce_sum)
         spec = _spec_for(prob, args.method)
         t_gen = time.perf_counter() - t_gen
-        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        uid = torch.zeros(128, dtype=torch.uint8, device=_DIST_DEV)
         if rank == 0:
-            uid.copy_(torch.frombuffer(bytearray(get_unique_id()), dtype=torch.uint8))
+            if args.comm == "ipc":   # the group's POSIX shm name, NUL padded
+                raw = ("/sflsqr_bench_%d_%d" % (os.getpid(), time.time_ns() % 10**9)).encode().ljust(128, b"\0")
+            else:
+                raw = get_unique_id()
+            uid.copy_(torch.frombuffer(bytearray(raw), dtype=torch.uint8))
         dist.broadcast(uid, 0)
+        comm_kw = (dict(ipc_name=bytes(uid.cpu().numpy()).rstrip(b"\0").decode()) if args.comm == "ipc"
+                   else dict(nccl_id=bytes(uid.cpu().numpy())))
         maxit = max(spec.maxit, W + K)
         t_up = time.perf_counter()
         s = SFLSQR(method=spec.method, window=spec.window, maxit=maxit, orth_mode=spec.orth_mode, tol=spec.tol,
                    eta=0.0, delta_e=prob.delta_e, device=local, use_graph=True, rank=rank, world=world,
-                   nccl_id=bytes(uid.cpu().numpy()), knobs=knobs)
+                   knobs=knobs, **comm_kw)
         A = prob.A_loc
         t = None if prob.T_loc is None else (prob.T_loc.rowptr, prob.T_loc.col, prob.T_loc.val)
         s.set_operator_shard(prob.m, prob.n, prob.a_rows[0], prob.a_rows[1], A.rowptr, A.col, A.val, t=t,
@@ -307,7 +328,9 @@ def main():
         b_host = prob.b_loc
         nnz_A = int(allreduce_sum(float(A.nnz)))
         nnz_T = int(allreduce_sum(float(prob.T_loc.nnz if prob.T_loc is not None else A.nnz)))
-        parallelism = f"shard{world} ({'ROWSHARD' if prob.T_loc is not None else 'COLSHARD'}, NCCL)"
+        transport = "NCCL" if args.comm == "nccl" else \
+            f"CUDA-IPC process ranks on {min(world, torch.cuda.device_count())} device(s), host rendezvous"
+        parallelism = f"shard{world} ({'ROWSHARD' if prob.T_loc is not None else 'COLSHARD'}, {transport})"
     else:
         prob = make_problem(args.config, **(dict(N=args.N) if args.N else {}))
         spec = _spec_for(prob, args.method)
@@ -472,8 +495,11 @@ def main():
                        "iterations_timed": f"{W + 1}..{W + K}", "history": "true residual (W path) on",
                        "l2": "inputs larger than L2 (operators ~30 GB vs 126 MB L2); no flush",
                        "parallelism": parallelism, "knobs": knobs,
+                       **({"functional_check_only": "process ranks share device(s): not a scaling measurement"}
+                          if (sharded and args.comm == "ipc" and world > torch.cuda.device_count()) else {}),
                        "launch": ("CUDA graph per iteration" + (" (NCCL collectives captured)" if sharded else ""))
-                                 if info_end["graph"] else "eager launches" + (" + NCCL" if sharded else ""),
+                                 if info_end["graph"] else "eager launches" + ((" + NCCL" if args.comm == "nccl" else
+                                                                                " + host-rendezvous collectives") if sharded else ""),
                        "per_kernel_timing": "second timed region of K iterations, eager launches with CUDA events "
                                             "on the library stream (ms_per_step_profiled)"},
             "roofline": roof,

@@ -53,3 +53,22 @@ def test_process_ranks_match_oracle_and_in_process_group(cfg, kw, method, world,
     _oracle_check(x, tr, sk, solve_problem(p, spec, maxit=K, eta=0.0), K)
     xl, trl, skl, _, _, _ = run_local_group(p, spec, world, maxit=K, eta=0.0, knobs=knobs)
     assert np.array_equal(x, xl) and np.array_equal(tr, trl) and np.array_equal(sk, skl)
+
+
+def test_bench_sharded_branch_under_torchrun_with_process_ranks():
+    # bench.py's N > 1 branch (each rank generates only its rows, strong scaling, rank 0 prints one
+    # line) launched the way the driver launches it, with --comm ipc so that two ranks fit one GPU
+    import json, os, subprocess, sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", "29541", "bench.py", "--gpus", "2", "--config", "3", "--comm", "ipc",
+           "--steps", "6", "--warmup", "3", "--no-windows"]
+    r = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1                               # rank 0 only
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["steps"] == 6 and d["value"] > 0
+    assert d["config"]["workload"].startswith("c3") and "COLSHARD" in d["config"]["parallelism"]
+    assert "functional_check_only" in d["config"]       # two ranks on one device: not a scaling number
+    assert d["status"]["k_done"] == 9 and d["gpu_launches"] > 0 and d["e2e"]["value"] > 0
