@@ -94,3 +94,17 @@ def test_knob_names_match_header():
     allbits = bits.pop("all")
     assert bits == B.KNOBS
     assert allbits == sum(bits.values())
+
+
+def test_comm_kinds_match_header_and_are_validated(lib):
+    from paper_2605_22281_b200 import sflsqr as B
+    txt = open(HEADER).read()
+    kinds = {m.group(1): int(m.group(2)) for m in re.finditer(r"#define SFLSQR_COMM_(\w+) (\d+)", txt)}
+    assert kinds == {"NCCL": B.COMM_NCCL, "LOCAL": B.COMM_LOCAL, "IPC": B.COMM_IPC}
+    # world > 1 needs its transport's argument (checked before any device or shared-memory use)
+    o = B.Opts()
+    o.method, o.window, o.maxit, o.world, o.rank = 0, 2, 5, 2, 0
+    for kind in (B.COMM_NCCL, B.COMM_IPC, B.COMM_LOCAL, 7):
+        o.comm_kind = kind
+        h = ctypes.c_void_p()
+        assert B.load_library().sflsqr_create(ctypes.byref(h), ctypes.byref(o)) == B.E_INVALID
