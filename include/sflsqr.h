@@ -251,6 +251,16 @@ int sflsqr_create(sflsqr_t **h, const sflsqr_opts *opts);
  * bytes with the caller's process group, pass as opts.nccl_id on every rank). */
 int sflsqr_get_unique_id(uint8_t id[128]);
 
+/* Test aid: drive the NCCL transport of the sharded path through a ONE-rank
+ * communicator on `device`: ncclGetUniqueId / CommInitRank, all-reduce (sum, max), all-gather,
+ * reduce-scatter, the byte all-gather used at setup, the barrier and share_buffer, then the same
+ * calls captured into a CUDA graph and replayed twice on changed inputs (the per-iteration graph
+ * of NCCL ranks).  One-rank collectives are the identity, so every result is compared with its
+ * input.  SFLSQR_OK; SFLSQR_E_UNSUPPORTED when libnccl cannot be loaded; SFLSQR_E_CUDA when a
+ * call, the capture or a replay fails or returns wrong data (sflsqr_last_error(NULL) says which);
+ * SFLSQR_E_INVALID for a bad device.  Touches no solver handle. */
+int sflsqr_debug_nccl_selftest(int32_t device);
+
 /* In-process rank group (SFLSQR_COMM_LOCAL): world ranks on one device, each
  * driven by its own host thread; collectives are host rendezvous + one reduction
  * kernel in fixed rank order.  Used to run the sharded path on one GPU.  The group

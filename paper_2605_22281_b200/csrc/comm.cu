@@ -574,12 +574,123 @@ Comm* ipc_comm_create(const char* shm_name, int rank, int world, int device, std
   c->name = shm_name;
   c->shm = static_cast<ShmHdr*>(m);
   // all ranks have mapped the segment after this rendezvous: the name can go
-  if (c->host_barrier(err)) {
+  const int brc = c->host_barrier(err);
+  if (rank == 0) shm_unlink(shm_name);  // also when a rank never came: no stale segment
+  if (brc) {
+    munmap(c->shm, sizeof(ShmHdr));
+    c->shm = nullptr;
     delete c;
     return nullptr;
   }
-  if (rank == 0) shm_unlink(shm_name);
   return c;
+}
+
+
+// ====================================================================== NCCL self-test (one rank)
+// Drives every NcclComm entry the sharded path uses through a world-1 communicator: the dlopen'ed
+// symbols and their argument order, the host all-gather, the barrier, and the capture of the NCCL
+// calls into a CUDA graph with two replays on changed inputs.  A one-rank all-reduce / all-gather /
+// reduce-scatter is the identity, so every result is checked against its input.
+namespace {
+__global__ void k_selftest_fill(double* a, size_t n, double scale) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    a[i] = scale * (double)(i + 1);
+}
+}  // namespace
+
+int nccl_selftest(int device, std::string& err) {
+  uint8_t id[128];
+  if (nccl_get_unique_id(id, err)) return -2;
+  Comm* c = nccl_comm_create(id, 0, 1, device, err);
+  if (!c) return -2;
+  const size_t n = 5000;
+  double *a = nullptr, *r = nullptr;
+  cudaStream_t s = nullptr;
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ge = nullptr;
+  std::vector<double> ha(n), hr(n);
+  int rc = -1;
+  auto same = [&](const double* dev, double scale, const char* what) {
+    cudaStreamSynchronize(s);
+    cudaMemcpy(hr.data(), dev, n * sizeof(double), cudaMemcpyDeviceToHost);
+    for (size_t i = 0; i < n; ++i)
+      if (hr[i] != scale * (double)(i + 1)) {
+        err = std::string("nccl self-test: wrong result after ") + what;
+        return false;
+      }
+    return true;
+  };
+  do {
+    if (cudaMalloc(&a, n * sizeof(double)) != cudaSuccess || cudaMalloc(&r, n * sizeof(double)) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) {
+      err = "nccl self-test: allocation failed";
+      break;
+    }
+    k_selftest_fill<<<8, 256, 0, s>>>(a, n, 1.0);
+    if (c->allreduce(a, n, false, s, err) || !same(a, 1.0, "allreduce(sum)")) break;
+    if (c->allreduce(a, n, true, s, err) || !same(a, 1.0, "allreduce(max)")) break;
+    cudaMemsetAsync(r, 0, n * sizeof(double), s);
+    if (c->allgather(a, r, n, s, err) || !same(r, 1.0, "allgather")) break;
+    cudaMemsetAsync(r, 0, n * sizeof(double), s);
+    if (c->reduce_scatter(a, r, n, s, err) || !same(r, 1.0, "reduce_scatter")) break;
+    if (c->barrier(s, err)) break;
+    char hs[64], hg[64];
+    for (int i = 0; i < 64; ++i) hs[i] = (char)(i * 3 + 1);
+    std::memset(hg, 0, sizeof(hg));
+    if (c->allgather_host(hs, hg, 64, err)) break;
+    if (std::memcmp(hs, hg, 64) != 0) {
+      err = "nccl self-test: wrong host all-gather";
+      break;
+    }
+    void* peers[kMaxLocal] = {};
+    if (c->share_buffer(a, peers, err)) break;
+    if (peers[0] != a) {
+      err = "nccl self-test: share_buffer did not return the local buffer for this rank";
+      break;
+    }
+    c->unshare_buffer(peers);
+    // the per-iteration graph of the sharded path: kernels and NCCL calls captured together
+    if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+      err = "nccl self-test: capture could not start";
+      break;
+    }
+    bool cap_ok = !c->allreduce(a, n, false, s, err) && !c->allgather(a, r, n, s, err) && !c->barrier(s, err);
+    if (cudaStreamEndCapture(s, &g) != cudaSuccess || !cap_ok || !g) {
+      cudaGetLastError();
+      if (err.empty()) err = "nccl self-test: the NCCL calls were not capturable";
+      rc = -3;
+      break;
+    }
+    if (cudaGraphInstantiate(&ge, g, 0) != cudaSuccess) {
+      err = "nccl self-test: graph instantiation failed";
+      rc = -3;
+      break;
+    }
+    bool ok = true;
+    for (int rep = 0; rep < 2 && ok; ++rep) {
+      const double sc = rep ? -2.5 : 3.0;
+      k_selftest_fill<<<8, 256, 0, s>>>(a, n, sc);
+      cudaMemsetAsync(r, 0, n * sizeof(double), s);
+      ok = cudaGraphLaunch(ge, s) == cudaSuccess && same(r, sc, "graph replay");
+      if (!ok && err.empty()) err = "nccl self-test: graph launch failed";
+    }
+    if (!ok) {
+      rc = -3;
+      break;
+    }
+    rc = 0;
+  } while (false);
+  if (ge) cudaGraphExecDestroy(ge);
+  if (g) cudaGraphDestroy(g);
+  if (s) {
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+  }
+  cudaFree(a);
+  cudaFree(r);
+  delete c;
+  cudaGetLastError();
+  return rc;
 }
 
 }  // namespace sfl

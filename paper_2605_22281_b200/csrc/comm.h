@@ -57,6 +57,10 @@ struct Comm {
 int nccl_get_unique_id(uint8_t id[128], std::string& err);
 Comm* nccl_comm_create(const uint8_t id[128], int rank, int world, int device, std::string& err);
 
+// One-rank self-test of the NCCL transport (every Comm entry, then the same calls captured into a
+// CUDA graph and replayed).  0 ok; -2 NCCL unavailable; -3 capture / replay failed; -1 otherwise.
+int nccl_selftest(int device, std::string& err);
+
 // ---------------------------------------------------------------- processes + CUDA IPC
 // World processes of one node: host rendezvous in the POSIX shared-memory segment `shm_name`
 // (created by whichever rank comes first, unlinked once every rank mapped it), data through

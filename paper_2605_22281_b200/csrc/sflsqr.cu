@@ -1723,6 +1723,19 @@ int sflsqr_get_unique_id(uint8_t id[128]) {
   return SFLSQR_OK;
 }
 
+int sflsqr_debug_nccl_selftest(int32_t device) {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(nullptr, SFLSQR_E_CUDA, "no CUDA device");
+  }
+  if (device < 0 || device >= ndev) return fail(nullptr, SFLSQR_E_INVALID, "bad device");
+  std::string e;
+  const int rc = nccl_selftest(device, e);
+  if (rc == 0) return SFLSQR_OK;
+  return fail(nullptr, rc == -2 ? SFLSQR_E_UNSUPPORTED : SFLSQR_E_CUDA, "%s", e.c_str());
+}
+
 int sflsqr_local_group_create(void** group, int32_t world, int32_t device) {
   if (!group) return fail(nullptr, SFLSQR_E_INVALID, "NULL group");
   int ndev = 0;

@@ -35,7 +35,7 @@ HIST_TRUE_RES = 1
 KC_NAMES = ["spmv_A", "spmv_T", "orth", "tau", "sketch", "ls", "xupd", "res", "stop"]
 
 EXPORTED = [
-    "sflsqr_version", "sflsqr_create", "sflsqr_get_unique_id", "sflsqr_local_group_create",
+    "sflsqr_version", "sflsqr_create", "sflsqr_get_unique_id", "sflsqr_debug_nccl_selftest", "sflsqr_local_group_create",
     "sflsqr_local_group_destroy", "sflsqr_set_operator_shard", "sflsqr_set_operator", "sflsqr_set_operator_blur", "sflsqr_set_sketch",
     "sflsqr_set_precond", "sflsqr_set_rhs", "sflsqr_iterate", "sflsqr_get_x", "sflsqr_get_residual_norms",
     "sflsqr_get_info", "sflsqr_debug_sketch_table", "sflsqr_debug_apply", "sflsqr_debug_basis", "sflsqr_debug_state",
@@ -109,6 +109,7 @@ def load_library(path: str = LIB_PATH):
         "sflsqr_set_operator": ([vp, i64, i64, vp, vp, vp, i32, vp, vp, vp, i32], ctypes.c_int),
         "sflsqr_set_operator_shard": ([vp, i64, i64, i64, i64, vp, vp, vp, i32, i64, i64, vp, vp, vp], ctypes.c_int),
         "sflsqr_get_unique_id": ([vp], ctypes.c_int),
+        "sflsqr_debug_nccl_selftest": ([i32], ctypes.c_int),
         "sflsqr_local_group_create": ([ctypes.POINTER(vp), i32, i32], ctypes.c_int),
         "sflsqr_local_group_destroy": ([vp], None),
         "sflsqr_set_operator_blur": ([vp, i32, i32, f64, i32], ctypes.c_int),
@@ -387,6 +388,14 @@ def get_unique_id() -> bytes:
     if rc != OK:
         raise SflsqrError(rc, lib.sflsqr_last_error(None).decode())
     return buf.raw
+
+
+def nccl_selftest(device=0) -> None:
+    """sflsqr_debug_nccl_selftest: the NCCL transport on a one-rank communicator, eagerly and captured."""
+    lib = load_library()
+    rc = lib.sflsqr_debug_nccl_selftest(int(device))
+    if rc != OK:
+        raise SflsqrError(rc, lib.sflsqr_last_error(None).decode())
 
 
 class LocalGroup:

@@ -70,5 +70,7 @@ def test_bench_sharded_branch_under_torchrun_with_process_ranks():
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["steps"] == 6 and d["value"] > 0
     assert d["config"]["workload"].startswith("c3") and "COLSHARD" in d["config"]["parallelism"]
-    assert "functional_check_only" in d["config"]       # two ranks on one device: not a scaling number
+    import torch
+    if torch.cuda.device_count() == 1:                   # two ranks on one device: not a scaling number
+        assert "functional_check_only" in d["config"]
     assert d["status"]["k_done"] == 9 and d["gpu_launches"] > 0 and d["e2e"]["value"] > 0

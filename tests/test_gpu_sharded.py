@@ -143,3 +143,12 @@ def test_peer_memory_collectives_bitwise_equal_to_collectives(cfg, world):
     r = solve_problem(p, spec, maxit=12, eta=0.0)
     x, tr, sk, _, _, _ = run_local_group(p, spec, world, maxit=12, eta=0.0)
     _check(x, tr, sk, r, 12)
+
+
+def test_nccl_transport_one_rank_selftest():
+    # the NCCL transport cannot run two ranks on one device; a ONE-rank communicator still drives
+    # every entry the sharded path uses (dlopen'ed symbols and argument order, all-reduce sum / max,
+    # all-gather, reduce-scatter, the setup byte all-gather, barrier, share_buffer) and the capture
+    # of those calls into a CUDA graph replayed on changed inputs; results are compared with inputs
+    from paper_2605_22281_b200.sflsqr import nccl_selftest
+    nccl_selftest(0)
