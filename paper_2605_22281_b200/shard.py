@@ -159,6 +159,27 @@ def run_ipc_processes(config, gen_kwargs, method, world: int, maxit, device=0, e
     return x, out[0][1], out[0][2], [o[3] for o in out], [(o[4], o[5]) for o in out], out
 
 
+def run_local_group_subprocess(config, gen_kwargs, method, world: int, maxit, device=0, eta=0.0, knobs=0, timeout=600):
+    """run_local_group in a fresh interpreter that regenerates the seeded problem the way the rank
+    processes of run_ipc_processes do (same environment, same host libraries): (x, true_res, sketch_res)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    import tempfile
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with tempfile.TemporaryDirectory() as tmp:
+        arg = dict(mode="local_group", config=config, gen_kwargs=gen_kwargs, method=method, world=world, maxit=maxit,
+                   device=device, eta=eta, knobs=knobs, out=os.path.join(tmp, "local.npz"))
+        r = subprocess.run([sys.executable, "-m", "paper_2605_22281_b200.shard", json.dumps(arg)], cwd=root,
+                           capture_output=True, text=True, timeout=timeout)
+        if r.returncode != 0:
+            raise RuntimeError("local group process exited %d:\n%s" % (r.returncode, (r.stdout + r.stderr)[-4000:]))
+        with np.load(arg["out"]) as f:
+            return f["x"], f["tr"], f["sk"]
+
+
 def _ipc_rank_main(argv):
     import json
     from gen import make_problem
@@ -166,6 +187,12 @@ def _ipc_rank_main(argv):
     a = json.loads(argv[0])
     prob = make_problem(a["config"], **a["gen_kwargs"])
     spec = [s for s in prob.solvers if s.method == a["method"]][0]
+    if a.get("mode") == "local_group":
+        # the in-process rank group from an interpreter set up exactly like the rank processes
+        x, tr, sk, _, _, _ = run_local_group(prob, spec, a["world"], maxit=a["maxit"], device=a["device"],
+                                             eta=a["eta"], knobs=a["knobs"])
+        np.savez(a["out"], x=x, tr=tr, sk=sk)
+        return
     plan = shard_plan(prob, a["world"])
     x, tr, sk, info, done, status, xg = rank_solve(prob, spec, plan, a["rank"], a["world"], a["maxit"], eta=a["eta"],
                                                    device=a["device"], knobs=a["knobs"], ipc_name=a["name"])

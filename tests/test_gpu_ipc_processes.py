@@ -14,6 +14,7 @@ pytestmark = pytest.mark.gpu
 
 C3R = dict(N=96, n_angles=70, nb=137)
 C4R = dict(N=128, n_angles=90, nb=183)
+C5R = dict(N=256, n_angles=180, nb=363)      # tests/horizons.py's reduced config 5
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -39,9 +40,11 @@ def _oracle_check(x, tr, sk, r, n):
     (3, C3R, "sflsmr", 3, 30, []),
     (4, C4R, "sflsqr", 2, 12, []),            # ROWSHARD (unmatched B), peer-memory all-gathers of z and w
     (3, C3R, "sflsqr", 2, 30, ["p2p_off"]),   # the staged collectives (all-gather / reduce-scatter kernels)
+    (4, C4R, "sflsqr", 2, 12, ["p2p_off"]),   # ROWSHARD through the staged all-gathers
+    (5, C5R, "sflsmr", 2, 40, []),            # BASELINE configs[4]'s recipe (IRN-l1, ell = 5, d = 600), reduced
 ])
 def test_process_ranks_match_oracle_and_in_process_group(cfg, kw, method, world, K, knobs):
-    from paper_2605_22281_b200.shard import run_ipc_processes, run_local_group
+    from paper_2605_22281_b200.shard import run_ipc_processes, run_local_group_subprocess
     p = make_problem(cfg, **kw)
     spec = [s for s in p.solvers if s.method == method][0]
     x, tr, sk, infos, st, out = run_ipc_processes(cfg, kw, method, world, K, eta=0.0, knobs=knobs)
@@ -51,8 +54,15 @@ def test_process_ranks_match_oracle_and_in_process_group(cfg, kw, method, world,
     for o in out:                                        # SFLSQR_X_GATHERED on every process
         assert np.array_equal(o[6], x)
     _oracle_check(x, tr, sk, solve_problem(p, spec, maxit=K, eta=0.0), K)
-    xl, trl, skl, _, _, _ = run_local_group(p, spec, world, maxit=K, eta=0.0, knobs=knobs)
-    assert np.array_equal(x, xl) and np.array_equal(tr, trl) and np.array_equal(sk, skl)
+    # bit for bit against the in-process group, run from an interpreter set up like the rank processes:
+    # they regenerate the seeded problem themselves, and the generator's host norms (numpy / OpenBLAS)
+    # can differ in the last bit between this long-lived pytest process and a fresh interpreter
+    # (measured: the same in-process run differs from its fresh-interpreter twin by 1e-14 from k = 2)
+    xl, trl, skl = run_local_group_subprocess(cfg, kw, method, world, K, eta=0.0, knobs=knobs)
+    diff = dict(x=float(np.max(np.abs(x - xl))), tr=float(np.max(np.abs(tr - trl) / trl)),
+                sk=float(np.max(np.abs(sk - skl) / skl)),
+                first_k=int(np.argmax((tr != trl) | (sk != skl))) + 1 if (np.any(tr != trl) or np.any(sk != skl)) else 0)
+    assert np.array_equal(x, xl) and np.array_equal(tr, trl) and np.array_equal(sk, skl), diff
 
 
 def test_bench_sharded_branch_under_torchrun_with_process_ranks():
